@@ -1,0 +1,149 @@
+/*
+ * rnnt.h — C-ABI of the B200 pruned RNN-T loss hot path (arXiv 2206.13236).
+ *
+ * Citations: P:<n> = line n of the paper source;
+ * D<k> = the reading of the paper recorded in DESIGN.md "Readings".
+ *
+ * The four entry points follow the paper's statement of the problem
+ * ("computing the core recursion ... twice"):
+ *   rnnt_simple_loss  : trivial joiner (Eq. 5-6) + recursion (Eq. 3)
+ *                       + occupancies y', empty' + am/lm gradients
+ *   rnnt_get_ranges   : locally optimal bounds (Eq. 8) + consistency
+ *                       adjustment (Eq. 9-10; algorithm D3)
+ *   rnnt_prune        : gather of the joiner input at the T*S band pairs
+ *   rnnt_pruned_loss  : full joiner W_out*tanh(.)+b on the band, log-softmax, pick and
+ *                       logit gradient fused (function merging), pruned
+ *                       recursion, all gradients.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer is a DEVICE pointer unless stated; the caller owns every buffer.
+ *    The library never allocates device memory: scratch comes from `workspace`
+ *    (size from rnnt_workspace_bytes).  No global mutable state: calls on distinct
+ *    streams with distinct workspaces may run concurrently.
+ *  - Every call only ENQUEUES work on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and never synchronises the host.
+ *  - Layouts are dense row-major with the padded batch maxima of rnnt_dims_t:
+ *    T = max_n T_n, U = max_n U_n.  Values at padded positions of inputs are never
+ *    read; all outputs at padded positions are written as exactly 0 (ranges: Umax_n).
+ *  - boundary is int64 (N,4) {0, 0, U_n, T_n} (begin_symbol, begin_frame,
+ *    end_symbol, end_frame); nonzero begins are not supported (RNNT_ERR_UNSUPPORTED
+ *    cannot be detected without a sync, so they are reported in status bit 4).
+ *  - symbols is int64 (N,U): y_1..y_{U_n} in [1,V) (D1); blank id is 0.
+ *  - bf16 tensors are passed as uint16_t bit patterns.
+ *  - Synchronous errors (returned): null pointer, dims out of range, misaligned
+ *    pointer (16 B), workspace too small, CUDA launch failure.  Nothing is launched
+ *    when an argument error is returned.
+ *  - Data-dependent errors go to the optional device `status` (N) int32 bitmask:
+ *      bit0  infeasible band: U_n > T_n (S-1) (no band-respecting path; D3)
+ *      bit1  non-finite loss
+ *      bit2  symbol outside [1,V)
+ *      bit3  normaliser underflow (sum_v exp(...) == 0 after offsets; D7)
+ *      bit4  nonzero begin_symbol / begin_frame in boundary
+ *    status is OR-ed into (callers zero it once per step).
+ *  - Gradients are grad_scale * d(sum_n loss_n)/dx, overwritten (not accumulated).
+ *    Pass 0.5 for the simple loss and 1.0 for the pruned loss.
+ */
+#ifndef RNNT_B200_H
+#define RNNT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RNNT_OK = 0,
+  RNNT_ERR_INVALID_ARG = 1,
+  RNNT_ERR_UNSUPPORTED = 2,
+  RNNT_ERR_WORKSPACE = 3,
+  RNNT_ERR_CUDA = 4
+} rnnt_status_t;
+
+/* Padded problem sizes. T, U are the batch maxima; V includes the blank id 0;
+ * J is the joiner hidden size; S the band width (s_range).
+ * Limits: 1 <= N, 1 <= T <= 65536, 0 <= U < T*64, 2 <= V, 8 <= J <= 4096 and
+ * J % 8 == 0, 1 <= S <= 32. */
+typedef struct {
+  int32_t N, T, U, V, J, S;
+} rnnt_dims_t;
+
+/* Bytes of device scratch needed by rnnt_simple_loss and rnnt_pruned_loss for these
+ * dims (one workspace may be reused by consecutive calls on the same stream). */
+size_t rnnt_workspace_bytes(const rnnt_dims_t* dims);
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* rnnt_status_string(rnnt_status_t s);
+
+/* Library build string: kernels compiled and the sm target. */
+const char* rnnt_version(void);
+
+/*
+ * Trivial-joiner loss, occupancies and gradients.
+ *   am  (N,T,V) fp32   L_enc(t,v)
+ *   lm  (N,U+1,V) fp32 L_dec(u,v)
+ *   L_norm(t,u) = log sum_v exp(am[t,v]+lm[u,v]) is evaluated as a max-shifted
+ *   contraction (Eq. 6, "after first applying offsets") without
+ *   materialising (T,U+1,V).
+ * Outputs:
+ *   loss    (N) fp32      -L_tot,n  (L_tot = alpha(T-1,U)+empty(T-1,U))
+ *   px_grad (N,T,U+1) fp32  y'(t,u)     = dL_tot/dy(t,u)      (unscaled, in [0,1])
+ *   py_grad (N,T,U+1) fp32  empty'(t,u) = dL_tot/dempty(t,u)  (unscaled, in [0,1])
+ *   am_grad (N,T,V) fp32, lm_grad (N,U+1,V) fp32 : grad_scale * d(sum loss)/d(am|lm);
+ *           either may be NULL to skip it.
+ *   status  (N) int32, nullable.
+ */
+rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* symbols,
+                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                               float* loss, float* px_grad, float* py_grad, float* am_grad,
+                               float* lm_grad, int32_t* status, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/*
+ * Pruning bounds.  For every frame t < T_n:
+ *   raw_t = argmax_{p=0..max(0,U_n-S+1)} ( -y'(t,p-1) + sum_{u=p}^{p+S-1} empty'(t,u) )  (Eq. 8)
+ * evaluated in fp64 from the fp32 inputs in a fixed order (u ascending, then the
+ * subtraction; D5) with ties to the smallest p — bit-exact w.r.t. the oracle on
+ * identical inputs.  Then the ADJ-scan adjustment (D3) enforces Eq. 9-10 plus
+ * p_0 = 0, p_{T_n-1} = Umax_n.  ranges (N,T) int32; padded frames get Umax_n;
+ * infeasible utterances (status bit0) get all-zero ranges.
+ * Uses dims N, T, U, S (V, J ignored).  No workspace.
+ */
+rnnt_status_t rnnt_get_ranges(const float* px_grad, const float* py_grad, const int64_t* boundary,
+                              const rnnt_dims_t* dims, int32_t* ranges, int32_t* status,
+                              void* stream);
+
+/*
+ * Joiner input on the band (joiner form D13):
+ *   h[n,t,s,:] = bf16_rn( tanh(enc_proj[n,t,:] + dec_proj[n,p_t+s,:]) )
+ * for t < T_n and p_t+s <= U_n; every other row (masked slot or padded frame) is 0.
+ *   enc_proj (N,T,J) fp32, dec_proj (N,U+1,J) fp32, ranges (N,T) int32,
+ *   h (N,T,S,J) bf16 (uint16 bits).
+ */
+rnnt_status_t rnnt_prune(const float* enc_proj, const float* dec_proj, const int32_t* ranges,
+                         const int64_t* boundary, const rnnt_dims_t* dims, uint16_t* h,
+                         void* stream);
+
+/*
+ * Pruned loss and gradients.
+ *   z[n,t,s,:] = W_out h[n,t,s,:] + b_out  (V), L(t,p_t+s,.) = log_softmax(z)
+ *   empty_p(t,u) = L(t,u,0), y_p(t,u) = L(t,u,y_{u+1}) (-inf at u=U_n), -inf off-band;
+ *   Eq. 3 recursion over the band -> loss (N) = -L_pruned,n (+inf if infeasible).
+ * Gradients (function merging): dz = gs((g_b+g_l) softmax(z) - g_b[v=0] - g_l[v=y]),
+ *   d_w (V,J) fp32 = sum dz h^T,  d_b (V) fp32 = sum dz  (overwritten, this batch only),
+ *   d_enc (N,T,J) fp32 = sum_s dpre, d_dec (N,U+1,J) fp32 = sum over band rows of dpre,
+ *   dpre = (W^T dz) * (1 - h^2).  d_enc / d_dec may be NULL.
+ *   w_out (V,J) bf16, b_out (V) bf16.
+ */
+rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                               const int64_t* symbols, const int32_t* ranges,
+                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                               float* loss, float* d_enc, float* d_dec, float* d_w, float* d_b,
+                               int32_t* status, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNNT_B200_H */

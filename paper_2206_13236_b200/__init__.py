@@ -1,0 +1,217 @@
+"""B200-native pruned RNN-T loss hot path (arXiv 2206.13236) — Python binding.
+
+Thin ctypes binding over ``librnnt_b200.so`` (the C-ABI of ``include/rnnt.h``):
+argument marshalling only, every step of the path runs in the library's sm_100a
+kernels.  PyTorch supplies device memory and streams.  There is no CPU fallback:
+if the shared library is missing or a tensor is not on a CUDA device, the calls
+raise.
+
+Two layers:
+  * ``rnnt_simple_loss``, ``rnnt_get_ranges``, ``rnnt_prune``, ``rnnt_pruned_loss``,
+    ``rnnt_workspace_bytes`` — same names and argument order as the C-ABI, taking
+    torch tensors (or None for nullable pointers).
+  * ``simple_loss``, ``get_ranges``, ``prune``, ``pruned_loss`` and ``step`` —
+    conveniences that allocate outputs with ``torch.empty`` and call the above.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librnnt_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "rnnt.h")
+
+RNNT_OK = 0
+STATUS_INFEASIBLE = 1
+STATUS_NONFINITE = 2
+STATUS_BAD_SYMBOL = 4
+STATUS_UNDERFLOW = 8
+STATUS_BAD_BOUNDARY = 16
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("T", ctypes.c_int32), ("U", ctypes.c_int32),
+                ("V", ctypes.c_int32), ("J", ctypes.c_int32), ("S", ctypes.c_int32)]
+
+
+class RNNTError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the C-ABI library (raises if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RNNTError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, I32, F, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_float, ctypes.c_size_t
+    DP = ctypes.POINTER(Dims)
+    lib.rnnt_workspace_bytes.argtypes = [DP]
+    lib.rnnt_workspace_bytes.restype = SZ
+    lib.rnnt_status_string.argtypes = [I32]
+    lib.rnnt_status_string.restype = ctypes.c_char_p
+    lib.rnnt_version.argtypes = []
+    lib.rnnt_version.restype = ctypes.c_char_p
+    lib.rnnt_simple_loss.argtypes = [P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
+    lib.rnnt_simple_loss.restype = I32
+    lib.rnnt_get_ranges.argtypes = [P, P, P, DP, P, P, P]
+    lib.rnnt_get_ranges.restype = I32
+    lib.rnnt_prune.argtypes = [P, P, P, P, DP, P, P]
+    lib.rnnt_prune.restype = I32
+    lib.rnnt_pruned_loss.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
+    lib.rnnt_pruned_loss.restype = I32
+    _lib = lib
+    return lib
+
+
+def header_functions(path: str = HEADER_PATH) -> list[str]:
+    """Names of the functions declared in include/rnnt.h."""
+    src = open(path).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rnnt_[a-z_]+)\s*\(", src)))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if not t.is_cuda:
+        raise RNNTError("tensor must be on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise RNNTError("tensor must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(rc: int, what: str):
+    if rc != RNNT_OK:
+        msg = load_library().rnnt_status_string(rc).decode()
+        raise RNNTError(f"{what} failed: {msg}")
+
+
+def make_dims(N, T, U, V, J, S) -> Dims:
+    return Dims(int(N), int(T), int(U), int(V), int(J), int(S))
+
+
+# ----------------------------------------------------------------- C-ABI mirror
+def rnnt_workspace_bytes(dims: Dims) -> int:
+    return int(load_library().rnnt_workspace_bytes(ctypes.byref(dims)))
+
+
+def rnnt_version() -> str:
+    return load_library().rnnt_version().decode()
+
+
+def rnnt_simple_loss(am, lm, symbols, boundary, dims, grad_scale, loss, px_grad, py_grad, am_grad,
+                     lm_grad, status, workspace, stream=None):
+    rc = load_library().rnnt_simple_loss(
+        _ptr(am), _ptr(lm), _ptr(symbols), _ptr(boundary), ctypes.byref(dims), float(grad_scale),
+        _ptr(loss), _ptr(px_grad), _ptr(py_grad), _ptr(am_grad), _ptr(lm_grad), _ptr(status),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_simple_loss")
+
+
+def rnnt_get_ranges(px_grad, py_grad, boundary, dims, ranges, status, stream=None):
+    rc = load_library().rnnt_get_ranges(_ptr(px_grad), _ptr(py_grad), _ptr(boundary), ctypes.byref(dims),
+                                        _ptr(ranges), _ptr(status), _stream(stream))
+    _check(rc, "rnnt_get_ranges")
+
+
+def rnnt_prune(enc_proj, dec_proj, ranges, boundary, dims, h, stream=None):
+    rc = load_library().rnnt_prune(_ptr(enc_proj), _ptr(dec_proj), _ptr(ranges), _ptr(boundary),
+                                   ctypes.byref(dims), _ptr(h), _stream(stream))
+    _check(rc, "rnnt_prune")
+
+
+def rnnt_pruned_loss(h, w_out, b_out, symbols, ranges, boundary, dims, grad_scale, loss, d_enc, d_dec,
+                     d_w, d_b, status, workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss(
+        _ptr(h), _ptr(w_out), _ptr(b_out), _ptr(symbols), _ptr(ranges), _ptr(boundary),
+        ctypes.byref(dims), float(grad_scale), _ptr(loss), _ptr(d_enc), _ptr(d_dec), _ptr(d_w),
+        _ptr(d_b), _ptr(status), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream(stream))
+    _check(rc, "rnnt_pruned_loss")
+
+
+# ----------------------------------------------------------------- conveniences
+class Workspace:
+    """Caches one device workspace per (device, size)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, dims: Dims, device) -> torch.Tensor:
+        need = rnnt_workspace_bytes(dims)
+        if need == 0:
+            raise RNNTError("invalid dims")
+        if self.buf is None or self.buf.numel() < need or self.buf.device != torch.device(device):
+            self.buf = torch.empty(need, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = Workspace()
+
+
+def dims_of(am, lm, w_out, S) -> Dims:
+    N, T, V = am.shape
+    U = lm.shape[1] - 1
+    J = w_out.shape[1]
+    return make_dims(N, T, U, V, J, S)
+
+
+def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
+         pruned_scale=1.0, status=None, workspace=None, out=None, stream=None):
+    """One fwd+bwd of the whole hot path: simple loss and its
+    gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
+    device tensors; ``out`` may supply preallocated outputs (same keys)."""
+    dims = dims_of(am, lm, w_out, S)
+    N, T, U, V, J = dims.N, dims.T, dims.U, dims.V, dims.J
+    dev = am.device
+    o = out if out is not None else alloc_outputs(dims, dev)
+    ws = workspace if workspace is not None else _WS.get(dims, dev)
+    st = o["status"] if status is None else status
+    rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
+                     o["py_grad"], o["am_grad"], o["lm_grad"], st, ws, stream)
+    rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, stream)
+    rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], stream)
+    rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
+                     o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, stream)
+    return o
+
+
+def alloc_outputs(dims: Dims, device) -> dict:
+    N, T, U, V, J, S = dims.N, dims.T, dims.U, dims.V, dims.J, dims.S
+    f32 = dict(dtype=torch.float32, device=device)
+    return dict(
+        loss_simple=torch.empty(N, **f32), px_grad=torch.empty(N, T, U + 1, **f32),
+        py_grad=torch.empty(N, T, U + 1, **f32), am_grad=torch.empty(N, T, V, **f32),
+        lm_grad=torch.empty(N, U + 1, V, **f32),
+        ranges=torch.empty(N, T, dtype=torch.int32, device=device),
+        h=torch.empty(N, T, S, J, dtype=torch.int16, device=device),
+        loss_pruned=torch.empty(N, **f32), d_enc=torch.empty(N, T, J, **f32),
+        d_dec=torch.empty(N, U + 1, J, **f32), d_w=torch.empty(V, J, **f32), d_b=torch.empty(V, **f32),
+        status=torch.zeros(N, dtype=torch.int32, device=device))
+
+
+def batch_to_device(batch, device="cuda") -> dict:
+    """Move a ``synth.Batch`` to device tensors (bf16 weights as int16 bit patterns)."""
+    import numpy as np
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    return dict(am=t(batch.am), lm=t(batch.lm), symbols=t(batch.symbols), boundary=t(batch.boundary),
+                enc_proj=t(batch.enc_proj), dec_proj=t(batch.dec_proj),
+                w_out=t(batch.w_out_bits.view(np.int16)), b_out=t(batch.b_out_bits.view(np.int16)))

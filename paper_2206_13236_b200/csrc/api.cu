@@ -1,0 +1,128 @@
+// api.cu — the C-ABI entry points of include/rnnt.h: argument validation, workspace
+// carving and launch sequencing.  Every call only enqueues on the caller's stream.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rnnt.h"
+#include "workspace.h"
+
+namespace rnnt {
+cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
+                               const int64_t* sym, const int64_t* bnd, float gs, float* loss,
+                               float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
+                               int32_t* status, cudaStream_t st);
+cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* py_grad, const int64_t* bnd,
+                              int32_t* ranges, int32_t* status, cudaStream_t st);
+cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
+                         const int64_t* bnd, uint16_t* h, cudaStream_t st);
+size_t pruned_recursion_smem(const Dims& d);
+cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                               const uint16_t* b, const int64_t* sym, const int32_t* ranges,
+                               const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
+                               float* d_w, float* d_b, int32_t* status, cudaStream_t st);
+}  // namespace rnnt
+
+using namespace rnnt;
+
+static bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static rnnt_status_t check_dims(const rnnt_dims_t* dims, Dims* d) {
+  if (!dims) return RNNT_ERR_INVALID_ARG;
+  d->N = dims->N; d->T = dims->T; d->U = dims->U; d->V = dims->V; d->J = dims->J; d->S = dims->S;
+  if (d->N < 1 || d->T < 1 || d->T > 65536 || d->U < 0 || d->V < 2 || d->S < 1 || d->S > 32)
+    return RNNT_ERR_INVALID_ARG;
+  if ((long long)d->U >= (long long)d->T * 64) return RNNT_ERR_INVALID_ARG;
+  if (d->J < 8 || d->J > 4096 || d->J % 8) return RNNT_ERR_INVALID_ARG;
+  if (d->LU() > 2048) return RNNT_ERR_UNSUPPORTED;   // recursion kernel: <= 8 warps x 8 columns
+  return RNNT_OK;
+}
+
+static rnnt_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? RNNT_OK : RNNT_ERR_CUDA; }
+
+extern "C" {
+
+size_t rnnt_workspace_bytes(const rnnt_dims_t* dims) {
+  Dims d;
+  if (check_dims(dims, &d) != RNNT_OK) return 0;
+  return carve(d, nullptr, nullptr, nullptr);
+}
+
+const char* rnnt_status_string(rnnt_status_t s) {
+  switch (s) {
+    case RNNT_OK: return "RNNT_OK";
+    case RNNT_ERR_INVALID_ARG: return "RNNT_ERR_INVALID_ARG";
+    case RNNT_ERR_UNSUPPORTED: return "RNNT_ERR_UNSUPPORTED";
+    case RNNT_ERR_WORKSPACE: return "RNNT_ERR_WORKSPACE";
+    case RNNT_ERR_CUDA: return "RNNT_ERR_CUDA";
+  }
+  return "RNNT_ERR_UNKNOWN";
+}
+
+const char* rnnt_version(void) { return "rnnt-b200 0.1 sm_100a (simt-v0 contractions)"; }
+
+static void* align_ws(void* ws) {
+  uintptr_t p = reinterpret_cast<uintptr_t>(ws);
+  return reinterpret_cast<void*>((p + 255) & ~uintptr_t(255));
+}
+
+rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* symbols,
+                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                               float* loss, float* px_grad, float* py_grad, float* am_grad,
+                               float* lm_grad, int32_t* status, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!am || !lm || !boundary || !loss || !px_grad || !py_grad || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(am) || !aligned16(lm)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(simple_loss_launch(d, sw, am, lm, symbols, boundary, grad_scale, loss, px_grad, py_grad,
+                                        am_grad, lm_grad, status, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_get_ranges(const float* px_grad, const float* py_grad, const int64_t* boundary,
+                              const rnnt_dims_t* dims, int32_t* ranges, int32_t* status, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!px_grad || !py_grad || !boundary || !ranges) return RNNT_ERR_INVALID_ARG;
+  return cuda_status(get_ranges_launch(d, px_grad, py_grad, boundary, ranges, status, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_prune(const float* enc_proj, const float* dec_proj, const int32_t* ranges,
+                         const int64_t* boundary, const rnnt_dims_t* dims, uint16_t* h, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!enc_proj || !dec_proj || !ranges || !boundary || !h) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(enc_proj) || !aligned16(dec_proj) || !aligned16(h)) return RNNT_ERR_INVALID_ARG;
+  return cuda_status(prune_launch(d, enc_proj, dec_proj, ranges, boundary, h, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                               const int64_t* symbols, const int32_t* ranges,
+                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                               float* loss, float* d_enc, float* d_dec, float* d_w, float* d_b,
+                               int32_t* status, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!h || !w_out || !b_out || !ranges || !boundary || !loss || !d_w || !d_b || !workspace)
+    return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(w_out)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  if (pruned_recursion_smem(d) > 200 * 1024) return RNNT_ERR_UNSUPPORTED;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_loss_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss,
+                                        d_enc, d_dec, d_w, d_b, status, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// workspace.h — carving of the caller-provided device workspace (host + device).
+// The simple-loss region and the pruned-loss region are disjoint, so one
+// workspace can serve rnnt_simple_loss and rnnt_pruned_loss concurrently.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+namespace rnnt {
+
+struct Dims {
+  int N, T, U, V, J, S;
+  int U1() const { return U + 1; }
+  int LU() const { return ((U + 1) + 7) / 8 * 8; }   // skewed row length (u), padded
+  int K() const { return T + U; }                       // number of anti-diagonals
+  long long rows() const { return (long long)N * T * S; }
+  int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
+};
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct SimpleWS {
+  float* m_am;    // (N,T)     row max of am
+  float* m_lm;    // (N,U+1)   row max of lm
+  float* px2;     // (N,K+1,LU) skewed y(t,u)*log2e      (k = t+u)
+  float* py2;     // (N,K+1,LU) skewed empty(t,u)*log2e
+  float* rS;      // (N,K+1,LU) skewed 1/sum_v exp(am-m_am+lm-m_lm)
+  double* alpha;  // (N,K+1,LU) skewed alpha*log2e (fp64)
+  double* beta;   // (N,K+1,LU) skewed beta*log2e  (fp64)
+  double* Ltot;   // (N)        L_tot (natural log)
+  float* Gt;      // (N,T,U+1)  (y'+empty') / S(t,u)   (t-major)
+};
+
+struct PrunedWS {
+  int32_t* rowinfo;  // (R) label y_{u+1} (V if u==U_n), -1 for masked/padded rows
+  float* z;          // (R,V) fp32 logits scratch (SIMT v0 path only)
+  uint16_t* Pt;      // (R,V) bf16 exp(z - m_tile)
+  float* mt;         // (R,ntile) tile maxima of z
+  float* lse;        // (R) log-sum-exp of z
+  float* px2;        // (R) y_p * log2e (band arcs)
+  float* py2;        // (R) empty_p * log2e
+  double* ap;        // (R) pruned alpha (log2)
+  double* bp;        // (R) pruned beta (log2)
+  double* Lp;        // (N) L_pruned
+  float* gb;         // (R) empty'_p
+  float* gl;         // (R) y'_p
+  float* sc;         // (R,ntile) gs*(gb+gl)*exp(m_tile-lse)
+  float* dpre;       // (R,J) fp32
+  float* dWp;        // (splits,V,J) split-K partials of d_w
+  float* dbp;        // (splits,V)   split-K partials of d_b
+  int splits;
+};
+
+inline int dw_splits(const Dims& d) {
+  long long rows = d.rows();
+  int s = (int)((rows + 4095) / 4096);
+  if (s < 1) s = 1;
+  if (s > 64) s = 64;
+  return s;
+}
+
+// Returns total bytes; if base != nullptr fills the structs.
+inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) -> void* {
+    void* p = b ? (void*)(b + off) : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const size_t N = d.N, T = d.T, U1 = d.U1(), LU = d.LU(), K1 = d.K() + 1;
+  const size_t R = (size_t)d.rows(), V = d.V, J = d.J, NT = d.ntile();
+  SimpleWS s;
+  s.m_am = (float*)take(N * T * 4);
+  s.m_lm = (float*)take(N * U1 * 4);
+  s.px2 = (float*)take(N * K1 * LU * 4);
+  s.py2 = (float*)take(N * K1 * LU * 4);
+  s.rS = (float*)take(N * K1 * LU * 4);
+  s.alpha = (double*)take(N * K1 * LU * 8);
+  s.beta = (double*)take(N * K1 * LU * 8);
+  s.Ltot = (double*)take(N * 8);
+  s.Gt = (float*)take(N * T * U1 * 4);
+  PrunedWS p;
+  p.splits = dw_splits(d);
+  p.rowinfo = (int32_t*)take(R * 4);
+  p.z = (float*)take(R * V * 4);
+  p.Pt = (uint16_t*)take(R * V * 2);
+  p.mt = (float*)take(R * NT * 4);
+  p.lse = (float*)take(R * 4);
+  p.px2 = (float*)take(R * 4);
+  p.py2 = (float*)take(R * 4);
+  p.ap = (double*)take(R * 8);
+  p.bp = (double*)take(R * 8);
+  p.Lp = (double*)take(N * 8);
+  p.gb = (float*)take(R * 4);
+  p.gl = (float*)take(R * 4);
+  p.sc = (float*)take(R * NT * 4);
+  p.dpre = (float*)take(R * J * 4);
+  p.dWp = (float*)take((size_t)p.splits * V * J * 4);
+  p.dbp = (float*)take((size_t)p.splits * V * 4);
+  if (sw) *sw = s;
+  if (pw) *pw = p;
+  return off + 256;  // slack for base alignment
+}
+
+}  // namespace rnnt

@@ -1,0 +1,172 @@
+"""GPU parity: every C-ABI stage against the fp64 oracle on the same seeded inputs.
+
+Each stage gets its inputs from the generator or the oracle (never from the CUDA
+path) so a mismatch is attributable to one stage.  Tolerances: gpu_common.py."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from gpu_common import (OCC_ATOL, assert_bf16_grad, assert_close_abs, assert_loss, oracle_h_bits,
+                        run_prune, run_pruned, run_ranges, run_simple, to_dev)
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_simple(b, gs=0.5):
+    r = dict(loss=np.zeros(b.N), px_grad=np.zeros((b.N, b.T, b.U + 1)), py_grad=np.zeros((b.N, b.T, b.U + 1)),
+             am_grad=np.zeros((b.N, b.T, b.V)), lm_grad=np.zeros((b.N, b.U + 1, b.V)))
+    for n in range(b.N):
+        d = b.utterance(n)
+        s = O.simple_loss(d["am"], d["lm"], d["y"], gs)
+        T, U = d["T"], d["U"]
+        r["loss"][n] = s["loss"]
+        r["px_grad"][n, :T, :U + 1] = s["px_grad"]
+        r["py_grad"][n, :T, :U + 1] = s["py_grad"]
+        r["am_grad"][n, :T] = s["am_grad"]
+        r["lm_grad"][n, :U + 1] = s["lm_grad"]
+    return r
+
+
+def _oracle_ranges(b, pxg, pyg):
+    rg = np.zeros((b.N, b.T), np.int64)
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        if not O.feasible(T, U, b.S):
+            continue
+        rg[n, :T] = O.adjust_bounds(O.raw_bounds(pxg[n, :T, :U + 1], pyg[n, :T, :U + 1], b.S), T, U, b.S)
+        rg[n, T:] = O.umax(U, b.S)
+    return rg
+
+
+def _oracle_pruned(b, ranges, gs=1.0):
+    r = dict(loss=np.zeros(b.N), d_enc=np.zeros((b.N, b.T, b.J)), d_dec=np.zeros((b.N, b.U + 1, b.J)),
+             d_w=np.zeros((b.V, b.J)), d_b=np.zeros(b.V))
+    for n in range(b.N):
+        d = b.utterance(n)
+        T, U = d["T"], d["U"]
+        if not O.feasible(T, U, b.S):
+            r["loss"][n] = np.inf
+            continue
+        p = O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"], ranges[n, :T], b.S, gs, matched=True)
+        r["loss"][n] = p["loss"]
+        r["d_enc"][n, :T] = p["d_enc"]
+        r["d_dec"][n, :U + 1] = p["d_dec"]
+        r["d_w"] += p["d_w"]
+        r["d_b"] += p["d_b"]
+    return r
+
+
+def check_simple(b):
+    g = run_simple(b)
+    o = _oracle_simple(b)
+    assert_loss(g["loss_simple"], o["loss"], "loss_simple")
+    assert_close_abs(g["px_grad"], o["px_grad"], OCC_ATOL, "px_grad")
+    assert_close_abs(g["py_grad"], o["py_grad"], OCC_ATOL, "py_grad")
+    assert_close_abs(g["am_grad"], o["am_grad"], OCC_ATOL, "am_grad")
+    assert_close_abs(g["lm_grad"], o["lm_grad"], OCC_ATOL, "lm_grad")
+    return g, o
+
+
+def check_ranges(b, o):
+    pxg = o["px_grad"].astype(np.float32)
+    pyg = o["py_grad"].astype(np.float32)
+    rg, st = run_ranges(b, pxg, pyg)
+    ref = _oracle_ranges(b, pxg, pyg)
+    assert np.array_equal(rg, ref), f"ranges differ at {np.argwhere(rg != ref)[:5]}"
+    return ref
+
+
+def check_prune(b, ranges):
+    h = run_prune(b, ranges)
+    ref = oracle_h_bits(b, ranges)
+    diff = h.astype(np.int32) - ref.astype(np.int32)
+    assert np.abs(diff).max() <= 1, "h differs by more than one bf16 ulp"
+    assert np.count_nonzero(diff) <= 1e-3 * diff.size, f"{np.count_nonzero(diff)} 1-ulp flips"
+    return ref
+
+
+def check_pruned(b, ranges, h_ref):
+    g = run_pruned(b, h_ref, ranges)
+    o = _oracle_pruned(b, ranges)
+    assert_loss(g["loss_pruned"], o["loss"], "loss_pruned")
+    for k in ("d_w", "d_b", "d_enc", "d_dec"):
+        assert_bf16_grad(g[k], o[k], k)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_stagewise_parity(cfg):
+    b = synth.make_batch(cfg)
+    g, o = check_simple(b)
+    ranges = check_ranges(b, o)
+    h_ref = check_prune(b, ranges)
+    check_pruned(b, ranges, h_ref)
+
+
+@pytest.mark.parametrize("case", [
+    dict(T=[1, 5, 9], U=[0, 0, 3], V=7, J=8, S=2),        # T=1, U=0 single-path utterances
+    dict(T=[40, 3, 17], U=[13, 2, 16], V=33, J=16, S=4),  # ragged, one S >= U+1, one U = T-1
+    dict(T=[70, 66], U=[40, 2], V=300, J=24, S=1),        # S = 1 (U=40 infeasible, U=2 infeasible)
+    dict(T=[7, 30], U=[20, 9], V=11, J=8, S=3),           # U=20 > T(S-1)=14 infeasible
+    dict(T=[300, 129], U=[257, 60], V=40, J=16, S=6),     # U+1 > 256: multi-warp recursion
+])
+def test_edge_cases(case):
+    b = synth.make_custom(case["T"], case["U"], case["V"], case["J"], case["S"], seed=11, logit_scale=2.0)
+    g, o = check_simple(b)
+    ranges = check_ranges(b, o)
+    h_ref = check_prune(b, ranges)
+    check_pruned(b, ranges, h_ref)
+
+
+def test_poison_padding():
+    """NaN in every padded input element: outputs finite, padded outputs exactly 0."""
+    b = synth.make_custom([12, 30, 5], [4, 9, 1], 19, 16, 3, seed=3, poison=True)
+    g = run_simple(b)
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        for k in ("px_grad", "py_grad"):
+            assert np.all(np.isfinite(g[k][n]))
+            assert np.all(g[k][n, T:] == 0) and np.all(g[k][n, :, U + 1:] == 0)
+        assert np.all(g["am_grad"][n, T:] == 0) and np.all(np.isfinite(g["am_grad"][n]))
+        assert np.all(g["lm_grad"][n, U + 1:] == 0) and np.all(np.isfinite(g["lm_grad"][n]))
+    o = _oracle_simple(b)
+    ranges = _oracle_ranges(b, o["px_grad"].astype(np.float32), o["py_grad"].astype(np.float32))
+    h = run_prune(b, ranges)
+    h_ref = oracle_h_bits(b, ranges)
+    assert np.abs(h.astype(np.int32) - h_ref.astype(np.int32)).max() <= 1
+    p = run_pruned(b, h_ref, ranges)
+    for k in ("d_w", "d_b", "d_enc", "d_dec", "loss_pruned"):
+        assert np.all(np.isfinite(p[k]))
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        assert np.all(p["d_enc"][n, T:] == 0) and np.all(p["d_dec"][n, U + 1:] == 0)
+
+
+def test_end_to_end_step_config2():
+    """The whole path on the GPU (its own ranges) against the whole oracle path.  Ranges may
+    differ only at frames whose oracle Eq. 8 top-2 gap is below 2(S+1)*1e-4 (D5); the pruned
+    loss is compared for utterances whose ranges agree."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    dev = to_dev(b)
+    o = R.step(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], dev["enc_proj"], dev["dec_proj"],
+               dev["w_out"], dev["b_out"], b.S)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in o.items()}
+    ref = O.full_step(b)
+    assert_loss(g["loss_simple"], ref["loss_simple"], "loss_simple")
+    mism = 0
+    same = []
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        diff = np.nonzero(g["ranges"][n, :T] != ref["ranges"][n, :T])[0]
+        mism += len(diff)
+        for t in diff:
+            v = O.bound_scores(ref["px_grad"][n, t, :U + 1], ref["py_grad"][n, t, :U + 1], b.S)
+            top = np.sort(v)[-2:]
+            assert top[1] - top[0] < 2 * (b.S + 1) * 1e-4, f"utt {n} frame {t}: not a near-tie"
+        if len(diff) == 0:
+            same.append(n)
+    assert len(same) > 0
+    assert_loss(g["loss_pruned"][same], ref["loss_pruned"][same], "loss_pruned")

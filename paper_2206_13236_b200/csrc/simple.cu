@@ -394,9 +394,9 @@ __global__ void am_picks_kernel(const float* __restrict__ px_grad, const float* 
   const float* yr = px_grad + ((size_t)n * T + t) * (U + 1);
   const float* br = py_grad + ((size_t)n * T + t) * (U + 1);
   float* g = am_grad + ((size_t)n * T + t) * V;
-  float sb = 0.f;
-  for (int u = 0; u <= Un; ++u) sb += br[u];
-  g[0] -= gs * sb;
+  double sb = 0.0;
+  for (int u = 0; u <= Un; ++u) sb += (double)br[u];
+  g[0] = (float)((double)g[0] - (double)gs * sb);
   for (int u = 0; u < Un; ++u) {
     long long y = sym[(size_t)n * U + u];
     if (y < 1 || y >= V) continue;
@@ -413,17 +413,17 @@ __global__ void lm_picks_kernel(const float* __restrict__ px_grad, const float* 
   int n = (int)(i / (U + 1)), u = (int)(i % (U + 1));
   int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   if (u > Un) return;
-  float sy = 0.f, sb = 0.f;
+  double sy = 0.0, sb = 0.0;
   for (int t = 0; t < Tn; ++t) {
     size_t o = ((size_t)n * T + t) * (U + 1) + u;
-    sy += px_grad[o];
-    sb += py_grad[o];
+    sy += (double)px_grad[o];
+    sb += (double)py_grad[o];
   }
   float* g = lm_grad + ((size_t)n * (U + 1) + u) * V;
-  g[0] -= gs * sb;
+  g[0] = (float)((double)g[0] - (double)gs * sb);
   if (u < Un) {
     long long y = sym[(size_t)n * U + u];
-    if (y >= 1 && y < V) g[y] -= gs * sy;
+    if (y >= 1 && y < V) g[y] = (float)((double)g[y] - (double)gs * sy);
   }
 }
 

@@ -86,8 +86,15 @@ def assert_bf16_grad(got, ref, name):
 
 
 def assert_close_abs(got, ref, atol, name):
-    err = np.max(np.abs(got - ref)) if got.size else 0.0
-    assert err <= atol, f"{name}: max|d|={err:.3e} > {atol:.1e}"
+    """|got - ref| <= atol * max(1, |ref|) elementwise: 1e-4 absolute for O(1) values (occupancies
+    in [0,1], most gradient entries), relative for the few entries far above 1 (e.g. lm_grad[u,0]
+    ~ -170 sums hundreds of blank occupancies, where an fp32 ulp alone is 1.5e-5).  DESIGN.md D6."""
+    if not got.size:
+        return
+    lim = atol * np.maximum(1.0, np.abs(ref))
+    bad = np.abs(got - ref) > lim
+    assert not bad.any(), (f"{name}: {bad.sum()} elements off, worst |d|="
+                           f"{np.max(np.abs(got - ref)):.3e} (ref there {ref.flat[np.argmax(np.abs(got - ref))]:.4g})")
 
 
 def assert_loss(got, ref, name):

@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the pruned RNN-T loss hot path (fwd+bwd) on B200 — BASELINE.json metric.
+
+One "step" = the whole hot path over one batch: rnnt_simple_loss (with am/lm grads),
+rnnt_get_ranges, rnnt_prune, rnnt_pruned_loss (all grads), plus the NCCL allreduce of
+d_w, d_b and the loss when world_size > 1.  Workload: BASELINE configs[1] (c2,
+LibriSpeech-shaped BPE, N=32 per GPU) at N=1; configs[4] (c5, same recipe, 32 per GPU,
+rank-seeded) when run under torchrun with N>1.  Synthetic seeded inputs (synth/).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "pruned RNN-T loss fwd+bwd frames(N·T)/sec and peak GB, 1/2/4/8 B200"
+UNIT = "frames/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=0, help="override BASELINE config (1-5)")
+    ap.add_argument("--profile-kernel", default="auto")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, world, rank):
+    cfg = args.config or (2 if world == 1 else 5)
+    b = synth.make_batch(cfg, rank=rank)
+    name = {2: "c2 LibriSpeech-shaped BPE (BASELINE configs[1])",
+            5: "c5 8-GPU data-parallel, c2 shapes 32/GPU (BASELINE configs[4])"}.get(cfg, synth.CONFIGS[cfg]["name"])
+    return cfg, b, name
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ roofline table
+def algorithmic(kernel, b):
+    """Algorithmic work of one launch of ``kernel`` on batch ``b``."""
+    T = b.T_n.astype(np.int64)
+    U1 = b.U_n.astype(np.int64) + 1
+    rows = int((T * b.S).sum())                 # real band rows sum_n T_n * S
+    V, J = b.V, b.J
+    if kernel in ("joiner_fwd_gemm", "joiner_dh_gemm", "joiner_dw_gemm"):
+        return "tensor", 2.0 * rows * J * V, "TFLOP/s"
+    if kernel == "simple_norm_gemm":
+        return "tensor", 2.0 * float((T * U1).sum()) * V, "TFLOP/s"
+    if kernel == "prune_gather":
+        # read enc row once per frame (L2 reuse across s) + dec rows, write h (bf16)
+        return "hbm", float(T.sum() * J * 4 + U1.sum() * J * 4 + rows * J * 2), "GB/s"
+    raise KeyError(kernel)
+
+
+def peaks():
+    p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    return (p.get("hbm_gbs", 6650.0), p.get("bf16_tflops_sustained", 1400.0),
+            "measured" if p else "fallback")
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def time_oracle(b, seconds, utt_order=None):
+    """Time the fp64 oracle (as it stands) on whole utterances of ``b`` until ``seconds``
+    elapse; returns (frames/s, frames, utts, elapsed, threads)."""
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        limiter = threadpool_limits(limits=1)
+    except Exception:
+        limiter = None
+    order = list(range(b.N)) if utt_order is None else utt_order
+    frames = 0
+    used = []
+    t0 = time.perf_counter()
+    for n in order:
+        d = b.utterance(n)
+        s = O.simple_loss(d["am"], d["lm"], d["y"], 0.5)
+        pxg, pyg = s["px_grad"].astype(np.float32), s["py_grad"].astype(np.float32)
+        if O.feasible(d["T"], d["U"], d["S"]):
+            p = O.adjust_bounds(O.raw_bounds(pxg, pyg, d["S"]), d["T"], d["U"], d["S"])
+            O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"], p, d["S"], 1.0, matched=True)
+        frames += d["T"]
+        used.append(n)
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    return frames / el, frames, used, el, 1
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    cfg, b, name = workload(args, 1, 0)
+    steps, warm = args.steps, args.warmup
+    per_step = 1   # utterances per step: a bounded sample so K+W steps finish in minutes
+    k = 0
+    for _ in range(warm):
+        time_oracle(b, 0.0, [k % b.N]); k += 1
+    frames = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        _, f, _, _, _ = time_oracle(b, 0.0, [(k + i) % b.N for i in range(per_step)])
+        frames += f
+        k += per_step
+    el = time.perf_counter() - t0
+    v = frames / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": 1000 * el / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "N": b.N, "V": b.V, "J": b.J, "S": b.S,
+                       "sample": f"{per_step} utterance(s) of the batch per step, rotating"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{steps} steps x {per_step} utterance(s), fp64 numpy, BLAS 1 thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    import torch
+    import paper_2206_13236_b200 as R
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    cfg, b, name = workload(args, world, rank)
+    dev = R.batch_to_device(b, "cuda")
+    dims = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
+    outs = R.alloc_outputs(dims, "cuda")
+    ws = torch.empty(R.rnnt_workspace_bytes(dims), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step(inp):
+        outs["status"].zero_()
+        R.step(inp["am"], inp["lm"], inp["symbols"], inp["boundary"], inp["enc_proj"], inp["dec_proj"],
+               inp["w_out"], inp["b_out"], b.S, out=outs, workspace=ws)
+        if pg is not None:
+            pg.all_reduce(outs["d_w"])
+            pg.all_reduce(outs["d_b"])
+            pg.all_reduce(outs["loss_pruned"][:1])
+
+    ids = R.kernel_ids()
+    kname = args.profile_kernel if args.profile_kernel != "auto" else "joiner_fwd_gemm"
+    kid = ids[kname]
+
+    for _ in range(args.warmup):
+        step(dev)
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.reset_peak_memory_stats()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, c in kev:   # materialise the event handles
+        a.record(); c.record()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = R.rnnt_launch_count()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    for i in range(K):
+        flush.zero_()                       # evict L2 between timed steps
+        R.rnnt_profile_kernel(kid, kev[i][0], kev[i][1])
+        ev[i][0].record(stream)
+        step(dev)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    R.rnnt_profile_kernel(0)
+    launches = R.rnnt_launch_count() - launches0
+    if pg is not None:
+        pg.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(c) for a, c in ev]
+    kern_ms = [a.elapsed_time(c) for a, c in kev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if pg is not None:
+        pg.all_reduce(tot, op=pg.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / K
+    frames_local = int(b.T_n.sum())
+    fr = torch.tensor([frames_local], dtype=torch.float64, device="cuda")
+    if pg is not None:
+        pg.all_reduce(fr)
+    frames = float(fr.item())
+    value = frames / (ms_per_step / 1000.0)
+    peak_gib = torch.cuda.max_memory_allocated() / 2 ** 30
+    # inputs+outputs+workspace actually held by the step (the flush buffer excluded)
+    step_gib = (peak_gib - flush.numel() / 2 ** 30)
+
+    # roofline of the profiled kernel
+    hbm, tfl, src = peaks()
+    bound, work, unit = algorithmic(kname, b)
+    kmean = statistics.mean(kern_ms)
+    if bound == "tensor":
+        achieved = work / (kmean / 1000) / 1e12
+        peak = tfl
+    else:
+        achieved = work / (kmean / 1000) / 1e9
+        peak = hbm
+    roof = {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": None, "kernel_ms": kmean,
+            "share_of_step": kmean / statistics.mean(step_ms), "peak_source": src}
+
+    # end-to-end: host pinned inputs -> device, step, loss -> host, all inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = {k: v.cpu().pin_memory() for k, v in dev.items()}
+        dbuf = {k: torch.empty_like(v) for k, v in dev.items()}
+        h2d = sum(v.numel() * v.element_size() for k, v in host.items() if k not in ("w_out", "b_out"))
+        loss_host = torch.empty(2, b.N, dtype=torch.float32).pin_memory()
+        d2h = loss_host.numel() * 4
+
+        def e2e_step():
+            for k, v in host.items():
+                if k in ("w_out", "b_out"):
+                    continue
+                dbuf[k].copy_(v, non_blocking=True)
+            dbuf["w_out"] = dev["w_out"]
+            dbuf["b_out"] = dev["b_out"]
+            step(dbuf)
+            loss_host[0].copy_(outs["loss_simple"], non_blocking=True)
+            loss_host[1].copy_(outs["loss_pruned"], non_blocking=True)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for i in range(K):
+            flush.zero_()
+            eev[i][0].record(stream)
+            e2e_step()
+            eev[i][1].record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([sum(a.elapsed_time(c) for a, c in eev)], dtype=torch.float64, device="cuda")
+        if pg is not None:
+            pg.all_reduce(et, op=pg.ReduceOp.MAX)
+        e_ms = float(et.item()) / K
+        e2e = {"value": frames / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, f, used, el, cores = time_oracle(b, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{len(used)} of {b.N} utterances ({f} frames) of the same batch, full fwd+bwd "
+                         f"oracle path, {el:.1f}s, fp64 numpy with BLAS limited to 1 thread"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16+f32", "data": "synthetic",
+                "config": {"workload": name, "N_per_gpu": b.N, "V": b.V, "J": b.J, "S": b.S,
+                           "frames": int(frames), "frames_per_gpu": frames_local,
+                           "padded_frames_per_gpu": int(b.N * b.T),
+                           "l2": "flushed between timed steps (256 MiB write, outside the timed events)",
+                           "kernels": R.rnnt_version()},
+                "peak_gib": step_gib, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk,
+                "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)}}
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

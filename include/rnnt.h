@@ -79,6 +79,19 @@ const char* rnnt_status_string(rnnt_status_t s);
 /* Library build string: kernels compiled and the sm target. */
 const char* rnnt_version(void);
 
+/* ---- Diagnostics (bench.py; not needed for computing the loss) ----
+ * rnnt_launch_count: number of kernels the library has launched from the calling host
+ *   thread (monotone counter).
+ * rnnt_kernel_count / rnnt_kernel_name: ids 1..count-1 of the library's kernel launch sites.
+ * rnnt_profile_kernel: from the calling thread on, every launch of kernel `kernel_id` is
+ *   bracketed by cudaEventRecord(start_event) / cudaEventRecord(stop_event) on the launch
+ *   stream (events are cudaEvent_t passed as void*, owned by the caller); id 0 disarms.
+ *   Returns RNNT_ERR_INVALID_ARG for an unknown id. */
+uint64_t rnnt_launch_count(void);
+int32_t rnnt_kernel_count(void);
+const char* rnnt_kernel_name(int32_t id);
+rnnt_status_t rnnt_profile_kernel(int32_t kernel_id, void* start_event, void* stop_event);
+
 /*
  * Trivial-joiner loss, occupancies and gradients.
  *   am  (N,T,V) fp32   L_enc(t,v)

@@ -69,6 +69,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_prune.restype = I32
     lib.rnnt_pruned_loss.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
     lib.rnnt_pruned_loss.restype = I32
+    lib.rnnt_launch_count.argtypes = []
+    lib.rnnt_launch_count.restype = ctypes.c_uint64
+    lib.rnnt_kernel_count.argtypes = []
+    lib.rnnt_kernel_count.restype = I32
+    lib.rnnt_kernel_name.argtypes = [I32]
+    lib.rnnt_kernel_name.restype = ctypes.c_char_p
+    lib.rnnt_profile_kernel.argtypes = [I32, P, P]
+    lib.rnnt_profile_kernel.restype = I32
     _lib = lib
     return lib
 
@@ -115,6 +123,24 @@ def rnnt_workspace_bytes(dims: Dims) -> int:
 
 def rnnt_version() -> str:
     return load_library().rnnt_version().decode()
+
+
+def rnnt_launch_count() -> int:
+    return int(load_library().rnnt_launch_count())
+
+
+def kernel_ids() -> dict:
+    """{kernel name: id} of the library's launch sites."""
+    lib = load_library()
+    return {lib.rnnt_kernel_name(i).decode(): i for i in range(1, lib.rnnt_kernel_count())}
+
+
+def rnnt_profile_kernel(kernel_id: int, start_event=None, stop_event=None):
+    """Bracket every later launch of ``kernel_id`` (from this thread) with the two
+    torch.cuda.Event objects (recorded on the launch stream); kernel_id 0 disarms."""
+    s = ctypes.c_void_p(start_event.cuda_event) if start_event is not None else None
+    e = ctypes.c_void_p(stop_event.cuda_event) if stop_event is not None else None
+    _check(load_library().rnnt_profile_kernel(int(kernel_id), s, e), "rnnt_profile_kernel")
 
 
 def rnnt_simple_loss(am, lm, symbols, boundary, dims, grad_scale, loss, px_grad, py_grad, am_grad,

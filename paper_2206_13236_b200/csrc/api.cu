@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/rnnt.h"
+#include "launch.h"
 #include "workspace.h"
 
 namespace rnnt {
@@ -20,6 +21,29 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
                                const uint16_t* b, const int64_t* sym, const int32_t* ranges,
                                const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
                                float* d_w, float* d_b, int32_t* status, cudaStream_t st);
+}  // namespace rnnt
+
+namespace rnnt {
+static thread_local unsigned long long g_launches = 0;
+static thread_local int g_prof_id = 0;
+static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+
+static const char* const kNames[KID_COUNT] = {
+    "none", "validate", "rowmax_am", "rowmax_lm", "simple_norm_gemm", "lattice_alpha", "lattice_beta",
+    "lattice_combine", "simple_am_grad_gemm", "simple_am_picks", "simple_lm_grad_gemm", "simple_lm_picks",
+    "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
+    "pruned_alpha", "pruned_beta", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",
+    "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad"};
+
+const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }
+
+void launch_begin(int id, cudaStream_t st) {
+  if (id == g_prof_id && g_prof_start) cudaEventRecord(g_prof_start, st);
+}
+void launch_end(int id, cudaStream_t st) {
+  ++g_launches;
+  if (id == g_prof_id && g_prof_stop) cudaEventRecord(g_prof_stop, st);
+}
 }  // namespace rnnt
 
 using namespace rnnt;
@@ -58,7 +82,21 @@ const char* rnnt_status_string(rnnt_status_t s) {
   return "RNNT_ERR_UNKNOWN";
 }
 
-const char* rnnt_version(void) { return "rnnt-b200 0.1 sm_100a (simt-v0 contractions)"; }
+uint64_t rnnt_launch_count(void) { return g_launches; }
+
+int32_t rnnt_kernel_count(void) { return KID_COUNT; }
+
+const char* rnnt_kernel_name(int32_t id) { return kernel_name(id); }
+
+rnnt_status_t rnnt_profile_kernel(int32_t kernel_id, void* start_event, void* stop_event) {
+  if (kernel_id < 0 || kernel_id >= KID_COUNT) return RNNT_ERR_INVALID_ARG;
+  g_prof_id = kernel_id;
+  g_prof_start = (cudaEvent_t)start_event;
+  g_prof_stop = (cudaEvent_t)stop_event;
+  return RNNT_OK;
+}
+
+const char* rnnt_version(void) { return "rnnt-b200 0.1 sm_100a (joiner_fwd: tcgen05; other contractions: simt-v0)"; }
 
 static void* align_ws(void* ws) {
   uintptr_t p = reinterpret_cast<uintptr_t>(ws);

@@ -1,0 +1,29 @@
+// launch.h — host-side launch bookkeeping: a per-thread count of kernels launched by the
+// library (bench.py's gpu_launches) and an optional per-kernel CUDA-event hook so the bench
+// can time one kernel live on the stream it is launched on (rnnt_profile_kernel).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace rnnt {
+
+enum KernelId {
+  KID_NONE = 0,
+  KID_VALIDATE, KID_ROWMAX_AM, KID_ROWMAX_LM, KID_NORM, KID_ALPHA, KID_BETA, KID_COMBINE,
+  KID_AMGRAD, KID_AMPICK, KID_LMGRAD, KID_LMPICK, KID_RAW, KID_ADJUST, KID_PRUNE, KID_ROWINFO,
+  KID_JOINER_FWD, KID_SOFTMAX, KID_PALPHA, KID_PBETA, KID_PCOMBINE, KID_DH, KID_DENC, KID_DDEC,
+  KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD,
+  KID_COUNT
+};
+
+const char* kernel_name(int id);
+void launch_begin(int id, cudaStream_t st);
+void launch_end(int id, cudaStream_t st);
+
+}  // namespace rnnt
+
+#define RNNT_LAUNCH(id, st, ...)           \
+  do {                                     \
+    ::rnnt::launch_begin((id), (st));      \
+    __VA_ARGS__;                           \
+    ::rnnt::launch_end((id), (st));        \
+  } while (0)

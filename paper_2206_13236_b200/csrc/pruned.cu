@@ -12,9 +12,13 @@
 //   K11 DwGemm (split-K)      d_w = sum dz h^T, d_b = sum dz, deterministic split reduction
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "launch.h"
 #include "workspace.h"
 
 namespace rnnt {
+
+cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                              const uint16_t* b, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
 // One thread per 8 consecutive j of one band row (16 B of bf16 out).
@@ -74,62 +78,6 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
     }
   }
   rowinfo[r] = info;
-}
-
-// ------------------------------------------------------------------ K8 (SIMT v0)
-struct ZGemm {
-  static constexpr bool kAMajorM = false, kBMajorN = false;
-  const uint16_t *h, *W, *b;
-  long long R;
-  int V, J;
-  float* z;
-  __device__ bool tile_active(int, int, int) const { return true; }
-  __device__ void krange(int, int, int, long long& kb, long long& ke) const { kb = 0; ke = J; }
-  __device__ float A(int, int r, long long j) const { return r < R ? bf16_bits_to_f(h[(size_t)r * J + j]) : 0.f; }
-  __device__ float B(int, int v, long long j) const { return v < V ? bf16_bits_to_f(W[(size_t)v * J + j]) : 0.f; }
-  __device__ void epi(int, int r, int v, float acc) const {
-    if (r < R && v < V) z[(size_t)r * V + v] = acc + bf16_bits_to_f(b[v]);
-  }
-};
-
-// Online log-softmax over V for one row (one warp per row), pick of blank / label, and the
-// stored unnormalised probabilities P~ = bf16(exp(z - m_tile)) with kVT-wide tile maxima.
-__global__ void softmax_rows_kernel(const float* __restrict__ z, const int32_t* __restrict__ rowinfo,
-                                    long long R, int V, uint16_t* __restrict__ Pt, float* __restrict__ mt,
-                                    float* __restrict__ lse_out, float* __restrict__ px2, float* __restrict__ py2) {
-  long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (r >= R) return;
-  const int info = rowinfo[r];
-  const int ntile = (V + kVT - 1) / kVT;
-  if (info < 0) {
-    if (lane == 0) { px2[r] = neg_inf_f(); py2[r] = neg_inf_f(); lse_out[r] = 0.f; }
-    return;
-  }
-  const float* zr = z + r * (long long)V;
-  float M = neg_inf_f(), sum = 0.f;
-  for (int tl = 0; tl < ntile; ++tl) {
-    float m = neg_inf_f();
-    for (int v = tl * kVT + lane; v < min(V, (tl + 1) * kVT); v += 32) m = fmaxf(m, zr[v]);
-    m = warp_max(m);
-    if (lane == 0) mt[r * ntile + tl] = m;
-    float s = 0.f;
-    for (int v = tl * kVT + lane; v < min(V, (tl + 1) * kVT); v += 32) {
-      float e = expf(zr[v] - m);
-      Pt[r * (long long)V + v] = f_to_bf16_bits_rn(e);
-      s += e;
-    }
-    s = warp_sum(s);
-    float Mn = fmaxf(M, m);
-    sum = sum * expf(M - Mn) + s * expf(m - Mn);
-    M = Mn;
-  }
-  if (lane == 0) {
-    const float lse = M + logf(sum);
-    lse_out[r] = lse;
-    py2[r] = (zr[0] - lse) * RNNT_LOG2E_F;
-    px2[r] = info < V ? (zr[info] - lse) * RNNT_LOG2E_F : neg_inf_f();
-  }
 }
 
 // ------------------------------------------------------------------ K9 pruned recursion
@@ -282,12 +230,12 @@ struct GradElem {
   const uint16_t* Pt;
   const float *sc, *gb, *gl;
   const int32_t* rowinfo;
-  int V, ntile;
+  int V, VP, ntile;
   float gs;
   __device__ float operator()(long long r, int v) const {
     const int info = rowinfo[r];
     if (info < 0 || v >= V) return 0.f;
-    float g = sc[r * ntile + v / kVT] * bf16_bits_to_f(Pt[r * (long long)V + v]);
+    float g = sc[r * ntile + v / kVT] * bf16_bits_to_f(Pt[r * (long long)VP + v]);
     if (v == 0) g -= gs * gb[r];
     if (v == info) g -= gs * gl[r];
     return g;
@@ -396,8 +344,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, 
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st) {
   long long work = d.rows() * (d.J / 8);
-  prune_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(enc, dec, ranges, bnd, d.N, d.T, d.U, d.J,
-                                                                 d.S, h);
+  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(enc, dec, ranges, bnd, d.N, d.T, d.U, d.J,
+                                                                 d.S, h));
   return cudaGetLastError();
 }
 
@@ -410,46 +358,43 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
-  rowinfo_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S,
-                                                               w.rowinfo);
-  {
-    ZGemm p{h, W, b, R, d.V, d.J, w.z};
-    if ((e = launch_simt_gemm(p, (int)R, d.V, 1, st)) != cudaSuccess) return e;
-  }
-  softmax_rows_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(w.z, w.rowinfo, R, d.V, w.Pt, w.mt, w.lse,
-                                                                w.px2, w.py2);
+  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S,
+                                                               w.rowinfo));
+  if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     size_t sm = pruned_recursion_smem(d);
     cudaFuncSetAttribute(pruned_alpha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(pruned_beta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pruned_alpha_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.ap, w.Lp, loss, status);
-    pruned_beta_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.bp);
+    RNNT_LAUNCH(KID_PALPHA, st, pruned_alpha_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.ap, w.Lp, loss, status));
+    RNNT_LAUNCH(KID_PBETA, st, pruned_beta_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.bp));
   }
-  pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
+  RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
       w.px2, w.py2, w.ap, w.bp, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
-      w.gl, w.sc);
-  GradElem ge{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, d.V, nt, gs};
+      w.gl, w.sc));
+  GradElem ge{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, d.V, d.VP(), nt, gs};
   if (d_enc || d_dec) {
     DhGemm p{ge, W, h, R, d.V, d.J, w.dpre};
-    if ((e = launch_simt_gemm(p, (int)R, d.J, 1, st)) != cudaSuccess) return e;
+    RNNT_LAUNCH(KID_DH, st, e = launch_simt_gemm(p, (int)R, d.J, 1, st));
+    if (e != cudaSuccess) return e;
     if (d_enc) {
       long long n = (long long)d.N * d.T * d.J;
-      denc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, bnd, d.N, d.T, d.S, d.J, d_enc);
+      RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, bnd, d.N, d.T, d.S, d.J, d_enc));
     }
     if (d_dec) {
       long long n = (long long)d.N * d.U1() * d.J;
-      ddec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J,
-                                                               d_dec);
+      RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J,
+                                                               d_dec));
     }
   }
   {
     const long long chunk = (R + w.splits - 1) / w.splits;
     DwGemm p{ge, h, R, chunk, d.V, d.J, w.dWp};
-    if ((e = launch_simt_gemm(p, d.V, d.J, w.splits, st)) != cudaSuccess) return e;
-    db_partial_kernel<<<dim3((d.V + 127) / 128, w.splits), 128, 0, st>>>(ge, R, chunk, d.V, w.dbp);
+    RNNT_LAUNCH(KID_DW, st, e = launch_simt_gemm(p, d.V, d.J, w.splits, st));
+    if (e != cudaSuccess) return e;
+    RNNT_LAUNCH(KID_DB, st, db_partial_kernel<<<dim3((d.V + 127) / 128, w.splits), 128, 0, st>>>(ge, R, chunk, d.V, w.dbp));
     long long M = (long long)d.V * d.J;
-    split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w);
-    split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b);
+    RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w));
+    RNNT_LAUNCH(KID_DB_REDUCE, st, split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b));
   }
   return cudaGetLastError();
 }

@@ -9,6 +9,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "launch.h"
 #include "workspace.h"
 
 namespace rnnt {
@@ -120,9 +121,9 @@ cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* 
                               int32_t* ranges, int32_t* status, cudaStream_t st) {
   // raw bounds and the monotone hull q are staged in the output buffer itself (no workspace).
   long long rows = (long long)d.N * d.T;
-  raw_bounds_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(px_grad, py_grad, bnd, d.N, d.T, d.U,
-                                                                 d.S, ranges);
-  adjust_kernel<<<d.N, 1024, 0, st>>>(ranges, bnd, d.T, d.S, ranges, ranges, status);
+  RNNT_LAUNCH(KID_RAW, st, raw_bounds_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(px_grad, py_grad, bnd, d.N, d.T, d.U,
+                                                                 d.S, ranges));
+  RNNT_LAUNCH(KID_ADJUST, st, adjust_kernel<<<d.N, 1024, 0, st>>>(ranges, bnd, d.T, d.S, ranges, ranges, status));
   return cudaGetLastError();
 }
 

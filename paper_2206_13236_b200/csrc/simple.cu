@@ -10,6 +10,7 @@
 //   K5 AmGrad/LmGrad + picks d(-L)/d am, d(-L)/d lm (chain rule through Eq. 5-6)
 #include "common.cuh"
 #include "gemm_simt.cuh"
+#include "launch.h"
 #include "workspace.h"
 
 namespace rnnt {
@@ -443,8 +444,8 @@ static cudaError_t launch_recursions(const Dims& d, const SimpleWS& w, const int
   const int LU = d.LU(), K = d.K();
   int threads = ((LU + R - 1) / R + 31) / 32 * 32;
   if (threads > 256) return cudaErrorInvalidConfiguration;
-  lattice_alpha_kernel<R, 4><<<d.N, threads, 0, st>>>(w.px2, w.py2, bnd, LU, K, w.alpha, w.Ltot, loss, status);
-  lattice_beta_kernel<R, 4><<<d.N, threads, 0, st>>>(w.px2, w.py2, bnd, LU, K, w.beta);
+  RNNT_LAUNCH(KID_ALPHA, st, lattice_alpha_kernel<R, 4><<<d.N, threads, 0, st>>>(w.px2, w.py2, bnd, LU, K, w.alpha, w.Ltot, loss, status));
+  RNNT_LAUNCH(KID_BETA, st, lattice_beta_kernel<R, 4><<<d.N, threads, 0, st>>>(w.px2, w.py2, bnd, LU, K, w.beta));
   return cudaGetLastError();
 }
 
@@ -453,16 +454,17 @@ cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am
                                float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
                                int32_t* status, cudaStream_t st) {
   cudaError_t e;
-  validate_kernel<<<d.N, 128, 0, st>>>(sym, bnd, d.N, d.U, d.V, status);
+  RNNT_LAUNCH(KID_VALIDATE, st, validate_kernel<<<d.N, 128, 0, st>>>(sym, bnd, d.N, d.U, d.V, status));
   {
     long long rows = (long long)d.N * d.T;
-    rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(am, d.N, d.T, d.V, bnd, 0, w.m_am);
+    RNNT_LAUNCH(KID_ROWMAX_AM, st, rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(am, d.N, d.T, d.V, bnd, 0, w.m_am));
     rows = (long long)d.N * d.U1();
-    rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(lm, d.N, d.U1(), d.V, bnd, 1, w.m_lm);
+    RNNT_LAUNCH(KID_ROWMAX_LM, st, rowmax_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(lm, d.N, d.U1(), d.V, bnd, 1, w.m_lm));
   }
   {
     NormGemm p{am, lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), w.px2, w.py2, w.rS, status};
-    if ((e = launch_simt_gemm(p, d.T, d.U1(), d.N, st)) != cudaSuccess) return e;
+    RNNT_LAUNCH(KID_NORM, st, e = launch_simt_gemm(p, d.T, d.U1(), d.N, st));
+    if (e != cudaSuccess) return e;
   }
   {
     int R = pick_R(d.LU());
@@ -474,22 +476,24 @@ cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am
   }
   {
     dim3 grid((d.K() + 31) / 32, (d.U1() + 31) / 32, d.N);
-    combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ltot, bnd, d.T, d.U,
-                                         d.LU(), d.K(), px_grad, py_grad, w.Gt);
+    RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ltot, bnd, d.T, d.U,
+                                         d.LU(), d.K(), px_grad, py_grad, w.Gt));
   }
   if (am_grad) {
     AmGradGemm p{am, lm, w.m_am, w.m_lm, w.Gt, bnd, d.T, d.U, d.V, gs, am_grad};
-    if ((e = launch_simt_gemm(p, d.T, d.V, d.N, st)) != cudaSuccess) return e;
+    RNNT_LAUNCH(KID_AMGRAD, st, e = launch_simt_gemm(p, d.T, d.V, d.N, st));
+    if (e != cudaSuccess) return e;
     long long rows = (long long)d.N * d.T;
-    am_picks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(px_grad, py_grad, sym, bnd, d.N, d.T,
-                                                                      d.U, d.V, gs, am_grad);
+    RNNT_LAUNCH(KID_AMPICK, st, am_picks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(px_grad, py_grad, sym, bnd, d.N, d.T,
+                                                                      d.U, d.V, gs, am_grad));
   }
   if (lm_grad) {
     LmGradGemm p{am, lm, w.m_am, w.m_lm, w.Gt, bnd, d.T, d.U, d.V, gs, lm_grad};
-    if ((e = launch_simt_gemm(p, d.U1(), d.V, d.N, st)) != cudaSuccess) return e;
+    RNNT_LAUNCH(KID_LMGRAD, st, e = launch_simt_gemm(p, d.U1(), d.V, d.N, st));
+    if (e != cudaSuccess) return e;
     long long rows = (long long)d.N * d.U1();
-    lm_picks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(px_grad, py_grad, sym, bnd, d.N, d.T,
-                                                                      d.U, d.V, gs, lm_grad);
+    RNNT_LAUNCH(KID_LMPICK, st, lm_picks_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(px_grad, py_grad, sym, bnd, d.N, d.T,
+                                                                      d.U, d.V, gs, lm_grad));
   }
   return cudaGetLastError();
 }

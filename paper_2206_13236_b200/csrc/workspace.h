@@ -14,6 +14,7 @@ struct Dims {
   int K() const { return T + U; }                       // number of anti-diagonals
   long long rows() const { return (long long)N * T * S; }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
+  int VP() const { return (V + 127) / 128 * 128; }      // padded row pitch of P~ (elements)
 };
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -32,8 +33,8 @@ struct SimpleWS {
 
 struct PrunedWS {
   int32_t* rowinfo;  // (R) label y_{u+1} (V if u==U_n), -1 for masked/padded rows
-  float* z;          // (R,V) fp32 logits scratch (SIMT v0 path only)
-  uint16_t* Pt;      // (R,V) bf16 exp(z - m_tile)
+  float* bias;       // (VP) fp32 copy of b_out, zero padded
+  uint16_t* Pt;      // (R,VP) bf16 exp(z - m_tile), pitch VP
   float* mt;         // (R,ntile) tile maxima of z
   float* lse;        // (R) log-sum-exp of z
   float* px2;        // (R) y_p * log2e (band arcs)
@@ -68,7 +69,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
     return p;
   };
   const size_t N = d.N, T = d.T, U1 = d.U1(), LU = d.LU(), K1 = d.K() + 1;
-  const size_t R = (size_t)d.rows(), V = d.V, J = d.J, NT = d.ntile();
+  const size_t R = (size_t)d.rows(), V = d.V, J = d.J, NT = d.ntile(), VP = d.VP();
   SimpleWS s;
   s.m_am = (float*)take(N * T * 4);
   s.m_lm = (float*)take(N * U1 * 4);
@@ -82,8 +83,8 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   PrunedWS p;
   p.splits = dw_splits(d);
   p.rowinfo = (int32_t*)take(R * 4);
-  p.z = (float*)take(R * V * 4);
-  p.Pt = (uint16_t*)take(R * V * 2);
+  p.bias = (float*)take(VP * 4);
+  p.Pt = (uint16_t*)take(R * VP * 2);
   p.mt = (float*)take(R * NT * 4);
   p.lse = (float*)take(R * 4);
   p.px2 = (float*)take(R * 4);

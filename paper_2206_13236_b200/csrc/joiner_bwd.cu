@@ -1,0 +1,394 @@
+// joiner_bwd.cu — K10 / K11: joiner backward on tcgen05 with the logit gradient formed in
+// the operand producer (function merging): nothing of size (R, V) is written in
+// the backward; P~ (bf16, from K8) is read and turned into
+//     dz[r,v] = sc[r, v/128] * P~[r,v] - gs g_b[r] [v=0] - gs g_l[r] [v=y_r]      (bf16)
+// directly in the swizzled shared-memory operand tile.
+//
+//   K10 joiner_dh:  dh[r, j] = sum_v dz[r,v] W[v,j]     A = dz (K-major, producer warps),
+//                   B = W (MN-major, TMA), epilogue dpre = dh (1 - h^2)  (d tanh)
+//   K11 joiner_dw:  dW[v, j] = sum_r dz[r,v] h[r,j]     A = dz^T (MN-major, producer warps),
+//                   B = h (MN-major, TMA), split-K over rows, fp32 partial tiles; the
+//                   producers also accumulate db = sum_r dz partials.
+// Warps 0-3: operand producers, then epilogue (TMEM lanes 32w..32w+31).
+// Warp 4: TMEM allocator, TMA issuer and single-thread MMA issuer.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+#include "tc.cuh"
+#include "tmap.h"
+#include "workspace.h"
+
+namespace rnnt {
+
+struct GradSrc {
+  const uint16_t* Pt;
+  const float *sc, *gb, *gl;
+  const int32_t* rowinfo;
+  long long R;
+  int V, VP, ntile;
+  float gs;
+  // 8 consecutive dz values (v = vc..vc+7) of row r packed as bf16.
+  __device__ __forceinline__ uint4 chunk(long long r, int vc, float* fsum) const {
+    if (r >= R) return make_uint4(0, 0, 0, 0);
+    const int info = rowinfo[r];
+    if (info < 0 || vc >= V) return make_uint4(0, 0, 0, 0);
+    const uint4 pv = *reinterpret_cast<const uint4*>(Pt + (size_t)r * VP + vc);
+    const float s = sc[(size_t)r * ntile + (vc >> 7)];
+    const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+    float g[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      g[2 * i] = s * __uint_as_float(w[i] << 16);
+      g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u);
+    }
+    if (vc == 0) g[0] -= gs * gb[r];
+    const int li = info - vc;
+    if ((unsigned)li < 8u) {
+      const float gl_ = gs * gl[r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j == li) g[j] -= gl_;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+      o[i] = *reinterpret_cast<uint32_t*>(&h2);
+      if (fsum) {
+        // db accumulates the bf16-rounded dz, the values the MMA consumes
+        fsum[2 * i] += __low2float(h2);
+        fsum[2 * i + 1] += __high2float(h2);
+      }
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+  }
+};
+
+// byte offset of 16-B chunk `c` (0..7) of 128-B row `r` in a SWIZZLE_128B atom stack
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+// ======================================================================= K10
+namespace jdh {
+constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 512, STAGES = 2;
+constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major
+constexpr int B_BYTES = MAXN * BK * 2;         // 64 KB, MN-major (8 boxes of 64 j x 64 v)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int THREADS = 160;
+}  // namespace jdh
+
+struct JoinerDhParams {
+  GradSrc g;
+  const uint16_t* h;
+  int J, nkb;
+  float* dpre;
+};
+
+__global__ void __launch_bounds__(jdh::THREADS, 1)
+    joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmW, JoinerDhParams p) {
+  using namespace jdh;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long m0 = (long long)blockIdx.x * BM;
+  const int j0 = blockIdx.y * MAXN;
+  const int nj = min(MAXN, p.J - j0);               // columns of this CTA
+  const int nsub = (nj + NSUB - 1) / NSUB;
+  const int nbox = (nj + 63) / 64;
+
+  int act = 0;
+  for (int i = threadIdx.x; i < BM; i += blockDim.x)
+    if (m0 + i < p.g.R && p.g.rowinfo[m0 + i] >= 0) act = 1;
+  const bool any = __syncthreads_or(act);
+  if (!any) {
+    // tile entirely masked: dpre rows are zero
+    for (int i = threadIdx.x; i < BM; i += blockDim.x) {
+      const long long r = m0 + i;
+      if (r >= p.g.R) break;
+      float4* o = reinterpret_cast<float4*>(p.dpre + (size_t)r * p.J + j0);
+      for (int j = 0; j < nj / 4; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
+  if (warp == 4 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 4 + 1); tc::mbar_init(&empty[s], 1); }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmW);
+  }
+  if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    // ---- producers: A = dz[m0.., kb*64..] (K-major)
+    int stage = 0;
+    uint32_t ph = 0;
+    const int c = threadIdx.x & 7;
+    const int rbase = threadIdx.x >> 3;   // 0..15
+    for (int kb = 0; kb < p.nkb; ++kb) {
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+#pragma unroll 4
+      for (int i = 0; i < 8; ++i) {
+        const int rl = rbase + 16 * i;
+        const uint4 v = p.g.chunk(m0 + rl, kb * BK + c * 8, nullptr);
+        *reinterpret_cast<uint4*>(sa + sw128(rl, c)) = v;
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+    // ---- epilogue: dpre = dh * (1 - h^2)
+    tc::mbar_wait(tfull, 0);
+    tc::fence_after_sync();
+    const long long r = m0 + threadIdx.x;
+    const bool valid = r < p.g.R && p.g.rowinfo[r] >= 0;
+    const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
+    for (int c0 = 0; c0 < nj; c0 += 32) {
+      float acc[32];
+      tc::tmem_ld32(tl + c0, acc);
+      if (r < p.g.R) {
+        float* o = p.dpre + (size_t)r * p.J + j0 + c0;
+        const uint4* hp = reinterpret_cast<const uint4*>(p.h + (size_t)r * p.J + j0 + c0);
+        const int nq = min(4, (nj - c0) / 8);   // J % 8 == 0
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= nq) break;
+          const uint4 hv = valid ? hp[q] : make_uint4(0, 0, 0, 0);
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+          float out[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float ha = __uint_as_float(hw[i] << 16), hb = __uint_as_float(hw[i] & 0xffff0000u);
+            out[2 * i] = valid ? acc[8 * q + 2 * i] * (1.f - ha * ha) : 0.f;
+            out[2 * i + 1] = valid ? acc[8 * q + 2 * i + 1] * (1.f - hb * hb) : 0.f;
+          }
+          reinterpret_cast<float4*>(o)[2 * q] = make_float4(out[0], out[1], out[2], out[3]);
+          reinterpret_cast<float4*>(o)[2 * q + 1] = make_float4(out[4], out[5], out[6], out[7]);
+        }
+      }
+    }
+  } else if (lane == 0) {
+    // ---- warp 4: B = W[kb*64.., j0..] via TMA (MN-major boxes of 64 j x 64 v) + MMA issue
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
+    int stage = 0;
+    uint32_t ph = 0;
+    int stage_m = 0;
+    uint32_t ph_m = 0;
+    const uint32_t bbytes = (uint32_t)nbox * 64 * BK * 2;
+    // prologue: issue the first STAGES B loads
+    int kb_load = 0;
+    for (int kb = 0; kb < p.nkb; ++kb) {
+      // keep the TMA one stage ahead of the MMA
+      while (kb_load < p.nkb && kb_load < kb + STAGES) {
+        tc::mbar_wait(&empty[stage], ph ^ 1);
+        uint8_t* sb = smem + stage * STAGE_BYTES + A_BYTES;
+        tc::mbar_arrive_expect_tx(&full[stage], bbytes);
+        for (int bx = 0; bx < nbox; ++bx)
+          tc::tma_load_2d(sb + bx * (64 * BK * 2), &tmW, &full[stage], j0 + bx * 64, kb_load * BK);
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        ++kb_load;
+      }
+      tc::mbar_wait(&full[stage_m], ph_m);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(smem + stage_m * STAGE_BYTES), b = a + A_BYTES;
+      for (int ns = 0; ns < nsub; ++ns) {
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          tc::mma_bf16(tbase + ns * NSUB, tc::sdesc(a + 32 * k, 16, 1024),
+                       tc::sdesc(b + ns * 4 * (64 * BK * 2) + 2048 * k, 64 * BK * 2, 1024), idesc, (kb | k) != 0);
+      }
+      tc::mma_commit(&empty[stage_m]);
+      if (++stage_m == STAGES) { stage_m = 0; ph_m ^= 1; }
+    }
+    tc::mma_commit(tfull);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 4) tc::tmem_dealloc(tbase, 512);
+}
+
+// ======================================================================= K11
+namespace jdw {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 atom columns of 64 v x 64 rows)
+constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4;
+constexpr int THREADS = 160;
+}  // namespace jdw
+
+struct JoinerDwParams {
+  GradSrc g;
+  int J;
+  long long kb_per_split, nkb_total;
+  float* dWp;   // (splits, V, J)
+  float* dbp;   // (splits, V)
+};
+
+__global__ void __launch_bounds__(jdw::THREADS, 1)
+    joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmH, JoinerDwParams p) {
+  using namespace jdw;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [8 row groups][128 v]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
+  const long long kb0 = (long long)split * p.kb_per_split;
+  const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
+  const int nkb = (int)max(0LL, kb1 - kb0);
+  const int V = p.g.V;
+  const int nj = min(BN, p.J - j0);
+  const int nbox = (nj + 63) / 64;
+
+  if (warp == 4 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 4 + 1); tc::mbar_init(&empty[s], 1); }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmH);
+  }
+  if (warp == 4) tc::tmem_alloc(tmem_slot, 256);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    // ---- producers: A = dz^T tile (v0..v0+127) x (64 rows), MN-major
+    int stage = 0;
+    uint32_t ph = 0;
+    const int c = threadIdx.x & 15;          // 8-v chunk 0..15
+    const int g8 = threadIdx.x >> 4;         // row group 0..7
+    float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const bool want_db = blockIdx.y == 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+      const long long rb = (kb0 + kb) * BK;
+#pragma unroll 4
+      for (int i = 0; i < 8; ++i) {
+        const int rl = g8 + 8 * i;
+        const uint4 v = p.g.chunk(rb + rl, v0 + c * 8, want_db ? dsum : nullptr);
+        *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) = v;
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+    if (want_db) {
+      // reduce the 8 row groups of each chunk deterministically through smem
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dbs[g8 * 128 + c * 8 + j] = dsum[j];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int v = threadIdx.x;   // 0..127
+      float s = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg) s += dbs[gg * 128 + v];
+      if (v0 + v < V) p.dbp[(size_t)split * V + v0 + v] = s;
+    }
+    // ---- epilogue: partial dW tile -> dWp[split]
+    if (nkb > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    const int v = v0 + threadIdx.x;
+    const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
+    for (int c0 = 0; c0 < nj; c0 += 32) {
+      float acc[32];
+      if (nkb > 0) {
+        tc::tmem_ld32(tl + c0, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      }
+      if (v < V) {
+        float4* o = reinterpret_cast<float4*>(p.dWp + ((size_t)split * V + v) * p.J + j0 + c0);
+        const int n4 = min(8, (nj - c0) / 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < n4) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      }
+    }
+  } else if (lane == 0 && nkb > 0) {
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+    int stage = 0, stage_m = 0;
+    uint32_t ph = 0, ph_m = 0;
+    const uint32_t bbytes = (uint32_t)nbox * 64 * BK * 2;
+    int kb_load = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      while (kb_load < nkb && kb_load < kb + STAGES) {
+        tc::mbar_wait(&empty[stage], ph ^ 1);
+        uint8_t* sb = smem + stage * STAGE_BYTES + A_BYTES;
+        tc::mbar_arrive_expect_tx(&full[stage], bbytes);
+        for (int bx = 0; bx < nbox; ++bx)
+          tc::tma_load_2d(sb + bx * (64 * BK * 2), &tmH, &full[stage], j0 + bx * 64, (int)((kb0 + kb_load) * BK));
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        ++kb_load;
+      }
+      tc::mbar_wait(&full[stage_m], ph_m);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(smem + stage_m * STAGE_BYTES), b = a + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k)
+        tc::mma_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024),
+                     idesc, (kb | k) != 0);
+      tc::mma_commit(&empty[stage_m]);
+      if (++stage_m == STAGES) { stage_m = 0; ph_m ^= 1; }
+    }
+    tc::mma_commit(tfull);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 4) tc::tmem_dealloc(tbase, 256);
+}
+
+// ======================================================================= host
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
+                             cudaStream_t st) {
+  CUtensorMap tw;
+  if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+    attr = true;
+  }
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, dpre};
+  dim3 grid((unsigned)((d.rows() + jdh::BM - 1) / jdh::BM), (d.J + jdh::MAXN - 1) / jdh::MAXN);
+  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tw, p));
+  return cudaGetLastError();
+}
+
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
+                             int splits, cudaStream_t st) {
+  CUtensorMap th;
+  if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(joiner_dw_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdw::SMEM_BYTES);
+    attr = true;
+  }
+  const long long nkb = (d.rows() + jdw::BK - 1) / jdw::BK;
+  const long long per = (nkb + splits - 1) / splits;
+  JoinerDwParams p{g, d.J, per, nkb, dWp, dbp};
+  dim3 grid((d.V + jdw::BM - 1) / jdw::BM, (d.J + jdw::BN - 1) / jdw::BN, splits);
+  RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<<<grid, jdw::THREADS, jdw::SMEM_BYTES, st>>>(th, p));
+  return cudaGetLastError();
+}
+
+}  // namespace rnnt

@@ -11,7 +11,6 @@
 //   K10 DhGemm + reduce       dpre = (W^T dz) (1-h^2); d_enc = sum_s dpre; d_dec gather-reduce
 //   K11 DwGemm (split-K)      d_w = sum dz h^T, d_b = sum dz, deterministic split reduction
 #include "common.cuh"
-#include "gemm_simt.cuh"
 #include "launch.h"
 #include "workspace.h"
 
@@ -19,6 +18,18 @@ namespace rnnt {
 
 cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, cudaStream_t st);
+struct GradSrc {
+  const uint16_t* Pt;
+  const float *sc, *gb, *gl;
+  const int32_t* rowinfo;
+  long long R;
+  int V, VP, ntile;
+  float gs;
+};
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
+                             cudaStream_t st);
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
+                             int splits, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
 // One thread per 8 consecutive j of one band row (16 B of bf16 out).
@@ -224,47 +235,6 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
     sc[r * ntile + tl] = (rowinfo[r] >= 0) ? gs * (bb + yb) * expf(mt[r * ntile + tl] - l) : 0.f;
 }
 
-// Logit gradient of one element (function merging):
-//   dz[r,v] = gs((g_b+g_l) softmax(z)[v] - g_b [v=0] - g_l [v=y]) = sc[r,v/kVT] P~[r,v] - picks.
-struct GradElem {
-  const uint16_t* Pt;
-  const float *sc, *gb, *gl;
-  const int32_t* rowinfo;
-  int V, VP, ntile;
-  float gs;
-  __device__ float operator()(long long r, int v) const {
-    const int info = rowinfo[r];
-    if (info < 0 || v >= V) return 0.f;
-    float g = sc[r * ntile + v / kVT] * bf16_bits_to_f(Pt[r * (long long)VP + v]);
-    if (v == 0) g -= gs * gb[r];
-    if (v == info) g -= gs * gl[r];
-    return g;
-  }
-};
-
-// ------------------------------------------------------------------ K10 (SIMT v0)
-struct DhGemm {
-  static constexpr bool kAMajorM = false, kBMajorN = true;
-  GradElem ge;
-  const uint16_t *W, *h;
-  long long R;
-  int V, J;
-  float* dpre;
-  __device__ bool tile_active(int, int, int) const { return true; }
-  __device__ void krange(int, int, int, long long& kb, long long& ke) const { kb = 0; ke = V; }
-  __device__ float A(int, int r, long long v) const { return r < R ? ge(r, (int)v) : 0.f; }
-  __device__ float B(int, int j, long long v) const { return j < J ? bf16_bits_to_f(W[(size_t)v * J + j]) : 0.f; }
-  __device__ void epi(int, int r, int j, float acc) const {
-    if (r >= R || j >= J) return;
-    float out = 0.f;
-    if (ge.rowinfo[r] >= 0) {
-      const float hv = bf16_bits_to_f(h[(size_t)r * J + j]);
-      out = acc * (1.f - hv * hv);   // d tanh
-    }
-    dpre[(size_t)r * J + j] = out;
-  }
-};
-
 // d_enc[n,t,:] = sum_s dpre[n,t,s,:];  d_dec[n,u,:] = sum_{t: p_t <= u < p_t+S} dpre[n,t,u-p_t,:]
 // (frames covering u form a contiguous range since p is monotone; summed in t order).
 __global__ void denc_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd, int N, int T,
@@ -299,36 +269,6 @@ __global__ void ddec_kernel(const float* __restrict__ dpre, const int32_t* __res
       acc += dpre[(((size_t)n * T + t) * S + (u - p[t])) * J + j];
   }
   d_dec[i] = acc;
-}
-
-// ------------------------------------------------------------------ K11 (SIMT v0, split-K)
-struct DwGemm {
-  static constexpr bool kAMajorM = true, kBMajorN = true;
-  GradElem ge;
-  const uint16_t* h;
-  long long R, chunk;
-  int V, J;
-  float* dWp;
-  __device__ bool tile_active(int, int, int) const { return true; }
-  __device__ void krange(int z, int, int, long long& kb, long long& ke) const {
-    kb = (long long)z * chunk;
-    ke = kb + chunk < R ? kb + chunk : R;
-  }
-  __device__ float A(int, int v, long long r) const { return ge(r, v); }
-  __device__ float B(int, int j, long long r) const { return j < J ? bf16_bits_to_f(h[(size_t)r * J + j]) : 0.f; }
-  __device__ void epi(int z, int v, int j, float acc) const {
-    if (v < V && j < J) dWp[((size_t)z * V + v) * J + j] = acc;
-  }
-};
-
-__global__ void db_partial_kernel(GradElem ge, long long R, long long chunk, int V, float* __restrict__ dbp) {
-  const int z = blockIdx.y;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const long long kb = (long long)z * chunk, ke = min(R, kb + chunk);
-  float acc = 0.f;
-  for (long long r = kb; r < ke; ++r) acc += ge(r, v);
-  dbp[(size_t)z * V + v] = acc;
 }
 
 __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, long long M,
@@ -371,11 +311,9 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
       w.px2, w.py2, w.ap, w.bp, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
       w.gl, w.sc));
-  GradElem ge{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, d.V, d.VP(), nt, gs};
+  GradSrc g{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, R, d.V, d.VP(), nt, gs};
   if (d_enc || d_dec) {
-    DhGemm p{ge, W, h, R, d.V, d.J, w.dpre};
-    RNNT_LAUNCH(KID_DH, st, e = launch_simt_gemm(p, (int)R, d.J, 1, st));
-    if (e != cudaSuccess) return e;
+    if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
     if (d_enc) {
       long long n = (long long)d.N * d.T * d.J;
       RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, bnd, d.N, d.T, d.S, d.J, d_enc));
@@ -387,11 +325,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
     }
   }
   {
-    const long long chunk = (R + w.splits - 1) / w.splits;
-    DwGemm p{ge, h, R, chunk, d.V, d.J, w.dWp};
-    RNNT_LAUNCH(KID_DW, st, e = launch_simt_gemm(p, d.V, d.J, w.splits, st));
-    if (e != cudaSuccess) return e;
-    RNNT_LAUNCH(KID_DB, st, db_partial_kernel<<<dim3((d.V + 127) / 128, w.splits), 128, 0, st>>>(ge, R, chunk, d.V, w.dbp));
+    if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
     long long M = (long long)d.V * d.J;
     RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w));
     RNNT_LAUNCH(KID_DB_REDUCE, st, split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b));

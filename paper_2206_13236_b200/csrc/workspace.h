@@ -51,12 +51,17 @@ struct PrunedWS {
   int splits;
 };
 
+// Split-K factor of the d_w GEMM (K11): about two CTAs per SM over the (V/128) x (J/256)
+// output tiles, at least 4 K-blocks of 64 rows per split.
 inline int dw_splits(const Dims& d) {
-  long long rows = d.rows();
-  int s = (int)((rows + 4095) / 4096);
-  if (s < 1) s = 1;
+  const long long nkb = (d.rows() + 63) / 64;
+  const long long tiles = (long long)((d.V + 127) / 128) * ((d.J + 255) / 256);
+  long long s = (2 * 148 + tiles - 1) / tiles;
+  const long long cap = nkb / 4 > 1 ? nkb / 4 : 1;
+  if (s > cap) s = cap;
   if (s > 64) s = 64;
-  return s;
+  if (s < 1) s = 1;
+  return (int)s;
 }
 
 // Returns total bytes; if base != nullptr fills the structs.

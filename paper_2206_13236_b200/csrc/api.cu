@@ -29,7 +29,7 @@ static thread_local int g_prof_id = 0;
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 static const char* const kNames[KID_COUNT] = {
-    "none", "validate", "rowmax_am", "rowmax_lm", "simple_norm_gemm", "lattice_alpha", "lattice_beta",
+    "none", "validate", "rowmax_am", "rowmax_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
     "lattice_combine", "simple_am_grad_gemm", "simple_am_picks", "simple_lm_grad_gemm", "simple_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
     "pruned_alpha", "pruned_beta", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",
@@ -57,7 +57,7 @@ static rnnt_status_t check_dims(const rnnt_dims_t* dims, Dims* d) {
     return RNNT_ERR_INVALID_ARG;
   if ((long long)d->U >= (long long)d->T * 64) return RNNT_ERR_INVALID_ARG;
   if (d->J < 8 || d->J > 4096 || d->J % 8) return RNNT_ERR_INVALID_ARG;
-  if (d->LU() > 2048) return RNNT_ERR_UNSUPPORTED;   // recursion kernel: <= 8 warps x 8 columns
+  if (d->lat_R() == 0) return RNNT_ERR_UNSUPPORTED;   // recursion kernel: one warp x <= 32 columns per lane
   return RNNT_OK;
 }
 

@@ -26,6 +26,10 @@ constexpr int kStatusBadBoundary = 16;
 // (D11 / DESIGN.md "K8"): P~[r,v] = bf16(exp(z[r,v] - m[r, v / kVT])).
 constexpr int kVT = 128;
 
+// "log 0" of the fp32 log-space recursions: finite, so LogAdd needs no -inf guard; any sum with it
+// stays below -1e29 for 1e8 steps, and exp2 of it is exactly 0.
+constexpr float kNegBig = -1.0e30f;
+
 __device__ __forceinline__ float neg_inf_f() { return __int_as_float(0xff800000); }
 __device__ __forceinline__ double neg_inf_d() { return __longlong_as_double(0xfff0000000000000ULL); }
 

@@ -1,0 +1,366 @@
+// lattice.cu — K3/K4: forward-backward on the simple (trivial-joiner) lattice.
+//
+//   alpha(t,u) = LogAdd(alpha(t-1,u) + empty(t-1,u), alpha(t,u-1) + y(t,u-1))   (Eq. 3-4)
+//   beta(t,u)  = LogAdd(beta(t+1,u) + empty(t,u),   beta(t,u+1) + y(t,u))      (backward half)
+//   y'(t,u) = exp(alpha + y + beta(t,u+1) - L), empty'(t,u) = exp(alpha + empty + beta(t+1,u) - L)
+//                                                                              (occupancies)
+// on the SKEWED (diagonal-major) layout [n][k = t+u][u] written by the normaliser epilogue, so that
+// every wavefront step reads one contiguous row of arcs.  Conventions of the arc arrays (base 2):
+//   px2 = y * log2e (kNegBig at u = U_n), py2 = empty * log2e (kNegBig at t = T_n-1, u < U_n:
+//   the only blank out of the last frame is the terminal one), kNegBig at every invalid cell.
+// With these sentinels neither recursion needs a validity mask: the virtual node (T_n, U_n) on
+// diagonal K_n = T_n + U_n receives alpha(T-1,U) + empty(T-1,U) = L_tot, and beta starts
+// from it (beta = 0 there).
+//
+// Precision (D9): the state is fp32 REBASED per diagonal, alpha-hat_k = alpha_k - A_k, with
+// A_k = max_u alpha_{k-2} (the max of the diagonal two steps back, from one CREDUX.MAX per step, so
+// it is off the critical path) accumulated in fp64; |alpha-hat| stays within a two-step drift of 0
+// where the mass is, so the fp32 rounding is ~1e-7 relative per step.  The occupancies are then
+// self-normalised per anti-diagonal (every path leaves every diagonal k < K_n exactly once, so the
+// outflow of a diagonal sums to 1), which removes the error common to a diagonal.
+//
+// Kernels
+//   skew_fill_kernel    kNegBig into every invalid cell of the skewed arc arrays
+//   lattice_fb_kernel   grid (N, 2): y = 0 alpha, y = 1 beta, concurrently.  Warp 1 streams the arc
+//                       rows into a 4-stage shared-memory ring with cp.async.bulk (mbarrier
+//                       complete_tx); warp 0 runs the wavefront, lane i owning columns [iR, iR+R)
+//                       (one shuffle per diagonal for the arc crossing a lane boundary).
+//   combine_kernel      per 32-diagonal block: outflow sums Z_k, then y', empty' / Z_k and
+//                       G~ = (y' + empty') / S(t,u), transposed through smem to the t-major outputs.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+#include "tc.cuh"
+#include "workspace.h"
+
+namespace rnnt {
+
+namespace lat {
+constexpr int NST = 4;   // ring stages
+// arc rows (diagonals) per staged chunk: the ring holds NST x 2 arrays x CH rows x 32R floats
+template <int R>
+constexpr int CH = R <= 8 ? 16 : (R <= 16 ? 8 : 4);
+template <int R>
+constexpr size_t smem_bytes = (size_t)NST * 2 * CH<R> * 32 * R * sizeof(float);
+}  // namespace lat
+
+// ------------------------------------------------------------------ sentinel fill
+__global__ void skew_fill_kernel(const int64_t* __restrict__ bnd, int LU, int K, float* __restrict__ px2,
+                                 float* __restrict__ py2) {
+  const int n = blockIdx.y;
+  const long long cells = (long long)(K + 1) * LU;
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const size_t base = (size_t)n * cells;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / LU), u = (int)(i - (long long)k * LU), t = k - u;
+    if (!(t >= 0 && t < Tn && u <= Un)) {
+      px2[base + i] = kNegBig;
+      py2[base + i] = kNegBig;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ wavefront
+// log2(2^a + 2^b) for finite (sentinel-safe) a, b; minus the rebasing increment c.
+__device__ __forceinline__ float lae2(float a, float b, float c) {
+  const float m = fmaxf(a, b);
+  const float e = ex2_approx(-fabsf(a - b));
+  return (m - c) + lg2_approx(1.0f + e);
+}
+
+template <int R>
+__device__ __forceinline__ void lds_row(const float* p, float (&x)[R]) {
+  if constexpr (R % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < R; j += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + j);
+      x[j] = q.x; x[j + 1] = q.y; x[j + 2] = q.z; x[j + 3] = q.w;
+    }
+  } else if constexpr (R % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < R; j += 2) {
+      const float2 q = *reinterpret_cast<const float2*>(p + j);
+      x[j] = q.x; x[j + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) x[j] = p[j];
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void stg_row(float* p, const float (&x)[R]) {
+  if constexpr (R % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < R; j += 4) *reinterpret_cast<float4*>(p + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+  } else if constexpr (R % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < R; j += 2) *reinterpret_cast<float2*>(p + j) = make_float2(x[j], x[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) p[j] = x[j];
+  }
+}
+
+__device__ __forceinline__ float warp_max_uniform(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// One direction of the wavefront.  FWD: alpha over diagonals 0 -> Kn; else beta over Kn -> 0.
+// `ring` holds the arc rows in consumption order: chunk c (CH rows) in stage c % NST.
+template <int R, bool FWD>
+__device__ __forceinline__ void wavefront(const float* ring, uint64_t* full, uint64_t* empty, int Kn, int Un,
+                                          float* out, double* shift, double* Ltot_n, float* loss_n,
+                                          int32_t* status, int n) {
+  using namespace lat;
+  constexpr int LU = 32 * R, C = CH<R>;
+  constexpr size_t STAGE = (size_t)2 * C * LU;
+  const int lane = threadIdx.x & 31;
+  const int u0 = lane * R;
+  float a[R];
+  const int start_u = FWD ? 0 : Un;
+#pragma unroll
+  for (int j = 0; j < R; ++j) a[j] = (u0 + j == start_u) ? 0.f : kNegBig;
+  stg_row<R>(out + (size_t)(FWD ? 0 : Kn) * LU + u0, a);
+  if (lane == 0) shift[FWD ? 0 : Kn] = 0.0;
+
+  double S = 0.0;                   // A_i (fp64) of the current diagonal
+  float Mm2 = 0.f, Mm1 = 0.f;       // max of diagonals i-2, i-1 (relative to their shifts)
+  float cprev = 0.f;                // rebasing increment of diagonal i-1
+  int stage = 0, slot = 0;
+  uint32_t phase = 0;
+  // beta consumes rows Kn-1 .. 0; its chunk c holds rows [max(0, Kn-(c+1)C), Kn-cC) in natural
+  // order, so the row of step i sits at slot (C-1-slot) except in the last, short chunk.
+  int first_slot_b = (Kn >= C) ? C - 1 : Kn - 1;   // slot index of the first row of the current chunk
+  int rows_left = Kn;
+  for (int i = 1; i <= Kn; ++i) {
+    if (slot == 0) tc::mbar_wait(&full[stage], phase);
+    const int sidx = FWD ? slot : first_slot_b - slot;
+    const float* rx = ring + stage * STAGE + (size_t)sidx * LU + u0;
+    float px[R], py[R];
+    lds_row<R>(rx, px);
+    lds_row<R>(rx + (size_t)C * LU, py);
+    const float ci = (i >= 2) ? Mm2 - cprev : 0.f;          // A_i = A_{i-2} + M_{i-2}
+    float nw[R];
+    if constexpr (FWD) {
+      float h[R], v[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) { h[j] = a[j] + py[j]; v[j] = a[j] + px[j]; }
+      float nb = __shfl_up_sync(0xffffffffu, v[R - 1], 1);
+      if (lane == 0) nb = kNegBig;
+#pragma unroll
+      for (int j = R - 1; j >= 1; --j) nw[j] = lae2(h[j], v[j - 1], ci);
+      nw[0] = lae2(h[0], nb, ci);
+    } else {
+      float nb = __shfl_down_sync(0xffffffffu, a[0], 1);
+      if (lane == 31) nb = kNegBig;
+#pragma unroll
+      for (int j = 0; j < R - 1; ++j) nw[j] = lae2(a[j] + py[j], a[j + 1] + px[j], ci);
+      nw[R - 1] = lae2(a[R - 1] + py[R - 1], nb + px[R - 1], ci);
+    }
+    if (++slot == C || i == Kn) {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[stage]);
+      slot = 0;
+      rows_left -= C;
+      first_slot_b = (rows_left >= C) ? C - 1 : rows_left - 1;
+      if (++stage == NST) { stage = 0; phase ^= 1; }
+    }
+    float mx = nw[0];
+#pragma unroll
+    for (int j = 0; j < R; ++j) { a[j] = nw[j]; mx = fmaxf(mx, nw[j]); }
+    const int orow = FWD ? i : Kn - i;
+    stg_row<R>(out + (size_t)orow * LU + u0, a);
+    S += (double)ci;
+    if (lane == 0) shift[orow] = S;
+    const float Mi = warp_max_uniform(mx);
+    Mm2 = Mm1;
+    Mm1 = Mi;
+    cprev = ci;
+  }
+  if constexpr (FWD) {
+    // L_tot = alpha at the virtual node (T_n, U_n) = alpha(T-1,U) + empty(T-1,U)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (u0 + j == Un) {
+        const double L = ((double)a[j] + S) * RNNT_LN2;
+        *Ltot_n = L;
+        *loss_n = (float)(-L);
+        if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+      }
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(64, 1) lattice_fb_kernel(
+    const float* __restrict__ px2, const float* __restrict__ py2, const int64_t* __restrict__ bnd, int K,
+    float* __restrict__ ahat, float* __restrict__ bhat, double* __restrict__ Ash, double* __restrict__ Bsh,
+    double* __restrict__ Ltot, float* __restrict__ loss, int32_t* __restrict__ status) {
+  using namespace lat;
+  constexpr int LU = 32 * R, C = CH<R>;
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const int n = blockIdx.x;
+  const bool fwd = blockIdx.y == 0;
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n), Kn = Tn + Un;
+  const size_t base = (size_t)n * (K + 1) * LU;
+  const size_t sbase = (size_t)n * (K + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == 1) {
+    // ---- loader: arc rows in consumption order (alpha ascending, beta descending)
+    if (lane == 0) {
+      const int nch = (Kn + C - 1) / C;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int c = 0; c < nch; ++c) {
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        int r0, r1;
+        if (fwd) { r0 = c * C; r1 = min(Kn, r0 + C); }
+        else { r1 = Kn - c * C; r0 = max(0, r1 - C); }
+        const uint32_t bytes = (uint32_t)(r1 - r0) * LU * 4u;
+        tc::mbar_arrive_expect_tx(&full[s], 2 * bytes);
+        float* dx = ring + (size_t)s * 2 * C * LU;
+        tc::bulk_load(dx, px2 + base + (size_t)r0 * LU, bytes, &full[s]);
+        tc::bulk_load(dx + (size_t)C * LU, py2 + base + (size_t)r0 * LU, bytes, &full[s]);
+        if (++s == NST) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+  if (fwd)
+    wavefront<R, true>(ring, full, empty, Kn, Un, ahat + base, Ash + sbase, Ltot + n, loss + n, status, n);
+  else
+    wavefront<R, false>(ring, full, empty, Kn, Un, bhat + base, Bsh + sbase, Ltot + n, loss + n, status, n);
+}
+
+// ------------------------------------------------------------------ K4 combine
+// Per block of 32 anti-diagonals: Z_k = sum_u (y'+empty') (should be 1), then the
+// normalised occupancies and G~ = (y'+empty')/S(t,u), written t-major through a 32x32 smem transpose.
+__global__ void __launch_bounds__(256) combine_kernel(
+    const float* __restrict__ px2, const float* __restrict__ py2, const float* __restrict__ rS,
+    const float* __restrict__ ahat, const float* __restrict__ bhat, const double* __restrict__ Ash,
+    const double* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
+    int U, int LU, int K, float* __restrict__ px_grad, float* __restrict__ py_grad, float* __restrict__ Gt) {
+  __shared__ float sy[32][33], sb[32][33], sg[32][33];
+  __shared__ float s_off[32], s_rz[32];
+  const int n = blockIdx.y;
+  const int k0 = blockIdx.x * 32;
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n), Kn = Tn + Un;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t base = (size_t)n * (K + 1) * LU;
+  const size_t sbase = (size_t)n * (K + 1);
+  const double L2 = Ltot[n] * RNNT_LOG2E;
+  const bool finite = isfinite(L2);
+  const int U1 = U + 1;
+
+  // pass 1: outflow of each diagonal
+  for (int kr = warp; kr < 32; kr += 8) {
+    const int k = k0 + kr;
+    float off = 0.f, rz = 0.f;
+    if (finite && k < Kn) {
+      off = (float)(Ash[sbase + k] + Bsh[sbase + k + 1] - L2);
+      const float* A = ahat + base + (size_t)k * LU;
+      const float* B = bhat + base + (size_t)(k + 1) * LU;
+      const float* X = px2 + base + (size_t)k * LU;
+      const float* Y = py2 + base + (size_t)k * LU;
+      const int ulo = max(0, k - Tn + 1), uhi = min(k, Un);
+      float z = 0.f;
+      for (int u = ulo + lane; u <= uhi; u += 32) {
+        const float a = A[u] + off;
+        z += ex2_approx(a + Y[u] + B[u]);
+        if (u < Un) z += ex2_approx(a + X[u] + B[u + 1]);
+      }
+      z = warp_sum(z);
+      rz = (z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
+    }
+    if (lane == 0) { s_off[kr] = off; s_rz[kr] = rz; }
+  }
+  __syncthreads();
+
+  const int t_base0 = k0 - 31;
+  for (int ub = 0; ub < U1; ub += 32) {
+    for (int kr = warp; kr < 32; kr += 8) {
+      const int k = k0 + kr, u = ub + lane, t = k - u;
+      float yv = 0.f, bv = 0.f, g = 0.f;
+      const float rz = s_rz[kr];
+      if (rz > 0.f && t >= 0 && t < Tn && u <= Un) {
+        const size_t i = base + (size_t)k * LU + u;
+        const float a = ahat[i] + s_off[kr];
+        const float* B = bhat + base + (size_t)(k + 1) * LU;
+        if (u < Un) yv = ex2_approx(a + px2[i] + B[u + 1]) * rz;
+        bv = ex2_approx(a + py2[i] + B[u]) * rz;
+        g = (yv + bv) * rS[i];
+      }
+      sy[kr][lane] = yv;
+      sb[kr][lane] = bv;
+      sg[kr][lane] = g;
+    }
+    __syncthreads();
+    const int t_base = t_base0 - ub;
+    for (int tr = warp; tr < 63; tr += 8) {
+      const int t = t_base + tr, u = ub + lane, kr = tr + lane - 31;
+      if (kr >= 0 && kr < 32 && t >= 0 && t < T && u < U1) {
+        const size_t o = ((size_t)n * T + t) * U1 + u;
+        px_grad[o] = sy[kr][lane];
+        py_grad[o] = sb[kr][lane];
+        Gt[o] = sg[kr][lane];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host
+template <int R>
+static cudaError_t launch_fb(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, int32_t* status,
+                             cudaStream_t st) {
+  constexpr size_t sm = lat::smem_bytes<R>;
+  cudaFuncSetAttribute(lattice_fb_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  RNNT_LAUNCH(KID_ALPHA, st, lattice_fb_kernel<R><<<dim3(d.N, 2), 64, sm, st>>>(
+      w.px2, w.py2, bnd, d.K(), w.alpha, w.beta, w.Ash, w.Bsh, w.Ltot, loss, status));
+  return cudaGetLastError();
+}
+
+cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st) {
+  const long long cells = (long long)(d.K() + 1) * d.LU();
+  const unsigned bx = (unsigned)std::min<long long>((cells + 255) / 256, 64);
+  RNNT_LAUNCH(KID_SKEW_FILL, st, skew_fill_kernel<<<dim3(bx, d.N), 256, 0, st>>>(bnd, d.LU(), d.K(), w.px2, w.py2));
+  return cudaGetLastError();
+}
+
+cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, float* px_grad,
+                           float* py_grad, int32_t* status, cudaStream_t st) {
+  cudaError_t e;
+  switch (d.lat_R()) {
+    case 1: e = launch_fb<1>(d, w, bnd, loss, status, st); break;
+    case 2: e = launch_fb<2>(d, w, bnd, loss, status, st); break;
+    case 4: e = launch_fb<4>(d, w, bnd, loss, status, st); break;
+    case 6: e = launch_fb<6>(d, w, bnd, loss, status, st); break;
+    case 8: e = launch_fb<8>(d, w, bnd, loss, status, st); break;
+    case 12: e = launch_fb<12>(d, w, bnd, loss, status, st); break;
+    case 16: e = launch_fb<16>(d, w, bnd, loss, status, st); break;
+    case 24: e = launch_fb<24>(d, w, bnd, loss, status, st); break;
+    case 32: e = launch_fb<32>(d, w, bnd, loss, status, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  dim3 grid((d.K() + 31) / 32, d.N);
+  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
+                                                                   w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), px_grad,
+                                                                   py_grad, w.Gt));
+  return cudaGetLastError();
+}
+
+}  // namespace rnnt

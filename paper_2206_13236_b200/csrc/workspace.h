@@ -10,7 +10,16 @@ namespace rnnt {
 struct Dims {
   int N, T, U, V, J, S;
   int U1() const { return U + 1; }
-  int LU() const { return ((U + 1) + 7) / 8 * 8; }   // skewed row length (u), padded
+  // Columns per lane of the wavefront warp (lattice.cu) and the skewed row pitch LU = 32 R, so
+  // every lane owns whole columns of every row (no partial lanes, no masks).
+  int lat_R() const {
+    const int need = (U + 1 + 31) / 32;
+    const int Rs[9] = {1, 2, 4, 6, 8, 12, 16, 24, 32};
+    for (int r : Rs)
+      if (r >= need) return r;
+    return 0;   // unsupported (U + 1 > 1024)
+  }
+  int LU() const { return 32 * lat_R(); }
   int K() const { return T + U; }                       // number of anti-diagonals
   long long rows() const { return (long long)N * T * S; }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
@@ -25,8 +34,10 @@ struct SimpleWS {
   float* px2;     // (N,K+1,LU) skewed y(t,u)*log2e      (k = t+u)
   float* py2;     // (N,K+1,LU) skewed empty(t,u)*log2e
   float* rS;      // (N,K+1,LU) skewed 1/sum_v exp(am-m_am+lm-m_lm)
-  double* alpha;  // (N,K+1,LU) skewed alpha*log2e (fp64)
-  double* beta;   // (N,K+1,LU) skewed beta*log2e  (fp64)
+  float* alpha;   // (N,K+1,LU) skewed alpha-hat = alpha*log2e - A_k (fp32, rebased)
+  float* beta;    // (N,K+1,LU) skewed beta-hat  = beta*log2e - B_k
+  double* Ash;    // (N,K+1)    A_k per diagonal (fp64)
+  double* Bsh;    // (N,K+1)    B_k per diagonal
   double* Ltot;   // (N)        L_tot (natural log)
   float* Gt;      // (N,T,U+1)  (y'+empty') / S(t,u)   (t-major)
 };
@@ -81,8 +92,10 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.px2 = (float*)take(N * K1 * LU * 4);
   s.py2 = (float*)take(N * K1 * LU * 4);
   s.rS = (float*)take(N * K1 * LU * 4);
-  s.alpha = (double*)take(N * K1 * LU * 8);
-  s.beta = (double*)take(N * K1 * LU * 8);
+  s.alpha = (float*)take(N * K1 * LU * 4);
+  s.beta = (float*)take(N * K1 * LU * 4);
+  s.Ash = (double*)take(N * K1 * 8);
+  s.Bsh = (double*)take(N * K1 * 8);
   s.Ltot = (double*)take(N * 8);
   s.Gt = (float*)take(N * T * U1 * 4);
   PrunedWS p;

@@ -32,7 +32,7 @@ static const char* const kNames[KID_COUNT] = {
     "none", "validate", "rowmax_am", "rowmax_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
     "lattice_combine", "simple_am_grad_gemm", "simple_am_picks", "simple_lm_grad_gemm", "simple_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
-    "pruned_alpha", "pruned_beta", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",
+    "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad"};
 
 const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }

@@ -206,11 +206,11 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
         const float l = M + lg2_approx(sum) * RNNT_LN2_F;
         p.lse[r] = l;
         p.py2[r] = (zb - l) * RNNT_LOG2E_F;
-        p.px2[r] = info < p.V ? (zl - l) * RNNT_LOG2E_F : neg_inf_f();
+        p.px2[r] = info < p.V ? (zl - l) * RNNT_LOG2E_F : kNegBig;   // y(t,U) = -inf
       } else {
         p.lse[r] = 0.f;
-        p.px2[r] = neg_inf_f();
-        p.py2[r] = neg_inf_f();
+        p.px2[r] = kNegBig;
+        p.py2[r] = kNegBig;
       }
     }
   }

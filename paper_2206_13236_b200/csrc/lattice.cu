@@ -37,12 +37,20 @@
 namespace rnnt {
 
 namespace lat {
-constexpr int NST = 4;   // ring stages
-// arc rows (diagonals) per staged chunk: the ring holds NST x 2 arrays x CH rows x 32R floats
+constexpr int NST = 6;   // arc-ring stages
+constexpr int NX = 8;    // boundary-exchange chunk slots (>= NST + 1: no overwrite before consumption)
+constexpr int MAXW = 4;  // strips (warps) per direction
+// arc rows (diagonals) per staged chunk; the ring holds NST x 2 arrays x C rows x LU floats
 template <int R>
-constexpr int CH = R <= 8 ? 16 : (R <= 16 ? 8 : 4);
+constexpr int CH = R <= 2 ? 16 : (R == 4 ? 8 : 4);
+struct Xchg {            // boundary values between neighbouring strips, per inbox warp
+  float v[MAXW][NX][16];
+  double s[MAXW][NX][16];
+};
 template <int R>
-constexpr size_t smem_bytes = (size_t)NST * 2 * CH<R> * 32 * R * sizeof(float);
+inline size_t smem_bytes(int W) {
+  return (size_t)NST * 2 * CH<R> * 32 * R * W * sizeof(float) + sizeof(Xchg);
+}
 }  // namespace lat
 
 // ------------------------------------------------------------------ sentinel fill
@@ -110,115 +118,158 @@ __device__ __forceinline__ float warp_max_uniform(float v) {
   return r;
 }
 
-// One direction of the wavefront.  FWD: alpha over diagonals 0 -> Kn; else beta over Kn -> 0.
-// `ring` holds the arc rows in consumption order: chunk c (CH rows) in stage c % NST.
-template <int R, bool FWD>
-__device__ __forceinline__ void wavefront(const float* ring, uint64_t* full, uint64_t* empty, int Kn, int Un,
-                                          float* out, double* shift, double* Ltot_n, float* loss_n,
-                                          int32_t* status, int n) {
-  using namespace lat;
-  constexpr int LU = 32 * R, C = CH<R>;
-  constexpr size_t STAGE = (size_t)2 * C * LU;
-  const int lane = threadIdx.x & 31;
-  const int u0 = lane * R;
-  float a[R];
-  const int start_u = FWD ? 0 : Un;
-#pragma unroll
-  for (int j = 0; j < R; ++j) a[j] = (u0 + j == start_u) ? 0.f : kNegBig;
-  stg_row<R>(out + (size_t)(FWD ? 0 : Kn) * LU + u0, a);
-  if (lane == 0) shift[FWD ? 0 : Kn] = 0.0;
+// One direction of the wavefront for strip (warp) w of Wn active strips.
+// FWD: alpha over diagonals 0 -> Kn (strips pipelined left to right); else beta over Kn -> 0
+// (right to left).  Strip w lags its upstream neighbour by one chunk: the neighbour's boundary
+// arc for every step of chunk c (with its fp64 shift) sits in the inbox before w starts chunk c.
+// R, W and the chunk length C are compile-time so that a full chunk is straight-line code with
+// immediate smem / global offsets (the per-step chain is then LogAdd + one shuffle, ~85 cycles).
+template <int R, int W, bool FWD>
+struct Wavefront {
+  static constexpr int C = lat::CH<R>;
+  static constexpr int LU = 32 * R * W;
+  static constexpr size_t STAGE = (size_t)2 * C * LU;
 
-  double S = 0.0;                   // A_i (fp64) of the current diagonal
-  float Mm2 = 0.f, Mm1 = 0.f;       // max of diagonals i-2, i-1 (relative to their shifts)
+  float a[R];
+  double S = 0.0;                   // this strip's shift of the current diagonal (fp64)
+  float Mm2 = 0.f, Mm1 = 0.f;       // strip max of diagonals i-2, i-1 (relative to their shifts)
   float cprev = 0.f;                // rebasing increment of diagonal i-1
-  int stage = 0, slot = 0;
-  uint32_t phase = 0;
-  // beta consumes rows Kn-1 .. 0; its chunk c holds rows [max(0, Kn-(c+1)C), Kn-cC) in natural
-  // order, so the row of step i sits at slot (C-1-slot) except in the last, short chunk.
-  int first_slot_b = (Kn >= C) ? C - 1 : Kn - 1;   // slot index of the first row of the current chunk
-  int rows_left = Kn;
-  for (int i = 1; i <= Kn; ++i) {
-    if (slot == 0) tc::mbar_wait(&full[stage], phase);
-    const int sidx = FWD ? slot : first_slot_b - slot;
-    const float* rx = ring + stage * STAGE + (size_t)sidx * LU + u0;
+  int lane, w;
+  bool has_in, has_out;
+
+  // Step i of the chunk: arcs at `rx`, boundary inbox/outbox slot `xs`, outputs at `orow` (row
+  // pointer of this lane's columns) and `oshift`.
+  __device__ __forceinline__ void step(const float* rx, int i, const float* xv_in, const double* xs_in, float* xv_out,
+                                       double* xs_out, float* orow, double* oshift) {
     float px[R], py[R];
     lds_row<R>(rx, px);
     lds_row<R>(rx + (size_t)C * LU, py);
-    const float ci = (i >= 2) ? Mm2 - cprev : 0.f;          // A_i = A_{i-2} + M_{i-2}
+    float xin = kNegBig;
+    if (has_in && lane == (FWD ? 0 : 31)) xin = *xv_in + (float)(*xs_in - S);
+    // A_i = A_{i-2} + M_{i-2}; a strip with no live cell two diagonals back keeps A_i = A_{i-1}
+    const float ci = (i >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
     float nw[R];
     if constexpr (FWD) {
       float h[R], v[R];
 #pragma unroll
-      for (int j = 0; j < R; ++j) { h[j] = a[j] + py[j]; v[j] = a[j] + px[j]; }
+      for (int q = 0; q < R; ++q) { h[q] = a[q] + py[q]; v[q] = a[q] + px[q]; }
+      if (has_out && lane == 31) { *xv_out = v[R - 1]; *xs_out = S; }
       float nb = __shfl_up_sync(0xffffffffu, v[R - 1], 1);
-      if (lane == 0) nb = kNegBig;
+      if (lane == 0) nb = xin;
 #pragma unroll
-      for (int j = R - 1; j >= 1; --j) nw[j] = lae2(h[j], v[j - 1], ci);
+      for (int q = R - 1; q >= 1; --q) nw[q] = lae2(h[q], v[q - 1], ci);
       nw[0] = lae2(h[0], nb, ci);
     } else {
+      if (has_out && lane == 0) { *xv_out = a[0]; *xs_out = S; }
       float nb = __shfl_down_sync(0xffffffffu, a[0], 1);
-      if (lane == 31) nb = kNegBig;
+      if (lane == 31) nb = xin;
 #pragma unroll
-      for (int j = 0; j < R - 1; ++j) nw[j] = lae2(a[j] + py[j], a[j + 1] + px[j], ci);
+      for (int q = 0; q < R - 1; ++q) nw[q] = lae2(a[q] + py[q], a[q + 1] + px[q], ci);
       nw[R - 1] = lae2(a[R - 1] + py[R - 1], nb + px[R - 1], ci);
-    }
-    if (++slot == C || i == Kn) {
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&empty[stage]);
-      slot = 0;
-      rows_left -= C;
-      first_slot_b = (rows_left >= C) ? C - 1 : rows_left - 1;
-      if (++stage == NST) { stage = 0; phase ^= 1; }
     }
     float mx = nw[0];
 #pragma unroll
-    for (int j = 0; j < R; ++j) { a[j] = nw[j]; mx = fmaxf(mx, nw[j]); }
-    const int orow = FWD ? i : Kn - i;
-    stg_row<R>(out + (size_t)orow * LU + u0, a);
+    for (int q = 0; q < R; ++q) { a[q] = nw[q]; mx = fmaxf(mx, nw[q]); }
+    stg_row<R>(orow, a);
     S += (double)ci;
-    if (lane == 0) shift[orow] = S;
+    if (lane == 0) *oshift = S;
     const float Mi = warp_max_uniform(mx);
     Mm2 = Mm1;
     Mm1 = Mi;
     cprev = ci;
   }
-  if constexpr (FWD) {
-    // L_tot = alpha at the virtual node (T_n, U_n) = alpha(T-1,U) + empty(T-1,U)
+
+  __device__ __forceinline__ void run(const float* ring, uint64_t* full, uint64_t* empty, uint64_t* xbar,
+                                      lat::Xchg* xc, int w_, int Wn, int Kn, int Un, float* out, double* shift,
+                                      double* Ltot_n, float* loss_n, int32_t* status, int n) {
+    using namespace lat;
+    lane = threadIdx.x & 31;
+    w = w_;
+    const int u0 = 32 * R * w + lane * R;
+    has_in = FWD ? (w > 0) : (w < Wn - 1);
+    has_out = FWD ? (w < Wn - 1) : (w > 0);
+    const int inbox = w, outbox = FWD ? w + 1 : w - 1;
+    const int start_u = FWD ? 0 : Un;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-      if (u0 + j == Un) {
-        const double L = ((double)a[j] + S) * RNNT_LN2;
-        *Ltot_n = L;
-        *loss_n = (float)(-L);
-        if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+    for (int q = 0; q < R; ++q) a[q] = (u0 + q == start_u) ? 0.f : kNegBig;
+    stg_row<R>(out + (size_t)(FWD ? 0 : Kn) * LU + u0, a);
+    if (lane == 0) shift[(size_t)(FWD ? 0 : Kn) * W + w] = 0.0;
+
+    constexpr int DR = FWD ? 1 : -1;     // output row direction
+    int stage = 0, done = 0;
+    uint32_t phase = 0;
+    for (int c = 0; done < Kn; ++c) {
+      const int rows = (Kn - done < C) ? Kn - done : C;
+      tc::mbar_wait(&full[stage], phase);
+      if (has_in) tc::mbar_wait(&xbar[inbox * NX + c % NX], (c / NX) & 1);
+      const float* rb = ring + stage * STAGE + u0;
+      const int slot = c % NX;
+      const float* xvi = &xc->v[inbox][slot][0];
+      const double* xsi = &xc->s[inbox][slot][0];
+      float* xvo = &xc->v[outbox < 0 ? 0 : (outbox >= MAXW ? MAXW - 1 : outbox)][slot][0];
+      double* xso = &xc->s[outbox < 0 ? 0 : (outbox >= MAXW ? MAXW - 1 : outbox)][slot][0];
+      const int orow0 = FWD ? done + 1 : Kn - done - 1;
+      float* ob = out + (size_t)orow0 * LU + u0;
+      double* osb = shift + (size_t)orow0 * W + w;
+      if (rows == C) {
+#pragma unroll
+        for (int j = 0; j < C; ++j)
+          step(rb + (FWD ? j : C - 1 - j) * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j, ob + DR * j * LU,
+               osb + DR * j * W);
+      } else {
+#pragma unroll 1
+        for (int j = 0; j < rows; ++j)
+          step(rb + (FWD ? j : rows - 1 - j) * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j,
+               ob + DR * j * LU, osb + DR * j * W);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[stage]);
+      if (has_out && lane == (FWD ? 31 : 0)) tc::mbar_arrive(&xbar[outbox * NX + slot]);
+      if (++stage == NST) { stage = 0; phase ^= 1; }
+      done += rows;
+    }
+    if constexpr (FWD) {
+      // L_tot = alpha at the virtual node (T_n, U_n) = alpha(T-1,U) + empty(T-1,U)
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (u0 + q == Un) {
+          const double L = ((double)a[q] + S) * RNNT_LN2;
+          *Ltot_n = L;
+          *loss_n = (float)(-L);
+          if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+        }
       }
     }
   }
-}
+};
 
-template <int R>
-__global__ void __launch_bounds__(64, 1) lattice_fb_kernel(
+// grid (N, 2): y = 0 alpha, y = 1 beta.  Warps 0..W-1: strips; warp W: bulk-copy loader.
+template <int R, int W>
+__global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const int64_t* __restrict__ bnd, int K,
     float* __restrict__ ahat, float* __restrict__ bhat, double* __restrict__ Ash, double* __restrict__ Bsh,
     double* __restrict__ Ltot, float* __restrict__ loss, int32_t* __restrict__ status) {
   using namespace lat;
-  constexpr int LU = 32 * R, C = CH<R>;
+  constexpr int C = CH<R>, LU = 32 * R * W;
   extern __shared__ __align__(128) float ring[];
-  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], xbar[MAXW * NX];
   const int n = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n), Kn = Tn + Un;
+  const int Wn = (Un + 1 + 32 * R - 1) / (32 * R);          // strips holding a column <= U_n
   const size_t base = (size_t)n * (K + 1) * LU;
-  const size_t sbase = (size_t)n * (K + 1);
+  const size_t sbase = (size_t)n * (K + 1) * W;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Xchg* xc = reinterpret_cast<Xchg*>(ring + (size_t)NST * 2 * C * LU);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], Wn); }
+    for (int s = 0; s < MAXW * NX; ++s) tc::mbar_init(&xbar[s], 1);
     tc::fence_barrier_init();
   }
   __syncthreads();
 
-  if (warp == 1) {
+  if (warp == W) {
     // ---- loader: arc rows in consumption order (alpha ascending, beta descending)
     if (lane == 0) {
       const int nch = (Kn + C - 1) / C;
@@ -239,10 +290,14 @@ __global__ void __launch_bounds__(64, 1) lattice_fb_kernel(
     }
     return;
   }
-  if (fwd)
-    wavefront<R, true>(ring, full, empty, Kn, Un, ahat + base, Ash + sbase, Ltot + n, loss + n, status, n);
-  else
-    wavefront<R, false>(ring, full, empty, Kn, Un, bhat + base, Bsh + sbase, Ltot + n, loss + n, status, n);
+  if (warp >= Wn) return;   // strip entirely beyond U_n: never holds a lattice cell
+  if (fwd) {
+    Wavefront<R, W, true> wf;
+    wf.run(ring, full, empty, xbar, xc, warp, Wn, Kn, Un, ahat + base, Ash + sbase, Ltot + n, loss + n, status, n);
+  } else {
+    Wavefront<R, W, false> wf;
+    wf.run(ring, full, empty, xbar, xc, warp, Wn, Kn, Un, bhat + base, Bsh + sbase, Ltot + n, loss + n, status, n);
+  }
 }
 
 // ------------------------------------------------------------------ K4 combine
@@ -252,15 +307,18 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const double* __restrict__ Ash,
     const double* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
-    int U, int LU, int K, float* __restrict__ px_grad, float* __restrict__ py_grad, float* __restrict__ Gt) {
+    int U, int LU, int K, int W, int SW, float* __restrict__ px_grad, float* __restrict__ py_grad,
+    float* __restrict__ Gt) {
   __shared__ float sy[32][33], sb[32][33], sg[32][33];
-  __shared__ float s_off[32], s_rz[32];
+  // per diagonal and strip: ob = A^w_k + B^w_{k+1} - L (blank arc, same column), ox = A^w_k +
+  // B^{w+1}_{k+1} - L (label arc out of the strip's last column into the next strip)
+  __shared__ float s_ob[32][lat::MAXW], s_ox[32][lat::MAXW], s_rz[32];
   const int n = blockIdx.y;
   const int k0 = blockIdx.x * 32;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n), Kn = Tn + Un;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t base = (size_t)n * (K + 1) * LU;
-  const size_t sbase = (size_t)n * (K + 1);
+  const size_t sbase = (size_t)n * (K + 1) * W;
   const double L2 = Ltot[n] * RNNT_LOG2E;
   const bool finite = isfinite(L2);
   const int U1 = U + 1;
@@ -268,24 +326,30 @@ __global__ void __launch_bounds__(256) combine_kernel(
   // pass 1: outflow of each diagonal
   for (int kr = warp; kr < 32; kr += 8) {
     const int k = k0 + kr;
-    float off = 0.f, rz = 0.f;
+    float rz = 0.f;
     if (finite && k < Kn) {
-      off = (float)(Ash[sbase + k] + Bsh[sbase + k + 1] - L2);
-      const float* A = ahat + base + (size_t)k * LU;
-      const float* B = bhat + base + (size_t)(k + 1) * LU;
+      if (lane < W) {
+        const double A = Ash[sbase + (size_t)k * W + lane];
+        s_ob[kr][lane] = (float)(A + Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
+        s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
+      }
+      __syncwarp();
+      const float* Ar = ahat + base + (size_t)k * LU;
+      const float* Br = bhat + base + (size_t)(k + 1) * LU;
       const float* X = px2 + base + (size_t)k * LU;
       const float* Y = py2 + base + (size_t)k * LU;
       const int ulo = max(0, k - Tn + 1), uhi = min(k, Un);
       float z = 0.f;
       for (int u = ulo + lane; u <= uhi; u += 32) {
-        const float a = A[u] + off;
-        z += ex2_approx(a + Y[u] + B[u]);
-        if (u < Un) z += ex2_approx(a + X[u] + B[u + 1]);
+        const int w = u / SW;
+        const float a = Ar[u];
+        z += ex2_approx(a + Y[u] + Br[u] + s_ob[kr][w]);
+        if (u < Un) z += ex2_approx(a + X[u] + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
       }
       z = warp_sum(z);
       rz = (z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
     }
-    if (lane == 0) { s_off[kr] = off; s_rz[kr] = rz; }
+    if (lane == 0) s_rz[kr] = rz;
   }
   __syncthreads();
 
@@ -297,10 +361,11 @@ __global__ void __launch_bounds__(256) combine_kernel(
       const float rz = s_rz[kr];
       if (rz > 0.f && t >= 0 && t < Tn && u <= Un) {
         const size_t i = base + (size_t)k * LU + u;
-        const float a = ahat[i] + s_off[kr];
-        const float* B = bhat + base + (size_t)(k + 1) * LU;
-        if (u < Un) yv = ex2_approx(a + px2[i] + B[u + 1]) * rz;
-        bv = ex2_approx(a + py2[i] + B[u]) * rz;
+        const int w = u / SW;
+        const float a = ahat[i];
+        const float* Br = bhat + base + (size_t)(k + 1) * LU;
+        if (u < Un) yv = ex2_approx(a + px2[i] + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w])) * rz;
+        bv = ex2_approx(a + py2[i] + Br[u] + s_ob[kr][w]) * rz;
         g = (yv + bv) * rS[i];
       }
       sy[kr][lane] = yv;
@@ -323,14 +388,26 @@ __global__ void __launch_bounds__(256) combine_kernel(
 }
 
 // ------------------------------------------------------------------ host
-template <int R>
+template <int R, int W>
 static cudaError_t launch_fb(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, int32_t* status,
                              cudaStream_t st) {
-  constexpr size_t sm = lat::smem_bytes<R>;
-  cudaFuncSetAttribute(lattice_fb_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  RNNT_LAUNCH(KID_ALPHA, st, lattice_fb_kernel<R><<<dim3(d.N, 2), 64, sm, st>>>(
+  const size_t sm = lat::smem_bytes<R>(W);
+  cudaFuncSetAttribute(lattice_fb_kernel<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  RNNT_LAUNCH(KID_ALPHA, st, lattice_fb_kernel<R, W><<<dim3(d.N, 2), 32 * (W + 1), sm, st>>>(
       w.px2, w.py2, bnd, d.K(), w.alpha, w.beta, w.Ash, w.Bsh, w.Ltot, loss, status));
   return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_fb_w(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, int32_t* status,
+                               cudaStream_t st) {
+  switch (d.lat_W()) {
+    case 1: return launch_fb<R, 1>(d, w, bnd, loss, status, st);
+    case 2: return launch_fb<R, 2>(d, w, bnd, loss, status, st);
+    case 3: return launch_fb<R, 3>(d, w, bnd, loss, status, st);
+    case 4: return launch_fb<R, 4>(d, w, bnd, loss, status, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st) {
@@ -344,22 +421,17 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
                            float* py_grad, int32_t* status, cudaStream_t st) {
   cudaError_t e;
   switch (d.lat_R()) {
-    case 1: e = launch_fb<1>(d, w, bnd, loss, status, st); break;
-    case 2: e = launch_fb<2>(d, w, bnd, loss, status, st); break;
-    case 4: e = launch_fb<4>(d, w, bnd, loss, status, st); break;
-    case 6: e = launch_fb<6>(d, w, bnd, loss, status, st); break;
-    case 8: e = launch_fb<8>(d, w, bnd, loss, status, st); break;
-    case 12: e = launch_fb<12>(d, w, bnd, loss, status, st); break;
-    case 16: e = launch_fb<16>(d, w, bnd, loss, status, st); break;
-    case 24: e = launch_fb<24>(d, w, bnd, loss, status, st); break;
-    case 32: e = launch_fb<32>(d, w, bnd, loss, status, st); break;
+    case 1: e = launch_fb_w<1>(d, w, bnd, loss, status, st); break;
+    case 2: e = launch_fb_w<2>(d, w, bnd, loss, status, st); break;
+    case 4: e = launch_fb_w<4>(d, w, bnd, loss, status, st); break;
+    case 8: e = launch_fb_w<8>(d, w, bnd, loss, status, st); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
   dim3 grid((d.K() + 31) / 32, d.N);
   RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
-                                                                   w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), px_grad,
-                                                                   py_grad, w.Gt));
+                                                                   w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
+                                                                   32 * d.lat_R(), px_grad, py_grad, w.Gt));
   return cudaGetLastError();
 }
 

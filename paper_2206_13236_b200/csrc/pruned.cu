@@ -16,6 +16,12 @@
 
 namespace rnnt {
 
+__device__ __forceinline__ float warp_max_uniform_p(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, cudaStream_t st);
 struct GradSrc {
@@ -71,46 +77,69 @@ __global__ void prune_kernel(const float* __restrict__ enc, const float* __restr
 
 __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t* __restrict__ sym,
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
-                               int32_t* __restrict__ rowinfo) {
+                               int32_t* __restrict__ rowinfo, int2* __restrict__ urange) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= (long long)N * T * S) return;
   const int s = (int)(r % S);
   const long long nt = r / S;
   const int t = (int)(nt % T), n = (int)(nt / T);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   int info = -1;
-  if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) {
-    const int u = ranges[(size_t)n * T + t] + s;
+  if (t < Tn && feasible) {
+    const int32_t* p = ranges + (size_t)n * T;
+    const int u = p[t] + s;
     if (u < Un) {
       long long y = sym[(size_t)n * U + u];
       info = (y >= 1 && y < V) ? (int)y : V;
     } else if (u == Un) {
       info = V;  // no label arc at u = U_n (y(t,U) = -inf)
     }
+    if (s == 0) {
+      // Frames covering token position u form the contiguous range [lo(u), hi(u)) (p monotone,
+      // Eq. 9).  Frame t is the first cover of u in (p_{t-1}+S-1, p_t+S-1] and the last cover of u
+      // in [p_t, p_{t+1}-1]; over t these intervals partition [0, U_n], so each entry is written once.
+      int2* ur = urange + (size_t)n * (U + 1);
+      const int a0 = (t == 0) ? 0 : p[t - 1] + S;
+      const int a1 = min(p[t] + S - 1, Un);
+      for (int uu = a0; uu <= a1; ++uu) ur[uu].x = t;
+      const int b1 = (t == Tn - 1) ? Un : p[t + 1] - 1;
+      for (int uu = p[t]; uu <= b1; ++uu) ur[uu].y = t + 1;
+    }
   }
   rowinfo[r] = info;
 }
 
 // ------------------------------------------------------------------ K9 pruned recursion
-// Lane s of one warp handles band slot s; it processes frame t at step d_t + s with
-// d_t = t + p_t (strictly increasing), i.e. the anti-diagonal of node (t, p_t + s).
-// Vertical in-arc from lane s-1 (same frame), horizontal in-arc from lane s + (p_t - p_{t-1})
-// (previous frame, same u); both produced exactly one step earlier.
-__global__ void __launch_bounds__(128) pruned_alpha_kernel(
+// Eq. 3 on the band (Fig. 1b lattice).  grid (N, 2): y = 0 alpha, y = 1 beta.
+// Lane s of warp 0 owns band slot s; it processes frame t at anti-diagonal k = d_t + s with
+// d_t = t + p_t strictly increasing (Eq. 9), so both in-arcs of a cell were produced one step
+// earlier: the vertical one by lane s-1 (same frame), the horizontal one by lane s + p_t - p_{t-1}
+// (previous frame).  The state is fp32 rebased per anti-diagonal exactly as in lattice.cu
+// (A_k = A_{k-2} + max of diagonal k-2, one CREDUX per step); shifts are kept in fp64.
+// Arcs (px2 = y_p log2e, py2 = empty_p log2e; kNegBig off the lattice) and p_t are staged in smem.
+__device__ __forceinline__ float plae2(float a, float b, float c) {
+  const float m = fmaxf(a, b);
+  return (m - c) + lg2_approx(1.0f + ex2_approx(-fabsf(a - b)));
+}
+
+__global__ void __launch_bounds__(128) pruned_fb_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const int32_t* __restrict__ ranges,
-    const int64_t* __restrict__ bnd, int T, int S, double* __restrict__ ap, double* __restrict__ Lp,
-    float* __restrict__ loss, int32_t* __restrict__ status) {
-  extern __shared__ unsigned char smem_raw[];
+    const int64_t* __restrict__ bnd, int T, int S, int K, float* __restrict__ ap, float* __restrict__ bp,
+    double* __restrict__ Aps, double* __restrict__ Bps, double* __restrict__ Lp, float* __restrict__ loss,
+    int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = blockIdx.x;
+  const bool fwd = blockIdx.y == 0;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   int* sp = reinterpret_cast<int*>(smem_raw);
   float* sx = reinterpret_cast<float*>(sp + T);
   float* sy = sx + (size_t)T * S;
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   if (!feasible) {
-    if (threadIdx.x == 0) {
+    if (fwd && threadIdx.x == 0) {
       Lp[n] = neg_inf_d();
-      loss[n] = __int_as_float(0x7f800000);  // +inf: no band-respecting path (kept visible)
+      loss[n] = __int_as_float(0x7f800000);  // +inf: no band-respecting path (kept visible, D16)
       set_status(status, n, kStatusInfeasible);
     }
     return;
@@ -121,92 +150,104 @@ __global__ void __launch_bounds__(128) pruned_alpha_kernel(
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int s = threadIdx.x;
-  const double NI = neg_inf_d();
-  double h_out = NI, v_out = NI;
-  int ts = 0;
-  const int kend = (Tn - 1) + sp[Tn - 1] + S - 1;
-  for (int k = 0; k <= kend; ++k) {
-    const bool act = (s < S) && (ts < Tn) && (ts + sp[ts] + s == k);
-    const int t = ts;
-    const int p = act ? sp[t] : 0;
-    const int src = act && t > 0 ? s + p - sp[t - 1] : s;
-    const double hin = __shfl_sync(0xffffffffu, h_out, src < 32 ? src : 31);
-    const double vin = __shfl_up_sync(0xffffffffu, v_out, 1);
-    if (act) {
-      const double left = (t > 0 && src < S) ? hin : NI;
-      const double below = s > 0 ? vin : NI;
-      const int u = p + s;
-      double a = (t == 0 && s == 0) ? 0.0 : logadd2_d(left, below);
-      const bool valid = u <= Un;
-      if (!valid) a = NI;
-      const float px = sx[t * S + s], py = sy[t * S + s];
-      h_out = valid ? a + (double)py : NI;
-      v_out = (valid && u < Un) ? a + (double)px : NI;
-      ap[rbase + (size_t)t * S + s] = a;
-      if (t == Tn - 1 && u == Un) {
-        const double L = h_out * RNNT_LN2;
-        Lp[n] = L;
-        loss[n] = (float)(-L);
-        if (!isfinite(L)) set_status(status, n, kStatusNonFinite);
-      }
-      ++ts;
-    }
-  }
-}
+  const bool lane_on = s < S;
+  const int kend = (Tn - 1) + sp[Tn - 1] + S - 1;   // last anti-diagonal holding a band cell
+  double* shift = (fwd ? Aps : Bps) + (size_t)n * (K + 1);
+  float* outv = (fwd ? ap : bp) + rbase;
 
-// beta in reverse diagonal order: beta(t,u) = LogAdd(beta(t+1,u)+empty(t,u), beta(t,u+1)+y(t,u)).
-__global__ void __launch_bounds__(128) pruned_beta_kernel(
-    const float* __restrict__ px2, const float* __restrict__ py2, const int32_t* __restrict__ ranges,
-    const int64_t* __restrict__ bnd, int T, int S, double* __restrict__ bp) {
-  extern __shared__ unsigned char smem_raw[];
-  const int n = blockIdx.x;
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  if ((long long)Un > (long long)Tn * (S - 1)) return;
-  int* sp = reinterpret_cast<int*>(smem_raw);
-  float* sx = reinterpret_cast<float*>(sp + T);
-  float* sy = sx + (size_t)T * S;
-  const size_t rbase = (size_t)n * T * S;
-  for (int i = threadIdx.x; i < Tn; i += blockDim.x) sp[i] = ranges[(size_t)n * T + i];
-  for (int i = threadIdx.x; i < Tn * S; i += blockDim.x) { sx[i] = px2[rbase + i]; sy[i] = py2[rbase + i]; }
-  __syncthreads();
-  if (threadIdx.x >= 32) return;
-  const int s = threadIdx.x;
-  const double NI = neg_inf_d();
-  double b_out = NI;
-  int ts = Tn - 1;
-  const int kend = (Tn - 1) + sp[Tn - 1] + S - 1;
-  for (int k = kend; k >= 0; --k) {
-    const bool act = (s < S) && (ts >= 0) && (ts + sp[ts] + s == k);
-    const int t = ts;
-    const int p = act ? sp[t] : 0;
-    const int src = (act && t < Tn - 1) ? s - (sp[t + 1] - p) : s;   // slot of (t+1, u) in frame t+1
-    const double rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : 0);
-    const double uin = __shfl_down_sync(0xffffffffu, b_out, 1);
-    if (act) {
-      const int u = p + s;
-      const bool valid = u <= Un;
-      const float px = sx[t * S + s], py = sy[t * S + s];
-      double right;
-      if (t == Tn - 1) right = (u == Un) ? (double)py : NI;          // terminal blank
-      else right = (src >= 0 && src < S) ? rin + (double)py : NI;
-      const double up = (u < Un && s + 1 < S) ? uin + (double)px : NI;
-      double b = logadd2_d(right, up);
-      if (!valid) b = NI;
-      b_out = b;
-      bp[rbase + (size_t)t * S + s] = b;
-      --ts;
+  double Sh = 0.0;
+  float Mm2 = 0.f, Mm1 = 0.f, cprev = 0.f;
+  if (fwd) {
+    float h_out = kNegBig, v_out = kNegBig;
+    int ts = 0;                                          // next frame of this lane
+    int dnext = lane_on ? sp[0] + s : 0x7fffffff;        // its anti-diagonal d_t + s
+    int pprev = 0;
+    for (int k = 0; k <= kend; ++k) {
+      // A_k = A_{k-2} + M_{k-2}; a diagonal with no live cell (max = kNegBig) keeps A_k = A_{k-1}
+      const float ci = (k >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
+      const bool act = (dnext == k);
+      const int t = ts;
+      const int p = act ? sp[t] : 0;
+      const int src = (act && t > 0) ? s + p - pprev : s;
+      const float hin = __shfl_sync(0xffffffffu, h_out, src < 32 ? src : 31);
+      const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
+      float mx = kNegBig;
+      if (act) {
+        const float left = (t > 0 && src < S) ? hin : kNegBig;
+        const float below = s > 0 ? vin : kNegBig;
+        const int u = p + s;
+        float a = (t == 0 && s == 0) ? -ci : plae2(left, below, ci);
+        if (u > Un) a = kNegBig;                           // masked slot (S > U_n + 1, D10)
+        h_out = a + sy[t * S + s];
+        v_out = a + sx[t * S + s];
+        outv[(size_t)t * S + s] = a;
+        mx = a;
+        if (t == Tn - 1 && u == Un) {
+          // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band)
+          const double L = ((double)h_out + Sh + (double)ci) * RNNT_LN2;
+          Lp[n] = L;
+          loss[n] = (float)(-L);
+          if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+        }
+        pprev = p;
+        ts = t + 1;
+        dnext = (ts < Tn) ? ts + sp[ts] + s : 0x7fffffff;
+      }
+      Sh += (double)ci;
+      if (s == 0) shift[k] = Sh;
+      const float Mk = warp_max_uniform_p(mx);
+      Mm2 = Mm1;
+      Mm1 = Mk;
+      cprev = ci;
+    }
+  } else {
+    float b_out = kNegBig;
+    int ts = Tn - 1;                                       // next frame of this lane (descending)
+    int dnext = lane_on ? (Tn - 1) + sp[Tn - 1] + s : -1;
+    for (int k = kend; k >= 0; --k) {
+      const int i = kend - k;
+      const float ci = (i >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
+      const bool act = (dnext == k);
+      const int t = ts;
+      const int p = act ? sp[t] : 0;
+      const int src = (act && t < Tn - 1) ? s - (sp[t + 1] - p) : s;   // slot of (t+1, u) in frame t+1
+      const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : 0);
+      const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
+      float mx = kNegBig;
+      if (act) {
+        const int u = p + s;
+        const float px = sx[t * S + s], py = sy[t * S + s];
+        float right;
+        if (t == Tn - 1) right = (u == Un) ? py : kNegBig;          // terminal blank (virtual end, beta = 0)
+        else right = (src >= 0 && src < S) ? rin + py : kNegBig;
+        const float up = (u < Un && s + 1 < S) ? uin + px : kNegBig;
+        float b = plae2(right, up, ci);
+        if (u > Un) b = kNegBig;
+        b_out = b;
+        outv[(size_t)t * S + s] = b;
+        mx = b;
+        ts = t - 1;
+        dnext = (ts >= 0) ? ts + sp[ts] + s : -1;
+      }
+      Sh += (double)ci;
+      if (s == 0) shift[k] = Sh;
+      const float Mk = warp_max_uniform_p(mx);
+      Mm2 = Mm1;
+      Mm1 = Mk;
+      cprev = ci;
     }
   }
 }
 
 // g_l = y'_p(t,u), g_b = empty'_p(t,u) for u = p_t + s (P:273-281 on the pruned lattice), and
-// the per-(row, tile) softmax scale of the logit gradient.
+// the per-(row, tile) softmax scale of the logit gradient sc = gs (g_b + g_l) exp(m_tile - lse).
 __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float* __restrict__ py2,
-                                      const double* __restrict__ ap, const double* __restrict__ bp,
+                                      const float* __restrict__ ap, const float* __restrict__ bp,
+                                      const double* __restrict__ Aps, const double* __restrict__ Bps,
                                       const double* __restrict__ Lp, const int32_t* __restrict__ ranges,
                                       const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
-                                      int N, int T, int S, int ntile, float gs, float* __restrict__ gb,
+                                      int N, int T, int S, int K, int ntile, float gs, float* __restrict__ gb,
                                       float* __restrict__ gl, float* __restrict__ sc) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= (long long)N * T * S) return;
@@ -218,14 +259,17 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   const double L2 = Lp[n] * RNNT_LOG2E;
   if (rowinfo[r] >= 0 && isfinite(L2)) {
     const int p = ranges[(size_t)n * T + t];
-    const int u = p + s;
-    const double a = ap[r];
-    if (u < Un && s + 1 < S) yb = ex2_approx((float)(a + (double)px2[r] + bp[r + 1] - L2));
+    const int u = p + s, k = t + u;
+    const double* A = Aps + (size_t)n * (K + 1);
+    const double* B = Bps + (size_t)n * (K + 1);
+    const float a = ap[r];
+    if (u < Un && s + 1 < S)
+      yb = ex2_approx(a + px2[r] + bp[r + 1] + (float)(A[k] + B[k + 1] - L2));
     if (t < Tn - 1) {
       const int s2 = u - ranges[(size_t)n * T + t + 1];
-      if (s2 >= 0 && s2 < S) bb = ex2_approx((float)(a + (double)py2[r] + bp[r + S + (s2 - s)] - L2));
+      if (s2 >= 0 && s2 < S) bb = ex2_approx(a + py2[r] + bp[r + S + (s2 - s)] + (float)(A[k] + B[k + 1] - L2));
     } else if (u == Un) {
-      bb = ex2_approx((float)(a + (double)py2[r] - L2));
+      bb = ex2_approx(a + py2[r] + (float)(A[k] - L2));
     }
   }
   gb[r] = bb;
@@ -235,40 +279,50 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
     sc[r * ntile + tl] = (rowinfo[r] >= 0) ? gs * (bb + yb) * expf(mt[r * ntile + tl] - l) : 0.f;
 }
 
-// d_enc[n,t,:] = sum_s dpre[n,t,s,:];  d_dec[n,u,:] = sum_{t: p_t <= u < p_t+S} dpre[n,t,u-p_t,:]
-// (frames covering u form a contiguous range since p is monotone; summed in t order).
-__global__ void denc_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd, int N, int T,
-                            int S, int J, float* __restrict__ d_enc) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)N * T * J) return;
-  const int j = (int)(i % J);
-  const long long nt = i / J;
+// d_enc[n,t,:] = sum_s dpre[n,t,s,:]: one CTA per frame, float4 over j.
+__global__ void __launch_bounds__(128) denc_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd,
+                                                   int T, int S, int J, float* __restrict__ d_enc) {
+  const long long nt = blockIdx.x;
   const int t = (int)(nt % T), n = (int)(nt / T);
-  float acc = 0.f;
-  if (t < utt_T(bnd, n))
-    for (int s = 0; s < S; ++s) acc += dpre[(nt * S + s) * J + j];
-  d_enc[i] = acc;
+  const bool valid = t < utt_T(bnd, n);
+  const int J4 = J / 4;
+  const float4* src = reinterpret_cast<const float4*>(dpre + (size_t)nt * S * J);
+  float4* dst = reinterpret_cast<float4*>(d_enc + (size_t)nt * J);
+  for (int j = threadIdx.x; j < J4; j += blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid)
+      for (int s = 0; s < S; ++s) {
+        const float4 v = src[(size_t)s * J4 + j];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    dst[j] = acc;
+  }
 }
 
-__global__ void ddec_kernel(const float* __restrict__ dpre, const int32_t* __restrict__ ranges,
-                            const int64_t* __restrict__ bnd, int N, int T, int U, int S, int J,
-                            float* __restrict__ d_dec) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)N * (U + 1) * J) return;
-  const int j = (int)(i % J);
-  const long long nu = i / J;
+// d_dec[n,u,:] = sum_{t in [lo(u), hi(u))} dpre[n,t,u-p_t,:], summed in t order (deterministic).
+__global__ void __launch_bounds__(128) ddec_kernel(const float* __restrict__ dpre, const int32_t* __restrict__ ranges,
+                                                   const int2* __restrict__ urange, const int64_t* __restrict__ bnd,
+                                                   int T, int U, int S, int J, float* __restrict__ d_dec) {
+  const long long nu = blockIdx.x;
   const int u = (int)(nu % (U + 1)), n = (int)(nu / (U + 1));
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  float acc = 0.f;
+  int lo = 0, hi = 0;
   if (u <= Un && (long long)Un <= (long long)Tn * (S - 1)) {
-    const int32_t* p = ranges + (size_t)n * T;
-    // first t with p_t + S - 1 >= u
-    int lo = 0, hi = Tn;
-    while (lo < hi) { int m = (lo + hi) >> 1; if (p[m] + S - 1 >= u) hi = m; else lo = m + 1; }
-    for (int t = lo; t < Tn && p[t] <= u; ++t)
-      acc += dpre[(((size_t)n * T + t) * S + (u - p[t])) * J + j];
+    const int2 r = urange[nu];
+    lo = r.x;
+    hi = r.y;
   }
-  d_dec[i] = acc;
+  const int J4 = J / 4;
+  const int32_t* p = ranges + (size_t)n * T;
+  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
+  for (int j = threadIdx.x; j < J4; j += blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = lo; t < hi; ++t) {
+      const float4 v = reinterpret_cast<const float4*>(dpre + (((size_t)n * T + t) * S + (u - p[t])) * J)[j];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    dst[j] = acc;
+  }
 }
 
 __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, long long M,
@@ -299,30 +353,26 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   const long long R = d.rows();
   const int nt = d.ntile();
   RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S,
-                                                               w.rowinfo));
+                                                               w.rowinfo, w.urange));
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
-    size_t sm = pruned_recursion_smem(d);
-    cudaFuncSetAttribute(pruned_alpha_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(pruned_beta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    RNNT_LAUNCH(KID_PALPHA, st, pruned_alpha_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.ap, w.Lp, loss, status));
-    RNNT_LAUNCH(KID_PBETA, st, pruned_beta_kernel<<<d.N, 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, w.bp));
+    const size_t sm = pruned_recursion_smem(d);
+    cudaFuncSetAttribute(pruned_fb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    RNNT_LAUNCH(KID_PALPHA, st, pruned_fb_kernel<<<dim3(d.N, 2), 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, d.K(),
+                                                                              w.ap, w.bp, w.Aps, w.Bps, w.Lp, loss,
+                                                                              status));
   }
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
-      w.px2, w.py2, w.ap, w.bp, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
-      w.gl, w.sc));
+      w.px2, w.py2, w.ap, w.bp, w.Aps, w.Bps, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, d.K(), nt,
+      gs, w.gb, w.gl, w.sc));
   GradSrc g{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, R, d.V, d.VP(), nt, gs};
   if (d_enc || d_dec) {
     if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
-    if (d_enc) {
-      long long n = (long long)d.N * d.T * d.J;
-      RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, bnd, d.N, d.T, d.S, d.J, d_enc));
-    }
-    if (d_dec) {
-      long long n = (long long)d.N * d.U1() * d.J;
-      RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J,
-                                                               d_dec));
-    }
+    if (d_enc)
+      RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((long long)d.N * d.T), 128, 0, st>>>(w.dpre, bnd, d.T, d.S, d.J, d_enc));
+    if (d_dec)
+      RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(w.dpre, ranges, w.urange, bnd, d.T,
+                                                                                          d.U, d.S, d.J, d_dec));
   }
   {
     if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;

@@ -10,16 +10,22 @@ namespace rnnt {
 struct Dims {
   int N, T, U, V, J, S;
   int U1() const { return U + 1; }
-  // Columns per lane of the wavefront warp (lattice.cu) and the skewed row pitch LU = 32 R, so
-  // every lane owns whole columns of every row (no partial lanes, no masks).
+  // Wavefront geometry of the simple lattice (lattice.cu): W strips (one warp each, on distinct
+  // SM sub-partitions) of 32 lanes x R columns; the skewed row pitch is LU = 32 R W, so every lane
+  // owns whole columns of every row (no partial lanes, no masks).  0 = unsupported (U+1 > 1024).
   int lat_R() const {
-    const int need = (U + 1 + 31) / 32;
-    const int Rs[9] = {1, 2, 4, 6, 8, 12, 16, 24, 32};
-    for (int r : Rs)
-      if (r >= need) return r;
-    return 0;   // unsupported (U + 1 > 1024)
+    const int need = (U + 1 + 31) / 32;   // columns per lane if one warp held the row
+    if (need <= 2) return need;
+    if (need <= 8) return 2;
+    if (need <= 16) return 4;
+    if (need <= 32) return 8;
+    return 0;
   }
-  int LU() const { return 32 * lat_R(); }
+  int lat_W() const {
+    const int r = lat_R();
+    return r ? ((U + 1 + 32 * r - 1) / (32 * r)) : 0;
+  }
+  int LU() const { return 32 * lat_R() * lat_W(); }
   int K() const { return T + U; }                       // number of anti-diagonals
   long long rows() const { return (long long)N * T * S; }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
@@ -36,22 +42,25 @@ struct SimpleWS {
   float* rS;      // (N,K+1,LU) skewed 1/sum_v exp(am-m_am+lm-m_lm)
   float* alpha;   // (N,K+1,LU) skewed alpha-hat = alpha*log2e - A_k (fp32, rebased)
   float* beta;    // (N,K+1,LU) skewed beta-hat  = beta*log2e - B_k
-  double* Ash;    // (N,K+1)    A_k per diagonal (fp64)
-  double* Bsh;    // (N,K+1)    B_k per diagonal
+  double* Ash;    // (N,K+1,W)  A_k per diagonal and strip (fp64)
+  double* Bsh;    // (N,K+1,W)  B_k per diagonal and strip
   double* Ltot;   // (N)        L_tot (natural log)
   float* Gt;      // (N,T,U+1)  (y'+empty') / S(t,u)   (t-major)
 };
 
 struct PrunedWS {
   int32_t* rowinfo;  // (R) label y_{u+1} (V if u==U_n), -1 for masked/padded rows
+  int2* urange;      // (N,U+1) frames [lo,hi) whose band covers token position u
   float* bias;       // (VP) fp32 copy of b_out, zero padded
   uint16_t* Pt;      // (R,VP) bf16 exp(z - m_tile), pitch VP
   float* mt;         // (R,ntile) tile maxima of z
   float* lse;        // (R) log-sum-exp of z
   float* px2;        // (R) y_p * log2e (band arcs)
   float* py2;        // (R) empty_p * log2e
-  double* ap;        // (R) pruned alpha (log2)
-  double* bp;        // (R) pruned beta (log2)
+  float* ap;         // (R) pruned alpha-hat (log2, rebased per anti-diagonal)
+  float* bp;         // (R) pruned beta-hat
+  double* Aps;       // (N,K+1) pruned alpha shift per anti-diagonal
+  double* Bps;       // (N,K+1) pruned beta shift
   double* Lp;        // (N) L_pruned
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
@@ -94,21 +103,24 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.rS = (float*)take(N * K1 * LU * 4);
   s.alpha = (float*)take(N * K1 * LU * 4);
   s.beta = (float*)take(N * K1 * LU * 4);
-  s.Ash = (double*)take(N * K1 * 8);
-  s.Bsh = (double*)take(N * K1 * 8);
+  s.Ash = (double*)take(N * K1 * (size_t)d.lat_W() * 8);
+  s.Bsh = (double*)take(N * K1 * (size_t)d.lat_W() * 8);
   s.Ltot = (double*)take(N * 8);
   s.Gt = (float*)take(N * T * U1 * 4);
   PrunedWS p;
   p.splits = dw_splits(d);
   p.rowinfo = (int32_t*)take(R * 4);
+  p.urange = (int2*)take(N * U1 * 8);
   p.bias = (float*)take(VP * 4);
   p.Pt = (uint16_t*)take(R * VP * 2);
   p.mt = (float*)take(R * NT * 4);
   p.lse = (float*)take(R * 4);
   p.px2 = (float*)take(R * 4);
   p.py2 = (float*)take(R * 4);
-  p.ap = (double*)take(R * 8);
-  p.bp = (double*)take(R * 8);
+  p.ap = (float*)take(R * 4);
+  p.bp = (float*)take(R * 4);
+  p.Aps = (double*)take(N * K1 * 8);
+  p.Bps = (double*)take(N * K1 * 8);
   p.Lp = (double*)take(N * 8);
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);

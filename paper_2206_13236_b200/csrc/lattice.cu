@@ -13,8 +13,8 @@
 // from it (beta = 0 there).
 //
 // Precision (D9): the state is fp32 REBASED per diagonal, alpha-hat_k = alpha_k - A_k, with
-// A_k = max_u alpha_{k-2} (the max of the diagonal two steps back, from one CREDUX.MAX per step, so
-// it is off the critical path) accumulated in fp64; |alpha-hat| stays within a two-step drift of 0
+// A_k = max_u alpha_{k-2} rounded to an integer (the max of the diagonal two steps back, from one
+// CREDUX.MAX per step, off the critical path), so the shifts accumulate exactly in fp32; |alpha-hat| stays within a two-step drift of 0
 // where the mass is, so the fp32 rounding is ~1e-7 relative per step.  The occupancies are then
 // self-normalised per anti-diagonal (every path leaves every diagonal k < K_n exactly once, so the
 // outflow of a diagonal sums to 1), which removes the error common to a diagonal.
@@ -45,7 +45,7 @@ template <int R>
 constexpr int CH = R <= 2 ? 16 : (R == 4 ? 8 : 4);
 struct Xchg {            // boundary values between neighbouring strips, per inbox warp
   float v[MAXW][NX][16];
-  double s[MAXW][NX][16];
+  float s[MAXW][NX][16];
 };
 template <int R>
 inline size_t smem_bytes(int W) {
@@ -131,7 +131,7 @@ struct Wavefront {
   static constexpr size_t STAGE = (size_t)2 * C * LU;
 
   float a[R];
-  double S = 0.0;                   // this strip's shift of the current diagonal (fp64)
+  float S = 0.f;                    // this strip's shift of the current diagonal (an integer, exact in fp32)
   float Mm2 = 0.f, Mm1 = 0.f;       // strip max of diagonals i-2, i-1 (relative to their shifts)
   float cprev = 0.f;                // rebasing increment of diagonal i-1
   int lane, w;
@@ -139,15 +139,15 @@ struct Wavefront {
 
   // Step i of the chunk: arcs at `rx`, boundary inbox/outbox slot `xs`, outputs at `orow` (row
   // pointer of this lane's columns) and `oshift`.
-  __device__ __forceinline__ void step(const float* rx, int i, const float* xv_in, const double* xs_in, float* xv_out,
-                                       double* xs_out, float* orow, double* oshift) {
+  __device__ __forceinline__ void step(const float* rx, int i, const float* xv_in, const float* xs_in, float* xv_out,
+                                       float* xs_out, float* orow, float* oshift) {
     float px[R], py[R];
     lds_row<R>(rx, px);
     lds_row<R>(rx + (size_t)C * LU, py);
     float xin = kNegBig;
-    if (has_in && lane == (FWD ? 0 : 31)) xin = *xv_in + (float)(*xs_in - S);
-    // A_i = A_{i-2} + M_{i-2}; a strip with no live cell two diagonals back keeps A_i = A_{i-1}
-    const float ci = (i >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
+    if (has_in && lane == (FWD ? 0 : 31)) xin = *xv_in + (*xs_in - S);   // shifts are integers: exact
+    // A_i = round(A_{i-2} + M_{i-2}); a strip with no live cell two diagonals back keeps A_i = A_{i-1}
+    const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
     float nw[R];
     if constexpr (FWD) {
       float h[R], v[R];
@@ -171,7 +171,7 @@ struct Wavefront {
 #pragma unroll
     for (int q = 0; q < R; ++q) { a[q] = nw[q]; mx = fmaxf(mx, nw[q]); }
     stg_row<R>(orow, a);
-    S += (double)ci;
+    S += ci;
     if (lane == 0) *oshift = S;
     const float Mi = warp_max_uniform(mx);
     Mm2 = Mm1;
@@ -180,7 +180,7 @@ struct Wavefront {
   }
 
   __device__ __forceinline__ void run(const float* ring, uint64_t* full, uint64_t* empty, uint64_t* xbar,
-                                      lat::Xchg* xc, int w_, int Wn, int Kn, int Un, float* out, double* shift,
+                                      lat::Xchg* xc, int w_, int Wn, int Kn, int Un, float* out, float* shift,
                                       double* Ltot_n, float* loss_n, int32_t* status, int n) {
     using namespace lat;
     lane = threadIdx.x & 31;
@@ -193,7 +193,7 @@ struct Wavefront {
 #pragma unroll
     for (int q = 0; q < R; ++q) a[q] = (u0 + q == start_u) ? 0.f : kNegBig;
     stg_row<R>(out + (size_t)(FWD ? 0 : Kn) * LU + u0, a);
-    if (lane == 0) shift[(size_t)(FWD ? 0 : Kn) * W + w] = 0.0;
+    if (lane == 0) shift[(size_t)(FWD ? 0 : Kn) * W + w] = 0.f;
 
     constexpr int DR = FWD ? 1 : -1;     // output row direction
     int stage = 0, done = 0;
@@ -205,12 +205,12 @@ struct Wavefront {
       const float* rb = ring + stage * STAGE + u0;
       const int slot = c % NX;
       const float* xvi = &xc->v[inbox][slot][0];
-      const double* xsi = &xc->s[inbox][slot][0];
+      const float* xsi = &xc->s[inbox][slot][0];
       float* xvo = &xc->v[outbox < 0 ? 0 : (outbox >= MAXW ? MAXW - 1 : outbox)][slot][0];
-      double* xso = &xc->s[outbox < 0 ? 0 : (outbox >= MAXW ? MAXW - 1 : outbox)][slot][0];
+      float* xso = &xc->s[outbox < 0 ? 0 : (outbox >= MAXW ? MAXW - 1 : outbox)][slot][0];
       const int orow0 = FWD ? done + 1 : Kn - done - 1;
       float* ob = out + (size_t)orow0 * LU + u0;
-      double* osb = shift + (size_t)orow0 * W + w;
+      float* osb = shift + (size_t)orow0 * W + w;
       if (rows == C) {
 #pragma unroll
         for (int j = 0; j < C; ++j)
@@ -233,7 +233,7 @@ struct Wavefront {
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (u0 + q == Un) {
-          const double L = ((double)a[q] + S) * RNNT_LN2;
+          const double L = ((double)a[q] + (double)S) * RNNT_LN2;
           *Ltot_n = L;
           *loss_n = (float)(-L);
           if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
@@ -247,7 +247,7 @@ struct Wavefront {
 template <int R, int W>
 __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const int64_t* __restrict__ bnd, int K,
-    float* __restrict__ ahat, float* __restrict__ bhat, double* __restrict__ Ash, double* __restrict__ Bsh,
+    float* __restrict__ ahat, float* __restrict__ bhat, float* __restrict__ Ash, float* __restrict__ Bsh,
     double* __restrict__ Ltot, float* __restrict__ loss, int32_t* __restrict__ status) {
   using namespace lat;
   constexpr int C = CH<R>, LU = 32 * R * W;
@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 // normalised occupancies and G~ = (y'+empty')/S(t,u), written t-major through a 32x32 smem transpose.
 __global__ void __launch_bounds__(256) combine_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const float* __restrict__ rS,
-    const float* __restrict__ ahat, const float* __restrict__ bhat, const double* __restrict__ Ash,
-    const double* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
+    const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
+    const float* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
     int U, int LU, int K, int W, int SW, float* __restrict__ px_grad, float* __restrict__ py_grad,
     float* __restrict__ Gt) {
   __shared__ float sy[32][33], sb[32][33], sg[32][33];
@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(256) combine_kernel(
     float rz = 0.f;
     if (finite && k < Kn) {
       if (lane < W) {
-        const double A = Ash[sbase + (size_t)k * W + lane];
-        s_ob[kr][lane] = (float)(A + Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
-        s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
+        const double A = (double)Ash[sbase + (size_t)k * W + lane];
+        s_ob[kr][lane] = (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
+        s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
       }
       __syncwarp();
       const float* Ar = ahat + base + (size_t)k * LU;

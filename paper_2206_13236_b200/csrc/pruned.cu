@@ -123,17 +123,19 @@ __device__ __forceinline__ float plae2(float a, float b, float c) {
   return (m - c) + lg2_approx(1.0f + ex2_approx(-fabsf(a - b)));
 }
 
-__global__ void __launch_bounds__(128) pruned_fb_kernel(
+__global__ void __launch_bounds__(256) pruned_fb_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const int32_t* __restrict__ ranges,
     const int64_t* __restrict__ bnd, int T, int S, int K, float* __restrict__ ap, float* __restrict__ bp,
-    double* __restrict__ Aps, double* __restrict__ Bps, double* __restrict__ Lp, float* __restrict__ loss,
+    float* __restrict__ Aps, float* __restrict__ Bps, double* __restrict__ Lp, float* __restrict__ loss,
     int32_t* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  // smem: p_t (T), frame-at-diagonal F[d] (T+U+1: F[t + p_t] = t, else -1), arcs (T*S each)
   int* sp = reinterpret_cast<int*>(smem_raw);
-  float* sx = reinterpret_cast<float*>(sp + T);
+  int* sF = sp + T;
+  float* sx = reinterpret_cast<float*>(sF + K + 1);
   float* sy = sx + (size_t)T * S;
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   if (!feasible) {
@@ -145,91 +147,117 @@ __global__ void __launch_bounds__(128) pruned_fb_kernel(
     return;
   }
   const size_t rbase = (size_t)n * T * S;
-  for (int i = threadIdx.x; i < Tn; i += blockDim.x) sp[i] = ranges[(size_t)n * T + i];
-  for (int i = threadIdx.x; i < Tn * S; i += blockDim.x) { sx[i] = px2[rbase + i]; sy[i] = py2[rbase + i]; }
+  const int dlast = (Tn - 1) + ranges[(size_t)n * T + Tn - 1];   // d_{T-1}
+  for (int i = threadIdx.x; i <= dlast; i += blockDim.x) sF[i] = -1;
+  __syncthreads();
+  for (int i = threadIdx.x; i < Tn; i += blockDim.x) {
+    const int p = ranges[(size_t)n * T + i];
+    sp[i] = p;
+    sF[i + p] = i;
+  }
+  {
+    const int m = Tn * S;
+    for (int i0 = threadIdx.x; i0 < m; i0 += 4 * blockDim.x) {
+      float x[4], y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q * blockDim.x;
+        x[q] = i < m ? px2[rbase + i] : 0.f;
+        y[q] = i < m ? py2[rbase + i] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q * blockDim.x;
+        if (i < m) { sx[i] = x[q]; sy[i] = y[q]; }
+      }
+    }
+  }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int s = threadIdx.x;
-  const bool lane_on = s < S;
-  const int kend = (Tn - 1) + sp[Tn - 1] + S - 1;   // last anti-diagonal holding a band cell
-  double* shift = (fwd ? Aps : Bps) + (size_t)n * (K + 1);
+  const int kend = dlast + S - 1;                    // last anti-diagonal holding a band cell
+  float* shift = (fwd ? Aps : Bps) + (size_t)n * (K + 1);
   float* outv = (fwd ? ap : bp) + rbase;
-
-  double Sh = 0.0;
+  const float NB = kNegBig;
+  float Sh = 0.f;   // shift of the current diagonal: an integer, exact in fp32
   float Mm2 = 0.f, Mm1 = 0.f, cprev = 0.f;
+
+  // Table-driven: at diagonal k lane s holds frame t = F[k - s] (or none).  Everything indexed by
+  // (k, s) is independent of the values, so the compiler can hoist it off the LogAdd chain.
   if (fwd) {
-    float h_out = kNegBig, v_out = kNegBig;
-    int ts = 0;                                          // next frame of this lane
-    int dnext = lane_on ? sp[0] + s : 0x7fffffff;        // its anti-diagonal d_t + s
-    int pprev = 0;
+    float h_out = NB, v_out = NB;
+    int k_loss = -1;
+    float hl = NB;
+#pragma unroll 4
     for (int k = 0; k <= kend; ++k) {
-      // A_k = A_{k-2} + M_{k-2}; a diagonal with no live cell (max = kNegBig) keeps A_k = A_{k-1}
-      const float ci = (k >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
-      const bool act = (dnext == k);
-      const int t = ts;
-      const int p = act ? sp[t] : 0;
-      const int src = (act && t > 0) ? s + p - pprev : s;
-      const float hin = __shfl_sync(0xffffffffu, h_out, src < 32 ? src : 31);
+      const int j = k - s;
+      const int t = (s < S && j >= 0 && j <= dlast) ? sF[j] : -1;
+      const bool act = t >= 0;
+      const int tt = act ? t : 0;
+      const int p = sp[tt];
+      const int src = (act && tt > 0) ? s + p - sp[tt - 1] : 32;
+      const float pxv = sx[tt * S + (s < S ? s : 0)], pyv = sy[tt * S + (s < S ? s : 0)];
+      // A_k = round(A_{k-2} + M_{k-2}); a diagonal with no live cell keeps A_k = A_{k-1}
+      const float ci = (k >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
+      const float hin = __shfl_sync(0xffffffffu, h_out, src < 32 ? src : 0);
       const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
-      float mx = kNegBig;
+      const float left = (src < S) ? hin : NB;
+      const float below = s > 0 ? vin : NB;
+      const int u = p + s;
+      float a = (tt == 0 && s == 0) ? -ci : plae2(left, below, ci);
+      if (u > Un) a = NB;                                  // masked slot (S > U_n + 1, D10)
+      float mx = NB;
       if (act) {
-        const float left = (t > 0 && src < S) ? hin : kNegBig;
-        const float below = s > 0 ? vin : kNegBig;
-        const int u = p + s;
-        float a = (t == 0 && s == 0) ? -ci : plae2(left, below, ci);
-        if (u > Un) a = kNegBig;                           // masked slot (S > U_n + 1, D10)
-        h_out = a + sy[t * S + s];
-        v_out = a + sx[t * S + s];
-        outv[(size_t)t * S + s] = a;
+        h_out = a + pyv;
+        v_out = a + pxv;
+        outv[tt * S + s] = a;
         mx = a;
-        if (t == Tn - 1 && u == Un) {
-          // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band)
-          const double L = ((double)h_out + Sh + (double)ci) * RNNT_LN2;
-          Lp[n] = L;
-          loss[n] = (float)(-L);
-          if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
-        }
-        pprev = p;
-        ts = t + 1;
-        dnext = (ts < Tn) ? ts + sp[ts] + s : 0x7fffffff;
+        if (tt == Tn - 1 && u == Un) { k_loss = k; hl = h_out; }
       }
-      Sh += (double)ci;
+      Sh += ci;
       if (s == 0) shift[k] = Sh;
+      if (k == k_loss) {
+        // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band), in the frame A_k
+        const double L = ((double)hl + (double)Sh) * RNNT_LN2;
+        Lp[n] = L;
+        loss[n] = (float)(-L);
+        if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+      }
       const float Mk = warp_max_uniform_p(mx);
       Mm2 = Mm1;
       Mm1 = Mk;
       cprev = ci;
     }
   } else {
-    float b_out = kNegBig;
-    int ts = Tn - 1;                                       // next frame of this lane (descending)
-    int dnext = lane_on ? (Tn - 1) + sp[Tn - 1] + s : -1;
+    float b_out = NB;
+#pragma unroll 4
     for (int k = kend; k >= 0; --k) {
       const int i = kend - k;
-      const float ci = (i >= 2 && Mm2 > -1e29f) ? Mm2 - cprev : 0.f;
-      const bool act = (dnext == k);
-      const int t = ts;
-      const int p = act ? sp[t] : 0;
-      const int src = (act && t < Tn - 1) ? s - (sp[t + 1] - p) : s;   // slot of (t+1, u) in frame t+1
+      const int j = k - s;
+      const int t = (s < S && j >= 0 && j <= dlast) ? sF[j] : -1;
+      const bool act = t >= 0;
+      const int tt = act ? t : 0;
+      const int p = sp[tt];
+      const bool last = (tt == Tn - 1);
+      const int src = last ? -1 : s - (sp[tt + 1 < Tn ? tt + 1 : tt] - p);   // slot of (t+1, u) in frame t+1
+      const float pxv = sx[tt * S + (s < S ? s : 0)], pyv = sy[tt * S + (s < S ? s : 0)];
+      const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
       const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : 0);
       const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
-      float mx = kNegBig;
+      const int u = p + s;
+      float right;
+      if (last) right = (u == Un) ? pyv : NB;              // terminal blank (virtual end, beta = 0)
+      else right = (src >= 0 && src < S) ? rin + pyv : NB;
+      const float up = (u < Un && s + 1 < S) ? uin + pxv : NB;
+      float b = plae2(right, up, ci);
+      if (u > Un) b = NB;
+      float mx = NB;
       if (act) {
-        const int u = p + s;
-        const float px = sx[t * S + s], py = sy[t * S + s];
-        float right;
-        if (t == Tn - 1) right = (u == Un) ? py : kNegBig;          // terminal blank (virtual end, beta = 0)
-        else right = (src >= 0 && src < S) ? rin + py : kNegBig;
-        const float up = (u < Un && s + 1 < S) ? uin + px : kNegBig;
-        float b = plae2(right, up, ci);
-        if (u > Un) b = kNegBig;
         b_out = b;
-        outv[(size_t)t * S + s] = b;
+        outv[tt * S + s] = b;
         mx = b;
-        ts = t - 1;
-        dnext = (ts >= 0) ? ts + sp[ts] + s : -1;
       }
-      Sh += (double)ci;
+      Sh += ci;
       if (s == 0) shift[k] = Sh;
       const float Mk = warp_max_uniform_p(mx);
       Mm2 = Mm1;
@@ -243,7 +271,7 @@ __global__ void __launch_bounds__(128) pruned_fb_kernel(
 // the per-(row, tile) softmax scale of the logit gradient sc = gs (g_b + g_l) exp(m_tile - lse).
 __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float* __restrict__ py2,
                                       const float* __restrict__ ap, const float* __restrict__ bp,
-                                      const double* __restrict__ Aps, const double* __restrict__ Bps,
+                                      const float* __restrict__ Aps, const float* __restrict__ Bps,
                                       const double* __restrict__ Lp, const int32_t* __restrict__ ranges,
                                       const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
@@ -260,16 +288,16 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   if (rowinfo[r] >= 0 && isfinite(L2)) {
     const int p = ranges[(size_t)n * T + t];
     const int u = p + s, k = t + u;
-    const double* A = Aps + (size_t)n * (K + 1);
-    const double* B = Bps + (size_t)n * (K + 1);
+    const float* A = Aps + (size_t)n * (K + 1);
+    const float* B = Bps + (size_t)n * (K + 1);
     const float a = ap[r];
     if (u < Un && s + 1 < S)
-      yb = ex2_approx(a + px2[r] + bp[r + 1] + (float)(A[k] + B[k + 1] - L2));
+      yb = ex2_approx(a + px2[r] + bp[r + 1] + (float)((double)A[k] + (double)B[k + 1] - L2));
     if (t < Tn - 1) {
       const int s2 = u - ranges[(size_t)n * T + t + 1];
-      if (s2 >= 0 && s2 < S) bb = ex2_approx(a + py2[r] + bp[r + S + (s2 - s)] + (float)(A[k] + B[k + 1] - L2));
+      if (s2 >= 0 && s2 < S) bb = ex2_approx(a + py2[r] + bp[r + S + (s2 - s)] + (float)((double)A[k] + (double)B[k + 1] - L2));
     } else if (u == Un) {
-      bb = ex2_approx(a + py2[r] + (float)(A[k] - L2));
+      bb = ex2_approx(a + py2[r] + (float)((double)A[k] - L2));
     }
   }
   gb[r] = bb;
@@ -343,7 +371,7 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
   return cudaGetLastError();
 }
 
-size_t pruned_recursion_smem(const Dims& d) { return (size_t)d.T * 4 + (size_t)d.T * d.S * 8; }
+size_t pruned_recursion_smem(const Dims& d) { return (size_t)d.T * 4 + (size_t)(d.K() + 1) * 4 + (size_t)d.T * d.S * 8; }
 
 cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                const uint16_t* b, const int64_t* sym, const int32_t* ranges,
@@ -358,7 +386,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   {
     const size_t sm = pruned_recursion_smem(d);
     cudaFuncSetAttribute(pruned_fb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    RNNT_LAUNCH(KID_PALPHA, st, pruned_fb_kernel<<<dim3(d.N, 2), 128, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, d.K(),
+    RNNT_LAUNCH(KID_PALPHA, st, pruned_fb_kernel<<<dim3(d.N, 2), 256, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, d.K(),
                                                                               w.ap, w.bp, w.Aps, w.Bps, w.Lp, loss,
                                                                               status));
   }

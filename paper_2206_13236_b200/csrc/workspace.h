@@ -42,8 +42,8 @@ struct SimpleWS {
   float* rS;      // (N,K+1,LU) skewed 1/sum_v exp(am-m_am+lm-m_lm)
   float* alpha;   // (N,K+1,LU) skewed alpha-hat = alpha*log2e - A_k (fp32, rebased)
   float* beta;    // (N,K+1,LU) skewed beta-hat  = beta*log2e - B_k
-  double* Ash;    // (N,K+1,W)  A_k per diagonal and strip (fp64)
-  double* Bsh;    // (N,K+1,W)  B_k per diagonal and strip
+  float* Ash;     // (N,K+1,W)  A_k per diagonal and strip (integer-valued)
+  float* Bsh;     // (N,K+1,W)  B_k per diagonal and strip
   double* Ltot;   // (N)        L_tot (natural log)
   float* Gt;      // (N,T,U+1)  (y'+empty') / S(t,u)   (t-major)
 };
@@ -59,8 +59,8 @@ struct PrunedWS {
   float* py2;        // (R) empty_p * log2e
   float* ap;         // (R) pruned alpha-hat (log2, rebased per anti-diagonal)
   float* bp;         // (R) pruned beta-hat
-  double* Aps;       // (N,K+1) pruned alpha shift per anti-diagonal
-  double* Bps;       // (N,K+1) pruned beta shift
+  float* Aps;        // (N,K+1) pruned alpha shift per anti-diagonal (integer-valued)
+  float* Bps;        // (N,K+1) pruned beta shift
   double* Lp;        // (N) L_pruned
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
@@ -103,8 +103,8 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.rS = (float*)take(N * K1 * LU * 4);
   s.alpha = (float*)take(N * K1 * LU * 4);
   s.beta = (float*)take(N * K1 * LU * 4);
-  s.Ash = (double*)take(N * K1 * (size_t)d.lat_W() * 8);
-  s.Bsh = (double*)take(N * K1 * (size_t)d.lat_W() * 8);
+  s.Ash = (float*)take(N * K1 * (size_t)d.lat_W() * 4);
+  s.Bsh = (float*)take(N * K1 * (size_t)d.lat_W() * 4);
   s.Ltot = (double*)take(N * 8);
   s.Gt = (float*)take(N * T * U1 * 4);
   PrunedWS p;
@@ -119,8 +119,8 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.py2 = (float*)take(R * 4);
   p.ap = (float*)take(R * 4);
   p.bp = (float*)take(R * 4);
-  p.Aps = (double*)take(N * K1 * 8);
-  p.Bps = (double*)take(N * K1 * 8);
+  p.Aps = (float*)take(N * K1 * 4);
+  p.Bps = (float*)take(N * K1 * 4);
   p.Lp = (double*)take(N * 8);
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);

@@ -1,16 +1,17 @@
-// joiner_bwd.cu — K10 / K11: joiner backward on tcgen05 with the logit gradient formed in
-// the operand producer (function merging): nothing of size (R, V) is written in
-// the backward; P~ (bf16, from K8) is read and turned into
+// joiner_bwd.cu — K10 / K11: joiner backward on tcgen05 with the logit gradient formed inside the
+// GEMM operand tiles (function merging): nothing of size (R, V) is written in the
+// backward.  P~ (bf16 exp(z - m_tile), from K8) is brought into the swizzled shared-memory operand
+// tile by TMA, and the producer warps turn it IN PLACE into
 //     dz[r,v] = sc[r, v/128] * P~[r,v] - gs g_b[r] [v=0] - gs g_l[r] [v=y_r]      (bf16)
-// directly in the swizzled shared-memory operand tile.
+// (the element-wise transform preserves the SWIZZLE_128B layout: logical 16-B chunk c of tile row r
+// sits at physical chunk c ^ (r % 8)), then release the stage to the MMA issuer.
 //
-//   K10 joiner_dh:  dh[r, j] = sum_v dz[r,v] W[v,j]     A = dz (K-major, producer warps),
-//                   B = W (MN-major, TMA), epilogue dpre = dh (1 - h^2)  (d tanh)
-//   K11 joiner_dw:  dW[v, j] = sum_r dz[r,v] h[r,j]     A = dz^T (MN-major, producer warps),
-//                   B = h (MN-major, TMA), split-K over rows, fp32 partial tiles; the
-//                   producers also accumulate db = sum_r dz partials.
-// Warps 0-3: operand producers, then epilogue (TMEM lanes 32w..32w+31).
-// Warp 4: TMEM allocator, TMA issuer and single-thread MMA issuer.
+//   K10 joiner_dh:  dh[r, j] = sum_v dz[r,v] W[v,j]     A = dz (K-major), B = W (MN-major);
+//                   epilogue dpre = dh (1 - h^2)  (d tanh)
+//   K11 joiner_dw:  dW[v, j] = sum_r dz[r,v] h[r,j]     A = dz^T (MN-major), B = h (MN-major);
+//                   split-K over rows, fp32 partial tiles; the producers also sum db partials.
+// Warps 0-3: in-place producers, then epilogue (TMEM lanes 32w..32w+31).
+// Warp 4: TMEM allocator, TMA issuer (one lane) and MMA issuer (another lane).
 #include <algorithm>
 
 #include "common.cuh"
@@ -28,44 +29,40 @@ struct GradSrc {
   long long R;
   int V, VP, ntile;
   float gs;
-  // 8 consecutive dz values (v = vc..vc+7) of row r packed as bf16.
-  __device__ __forceinline__ uint4 chunk(long long r, int vc, float* fsum) const {
-    if (r >= R) return make_uint4(0, 0, 0, 0);
-    const int info = rowinfo[r];
-    if (info < 0 || vc >= V) return make_uint4(0, 0, 0, 0);
-    const uint4 pv = *reinterpret_cast<const uint4*>(Pt + (size_t)r * VP + vc);
-    const float s = sc[(size_t)r * ntile + (vc >> 7)];
-    const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
-    float g[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      g[2 * i] = s * __uint_as_float(w[i] << 16);
-      g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u);
-    }
-    if (vc == 0) g[0] -= gs * gb[r];
-    const int li = info - vc;
-    if ((unsigned)li < 8u) {
-      const float gl_ = gs * gl[r];
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j == li) g[j] -= gl_;
-    }
-    uint32_t o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
-      o[i] = *reinterpret_cast<uint32_t*>(&h2);
-      if (fsum) {
-        // db accumulates the bf16-rounded dz, the values the MMA consumes
-        fsum[2 * i] += __low2float(h2);
-        fsum[2 * i + 1] += __high2float(h2);
-      }
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-  }
 };
 
-// byte offset of 16-B chunk `c` (0..7) of 128-B row `r` in a SWIZZLE_128B atom stack
+// dz for the 8 logits v = vc..vc+7 of one row, from the packed bf16 P~ chunk `pv`, the row's
+// scale s, the picks gbs = gs g_b (v = 0) and gls = gs g_l (v = label `info`).  Returns the bf16
+// chunk and adds the bf16-rounded values (what the MMA consumes) to fsum when given.
+__device__ __forceinline__ uint4 dz_chunk(uint4 pv, float s, float gbs, float gls, int info, int vc, float* fsum) {
+  const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    g[2 * i] = s * __uint_as_float(w[i] << 16);
+    g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u);
+  }
+  if (vc == 0) g[0] -= gbs;
+  const int li = info - vc;
+  if ((unsigned)li < 8u) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j == li) g[j] -= gls;
+  }
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+    o[i] = *reinterpret_cast<uint32_t*>(&h2);
+    if (fsum) {
+      fsum[2 * i] += __low2float(h2);
+      fsum[2 * i + 1] += __high2float(h2);
+    }
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// byte offset of logical 16-B chunk `c` (0..7) of 128-B row `r` in a SWIZZLE_128B atom stack
 __device__ __forceinline__ uint32_t sw128(int r, int c) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
 }
@@ -73,7 +70,7 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 // ======================================================================= K10
 namespace jdh {
 constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 512, STAGES = 2;
-constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major
+constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
 constexpr int B_BYTES = MAXN * BK * 2;         // 64 KB, MN-major (8 boxes of 64 j x 64 v)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
@@ -88,11 +85,13 @@ struct JoinerDhParams {
 };
 
 __global__ void __launch_bounds__(jdh::THREADS, 1)
-    joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmW, JoinerDhParams p) {
+    joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
+                        JoinerDhParams p) {
   using namespace jdh;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
@@ -118,9 +117,14 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
     return;
   }
   if (warp == 4 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 4 + 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&loaded[s], 1);
+      tc::mbar_init(&full[s], 4);
+      tc::mbar_init(&empty[s], 1);
+    }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
+    tc::tma_prefetch(&tmP);
     tc::tma_prefetch(&tmW);
   }
   if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
@@ -130,19 +134,27 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   const uint32_t tbase = *tmem_slot;
 
   if (warp < 4) {
-    // ---- producers: A = dz[m0.., kb*64..] (K-major)
+    // ---- producers: thread = tile row; transform the 8 chunks of its row in place
+    const int rl = threadIdx.x;
+    const long long r = m0 + rl;
+    const int info = (r < p.g.R) ? p.g.rowinfo[r] : -1;
+    const bool live = info >= 0;
+    const float gbs = live ? p.g.gs * p.g.gb[r] : 0.f;
+    const float gls = live ? p.g.gs * p.g.gl[r] : 0.f;
+    const float* scr = p.g.sc + (size_t)(live ? r : 0) * p.g.ntile;
     int stage = 0;
     uint32_t ph = 0;
-    const int c = threadIdx.x & 7;
-    const int rbase = threadIdx.x >> 3;   // 0..15
+    float s_cur = live ? scr[0] : 0.f;
     for (int kb = 0; kb < p.nkb; ++kb) {
-      tc::mbar_wait(&empty[stage], ph ^ 1);
+      const int v0 = kb * BK;
+      const float s = (v0 >> 7) == 0 ? s_cur : (live ? scr[v0 >> 7] : 0.f);
+      tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
-#pragma unroll 4
-      for (int i = 0; i < 8; ++i) {
-        const int rl = rbase + 16 * i;
-        const uint4 v = p.g.chunk(m0 + rl, kb * BK + c * 8, nullptr);
-        *reinterpret_cast<uint4*>(sa + sw128(rl, c)) = v;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4* q = reinterpret_cast<uint4*>(sa + sw128(rl, c));
+        const uint4 pv = *q;
+        *q = live ? dz_chunk(pv, s, gbs, gls, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -152,8 +164,6 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
     // ---- epilogue: dpre = dh * (1 - h^2)
     tc::mbar_wait(tfull, 0);
     tc::fence_after_sync();
-    const long long r = m0 + threadIdx.x;
-    const bool valid = r < p.g.R && p.g.rowinfo[r] >= 0;
     const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
     for (int c0 = 0; c0 < nj; c0 += 32) {
       float acc[32];
@@ -165,14 +175,14 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (q >= nq) break;
-          const uint4 hv = valid ? hp[q] : make_uint4(0, 0, 0, 0);
+          const uint4 hv = live ? hp[q] : make_uint4(0, 0, 0, 0);
           const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
           float out[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float ha = __uint_as_float(hw[i] << 16), hb = __uint_as_float(hw[i] & 0xffff0000u);
-            out[2 * i] = valid ? acc[8 * q + 2 * i] * (1.f - ha * ha) : 0.f;
-            out[2 * i + 1] = valid ? acc[8 * q + 2 * i + 1] * (1.f - hb * hb) : 0.f;
+            out[2 * i] = live ? acc[8 * q + 2 * i] * (1.f - ha * ha) : 0.f;
+            out[2 * i + 1] = live ? acc[8 * q + 2 * i + 1] * (1.f - hb * hb) : 0.f;
           }
           reinterpret_cast<float4*>(o)[2 * q] = make_float4(out[0], out[1], out[2], out[3]);
           reinterpret_cast<float4*>(o)[2 * q + 1] = make_float4(out[4], out[5], out[6], out[7]);
@@ -180,37 +190,36 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       }
     }
   } else if (lane == 0) {
-    // ---- warp 4: B = W[kb*64.., j0..] via TMA (MN-major boxes of 64 j x 64 v) + MMA issue
+    // ---- warp 4 lane 0: TMA for A = P~[m0.., kb*64..] and B = W[kb*64.., j0..]
+    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2;
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < p.nkb; ++kb) {
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+      tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
+      tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
+      for (int bx = 0; bx < nbox; ++bx)
+        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (lane == 1) {
+    // ---- warp 4 lane 1: MMA issuer
     constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
     int stage = 0;
     uint32_t ph = 0;
-    int stage_m = 0;
-    uint32_t ph_m = 0;
-    const uint32_t bbytes = (uint32_t)nbox * 64 * BK * 2;
-    // prologue: issue the first STAGES B loads
-    int kb_load = 0;
     for (int kb = 0; kb < p.nkb; ++kb) {
-      // keep the TMA one stage ahead of the MMA
-      while (kb_load < p.nkb && kb_load < kb + STAGES) {
-        tc::mbar_wait(&empty[stage], ph ^ 1);
-        uint8_t* sb = smem + stage * STAGE_BYTES + A_BYTES;
-        tc::mbar_arrive_expect_tx(&full[stage], bbytes);
-        for (int bx = 0; bx < nbox; ++bx)
-          tc::tma_load_2d(sb + bx * (64 * BK * 2), &tmW, &full[stage], j0 + bx * 64, kb_load * BK);
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        ++kb_load;
-      }
-      tc::mbar_wait(&full[stage_m], ph_m);
+      tc::mbar_wait(&full[stage], ph);
       tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(smem + stage_m * STAGE_BYTES), b = a + A_BYTES;
+      const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
       for (int ns = 0; ns < nsub; ++ns) {
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           tc::mma_bf16(tbase + ns * NSUB, tc::sdesc(a + 32 * k, 16, 1024),
                        tc::sdesc(b + ns * 4 * (64 * BK * 2) + 2048 * k, 64 * BK * 2, 1024), idesc, (kb | k) != 0);
       }
-      tc::mma_commit(&empty[stage_m]);
-      if (++stage_m == STAGES) { stage_m = 0; ph_m ^= 1; }
+      tc::mma_commit(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
     tc::mma_commit(tfull);
   }
@@ -222,10 +231,11 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
 // ======================================================================= K11
 namespace jdw {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 atom columns of 64 v x 64 rows)
-constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows)
+constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 TMA boxes of 64 v x 64 rows of P~)
+constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows of h)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4;
+constexpr int SCAL_BYTES = 2 * BK * 16;  // per-row scalars of two k-blocks (double buffer)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4 + SCAL_BYTES;
 constexpr int THREADS = 160;
 }  // namespace jdw
 
@@ -238,15 +248,18 @@ struct JoinerDwParams {
 };
 
 __global__ void __launch_bounds__(jdw::THREADS, 1)
-    joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmH, JoinerDwParams p) {
+    joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
+                        JoinerDwParams p) {
   using namespace jdw;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [8 row groups][128 v]
+  float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][128 v]
+  float4* scal = reinterpret_cast<float4*>(smem + STAGES * STAGE_BYTES + 256 + 128 * 16 * 4);  // [2][64]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
   const long long kb0 = (long long)split * p.kb_per_split;
@@ -255,11 +268,17 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
   const int V = p.g.V;
   const int nj = min(BN, p.J - j0);
   const int nbox = (nj + 63) / 64;
+  const int vtile = v0 >> 7;
 
   if (warp == 4 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 4 + 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&loaded[s], 1);
+      tc::mbar_init(&full[s], 4);
+      tc::mbar_init(&empty[s], 1);
+    }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
+    tc::tma_prefetch(&tmP);
     tc::tma_prefetch(&tmH);
   }
   if (warp == 4) tc::tmem_alloc(tmem_slot, 256);
@@ -269,22 +288,38 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
   const uint32_t tbase = *tmem_slot;
 
   if (warp < 4) {
-    // ---- producers: A = dz^T tile (v0..v0+127) x (64 rows), MN-major
-    int stage = 0;
-    uint32_t ph = 0;
+    // ---- producers: thread handles v chunk c (8 logits) of rows g8 + 8 i of each k-block
     const int c = threadIdx.x & 15;          // 8-v chunk 0..15
     const int g8 = threadIdx.x >> 4;         // row group 0..7
     float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool want_db = blockIdx.y == 0;
+    // per-row scalars {sc, gs g_b, gs g_l, info} of a k-block, gathered by threads 0..63
+    auto fetch = [&](int kb) -> float4 {
+      const long long r = (kb0 + kb) * BK + threadIdx.x;
+      if (threadIdx.x >= BK || r >= p.g.R) return make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+      const int info = p.g.rowinfo[r];
+      if (info < 0) return make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+      return make_float4(p.g.sc[(size_t)r * p.g.ntile + vtile], p.g.gs * p.g.gb[r], p.g.gs * p.g.gl[r],
+                         __int_as_float(info));
+    };
+    float4 nxt = nkb > 0 ? fetch(0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    int stage = 0;
+    uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(&empty[stage], ph ^ 1);
+      if (threadIdx.x < BK) scal[(kb & 1) * BK + threadIdx.x] = nxt;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (kb + 1 < nkb) nxt = fetch(kb + 1);
+      tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
-      const long long rb = (kb0 + kb) * BK;
 #pragma unroll 4
       for (int i = 0; i < 8; ++i) {
         const int rl = g8 + 8 * i;
-        const uint4 v = p.g.chunk(rb + rl, v0 + c * 8, want_db ? dsum : nullptr);
-        *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) = v;
+        const float4 sr = scal[(kb & 1) * BK + rl];
+        const int info = __float_as_int(sr.w);
+        uint4* q = reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
+        const uint4 pv = *q;
+        *q = info >= 0 ? dz_chunk(pv, sr.x, sr.y, sr.z, info, v0 + c * 8, want_db ? dsum : nullptr)
+                       : make_uint4(0, 0, 0, 0);
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -326,30 +361,36 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
-    int stage = 0, stage_m = 0;
-    uint32_t ph = 0, ph_m = 0;
-    const uint32_t bbytes = (uint32_t)nbox * 64 * BK * 2;
-    int kb_load = 0;
+    // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes) and B = h[rows, j0..] (nbox boxes)
+    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2;
+    int stage = 0;
+    uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      while (kb_load < nkb && kb_load < kb + STAGES) {
-        tc::mbar_wait(&empty[stage], ph ^ 1);
-        uint8_t* sb = smem + stage * STAGE_BYTES + A_BYTES;
-        tc::mbar_arrive_expect_tx(&full[stage], bbytes);
-        for (int bx = 0; bx < nbox; ++bx)
-          tc::tma_load_2d(sb + bx * (64 * BK * 2), &tmH, &full[stage], j0 + bx * 64, (int)((kb0 + kb_load) * BK));
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        ++kb_load;
-      }
-      tc::mbar_wait(&full[stage_m], ph_m);
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+      const int rrow = (int)((kb0 + kb) * BK);
+      tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
+      tc::tma_load_2d(sa, &tmP, &loaded[stage], v0, rrow);
+      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, &loaded[stage], v0 + 64, rrow);
+      for (int bx = 0; bx < nbox; ++bx)
+        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, &loaded[stage], j0 + bx * 64, rrow);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (lane == 1 && nkb > 0) {
+    // ---- warp 4 lane 1: MMA issuer
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait(&full[stage], ph);
       tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(smem + stage_m * STAGE_BYTES), b = a + A_BYTES;
+      const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
 #pragma unroll
       for (int k = 0; k < BK / 16; ++k)
         tc::mma_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024),
                      idesc, (kb | k) != 0);
-      tc::mma_commit(&empty[stage_m]);
-      if (++stage_m == STAGES) { stage_m = 0; ph_m ^= 1; }
+      tc::mma_commit(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
     tc::mma_commit(tfull);
   }
@@ -361,7 +402,8 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
 // ======================================================================= host
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
                              cudaStream_t st) {
-  CUtensorMap tw;
+  CUtensorMap tp, tw;
+  if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -370,13 +412,14 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   }
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, dpre};
   dim3 grid((unsigned)((d.rows() + jdh::BM - 1) / jdh::BM), (d.J + jdh::MAXN - 1) / jdh::MAXN);
-  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tw, p));
+  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, p));
   return cudaGetLastError();
 }
 
 cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
                              int splits, cudaStream_t st) {
-  CUtensorMap th;
+  CUtensorMap tp, th;
+  if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -387,7 +430,7 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   const long long per = (nkb + splits - 1) / splits;
   JoinerDwParams p{g, d.J, per, nkb, dWp, dbp};
   dim3 grid((d.V + jdw::BM - 1) / jdw::BM, (d.J + jdw::BN - 1) / jdw::BN, splits);
-  RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<<<grid, jdw::THREADS, jdw::SMEM_BYTES, st>>>(th, p));
+  RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<<<grid, jdw::THREADS, jdw::SMEM_BYTES, st>>>(tp, th, p));
   return cudaGetLastError();
 }
 

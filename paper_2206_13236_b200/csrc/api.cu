@@ -29,11 +29,11 @@ static thread_local int g_prof_id = 0;
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 static const char* const kNames[KID_COUNT] = {
-    "none", "validate", "rowmax_am", "rowmax_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
-    "lattice_combine", "simple_am_grad_gemm", "simple_am_picks", "simple_lm_grad_gemm", "simple_lm_picks",
+    "none", "validate", "exp_split_am", "exp_split_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
+    "lattice_combine", "simple_am_grad_gemm", "unused_am_picks", "simple_lm_grad_gemm", "unused_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",
-    "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad"};
+    "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums"};
 
 const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }
 
@@ -96,7 +96,7 @@ rnnt_status_t rnnt_profile_kernel(int32_t kernel_id, void* start_event, void* st
   return RNNT_OK;
 }
 
-const char* rnnt_version(void) { return "rnnt-b200 0.1 sm_100a (joiner_fwd: tcgen05; other contractions: simt-v0)"; }
+const char* rnnt_version(void) { return "rnnt-b200 0.2 sm_100a (all contractions tcgen05: simple bf16x3, joiner bf16)"; }
 
 static void* align_ws(void* ws) {
   uintptr_t p = reinterpret_cast<uintptr_t>(ws);

@@ -302,13 +302,15 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 
 // ------------------------------------------------------------------ K4 combine
 // Per block of 32 anti-diagonals: Z_k = sum_u (y'+empty') (should be 1), then the
-// normalised occupancies and G~ = (y'+empty')/S(t,u), written t-major through a 32x32 smem transpose.
+// normalised occupancies and G~ = (y'+empty')/S(t,u) (bf16 hi+lo), written t-major through a 32x32
+// smem transpose.
 __global__ void __launch_bounds__(256) combine_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
     const float* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
-    int U, int LU, int K, int W, int SW, float* __restrict__ px_grad, float* __restrict__ py_grad,
-    float* __restrict__ Gt) {
+    int U, int LU, int K, int W, int SW, int UP, float* __restrict__ px_grad, float* __restrict__ py_grad,
+    uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo, uint16_t* __restrict__ Yp_hi,
+    uint16_t* __restrict__ Yp_lo) {
   __shared__ float sy[32][33], sb[32][33], sg[32][33];
   // per diagonal and strip: ob = A^w_k + B^w_{k+1} - L (blank arc, same column), ox = A^w_k +
   // B^{w+1}_{k+1} - L (label arc out of the strip's last column into the next strip)
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
   __syncthreads();
 
   const int t_base0 = k0 - 31;
-  for (int ub = 0; ub < U1; ub += 32) {
+  for (int ub = 0; ub < UP; ub += 32) {
     for (int kr = warp; kr < 32; kr += 8) {
       const int k = k0 + kr, u = ub + lane, t = k - u;
       float yv = 0.f, bv = 0.f, g = 0.f;
@@ -376,11 +378,25 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const int t_base = t_base0 - ub;
     for (int tr = warp; tr < 63; tr += 8) {
       const int t = t_base + tr, u = ub + lane, kr = tr + lane - 31;
-      if (kr >= 0 && kr < 32 && t >= 0 && t < T && u < U1) {
-        const size_t o = ((size_t)n * T + t) * U1 + u;
-        px_grad[o] = sy[kr][lane];
-        py_grad[o] = sb[kr][lane];
-        Gt[o] = sg[kr][lane];
+      if (kr >= 0 && kr < 32 && t >= 0 && t < T) {
+        if (u < U1) {
+          const size_t o = ((size_t)n * T + t) * U1 + u;
+          px_grad[o] = sy[kr][lane];
+          py_grad[o] = sb[kr][lane];
+        }
+        // G~ for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP (zero padded)
+        const float g = sg[kr][lane];
+        const __nv_bfloat16 gh = __float2bfloat16_rn(g);
+        const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
+        const size_t og = ((size_t)n * T + t) * UP + u;
+        Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
+        Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
+        // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
+        const float yv = sy[kr][lane];
+        const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
+        const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
+        Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
+        Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
       }
     }
     __syncthreads();
@@ -428,10 +444,12 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
-  dim3 grid((d.K() + 31) / 32, d.N);
+  // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
+  dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
   RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
-                                                                   32 * d.lat_R(), px_grad, py_grad, w.Gt));
+                                                                   32 * d.lat_R(), d.UP(), px_grad, py_grad, w.Gt_hi,
+                                                                   w.Gt_lo, w.Yp_hi, w.Yp_lo));
   return cudaGetLastError();
 }
 

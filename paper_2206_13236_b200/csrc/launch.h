@@ -11,7 +11,7 @@ enum KernelId {
   KID_VALIDATE, KID_ROWMAX_AM, KID_ROWMAX_LM, KID_NORM, KID_SKEW_FILL, KID_ALPHA, KID_COMBINE,
   KID_AMGRAD, KID_AMPICK, KID_LMGRAD, KID_LMPICK, KID_RAW, KID_ADJUST, KID_PRUNE, KID_ROWINFO,
   KID_JOINER_FWD, KID_SOFTMAX, KID_PALPHA, KID_PBETA, KID_PCOMBINE, KID_DH, KID_DENC, KID_DDEC,
-  KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD,
+  KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD, KID_OCCSUMS,
   KID_COUNT
 };
 

@@ -1,0 +1,703 @@
+// simple_tc.cu — the contractions of the simple (trivial-joiner) loss on tcgen05.
+//
+//   K1 exp_split_kernel   m(row) = max_v x[row,v] (the offsets of Eq. 6, "after first applying
+//                         offsets") and E = e^{x - m} split into bf16 hi + lo
+//                         (E = hi + lo to 2^-17 relative; D7 "bf16x3")
+//   K2 norm (gemm3)       S(t,u) = sum_v E_am[t,v] E_lm[u,v]        (Eq. 6 as a contraction, never
+//                         materialising (T,U+1,V)); epilogue: L_norm = log S + m_am + m_lm and the
+//                         skewed lattice arcs px2 = y(t,u) log2e, py2 = empty(t,u) log2e (Eq. 1-2,
+//                         Eq. 5), 1/S — written diagonal-major through a per-warp smem transpose
+//   K5a am_grad (gemm3)   am_grad[t,v] = gs (E_am[t,v] sum_u G~[t,u] E_lm[u,v] - picks)
+//   K5b lm_grad (gemm3)   lm_grad[u,v] = gs (E_lm[u,v] sum_t G~[t,u] E_am[t,v] - picks)
+//                         with G~ = (y' + empty') / S and the picks sum_u y'[v = y_{u+1}] +
+//                         [v = 0] sum_u empty' (chain rule through Eq. 5-6)
+// gemm3: one 128 x BN output tile per CTA, fp32 accumulator in TMEM, bf16x3 products
+// hi*hi + hi*lo + lo*hi issued as three tcgen05.mma.kind::f16 per K slice.  Operands come from
+// per-utterance 3-D TMA tensor maps (a box never spills into the next utterance: OOB reads 0).
+// Warp 4: TMEM allocator, lane 0 TMA producer, lane 1 MMA issuer; warps 0-3: prologue (per-tile
+// tables in smem, overlapping the mainloop) and epilogue (TMEM lane = tile row = thread).
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+#include "tc.cuh"
+#include "tmap.h"
+#include "workspace.h"
+
+namespace rnnt {
+
+// ------------------------------------------------------------------ K1
+// One warp per row of am (which = 0, rows t of T) or lm (which = 1, rows u of U+1).  am rows also
+// gather amy[t,u] = am[t, y_{u+1}] (the label logit the normaliser epilogue needs, read here while
+// the row is in L1); lm rows also write the one-hot row [v == y_{u+1}] of the am pick contraction.
+__global__ void __launch_bounds__(256) exp_split_kernel(const float* __restrict__ x, const int64_t* __restrict__ sym,
+                                                        const int64_t* __restrict__ bnd, int N, int rows_per_n,
+                                                        int U, int V, int VP, int which, float* __restrict__ m,
+                                                        uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
+                                                        float* __restrict__ amy, int UPa, uint16_t* __restrict__ onehot) {
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)N * rows_per_n) return;
+  const int n = (int)(row / rows_per_n), r = (int)(row % rows_per_n);
+  const int Un = utt_U(bnd, n);
+  const int lim = which == 0 ? utt_T(bnd, n) : Un + 1;
+  uint32_t* H = reinterpret_cast<uint32_t*>(hi + row * (long long)VP);
+  uint32_t* L = reinterpret_cast<uint32_t*>(lo + row * (long long)VP);
+  int label = -1;                                    // lm rows: y_{u+1} (u < U_n)
+  if (which == 1 && r < Un) {
+    const long long y = sym[(size_t)n * U + r];
+    label = (y >= 1 && y < V) ? (int)y : -1;
+  }
+  if (which == 1) {
+    uint32_t* O = reinterpret_cast<uint32_t*>(onehot + row * (long long)VP);
+    for (int v2 = lane; v2 < VP / 2; v2 += 32)
+      O[v2] = (2 * v2 == label) ? 0x3f80u : ((2 * v2 + 1 == label) ? 0x3f800000u : 0u);   // bf16 1.0
+  }
+  if (r >= lim) {   // padded row: zero operand, never read otherwise
+    for (int v2 = lane; v2 < VP / 2; v2 += 32) { H[v2] = 0u; L[v2] = 0u; }
+    if (lane == 0) m[row] = 0.f;
+    return;
+  }
+  const float* p = x + row * (long long)V;
+  float mx = neg_inf_f();
+  for (int v = lane; v < V; v += 32) mx = fmaxf(mx, p[v]);
+  mx = warp_max(mx);
+  if (lane == 0) m[row] = mx;
+  for (int v2 = lane; v2 < VP / 2; v2 += 32) {
+    const int v = 2 * v2;
+    const float e0 = v < V ? __expf(p[v] - mx) : 0.f;
+    const float e1 = v + 1 < V ? __expf(p[v + 1] - mx) : 0.f;
+    const __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(e0 - __low2float(h), e1 - __high2float(h));
+    H[v2] = *reinterpret_cast<const uint32_t*>(&h);
+    L[v2] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+  if (which == 0) {
+    float* ay = amy + ((size_t)n * rows_per_n + r) * UPa;
+    for (int u = lane; u <= Un; u += 32) {
+      float val = 0.f;
+      if (u < Un) {
+        long long y = sym[(size_t)n * U + u];
+        y = y < 0 ? 0 : (y >= V ? V - 1 : y);        // address safety; bad symbols flagged in status
+        val = p[y];
+      }
+      ay[u] = val;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ occupancy sums
+// rowb[n,t] = sum_u empty'(t,u); colpy/colpb[n,tb,u] = sum_{t in 32-frame block tb} y'(t,u), empty'(t,u)
+__global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__ px_grad,
+                                                       const float* __restrict__ py_grad, int T, int U, int ntb,
+                                                       float* __restrict__ rowb, float* __restrict__ colpy,
+                                                       float* __restrict__ colpb) {
+  const int tb = blockIdx.x, n = blockIdx.y, U1 = U + 1, t0 = tb * 32;
+  const int t1 = min(T, t0 + 32);
+  for (int u = threadIdx.x; u < U1; u += blockDim.x) {
+    float sy = 0.f, sb = 0.f;
+    for (int t = t0; t < t1; ++t) {
+      const size_t o = ((size_t)n * T + t) * U1 + u;
+      sy += px_grad[o];
+      sb += py_grad[o];
+    }
+    colpy[((size_t)n * ntb + tb) * U1 + u] = sy;
+    colpb[((size_t)n * ntb + tb) * U1 + u] = sb;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = t0 + warp; t < t1; t += blockDim.x / 32) {
+    float s = 0.f;
+    for (int u = lane; u < U1; u += 32) s += py_grad[((size_t)n * T + t) * U1 + u];
+    s = warp_sum(s);
+    if (lane == 0) rowb[(size_t)n * T + t] = s;
+  }
+}
+
+// ------------------------------------------------------------------ gemm3 mainloop
+namespace sg {
+constexpr int BM = 128, BK = 64, STAGES = 2, THREADS = 160;
+constexpr int A_BYTES = BM * BK * 2;                        // 16 KB per hi | lo
+constexpr int B_BYTES = 256 * BK * 2;                       // 32 KB per hi | lo (BN <= 256)
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
+constexpr int AUX_BYTES = 8192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + AUX_BYTES + 1024 + 256;
+constexpr int SCR = 32 * 33;                                // per-warp 32x32 staging block (floats)
+}  // namespace sg
+
+struct Tile {
+  int n, m0, n0, nkb0, nkb1;   // k-blocks of phase 0 (bf16x3 product) and phase 1 (hi/lo x exact B)
+};
+struct Maps {
+  CUtensorMap m[6];            // phase 0: A hi, A lo, B hi, B lo; phase 1: A' hi, A' lo
+  CUtensorMap b1;              // phase 1: B' (exact)
+  CUtensorMap ein, eout;       // epilogue fp32 input tiles (loaded after the mainloop) / output tiles
+};
+// Epilogue fp32 tiles: chunk c (32 columns x 128 rows, SWIZZLE_128B) at smem + c * EP_BYTES.
+constexpr int EP_BYTES = 128 * 32 * 4;
+// row r, 16-B chunk q of an epilogue tile
+__device__ __forceinline__ float4* ep_at(uint8_t* tile, int r, int q) {
+  return reinterpret_cast<float4*>(tile + r * 128 + ((q ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int k) { return tc::sdesc(base + 32 * k, 16, 1024); }
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) { return tc::sdesc(base + 2048 * k, 8192, 1024); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Phase 0: acc0 (TMEM columns 0..255) += A_hi B_hi + A_hi B_lo + A_lo B_hi   (bf16x3)
+// Phase 1: acc1 (TMEM columns 256..511) += A'_hi B' + A'_lo B'               (B' exact in bf16)
+template <class P>
+__global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_constant__ Maps mp, P p) {
+  using namespace sg;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* aux = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux + AUX_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* ep_full = tfull + 1;                              // [8] epilogue input tiles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ep_full + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Tile tl = p.tile();
+  if (tl.n < 0) return;
+  constexpr uint32_t kCols = P::kPhases == 2 ? 512 : 256;
+  const int nk = tl.nkb0 + (P::kPhases == 2 ? tl.nkb1 : 0);
+
+  if (warp == 4 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    tc::mbar_init(tfull, 1);
+    for (int c = 0; c < 8; ++c) tc::mbar_init(&ep_full[c], 1);
+    tc::fence_barrier_init();
+    for (int i = 0; i < 4 + (P::kPhases == 2 ? 2 : 0); ++i) tc::tma_prefetch(&mp.m[i]);
+    if (P::kPhases == 2) tc::tma_prefetch(&mp.b1);
+  }
+  if (warp == 4) tc::tmem_alloc(tmem_slot, kCols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 4) {
+    p.prologue(aux, tl);
+    if (nk > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    p.epilogue(smem, aux, tl, tbase + ((uint32_t)(32 * warp) << 16), ep_full, mp);
+  } else if (lane == 0 && nk > 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nk; ++i) {
+      const int phase = i < tl.nkb0 ? 0 : 1, kb = phase == 0 ? i : i - tl.nkb0;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      tc::mbar_arrive_expect_tx(&full[s], p.bytes(phase));
+      p.load(smem + s * STAGE_BYTES, phase, kb, tl, &full[s], mp);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+    // epilogue input tiles into the (now idle) stage buffers, as soon as the MMAs are done
+    const int nep = p.epi_chunks(tl);
+    if (nep > 0) {
+      tc::mbar_wait(tfull, 0);
+      for (int c = 0; c < nep; ++c) {
+        tc::mbar_arrive_expect_tx(&ep_full[c], EP_BYTES);
+        p.epi_load(c, smem + c * EP_BYTES, &ep_full[c], tl, mp);
+      }
+    }
+  } else if (lane == 1 && nk > 0) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nk; ++i) {
+      const int phase = i < tl.nkb0 ? 0 : 1, kb = phase == 0 ? i : i - tl.nkb0;
+      const uint32_t idesc = p.idesc(phase);
+      tc::mbar_wait(&full[s], ph);
+      tc::fence_after_sync();
+      const uint32_t ah = tc::smem_u32(smem + s * STAGE_BYTES), al = ah + A_BYTES;
+      const uint32_t bh = ah + 2 * A_BYTES, bl = bh + B_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint64_t dah = P::kA_MN ? mndesc(ah, k) : kdesc(ah, k);
+        const uint64_t dal = P::kA_MN ? mndesc(al, k) : kdesc(al, k);
+        const uint64_t dbh = P::kB_MN ? mndesc(bh, k) : kdesc(bh, k);
+        if (phase == 0) {
+          const uint64_t dbl = P::kB_MN ? mndesc(bl, k) : kdesc(bl, k);
+          tc::mma_bf16(tbase, dah, dbh, idesc, (kb | k) != 0);   // hi * hi
+          tc::mma_bf16(tbase, dah, dbl, idesc, 1);               // hi * lo
+          tc::mma_bf16(tbase, dal, dbh, idesc, 1);               // lo * hi
+        } else {
+          tc::mma_bf16(tbase + 256, dah, dbh, idesc, (kb | k) != 0);
+          tc::mma_bf16(tbase + 256, dal, dbh, idesc, 1);
+        }
+      }
+      tc::mma_commit(&empty[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+    tc::mma_commit(tfull);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 4) tc::tmem_dealloc(tbase, kCols);
+}
+
+// Coalesced warp I/O of a 32-row x 32-column fp32 block through the per-warp staging buffer:
+// row i of the block is rows0 + i (valid if i < nrows), columns c0 + lane (valid if < ncols).
+__device__ __forceinline__ void warp_load_block(float (*buf)[33], const float* src, size_t ld, int nrows, int ncols,
+                                                int lane) {
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) buf[i][lane] = (i < nrows && lane < ncols) ? src[(size_t)i * ld + lane] : 0.f;
+  __syncwarp();
+}
+__device__ __forceinline__ void warp_store_block(const float (*buf)[33], float* dst, size_t ld, int nrows, int ncols,
+                                                 int lane) {
+  __syncwarp();
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i)
+    if (i < nrows && lane < ncols) dst[(size_t)i * ld + lane] = buf[i][lane];
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------ K2: normaliser + lattice arcs
+struct NormProb {
+  static constexpr bool kA_MN = false, kB_MN = false;
+  static constexpr int kPhases = 1;
+  const float *lm, *m_am, *m_lm;
+  const int64_t *sym, *bnd;
+  int T, U, V, LU, K, BN, nkb;
+  float *px2, *py2, *rS;
+  int32_t* status;
+  const float* am;
+
+  __device__ Tile tile() const {
+    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * BN, nkb, 0};
+    if (t.m0 >= utt_T(bnd, t.n) || t.n0 > utt_U(bnd, t.n)) t.n = -1;
+    return t;
+  }
+  __device__ uint32_t bytes(int) const { return 2 * sg::A_BYTES + 2 * BN * sg::BK * 2; }
+  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, BN, false, false); }
+  __device__ void load(uint8_t* st, int, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
+    tc::tma_load_3d(st, &mp.m[0], bar, kb * sg::BK, t.m0, t.n);
+    tc::tma_load_3d(st + sg::A_BYTES, &mp.m[1], bar, kb * sg::BK, t.m0, t.n);
+    tc::tma_load_3d(st + 2 * sg::A_BYTES, &mp.m[2], bar, kb * sg::BK, t.n0, t.n);
+    tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
+  }
+  __device__ int epi_chunks(const Tile& t) const {
+    const int Un = utt_U(bnd, t.n);
+    return (min(BN, Un + 1 - t.n0) + 31) / 32;   // 32-column chunks with at least one u <= U_n
+  }
+  // amy[t, u] = am[t, y_{u+1}] tile (pitch UP), columns u0..u0+31
+  __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
+    tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
+  }
+  // per-column tables of the tile: lm[u, y_{u+1}], lm[u, 0], m_lm[u]
+  __device__ void prologue(uint8_t* aux, const Tile& t) const {
+    float* lmy = reinterpret_cast<float*>(aux);
+    float* lm0 = lmy + 256;
+    float* mlm = lm0 + 256;
+    const int Un = utt_U(bnd, t.n);
+    for (int j = threadIdx.x; j < BN; j += 128) {
+      const int u = t.n0 + j;
+      float a = 0.f, b = 0.f, c = 0.f;
+      if (u <= Un) {
+        const float* l = lm + ((size_t)t.n * (U + 1) + u) * V;
+        if (u < Un) {
+          long long yy = sym[(size_t)t.n * U + u];
+          a = l[yy < 0 ? 0 : (yy >= V ? V - 1 : yy)];   // address safety; bad symbols flagged in status
+        }
+        b = l[0];
+        c = m_lm[(size_t)t.n * (U + 1) + u];
+      }
+      lmy[j] = a; lm0[j] = b; mlm[j] = c;
+    }
+    epi_bar();
+  }
+  __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, uint32_t taddr, uint64_t* ep_full,
+                           const Maps&) const {
+    const float* lmy = reinterpret_cast<const float*>(aux);
+    const float* lm0 = lmy + 256;
+    const float* mlm = lm0 + 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
+    const int trow = t.m0 + threadIdx.x;
+    const bool rowok = trow < Tn;
+    const int t0w = t.m0 + 32 * warp;
+    // transposition scratch after the 8 epilogue input tiles (8 x 16 KB)
+    float (*bx)[33] = reinterpret_cast<float (*)[33]>(smem + 8 * EP_BYTES + warp * 3 * sg::SCR * 4);
+    float (*by)[33] = bx + 32;
+    float (*bz)[33] = by + 32;
+    const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
+    const float mam = rowok ? m_am[arow] : 0.f;
+    const float am0 = rowok ? am[arow * V] : 0.f;
+    const size_t nbase = (size_t)t.n * (K + 1);
+    bool under = false;
+    const int nep = epi_chunks(t);
+    for (int c = 0; c < nep; ++c) {
+      const int c0 = 32 * c, u0 = t.n0 + c0;
+      float acc[32], ay[32];
+      tc::tmem_ld32(taddr + c0, acc);
+      tc::mbar_wait(&ep_full[c], 0);
+      uint8_t* tile = smem + c * EP_BYTES;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 v = *ep_at(tile, threadIdx.x, q);
+        ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
+      }
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int u = u0 + j;
+        float px = kNegBig, py = kNegBig, rs = 0.f;
+        if (rowok && u <= Un) {
+          const float S = acc[j];
+          under |= !(S > 0.f);
+          const float Lnorm = logf(S) + mam + mlm[c0 + j];           // L_normalizer(t,u), Eq. 6
+          if (u < Un) px = (ay[j] + lmy[c0 + j] - Lnorm) * RNNT_LOG2E_F;   // y(t,u), Eq. 1 + 5
+          // empty(t,u), Eq. 2 + 5; out of the last frame only the terminal blank exists
+          if (!(trow == Tn - 1 && u < Un)) py = (am0 + lm0[c0 + j] - Lnorm) * RNNT_LOG2E_F;
+          rs = 1.0f / S;
+        }
+        bx[lane][j] = px;
+        by[lane][j] = py;
+        bz[lane][j] = rs;
+      }
+      __syncwarp();
+      // diagonal-major write: for diagonal k = t0w + u0 + d, lane l holds column u0 + l (t = k - u)
+      const int u = u0 + lane;
+      for (int d = 0; d < 63; ++d) {
+        const int tl_ = d - lane, tt = t0w + tl_;
+        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) {
+          const size_t idx = (nbase + tt + u) * LU + u;
+          px2[idx] = bx[tl_][lane];
+          py2[idx] = by[tl_][lane];
+          rS[idx] = bz[tl_][lane];
+        }
+      }
+      __syncwarp();
+    }
+    if (under) set_status(status, t.n, kStatusUnderflow);
+  }
+};
+
+// ------------------------------------------------------------------ K5a: am_grad
+struct AmProb {
+  static constexpr bool kA_MN = false, kB_MN = true;
+  static constexpr int kPhases = 2;
+  const float *am, *m_am, *rowb;
+  const int64_t* bnd;
+  int T, U, V;
+  float gs;
+  float* am_grad;
+
+  __device__ Tile tile() const {
+    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
+    const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
+    t.nkb0 = (t.m0 < Tn) ? (Un + 1 + sg::BK - 1) / sg::BK : 0;
+    t.nkb1 = (t.m0 < Tn && Un > 0) ? (Un + sg::BK - 1) / sg::BK : 0;   // label arcs exist for u < U_n
+    return t;
+  }
+  __device__ uint32_t bytes(int phase) const {
+    return phase == 0 ? 2 * sg::A_BYTES + 2 * sg::B_BYTES : 2 * sg::A_BYTES + sg::B_BYTES;
+  }
+  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, 256, false, true); }
+  // phase 0: A = G~ (hi, lo; K-major over u), B = E_lm (hi, lo; MN-major);
+  // phase 1: A = y' (hi, lo), B = one-hot of the labels [v == y_{u+1}] (exact)
+  __device__ void load(uint8_t* st, int phase, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
+    const CUtensorMap* ah = phase == 0 ? &mp.m[0] : &mp.m[4];
+    const CUtensorMap* al = phase == 0 ? &mp.m[1] : &mp.m[5];
+    tc::tma_load_3d(st, ah, bar, kb * sg::BK, t.m0, t.n);
+    tc::tma_load_3d(st + sg::A_BYTES, al, bar, kb * sg::BK, t.m0, t.n);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (phase == 0) {
+        tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.m[2], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+        tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i, kb * sg::BK,
+                        t.n);
+      } else {
+        tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.b1, bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+      }
+    }
+  }
+  bool tma_io;   // V % 4 == 0: fp32 rows are 16-B aligned, tiles move by TMA
+  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
+  __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
+    tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
+  }
+  __device__ void prologue(uint8_t*, const Tile&) const {}
+  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, uint32_t taddr, uint64_t* ep_full,
+                           const Maps& mp) const {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Tn = utt_T(bnd, t.n);
+    const int trow = t.m0 + threadIdx.x;
+    const bool live = trow < Tn;
+    const int nep = epi_chunks(t);
+    if (nep > 0) {
+      // d(-L_simple)/d am = E_am (G~ E_lm) - y' onehot - [v=0] sum_u empty'   (times gs), tile in place
+      const size_t row = (size_t)t.n * T + (live ? trow : 0);
+      const float mam = live ? m_am[row] : 0.f;
+      const float rb = live ? rowb[row] : 0.f;
+      for (int c = 0; c < nep; ++c) {
+        const int vc = t.n0 + 32 * c;
+        float a0[32], a1[32];
+        tc::tmem_ld32(taddr + 32 * c, a0);
+        tc::tmem_ld32(taddr + 256 + 32 * c, a1);
+        if (t.nkb1 == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a1[j] = 0.f;
+        }
+        tc::mbar_wait(&ep_full[c], 0);
+        uint8_t* tile = smem + c * EP_BYTES;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4* pq = ep_at(tile, threadIdx.x, q);
+          const float4 x = *pq;
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          float o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = 4 * q + i;
+            const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
+            o[i] = live ? gs * (__expf(xs[i] - mam) * a0[j] - pick) : 0.f;
+          }
+          *pq = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        tc::fence_proxy_async();
+        epi_bar();
+        if (threadIdx.x == 0) {
+          tc::tma_store_3d(&mp.eout, tile, vc, t.m0, t.n);
+          tc::bulk_commit();
+        }
+      }
+      if (threadIdx.x == 0) tc::bulk_wait_read0();
+      return;
+    }
+    // generic path (V % 4 != 0, or a tile of padded rows only): coalesced warp I/O through smem
+    const int t0w = t.m0 + 32 * warp;
+    if (t0w >= T) return;                               // whole warp beyond the padded rows
+    const size_t row0 = (size_t)t.n * T + t0w;
+    const float mam = live ? m_am[row0 + lane] : 0.f;
+    const float rb = live ? rowb[row0 + lane] : 0.f;
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + warp * sg::SCR * 4);
+    const int nin = min(32, Tn - t0w), nout = min(32, T - t0w);
+    for (int c = 0; c < 8; ++c) {
+      const int vc = t.n0 + 32 * c;
+      if (vc >= V) break;
+      float a0[32], a1[32];
+      if (t.nkb0 > 0) {
+        tc::tmem_ld32(taddr + 32 * c, a0);
+        tc::tmem_ld32(taddr + 256 + 32 * c, a1);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { a0[j] = 0.f; a1[j] = 0.f; }
+      }
+      if (t.nkb1 == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a1[j] = 0.f;
+      }
+      const int nc = min(32, V - vc);
+      warp_load_block(buf, am + row0 * V + vc, V, nin, nc, lane);
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
+        buf[lane][j] = live ? gs * (__expf(buf[lane][j] - mam) * a0[j] - pick) : 0.f;
+      }
+      warp_store_block(buf, am_grad + row0 * V + vc, V, nout, nc, lane);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ K5b: lm_grad
+struct LmProb {
+  static constexpr bool kA_MN = true, kB_MN = true;
+  static constexpr int kPhases = 1;
+  const float *lm, *m_lm, *colpy, *colpb;
+  const int64_t *sym, *bnd;
+  int T, U, V, ntb;
+  float gs;
+  float* lm_grad;
+
+  __device__ Tile tile() const {
+    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
+    const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
+    t.nkb0 = (t.m0 <= Un) ? (Tn + sg::BK - 1) / sg::BK : 0;
+    return t;
+  }
+  __device__ uint32_t bytes(int) const { return 2 * sg::A_BYTES + 2 * sg::B_BYTES; }
+  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, 256, true, true); }
+  __device__ void load(uint8_t* st, int, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      tc::tma_load_3d(st + i * 8192, &mp.m[0], bar, t.m0 + 64 * i, kb * sg::BK, t.n);
+      tc::tma_load_3d(st + sg::A_BYTES + i * 8192, &mp.m[1], bar, t.m0 + 64 * i, kb * sg::BK, t.n);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.m[2], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+      tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+    }
+  }
+  bool tma_io;
+  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
+  __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
+    tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
+  }
+  __device__ void prologue(uint8_t*, const Tile&) const {}
+  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, uint32_t taddr, uint64_t* ep_full,
+                           const Maps& mp) const {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Un = utt_U(bnd, t.n), U1 = U + 1;
+    const int urow = t.m0 + threadIdx.x;
+    const bool live = urow <= Un;
+    float csy = 0.f, csb = 0.f;
+    int y = -1;
+    if (live) {
+      for (int tb = 0; tb < ntb; ++tb) {
+        csy += colpy[((size_t)t.n * ntb + tb) * U1 + urow];
+        csb += colpb[((size_t)t.n * ntb + tb) * U1 + urow];
+      }
+      if (urow < Un) y = (int)sym[(size_t)t.n * U + urow];
+    }
+    const int nep = epi_chunks(t);
+    if (nep > 0) {
+      const float mlm = live ? m_lm[(size_t)t.n * U1 + urow] : 0.f;
+      for (int c = 0; c < nep; ++c) {
+        const int vc = t.n0 + 32 * c;
+        float acc[32];
+        tc::tmem_ld32(taddr + 32 * c, acc);
+        tc::mbar_wait(&ep_full[c], 0);
+        uint8_t* tile = smem + c * EP_BYTES;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4* pq = ep_at(tile, threadIdx.x, q);
+          const float4 x = *pq;
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          float o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = 4 * q + i, v = vc + j;
+            const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);
+            o[i] = live ? gs * (__expf(xs[i] - mlm) * acc[j] - pick) : 0.f;
+          }
+          *pq = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        tc::fence_proxy_async();
+        epi_bar();
+        if (threadIdx.x == 0) {
+          tc::tma_store_3d(&mp.eout, tile, vc, t.m0, t.n);
+          tc::bulk_commit();
+        }
+      }
+      if (threadIdx.x == 0) tc::bulk_wait_read0();
+      return;
+    }
+    const int u0w = t.m0 + 32 * warp;
+    if (u0w >= U1) return;                               // whole warp beyond the padded rows
+    const size_t row0 = (size_t)t.n * U1 + u0w;
+    const float mlm = live ? m_lm[row0 + lane] : 0.f;
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + warp * sg::SCR * 4);
+    const int nin = min(32, Un + 1 - u0w), nout = min(32, U1 - u0w);
+    for (int c = 0; c < 8; ++c) {
+      const int vc = t.n0 + 32 * c;
+      if (vc >= V) break;
+      float acc[32];
+      if (t.nkb0 > 0) {
+        tc::tmem_ld32(taddr + 32 * c, acc);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      }
+      const int nc = min(32, V - vc);
+      warp_load_block(buf, lm + row0 * V + vc, V, nin, nc, lane);
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const int v = vc + j;
+        const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);
+        buf[lane][j] = live ? gs * (__expf(buf[lane][j] - mlm) * acc[j] - pick) : 0.f;
+      }
+      warp_store_block(buf, lm_grad + row0 * V + vc, V, nout, nc, lane);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ host
+template <class P>
+static cudaError_t launch_gemm3(const P& p, dim3 grid, const Maps& mp, int kid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm3_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg::SMEM_BYTES);
+    attr = true;
+  }
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return cudaSuccess;
+  RNNT_LAUNCH(kid, st, gemm3_kernel<P><<<grid, sg::THREADS, sg::SMEM_BYTES, st>>>(mp, p));
+  return cudaGetLastError();
+}
+
+static bool tm3(CUtensorMap* m, const uint16_t* base, int pitch, int rows, int N, int box_rows) {
+  return make_tmap_bf16_3d(m, base, (uint64_t)pitch, (uint64_t)rows, (uint64_t)N, (uint64_t)pitch * 2,
+                           (uint64_t)pitch * rows * 2, 64, (uint32_t)box_rows);
+}
+
+cudaError_t exp_split_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
+                             const int64_t* bnd, cudaStream_t st) {
+  long long rows = (long long)d.N * d.T;
+  RNNT_LAUNCH(KID_ROWMAX_AM, st, exp_split_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      am, sym, bnd, d.N, d.T, d.U, d.V, d.VP64(), 0, w.m_am, w.Eam_hi, w.Eam_lo, w.amy, d.UP(), nullptr));
+  rows = (long long)d.N * d.U1();
+  RNNT_LAUNCH(KID_ROWMAX_LM, st, exp_split_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
+      lm, sym, bnd, d.N, d.U1(), d.U, d.V, d.VP64(), 1, w.m_lm, w.Elm_hi, w.Elm_lo, nullptr, 0, w.onehot));
+  return cudaGetLastError();
+}
+
+cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
+                             const int64_t* bnd, int32_t* status, cudaStream_t st) {
+  const int BN = std::min(256, (d.U1() + 15) / 16 * 16);
+  Maps mp;
+  if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
+      !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))
+    return cudaErrorInvalidValue;
+  if (!make_tmap_f32_3d(&mp.ein, w.amy, d.UP(), d.T, d.N, (uint64_t)d.UP() * 4, (uint64_t)d.UP() * d.T * 4, 32,
+                        sg::BM))
+    return cudaErrorInvalidValue;
+  NormProb p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64,
+             w.px2, w.py2, w.rS, status, am};
+  dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.U1() + BN - 1) / BN, d.N);
+  return launch_gemm3(p, grid, mp, KID_NORM, st);
+}
+
+cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
+                                const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
+                                float gs, float* am_grad, float* lm_grad, cudaStream_t st) {
+  if (!am_grad && !lm_grad) return cudaSuccess;
+  RNNT_LAUNCH(KID_OCCSUMS, st, occ_sums_kernel<<<dim3(d.ntb(), d.N), 256, 0, st>>>(px_grad, py_grad, d.T, d.U, d.ntb(),
+                                                                                   w.rowb, w.colpy, w.colpb));
+  cudaError_t e;
+  if (am_grad) {
+    Maps mp;
+    if (!tm3(&mp.m[0], w.Gt_hi, d.UP(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Gt_lo, d.UP(), d.T, d.N, sg::BM) ||
+        !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, 64) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, 64) ||
+        !tm3(&mp.m[4], w.Yp_hi, d.UP(), d.T, d.N, sg::BM) || !tm3(&mp.m[5], w.Yp_lo, d.UP(), d.T, d.N, sg::BM) ||
+        !tm3(&mp.b1, w.onehot, d.VP64(), d.U1(), d.N, 64))
+      return cudaErrorInvalidValue;
+    const bool io = d.V % 4 == 0;
+    if (io && (!make_tmap_f32_3d(&mp.ein, am, d.V, d.T, d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.T * 4, 32, sg::BM) ||
+               !make_tmap_f32_3d(&mp.eout, am_grad, d.V, d.T, d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.T * 4, 32,
+                                 sg::BM)))
+      return cudaErrorInvalidValue;
+    AmProb p{am, w.m_am, w.rowb, bnd, d.T, d.U, d.V, gs, am_grad, io};
+    dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
+    if ((e = launch_gemm3(p, grid, mp, KID_AMGRAD, st)) != cudaSuccess) return e;
+  }
+  if (lm_grad) {
+    Maps mp;
+    if (!tm3(&mp.m[0], w.Gt_hi, d.UP(), d.T, d.N, 64) || !tm3(&mp.m[1], w.Gt_lo, d.UP(), d.T, d.N, 64) ||
+        !tm3(&mp.m[2], w.Eam_hi, d.VP64(), d.T, d.N, 64) || !tm3(&mp.m[3], w.Eam_lo, d.VP64(), d.T, d.N, 64))
+      return cudaErrorInvalidValue;
+    const bool io = d.V % 4 == 0;
+    if (io && (!make_tmap_f32_3d(&mp.ein, lm, d.V, d.U1(), d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.U1() * 4, 32,
+                                 sg::BM) ||
+               !make_tmap_f32_3d(&mp.eout, lm_grad, d.V, d.U1(), d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.U1() * 4,
+                                 32, sg::BM)))
+      return cudaErrorInvalidValue;
+    LmProb p{lm, w.m_lm, w.colpy, w.colpb, sym, bnd, d.T, d.U, d.V, d.ntb(), gs, lm_grad, io};
+    dim3 grid((d.U1() + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
+    if ((e = launch_gemm3(p, grid, mp, KID_LMGRAD, st)) != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace rnnt

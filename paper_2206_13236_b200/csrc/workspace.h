@@ -28,6 +28,9 @@ struct Dims {
   int LU() const { return 32 * lat_R() * lat_W(); }
   int K() const { return T + U; }                       // number of anti-diagonals
   long long rows() const { return (long long)N * T * S; }
+  int VP64() const { return (V + 63) / 64 * 64; }       // bf16 pitch of the E operands (K-major boxes of 64)
+  int UP() const { return (U + 1 + 63) / 64 * 64; }      // bf16 pitch of G~ (t-major, K-major boxes of 64)
+  int ntb() const { return (T + 31) / 32; }              // 32-frame blocks of the occupancy column partials
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
   int VP() const { return (V + 127) / 128 * 128; }      // padded row pitch of P~ (elements)
 };
@@ -45,7 +48,19 @@ struct SimpleWS {
   float* Ash;     // (N,K+1,W)  A_k per diagonal and strip (integer-valued)
   float* Bsh;     // (N,K+1,W)  B_k per diagonal and strip
   double* Ltot;   // (N)        L_tot (natural log)
-  float* Gt;      // (N,T,U+1)  (y'+empty') / S(t,u)   (t-major)
+  uint16_t* Eam_hi;  // (N,T,VP64) bf16 hi of e^{am - m_am} (zero rows t >= T_n, zero cols v >= V)
+  uint16_t* Eam_lo;  // (N,T,VP64) bf16 lo = bf16(e - hi)
+  uint16_t* Elm_hi;  // (N,U+1,VP64)
+  uint16_t* Elm_lo;
+  uint16_t* Gt_hi;   // (N,T,UP)   bf16 hi/lo of G~ = (y'+empty')/S(t,u) (t-major, zero padded)
+  uint16_t* Gt_lo;
+  uint16_t* Yp_hi;   // (N,T,UP)   bf16 hi/lo of y'(t,u) (t-major, zero padded): A of the am pick GEMM
+  uint16_t* Yp_lo;
+  uint16_t* onehot;  // (N,U+1,VP64) bf16 [v == y_{u+1}] (u < U_n): B of the am pick GEMM
+  float* amy;        // (N,T,UP)   am[t, y_{u+1}] (gathered by exp_split for the normaliser epilogue)
+  float* rowb;       // (N,T)      sum_u empty'(t,u)
+  float* colpy;      // (N,ntb,U+1) per-32-frame-block partial sums of y'(t,u) over t
+  float* colpb;      // (N,ntb,U+1) ... of empty'(t,u)
 };
 
 struct PrunedWS {
@@ -106,7 +121,20 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.Ash = (float*)take(N * K1 * (size_t)d.lat_W() * 4);
   s.Bsh = (float*)take(N * K1 * (size_t)d.lat_W() * 4);
   s.Ltot = (double*)take(N * 8);
-  s.Gt = (float*)take(N * T * U1 * 4);
+  const size_t VP64 = d.VP64(), UP = d.UP(), NTB = d.ntb();
+  s.Eam_hi = (uint16_t*)take(N * T * VP64 * 2);
+  s.Eam_lo = (uint16_t*)take(N * T * VP64 * 2);
+  s.Elm_hi = (uint16_t*)take(N * U1 * VP64 * 2);
+  s.Elm_lo = (uint16_t*)take(N * U1 * VP64 * 2);
+  s.Gt_hi = (uint16_t*)take(N * T * UP * 2);
+  s.Gt_lo = (uint16_t*)take(N * T * UP * 2);
+  s.Yp_hi = (uint16_t*)take(N * T * UP * 2);
+  s.Yp_lo = (uint16_t*)take(N * T * UP * 2);
+  s.onehot = (uint16_t*)take(N * U1 * VP64 * 2);
+  s.amy = (float*)take(N * T * UP * 4);
+  s.rowb = (float*)take(N * T * 4);
+  s.colpy = (float*)take(N * NTB * U1 * 4);
+  s.colpb = (float*)take(N * NTB * U1 * 4);
   PrunedWS p;
   p.splits = dw_splits(d);
   p.rowinfo = (int32_t*)take(R * 4);

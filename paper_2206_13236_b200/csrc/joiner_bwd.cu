@@ -24,11 +24,10 @@ namespace rnnt {
 
 struct GradSrc {
   const uint16_t* Pt;
-  const float *sc, *gb, *gl;
+  const float4* gpk;       // (ntile, R) {sc, gs g_b, gs g_l, label bits}, written by pruned_combine
   const int32_t* rowinfo;
   long long R;
   int V, VP, ntile;
-  float gs;
 };
 
 // dz for the 8 logits v = vc..vc+7 of one row, from the packed bf16 P~ chunk `pv`, the row's
@@ -72,21 +71,22 @@ namespace jdh {
 constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 512, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
 constexpr int B_BYTES = MAXN * BK * 2;         // 64 KB, MN-major (8 boxes of 64 j x 64 v)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
+constexpr int H_BYTES = BM * 64 * 2;           // 16 KB: one 64-column box of h for the epilogue
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int THREADS = 160;
 }  // namespace jdh
 
 struct JoinerDhParams {
   GradSrc g;
-  const uint16_t* h;
   int J, nkb;
   float* dpre;
 };
 
 __global__ void __launch_bounds__(jdh::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
-                        JoinerDhParams p) {
+                        const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
   using namespace jdh;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* hfull = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long m0 = (long long)blockIdx.x * BM;
   const int j0 = blockIdx.y * MAXN;
@@ -123,66 +124,68 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tfull, 1);
+    tc::mbar_init(hfull, 1);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
     tc::tma_prefetch(&tmW);
+    tc::tma_prefetch(&tmH);
   }
   if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
+  const int grows = (int)min((long long)BM, p.g.R - m0);   // rows of the packed-scalar copy
 
   if (warp < 4) {
     // ---- producers: thread = tile row; transform the 8 chunks of its row in place
     const int rl = threadIdx.x;
     const long long r = m0 + rl;
-    const int info = (r < p.g.R) ? p.g.rowinfo[r] : -1;
-    const bool live = info >= 0;
-    const float gbs = live ? p.g.gs * p.g.gb[r] : 0.f;
-    const float gls = live ? p.g.gs * p.g.gl[r] : 0.f;
-    const float* scr = p.g.sc + (size_t)(live ? r : 0) * p.g.ntile;
     int stage = 0;
     uint32_t ph = 0;
-    float s_cur = live ? scr[0] : 0.f;
     for (int kb = 0; kb < p.nkb; ++kb) {
       const int v0 = kb * BK;
-      const float s = (v0 >> 7) == 0 ? s_cur : (live ? scr[v0 >> 7] : 0.f);
       tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
+      const float4 gq = rl < grows ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
+                                   : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+      const int info = __float_as_int(gq.w);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint4* q = reinterpret_cast<uint4*>(sa + sw128(rl, c));
         const uint4 pv = *q;
-        *q = live ? dz_chunk(pv, s, gbs, gls, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
+        *q = info >= 0 ? dz_chunk(pv, gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
       }
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&full[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
-    // ---- epilogue: dpre = dh * (1 - h^2)
+    // ---- epilogue: dpre = dh * (1 - h^2), h from the TMA tiles loaded after the mainloop
     tc::mbar_wait(tfull, 0);
     tc::fence_after_sync();
+    tc::mbar_wait(hfull, 0);
+    const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
     const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
     for (int c0 = 0; c0 < nj; c0 += 32) {
       float acc[32];
       tc::tmem_ld32(tl + c0, acc);
       if (r < p.g.R) {
         float* o = p.dpre + (size_t)r * p.J + j0 + c0;
-        const uint4* hp = reinterpret_cast<const uint4*>(p.h + (size_t)r * p.J + j0 + c0);
-        const int nq = min(4, (nj - c0) / 8);   // J % 8 == 0
+        const uint8_t* hb = smem + (c0 >> 6) * H_BYTES;       // 64-column box
+        const int qh = ((c0 >> 5) & 1) * 4;                   // 16-B chunk of the 32-column half
+        const int nq = min(4, (nj - c0) / 8);                 // J % 8 == 0
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (q >= nq) break;
-          const uint4 hv = live ? hp[q] : make_uint4(0, 0, 0, 0);
+          const uint4 hv = live ? *reinterpret_cast<const uint4*>(hb + sw128(rl, qh + q)) : make_uint4(0, 0, 0, 0);
           const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
           float out[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float ha = __uint_as_float(hw[i] << 16), hb = __uint_as_float(hw[i] & 0xffff0000u);
+            const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
             out[2 * i] = live ? acc[8 * q + 2 * i] * (1.f - ha * ha) : 0.f;
-            out[2 * i + 1] = live ? acc[8 * q + 2 * i + 1] * (1.f - hb * hb) : 0.f;
+            out[2 * i + 1] = live ? acc[8 * q + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
           }
           reinterpret_cast<float4*>(o)[2 * q] = make_float4(out[0], out[1], out[2], out[3]);
           reinterpret_cast<float4*>(o)[2 * q + 1] = make_float4(out[4], out[5], out[6], out[7]);
@@ -190,8 +193,9 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       }
     }
   } else if (lane == 0) {
-    // ---- warp 4 lane 0: TMA for A = P~[m0.., kb*64..] and B = W[kb*64.., j0..]
-    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2;
+    // ---- warp 4 lane 0: TMA for A = P~[m0.., kb*64..], B = W[kb*64.., j0..] and the rows' scalars
+    const uint32_t gbytes = (uint32_t)grows * 16u;
+    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < p.nkb; ++kb) {
@@ -201,8 +205,13 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
       for (int bx = 0; bx < nbox; ++bx)
         tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
+      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0, gbytes, &loaded[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
+    // h tiles for the epilogue, into the idle stage buffers once the MMAs are done
+    tc::mbar_wait(tfull, 0);
+    tc::mbar_arrive_expect_tx(hfull, (uint32_t)nbox * H_BYTES);
+    for (int bx = 0; bx < nbox; ++bx) tc::tma_load_2d(smem + bx * H_BYTES, &tmH, hfull, j0 + bx * 64, (int)m0);
   } else if (lane == 1) {
     // ---- warp 4 lane 1: MMA issuer
     constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
@@ -233,9 +242,9 @@ namespace jdw {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 TMA boxes of 64 v x 64 rows of P~)
 constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows of h)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SCAL_BYTES = 2 * BK * 16;  // per-row scalars of two k-blocks (double buffer)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4 + SCAL_BYTES;
+constexpr int G_BYTES = BK * 16;         // 1 KB: the k-block rows' packed scalars for this V tile
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4;
 constexpr int THREADS = 160;
 }  // namespace jdw
 
@@ -259,7 +268,6 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][128 v]
-  float4* scal = reinterpret_cast<float4*>(smem + STAGES * STAGE_BYTES + 256 + 128 * 16 * 4);  // [2][64]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
   const long long kb0 = (long long)split * p.kb_per_split;
@@ -293,28 +301,18 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
     const int g8 = threadIdx.x >> 4;         // row group 0..7
     float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool want_db = blockIdx.y == 0;
-    // per-row scalars {sc, gs g_b, gs g_l, info} of a k-block, gathered by threads 0..63
-    auto fetch = [&](int kb) -> float4 {
-      const long long r = (kb0 + kb) * BK + threadIdx.x;
-      if (threadIdx.x >= BK || r >= p.g.R) return make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-      const int info = p.g.rowinfo[r];
-      if (info < 0) return make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-      return make_float4(p.g.sc[(size_t)r * p.g.ntile + vtile], p.g.gs * p.g.gb[r], p.g.gs * p.g.gl[r],
-                         __int_as_float(info));
-    };
-    float4 nxt = nkb > 0 ? fetch(0) : make_float4(0.f, 0.f, 0.f, 0.f);
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      if (threadIdx.x < BK) scal[(kb & 1) * BK + threadIdx.x] = nxt;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (kb + 1 < nkb) nxt = fetch(kb + 1);
+      const long long rb = (kb0 + kb) * BK;
+      const int grows = (int)min((long long)BK, p.g.R - rb);
       tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
+      const float4* gq = reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES);
 #pragma unroll 4
       for (int i = 0; i < 8; ++i) {
         const int rl = g8 + 8 * i;
-        const float4 sr = scal[(kb & 1) * BK + rl];
+        const float4 sr = rl < grows ? gq[rl] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
         const int info = __float_as_int(sr.w);
         uint4* q = reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
         const uint4 pv = *q;
@@ -361,19 +359,21 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes) and B = h[rows, j0..] (nbox boxes)
-    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2;
+    // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes), B = h[rows, j0..] and the scalars
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
+      const long long rb = (kb0 + kb) * BK;
+      const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
+      const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;
       tc::mbar_wait(&empty[stage], ph ^ 1);
       uint8_t* sa = smem + stage * STAGE_BYTES;
-      const int rrow = (int)((kb0 + kb) * BK);
       tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
-      tc::tma_load_2d(sa, &tmP, &loaded[stage], v0, rrow);
-      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, &loaded[stage], v0 + 64, rrow);
+      tc::tma_load_2d(sa, &tmP, &loaded[stage], v0, (int)rb);
+      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, &loaded[stage], v0 + 64, (int)rb);
       for (int bx = 0; bx < nbox; ++bx)
-        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, &loaded[stage], j0 + bx * 64, rrow);
+        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, &loaded[stage], j0 + bx * 64, (int)rb);
+      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, &loaded[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
   } else if (lane == 1 && nkb > 0) {
@@ -402,17 +402,18 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
 // ======================================================================= host
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
                              cudaStream_t st) {
-  CUtensorMap tp, tw;
+  CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
     attr = true;
   }
-  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, dpre};
+  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, dpre};
   dim3 grid((unsigned)((d.rows() + jdh::BM - 1) / jdh::BM), (d.J + jdh::MAXN - 1) / jdh::MAXN);
-  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, p));
+  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   return cudaGetLastError();
 }
 

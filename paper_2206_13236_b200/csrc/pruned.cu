@@ -26,11 +26,10 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
                               const uint16_t* b, cudaStream_t st);
 struct GradSrc {
   const uint16_t* Pt;
-  const float *sc, *gb, *gl;
+  const float4* gpk;
   const int32_t* rowinfo;
   long long R;
   int V, VP, ntile;
-  float gs;
 };
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
                              cudaStream_t st);
@@ -276,16 +275,18 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
                                       const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
                                       int N, int T, int S, int K, int ntile, float gs, float* __restrict__ gb,
-                                      float* __restrict__ gl, float* __restrict__ sc) {
+                                      float* __restrict__ gl, float4* __restrict__ gpk) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (long long)N * T * S) return;
+  const long long R = (long long)N * T * S;
+  if (r >= R) return;
   const int s = (int)(r % S);
   const long long nt = r / S;
   const int t = (int)(nt % T), n = (int)(nt / T);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   float yb = 0.f, bb = 0.f;
   const double L2 = Lp[n] * RNNT_LOG2E;
-  if (rowinfo[r] >= 0 && isfinite(L2)) {
+  const int info = rowinfo[r];
+  if (info >= 0 && isfinite(L2)) {
     const int p = ranges[(size_t)n * T + t];
     const int u = p + s, k = t + u;
     const float* A = Aps + (size_t)n * (K + 1);
@@ -302,9 +303,14 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   }
   gb[r] = bb;
   gl[r] = yb;
+  // packed per (V tile, row) operand scalars of the joiner backward (joiner_bwd.cu):
+  // {gs (g_b + g_l) exp(m_tile - lse), gs g_b, gs g_l, label}; dead rows {0, 0, 0, -1}
   const float l = lse[r];
-  for (int tl = 0; tl < ntile; ++tl)
-    sc[r * ntile + tl] = (rowinfo[r] >= 0) ? gs * (bb + yb) * expf(mt[r * ntile + tl] - l) : 0.f;
+  for (int tl = 0; tl < ntile; ++tl) {
+    float4 q = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+    if (info >= 0) q = make_float4(gs * (bb + yb) * expf(mt[r * ntile + tl] - l), gs * bb, gs * yb, __int_as_float(info));
+    gpk[(size_t)tl * R + r] = q;
+  }
 }
 
 // d_enc[n,t,:] = sum_s dpre[n,t,s,:]: one CTA per frame, float4 over j.
@@ -328,9 +334,11 @@ __global__ void __launch_bounds__(128) denc_kernel(const float* __restrict__ dpr
 }
 
 // d_dec[n,u,:] = sum_{t in [lo(u), hi(u))} dpre[n,t,u-p_t,:], summed in t order (deterministic).
+// The covering frames' row offsets are staged in smem first so the dpre loads are independent.
 __global__ void __launch_bounds__(128) ddec_kernel(const float* __restrict__ dpre, const int32_t* __restrict__ ranges,
                                                    const int2* __restrict__ urange, const int64_t* __restrict__ bnd,
                                                    int T, int U, int S, int J, float* __restrict__ d_dec) {
+  __shared__ int srow[256];
   const long long nu = blockIdx.x;
   const int u = (int)(nu % (U + 1)), n = (int)(nu / (U + 1));
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
@@ -343,13 +351,36 @@ __global__ void __launch_bounds__(128) ddec_kernel(const float* __restrict__ dpr
   const int J4 = J / 4;
   const int32_t* p = ranges + (size_t)n * T;
   float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
-  for (int j = threadIdx.x; j < J4; j += blockDim.x) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int t = lo; t < hi; ++t) {
-      const float4 v = reinterpret_cast<const float4*>(dpre + (((size_t)n * T + t) * S + (u - p[t])) * J)[j];
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  float4 acc[4];
+  for (int jb = 0; jb < J4; jb += 4 * blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t0 = lo; t0 < hi; t0 += 256) {
+      const int m = min(256, hi - t0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int t = t0 + i;
+        srow[i] = (int)((((size_t)n * T + t) * S + (u - p[t])));   // band row of (t, u)
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int i = 0; i < m; ++i) {
+        const float4* src = reinterpret_cast<const float4*>(dpre + (size_t)srow[i] * J);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = jb + threadIdx.x + q * blockDim.x;
+          if (j < J4) {
+            const float4 v = src[j];
+            acc[q].x += v.x; acc[q].y += v.y; acc[q].z += v.z; acc[q].w += v.w;
+          }
+        }
+      }
     }
-    dst[j] = acc;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = jb + threadIdx.x + q * blockDim.x;
+      if (j < J4) dst[j] = acc[q];
+    }
   }
 }
 
@@ -392,8 +423,8 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   }
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
       w.px2, w.py2, w.ap, w.bp, w.Aps, w.Bps, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, d.K(), nt,
-      gs, w.gb, w.gl, w.sc));
-  GradSrc g{w.Pt, w.sc, w.gb, w.gl, w.rowinfo, R, d.V, d.VP(), nt, gs};
+      gs, w.gb, w.gl, w.gpk));
+  GradSrc g{w.Pt, w.gpk, w.rowinfo, R, d.V, d.VP(), nt};
   if (d_enc || d_dec) {
     if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
     if (d_enc)

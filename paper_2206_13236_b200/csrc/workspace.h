@@ -79,7 +79,7 @@ struct PrunedWS {
   double* Lp;        // (N) L_pruned
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
-  float* sc;         // (R,ntile) gs*(gb+gl)*exp(m_tile-lse)
+  float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
   float* dpre;       // (R,J) fp32
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
@@ -152,7 +152,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.Lp = (double*)take(N * 8);
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);
-  p.sc = (float*)take(R * NT * 4);
+  p.gpk = (float4*)take(R * NT * 16);
   p.dpre = (float*)take(R * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);

@@ -114,6 +114,22 @@ rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* 
                                size_t workspace_bytes, void* stream);
 
 /*
+ * The am/lm gradients of rnnt_simple_loss as a separate call, so that a caller can run them on a
+ * second stream concurrently with rnnt_get_ranges / rnnt_prune / rnnt_pruned_loss (they depend on
+ * nothing downstream).  Precondition: rnnt_simple_loss was enqueued earlier, in stream order, with
+ * the same dims and workspace (it leaves the normaliser operands and G~ = (y'+empty')/S in the
+ * simple-loss region of the workspace, which rnnt_pruned_loss never touches), and px_grad /
+ * py_grad are its outputs.  rnnt_simple_loss(..., am_grad = lm_grad = NULL, ...) followed by this
+ * call computes exactly what rnnt_simple_loss with both gradient pointers computes.
+ *   am_grad (N,T,V), lm_grad (N,U+1,V) fp32: grad_scale * d(sum loss)/d(am|lm); one may be NULL.
+ */
+rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const float* px_grad,
+                                        const float* py_grad, const int64_t* symbols,
+                                        const int64_t* boundary, const rnnt_dims_t* dims,
+                                        float grad_scale, float* am_grad, float* lm_grad,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Pruning bounds.  For every frame t < T_n:
  *   raw_t = argmax_{p=0..max(0,U_n-S+1)} ( -y'(t,p-1) + sum_{u=p}^{p+S-1} empty'(t,u) )  (Eq. 8)
  * evaluated in fp64 from the fp32 inputs in a fixed order (u ascending, then the

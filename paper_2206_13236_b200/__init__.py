@@ -63,6 +63,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_version.restype = ctypes.c_char_p
     lib.rnnt_simple_loss.argtypes = [P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
     lib.rnnt_simple_loss.restype = I32
+    lib.rnnt_simple_loss_backward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
+    lib.rnnt_simple_loss_backward.restype = I32
     lib.rnnt_get_ranges.argtypes = [P, P, P, DP, P, P, P]
     lib.rnnt_get_ranges.restype = I32
     lib.rnnt_prune.argtypes = [P, P, P, P, DP, P, P]
@@ -152,6 +154,15 @@ def rnnt_simple_loss(am, lm, symbols, boundary, dims, grad_scale, loss, px_grad,
     _check(rc, "rnnt_simple_loss")
 
 
+def rnnt_simple_loss_backward(am, lm, px_grad, py_grad, symbols, boundary, dims, grad_scale, am_grad, lm_grad,
+                              workspace, stream=None):
+    rc = load_library().rnnt_simple_loss_backward(
+        _ptr(am), _ptr(lm), _ptr(px_grad), _ptr(py_grad), _ptr(symbols), _ptr(boundary), ctypes.byref(dims),
+        float(grad_scale), _ptr(am_grad), _ptr(lm_grad), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream(stream))
+    _check(rc, "rnnt_simple_loss_backward")
+
+
 def rnnt_get_ranges(px_grad, py_grad, boundary, dims, ranges, status, stream=None):
     rc = load_library().rnnt_get_ranges(_ptr(px_grad), _ptr(py_grad), _ptr(boundary), ctypes.byref(dims),
                                         _ptr(ranges), _ptr(status), _stream(stream))
@@ -200,23 +211,48 @@ def dims_of(am, lm, w_out, S) -> Dims:
     return make_dims(N, T, U, V, J, S)
 
 
+_SIDE = {}
+
+
+def _side_stream(device):
+    key = torch.device(device).index
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
-         pruned_scale=1.0, status=None, workspace=None, out=None, stream=None):
+         pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True):
     """One fwd+bwd of the whole hot path: simple loss and its
     gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
-    device tensors; ``out`` may supply preallocated outputs (same keys)."""
+    device tensors; ``out`` may supply preallocated outputs (same keys).
+
+    With ``overlap`` the am/lm gradients (rnnt_simple_loss_backward) run on a side stream
+    concurrently with the pruned stage, joined back into ``stream`` before returning."""
     dims = dims_of(am, lm, w_out, S)
-    N, T, U, V, J = dims.N, dims.T, dims.U, dims.V, dims.J
     dev = am.device
     o = out if out is not None else alloc_outputs(dims, dev)
     ws = workspace if workspace is not None else _WS.get(dims, dev)
     st = o["status"] if status is None else status
-    rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
-                     o["py_grad"], o["am_grad"], o["lm_grad"], st, ws, stream)
-    rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, stream)
-    rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], stream)
+    cur = stream if stream is not None else torch.cuda.current_stream(dev)
+    if overlap:
+        rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
+                         o["py_grad"], None, None, st, ws, cur)
+        side = _side_stream(dev)
+        side.wait_stream(cur)
+        rnnt_simple_loss_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims, simple_scale,
+                                  o["am_grad"], o["lm_grad"], ws, side)
+    else:
+        rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
+                         o["py_grad"], o["am_grad"], o["lm_grad"], st, ws, cur)
+    rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
+    rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], cur)
     rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
-                     o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, stream)
+                     o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)
+    if overlap:
+        cur.wait_stream(side)
+        for t in (am, lm, o["px_grad"], o["py_grad"], o["am_grad"], o["lm_grad"], ws, symbols, boundary):
+            t.record_stream(side)
     return o
 
 

@@ -16,6 +16,9 @@ cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* 
                               int32_t* ranges, int32_t* status, cudaStream_t st);
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st);
+cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
+                                const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
+                                float gs, float* am_grad, float* lm_grad, cudaStream_t st);
 size_t pruned_recursion_smem(const Dims& d);
 cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                const uint16_t* b, const int64_t* sym, const int32_t* ranges,
@@ -120,6 +123,25 @@ rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* 
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(simple_loss_launch(d, sw, am, lm, symbols, boundary, grad_scale, loss, px_grad, py_grad,
                                         am_grad, lm_grad, status, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const float* px_grad,
+                                        const float* py_grad, const int64_t* symbols, const int64_t* boundary,
+                                        const rnnt_dims_t* dims, float grad_scale, float* am_grad, float* lm_grad,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!am || !lm || !px_grad || !py_grad || !boundary || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (!am_grad && !lm_grad) return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(am) || !aligned16(lm) || !aligned16(am_grad) || !aligned16(lm_grad)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(simple_grads_launch(d, sw, am, lm, px_grad, py_grad, symbols, boundary, grad_scale, am_grad,
+                                         lm_grad, (cudaStream_t)stream));
 }
 
 rnnt_status_t rnnt_get_ranges(const float* px_grad, const float* py_grad, const int64_t* boundary,

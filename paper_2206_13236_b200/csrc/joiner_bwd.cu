@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
                         const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
   using namespace jdh;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = tc::align1024(smem_raw);
   uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
                         JoinerDwParams p) {
   using namespace jdw;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = tc::align1024(smem_raw);
   uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;

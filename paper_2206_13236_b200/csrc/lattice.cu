@@ -54,18 +54,17 @@ inline size_t smem_bytes(int W) {
 }  // namespace lat
 
 // ------------------------------------------------------------------ sentinel fill
+// grid (K+1 rows, N), threads over the row's LU columns: cell (k, u) holds (t = k - u, u).
 __global__ void skew_fill_kernel(const int64_t* __restrict__ bnd, int LU, int K, float* __restrict__ px2,
                                  float* __restrict__ py2) {
-  const int n = blockIdx.y;
-  const long long cells = (long long)(K + 1) * LU;
+  const int k = blockIdx.x, n = blockIdx.y;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  const size_t base = (size_t)n * cells;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(i / LU), u = (int)(i - (long long)k * LU), t = k - u;
+  const size_t base = ((size_t)n * (K + 1) + k) * LU;
+  for (int u = threadIdx.x; u < LU; u += blockDim.x) {
+    const int t = k - u;
     if (!(t >= 0 && t < Tn && u <= Un)) {
-      px2[base + i] = kNegBig;
-      py2[base + i] = kNegBig;
+      px2[base + u] = kNegBig;
+      py2[base + u] = kNegBig;
     }
   }
 }
@@ -427,9 +426,8 @@ static cudaError_t launch_fb_w(const Dims& d, const SimpleWS& w, const int64_t* 
 }
 
 cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st) {
-  const long long cells = (long long)(d.K() + 1) * d.LU();
-  const unsigned bx = (unsigned)std::min<long long>((cells + 255) / 256, 64);
-  RNNT_LAUNCH(KID_SKEW_FILL, st, skew_fill_kernel<<<dim3(bx, d.N), 256, 0, st>>>(bnd, d.LU(), d.K(), w.px2, w.py2));
+  RNNT_LAUNCH(KID_SKEW_FILL, st, skew_fill_kernel<<<dim3(d.K() + 1, d.N), std::min(d.LU(), 256), 0, st>>>(
+      bnd, d.LU(), d.K(), w.px2, w.py2));
   return cudaGetLastError();
 }
 

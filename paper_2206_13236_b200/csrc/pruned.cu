@@ -37,41 +37,38 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                              int splits, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
-// One thread per 8 consecutive j of one band row (16 B of bf16 out).
-__global__ void prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
-                             const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
-                             int N, int T, int U, int J, int S, uint16_t* __restrict__ h) {
-  const int J8 = J / 8;
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long R = (long long)N * T * S;
-  if (i >= R * J8) return;
-  const long long r = i / J8;
-  const int j0 = (int)(i % J8) * 8;
-  const int s = (int)(r % S);
-  const long long nt = r / S;
-  const int t = (int)(nt % T), n = (int)(nt / T);
+// One CTA per frame (n, t); threads over (slot s, 8-column group) of its S band rows: 16 B of
+// bf16 out per thread (enc[t] is read once per frame and reused from L1 across the S rows).
+__global__ void __launch_bounds__(256) prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
+                                                    const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
+                                                    int T, int U, int J, int S, uint16_t* __restrict__ h) {
+  const int nt = blockIdx.x;
+  const int n = nt / T, t = nt - n * T;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  uint4 out = make_uint4(0, 0, 0, 0);
-  if (t < Tn) {
-    const int u = ranges[(size_t)n * T + t] + s;
-    if (u <= Un) {
-      const float* e = enc + ((size_t)n * T + t) * J + j0;
+  const int J8 = J / 8;
+  const int p = t < Tn ? ranges[(size_t)n * T + t] : 0;
+  const float* e = enc + (size_t)nt * J;
+  for (int idx = threadIdx.x; idx < S * J8; idx += blockDim.x) {
+    const int s = idx / J8, j0 = (idx - s * J8) * 8;
+    const int u = p + s;
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (t < Tn && u <= Un) {
       const float* d = dec + ((size_t)n * (U + 1) + u) * J + j0;
-      float4 e0 = *reinterpret_cast<const float4*>(e), e1 = *reinterpret_cast<const float4*>(e + 4);
-      float4 d0 = *reinterpret_cast<const float4*>(d), d1 = *reinterpret_cast<const float4*>(d + 4);
-      float x[8] = {e0.x + d0.x, e0.y + d0.y, e0.z + d0.z, e0.w + d0.w,
-                    e1.x + d1.x, e1.y + d1.y, e1.z + d1.z, e1.w + d1.w};
+      const float4 e0 = *reinterpret_cast<const float4*>(e + j0), e1 = *reinterpret_cast<const float4*>(e + j0 + 4);
+      const float4 d0 = *reinterpret_cast<const float4*>(d), d1 = *reinterpret_cast<const float4*>(d + 4);
+      const float x[8] = {e0.x + d0.x, e0.y + d0.y, e0.z + d0.z, e0.w + d0.w,
+                          e1.x + d1.x, e1.y + d1.y, e1.z + d1.z, e1.w + d1.w};
       uint32_t w[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint32_t lo = f_to_bf16_bits_rn(tanhf(x[2 * q]));
-        uint32_t hi = f_to_bf16_bits_rn(tanhf(x[2 * q + 1]));
+        const uint32_t lo = f_to_bf16_bits_rn(tanh_fast(x[2 * q]));
+        const uint32_t hi = f_to_bf16_bits_rn(tanh_fast(x[2 * q + 1]));
         w[q] = lo | (hi << 16);
       }
       out = make_uint4(w[0], w[1], w[2], w[3]);
     }
+    *reinterpret_cast<uint4*>(h + ((size_t)nt * S + s) * J + j0) = out;
   }
-  *reinterpret_cast<uint4*>(h + r * J + j0) = out;
 }
 
 __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t* __restrict__ sym,
@@ -396,9 +393,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, 
 // ------------------------------------------------------------------ host drivers
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st) {
-  long long work = d.rows() * (d.J / 8);
-  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(enc, dec, ranges, bnd, d.N, d.T, d.U, d.J,
-                                                                 d.S, h));
+  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((long long)d.N * d.T), 256, 0, st>>>(enc, dec, ranges, bnd, d.T, d.U,
+                                                                                      d.J, d.S, h));
   return cudaGetLastError();
 }
 

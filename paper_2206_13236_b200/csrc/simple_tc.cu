@@ -149,7 +149,7 @@ template <class P>
 __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_constant__ Maps mp, P p) {
   using namespace sg;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = tc::align1024(smem_raw);
   uint8_t* aux = smem + STAGES * STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(aux + AUX_BYTES);
   uint64_t* empty = full + STAGES;

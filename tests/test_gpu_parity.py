@@ -176,3 +176,28 @@ def test_end_to_end_step_config2():
             same.append(n)
     assert len(same) > 0
     assert_loss(g["loss_pruned"][same], ref["loss_pruned"][same], "loss_pruned")
+
+
+def test_simple_backward_split_matches():
+    """rnnt_simple_loss(grads=NULL) + rnnt_simple_loss_backward on a side stream gives bit-identical
+    am/lm gradients to rnnt_simple_loss with both gradient pointers (include/rnnt.h)."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    dev = to_dev(b)
+    d = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
+    ws = torch.empty(R.rnnt_workspace_bytes(d), dtype=torch.uint8, device="cuda")
+    o1 = R.alloc_outputs(d, "cuda")
+    R.rnnt_simple_loss(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], d, 0.5, o1["loss_simple"], o1["px_grad"],
+                       o1["py_grad"], o1["am_grad"], o1["lm_grad"], o1["status"], ws)
+    o2 = R.alloc_outputs(d, "cuda")
+    R.rnnt_simple_loss(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], d, 0.5, o2["loss_simple"], o2["px_grad"],
+                       o2["py_grad"], None, None, o2["status"], ws)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    R.rnnt_simple_loss_backward(dev["am"], dev["lm"], o2["px_grad"], o2["py_grad"], dev["symbols"], dev["boundary"], d,
+                                0.5, o2["am_grad"], o2["lm_grad"], ws, side)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    for k in ("loss_simple", "px_grad", "py_grad", "am_grad", "lm_grad"):
+        assert torch.equal(o1[k], o2[k]), k

@@ -172,6 +172,30 @@ rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const u
                                int32_t* status, void* workspace, size_t workspace_bytes,
                                void* stream);
 
+/*
+ * rnnt_pruned_loss as three calls (forward, backward to the joiner input, backward to the joiner
+ * weights), so that the two backward halves — which only read what the forward left in the
+ * pruned-loss region of the workspace and write disjoint outputs — can run on two streams.
+ * In stream order: forward, then backward_input and backward_weight (in either order or
+ * concurrently); together they compute exactly what rnnt_pruned_loss computes.
+ *   rnnt_pruned_loss_forward:          loss (N), status; leaves P~, the tile maxima and the
+ *                                      occupancies (times grad_scale) in the workspace.
+ *   rnnt_pruned_loss_backward_input:   d_enc (N,T,J) and/or d_dec (N,U+1,J) (one may be NULL).
+ *   rnnt_pruned_loss_backward_weight:  d_w (V,J), d_b (V).
+ */
+rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                                       const int64_t* symbols, const int32_t* ranges,
+                                       const int64_t* boundary, const rnnt_dims_t* dims,
+                                       float grad_scale, float* loss, int32_t* status, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+rnnt_status_t rnnt_pruned_loss_backward_input(const uint16_t* h, const uint16_t* w_out,
+                                              const int32_t* ranges, const int64_t* boundary,
+                                              const rnnt_dims_t* dims, float* d_enc, float* d_dec,
+                                              void* workspace, size_t workspace_bytes, void* stream);
+rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dims_t* dims, float* d_w,
+                                               float* d_b, void* workspace, size_t workspace_bytes,
+                                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_prune.restype = I32
     lib.rnnt_pruned_loss.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
     lib.rnnt_pruned_loss.restype = I32
+    lib.rnnt_pruned_loss_forward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
+    lib.rnnt_pruned_loss_forward.restype = I32
+    lib.rnnt_pruned_loss_backward_input.argtypes = [P, P, P, P, DP, P, P, P, SZ, P]
+    lib.rnnt_pruned_loss_backward_input.restype = I32
+    lib.rnnt_pruned_loss_backward_weight.argtypes = [P, DP, P, P, P, SZ, P]
+    lib.rnnt_pruned_loss_backward_weight.restype = I32
     lib.rnnt_launch_count.argtypes = []
     lib.rnnt_launch_count.restype = ctypes.c_uint64
     lib.rnnt_kernel_count.argtypes = []
@@ -185,6 +191,29 @@ def rnnt_pruned_loss(h, w_out, b_out, symbols, ranges, boundary, dims, grad_scal
     _check(rc, "rnnt_pruned_loss")
 
 
+def rnnt_pruned_loss_forward(h, w_out, b_out, symbols, ranges, boundary, dims, grad_scale, loss, status, workspace,
+                             stream=None):
+    rc = load_library().rnnt_pruned_loss_forward(
+        _ptr(h), _ptr(w_out), _ptr(b_out), _ptr(symbols), _ptr(ranges), _ptr(boundary), ctypes.byref(dims),
+        float(grad_scale), _ptr(loss), _ptr(status), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream(stream))
+    _check(rc, "rnnt_pruned_loss_forward")
+
+
+def rnnt_pruned_loss_backward_input(h, w_out, ranges, boundary, dims, d_enc, d_dec, workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss_backward_input(
+        _ptr(h), _ptr(w_out), _ptr(ranges), _ptr(boundary), ctypes.byref(dims), _ptr(d_enc), _ptr(d_dec),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_pruned_loss_backward_input")
+
+
+def rnnt_pruned_loss_backward_weight(h, dims, d_w, d_b, workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss_backward_weight(
+        _ptr(h), ctypes.byref(dims), _ptr(d_w), _ptr(d_b), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream(stream))
+    _check(rc, "rnnt_pruned_loss_backward_weight")
+
+
 # ----------------------------------------------------------------- conveniences
 class Workspace:
     """Caches one device workspace per (device, size)."""
@@ -214,8 +243,8 @@ def dims_of(am, lm, w_out, S) -> Dims:
 _SIDE = {}
 
 
-def _side_stream(device):
-    key = torch.device(device).index
+def _side_stream(device, which=0):
+    key = (torch.device(device).index, which)
     if key not in _SIDE:
         _SIDE[key] = torch.cuda.Stream(device=device)
     return _SIDE[key]
@@ -247,12 +276,22 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
                          o["py_grad"], o["am_grad"], o["lm_grad"], st, ws, cur)
     rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
     rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], cur)
-    rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
-                     o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)
     if overlap:
+        rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
+                                 o["loss_pruned"], st, ws, cur)
+        side2 = _side_stream(dev, 1)
+        side2.wait_stream(cur)
+        rnnt_pruned_loss_backward_weight(o["h"], dims, o["d_w"], o["d_b"], ws, side2)
+        rnnt_pruned_loss_backward_input(o["h"], w_out, o["ranges"], boundary, dims, o["d_enc"], o["d_dec"], ws, cur)
         cur.wait_stream(side)
+        cur.wait_stream(side2)
         for t in (am, lm, o["px_grad"], o["py_grad"], o["am_grad"], o["lm_grad"], ws, symbols, boundary):
             t.record_stream(side)
+        for t in (o["h"], o["d_w"], o["d_b"], ws):
+            t.record_stream(side2)
+    else:
+        rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
+                         o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)
     return o
 
 

@@ -20,6 +20,14 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
                                 float gs, float* am_grad, float* lm_grad, cudaStream_t st);
 size_t pruned_recursion_smem(const Dims& d);
+cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                              const uint16_t* b, const int64_t* sym, const int32_t* ranges, const int64_t* bnd,
+                              float gs, float* loss, int32_t* status, cudaStream_t st);
+cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                                    const int32_t* ranges, const int64_t* bnd, float* d_enc, float* d_dec,
+                                    cudaStream_t st);
+cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
+                                     cudaStream_t st);
 cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                const uint16_t* b, const int64_t* sym, const int32_t* ranges,
                                const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
@@ -183,6 +191,54 @@ rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const u
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_loss_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss,
                                         d_enc, d_dec, d_w, d_b, status, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                                       const int64_t* symbols, const int32_t* ranges, const int64_t* boundary,
+                                       const rnnt_dims_t* dims, float grad_scale, float* loss, int32_t* status,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!h || !w_out || !b_out || !ranges || !boundary || !loss || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(w_out)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  if (pruned_recursion_smem(d) > 200 * 1024) return RNNT_ERR_UNSUPPORTED;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_fwd_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss, status,
+                                       (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_pruned_loss_backward_input(const uint16_t* h, const uint16_t* w_out, const int32_t* ranges,
+                                              const int64_t* boundary, const rnnt_dims_t* dims, float* d_enc,
+                                              float* d_dec, void* workspace, size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!h || !w_out || !ranges || !boundary || !workspace || (!d_enc && !d_dec)) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(w_out) || !aligned16(d_enc) || !aligned16(d_dec)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_bwd_input_launch(d, pw, h, w_out, ranges, boundary, d_enc, d_dec, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dims_t* dims, float* d_w, float* d_b,
+                                               void* workspace, size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!h || !d_w || !d_b || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(d_w)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream));
 }
 
 }  // extern "C"

@@ -400,10 +400,11 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
 
 size_t pruned_recursion_smem(const Dims& d) { return (size_t)d.T * 4 + (size_t)(d.K() + 1) * 4 + (size_t)d.T * d.S * 8; }
 
-cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
-                               const uint16_t* b, const int64_t* sym, const int32_t* ranges,
-                               const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
-                               float* d_w, float* d_b, int32_t* status, cudaStream_t st) {
+// Forward: per-row info, K8 joiner with fused log-softmax, K9 recursion, the occupancies and the
+// packed backward scalars.
+cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                              const uint16_t* b, const int64_t* sym, const int32_t* ranges, const int64_t* bnd,
+                              float gs, float* loss, int32_t* status, cudaStream_t st) {
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
@@ -420,22 +421,45 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
       w.px2, w.py2, w.ap, w.bp, w.Aps, w.Bps, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, d.K(), nt,
       gs, w.gb, w.gl, w.gpk));
-  GradSrc g{w.Pt, w.gpk, w.rowinfo, R, d.V, d.VP(), nt};
-  if (d_enc || d_dec) {
-    if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
-    if (d_enc)
-      RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((long long)d.N * d.T), 128, 0, st>>>(w.dpre, bnd, d.T, d.S, d.J, d_enc));
-    if (d_dec)
-      RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(w.dpre, ranges, w.urange, bnd, d.T,
-                                                                                          d.U, d.S, d.J, d_dec));
-  }
-  {
-    if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
-    long long M = (long long)d.V * d.J;
-    RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w));
-    RNNT_LAUNCH(KID_DB_REDUCE, st, split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b));
-  }
   return cudaGetLastError();
+}
+
+// Backward to the joiner input: K10 dh (and dpre), then d_enc / d_dec reductions.
+cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                                    const int32_t* ranges, const int64_t* bnd, float* d_enc, float* d_dec,
+                                    cudaStream_t st) {
+  cudaError_t e;
+  GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
+  if (!d_enc && !d_dec) return cudaSuccess;
+  if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
+  if (d_enc)
+    RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((long long)d.N * d.T), 128, 0, st>>>(w.dpre, bnd, d.T, d.S, d.J, d_enc));
+  if (d_dec)
+    RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(w.dpre, ranges, w.urange, bnd, d.T,
+                                                                                        d.U, d.S, d.J, d_dec));
+  return cudaGetLastError();
+}
+
+// Backward to the joiner weights: K11 dW (split-K) + db, deterministic split reduction.
+cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
+                                     cudaStream_t st) {
+  cudaError_t e;
+  GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
+  if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
+  const long long M = (long long)d.V * d.J;
+  RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w));
+  RNNT_LAUNCH(KID_DB_REDUCE, st, split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b));
+  return cudaGetLastError();
+}
+
+cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
+                               const uint16_t* b, const int64_t* sym, const int32_t* ranges,
+                               const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
+                               float* d_w, float* d_b, int32_t* status, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = pruned_fwd_launch(d, w, h, W, b, sym, ranges, bnd, gs, loss, status, st)) != cudaSuccess) return e;
+  if ((e = pruned_bwd_input_launch(d, w, h, W, ranges, bnd, d_enc, d_dec, st)) != cudaSuccess) return e;
+  return pruned_bwd_weight_launch(d, w, h, d_w, d_b, st);
 }
 
 }  // namespace rnnt

@@ -67,6 +67,14 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 }
 
 // ======================================================================= K10
+// Frame-aligned row tiles: tile i holds the F = floor(128/S) frames [iF, iF+F) of the flattened
+// (n, t) frame index, i.e. rows [iFS, iFS + FS) (the MMA computes 128 rows; the rest is ignored).
+// The epilogue forms dpre = dh (1 - h^2) for a 32-column chunk in smem and reduces it there:
+//   d_enc[n,t,:] = sum_s dpre[(n,t,s),:]                                      (complete in the tile)
+//   d_dec[n,u,:] = sum over band rows (t, s) with p_t + s = u of dpre         (frames covering u are
+//   contiguous, Eq. 9; u whose covering frames all lie in the tile are written directly, the <= S
+//   u at each end of a tile's utterance segment go to a boundary-partial buffer that
+//   ddec_fixup_kernel sums in tile order: deterministic, and dpre never leaves the SM).
 namespace jdh {
 constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 512, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
@@ -74,14 +82,29 @@ constexpr int B_BYTES = MAXN * BK * 2;         // 64 KB, MN-major (8 boxes of 64
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
 constexpr int H_BYTES = BM * 64 * 2;           // 16 KB: one 64-column box of h for the epilogue
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int D_OFF = 8 * H_BYTES;             // dpre staging block [128][32] fp32 after the h boxes
+constexpr int MAXSEG = 128;
+constexpr int TAB_BYTES = 4 * 128 + MAXSEG * 8 * 4 + 4 * 128 + 16 + 128 * 16 + 3 * 4 * 128;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + TAB_BYTES;
 constexpr int THREADS = 160;
 }  // namespace jdh
 
 struct JoinerDhParams {
   GradSrc g;
   int J, nkb;
-  float* dpre;
+  int N, T, U, S, F;
+  const int32_t* ranges;   // (N,T) p_t
+  const int2* urange;      // (N,U+1) frames [lo, hi) covering u
+  const int64_t* bnd;
+  float* d_enc;            // (N,T,J) nullable
+  float* d_dec;            // (N,U+1,J) nullable
+  float* part;             // (ntiles, 2, S, J) boundary partials of d_dec
+};
+
+// per-tile utterance segment: live frames f in [fb, fe) of utterance n, token positions [ub, ue],
+// its entries e in [off, off + ue - ub + 1); pnext = p at the frame after the segment (if covered)
+struct Seg {
+  int n, fb, fe, ub, ue, off, pnext, ta;
 };
 
 __global__ void __launch_bounds__(jdh::THREADS, 1)
@@ -96,25 +119,55 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* hfull = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 1);
+  int* sp = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);   // [128] p of tile frames (-1 dead)
+  Seg* seg = reinterpret_cast<Seg*>(sp + 128);                          // [MAXSEG]
+  uint8_t* eseg = reinterpret_cast<uint8_t*>(seg + MAXSEG);             // [128] segment of entry e
+  int* nseg_ent = reinterpret_cast<int*>(eseg + 128);                   // {#segments, #entries}
+  int4* ent = reinterpret_cast<int4*>(nseg_ent + 4);                   // [128] {fl, fh, u, dst row}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long m0 = (long long)blockIdx.x * BM;
+  const int S = p.S, F = p.F, RT = F * S;
+  const long long g0 = (long long)blockIdx.x * F;                      // first flattened frame
+  const long long m0 = g0 * S;                                          // first row
+  const long long NT = (long long)p.N * p.T;
   const int j0 = blockIdx.y * MAXN;
   const int nj = min(MAXN, p.J - j0);               // columns of this CTA
   const int nsub = (nj + NSUB - 1) / NSUB;
   const int nbox = (nj + 63) / 64;
 
+  // ---- per-frame tables of the tile (parallel global loads): p_t (dead = -1), p_{t+1}, n, t
+  int* spn = reinterpret_cast<int*>(ent + 128);                          // [128] p_{t+1}
+  int* sfn = spn + 128;                                                  // [128] utterance n
+  int* sft = sfn + 128;                                                  // [128] frame t
+  if (threadIdx.x < F) {
+    const long long g = g0 + threadIdx.x;
+    int pv = -1, pn = 0, n = -1, t = 0;
+    if (g < NT) {
+      n = (int)(g / p.T);
+      t = (int)(g - (long long)n * p.T);
+      const int Tn = utt_T(p.bnd, n), Un = utt_U(p.bnd, n);
+      if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) {
+        pv = p.ranges[(size_t)n * p.T + t];
+        if (t + 1 < Tn) pn = p.ranges[(size_t)n * p.T + t + 1];
+      }
+    }
+    sp[threadIdx.x] = pv;
+    spn[threadIdx.x] = pn;
+    sfn[threadIdx.x] = n;
+    sft[threadIdx.x] = t;
+  }
   int act = 0;
-  for (int i = threadIdx.x; i < BM; i += blockDim.x)
+  for (int i = threadIdx.x; i < RT; i += blockDim.x)
     if (m0 + i < p.g.R && p.g.rowinfo[m0 + i] >= 0) act = 1;
   const bool any = __syncthreads_or(act);
+
   if (!any) {
-    // tile entirely masked: dpre rows are zero
-    for (int i = threadIdx.x; i < BM; i += blockDim.x) {
-      const long long r = m0 + i;
-      if (r >= p.g.R) break;
-      float4* o = reinterpret_cast<float4*>(p.dpre + (size_t)r * p.J + j0);
-      for (int j = 0; j < nj / 4; ++j) o[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    // no live row: d_enc of the tile's frames is zero (d_dec gets nothing from this tile)
+    if (p.d_enc)
+      for (int idx = threadIdx.x; idx < F * (nj / 4); idx += blockDim.x) {
+        const int f = idx / (nj / 4), jq = idx - f * (nj / 4);
+        if (g0 + f < NT)
+          reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0)[jq] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     return;
   }
   if (warp == 4 && lane == 0) {
@@ -147,8 +200,8 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       const int v0 = kb * BK;
       tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
-      const float4 gq = rl < grows ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
-                                   : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+      const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
+                                                : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
       const int info = __float_as_int(gq.w);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -161,37 +214,113 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       if (lane == 0) tc::mbar_arrive(&full[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
-    // ---- epilogue: dpre = dh * (1 - h^2), h from the TMA tiles loaded after the mainloop
+    // ---- tile tables (while the last MMAs drain): utterance segments from the per-frame smem
+    // tables, then one entry per token position of a segment: covering frames and destination
+    if (threadIdx.x == 0) {
+      int ns = 0, ne = 0;
+      for (int f = 0; f < F;) {
+        if (sp[f] < 0) { ++f; continue; }
+        const int n = sfn[f];
+        int fe = f + 1;
+        while (fe < F && sp[fe] >= 0 && sfn[fe] == n) ++fe;
+        Seg q;
+        q.n = n; q.fb = f; q.fe = fe; q.ta = sft[f];
+        q.ub = sp[f];
+        q.ue = min(utt_U(p.bnd, n), sp[fe - 1] + S - 1);
+        q.off = ne;
+        q.pnext = spn[fe - 1];
+        if (ns < MAXSEG) {
+          seg[ns] = q;
+          for (int e = 0; e <= q.ue - q.ub && ne + e < 128; ++e) eseg[ne + e] = (uint8_t)ns;
+          ++ns;
+          ne += q.ue - q.ub + 1;
+        }
+        f = fe;
+      }
+      nseg_ent[0] = ns;
+      nseg_ent[1] = min(ne, 128);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    //   dst >= 0: row n(U+1)+u of d_dec (complete here); dst < 0: row -(1+dst) of the partial buffer
+    if (threadIdx.x < nseg_ent[1]) {
+      const int e = threadIdx.x;
+      const Seg q = seg[eseg[e]];
+      const int u = q.ub + (e - q.off);
+      const int2 cov = p.urange[(size_t)q.n * (p.U + 1) + u];           // frames [lo, hi) covering u
+      const int fl = max(q.fb, cov.x - q.ta + q.fb), fh = min(q.fe, cov.y - q.ta + q.fb);
+      const int tb = q.ta + (q.fe - q.fb);
+      int dst;
+      if (cov.x >= q.ta && cov.y <= tb) dst = q.n * (p.U + 1) + u;                               // complete here
+      else if (cov.x < q.ta) dst = -1 - (int)((blockIdx.x * 2 + 0) * S + (u - q.ub));          // left boundary
+      else dst = -1 - (int)((blockIdx.x * 2 + 1) * S + (u - q.pnext));                          // right boundary
+      ent[e] = make_int4(fl, fh, u, dst);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    // ---- epilogue
     tc::mbar_wait(tfull, 0);
     tc::fence_after_sync();
     tc::mbar_wait(hfull, 0);
-    const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
+    const bool live = rl < RT && r < p.g.R && p.g.rowinfo[r] >= 0;
     const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
+    // dpre chunk staging: row r, float4 group q (columns 4q..4q+3) at D4[r * 8 + (q ^ (r & 7))]
+    float4* D4 = reinterpret_cast<float4*>(smem + D_OFF);
+    const int nseg = nseg_ent[0], nent = nseg_ent[1];
     for (int c0 = 0; c0 < nj; c0 += 32) {
       float acc[32];
       tc::tmem_ld32(tl + c0, acc);
-      if (r < p.g.R) {
-        float* o = p.dpre + (size_t)r * p.J + j0 + c0;
-        const uint8_t* hb = smem + (c0 >> 6) * H_BYTES;       // 64-column box
-        const int qh = ((c0 >> 5) & 1) * 4;                   // 16-B chunk of the 32-column half
-        const int nq = min(4, (nj - c0) / 8);                 // J % 8 == 0
+      const uint8_t* hb = smem + (c0 >> 6) * H_BYTES;         // 64-column box of h
+      const int qh = ((c0 >> 5) & 1) * 4;                     // 16-B chunk of the 32-column half
+      const int nq = min(4, (nj - c0) / 8);                   // J % 8 == 0
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q >= nq) break;
-          const uint4 hv = live ? *reinterpret_cast<const uint4*>(hb + sw128(rl, qh + q)) : make_uint4(0, 0, 0, 0);
+      for (int q = 0; q < 4; ++q) {
+        float out[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (q < nq && live) {
+          const uint4 hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, qh + q));
           const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
-          float out[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
-            out[2 * i] = live ? acc[8 * q + 2 * i] * (1.f - ha * ha) : 0.f;
-            out[2 * i + 1] = live ? acc[8 * q + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
+            out[2 * i] = acc[8 * q + 2 * i] * (1.f - ha * ha);            // d tanh
+            out[2 * i + 1] = acc[8 * q + 2 * i + 1] * (1.f - hb2 * hb2);
           }
-          reinterpret_cast<float4*>(o)[2 * q] = make_float4(out[0], out[1], out[2], out[3]);
-          reinterpret_cast<float4*>(o)[2 * q + 1] = make_float4(out[4], out[5], out[6], out[7]);
         }
+        D4[rl * 8 + ((2 * q) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
+        D4[rl * 8 + ((2 * q + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
       }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int ncol4 = min(32, nj - c0) / 4;
+      // d_enc: one float4 output per (frame, 4-column group)
+      if (p.d_enc)
+        for (int idx = threadIdx.x; idx < F * 8; idx += 128) {
+          const int f = idx >> 3, q = idx & 7;
+          if (q < ncol4 && g0 + f < NT) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s = 0; s < S; ++s) {
+              const int rr = f * S + s;
+              const float4 x = D4[rr * 8 + (q ^ (rr & 7))];
+              v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+            }
+            reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0 + c0)[q] = v;
+          }
+        }
+      // d_dec: one float4 output per (token position of a segment, 4-column group)
+      if (p.d_dec)
+        for (int idx = threadIdx.x; idx < nent * 8; idx += 128) {
+          const int e = idx >> 3, q = idx & 7;
+          if (q >= ncol4) continue;
+          const int4 en = ent[e];
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int f = en.x; f < en.y; ++f) {
+            const int rr = f * S + (en.z - sp[f]);
+            const float4 x = D4[rr * 8 + (q ^ (rr & 7))];
+            v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+          }
+          float* dst = en.w >= 0 ? p.d_dec + (size_t)en.w * p.J : p.part + (size_t)(-1 - en.w) * p.J;
+          reinterpret_cast<float4*>(dst + j0 + c0)[q] = v;
+        }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
     }
+    (void)nseg;
   } else if (lane == 0) {
     // ---- warp 4 lane 0: TMA for A = P~[m0.., kb*64..], B = W[kb*64.., j0..] and the rows' scalars
     const uint32_t gbytes = (uint32_t)grows * 16u;
@@ -235,6 +364,39 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 4) tc::tmem_dealloc(tbase, 512);
+}
+
+// d_dec for the token positions whose covering frames span several tiles (sum of the boundary
+// partials in tile order), and zeros for u > U_n / infeasible utterances.  Positions complete in
+// one tile were written by joiner_dh_tc_kernel and are left untouched.
+__global__ void __launch_bounds__(128) ddec_fixup_kernel(const int32_t* __restrict__ ranges,
+                                                         const int2* __restrict__ urange,
+                                                         const int64_t* __restrict__ bnd, int T, int U, int S, int F,
+                                                         int J, const float* __restrict__ part,
+                                                         float* __restrict__ d_dec) {
+  const long long nu = blockIdx.x;
+  const int u = (int)(nu % (U + 1)), n = (int)(nu / (U + 1));
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  float* dst = d_dec + (size_t)nu * J;
+  if (u > Un || (long long)Un > (long long)Tn * (S - 1)) {
+    for (int j = threadIdx.x; j < J; j += blockDim.x) dst[j] = 0.f;
+    return;
+  }
+  const int2 cov = urange[nu];
+  const long long gbase = (long long)n * T;
+  const long long k0 = (gbase + cov.x) / F, k1 = (gbase + cov.y - 1) / F;
+  if (k0 == k1) return;
+  const int32_t* pr = ranges + (size_t)n * T;
+  const int tb0 = (int)((k0 + 1) * F - gbase);                     // first frame of tile k0 + 1
+  const float* first = part + (((size_t)k0 * 2 + 1) * S + (u - pr[tb0])) * J;
+  for (int j = threadIdx.x; j < J; j += blockDim.x) {
+    float v = first[j];
+    for (long long k = k0 + 1; k <= k1; ++k) {
+      const int ta = (int)(k * F - gbase);
+      v += part[(((size_t)k * 2 + 0) * S + (u - pr[ta])) * J + j];
+    }
+    dst[j] = v;
+  }
 }
 
 // ======================================================================= K11
@@ -400,8 +562,9 @@ __global__ void __launch_bounds__(jdw::THREADS, 1)
 }
 
 // ======================================================================= host
-cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
-                             cudaStream_t st) {
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
+                             const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
+                             float* d_dec, float* part, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
@@ -411,9 +574,14 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
     attr = true;
   }
-  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, dpre};
-  dim3 grid((unsigned)((d.rows() + jdh::BM - 1) / jdh::BM), (d.J + jdh::MAXN - 1) / jdh::MAXN);
+  const int F = d.dh_frames();
+  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, d.N, d.T, d.U, d.S, F, ranges, urange, bnd, d_enc, d_dec,
+                   part};
+  dim3 grid((unsigned)d.dh_tiles(), (d.J + jdh::MAXN - 1) / jdh::MAXN);
   RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  if (d_dec)
+    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(
+        ranges, urange, bnd, d.T, d.U, d.S, F, d.J, part, d_dec));
   return cudaGetLastError();
 }
 

@@ -31,8 +31,9 @@ struct GradSrc {
   long long R;
   int V, VP, ntile;
 };
-cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, float* dpre,
-                             cudaStream_t st);
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
+                             const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
+                             float* d_dec, float* part, cudaStream_t st);
 cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
                              int splits, cudaStream_t st);
 
@@ -310,77 +311,6 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   }
 }
 
-// d_enc[n,t,:] = sum_s dpre[n,t,s,:]: one CTA per frame, float4 over j.
-__global__ void __launch_bounds__(128) denc_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd,
-                                                   int T, int S, int J, float* __restrict__ d_enc) {
-  const long long nt = blockIdx.x;
-  const int t = (int)(nt % T), n = (int)(nt / T);
-  const bool valid = t < utt_T(bnd, n);
-  const int J4 = J / 4;
-  const float4* src = reinterpret_cast<const float4*>(dpre + (size_t)nt * S * J);
-  float4* dst = reinterpret_cast<float4*>(d_enc + (size_t)nt * J);
-  for (int j = threadIdx.x; j < J4; j += blockDim.x) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid)
-      for (int s = 0; s < S; ++s) {
-        const float4 v = src[(size_t)s * J4 + j];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-    dst[j] = acc;
-  }
-}
-
-// d_dec[n,u,:] = sum_{t in [lo(u), hi(u))} dpre[n,t,u-p_t,:], summed in t order (deterministic).
-// The covering frames' row offsets are staged in smem first so the dpre loads are independent.
-__global__ void __launch_bounds__(128) ddec_kernel(const float* __restrict__ dpre, const int32_t* __restrict__ ranges,
-                                                   const int2* __restrict__ urange, const int64_t* __restrict__ bnd,
-                                                   int T, int U, int S, int J, float* __restrict__ d_dec) {
-  __shared__ int srow[256];
-  const long long nu = blockIdx.x;
-  const int u = (int)(nu % (U + 1)), n = (int)(nu / (U + 1));
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  int lo = 0, hi = 0;
-  if (u <= Un && (long long)Un <= (long long)Tn * (S - 1)) {
-    const int2 r = urange[nu];
-    lo = r.x;
-    hi = r.y;
-  }
-  const int J4 = J / 4;
-  const int32_t* p = ranges + (size_t)n * T;
-  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
-  float4 acc[4];
-  for (int jb = 0; jb < J4; jb += 4 * blockDim.x) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int t0 = lo; t0 < hi; t0 += 256) {
-      const int m = min(256, hi - t0);
-      __syncthreads();
-      for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const int t = t0 + i;
-        srow[i] = (int)((((size_t)n * T + t) * S + (u - p[t])));   // band row of (t, u)
-      }
-      __syncthreads();
-#pragma unroll 4
-      for (int i = 0; i < m; ++i) {
-        const float4* src = reinterpret_cast<const float4*>(dpre + (size_t)srow[i] * J);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = jb + threadIdx.x + q * blockDim.x;
-          if (j < J4) {
-            const float4 v = src[j];
-            acc[q].x += v.x; acc[q].y += v.y; acc[q].z += v.z; acc[q].w += v.w;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = jb + threadIdx.x + q * blockDim.x;
-      if (j < J4) dst[j] = acc[q];
-    }
-  }
-}
-
 __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, long long M,
                                     float* __restrict__ out) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -431,12 +361,7 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
-  if ((e = joiner_dh_launch(d, g, h, W, w.dpre, st)) != cudaSuccess) return e;
-  if (d_enc)
-    RNNT_LAUNCH(KID_DENC, st, denc_kernel<<<(unsigned)((long long)d.N * d.T), 128, 0, st>>>(w.dpre, bnd, d.T, d.S, d.J, d_enc));
-  if (d_dec)
-    RNNT_LAUNCH(KID_DDEC, st, ddec_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(w.dpre, ranges, w.urange, bnd, d.T,
-                                                                                        d.U, d.S, d.J, d_dec));
+  if ((e = joiner_dh_launch(d, g, h, W, ranges, w.urange, bnd, d_enc, d_dec, w.dpart, st)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

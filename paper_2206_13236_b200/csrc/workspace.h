@@ -31,6 +31,8 @@ struct Dims {
   int VP64() const { return (V + 63) / 64 * 64; }       // bf16 pitch of the E operands (K-major boxes of 64)
   int UP() const { return (U + 1 + 63) / 64 * 64; }      // bf16 pitch of G~ (t-major, K-major boxes of 64)
   int ntb() const { return (T + 31) / 32; }              // 32-frame blocks of the occupancy column partials
+  int dh_frames() const { return 128 / S; }                                // frames per joiner_dh tile
+  long long dh_tiles() const { return ((long long)N * T + dh_frames() - 1) / dh_frames(); }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
   int VP() const { return (V + 127) / 128 * 128; }      // padded row pitch of P~ (elements)
 };
@@ -80,7 +82,7 @@ struct PrunedWS {
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
-  float* dpre;       // (R,J) fp32
+  float* dpart;      // (dh_tiles,2,S,J) d_dec boundary partials of the joiner_dh tiles
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
   int splits;
@@ -153,7 +155,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);
   p.gpk = (float4*)take(R * NT * 16);
-  p.dpre = (float*)take(R * J * 4);
+  p.dpart = (float*)take((size_t)d.dh_tiles() * 2 * d.S * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);
   if (sw) *sw = s;

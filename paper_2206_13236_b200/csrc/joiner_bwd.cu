@@ -76,13 +76,15 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 //   u at each end of a tile's utterance segment go to a boundary-partial buffer that
 //   ddec_fixup_kernel sums in tile order: deterministic, and dpre never leaves the SM).
 namespace jdh {
-constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 512, STAGES = 2;
+// 256 output columns per CTA (TMEM 256 of 512 columns, ~102 KB smem): two CTAs per SM, so one
+// CTA's epilogue overlaps the other's mainloop.
+constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 256, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
-constexpr int B_BYTES = MAXN * BK * 2;         // 64 KB, MN-major (8 boxes of 64 j x 64 v)
+constexpr int B_BYTES = MAXN * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
 constexpr int H_BYTES = BM * 64 * 2;           // 16 KB: one 64-column box of h for the epilogue
-constexpr int D_OFF = 8 * H_BYTES;             // dpre staging block [128][32] fp32 after the h boxes
+constexpr int D_OFF = 4 * H_BYTES;             // dpre staging block [128][32] fp32 after the h boxes
 constexpr int MAXSEG = 128;
 constexpr int TAB_BYTES = 4 * 128 + MAXSEG * 8 * 4 + 4 * 128 + 16 + 128 * 16 + 3 * 4 * 128;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + TAB_BYTES;
@@ -107,7 +109,7 @@ struct Seg {
   int n, fb, fe, ub, ue, off, pnext, ta;
 };
 
-__global__ void __launch_bounds__(jdh::THREADS, 1)
+__global__ void __launch_bounds__(jdh::THREADS, 2)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
   using namespace jdh;
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
     tc::tma_prefetch(&tmW);
     tc::tma_prefetch(&tmH);
   }
-  if (warp == 4) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 4) tc::tmem_alloc(tmem_slot, MAXN);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) tc::tmem_dealloc(tbase, 512);
+  if (warp == 4) tc::tmem_dealloc(tbase, MAXN);
 }
 
 // d_dec for the token positions whose covering frames span several tiles (sum of the boundary

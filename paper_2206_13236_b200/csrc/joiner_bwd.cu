@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(128) ddec_fixup_kernel(const int32_t* __restri
 
 // ======================================================================= K11
 namespace jdw {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+// 2 stages (~108 KB smem, TMEM 256 columns): two CTAs per SM keep four stages in flight per SM.
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 2;
 constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 TMA boxes of 64 v x 64 rows of P~)
 constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows of h)
 constexpr int G_BYTES = BK * 16;         // 1 KB: the k-block rows' packed scalars for this V tile
@@ -420,7 +421,7 @@ struct JoinerDwParams {
   float* dbp;   // (splits, V)
 };
 
-__global__ void __launch_bounds__(jdw::THREADS, 1)
+__global__ void __launch_bounds__(jdw::THREADS, 2)
     joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
                         JoinerDwParams p) {
   using namespace jdw;

@@ -20,9 +20,11 @@
 namespace rnnt {
 
 namespace jf {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+// 128-column V tiles, double-buffered accumulators (2 x 128 TMEM columns) and a 3-stage ring
+// (~97 KB smem): two CTAs per SM, so one CTA's softmax epilogue overlaps the other's MMAs.
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
-constexpr int B_BYTES = BN * BK * 2;        // 32 KB
+constexpr int B_BYTES = BN * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr int THREADS = 192;
@@ -40,7 +42,7 @@ struct JoinerFwdParams {
   float* py2;
 };
 
-__global__ void __launch_bounds__(jf::THREADS, 1)
+__global__ void __launch_bounds__(jf::THREADS, 2)
     joiner_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          JoinerFwdParams p) {
   using namespace jf;
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -124,11 +126,9 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
       const int acc = nt & 1;
       tc::mbar_wait(&tfull[acc], (nt >> 1) & 1);
       tc::fence_after_sync();
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
-        const int v0 = nt * BN + half * 128;
-        if (v0 >= p.V) break;
-        const uint32_t tcol = tl + acc * BN + half * 128;
+      {
+        const int v0 = nt * BN;
+        const uint32_t tcol = tl + acc * BN;
         float m = neg_inf_f();
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+  if (warp == 1) tc::tmem_dealloc(tbase, 2 * BN);
 }
 
 __global__ void bias_pad_kernel(const uint16_t* __restrict__ b, int V, int VP, float* __restrict__ out) {

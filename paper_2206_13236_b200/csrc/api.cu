@@ -35,6 +35,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
 }  // namespace rnnt
 
 namespace rnnt {
+void set_timeline(void* buf);
 static thread_local unsigned long long g_launches = 0;
 static thread_local int g_prof_id = 0;
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
@@ -240,5 +241,8 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream));
 }
+
+/* diagnostics (not in rnnt.h): per-CTA phase timestamps of the simple-loss GEMMs into buf */
+void rnnt_debug_timeline(void* buf) { rnnt::set_timeline(buf); }
 
 }  // extern "C"

@@ -6,7 +6,7 @@
 //                                                                              (occupancies)
 // on the SKEWED (diagonal-major) layout [n][k = t+u][u] written by the normaliser epilogue, so that
 // every wavefront step reads one contiguous row of arcs.  Conventions of the arc arrays (base 2):
-//   px2 = y * log2e (kNegBig at u = U_n), py2 = empty * log2e (kNegBig at t = T_n-1, u < U_n:
+//   pxy = {y, empty} * log2e (y = kNegBig at u = U_n; empty = kNegBig at t = T_n-1, u < U_n:
 //   the only blank out of the last frame is the terminal one), kNegBig at every invalid cell.
 // With these sentinels neither recursion needs a validity mask: the virtual node (T_n, U_n) on
 // diagonal K_n = T_n + U_n receives alpha(T-1,U) + empty(T-1,U) = L_tot, and beta starts
@@ -55,17 +55,13 @@ inline size_t smem_bytes(int W) {
 
 // ------------------------------------------------------------------ sentinel fill
 // grid (K+1 rows, N), threads over the row's LU columns: cell (k, u) holds (t = k - u, u).
-__global__ void skew_fill_kernel(const int64_t* __restrict__ bnd, int LU, int K, float* __restrict__ px2,
-                                 float* __restrict__ py2) {
+__global__ void skew_fill_kernel(const int64_t* __restrict__ bnd, int LU, int K, float2* __restrict__ pxy) {
   const int k = blockIdx.x, n = blockIdx.y;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   const size_t base = ((size_t)n * (K + 1) + k) * LU;
   for (int u = threadIdx.x; u < LU; u += blockDim.x) {
     const int t = k - u;
-    if (!(t >= 0 && t < Tn && u <= Un)) {
-      px2[base + u] = kNegBig;
-      py2[base + u] = kNegBig;
-    }
+    if (!(t >= 0 && t < Tn && u <= Un)) pxy[base + u] = make_float2(kNegBig, kNegBig);
   }
 }
 
@@ -94,6 +90,24 @@ __device__ __forceinline__ void lds_row(const float* p, float (&x)[R]) {
   } else {
 #pragma unroll
     for (int j = 0; j < R; ++j) x[j] = p[j];
+  }
+}
+
+// R interleaved {px, py} pairs of this lane's columns
+template <int R>
+__device__ __forceinline__ void lds_pairs(const float* p, float (&px)[R], float (&py)[R]) {
+  if constexpr (R % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < R; j += 2) {
+      const float4 q = *reinterpret_cast<const float4*>(p + 2 * j);
+      px[j] = q.x; py[j] = q.y; px[j + 1] = q.z; py[j + 1] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float2 q = *reinterpret_cast<const float2*>(p + 2 * j);
+      px[j] = q.x; py[j] = q.y;
+    }
   }
 }
 
@@ -141,8 +155,7 @@ struct Wavefront {
   __device__ __forceinline__ void step(const float* rx, int i, const float* xv_in, const float* xs_in, float* xv_out,
                                        float* xs_out, float* orow, float* oshift) {
     float px[R], py[R];
-    lds_row<R>(rx, px);
-    lds_row<R>(rx + (size_t)C * LU, py);
+    lds_pairs<R>(rx, px, py);
     float xin = kNegBig;
     if (has_in && lane == (FWD ? 0 : 31)) xin = *xv_in + (*xs_in - S);   // shifts are integers: exact
     // A_i = round(A_{i-2} + M_{i-2}); a strip with no live cell two diagonals back keeps A_i = A_{i-1}
@@ -201,7 +214,7 @@ struct Wavefront {
       const int rows = (Kn - done < C) ? Kn - done : C;
       tc::mbar_wait(&full[stage], phase);
       if (has_in) tc::mbar_wait(&xbar[inbox * NX + c % NX], (c / NX) & 1);
-      const float* rb = ring + stage * STAGE + u0;
+      const float* rb = ring + stage * STAGE + 2 * u0;
       const int slot = c % NX;
       const float* xvi = &xc->v[inbox][slot][0];
       const float* xsi = &xc->s[inbox][slot][0];
@@ -213,12 +226,12 @@ struct Wavefront {
       if (rows == C) {
 #pragma unroll
         for (int j = 0; j < C; ++j)
-          step(rb + (FWD ? j : C - 1 - j) * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j, ob + DR * j * LU,
-               osb + DR * j * W);
+          step(rb + (FWD ? j : C - 1 - j) * 2 * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j,
+               ob + DR * j * LU, osb + DR * j * W);
       } else {
 #pragma unroll 1
         for (int j = 0; j < rows; ++j)
-          step(rb + (FWD ? j : rows - 1 - j) * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j,
+          step(rb + (FWD ? j : rows - 1 - j) * 2 * LU, done + j + 1, xvi + j, xsi + j, xvo + j, xso + j,
                ob + DR * j * LU, osb + DR * j * W);
       }
       __syncwarp();
@@ -245,7 +258,7 @@ struct Wavefront {
 // grid (N, 2): y = 0 alpha, y = 1 beta.  Warps 0..W-1: strips; warp W: bulk-copy loader.
 template <int R, int W>
 __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
-    const float* __restrict__ px2, const float* __restrict__ py2, const int64_t* __restrict__ bnd, int K,
+    const float2* __restrict__ pxy, const int64_t* __restrict__ bnd, int K,
     float* __restrict__ ahat, float* __restrict__ bhat, float* __restrict__ Ash, float* __restrict__ Bsh,
     double* __restrict__ Ltot, float* __restrict__ loss, int32_t* __restrict__ status) {
   using namespace lat;
@@ -279,11 +292,10 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
         int r0, r1;
         if (fwd) { r0 = c * C; r1 = min(Kn, r0 + C); }
         else { r1 = Kn - c * C; r0 = max(0, r1 - C); }
-        const uint32_t bytes = (uint32_t)(r1 - r0) * LU * 4u;
-        tc::mbar_arrive_expect_tx(&full[s], 2 * bytes);
+        const uint32_t bytes = (uint32_t)(r1 - r0) * LU * 8u;
+        tc::mbar_arrive_expect_tx(&full[s], bytes);
         float* dx = ring + (size_t)s * 2 * C * LU;
-        tc::bulk_load(dx, px2 + base + (size_t)r0 * LU, bytes, &full[s]);
-        tc::bulk_load(dx + (size_t)C * LU, py2 + base + (size_t)r0 * LU, bytes, &full[s]);
+        tc::bulk_load(dx, pxy + base + (size_t)r0 * LU, bytes, &full[s]);
         if (++s == NST) { s = 0; ph ^= 1; }
       }
     }
@@ -304,7 +316,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 // normalised occupancies and G~ = (y'+empty')/S(t,u) (bf16 hi+lo), written t-major through a 32x32
 // smem transpose.
 __global__ void __launch_bounds__(256) combine_kernel(
-    const float* __restrict__ px2, const float* __restrict__ py2, const float* __restrict__ rS,
+    const float2* __restrict__ pxy, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
     const float* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
     int U, int LU, int K, int W, int SW, int UP, float* __restrict__ px_grad, float* __restrict__ py_grad,
@@ -337,15 +349,15 @@ __global__ void __launch_bounds__(256) combine_kernel(
       __syncwarp();
       const float* Ar = ahat + base + (size_t)k * LU;
       const float* Br = bhat + base + (size_t)(k + 1) * LU;
-      const float* X = px2 + base + (size_t)k * LU;
-      const float* Y = py2 + base + (size_t)k * LU;
+      const float2* XY = pxy + base + (size_t)k * LU;
       const int ulo = max(0, k - Tn + 1), uhi = min(k, Un);
       float z = 0.f;
       for (int u = ulo + lane; u <= uhi; u += 32) {
         const int w = u / SW;
         const float a = Ar[u];
-        z += ex2_approx(a + Y[u] + Br[u] + s_ob[kr][w]);
-        if (u < Un) z += ex2_approx(a + X[u] + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+        const float2 xy = XY[u];
+        z += ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]);
+        if (u < Un) z += ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
       }
       z = warp_sum(z);
       rz = (z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
@@ -365,9 +377,10 @@ __global__ void __launch_bounds__(256) combine_kernel(
         const int w = u / SW;
         const float a = ahat[i];
         const float* Br = bhat + base + (size_t)(k + 1) * LU;
-        if (u < Un) yv = ex2_approx(a + px2[i] + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w])) * rz;
-        bv = ex2_approx(a + py2[i] + Br[u] + s_ob[kr][w]) * rz;
-        g = (yv + bv) * rS[i];
+        const float2 xy = pxy[i];
+        if (u < Un) yv = ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w])) * rz;
+        bv = ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]) * rz;
+        g = yv + bv;                                   // divided by S(t,u) in the t-major write below
       }
       sy[kr][lane] = yv;
       sb[kr][lane] = bv;
@@ -383,11 +396,12 @@ __global__ void __launch_bounds__(256) combine_kernel(
           px_grad[o] = sy[kr][lane];
           py_grad[o] = sb[kr][lane];
         }
-        // G~ for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP (zero padded)
-        const float g = sg[kr][lane];
+        // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
+        const size_t og = ((size_t)n * T + t) * UP + u;
+        const float sgv = sg[kr][lane];
+        const float g = (u < U1 && sgv != 0.f) ? sgv * rS[og] : 0.f;   // rS is only written for live cells
         const __nv_bfloat16 gh = __float2bfloat16_rn(g);
         const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
-        const size_t og = ((size_t)n * T + t) * UP + u;
         Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
         Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
         // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
@@ -409,7 +423,7 @@ static cudaError_t launch_fb(const Dims& d, const SimpleWS& w, const int64_t* bn
   const size_t sm = lat::smem_bytes<R>(W);
   cudaFuncSetAttribute(lattice_fb_kernel<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   RNNT_LAUNCH(KID_ALPHA, st, lattice_fb_kernel<R, W><<<dim3(d.N, 2), 32 * (W + 1), sm, st>>>(
-      w.px2, w.py2, bnd, d.K(), w.alpha, w.beta, w.Ash, w.Bsh, w.Ltot, loss, status));
+      w.pxy, bnd, d.K(), w.alpha, w.beta, w.Ash, w.Bsh, w.Ltot, loss, status));
   return cudaGetLastError();
 }
 
@@ -427,7 +441,7 @@ static cudaError_t launch_fb_w(const Dims& d, const SimpleWS& w, const int64_t* 
 
 cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st) {
   RNNT_LAUNCH(KID_SKEW_FILL, st, skew_fill_kernel<<<dim3(d.K() + 1, d.N), std::min(d.LU(), 256), 0, st>>>(
-      bnd, d.LU(), d.K(), w.px2, w.py2));
+      bnd, d.LU(), d.K(), w.pxy));
   return cudaGetLastError();
 }
 
@@ -444,7 +458,7 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   if (e != cudaSuccess) return e;
   // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
   dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
-  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.px2, w.py2, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
+  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
                                                                    32 * d.lat_R(), d.UP(), px_grad, py_grad, w.Gt_hi,
                                                                    w.Gt_lo, w.Yp_hi, w.Yp_lo));

@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__
 
 // ------------------------------------------------------------------ gemm3 mainloop
 namespace sg {
-constexpr int BM = 128, BK = 64, STAGES = 2, THREADS = 160;
+constexpr int BM = 128, BK = 64, STAGES = 2;
+constexpr int EPI_WARPS = 8, THREADS = 32 * (EPI_WARPS + 1);   // warps 0-7 epilogue, warp 8 TMA + MMA
 constexpr int A_BYTES = BM * BK * 2;                        // 16 KB per hi | lo
 constexpr int B_BYTES = 256 * BK * 2;                       // 32 KB per hi | lo (BN <= 256)
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
@@ -141,7 +142,23 @@ __device__ __forceinline__ float4* ep_at(uint8_t* tile, int r, int q) {
 
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int k) { return tc::sdesc(base + 32 * k, 16, 1024); }
 __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) { return tc::sdesc(base + 2048 * k, 8192, 1024); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// all 8 epilogue warps / the 4 warps of epilogue group g (one warp per TMEM lane quadrant)
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void group_bar(int g) { asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory"); }
+
+// Epilogue context of one thread: group g (0/1) takes the 32-column chunks c with c % 2 == g;
+// quadrant q = warp % 4 owns TMEM lanes (tile rows) 32q..32q+31; row = 32q + lane.
+struct Epi {
+  int warp, lane, g, q, row;
+  uint32_t taddr;   // TMEM address of this thread's lane, column 0
+};
+
+__device__ unsigned long long* g_timeline = nullptr;   // diagnostics: per-CTA phase timestamps
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Phase 0: acc0 (TMEM columns 0..255) += A_hi B_hi + A_hi B_lo + A_lo B_hi   (bf16x3)
 // Phase 1: acc1 (TMEM columns 256..511) += A'_hi B' + A'_lo B'               (B' exact in bf16)
@@ -162,7 +179,7 @@ __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_cons
   constexpr uint32_t kCols = P::kPhases == 2 ? 512 : 256;
   const int nk = tl.nkb0 + (P::kPhases == 2 ? tl.nkb1 : 0);
 
-  if (warp == 4 && lane == 0) {
+  if (warp == EPI_WARPS && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     tc::mbar_init(tfull, 1);
     for (int c = 0; c < 8; ++c) tc::mbar_init(&ep_full[c], 1);
@@ -170,19 +187,31 @@ __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_cons
     for (int i = 0; i < 4 + (P::kPhases == 2 ? 2 : 0); ++i) tc::tma_prefetch(&mp.m[i]);
     if (P::kPhases == 2) tc::tma_prefetch(&mp.b1);
   }
-  if (warp == 4) tc::tmem_alloc(tmem_slot, kCols);
+  if (warp == EPI_WARPS) tc::tmem_alloc(tmem_slot, kCols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp < 4) {
+  unsigned long long* tlog = nullptr;
+  if (g_timeline && threadIdx.x == 0) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    tlog = g_timeline + (size_t)cta * 4;
+    tlog[0] = gtime();
+  }
+  if (warp < EPI_WARPS) {
+    Epi e;
+    e.warp = warp; e.lane = lane; e.g = warp >> 2; e.q = warp & 3; e.row = 32 * e.q + lane;
+    e.taddr = tbase + ((uint32_t)(32 * e.q) << 16);
     p.prologue(aux, tl);
+    if (tlog) tlog[1] = gtime();
     if (nk > 0) {
       tc::mbar_wait(tfull, 0);
       tc::fence_after_sync();
     }
-    p.epilogue(smem, aux, tl, tbase + ((uint32_t)(32 * warp) << 16), ep_full, mp);
+    if (tlog) tlog[2] = gtime();
+    p.epilogue(smem, aux, tl, e, ep_full, mp);
+    if (tlog) tlog[3] = gtime();
   } else if (lane == 0 && nk > 0) {
     int s = 0;
     uint32_t ph = 0;
@@ -234,7 +263,7 @@ __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_cons
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) tc::tmem_dealloc(tbase, kCols);
+  if (warp == EPI_WARPS) tc::tmem_dealloc(tbase, kCols);
 }
 
 // Coalesced warp I/O of a 32-row x 32-column fp32 block through the per-warp staging buffer:
@@ -260,10 +289,11 @@ struct NormProb {
   static constexpr int kPhases = 1;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
-  int T, U, V, LU, K, BN, nkb;
-  float *px2, *py2, *rS;
+  int T, U, V, LU, K, BN, nkb, UPa;
+  float2* pxy;     // (N,K+1,LU) skewed {y, empty} * log2e
+  float* rS;       // (N,T,UPa) t-major 1/S(t,u)
   int32_t* status;
-  const float* am;
+  const float *am, *amy;
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * BN, nkb, 0};
@@ -278,21 +308,15 @@ struct NormProb {
     tc::tma_load_3d(st + 2 * sg::A_BYTES, &mp.m[2], bar, kb * sg::BK, t.n0, t.n);
     tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
   }
-  __device__ int epi_chunks(const Tile& t) const {
-    const int Un = utt_U(bnd, t.n);
-    return (min(BN, Un + 1 - t.n0) + 31) / 32;   // 32-column chunks with at least one u <= U_n
-  }
-  // amy[t, u] = am[t, y_{u+1}] tile (pitch UP), columns u0..u0+31
-  __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
-    tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
-  }
+  __device__ int epi_chunks(const Tile&) const { return 0; }
+  __device__ void epi_load(int, uint8_t*, uint64_t*, const Tile&, const Maps&) const {}
   // per-column tables of the tile: lm[u, y_{u+1}], lm[u, 0], m_lm[u]
   __device__ void prologue(uint8_t* aux, const Tile& t) const {
     float* lmy = reinterpret_cast<float*>(aux);
     float* lm0 = lmy + 256;
     float* mlm = lm0 + 256;
     const int Un = utt_U(bnd, t.n);
-    for (int j = threadIdx.x; j < BN; j += 128) {
+    for (int j = threadIdx.x; j < BN; j += 32 * sg::EPI_WARPS) {
       const int u = t.n0 + j;
       float a = 0.f, b = 0.f, c = 0.f;
       if (u <= Un) {
@@ -308,65 +332,61 @@ struct NormProb {
     }
     epi_bar();
   }
-  __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, uint32_t taddr, uint64_t* ep_full,
-                           const Maps&) const {
+  __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t*, const Maps&) const {
     const float* lmy = reinterpret_cast<const float*>(aux);
     const float* lm0 = lmy + 256;
     const float* mlm = lm0 + 256;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
-    const int trow = t.m0 + threadIdx.x;
+    const int trow = t.m0 + e.row;
     const bool rowok = trow < Tn;
-    const int t0w = t.m0 + 32 * warp;
-    // transposition scratch after the 8 epilogue input tiles (8 x 16 KB)
-    float (*bx)[33] = reinterpret_cast<float (*)[33]>(smem + 8 * EP_BYTES + warp * 3 * sg::SCR * 4);
-    float (*by)[33] = bx + 32;
-    float (*bz)[33] = by + 32;
+    const int t0w = t.m0 + 32 * e.q;
+    float2 (*bxy)[33] = reinterpret_cast<float2 (*)[33]>(smem + e.warp * 32 * 33 * 8);
     const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
     const float mam = rowok ? m_am[arow] : 0.f;
     const float am0 = rowok ? am[arow * V] : 0.f;
+    const float* ayr = amy + arow * UPa;
+    float* rSr = rS + arow * UPa;
     const size_t nbase = (size_t)t.n * (K + 1);
     bool under = false;
-    const int nep = epi_chunks(t);
-    for (int c = 0; c < nep; ++c) {
+    const int nch = (min(BN, Un + 1 - t.n0) + 31) / 32;   // 32-column chunks with at least one u <= U_n
+    for (int c = e.g; c < nch; c += 2) {
       const int c0 = 32 * c, u0 = t.n0 + c0;
-      float acc[32], ay[32];
-      tc::tmem_ld32(taddr + c0, acc);
-      tc::mbar_wait(&ep_full[c], 0);
-      uint8_t* tile = smem + c * EP_BYTES;
+      float acc[32], ay[32], rs[32];
+      tc::tmem_ld32(e.taddr + c0, acc);
+      if (rowok) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = *ep_at(tile, threadIdx.x, q);
-        ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = reinterpret_cast<const float4*>(ayr + u0)[q];
+          ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
+        }
       }
 #pragma unroll 4
       for (int j = 0; j < 32; ++j) {
         const int u = u0 + j;
-        float px = kNegBig, py = kNegBig, rs = 0.f;
+        float px = kNegBig, py = kNegBig, r = 0.f;
         if (rowok && u <= Un) {
           const float S = acc[j];
           under |= !(S > 0.f);
-          const float Lnorm = logf(S) + mam + mlm[c0 + j];           // L_normalizer(t,u), Eq. 6
+          const float Lnorm = __logf(S) + mam + mlm[c0 + j];         // L_normalizer(t,u), Eq. 6
           if (u < Un) px = (ay[j] + lmy[c0 + j] - Lnorm) * RNNT_LOG2E_F;   // y(t,u), Eq. 1 + 5
           // empty(t,u), Eq. 2 + 5; out of the last frame only the terminal blank exists
           if (!(trow == Tn - 1 && u < Un)) py = (am0 + lm0[c0 + j] - Lnorm) * RNNT_LOG2E_F;
-          rs = 1.0f / S;
+          r = __frcp_rn(S);
         }
-        bx[lane][j] = px;
-        by[lane][j] = py;
-        bz[lane][j] = rs;
+        bxy[e.lane][j] = make_float2(px, py);
+        rs[j] = r;
+      }
+      if (rowok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(rSr + u0)[q] = make_float4(rs[4 * q], rs[4 * q + 1], rs[4 * q + 2], rs[4 * q + 3]);
       }
       __syncwarp();
       // diagonal-major write: for diagonal k = t0w + u0 + d, lane l holds column u0 + l (t = k - u)
-      const int u = u0 + lane;
+      const int u = u0 + e.lane;
       for (int d = 0; d < 63; ++d) {
-        const int tl_ = d - lane, tt = t0w + tl_;
-        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) {
-          const size_t idx = (nbase + tt + u) * LU + u;
-          px2[idx] = bx[tl_][lane];
-          py2[idx] = by[tl_][lane];
-          rS[idx] = bz[tl_][lane];
-        }
+        const int tl_ = d - e.lane, tt = t0w + tl_;
+        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) pxy[(nbase + tt + u) * LU + u] = bxy[tl_][e.lane];
       }
       __syncwarp();
     }
@@ -383,6 +403,7 @@ struct AmProb {
   int T, U, V;
   float gs;
   float* am_grad;
+  bool tma_io;   // V % 4 == 0: fp32 rows are 16-B aligned, tiles move by TMA
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
@@ -413,17 +434,15 @@ struct AmProb {
       }
     }
   }
-  bool tma_io;   // V % 4 == 0: fp32 rows are 16-B aligned, tiles move by TMA
   __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
   __device__ void prologue(uint8_t*, const Tile&) const {}
-  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, uint32_t taddr, uint64_t* ep_full,
+  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Tn = utt_T(bnd, t.n);
-    const int trow = t.m0 + threadIdx.x;
+    const int trow = t.m0 + e.row;
     const bool live = trow < Tn;
     const int nep = epi_chunks(t);
     if (nep > 0) {
@@ -431,11 +450,11 @@ struct AmProb {
       const size_t row = (size_t)t.n * T + (live ? trow : 0);
       const float mam = live ? m_am[row] : 0.f;
       const float rb = live ? rowb[row] : 0.f;
-      for (int c = 0; c < nep; ++c) {
+      for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
         float a0[32], a1[32];
-        tc::tmem_ld32(taddr + 32 * c, a0);
-        tc::tmem_ld32(taddr + 256 + 32 * c, a1);
+        tc::tmem_ld32(e.taddr + 32 * c, a0);
+        tc::tmem_ld32(e.taddr + 256 + 32 * c, a1);
         if (t.nkb1 == 0) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) a1[j] = 0.f;
@@ -444,7 +463,7 @@ struct AmProb {
         uint8_t* tile = smem + c * EP_BYTES;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          float4* pq = ep_at(tile, threadIdx.x, q);
+          float4* pq = ep_at(tile, e.row, q);
           const float4 x = *pq;
           const float xs[4] = {x.x, x.y, x.z, x.w};
           float o[4];
@@ -457,30 +476,30 @@ struct AmProb {
           *pq = make_float4(o[0], o[1], o[2], o[3]);
         }
         tc::fence_proxy_async();
-        epi_bar();
-        if (threadIdx.x == 0) {
+        group_bar(e.g);
+        if (e.row == 0) {
           tc::tma_store_3d(&mp.eout, tile, vc, t.m0, t.n);
           tc::bulk_commit();
         }
       }
-      if (threadIdx.x == 0) tc::bulk_wait_read0();
+      if (e.row == 0) tc::bulk_wait_read0();
       return;
     }
     // generic path (V % 4 != 0, or a tile of padded rows only): coalesced warp I/O through smem
-    const int t0w = t.m0 + 32 * warp;
+    const int t0w = t.m0 + 32 * e.q;
     if (t0w >= T) return;                               // whole warp beyond the padded rows
     const size_t row0 = (size_t)t.n * T + t0w;
-    const float mam = live ? m_am[row0 + lane] : 0.f;
-    const float rb = live ? rowb[row0 + lane] : 0.f;
-    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + warp * sg::SCR * 4);
+    const float mam = live ? m_am[row0 + e.lane] : 0.f;
+    const float rb = live ? rowb[row0 + e.lane] : 0.f;
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + e.warp * sg::SCR * 4);
     const int nin = min(32, Tn - t0w), nout = min(32, T - t0w);
-    for (int c = 0; c < 8; ++c) {
+    for (int c = e.g; c < 8; c += 2) {
       const int vc = t.n0 + 32 * c;
       if (vc >= V) break;
       float a0[32], a1[32];
       if (t.nkb0 > 0) {
-        tc::tmem_ld32(taddr + 32 * c, a0);
-        tc::tmem_ld32(taddr + 256 + 32 * c, a1);
+        tc::tmem_ld32(e.taddr + 32 * c, a0);
+        tc::tmem_ld32(e.taddr + 256 + 32 * c, a1);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) { a0[j] = 0.f; a1[j] = 0.f; }
@@ -490,13 +509,13 @@ struct AmProb {
         for (int j = 0; j < 32; ++j) a1[j] = 0.f;
       }
       const int nc = min(32, V - vc);
-      warp_load_block(buf, am + row0 * V + vc, V, nin, nc, lane);
+      warp_load_block(buf, am + row0 * V + vc, V, nin, nc, e.lane);
 #pragma unroll 8
       for (int j = 0; j < 32; ++j) {
         const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
-        buf[lane][j] = live ? gs * (__expf(buf[lane][j] - mam) * a0[j] - pick) : 0.f;
+        buf[e.lane][j] = live ? gs * (__expf(buf[e.lane][j] - mam) * a0[j] - pick) : 0.f;
       }
-      warp_store_block(buf, am_grad + row0 * V + vc, V, nout, nc, lane);
+      warp_store_block(buf, am_grad + row0 * V + vc, V, nout, nc, e.lane);
     }
   }
 };
@@ -510,6 +529,7 @@ struct LmProb {
   int T, U, V, ntb;
   float gs;
   float* lm_grad;
+  bool tma_io;
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
@@ -531,17 +551,15 @@ struct LmProb {
       tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
     }
   }
-  bool tma_io;
   __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
   __device__ void prologue(uint8_t*, const Tile&) const {}
-  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, uint32_t taddr, uint64_t* ep_full,
+  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Un = utt_U(bnd, t.n), U1 = U + 1;
-    const int urow = t.m0 + threadIdx.x;
+    const int urow = t.m0 + e.row;
     const bool live = urow <= Un;
     float csy = 0.f, csb = 0.f;
     int y = -1;
@@ -555,15 +573,15 @@ struct LmProb {
     const int nep = epi_chunks(t);
     if (nep > 0) {
       const float mlm = live ? m_lm[(size_t)t.n * U1 + urow] : 0.f;
-      for (int c = 0; c < nep; ++c) {
+      for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
         float acc[32];
-        tc::tmem_ld32(taddr + 32 * c, acc);
+        tc::tmem_ld32(e.taddr + 32 * c, acc);
         tc::mbar_wait(&ep_full[c], 0);
         uint8_t* tile = smem + c * EP_BYTES;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          float4* pq = ep_at(tile, threadIdx.x, q);
+          float4* pq = ep_at(tile, e.row, q);
           const float4 x = *pq;
           const float xs[4] = {x.x, x.y, x.z, x.w};
           float o[4];
@@ -576,40 +594,40 @@ struct LmProb {
           *pq = make_float4(o[0], o[1], o[2], o[3]);
         }
         tc::fence_proxy_async();
-        epi_bar();
-        if (threadIdx.x == 0) {
+        group_bar(e.g);
+        if (e.row == 0) {
           tc::tma_store_3d(&mp.eout, tile, vc, t.m0, t.n);
           tc::bulk_commit();
         }
       }
-      if (threadIdx.x == 0) tc::bulk_wait_read0();
+      if (e.row == 0) tc::bulk_wait_read0();
       return;
     }
-    const int u0w = t.m0 + 32 * warp;
+    const int u0w = t.m0 + 32 * e.q;
     if (u0w >= U1) return;                               // whole warp beyond the padded rows
     const size_t row0 = (size_t)t.n * U1 + u0w;
-    const float mlm = live ? m_lm[row0 + lane] : 0.f;
-    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + warp * sg::SCR * 4);
+    const float mlm = live ? m_lm[row0 + e.lane] : 0.f;
+    float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + e.warp * sg::SCR * 4);
     const int nin = min(32, Un + 1 - u0w), nout = min(32, U1 - u0w);
-    for (int c = 0; c < 8; ++c) {
+    for (int c = e.g; c < 8; c += 2) {
       const int vc = t.n0 + 32 * c;
       if (vc >= V) break;
       float acc[32];
       if (t.nkb0 > 0) {
-        tc::tmem_ld32(taddr + 32 * c, acc);
+        tc::tmem_ld32(e.taddr + 32 * c, acc);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
       }
       const int nc = min(32, V - vc);
-      warp_load_block(buf, lm + row0 * V + vc, V, nin, nc, lane);
+      warp_load_block(buf, lm + row0 * V + vc, V, nin, nc, e.lane);
 #pragma unroll 8
       for (int j = 0; j < 32; ++j) {
         const int v = vc + j;
         const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);
-        buf[lane][j] = live ? gs * (__expf(buf[lane][j] - mlm) * acc[j] - pick) : 0.f;
+        buf[e.lane][j] = live ? gs * (__expf(buf[e.lane][j] - mlm) * acc[j] - pick) : 0.f;
       }
-      warp_store_block(buf, lm_grad + row0 * V + vc, V, nout, nc, lane);
+      warp_store_block(buf, lm_grad + row0 * V + vc, V, nout, nc, e.lane);
     }
   }
 };
@@ -632,6 +650,8 @@ static bool tm3(CUtensorMap* m, const uint16_t* base, int pitch, int rows, int N
                            (uint64_t)pitch * rows * 2, 64, (uint32_t)box_rows);
 }
 
+void set_timeline(void* buf) { cudaMemcpyToSymbol(g_timeline, &buf, sizeof(buf)); }
+
 cudaError_t exp_split_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
                              const int64_t* bnd, cudaStream_t st) {
   long long rows = (long long)d.N * d.T;
@@ -650,11 +670,8 @@ cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, 
   if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
       !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))
     return cudaErrorInvalidValue;
-  if (!make_tmap_f32_3d(&mp.ein, w.amy, d.UP(), d.T, d.N, (uint64_t)d.UP() * 4, (uint64_t)d.UP() * d.T * 4, 32,
-                        sg::BM))
-    return cudaErrorInvalidValue;
-  NormProb p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64,
-             w.px2, w.py2, w.rS, status, am};
+  NormProb p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64, d.UP(),
+             w.pxy, w.rS, status, am, w.amy};
   dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.U1() + BN - 1) / BN, d.N);
   return launch_gemm3(p, grid, mp, KID_NORM, st);
 }

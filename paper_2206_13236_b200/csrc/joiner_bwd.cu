@@ -370,18 +370,21 @@ __global__ void __launch_bounds__(jdh::THREADS, 2)
 
 // d_dec for the token positions whose covering frames span several tiles (sum of the boundary
 // partials in tile order), and zeros for u > U_n / infeasible utterances.  Positions complete in
-// one tile were written by joiner_dh_tc_kernel and are left untouched.
-__global__ void __launch_bounds__(128) ddec_fixup_kernel(const int32_t* __restrict__ ranges,
+// one tile were written by joiner_dh_tc_kernel and are left untouched.  One warp per (n, u).
+__global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restrict__ ranges,
                                                          const int2* __restrict__ urange,
-                                                         const int64_t* __restrict__ bnd, int T, int U, int S, int F,
-                                                         int J, const float* __restrict__ part,
+                                                         const int64_t* __restrict__ bnd, int N, int T, int U, int S,
+                                                         int F, int J, const float* __restrict__ part,
                                                          float* __restrict__ d_dec) {
-  const long long nu = blockIdx.x;
-  const int u = (int)(nu % (U + 1)), n = (int)(nu / (U + 1));
+  const long long nu = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (nu >= (long long)N * (U + 1)) return;
+  const int n = (int)(nu / (U + 1)), u = (int)(nu - (long long)n * (U + 1));
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  float* dst = d_dec + (size_t)nu * J;
+  const int J4 = J / 4;
+  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
   if (u > Un || (long long)Un > (long long)Tn * (S - 1)) {
-    for (int j = threadIdx.x; j < J; j += blockDim.x) dst[j] = 0.f;
+    for (int j = lane; j < J4; j += 32) dst[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
   const int2 cov = urange[nu];
@@ -390,12 +393,33 @@ __global__ void __launch_bounds__(128) ddec_fixup_kernel(const int32_t* __restri
   if (k0 == k1) return;
   const int32_t* pr = ranges + (size_t)n * T;
   const int tb0 = (int)((k0 + 1) * F - gbase);                     // first frame of tile k0 + 1
-  const float* first = part + (((size_t)k0 * 2 + 1) * S + (u - pr[tb0])) * J;
-  for (int j = threadIdx.x; j < J; j += blockDim.x) {
-    float v = first[j];
+  const float4* first = reinterpret_cast<const float4*>(part + (((size_t)k0 * 2 + 1) * S + (u - pr[tb0])) * J);
+  float4 acc[4];
+  for (int q = 0; q < 4; ++q) {
+    const int j = lane + 32 * q;
+    acc[q] = j < J4 ? first[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (long long k = k0 + 1; k <= k1; ++k) {
+    const int ta = (int)(k * F - gbase);
+    const float4* src = reinterpret_cast<const float4*>(part + (((size_t)k * 2 + 0) * S + (u - pr[ta])) * J);
+    for (int q = 0; q < 4; ++q) {
+      const int j = lane + 32 * q;
+      if (j < J4) {
+        const float4 x = src[j];
+        acc[q].x += x.x; acc[q].y += x.y; acc[q].z += x.z; acc[q].w += x.w;
+      }
+    }
+  }
+  for (int q = 0; q < 4; ++q) {
+    const int j = lane + 32 * q;
+    if (j < J4) dst[j] = acc[q];
+  }
+  for (int j = lane + 128; j < J4; j += 32) {   // J > 512: remaining columns
+    float4 v = first[j];
     for (long long k = k0 + 1; k <= k1; ++k) {
       const int ta = (int)(k * F - gbase);
-      v += part[(((size_t)k * 2 + 0) * S + (u - pr[ta])) * J + j];
+      const float4 x = reinterpret_cast<const float4*>(part + (((size_t)k * 2 + 0) * S + (u - pr[ta])) * J)[j];
+      v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
     }
     dst[j] = v;
   }
@@ -583,8 +607,8 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   dim3 grid((unsigned)d.dh_tiles(), (d.J + jdh::MAXN - 1) / jdh::MAXN);
   RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   if (d_dec)
-    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)((long long)d.N * d.U1()), 128, 0, st>>>(
-        ranges, urange, bnd, d.T, d.U, d.S, F, d.J, part, d_dec));
+    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(
+        ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, part, d_dec));
   return cudaGetLastError();
 }
 

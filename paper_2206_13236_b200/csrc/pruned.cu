@@ -120,6 +120,12 @@ __device__ __forceinline__ float plae2(float a, float b, float c) {
   return (m - c) + lg2_approx(1.0f + ex2_approx(-fabsf(a - b)));
 }
 
+// Per (anti-diagonal k, slot s) step record, built in a parallel prepass so that the wavefront
+// loop only does value arithmetic: arcs {y, empty} and a code word
+//   bits 0-15 frame t | 16-21 source lane + 1 of the frame-crossing arc (0: none) | flags below.
+constexpr int kPfAct = 1 << 22, kPfMasked = 1 << 23, kPfFirst = 1 << 24, kPfLast = 1 << 25, kPfUeq = 1 << 26,
+              kPfUlt = 1 << 27;
+
 __global__ void __launch_bounds__(256) pruned_fb_kernel(
     const float* __restrict__ px2, const float* __restrict__ py2, const int32_t* __restrict__ ranges,
     const int64_t* __restrict__ bnd, int T, int S, int K, float* __restrict__ ap, float* __restrict__ bp,
@@ -129,11 +135,6 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
   const int n = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  // smem: p_t (T), frame-at-diagonal F[d] (T+U+1: F[t + p_t] = t, else -1), arcs (T*S each)
-  int* sp = reinterpret_cast<int*>(smem_raw);
-  int* sF = sp + T;
-  float* sx = reinterpret_cast<float*>(sF + K + 1);
-  float* sy = sx + (size_t)T * S;
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   if (!feasible) {
     if (fwd && threadIdx.x == 0) {
@@ -144,72 +145,70 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
     return;
   }
   const size_t rbase = (size_t)n * T * S;
-  const int dlast = (Tn - 1) + ranges[(size_t)n * T + Tn - 1];   // d_{T-1}
-  for (int i = threadIdx.x; i <= dlast; i += blockDim.x) sF[i] = -1;
+  const int* pr = ranges + (size_t)n * T;
+  const int dlast = (Tn - 1) + pr[Tn - 1];          // d_{T-1}
+  const int kend = dlast + S - 1;                    // last anti-diagonal holding a band cell
+  // smem: records [(kend+1) * S] {float2 arcs, int code}
+  float2* rxy = reinterpret_cast<float2*>(smem_raw);
+  int* rcode = reinterpret_cast<int*>(rxy + (size_t)(K + 1) * S);
+  const int nrec = (kend + 1) * S;
+  for (int i = threadIdx.x; i < nrec; i += blockDim.x) rcode[i] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < Tn; i += blockDim.x) {
-    const int p = ranges[(size_t)n * T + i];
-    sp[i] = p;
-    sF[i + p] = i;
-  }
-  {
-    const int m = Tn * S;
-    for (int i0 = threadIdx.x; i0 < m; i0 += 4 * blockDim.x) {
-      float x[4], y[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q * blockDim.x;
-        x[q] = i < m ? px2[rbase + i] : 0.f;
-        y[q] = i < m ? py2[rbase + i] : 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q * blockDim.x;
-        if (i < m) { sx[i] = x[q]; sy[i] = y[q]; }
+  for (int i = threadIdx.x; i < Tn * S; i += blockDim.x) {
+    const int t = i / S, sl = i - t * S;
+    const int p = pr[t], u = p + sl, k = t + p + sl;
+    int src1 = 0;   // source lane + 1 of the arc crossing frames
+    if (fwd) {
+      if (t > 0) src1 = sl + p - pr[t - 1] + 1;                       // (t-1, u) in frame t-1
+    } else {
+      if (t < Tn - 1) {
+        const int s2 = sl - (pr[t + 1] - p);                          // (t+1, u) in frame t+1
+        src1 = s2 >= 0 ? s2 + 1 : 0;
       }
     }
+    int code = t | (min(src1, 63) << 16) | kPfAct;
+    if (u > Un) code |= kPfMasked;
+    if (t == 0) code |= kPfFirst;
+    if (t == Tn - 1) code |= kPfLast;
+    if (u == Un) code |= kPfUeq;
+    if (u < Un) code |= kPfUlt;
+    rxy[k * S + sl] = make_float2(px2[rbase + i], py2[rbase + i]);
+    rcode[k * S + sl] = code;
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int s = threadIdx.x;
-  const int kend = dlast + S - 1;                    // last anti-diagonal holding a band cell
+  const bool on = s < S;
   float* shift = (fwd ? Aps : Bps) + (size_t)n * (K + 1);
   float* outv = (fwd ? ap : bp) + rbase;
   const float NB = kNegBig;
   float Sh = 0.f;   // shift of the current diagonal: an integer, exact in fp32
   float Mm2 = 0.f, Mm1 = 0.f, cprev = 0.f;
 
-  // Table-driven: at diagonal k lane s holds frame t = F[k - s] (or none).  Everything indexed by
-  // (k, s) is independent of the values, so the compiler can hoist it off the LogAdd chain.
   if (fwd) {
     float h_out = NB, v_out = NB;
     int k_loss = -1;
     float hl = NB;
 #pragma unroll 4
     for (int k = 0; k <= kend; ++k) {
-      const int j = k - s;
-      const int t = (s < S && j >= 0 && j <= dlast) ? sF[j] : -1;
-      const bool act = t >= 0;
-      const int tt = act ? t : 0;
-      const int p = sp[tt];
-      const int src = (act && tt > 0) ? s + p - sp[tt - 1] : 32;
-      const float pxv = sx[tt * S + (s < S ? s : 0)], pyv = sy[tt * S + (s < S ? s : 0)];
+      const int code = on ? rcode[k * S + s] : 0;
+      const float2 xy = on ? rxy[k * S + s] : make_float2(NB, NB);
+      const int src = ((code >> 16) & 63) - 1;
       // A_k = round(A_{k-2} + M_{k-2}); a diagonal with no live cell keeps A_k = A_{k-1}
       const float ci = (k >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-      const float hin = __shfl_sync(0xffffffffu, h_out, src < 32 ? src : 0);
+      const float hin = __shfl_sync(0xffffffffu, h_out, src >= 0 ? src : s);
       const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
-      const float left = (src < S) ? hin : NB;
+      const float left = (src >= 0 && src < S) ? hin : NB;
       const float below = s > 0 ? vin : NB;
-      const int u = p + s;
-      float a = (tt == 0 && s == 0) ? -ci : plae2(left, below, ci);
-      if (u > Un) a = NB;                                  // masked slot (S > U_n + 1, D10)
+      float a = ((code & kPfFirst) && s == 0) ? -ci : plae2(left, below, ci);
+      if (code & kPfMasked) a = NB;                        // masked slot (S > U_n + 1, D10)
       float mx = NB;
-      if (act) {
-        h_out = a + pyv;
-        v_out = a + pxv;
-        outv[tt * S + s] = a;
+      if (code & kPfAct) {
+        h_out = a + xy.y;
+        v_out = a + xy.x;
+        outv[(code & 0xffff) * S + s] = a;
         mx = a;
-        if (tt == Tn - 1 && u == Un) { k_loss = k; hl = h_out; }
+        if ((code & kPfLast) && (code & kPfUeq)) { k_loss = k; hl = h_out; }
       }
       Sh += ci;
       if (s == 0) shift[k] = Sh;
@@ -230,28 +229,22 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
 #pragma unroll 4
     for (int k = kend; k >= 0; --k) {
       const int i = kend - k;
-      const int j = k - s;
-      const int t = (s < S && j >= 0 && j <= dlast) ? sF[j] : -1;
-      const bool act = t >= 0;
-      const int tt = act ? t : 0;
-      const int p = sp[tt];
-      const bool last = (tt == Tn - 1);
-      const int src = last ? -1 : s - (sp[tt + 1 < Tn ? tt + 1 : tt] - p);   // slot of (t+1, u) in frame t+1
-      const float pxv = sx[tt * S + (s < S ? s : 0)], pyv = sy[tt * S + (s < S ? s : 0)];
+      const int code = on ? rcode[k * S + s] : 0;
+      const float2 xy = on ? rxy[k * S + s] : make_float2(NB, NB);
+      const int src = ((code >> 16) & 63) - 1;
       const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-      const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : 0);
+      const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : s);
       const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
-      const int u = p + s;
       float right;
-      if (last) right = (u == Un) ? pyv : NB;              // terminal blank (virtual end, beta = 0)
-      else right = (src >= 0 && src < S) ? rin + pyv : NB;
-      const float up = (u < Un && s + 1 < S) ? uin + pxv : NB;
+      if (code & kPfLast) right = (code & kPfUeq) ? xy.y : NB;          // terminal blank (virtual end, beta = 0)
+      else right = (src >= 0 && src < S) ? rin + xy.y : NB;
+      const float up = ((code & kPfUlt) && s + 1 < S) ? uin + xy.x : NB;
       float b = plae2(right, up, ci);
-      if (u > Un) b = NB;
+      if (code & kPfMasked) b = NB;
       float mx = NB;
-      if (act) {
+      if (code & kPfAct) {
         b_out = b;
-        outv[tt * S + s] = b;
+        outv[(code & 0xffff) * S + s] = b;
         mx = b;
       }
       Sh += ci;
@@ -328,7 +321,7 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
   return cudaGetLastError();
 }
 
-size_t pruned_recursion_smem(const Dims& d) { return (size_t)d.T * 4 + (size_t)(d.K() + 1) * 4 + (size_t)d.T * d.S * 8; }
+size_t pruned_recursion_smem(const Dims& d) { return (size_t)(d.K() + 1) * d.S * 12; }
 
 // Forward: per-row info, K8 joiner with fused log-softmax, K9 recursion, the occupancies and the
 // packed backward scalars.

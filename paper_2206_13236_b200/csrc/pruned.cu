@@ -154,26 +154,43 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
   const int nrec = (kend + 1) * S;
   for (int i = threadIdx.x; i < nrec; i += blockDim.x) rcode[i] = 0;
   __syncthreads();
-  for (int i = threadIdx.x; i < Tn * S; i += blockDim.x) {
-    const int t = i / S, sl = i - t * S;
-    const int p = pr[t], u = p + sl, k = t + p + sl;
-    int src1 = 0;   // source lane + 1 of the arc crossing frames
-    if (fwd) {
-      if (t > 0) src1 = sl + p - pr[t - 1] + 1;                       // (t-1, u) in frame t-1
-    } else {
-      if (t < Tn - 1) {
-        const int s2 = sl - (pr[t + 1] - p);                          // (t+1, u) in frame t+1
-        src1 = s2 >= 0 ? s2 + 1 : 0;
+  for (int i0 = threadIdx.x; i0 < Tn * S; i0 += 4 * blockDim.x) {
+    float x[4], y[4];
+    int pp[4], pn[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {                 // all loads of the four entries first (MLP)
+      const int i = i0 + q * blockDim.x;
+      x[q] = 0.f; y[q] = 0.f; pp[q] = 0; pn[q] = 0;
+      if (i < Tn * S) {
+        const int t = i / S;
+        x[q] = px2[rbase + i];
+        y[q] = py2[rbase + i];
+        pp[q] = pr[t];
+        pn[q] = fwd ? (t > 0 ? pr[t - 1] : 0) : (t < Tn - 1 ? pr[t + 1] : 0);
       }
     }
-    int code = t | (min(src1, 63) << 16) | kPfAct;
-    if (u > Un) code |= kPfMasked;
-    if (t == 0) code |= kPfFirst;
-    if (t == Tn - 1) code |= kPfLast;
-    if (u == Un) code |= kPfUeq;
-    if (u < Un) code |= kPfUlt;
-    rxy[k * S + sl] = make_float2(px2[rbase + i], py2[rbase + i]);
-    rcode[k * S + sl] = code;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + q * blockDim.x;
+      if (i >= Tn * S) break;
+      const int t = i / S, sl = i - t * S;
+      const int p = pp[q], u = p + sl, k = t + p + sl;
+      int src1 = 0;   // source lane + 1 of the arc crossing frames
+      if (fwd) {
+        if (t > 0) src1 = sl + p - pn[q] + 1;                          // (t-1, u) in frame t-1
+      } else if (t < Tn - 1) {
+        const int s2 = sl - (pn[q] - p);                               // (t+1, u) in frame t+1
+        src1 = s2 >= 0 ? s2 + 1 : 0;
+      }
+      int code = t | (min(src1, 63) << 16) | kPfAct;
+      if (u > Un) code |= kPfMasked;
+      if (t == 0) code |= kPfFirst;
+      if (t == Tn - 1) code |= kPfLast;
+      if (u == Un) code |= kPfUeq;
+      if (u < Un) code |= kPfUlt;
+      rxy[k * S + sl] = make_float2(x[q], y[q]);
+      rcode[k * S + sl] = code;
+    }
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
@@ -185,74 +202,94 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
   float Sh = 0.f;   // shift of the current diagonal: an integer, exact in fp32
   float Mm2 = 0.f, Mm1 = 0.f, cprev = 0.f;
 
+  // Blocks of 8 diagonals: the records of the block are loaded up front, then 8 straight-line steps.
+  constexpr int KB = 8;
   if (fwd) {
     float h_out = NB, v_out = NB;
     int k_loss = -1;
     float hl = NB;
-#pragma unroll 4
-    for (int k = 0; k <= kend; ++k) {
-      const int code = on ? rcode[k * S + s] : 0;
-      const float2 xy = on ? rxy[k * S + s] : make_float2(NB, NB);
-      const int src = ((code >> 16) & 63) - 1;
-      // A_k = round(A_{k-2} + M_{k-2}); a diagonal with no live cell keeps A_k = A_{k-1}
-      const float ci = (k >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-      const float hin = __shfl_sync(0xffffffffu, h_out, src >= 0 ? src : s);
-      const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
-      const float left = (src >= 0 && src < S) ? hin : NB;
-      const float below = s > 0 ? vin : NB;
-      float a = ((code & kPfFirst) && s == 0) ? -ci : plae2(left, below, ci);
-      if (code & kPfMasked) a = NB;                        // masked slot (S > U_n + 1, D10)
-      float mx = NB;
-      if (code & kPfAct) {
-        h_out = a + xy.y;
-        v_out = a + xy.x;
-        outv[(code & 0xffff) * S + s] = a;
-        mx = a;
-        if ((code & kPfLast) && (code & kPfUeq)) { k_loss = k; hl = h_out; }
+    for (int kb = 0; kb <= kend; kb += KB) {
+      int cd[KB];
+      float2 xy[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb + j;
+        const bool ok = on && k <= kend;
+        cd[j] = ok ? rcode[k * S + s] : 0;
+        xy[j] = ok ? rxy[k * S + s] : make_float2(NB, NB);
       }
-      Sh += ci;
-      if (s == 0) shift[k] = Sh;
-      if (k == k_loss) {
-        // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band), in the frame A_k
-        const double L = ((double)hl + (double)Sh) * RNNT_LN2;
-        Lp[n] = L;
-        loss[n] = (float)(-L);
-        if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb + j, code = cd[j];
+        const int src = ((code >> 16) & 63) - 1;
+        // A_k = round(A_{k-2} + M_{k-2}); a diagonal with no live cell keeps A_k = A_{k-1}
+        const float ci = (k >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
+        const float hin = __shfl_sync(0xffffffffu, h_out, src >= 0 ? src : s);
+        const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
+        const float left = (src >= 0 && src < S) ? hin : NB;
+        const float below = s > 0 ? vin : NB;
+        float a = ((code & kPfFirst) && s == 0) ? -ci : plae2(left, below, ci);
+        if (code & kPfMasked) a = NB;                      // masked slot (S > U_n + 1, D10)
+        const bool act = (code & kPfAct) != 0;
+        const float hn = a + xy[j].y, vn = a + xy[j].x;
+        h_out = act ? hn : h_out;
+        v_out = act ? vn : v_out;
+        if (act) outv[(code & 0xffff) * S + s] = a;
+        const float mx = act ? a : NB;
+        const bool fin = act && (code & kPfLast) && (code & kPfUeq);
+        k_loss = fin ? k : k_loss;
+        hl = fin ? hn : hl;
+        Sh += ci;
+        if (s == 0 && k <= kend) shift[k] = Sh;
+        if (k == k_loss && fin) {
+          // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band), in the frame A_k
+          const double L = ((double)hl + (double)Sh) * RNNT_LN2;
+          Lp[n] = L;
+          loss[n] = (float)(-L);
+          if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
+        }
+        const float Mk = warp_max_uniform_p(mx);
+        Mm2 = Mm1;
+        Mm1 = Mk;
+        cprev = ci;
       }
-      const float Mk = warp_max_uniform_p(mx);
-      Mm2 = Mm1;
-      Mm1 = Mk;
-      cprev = ci;
     }
   } else {
     float b_out = NB;
-#pragma unroll 4
-    for (int k = kend; k >= 0; --k) {
-      const int i = kend - k;
-      const int code = on ? rcode[k * S + s] : 0;
-      const float2 xy = on ? rxy[k * S + s] : make_float2(NB, NB);
-      const int src = ((code >> 16) & 63) - 1;
-      const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-      const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : s);
-      const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
-      float right;
-      if (code & kPfLast) right = (code & kPfUeq) ? xy.y : NB;          // terminal blank (virtual end, beta = 0)
-      else right = (src >= 0 && src < S) ? rin + xy.y : NB;
-      const float up = ((code & kPfUlt) && s + 1 < S) ? uin + xy.x : NB;
-      float b = plae2(right, up, ci);
-      if (code & kPfMasked) b = NB;
-      float mx = NB;
-      if (code & kPfAct) {
-        b_out = b;
-        outv[(code & 0xffff) * S + s] = b;
-        mx = b;
+    for (int kb = kend; kb >= 0; kb -= KB) {
+      int cd[KB];
+      float2 xy[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb - j;
+        const bool ok = on && k >= 0;
+        cd[j] = ok ? rcode[k * S + s] : 0;
+        xy[j] = ok ? rxy[k * S + s] : make_float2(NB, NB);
       }
-      Sh += ci;
-      if (s == 0) shift[k] = Sh;
-      const float Mk = warp_max_uniform_p(mx);
-      Mm2 = Mm1;
-      Mm1 = Mk;
-      cprev = ci;
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb - j, i = kend - k, code = cd[j];
+        const int src = ((code >> 16) & 63) - 1;
+        const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
+        const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : s);
+        const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
+        float right;
+        if (code & kPfLast) right = (code & kPfUeq) ? xy[j].y : NB;       // terminal blank (virtual end, beta = 0)
+        else right = (src >= 0 && src < S) ? rin + xy[j].y : NB;
+        const float up = ((code & kPfUlt) && s + 1 < S) ? uin + xy[j].x : NB;
+        float b = plae2(right, up, ci);
+        if (code & kPfMasked) b = NB;
+        const bool act = (code & kPfAct) != 0;
+        b_out = act ? b : b_out;
+        if (act) outv[(code & 0xffff) * S + s] = b;
+        const float mx = act ? b : NB;
+        Sh += ci;
+        if (s == 0 && k >= 0) shift[k] = Sh;
+        const float Mk = warp_max_uniform_p(mx);
+        Mm2 = Mm1;
+        Mm1 = Mk;
+        cprev = ci;
+      }
     }
   }
 }

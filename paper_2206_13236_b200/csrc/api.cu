@@ -41,7 +41,7 @@ static thread_local int g_prof_id = 0;
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 static const char* const kNames[KID_COUNT] = {
-    "none", "validate", "exp_split_am", "exp_split_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
+    "none", "validate", "simple_prep", "unused_exp_split_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
     "lattice_combine", "simple_am_grad_gemm", "unused_am_picks", "simple_lm_grad_gemm", "unused_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_d_enc", "joiner_d_dec",

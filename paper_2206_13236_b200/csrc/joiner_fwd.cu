@@ -219,16 +219,10 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
   if (warp == 1) tc::tmem_dealloc(tbase, 2 * BN);
 }
 
-__global__ void bias_pad_kernel(const uint16_t* __restrict__ b, int V, int VP, float* __restrict__ out) {
-  int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < VP) out[v] = v < V ? bf16_bits_to_f(b[v]) : 0.f;
-}
-
 cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
   const int VP = d.VP();
-  RNNT_LAUNCH(KID_BIAS_PAD, st, bias_pad_kernel<<<(VP + 255) / 256, 256, 0, st>>>(b, d.V, VP, w.bias));
   CUtensorMap ta, tb;
   if (!make_tmap_bf16_2d(&ta, h, d.J, R, (uint64_t)d.J * 2, jf::BK, jf::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tb, W, d.J, d.V, (uint64_t)d.J * 2, jf::BK, jf::BN)) return cudaErrorInvalidValue;

@@ -20,7 +20,7 @@
 // outflow of a diagonal sums to 1), which removes the error common to a diagonal.
 //
 // Kernels
-//   skew_fill_kernel    kNegBig into every invalid cell of the skewed arc arrays
+//   (the sentinels of the invalid skewed cells are written by simple_prep_kernel, simple_tc.cu)
 //   lattice_fb_kernel   grid (N, 2): y = 0 alpha, y = 1 beta, concurrently.  Warp 1 streams the arc
 //                       rows into a 4-stage shared-memory ring with cp.async.bulk (mbarrier
 //                       complete_tx); warp 0 runs the wavefront, lane i owning columns [iR, iR+R)
@@ -52,18 +52,6 @@ inline size_t smem_bytes(int W) {
   return (size_t)NST * 2 * CH<R> * 32 * R * W * sizeof(float) + sizeof(Xchg);
 }
 }  // namespace lat
-
-// ------------------------------------------------------------------ sentinel fill
-// grid (K+1 rows, N), threads over the row's LU columns: cell (k, u) holds (t = k - u, u).
-__global__ void skew_fill_kernel(const int64_t* __restrict__ bnd, int LU, int K, float2* __restrict__ pxy) {
-  const int k = blockIdx.x, n = blockIdx.y;
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  const size_t base = ((size_t)n * (K + 1) + k) * LU;
-  for (int u = threadIdx.x; u < LU; u += blockDim.x) {
-    const int t = k - u;
-    if (!(t >= 0 && t < Tn && u <= Un)) pxy[base + u] = make_float2(kNegBig, kNegBig);
-  }
-}
 
 // ------------------------------------------------------------------ wavefront
 // log2(2^a + 2^b) for finite (sentinel-safe) a, b; minus the rebasing increment c.
@@ -437,12 +425,6 @@ static cudaError_t launch_fb_w(const Dims& d, const SimpleWS& w, const int64_t* 
     case 4: return launch_fb<R, 4>(d, w, bnd, loss, status, st);
   }
   return cudaErrorInvalidValue;
-}
-
-cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st) {
-  RNNT_LAUNCH(KID_SKEW_FILL, st, skew_fill_kernel<<<dim3(d.K() + 1, d.N), std::min(d.LU(), 256), 0, st>>>(
-      bnd, d.LU(), d.K(), w.pxy));
-  return cudaGetLastError();
 }
 
 cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, float* px_grad,

@@ -72,9 +72,16 @@ __global__ void __launch_bounds__(256) prune_kernel(const float* __restrict__ en
   }
 }
 
+// blocks [0, nb_rows): per band row label info (and the frames covering each u); the last block
+// pads the bias to fp32 (VP columns, zero beyond V) for the joiner epilogue.
 __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t* __restrict__ sym,
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
-                               int32_t* __restrict__ rowinfo, int2* __restrict__ urange) {
+                               int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
+                               const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias) {
+  if (blockIdx.x == gridDim.x - 1) {
+    for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : 0.f;
+    return;
+  }
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= (long long)N * T * S) return;
   const int s = (int)(r % S);
@@ -368,8 +375,8 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
-  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S,
-                                                               w.rowinfo, w.urange));
+  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256 + 1), 256, 0, st>>>(
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias));
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);

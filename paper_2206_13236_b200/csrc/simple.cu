@@ -2,9 +2,9 @@
 // recursion (Eq. 3) and occupancies, and the am/lm gradients.
 //
 // Sequence (all on the caller's stream):
-//   validate_kernel                    symbol / boundary checks -> status
-//   K1 exp_split (simple_tc.cu)        row maxima (Eq. 6 offsets), bf16 hi/lo of e^{x-m}
-//   skew_fill (lattice.cu)             sentinels in the invalid cells of the skewed arc arrays
+//   K1 simple_prep (simple_tc.cu)      one launch: row maxima (Eq. 6 offsets), bf16 hi/lo
+//                                      of e^{x-m}, amy gather, one-hot rows, sentinels in the invalid
+//                                      skewed cells, symbol / boundary validation -> status
 //   K2 norm gemm3 (simple_tc.cu)       S(t,u) on tcgen05, epilogue: skewed arcs px2/py2 and 1/S
 //   K3/K4 (lattice.cu)                 alpha || beta wavefronts, occupancies, G~
 //   K5 am/lm grad gemm3 (simple_tc.cu) d(-L)/d am, d(-L)/d lm (chain rule through Eq. 5-6)
@@ -14,27 +14,12 @@
 
 namespace rnnt {
 
-// ------------------------------------------------------------------ validation
-__global__ void validate_kernel(const int64_t* symbols, const int64_t* boundary, int N, int U, int V,
-                                int32_t* status) {
-  int n = blockIdx.x;
-  int Un = utt_U(boundary, n);
-  int bits = 0;
-  if (threadIdx.x == 0 && (boundary[4 * n] != 0 || boundary[4 * n + 1] != 0)) bits |= kStatusBadBoundary;
-  for (int u = threadIdx.x; u < Un && u < U; u += blockDim.x) {
-    int64_t y = symbols[(size_t)n * U + u];
-    if (y < 1 || y >= V) bits |= kStatusBadSymbol;
-  }
-  set_status(status, n, bits);
-}
-
 // ------------------------------------------------------------------ host driver
-cudaError_t skew_fill_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, cudaStream_t st);
 cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, float* px_grad,
                            float* py_grad, int32_t* status, cudaStream_t st);
 
-cudaError_t exp_split_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
-                             const int64_t* bnd, cudaStream_t st);
+cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
+                               const int64_t* bnd, int32_t* status, cudaStream_t st);
 cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
                              const int64_t* bnd, int32_t* status, cudaStream_t st);
 cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
@@ -46,9 +31,7 @@ cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am
                                float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
                                int32_t* status, cudaStream_t st) {
   cudaError_t e;
-  RNNT_LAUNCH(KID_VALIDATE, st, validate_kernel<<<d.N, 128, 0, st>>>(sym, bnd, d.N, d.U, d.V, status));
-  if ((e = exp_split_launch(d, w, am, lm, sym, bnd, st)) != cudaSuccess) return e;
-  if ((e = skew_fill_launch(d, w, bnd, st)) != cudaSuccess) return e;
+  if ((e = simple_prep_launch(d, w, am, lm, sym, bnd, status, st)) != cudaSuccess) return e;
   if ((e = norm_gemm_launch(d, w, am, lm, sym, bnd, status, st)) != cudaSuccess) return e;
   if ((e = lattice_launch(d, w, bnd, loss, px_grad, py_grad, status, st)) != cudaSuccess) return e;
   if ((e = simple_grads_launch(d, w, am, lm, px_grad, py_grad, sym, bnd, gs, am_grad, lm_grad, st)) != cudaSuccess)

@@ -30,12 +30,12 @@ namespace rnnt {
 // One warp per row of am (which = 0, rows t of T) or lm (which = 1, rows u of U+1).  am rows also
 // gather amy[t,u] = am[t, y_{u+1}] (the label logit the normaliser epilogue needs, read here while
 // the row is in L1); lm rows also write the one-hot row [v == y_{u+1}] of the am pick contraction.
-__global__ void __launch_bounds__(256) exp_split_kernel(const float* __restrict__ x, const int64_t* __restrict__ sym,
-                                                        const int64_t* __restrict__ bnd, int N, int rows_per_n,
-                                                        int U, int V, int VP, int which, float* __restrict__ m,
-                                                        uint16_t* __restrict__ hi, uint16_t* __restrict__ lo,
-                                                        float* __restrict__ amy, int UPa, uint16_t* __restrict__ onehot) {
-  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+__device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, const int64_t* __restrict__ sym,
+                                               const int64_t* __restrict__ bnd, int N, int rows_per_n, int U, int V,
+                                               int VP, int which, float* __restrict__ m, uint16_t* __restrict__ hi,
+                                               uint16_t* __restrict__ lo, float* __restrict__ amy, int UPa,
+                                               uint16_t* __restrict__ onehot, int blk) {
+  const long long row = (long long)blk * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * rows_per_n) return;
   const int n = (int)(row / rows_per_n), r = (int)(row % rows_per_n);
@@ -84,6 +84,61 @@ __global__ void __launch_bounds__(256) exp_split_kernel(const float* __restrict_
       ay[u] = val;
     }
   }
+}
+
+// One launch for the independent prologue work of the simple loss, dispatched by block index:
+// am rows (exp split + amy), lm rows (exp split + one-hot), skewed-arc sentinels, validation.
+struct PrepParams {
+  const float *am, *lm;
+  const int64_t *sym, *bnd;
+  int N, T, U, V, VP, UP, LU, K;
+  float *m_am, *m_lm, *amy;
+  uint16_t *eam_hi, *eam_lo, *elm_hi, *elm_lo, *onehot;
+  float2* pxy;
+  int32_t* status;
+  int nb_am, nb_lm, nb_fill;
+};
+
+__global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
+  int b = blockIdx.x;
+  if (b < p.nb_am) {
+    exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr, b);
+    return;
+  }
+  b -= p.nb_am;
+  if (b < p.nb_lm) {
+    exp_split_rows(p.lm, p.sym, p.bnd, p.N, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
+                   p.onehot, b);
+    return;
+  }
+  b -= p.nb_lm;
+  if (b < p.nb_fill) {
+    // kNegBig in every invalid cell of the skewed arcs (lattice.cu conventions): 8 rows per block
+    const long long rows = (long long)p.N * (p.K + 1);
+    for (int rr = 0; rr < 8; ++rr) {
+      const long long row = (long long)b * 8 + rr;
+      if (row >= rows) break;
+      const int n = (int)(row / (p.K + 1)), k = (int)(row - (long long)n * (p.K + 1));
+      const int Tn = utt_T(p.bnd, n), Un = utt_U(p.bnd, n);
+      float2* r = p.pxy + row * p.LU;
+      for (int u = threadIdx.x; u < p.LU; u += blockDim.x) {
+        const int t = k - u;
+        if (!(t >= 0 && t < Tn && u <= Un)) r[u] = make_float2(kNegBig, kNegBig);
+      }
+    }
+    return;
+  }
+  b -= p.nb_fill;
+  // validation of utterance b: symbols in [1, V), zero begins
+  const int n = b, Un = utt_U(p.bnd, n);
+  int bits = 0;
+  if (threadIdx.x == 0 && (p.bnd[4 * n] != 0 || p.bnd[4 * n + 1] != 0)) bits |= kStatusBadBoundary;
+  for (int u = threadIdx.x; u < Un && u < p.U; u += blockDim.x) {
+    const int64_t y = p.sym[(size_t)n * p.U + u];
+    if (y < 1 || y >= p.V) bits |= kStatusBadSymbol;
+  }
+  bits = __syncthreads_or(bits & kStatusBadSymbol) ? (bits | kStatusBadSymbol) : bits;
+  if (threadIdx.x == 0) set_status(p.status, n, bits);
 }
 
 // ------------------------------------------------------------------ occupancy sums
@@ -652,14 +707,19 @@ static bool tm3(CUtensorMap* m, const uint16_t* base, int pitch, int rows, int N
 
 void set_timeline(void* buf) { cudaMemcpyToSymbol(g_timeline, &buf, sizeof(buf)); }
 
-cudaError_t exp_split_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
-                             const int64_t* bnd, cudaStream_t st) {
-  long long rows = (long long)d.N * d.T;
-  RNNT_LAUNCH(KID_ROWMAX_AM, st, exp_split_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      am, sym, bnd, d.N, d.T, d.U, d.V, d.VP64(), 0, w.m_am, w.Eam_hi, w.Eam_lo, w.amy, d.UP(), nullptr));
-  rows = (long long)d.N * d.U1();
-  RNNT_LAUNCH(KID_ROWMAX_LM, st, exp_split_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(
-      lm, sym, bnd, d.N, d.U1(), d.U, d.V, d.VP64(), 1, w.m_lm, w.Elm_hi, w.Elm_lo, nullptr, 0, w.onehot));
+cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
+                               const int64_t* bnd, int32_t* status, cudaStream_t st) {
+  PrepParams p;
+  p.am = am; p.lm = lm; p.sym = sym; p.bnd = bnd;
+  p.N = d.N; p.T = d.T; p.U = d.U; p.V = d.V; p.VP = d.VP64(); p.UP = d.UP(); p.LU = d.LU(); p.K = d.K();
+  p.m_am = w.m_am; p.m_lm = w.m_lm; p.amy = w.amy;
+  p.eam_hi = w.Eam_hi; p.eam_lo = w.Eam_lo; p.elm_hi = w.Elm_hi; p.elm_lo = w.Elm_lo; p.onehot = w.onehot;
+  p.pxy = w.pxy; p.status = status;
+  p.nb_am = (int)(((long long)d.N * d.T + 7) / 8);
+  p.nb_lm = (int)(((long long)d.N * d.U1() + 7) / 8);
+  p.nb_fill = (int)(((long long)d.N * (d.K() + 1) + 7) / 8);
+  const unsigned grid = (unsigned)(p.nb_am + p.nb_lm + p.nb_fill + d.N);
+  RNNT_LAUNCH(KID_ROWMAX_AM, st, simple_prep_kernel<<<grid, 256, 0, st>>>(p));
   return cudaGetLastError();
 }
 

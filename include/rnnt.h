@@ -63,8 +63,8 @@ typedef enum {
 
 /* Padded problem sizes. T, U are the batch maxima; V includes the blank id 0;
  * J is the joiner hidden size; S the band width (s_range).
- * Limits: 1 <= N, 1 <= T <= 65536, 0 <= U < T*64, 2 <= V, 8 <= J <= 4096 and
- * J % 8 == 0, 1 <= S <= 32. */
+ * Limits: 1 <= N, 1 <= T <= 65536, 0 <= U <= 831 and U < T*64, 2 <= V, 8 <= J <= 4096 and
+ * J % 8 == 0, 1 <= S <= 32 (larger sizes return RNNT_ERR_UNSUPPORTED / RNNT_ERR_INVALID_ARG). */
 typedef struct {
   int32_t N, T, U, V, J, S;
 } rnnt_dims_t;

@@ -300,9 +300,11 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 }
 
 // ------------------------------------------------------------------ K4 combine
-// Per block of 32 anti-diagonals: Z_k = sum_u (y'+empty') (should be 1), then the
-// normalised occupancies and G~ = (y'+empty')/S(t,u) (bf16 hi+lo), written t-major through a 32x32
-// smem transpose.
+// Per block of 32 anti-diagonals (dynamic smem: the block's raw outflows Y, B [32][UP]):
+//   phase A: raw y' and empty' of every cell of the 32 diagonals (one pass over alpha, beta and the
+//            arcs) and their diagonal sums Z_k (the outflow of a diagonal sums to 1);
+//   phase B: normalised occupancies and G~ = (y'+empty')/S(t,u) (bf16 hi+lo), and y' hi+lo, written
+//            t-major: the cells of row t in this block are the contiguous columns u = k - t.
 __global__ void __launch_bounds__(256) combine_kernel(
     const float2* __restrict__ pxy, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
@@ -310,7 +312,9 @@ __global__ void __launch_bounds__(256) combine_kernel(
     int U, int LU, int K, int W, int SW, int UP, float* __restrict__ px_grad, float* __restrict__ py_grad,
     uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo, uint16_t* __restrict__ Yp_hi,
     uint16_t* __restrict__ Yp_lo) {
-  __shared__ float sy[32][33], sb[32][33], sg[32][33];
+  extern __shared__ __align__(16) float cbuf[];
+  float* Ys = cbuf;                     // [32][UP]
+  float* Bs = cbuf + 32 * UP;           // [32][UP]
   // per diagonal and strip: ob = A^w_k + B^w_{k+1} - L (blank arc, same column), ox = A^w_k +
   // B^{w+1}_{k+1} - L (label arc out of the strip's last column into the next strip)
   __shared__ float s_ob[32][lat::MAXW], s_ox[32][lat::MAXW], s_rz[32];
@@ -324,83 +328,64 @@ __global__ void __launch_bounds__(256) combine_kernel(
   const bool finite = isfinite(L2);
   const int U1 = U + 1;
 
-  // pass 1: outflow of each diagonal
+  // phase A: one warp per diagonal of the block
   for (int kr = warp; kr < 32; kr += 8) {
     const int k = k0 + kr;
-    float rz = 0.f;
-    if (finite && k < Kn) {
-      if (lane < W) {
-        const double A = (double)Ash[sbase + (size_t)k * W + lane];
-        s_ob[kr][lane] = (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
-        s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
-      }
-      __syncwarp();
-      const float* Ar = ahat + base + (size_t)k * LU;
-      const float* Br = bhat + base + (size_t)(k + 1) * LU;
-      const float2* XY = pxy + base + (size_t)k * LU;
-      const int ulo = max(0, k - Tn + 1), uhi = min(k, Un);
-      float z = 0.f;
-      for (int u = ulo + lane; u <= uhi; u += 32) {
+    const bool live = finite && k < Kn;
+    if (live && lane < W) {
+      const double A = (double)Ash[sbase + (size_t)k * W + lane];
+      s_ob[kr][lane] = (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
+      s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
+    }
+    __syncwarp();
+    const int ulo = live ? max(0, k - Tn + 1) : 1, uhi = live ? min(k, Un) : 0;
+    const float* Ar = ahat + base + (size_t)k * LU;
+    const float* Br = bhat + base + (size_t)(k + 1) * LU;
+    const float2* XY = pxy + base + (size_t)k * LU;
+    float z = 0.f;
+    for (int u = lane; u < UP; u += 32) {
+      float yv = 0.f, bv = 0.f;
+      if (u >= ulo && u <= uhi) {
         const int w = u / SW;
         const float a = Ar[u];
         const float2 xy = XY[u];
-        z += ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]);
-        if (u < Un) z += ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+        bv = ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]);
+        if (u < Un) yv = ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
       }
-      z = warp_sum(z);
-      rz = (z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
+      Ys[kr * UP + u] = yv;
+      Bs[kr * UP + u] = bv;
+      z += yv + bv;
     }
-    if (lane == 0) s_rz[kr] = rz;
+    z = warp_sum(z);
+    if (lane == 0) s_rz[kr] = (live && z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
   }
   __syncthreads();
 
-  const int t_base0 = k0 - 31;
-  for (int ub = 0; ub < UP; ub += 32) {
-    for (int kr = warp; kr < 32; kr += 8) {
-      const int k = k0 + kr, u = ub + lane, t = k - u;
-      float yv = 0.f, bv = 0.f, g = 0.f;
-      const float rz = s_rz[kr];
-      if (rz > 0.f && t >= 0 && t < Tn && u <= Un) {
-        const size_t i = base + (size_t)k * LU + u;
-        const int w = u / SW;
-        const float a = ahat[i];
-        const float* Br = bhat + base + (size_t)(k + 1) * LU;
-        const float2 xy = pxy[i];
-        if (u < Un) yv = ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w])) * rz;
-        bv = ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]) * rz;
-        g = yv + bv;                                   // divided by S(t,u) in the t-major write below
-      }
-      sy[kr][lane] = yv;
-      sb[kr][lane] = bv;
-      sg[kr][lane] = g;
+  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t
+  const int tlo = max(0, k0 - UP + 1), thi = min(T - 1, k0 + 31);
+  for (int t = tlo + warp; t <= thi; t += 8) {
+    const int kr = lane, u = k0 + kr - t;
+    if (u < 0 || u >= UP) continue;
+    const float rz = s_rz[kr];
+    const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
+    if (u < U1) {
+      const size_t o = ((size_t)n * T + t) * U1 + u;
+      px_grad[o] = yv;
+      py_grad[o] = bv;
     }
-    __syncthreads();
-    const int t_base = t_base0 - ub;
-    for (int tr = warp; tr < 63; tr += 8) {
-      const int t = t_base + tr, u = ub + lane, kr = tr + lane - 31;
-      if (kr >= 0 && kr < 32 && t >= 0 && t < T) {
-        if (u < U1) {
-          const size_t o = ((size_t)n * T + t) * U1 + u;
-          px_grad[o] = sy[kr][lane];
-          py_grad[o] = sb[kr][lane];
-        }
-        // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
-        const size_t og = ((size_t)n * T + t) * UP + u;
-        const float sgv = sg[kr][lane];
-        const float g = (u < U1 && sgv != 0.f) ? sgv * rS[og] : 0.f;   // rS is only written for live cells
-        const __nv_bfloat16 gh = __float2bfloat16_rn(g);
-        const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
-        Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
-        Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
-        // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
-        const float yv = sy[kr][lane];
-        const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
-        const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
-        Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
-        Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
-      }
-    }
-    __syncthreads();
+    // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
+    const size_t og = ((size_t)n * T + t) * UP + u;
+    const float sgv = yv + bv;
+    const float g = (u < U1 && sgv != 0.f) ? sgv * rS[og] : 0.f;   // rS is only written for live cells
+    const __nv_bfloat16 gh = __float2bfloat16_rn(g);
+    const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
+    Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
+    Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
+    // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
+    const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
+    const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
+    Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
+    Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
   }
 }
 
@@ -440,7 +425,9 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   if (e != cudaSuccess) return e;
   // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
   dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
-  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, 0, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
+  const size_t csm = (size_t)2 * 32 * d.UP() * sizeof(float);
+  cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, csm, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
                                                                    32 * d.lat_R(), d.UP(), px_grad, py_grad, w.Gt_hi,
                                                                    w.Gt_lo, w.Yp_hi, w.Yp_lo));

@@ -215,6 +215,9 @@ def main():
     dev = R.batch_to_device(b, "cuda")
     dims = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
     outs = R.alloc_outputs(dims, "cuda")
+    from paper_2206_13236_b200.dist import GradBuffer, allreduce_grads
+    gbuf = GradBuffer(b.V, b.J, "cuda")          # d_w, d_b and the loss sums: one all_reduce per step
+    outs["d_w"], outs["d_b"] = gbuf.d_w, gbuf.d_b
     ws = torch.empty(R.rnnt_workspace_bytes(dims), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -224,9 +227,8 @@ def main():
         R.step(inp["am"], inp["lm"], inp["symbols"], inp["boundary"], inp["enc_proj"], inp["dec_proj"],
                inp["w_out"], inp["b_out"], b.S, out=outs, workspace=ws)
         if pg is not None:
-            pg.all_reduce(outs["d_w"])
-            pg.all_reduce(outs["d_b"])
-            pg.all_reduce(outs["loss_pruned"][:1])
+            gbuf.set_losses(outs["loss_simple"], outs["loss_pruned"])
+            allreduce_grads(gbuf)
 
     ids = R.kernel_ids()
     kname = args.profile_kernel if args.profile_kernel != "auto" else "joiner_fwd_gemm"

@@ -156,8 +156,11 @@ def make_batch(config: int, rank: int = 0, seed: int | None = None, poison: bool
     for n in range(N):
         dec[n, :U_n[n] + 1] = rng.standard_normal((int(U_n[n]) + 1, J), dtype=np.float32)
     a = math.sqrt(6.0 / (J + V))  # Xavier-uniform bound; reused for b (D13)
-    W = rng.uniform(-a, a, size=(V, J)).astype(np.float32)
-    b = rng.uniform(-a, a, size=(V,)).astype(np.float32)
+    # c5 (data parallel): every rank shares the joiner weights, so they come from a rank-independent
+    # stream; the other configs keep the single fixed draw order.
+    wrng = np.random.Generator(np.random.PCG64(SEED_BASE + 100 * config)) if config == 5 else rng
+    W = wrng.uniform(-a, a, size=(V, J)).astype(np.float32)
+    b = wrng.uniform(-a, a, size=(V,)).astype(np.float32)
     if zero_logits:
         for n in range(N):
             am[n, :T_n[n]] = 0

@@ -6,11 +6,14 @@
 //   py2[r] = (z[r,0] - lse) log2e, px2[r] = (z[r,y] - lse) log2e   (-inf at u = U_n)
 //   P~[r,v] = bf16(exp(z[r,v] - m[r, v/128])), m = per-128-column max  (read by K10/K11)
 //
-// One CTA per 128-row tile of the band rows; it sweeps all of V in 256-column MMA tiles
-// (N=256, K-loop over J in 64-wide TMA boxes, 4-stage mbarrier ring), double-buffered TMEM
-// accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Persistent CTAs (two per SM) loop over the live 128-row tiles of the band rows; each sweeps all of
+// V in 128-column MMA tiles (K-loop over J in 64-wide TMA boxes, 3-stage mbarrier ring) with
+// double-buffered TMEM accumulators (2 x 128 columns) so the epilogue of one tile overlaps the
+// MMAs of the next.
 // Warp 0: TMA producer.  Warp 1: TMEM allocator + single-thread MMA issuer.  Warps 2-5:
 // epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 #include "tc.cuh"
@@ -32,9 +35,12 @@ constexpr int THREADS = 192;
 
 struct JoinerFwdParams {
   const float* bias;      // (VP) fp32, padded
+  const float* bmax;      // (ntile) max of the bias over each 128-column tile
   const int32_t* rowinfo; // (R)
+  const uint8_t* tlive;   // (ntiles_rows) 1 if the 128-row tile holds a live row (rowinfo_kernel)
+  int* counter;           // dynamic tile scheduler (zeroed by rowinfo_kernel)
   long long R;
-  int V, VP, J, nvt, nkb, ntile;
+  int ntiles, V, VP, J, nvt, nkb, ntile;
   uint16_t* Pt;           // (R, VP)
   float* mt;              // (R, ntile)
   float* lse;
@@ -42,6 +48,9 @@ struct JoinerFwdParams {
   float* py2;
 };
 
+// Persistent: CTA c processes the live 128-row tiles c, c + gridDim.x, ...; the TMA ring, the
+// MMA issue and the double-buffered TMEM accumulators run continuously across row tiles, so the
+// softmax epilogue of one (row tile, V tile) overlaps the MMAs of the next.
 __global__ void __launch_bounds__(jf::THREADS, 2)
     joiner_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          JoinerFwdParams p) {
@@ -52,19 +61,16 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* qfull = tempty + 2;          // [4] tile queue: producer -> MMA issuer + epilogue
+  uint64_t* qempty = qfull + 4;
+  int* tq = reinterpret_cast<int*>(qempty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long m0 = (long long)blockIdx.x * BM;
-
-  int act = 0;
-  for (int i = threadIdx.x; i < BM; i += blockDim.x)
-    if (m0 + i < p.R && p.rowinfo[m0 + i] >= 0) act = 1;
-  if (!__syncthreads_or(act)) return;   // tile entirely masked / padding
-
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 4; ++s) { tc::mbar_init(&qfull[s], 1); tc::mbar_init(&qempty[s], 5); }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
@@ -78,75 +84,102 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      int stage = 0;
+      int stage = 0, qi = 0;
       uint32_t ph = 0;
-      for (int nt = 0; nt < nvt; ++nt) {
-        for (int kb = 0; kb < nkb; ++kb) {
-          tc::mbar_wait(&empty[stage], ph ^ 1);
-          tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          tc::tma_load_2d(sa, &tmA, &full[stage], kb * BK, (int)m0);
-          tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
-          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      for (;;) {
+        // next live row tile from the global counter, published to the other roles
+        int rt = atomicAdd(p.counter, 1);
+        while (rt < p.ntiles && !p.tlive[rt]) rt = atomicAdd(p.counter, 1);
+        if (rt >= p.ntiles) rt = -1;
+        tc::mbar_wait(&qempty[qi & 3], ((qi >> 2) & 1) ^ 1);
+        tq[qi & 3] = rt;
+        tc::mbar_arrive(&qfull[qi & 3]);
+        ++qi;
+        if (rt < 0) break;
+        const int m0 = rt * BM;
+        for (int nt = 0; nt < nvt; ++nt) {
+          for (int kb = 0; kb < nkb; ++kb) {
+            tc::mbar_wait(&empty[stage], ph ^ 1);
+            tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            tc::tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+            tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+            if (++stage == STAGES) { stage = 0; ph ^= 1; }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, false);
-      int stage = 0;
+      int stage = 0, it = 0, qi = 0;
       uint32_t ph = 0;
-      for (int nt = 0; nt < nvt; ++nt) {
-        const int acc = nt & 1;
-        tc::mbar_wait(&tempty[acc], ((nt >> 1) & 1) ^ 1);
-        tc::fence_after_sync();
-        const uint32_t d = tbase + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
-          tc::mbar_wait(&full[stage], ph);
+      for (;;) {
+        tc::mbar_wait(&qfull[qi & 3], (qi >> 2) & 1);
+        const int rt = tq[qi & 3];
+        tc::mbar_arrive(&qempty[qi & 3]);
+        ++qi;
+        if (rt < 0) break;
+        for (int nt = 0; nt < nvt; ++nt, ++it) {
+          const int acc = it & 1;
+          tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           tc::fence_after_sync();
-          const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
+          const uint32_t d = tbase + acc * BN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            tc::mbar_wait(&full[stage], ph);
+            tc::fence_after_sync();
+            const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 32 * k, 16, 1024), idesc,
-                         (kb | k) != 0);
-          tc::mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 32 * k, 16, 1024), idesc,
+                           (kb | k) != 0);
+            tc::mma_commit(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; ph ^= 1; }
+          }
+          tc::mma_commit(&tfull[acc]);
         }
-        tc::mma_commit(&tfull[acc]);
       }
     }
   } else {
     const int q = warp & 3;
-    const long long r = m0 + 32 * q + lane;
-    const int info = (r < p.R) ? p.rowinfo[r] : -1;
     const uint32_t tl = tbase + ((uint32_t)(32 * q) << 16);
-    float M = neg_inf_f(), sum = 0.f, zb = neg_inf_f(), zl = neg_inf_f();
-    uint16_t* prow = p.Pt + (size_t)(info >= 0 ? r : 0) * p.VP;
-    for (int nt = 0; nt < nvt; ++nt) {
-      const int acc = nt & 1;
-      tc::mbar_wait(&tfull[acc], (nt >> 1) & 1);
-      tc::fence_after_sync();
-      {
+    int it = 0, qi = 0;
+    for (;;) {
+      tc::mbar_wait(&qfull[qi & 3], (qi >> 2) & 1);
+      const int rt = tq[qi & 3];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&qempty[qi & 3]);
+      ++qi;
+      if (rt < 0) break;
+      const long long r = (long long)rt * BM + 32 * q + lane;
+      const int info = (r < p.R) ? p.rowinfo[r] : -1;
+      float M = neg_inf_f(), sum = 0.f, zb = neg_inf_f(), zl = neg_inf_f();
+      uint16_t* prow = p.Pt + (size_t)(info >= 0 ? r : 0) * p.VP;
+      for (int nt = 0; nt < nvt; ++nt, ++it) {
+        const int acc = it & 1;
         const int v0 = nt * BN;
+        const bool tail = v0 + BN > p.V;                // columns >= V exist in this tile
+        const float bm = p.bmax[nt];
+        tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        tc::fence_after_sync();
         const uint32_t tcol = tl + acc * BN;
+        // pass 1: an upper bound of the tile max of z + b: max of the raw accumulators + max bias
+        // (tail tile: exact masked max, the zero-filled W rows past V would otherwise count)
         float m = neg_inf_f();
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           float z[32];
           tc::tmem_ld32(tcol + 32 * c, z);
-          const float4* bb = reinterpret_cast<const float4*>(p.bias + v0 + 32 * c);
+          if (!tail) {
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            float4 b4 = __ldg(bb + j4);
-            float bj[4] = {b4.x, b4.y, b4.z, b4.w};
+            for (int j = 0; j < 32; ++j) m = fmaxf(m, z[j]);
+          } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int j = 4 * j4 + i;
-              const float zz = (v0 + 32 * c + j < p.V) ? z[j] + bj[i] : neg_inf_f();
-              m = fmaxf(m, zz);
-            }
+            for (int j = 0; j < 32; ++j)
+              if (v0 + 32 * c + j < p.V) m = fmaxf(m, z[j] + __ldg(p.bias + v0 + 32 * c + j));
           }
         }
+        if (!tail) m += bm;
         const float mL = m * RNNT_LOG2E_F;
         float s = 0.f;
 #pragma unroll 1
@@ -155,26 +188,22 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
           tc::tmem_ld32(tcol + 32 * c, z);
           const int vc = v0 + 32 * c;
           const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
-          uint32_t pk[16];
 #pragma unroll
           for (int j4 = 0; j4 < 8; ++j4) {
-            float4 b4 = __ldg(bb + j4);
-            float bj[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int j = 4 * j4 + i;
-              z[j] = (vc + j < p.V) ? z[j] + bj[i] : neg_inf_f();
-            }
+            const float4 b4 = __ldg(bb + j4);
+            z[4 * j4] += b4.x; z[4 * j4 + 1] += b4.y; z[4 * j4 + 2] += b4.z; z[4 * j4 + 3] += b4.w;
           }
-          float e[32];
+          if (tail) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            e[j] = ex2_approx(fmaf(z[j], RNNT_LOG2E_F, -mL));
-            s += e[j];
+            for (int j = 0; j < 32; ++j) z[j] = (vc + j < p.V) ? z[j] : neg_inf_f();
           }
+          uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(e[2 * j], e[2 * j + 1]);
+            const float e0 = ex2_approx(fmaf(z[2 * j], RNNT_LOG2E_F, -mL));
+            const float e1 = ex2_approx(fmaf(z[2 * j + 1], RNNT_LOG2E_F, -mL));
+            s += e0 + e1;
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
             pk[j] = *reinterpret_cast<uint32_t*>(&h2);
           }
           if (info >= 0) {
@@ -192,25 +221,25 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
             if (hit) zl = sel;
           }
         }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         if (info >= 0) p.mt[(size_t)r * p.ntile + v0 / 128] = m;
         const float Mn = fmaxf(M, m);
         sum = sum * ex2_approx((M - Mn) * RNNT_LOG2E_F) + s * ex2_approx((m - Mn) * RNNT_LOG2E_F);
         M = Mn;
       }
-      tc::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-    }
-    if (r < p.R) {
-      if (info >= 0) {
-        const float l = M + lg2_approx(sum) * RNNT_LN2_F;
-        p.lse[r] = l;
-        p.py2[r] = (zb - l) * RNNT_LOG2E_F;
-        p.px2[r] = info < p.V ? (zl - l) * RNNT_LOG2E_F : kNegBig;   // y(t,U) = -inf
-      } else {
-        p.lse[r] = 0.f;
-        p.px2[r] = kNegBig;
-        p.py2[r] = kNegBig;
+      if (r < p.R) {
+        if (info >= 0) {
+          const float l = M + lg2_approx(sum) * RNNT_LN2_F;
+          p.lse[r] = l;
+          p.py2[r] = (zb - l) * RNNT_LOG2E_F;
+          p.px2[r] = info < p.V ? (zl - l) * RNNT_LOG2E_F : kNegBig;   // y(t,U) = -inf
+        } else {
+          p.lse[r] = 0.f;
+          p.px2[r] = kNegBig;
+          p.py2[r] = kNegBig;
+        }
       }
     }
   }
@@ -226,14 +255,17 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   CUtensorMap ta, tb;
   if (!make_tmap_bf16_2d(&ta, h, d.J, R, (uint64_t)d.J * 2, jf::BK, jf::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tb, W, d.J, d.V, (uint64_t)d.J * 2, jf::BK, jf::BN)) return cudaErrorInvalidValue;
-  JoinerFwdParams p{w.bias, w.rowinfo, R, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN, (d.J + jf::BK - 1) / jf::BK,
-                    d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2};
+  const int ntiles = (int)((R + jf::BM - 1) / jf::BM);
+  JoinerFwdParams p{w.bias, w.bmax, w.rowinfo, w.tlive, w.tcounter, R, ntiles, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN,
+                    (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2};
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(joiner_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jf::SMEM_BYTES);
     attr = true;
   }
-  const unsigned grid = (unsigned)((R + jf::BM - 1) / jf::BM);
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid = (unsigned)std::min(ntiles, 2 * nsm);   // persistent: two CTAs per SM
   RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, p));
   return cudaGetLastError();
 }

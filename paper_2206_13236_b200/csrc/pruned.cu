@@ -77,41 +77,61 @@ __global__ void __launch_bounds__(256) prune_kernel(const float* __restrict__ en
 __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t* __restrict__ sym,
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
-                               const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias) {
+                               const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
+                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter) {
   if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x == 0) *tcounter = 0;
     for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : 0.f;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int tl = warp; tl < VP / 128; tl += blockDim.x / 32) {   // bias max per 128-column tile
+      float m = neg_inf_f();
+      for (int j = lane; j < 128; j += 32)
+        if (tl * 128 + j < V) m = fmaxf(m, bias[tl * 128 + j]);
+      m = warp_max(m);
+      if (lane == 0) bmax[tl] = m;
+    }
     return;
   }
-  long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (long long)N * T * S) return;
-  const int s = (int)(r % S);
-  const long long nt = r / S;
-  const int t = (int)(nt % T), n = (int)(nt / T);
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long R = (long long)N * T * S;
   int info = -1;
-  if (t < Tn && feasible) {
-    const int32_t* p = ranges + (size_t)n * T;
-    const int u = p[t] + s;
-    if (u < Un) {
-      long long y = sym[(size_t)n * U + u];
-      info = (y >= 1 && y < V) ? (int)y : V;
-    } else if (u == Un) {
-      info = V;  // no label arc at u = U_n (y(t,U) = -inf)
+  if (r < R) {
+    const int s = (int)(r % S);
+    const long long nt = r / S;
+    const int t = (int)(nt % T), n = (int)(nt / T);
+    const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+    const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
+    if (t < Tn && feasible) {
+      const int32_t* p = ranges + (size_t)n * T;
+      const int u = p[t] + s;
+      if (u < Un) {
+        long long y = sym[(size_t)n * U + u];
+        info = (y >= 1 && y < V) ? (int)y : V;
+      } else if (u == Un) {
+        info = V;  // no label arc at u = U_n (y(t,U) = -inf)
+      }
+      if (s == 0) {
+        // Frames covering token position u form the contiguous range [lo(u), hi(u)) (p monotone,
+        // Eq. 9).  Frame t is the first cover of u in (p_{t-1}+S-1, p_t+S-1] and the last cover of
+        // u in [p_t, p_{t+1}-1]; over t these intervals partition [0, U_n], so each entry is
+        // written once.
+        int2* ur = urange + (size_t)n * (U + 1);
+        const int a0 = (t == 0) ? 0 : p[t - 1] + S;
+        const int a1 = min(p[t] + S - 1, Un);
+        for (int uu = a0; uu <= a1; ++uu) ur[uu].x = t;
+        const int b1 = (t == Tn - 1) ? Un : p[t + 1] - 1;
+        for (int uu = p[t]; uu <= b1; ++uu) ur[uu].y = t + 1;
+      }
     }
-    if (s == 0) {
-      // Frames covering token position u form the contiguous range [lo(u), hi(u)) (p monotone,
-      // Eq. 9).  Frame t is the first cover of u in (p_{t-1}+S-1, p_t+S-1] and the last cover of u
-      // in [p_t, p_{t+1}-1]; over t these intervals partition [0, U_n], so each entry is written once.
-      int2* ur = urange + (size_t)n * (U + 1);
-      const int a0 = (t == 0) ? 0 : p[t - 1] + S;
-      const int a1 = min(p[t] + S - 1, Un);
-      for (int uu = a0; uu <= a1; ++uu) ur[uu].x = t;
-      const int b1 = (t == Tn - 1) ? Un : p[t + 1] - 1;
-      for (int uu = p[t]; uu <= b1; ++uu) ur[uu].y = t + 1;
-    }
+    rowinfo[r] = info;
   }
-  rowinfo[r] = info;
+  // 128-row tile liveness for the persistent joiner: a 256-thread block holds two whole tiles
+  const bool live = info >= 0;
+  const bool lo = __syncthreads_or(live && threadIdx.x < 128);
+  const bool hi = __syncthreads_or(live && threadIdx.x >= 128);
+  if (threadIdx.x == 0 && r < R) tlive[r / 128] = lo ? 1 : 0;
+  if (threadIdx.x == 128 && r < R) tlive[r / 128] = hi ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ K9 pruned recursion
@@ -376,7 +396,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   const long long R = d.rows();
   const int nt = d.ntile();
   RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256 + 1), 256, 0, st>>>(
-      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias));
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);

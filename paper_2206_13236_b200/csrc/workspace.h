@@ -68,6 +68,9 @@ struct PrunedWS {
   int32_t* rowinfo;  // (R) label y_{u+1} (V if u==U_n), -1 for masked/padded rows
   int2* urange;      // (N,U+1) frames [lo,hi) whose band covers token position u
   float* bias;       // (VP) fp32 copy of b_out, zero padded
+  float* bmax;       // (ntile) max of the bias over each 128-column tile
+  uint8_t* tlive;    // (ceil(R/128)) 128-row tile holds a live band row
+  int* tcounter;     // tile scheduler counter of the persistent joiner forward
   uint16_t* Pt;      // (R,VP) bf16 exp(z - m_tile), pitch VP
   float* mt;         // (R,ntile) tile maxima of z
   float* lse;        // (R) log-sum-exp of z
@@ -140,6 +143,9 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.rowinfo = (int32_t*)take(R * 4);
   p.urange = (int2*)take(N * U1 * 8);
   p.bias = (float*)take(VP * 4);
+  p.bmax = (float*)take(NT * 4);
+  p.tlive = (uint8_t*)take((R + 127) / 128);
+  p.tcounter = (int*)take(16);
   p.Pt = (uint16_t*)take(R * VP * 2);
   p.mt = (float*)take(R * NT * 4);
   p.lse = (float*)take(R * 4);

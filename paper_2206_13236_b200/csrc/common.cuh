@@ -48,19 +48,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // 1 - 2 / (e^{2|x|} + 1) with MUFU ex2 / rcp above (two MUFU, no division, no cancellation
 // below 0.245).
 __device__ __forceinline__ float tanh_fast(float x) {
+  // branch-free (no divergence within a warp): both forms are evaluated, the select picks one
   const float ax = fabsf(x);
-  if (ax < 0.25f) {
-    const float x2 = x * x;
-    float p = -1382.f / 155925.f;
-    p = fmaf(p, x2, 62.f / 2835.f);
-    p = fmaf(p, x2, -17.f / 315.f);
-    p = fmaf(p, x2, 2.f / 15.f);
-    p = fmaf(p, x2, -1.f / 3.f);
-    return fmaf(p * x2, x, x);
-  }
+  const float x2 = x * x;
+  float p = -1382.f / 155925.f;
+  p = fmaf(p, x2, 62.f / 2835.f);
+  p = fmaf(p, x2, -17.f / 315.f);
+  p = fmaf(p, x2, 2.f / 15.f);
+  p = fmaf(p, x2, -1.f / 3.f);
+  const float small = fmaf(p * x2, x, x);
   const float e = ex2_approx(ax * (2.0f * 1.4426950408889634f));
-  const float t = fmaf(-2.0f, rcp_approx(e + 1.0f), 1.0f);
-  return copysignf(t, x);
+  const float big = copysignf(fmaf(-2.0f, rcp_approx(e + 1.0f), 1.0f), x);
+  return ax < 0.25f ? small : big;
 }
 __device__ __forceinline__ float lg2_approx(float x) {
   float y;

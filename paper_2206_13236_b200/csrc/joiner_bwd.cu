@@ -75,297 +75,389 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 //   contiguous, Eq. 9; u whose covering frames all lie in the tile are written directly, the <= S
 //   u at each end of a tile's utterance segment go to a boundary-partial buffer that
 //   ddec_fixup_kernel sums in tile order: deterministic, and dpre never leaves the SM).
+//
+// The per-tile tables (band offsets of the tile's frames and the d_dec entries) depend only on the
+// ranges: dh_tables_kernel builds them once per tile, lists the live tiles and zeroes d_enc of the
+// dead ones; the persistent joiner_dh_tc_kernel then walks (live tile, 256-column part of J) work
+// items with every role pipelined across items:
+//   warp 0      lane 0: TMA producer: per item the tile table (bulk), per 64-logit k-block the P~
+//               tile, the W boxes and the rows' packed scalars, into a 3-stage ring;
+//               lane 1: the epilogue's h boxes (64 columns x 128 rows) into a 2-slot ring
+//   warp 1      TMEM allocator (2 x 256 columns) and single-thread MMA issuer
+//   warps 2-5   in-place dz producers (thread = tile row), release each stage to the MMA
+//   warps 6-13  epilogue, two groups of four (one per TMEM lane quadrant), alternate 32-column
+//               chunks; the accumulator of item k+1 fills while item k drains.
+struct DhTab {
+  int sp[128];     // band offset p_t of the tile's frames (-1: dead frame)
+  int4 ent[128];   // d_dec entries {first frame, end frame, u, destination}: dst >= 0 row of d_dec,
+                   // dst < 0 row -(1 + dst) of the boundary-partial buffer
+  int nent, pad[3];
+};
+static_assert(sizeof(DhTab) == 2576, "DhTab layout: 16-B multiple for the bulk copy");
+
 namespace jdh {
-// 256 output columns per CTA (TMEM 256 of 512 columns, ~102 KB smem): two CTAs per SM, so one
-// CTA's epilogue overlaps the other's mainloop.
-constexpr int BM = 128, BK = 64, NSUB = 256, MAXN = 256, STAGES = 2;
+constexpr int BM = 128, BK = 64, NSUB = 256, STAGES = 3;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
-constexpr int B_BYTES = MAXN * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
+constexpr int B_BYTES = NSUB * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
-constexpr int H_BYTES = BM * 64 * 2;           // 16 KB: one 64-column box of h for the epilogue
-constexpr int D_OFF = 4 * H_BYTES;             // dpre staging block [128][32] fp32 after the h boxes
-constexpr int MAXSEG = 128;
-constexpr int TAB_BYTES = 4 * 128 + MAXSEG * 8 * 4 + 4 * 128 + 16 + 128 * 16 + 3 * 4 * 128;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + TAB_BYTES;
-constexpr int THREADS = 160;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;   // 50 KB (1024-aligned)
+constexpr int D_BYTES = BM * 32 * 4;           // dpre staging [128][32] fp32, one per epilogue group
+constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B), ring of 2
+constexpr int TAB_BYTES = 3072;                // one DhTab slot (2576 B, padded)
+constexpr int NTAB = 2;
+constexpr int H_OFF = STAGES * STAGE_BYTES + 2 * D_BYTES;
+constexpr int TAB_OFF = H_OFF + 2 * H_BYTES;
+constexpr int BAR_OFF = TAB_OFF + NTAB * TAB_BYTES;
+constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
+constexpr int THREADS = 14 * 32;
 }  // namespace jdh
 
 struct JoinerDhParams {
   GradSrc g;
-  int J, nkb;
+  const uint16_t* h;       // (R, J) bf16
+  int J, nkb, njp;
   int N, T, U, S, F;
-  const int32_t* ranges;   // (N,T) p_t
-  const int2* urange;      // (N,U+1) frames [lo, hi) covering u
-  const int64_t* bnd;
+  const DhTab* tabs;       // (dh_tiles)
+  const int* live;         // ids of the tiles with a live row (dh_tables_kernel; order irrelevant)
+  const int* nlive;        // their count
   float* d_enc;            // (N,T,J) nullable
   float* d_dec;            // (N,U+1,J) nullable
-  float* part;             // (ntiles, 2, S, J) boundary partials of d_dec
+  float* g_part;           // (ntiles, 2, S, J) boundary partials of d_dec
 };
 
-// per-tile utterance segment: live frames f in [fb, fe) of utterance n, token positions [ub, ue],
-// its entries e in [off, off + ue - ub + 1); pnext = p at the frame after the segment (if covered)
-struct Seg {
-  int n, fb, fe, ub, ue, off, pnext, ta;
-};
+// One CTA of 128 threads per frame-aligned tile: the tile table, the live-tile list, and zeros of
+// d_enc for a tile without a live row (the persistent kernel never visits it).
+__global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restrict__ ranges,
+                                                        const int2* __restrict__ urange,
+                                                        const int64_t* __restrict__ bnd, int N, int T, int U, int S,
+                                                        int F, int J, DhTab* __restrict__ tabs, int* __restrict__ live,
+                                                        int* __restrict__ nlive, float* __restrict__ d_enc) {
+  __shared__ int sp[128], spn[128], sfn[128], sft[128];
+  __shared__ int4 segs[128];       // {n, fb, fe, ta}
+  __shared__ int2 segu[128];       // {ub, ue}
+  __shared__ int segx[128][2];     // {off, pnext}
+  __shared__ unsigned char eseg[128];
+  __shared__ int s_ne;
+  const long long tile = blockIdx.x;
+  const long long g0 = tile * F;
+  const long long NT = (long long)N * T;
+  DhTab* tb = tabs + tile;
+  const int f = threadIdx.x;
+  int pv = -1;
+  if (f < F) {
+    const long long g = g0 + f;
+    int pn = 0, n = -1, t = 0;
+    if (g < NT) {
+      n = (int)(g / T);
+      t = (int)(g - (long long)n * T);
+      const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+      if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) {
+        pv = ranges[(size_t)n * T + t];
+        if (t + 1 < Tn) pn = ranges[(size_t)n * T + t + 1];
+      }
+    }
+    sp[f] = pv; spn[f] = pn; sfn[f] = n; sft[f] = t;
+  }
+  if (f < 128) tb->sp[f] = (f < F) ? pv : -1;
+  const bool any = __syncthreads_or(pv >= 0);
+  if (!any) {
+    if (threadIdx.x == 0) tb->nent = 0;
+    if (d_enc)
+      for (int idx = threadIdx.x; idx < F * (J / 4); idx += blockDim.x) {
+        const int ff = idx / (J / 4), jq = idx - ff * (J / 4);
+        if (g0 + ff < NT) reinterpret_cast<float4*>(d_enc + (size_t)(g0 + ff) * J)[jq] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    live[atomicAdd(nlive, 1)] = (int)tile;
+    // utterance segments of the tile, then one entry per token position of a segment
+    int ns = 0, ne = 0;
+    for (int ff = 0; ff < F;) {
+      if (sp[ff] < 0) { ++ff; continue; }
+      const int n = sfn[ff];
+      int fe = ff + 1;
+      while (fe < F && sp[fe] >= 0 && sfn[fe] == n) ++fe;
+      const int ub = sp[ff], ue = min(utt_U(bnd, n), sp[fe - 1] + S - 1);
+      if (ns < 128) {
+        segs[ns] = make_int4(n, ff, fe, sft[ff]);
+        segu[ns] = make_int2(ub, ue);
+        segx[ns][0] = ne;
+        segx[ns][1] = spn[fe - 1];
+        for (int e = 0; e <= ue - ub && ne + e < 128; ++e) eseg[ne + e] = (unsigned char)ns;
+        ++ns;
+        ne += ue - ub + 1;
+      }
+      ff = fe;
+    }
+    s_ne = min(ne, 128);
+    tb->nent = s_ne;
+  }
+  __syncthreads();
+  if (threadIdx.x < s_ne) {
+    const int e = threadIdx.x;
+    const int si = eseg[e];
+    const int4 q = segs[si];          // {n, fb, fe, ta}
+    const int ub = segu[si].x, off = segx[si][0], pnext = segx[si][1];
+    const int u = ub + (e - off);
+    const int2 cov = urange[(size_t)q.x * (U + 1) + u];          // frames [lo, hi) covering u
+    const int fl = max(q.y, cov.x - q.w + q.y), fh = min(q.z, cov.y - q.w + q.y);
+    const int tbd = q.w + (q.z - q.y);
+    int dst;
+    if (cov.x >= q.w && cov.y <= tbd) dst = q.x * (U + 1) + u;                             // complete here
+    else if (cov.x < q.w) dst = -1 - (int)((tile * 2 + 0) * S + (u - ub));                 // left boundary
+    else dst = -1 - (int)((tile * 2 + 1) * S + (u - pnext));                                // right boundary
+    tb->ent[e] = make_int4(fl, fh, u, dst);
+  }
+}
 
-__global__ void __launch_bounds__(jdh::THREADS, 2)
+__global__ void __launch_bounds__(jdh::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
   using namespace jdh;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
-  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* hfull = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 1);
-  int* sp = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);   // [128] p of tile frames (-1 dead)
-  Seg* seg = reinterpret_cast<Seg*>(sp + 128);                          // [MAXSEG]
-  uint8_t* eseg = reinterpret_cast<uint8_t*>(seg + MAXSEG);             // [128] segment of entry e
-  int* nseg_ent = reinterpret_cast<int*>(eseg + 128);                   // {#segments, #entries}
-  int4* ent = reinterpret_cast<int4*>(nseg_ent + 4);                   // [128] {fl, fh, u, dst row}
+  uint64_t* tfull = empty + STAGES;       // [2]
+  uint64_t* tempty = tfull + 2;           // [2]
+  uint64_t* tabfull = tempty + 2;         // [2]
+  uint64_t* tabempty = tabfull + 2;       // [2]
+  uint64_t* hfull = tabempty + 2;         // [2]
+  uint64_t* hempty = hfull + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
+  uint8_t* dstage = smem + STAGES * STAGE_BYTES;                    // [2 groups][128][32] fp32
+  const DhTab* tabs_s = reinterpret_cast<const DhTab*>(smem + TAB_OFF);
+  uint8_t* hbuf = smem + H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.S, F = p.F, RT = F * S;
-  const long long g0 = (long long)blockIdx.x * F;                      // first flattened frame
-  const long long m0 = g0 * S;                                          // first row
   const long long NT = (long long)p.N * p.T;
-  const int j0 = blockIdx.y * MAXN;
-  const int nj = min(MAXN, p.J - j0);               // columns of this CTA
-  const int nsub = (nj + NSUB - 1) / NSUB;
-  const int nbox = (nj + 63) / 64;
+  const long long nitems = (long long)(*p.nlive) * p.njp;
 
-  // ---- per-frame tables of the tile (parallel global loads): p_t (dead = -1), p_{t+1}, n, t
-  int* spn = reinterpret_cast<int*>(ent + 128);                          // [128] p_{t+1}
-  int* sfn = spn + 128;                                                  // [128] utterance n
-  int* sft = sfn + 128;                                                  // [128] frame t
-  if (threadIdx.x < F) {
-    const long long g = g0 + threadIdx.x;
-    int pv = -1, pn = 0, n = -1, t = 0;
-    if (g < NT) {
-      n = (int)(g / p.T);
-      t = (int)(g - (long long)n * p.T);
-      const int Tn = utt_T(p.bnd, n), Un = utt_U(p.bnd, n);
-      if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) {
-        pv = p.ranges[(size_t)n * p.T + t];
-        if (t + 1 < Tn) pn = p.ranges[(size_t)n * p.T + t + 1];
-      }
-    }
-    sp[threadIdx.x] = pv;
-    spn[threadIdx.x] = pn;
-    sfn[threadIdx.x] = n;
-    sft[threadIdx.x] = t;
-  }
-  int act = 0;
-  for (int i = threadIdx.x; i < RT; i += blockDim.x)
-    if (m0 + i < p.g.R && p.g.rowinfo[m0 + i] >= 0) act = 1;
-  const bool any = __syncthreads_or(act);
-
-  if (!any) {
-    // no live row: d_enc of the tile's frames is zero (d_dec gets nothing from this tile)
-    if (p.d_enc)
-      for (int idx = threadIdx.x; idx < F * (nj / 4); idx += blockDim.x) {
-        const int f = idx / (nj / 4), jq = idx - f * (nj / 4);
-        if (g0 + f < NT)
-          reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0)[jq] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    return;
-  }
-  if (warp == 4 && lane == 0) {
+  if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
       tc::mbar_init(&full[s], 4);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(tfull, 1);
-    tc::mbar_init(hfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 8);
+      tc::mbar_init(&tabfull[s], 1);
+      tc::mbar_init(&tabempty[s], 8);
+      tc::mbar_init(&hfull[s], 1);
+      tc::mbar_init(&hempty[s], 8);
+    }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
     tc::tma_prefetch(&tmW);
     tc::tma_prefetch(&tmH);
   }
-  if (warp == 4) tc::tmem_alloc(tmem_slot, MAXN);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * NSUB);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
-  const int grows = (int)min((long long)BM, p.g.R - m0);   // rows of the packed-scalar copy
 
-  if (warp < 4) {
-    // ---- producers: thread = tile row; transform the 8 chunks of its row in place
-    const int rl = threadIdx.x;
-    const long long r = m0 + rl;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer
+      int stage = 0, it = 0;
+      uint32_t ph = 0;
+      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
+        const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+        const int slot = it & 1;
+        tc::mbar_wait(&tabempty[slot], ((it >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&tabfull[slot], (uint32_t)sizeof(DhTab));
+        tc::bulk_load(smem + TAB_OFF + slot * TAB_BYTES, p.tabs + tile,
+                      (uint32_t)sizeof(DhTab), &tabfull[slot]);
+        const long long m0 = (long long)tile * RT;
+        const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
+        const int grows = (int)min((long long)BM, p.g.R - m0);
+        const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + (uint32_t)grows * 16u;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          tc::mbar_wait(&empty[stage], ph ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
+          tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
+          for (int bx = 0; bx < nbox; ++bx)
+            tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
+          tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0,
+                        (uint32_t)grows * 16u, &loaded[stage]);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+      }
+    } else if (lane == 1) {
+      // ---- h boxes for the epilogue: box i (columns j0 + 64 i) serves chunk 2i of group 0 and 2i+1 of group 1
+      int slot = 0;
+      uint32_t ph = 0;
+      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+        const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+        const int m0 = tile * RT, j0 = jp * NSUB;
+        const int nbox = (min(NSUB, p.J - j0) + 63) / 64;
+        for (int bx = 0; bx < nbox; ++bx) {
+          tc::mbar_wait(&hempty[slot], ph ^ 1);
+          tc::mbar_arrive_expect_tx(&hfull[slot], H_BYTES);
+          tc::tma_load_2d(hbuf + slot * H_BYTES, &tmH, &hfull[slot], j0 + bx * 64, m0);
+          if (++slot == 2) { slot = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer
+      constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
+      int stage = 0, it = 0;
+      uint32_t ph = 0;
+      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t d = tbase + acc * NSUB;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          tc::mbar_wait(&full[stage], ph);
+          tc::fence_after_sync();
+          const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024), idesc,
+                         (kb | k) != 0);
+          tc::mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        }
+        tc::mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp < 6) {
+    // ---- in-place dz producers: thread = tile row; transform the 8 chunks of its row
+    const int rl = threadIdx.x - 64;
     int stage = 0;
     uint32_t ph = 0;
-    for (int kb = 0; kb < p.nkb; ++kb) {
-      const int v0 = kb * BK;
-      tc::mbar_wait(&loaded[stage], ph);
-      uint8_t* sa = smem + stage * STAGE_BYTES;
-      const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
-                                                : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-      const int info = __float_as_int(gq.w);
+    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+      const int tile = p.live[idx / p.njp];
+      const long long m0 = (long long)tile * RT;
+      const int grows = (int)min((long long)BM, p.g.R - m0);
+      for (int kb = 0; kb < p.nkb; ++kb) {
+        const int v0 = kb * BK;
+        tc::mbar_wait(&loaded[stage], ph);
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
+                                                  : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        const int info = __float_as_int(gq.w);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4* q = reinterpret_cast<uint4*>(sa + sw128(rl, c));
-        const uint4 pv = *q;
-        *q = info >= 0 ? dz_chunk(pv, gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
-      }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&full[stage]);
-      if (++stage == STAGES) { stage = 0; ph ^= 1; }
-    }
-    // ---- tile tables (while the last MMAs drain): utterance segments from the per-frame smem
-    // tables, then one entry per token position of a segment: covering frames and destination
-    if (threadIdx.x == 0) {
-      int ns = 0, ne = 0;
-      for (int f = 0; f < F;) {
-        if (sp[f] < 0) { ++f; continue; }
-        const int n = sfn[f];
-        int fe = f + 1;
-        while (fe < F && sp[fe] >= 0 && sfn[fe] == n) ++fe;
-        Seg q;
-        q.n = n; q.fb = f; q.fe = fe; q.ta = sft[f];
-        q.ub = sp[f];
-        q.ue = min(utt_U(p.bnd, n), sp[fe - 1] + S - 1);
-        q.off = ne;
-        q.pnext = spn[fe - 1];
-        if (ns < MAXSEG) {
-          seg[ns] = q;
-          for (int e = 0; e <= q.ue - q.ub && ne + e < 128; ++e) eseg[ne + e] = (uint8_t)ns;
-          ++ns;
-          ne += q.ue - q.ub + 1;
+        for (int c = 0; c < 8; ++c) {
+          uint4* q = reinterpret_cast<uint4*>(sa + sw128(rl, c));
+          const uint4 pv = *q;
+          *q = info >= 0 ? dz_chunk(pv, gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
         }
-        f = fe;
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&full[stage]);
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
       }
-      nseg_ent[0] = ns;
-      nseg_ent[1] = min(ne, 128);
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    //   dst >= 0: row n(U+1)+u of d_dec (complete here); dst < 0: row -(1+dst) of the partial buffer
-    if (threadIdx.x < nseg_ent[1]) {
-      const int e = threadIdx.x;
-      const Seg q = seg[eseg[e]];
-      const int u = q.ub + (e - q.off);
-      const int2 cov = p.urange[(size_t)q.n * (p.U + 1) + u];           // frames [lo, hi) covering u
-      const int fl = max(q.fb, cov.x - q.ta + q.fb), fh = min(q.fe, cov.y - q.ta + q.fb);
-      const int tb = q.ta + (q.fe - q.fb);
-      int dst;
-      if (cov.x >= q.ta && cov.y <= tb) dst = q.n * (p.U + 1) + u;                               // complete here
-      else if (cov.x < q.ta) dst = -1 - (int)((blockIdx.x * 2 + 0) * S + (u - q.ub));          // left boundary
-      else dst = -1 - (int)((blockIdx.x * 2 + 1) * S + (u - q.pnext));                          // right boundary
-      ent[e] = make_int4(fl, fh, u, dst);
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    // ---- epilogue
-    tc::mbar_wait(tfull, 0);
-    tc::fence_after_sync();
-    tc::mbar_wait(hfull, 0);
-    const bool live = rl < RT && r < p.g.R && p.g.rowinfo[r] >= 0;
-    const uint32_t tl = tbase + ((uint32_t)(32 * warp) << 16);
-    // dpre chunk staging: row r, float4 group q (columns 4q..4q+3) at D4[r * 8 + (q ^ (r & 7))]
-    float4* D4 = reinterpret_cast<float4*>(smem + D_OFF);
-    const int nseg = nseg_ent[0], nent = nseg_ent[1];
-    for (int c0 = 0; c0 < nj; c0 += 32) {
-      float acc[32];
-      tc::tmem_ld32(tl + c0, acc);
-      const uint8_t* hb = smem + (c0 >> 6) * H_BYTES;         // 64-column box of h
-      const int qh = ((c0 >> 5) & 1) * 4;                     // 16-B chunk of the 32-column half
-      const int nq = min(4, (nj - c0) / 8);                   // J % 8 == 0
+  } else {
+    // ---- epilogue: group g (warps 6-9 / 10-13) takes the 32-column chunks c0 = 32 (2i + g);
+    // quadrant q = warp % 4 owns TMEM lanes (tile rows) 32q..32q+31
+    const int q4 = warp & 3, g = (warp - 6) >> 2;
+    const int rl = 32 * q4 + lane;                      // tile row of this thread
+    const int gt = threadIdx.x - 192 - 128 * g;          // 0..127 within the group
+    float4* D4 = reinterpret_cast<float4*>(dstage + g * D_BYTES);
+    const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
+    int it = 0, hslot = 0;
+    uint32_t hph = 0;
+    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
+      const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+      const int slot = it & 1, acc = it & 1;
+      const long long m0 = (long long)tile * RT, g0 = (long long)tile * F;
+      const long long r = m0 + rl;
+      const bool live = rl < RT && r < p.g.R && p.g.rowinfo[r] >= 0;
+      const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
+      const int nbox = (nj + 63) / 64;
+      const DhTab* tb = reinterpret_cast<const DhTab*>(reinterpret_cast<const uint8_t*>(tabs_s) + slot * TAB_BYTES);
+      tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::fence_after_sync();
+      const int nent = tb->nent;
+      for (int bx = 0; bx < nbox; ++bx) {
+        const int c0 = 64 * bx + 32 * g;
+        tc::mbar_wait(&hfull[hslot], hph);
+        const bool have = c0 < nj;
+        float accv[32];
+        if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
+        const uint8_t* hb = hbuf + hslot * H_BYTES;
+        const int nq = have ? min(4, (nj - c0) / 8) : 0;           // J % 8 == 0
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float out[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (q < nq && live) {
-          const uint4 hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, qh + q));
-          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+        for (int qq = 0; qq < 4; ++qq) {
+          float out[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (qq < nq && live) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, 4 * g + qq));
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
-            out[2 * i] = acc[8 * q + 2 * i] * (1.f - ha * ha);            // d tanh
-            out[2 * i + 1] = acc[8 * q + 2 * i + 1] * (1.f - hb2 * hb2);
+            for (int i = 0; i < 4; ++i) {
+              const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
+              out[2 * i] = accv[8 * qq + 2 * i] * (1.f - ha * ha);            // d tanh
+              out[2 * i + 1] = accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2);
+            }
           }
+          D4[rl * 8 + ((2 * qq) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
+          D4[rl * 8 + ((2 * qq + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
         }
-        D4[rl * 8 + ((2 * q) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
-        D4[rl * 8 + ((2 * q + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int ncol4 = min(32, nj - c0) / 4;
-      // d_enc: one float4 output per (frame, 4-column group)
-      if (p.d_enc)
-        for (int idx = threadIdx.x; idx < F * 8; idx += 128) {
-          const int f = idx >> 3, q = idx & 7;
-          if (q < ncol4 && g0 + f < NT) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
+        if (++hslot == 2) { hslot = 0; hph ^= 1; }
+        if (!have) continue;
+        if (c0 + 64 >= nj) {            // last TMEM read of this accumulator by this warp
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        const int ncol4 = min(32, nj - c0) / 4;
+        // d_enc: one float4 output per (frame, 4-column group)
+        if (p.d_enc)
+          for (int i = gt; i < F * 8; i += 128) {
+            const int f = i >> 3, qq = i & 7;
+            if (qq < ncol4 && g0 + f < NT) {
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int s = 0; s < S; ++s) {
+                const int rr = f * S + s;
+                const float4 x = D4[rr * 8 + (qq ^ (rr & 7))];
+                v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+              }
+              reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0 + c0)[qq] = v;
+            }
+          }
+        // d_dec: one float4 output per (token position of a segment, 4-column group)
+        if (p.d_dec)
+          for (int i = gt; i < nent * 8; i += 128) {
+            const int e = i >> 3, qq = i & 7;
+            if (qq >= ncol4) continue;
+            const int4 en = tb->ent[e];
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s = 0; s < S; ++s) {
-              const int rr = f * S + s;
-              const float4 x = D4[rr * 8 + (q ^ (rr & 7))];
+            for (int f = en.x; f < en.y; ++f) {
+              const int rr = f * S + (en.z - tb->sp[f]);
+              const float4 x = D4[rr * 8 + (qq ^ (rr & 7))];
               v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
             }
-            reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0 + c0)[q] = v;
+            float* dst = en.w >= 0 ? p.d_dec + (size_t)en.w * p.J : p.g_part + (size_t)(-1 - en.w) * p.J;
+            reinterpret_cast<float4*>(dst + j0 + c0)[qq] = v;
           }
-        }
-      // d_dec: one float4 output per (token position of a segment, 4-column group)
-      if (p.d_dec)
-        for (int idx = threadIdx.x; idx < nent * 8; idx += 128) {
-          const int e = idx >> 3, q = idx & 7;
-          if (q >= ncol4) continue;
-          const int4 en = ent[e];
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int f = en.x; f < en.y; ++f) {
-            const int rr = f * S + (en.z - sp[f]);
-            const float4 x = D4[rr * 8 + (q ^ (rr & 7))];
-            v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
-          }
-          float* dst = en.w >= 0 ? p.d_dec + (size_t)en.w * p.J : p.part + (size_t)(-1 - en.w) * p.J;
-          reinterpret_cast<float4*>(dst + j0 + c0)[q] = v;
-        }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-    }
-    (void)nseg;
-  } else if (lane == 0) {
-    // ---- warp 4 lane 0: TMA for A = P~[m0.., kb*64..], B = W[kb*64.., j0..] and the rows' scalars
-    const uint32_t gbytes = (uint32_t)grows * 16u;
-    const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;
-    int stage = 0;
-    uint32_t ph = 0;
-    for (int kb = 0; kb < p.nkb; ++kb) {
-      tc::mbar_wait(&empty[stage], ph ^ 1);
-      uint8_t* sa = smem + stage * STAGE_BYTES;
-      tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
-      tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
-      for (int bx = 0; bx < nbox; ++bx)
-        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
-      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0, gbytes, &loaded[stage]);
-      if (++stage == STAGES) { stage = 0; ph ^= 1; }
-    }
-    // h tiles for the epilogue, into the idle stage buffers once the MMAs are done
-    tc::mbar_wait(tfull, 0);
-    tc::mbar_arrive_expect_tx(hfull, (uint32_t)nbox * H_BYTES);
-    for (int bx = 0; bx < nbox; ++bx) tc::tma_load_2d(smem + bx * H_BYTES, &tmH, hfull, j0 + bx * 64, (int)m0);
-  } else if (lane == 1) {
-    // ---- warp 4 lane 1: MMA issuer
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
-    int stage = 0;
-    uint32_t ph = 0;
-    for (int kb = 0; kb < p.nkb; ++kb) {
-      tc::mbar_wait(&full[stage], ph);
-      tc::fence_after_sync();
-      const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
-      for (int ns = 0; ns < nsub; ++ns) {
-#pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          tc::mma_bf16(tbase + ns * NSUB, tc::sdesc(a + 32 * k, 16, 1024),
-                       tc::sdesc(b + ns * 4 * (64 * BK * 2) + 2048 * k, 64 * BK * 2, 1024), idesc, (kb | k) != 0);
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
       }
-      tc::mma_commit(&empty[stage]);
-      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      if (nj <= 32 * g) {               // this group had no chunk: still release the accumulator
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tabempty[slot]);
     }
-    tc::mma_commit(tfull);
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) tc::tmem_dealloc(tbase, MAXN);
+  if (warp == 1) tc::tmem_dealloc(tbase, 2 * NSUB);
 }
 
 // d_dec for the token positions whose covering frames span several tiles (sum of the boundary
@@ -591,7 +683,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
 // ======================================================================= host
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
                              const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
-                             float* d_dec, float* part, cudaStream_t st) {
+                             float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
@@ -602,9 +694,16 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     attr = true;
   }
   const int F = d.dh_frames();
-  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, d.N, d.T, d.U, d.S, F, ranges, urange, bnd, d_enc, d_dec,
-                   part};
-  dim3 grid((unsigned)d.dh_tiles(), (d.J + jdh::MAXN - 1) / jdh::MAXN);
+  const long long ntiles = d.dh_tiles();
+  cudaMemsetAsync(nlive, 0, sizeof(int), st);
+  RNNT_LAUNCH(KID_DENC, st, dh_tables_kernel<<<(unsigned)ntiles, 128, 0, st>>>(
+      ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, static_cast<DhTab*>(tabs), live, nlive, d_enc));
+  const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
+                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part};
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
   RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   if (d_dec)
     RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(

@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float* Br = bhat + base + (size_t)(k + 1) * LU;
     const float2* XY = pxy + base + (size_t)k * LU;
     float z = 0.f;
+#pragma unroll 2
     for (int u = lane; u < UP; u += 32) {
       float yv = 0.f, bv = 0.f;
       if (u >= ulo && u <= uhi) {
@@ -361,31 +362,43 @@ __global__ void __launch_bounds__(256) combine_kernel(
   }
   __syncthreads();
 
-  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t
+  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t.
+  // Four rows per warp iteration with their 1/S loads issued first (the loop is load-latency bound).
   const int tlo = max(0, k0 - UP + 1), thi = min(T - 1, k0 + 31);
-  for (int t = tlo + warp; t <= thi; t += 8) {
-    const int kr = lane, u = k0 + kr - t;
-    if (u < 0 || u >= UP) continue;
-    const float rz = s_rz[kr];
-    const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
-    if (u < U1) {
-      const size_t o = ((size_t)n * T + t) * U1 + u;
-      px_grad[o] = yv;
-      py_grad[o] = bv;
+  constexpr int RB = 4;
+  for (int tb = tlo + warp * RB; tb <= thi; tb += 8 * RB) {
+    const int kr = lane;
+    float rsv[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int t = tb + i, u = k0 + kr - t;
+      rsv[i] = (t <= thi && u >= 0 && u < U1) ? rS[((size_t)n * T + t) * UP + u] : 0.f;   // rS: live cells only
     }
-    // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
-    const size_t og = ((size_t)n * T + t) * UP + u;
-    const float sgv = yv + bv;
-    const float g = (u < U1 && sgv != 0.f) ? sgv * rS[og] : 0.f;   // rS is only written for live cells
-    const __nv_bfloat16 gh = __float2bfloat16_rn(g);
-    const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
-    Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
-    Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
-    // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
-    const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
-    const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
-    Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
-    Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
+    const float rz = s_rz[kr];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int t = tb + i, u = k0 + kr - t;
+      if (t > thi || u < 0 || u >= UP) continue;
+      const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
+      if (u < U1) {
+        const size_t o = ((size_t)n * T + t) * U1 + u;
+        px_grad[o] = yv;
+        py_grad[o] = bv;
+      }
+      // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
+      const size_t og = ((size_t)n * T + t) * UP + u;
+      const float sgv = yv + bv;
+      const float g = (u < U1 && sgv != 0.f) ? sgv * rsv[i] : 0.f;
+      const __nv_bfloat16 gh = __float2bfloat16_rn(g);
+      const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
+      Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
+      Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
+      // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
+      const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
+      const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
+      Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
+      Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
+    }
   }
 }
 

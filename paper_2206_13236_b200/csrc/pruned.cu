@@ -10,6 +10,8 @@
 //   K9c pruned_combine        g_b = empty'_p, g_l = y'_p per row; sc = gs (g_b+g_l) e^{m_tile-lse}
 //   K10 DhGemm + reduce       dpre = (W^T dz) (1-h^2); d_enc = sum_s dpre; d_dec gather-reduce
 //   K11 DwGemm (split-K)      d_w = sum dz h^T, d_b = sum dz, deterministic split reduction
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 #include "workspace.h"
@@ -33,16 +35,18 @@ struct GradSrc {
 };
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
                              const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
-                             float* d_dec, float* part, cudaStream_t st);
+                             float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st);
 cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
                              int splits, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
-// One CTA per frame (n, t); threads over (slot s, 8-column group) of its S band rows: 16 B of
-// bf16 out per thread (enc[t] is read once per frame and reused from L1 across the S rows).
-__global__ void __launch_bounds__(256) prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
-                                                    const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
-                                                    int T, int U, int J, int S, uint16_t* __restrict__ h) {
+// One CTA per frame (n, t), one thread per (slot s, 8-column group) of its S band rows (blockDim =
+// S * J/8 rounded up to a warp, looping only when that exceeds 1024): 16 B of bf16 out per thread;
+// enc[t] is read once per frame and reused from L1 across the S rows.  Rows of padded frames and
+// masked slots are written as zeros (the joiner GEMMs read whole 128-row tiles).
+__global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
+                                                     const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
+                                                     int T, int U, int J, int S, uint16_t* __restrict__ h) {
   const int nt = blockIdx.x;
   const int n = nt / T, t = nt - n * T;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
@@ -55,16 +59,15 @@ __global__ void __launch_bounds__(256) prune_kernel(const float* __restrict__ en
     uint4 out = make_uint4(0, 0, 0, 0);
     if (t < Tn && u <= Un) {
       const float* d = dec + ((size_t)n * (U + 1) + u) * J + j0;
-      const float4 e0 = *reinterpret_cast<const float4*>(e + j0), e1 = *reinterpret_cast<const float4*>(e + j0 + 4);
-      const float4 d0 = *reinterpret_cast<const float4*>(d), d1 = *reinterpret_cast<const float4*>(d + 4);
+      const float4 e0 = __ldg(reinterpret_cast<const float4*>(e + j0)), e1 = __ldg(reinterpret_cast<const float4*>(e + j0 + 4));
+      const float4 d0 = __ldg(reinterpret_cast<const float4*>(d)), d1 = __ldg(reinterpret_cast<const float4*>(d + 4));
       const float x[8] = {e0.x + d0.x, e0.y + d0.y, e0.z + d0.z, e0.w + d0.w,
                           e1.x + d1.x, e1.y + d1.y, e1.z + d1.z, e1.w + d1.w};
       uint32_t w[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint32_t lo = f_to_bf16_bits_rn(tanh_fast(x[2 * q]));
-        const uint32_t hi = f_to_bf16_bits_rn(tanh_fast(x[2 * q + 1]));
-        w[q] = lo | (hi << 16);
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(tanh_fast(x[2 * q]), tanh_fast(x[2 * q + 1]));
+        w[q] = *reinterpret_cast<const uint32_t*>(&h2);
       }
       out = make_uint4(w[0], w[1], w[2], w[3]);
     }
@@ -135,187 +138,273 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
 }
 
 // ------------------------------------------------------------------ K9 pruned recursion
-// Eq. 3 on the band (Fig. 1b lattice).  grid (N, 2): y = 0 alpha, y = 1 beta.
-// Lane s of warp 0 owns band slot s; it processes frame t at anti-diagonal k = d_t + s with
-// d_t = t + p_t strictly increasing (Eq. 9), so both in-arcs of a cell were produced one step
-// earlier: the vertical one by lane s-1 (same frame), the horizontal one by lane s + p_t - p_{t-1}
-// (previous frame).  The state is fp32 rebased per anti-diagonal exactly as in lattice.cu
-// (A_k = A_{k-2} + max of diagonal k-2, one CREDUX per step); shifts are kept in fp64.
-// Arcs (px2 = y_p log2e, py2 = empty_p log2e; kNegBig off the lattice) and p_t are staged in smem.
-__device__ __forceinline__ float plae2(float a, float b, float c) {
+// Eq. 3 on the band (Fig. 1b lattice) as a chunked scan over frames in the
+// (log-add, +) semiring.  Slot s of frame t is node (t, p_t + s).  Forward, frame t >= 1:
+//   h[s] = alpha(t-1, s + d_t) + empty(t-1, s + d_t)        (d_t = p_t - p_{t-1}; -inf if s+d_t >= S)
+//   alpha(t, s) = LogAdd(h[s], alpha(t, s-1) + y(t, s-1))    (the vertical chain inside the frame)
+// i.e. alpha_t = alpha_{t-1} (x) M_t with an S x S transfer matrix M_t.  Backward mirrors it:
+//   g[s] = beta(t+1, s - d_{t+1}) + empty(t, s),  beta(t, s) = LogAdd(g[s], beta(t, s+1) + y(t, s)),
+// with beta(T-1, U - p_{T-1}) = empty(T-1, U) (the terminal blank).
+// Instead of T_n + U_n dependent anti-diagonal steps the kernel does three short phases:
+//   A  (parallel over chunks of C frames) the chunk transfer matrix P_c = M_{t0} (x) ... (x) M_{t1-1},
+//      lane s of an S-lane segment holding column s (forward) / row s (backward) in registers;
+//   B  (one segment) the boundary vectors alpha_{end of chunk c} = alpha_{start} (x) P_c, sequentially;
+//   C  (parallel over chunks) every frame of the chunk from its boundary vector; writes alpha-hat.
+// The frame step is one shuffle (the band shift d_t) plus S-1 shuffle + LogAdd steps (the chain).
+// Precision: every vector / matrix is rebased before each frame by an integer (exact in fp32)
+// taken from slot 0 -- node (t, p_t) is reachable from (0,0) and reaches (T-1, U_n) on every
+// consistent band (Eq. 9-10), so its value is finite -- and the shifts are summed in fp64 per frame:
+//   alpha(t,s) log2e = ap[r] + Af[n,t],  beta(t,s) log2e = bp[r] + Bf[n,t].
+// Arcs are base 2 (px2 = y log2e, py2 = empty log2e, kNegBig off the lattice / at masked slots).
+__device__ __forceinline__ float lae2(float a, float b) {
   const float m = fmaxf(a, b);
-  return (m - c) + lg2_approx(1.0f + ex2_approx(-fabsf(a - b)));
+  return m + lg2_approx(1.0f + ex2_approx(-fabsf(a - b)));
 }
+__device__ __forceinline__ float rebase_of(float v) { return v > -1e29f ? rintf(v) : 0.f; }
 
-// Per (anti-diagonal k, slot s) step record, built in a parallel prepass so that the wavefront
-// loop only does value arithmetic: arcs {y, empty} and a code word
-//   bits 0-15 frame t | 16-21 source lane + 1 of the frame-crossing arc (0: none) | flags below.
-constexpr int kPfAct = 1 << 22, kPfMasked = 1 << 23, kPfFirst = 1 << 24, kPfLast = 1 << 25, kPfUeq = 1 << 26,
-              kPfUlt = 1 << 27;
+struct StepIn {
+  int t, d;
+  bool act;
+  float py, px;
+};
 
-__global__ void __launch_bounds__(256) pruned_fb_kernel(
-    const float* __restrict__ px2, const float* __restrict__ py2, const int32_t* __restrict__ ranges,
-    const int64_t* __restrict__ bnd, int T, int S, int K, float* __restrict__ ap, float* __restrict__ bp,
-    float* __restrict__ Aps, float* __restrict__ Bps, double* __restrict__ Lp, float* __restrict__ loss,
-    int32_t* __restrict__ status) {
+struct ScanParams {
+  const float *px2, *py2;
+  const int32_t* ranges;
+  const int64_t* bnd;
+  int T, S, C, ncmax;
+  float *ap, *bp;
+  double *Af, *Bf;   // (N, T) per-frame shifts (log2 units)
+  double* Lp;
+  float* loss;
+  int32_t* status;
+};
+
+template <int SMAX>
+__global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const int S = q.S, C = q.C;
+  const int Tn = utt_T(q.bnd, n), Un = utt_U(q.bnd, n);
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   if (!feasible) {
     if (fwd && threadIdx.x == 0) {
-      Lp[n] = neg_inf_d();
-      loss[n] = __int_as_float(0x7f800000);  // +inf: no band-respecting path (kept visible, D16)
-      set_status(status, n, kStatusInfeasible);
+      q.Lp[n] = neg_inf_d();
+      q.loss[n] = __int_as_float(0x7f800000);  // +inf: no band-respecting path (kept visible, D16)
+      set_status(q.status, n, kStatusInfeasible);
     }
     return;
   }
-  const size_t rbase = (size_t)n * T * S;
-  const int* pr = ranges + (size_t)n * T;
-  const int dlast = (Tn - 1) + pr[Tn - 1];          // d_{T-1}
-  const int kend = dlast + S - 1;                    // last anti-diagonal holding a band cell
-  // smem: records [(kend+1) * S] {float2 arcs, int code}
-  float2* rxy = reinterpret_cast<float2*>(smem_raw);
-  int* rcode = reinterpret_cast<int*>(rxy + (size_t)(K + 1) * S);
-  const int nrec = (kend + 1) * S;
-  for (int i = threadIdx.x; i < nrec; i += blockDim.x) rcode[i] = 0;
-  __syncthreads();
-  for (int i0 = threadIdx.x; i0 < Tn * S; i0 += 4 * blockDim.x) {
-    float x[4], y[4];
-    int pp[4], pn[4];
+  // smem: chunk matrices Pm[c][lane s][i], their shifts, boundary vectors and their shifts
+  float* Pm = reinterpret_cast<float*>(smem_raw);
+  float* psh = Pm + (size_t)q.ncmax * S * S;
+  float* bv = psh + q.ncmax;
+  double* bsh = reinterpret_cast<double*>(smem_raw + ((((size_t)q.ncmax * S * S + q.ncmax + (size_t)(q.ncmax + 1) * S) * 4 + 15) / 16) * 16);
+  const size_t rb = (size_t)n * q.T * S;
+  const int* pr = q.ranges + (size_t)n * q.T;
+  const float* PX = q.px2 + rb;
+  const float* PY = q.py2 + rb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int spw = 32 / S;                       // segments per warp
+  const int seg = warp * spw + lane / S, s = lane % S;
+  const bool on = lane < spw * S;
+  const int base = lane - s;
+  const int nseg = 8 * spw;
+  const int nc = (Tn - 1 + C - 1) / C;          // chunks over frames 1..Tn-1 (fwd) / Tn-2..0 (bwd)
+  const float NB = kNegBig;
+  const int sU = Un - pr[Tn - 1];               // slot of (T-1, U)
+
+  // step i of chunk c: its frame (processing order), band shift and this lane's two arcs
+  //   fwd: d = p_t - p_{t-1}, py = empty(t-1, s) (sent along the shift), px = y(t, s) (sent up the chain)
+  //   bwd: d = p_{t+1} - p_t, py = empty(t, s), px = y(t, s) (both added on arrival)
+  // (neutral values on inactive lanes keep every shuffle warp-uniform)
+  auto load_step = [&](int c, int i, bool cact) {
+    StepIn r;
+    r.t = fwd ? 1 + c * C + i : Tn - 2 - c * C - i;
+    r.act = cact && (fwd ? r.t < Tn : r.t >= 0);
+    r.d = 0; r.py = NB; r.px = NB;
+    if (r.act) {
+      const int t = r.t;
+      r.d = fwd ? pr[t] - pr[t - 1] : pr[t + 1] - pr[t];
+      r.py = PY[(size_t)(fwd ? t - 1 : t) * S + s];
+      r.px = PX[(size_t)t * S + s];
+    }
+    return r;
+  };
+
+  // ---------------- phase A: chunk transfer matrices
+  const int rounds = (nc + nseg - 1) / nseg;
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int c = seg + rd * nseg;
+    const bool cact = on && c < nc;
+    float P[SMAX];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {                 // all loads of the four entries first (MLP)
-      const int i = i0 + q * blockDim.x;
-      x[q] = 0.f; y[q] = 0.f; pp[q] = 0; pn[q] = 0;
-      if (i < Tn * S) {
-        const int t = i / S;
-        x[q] = px2[rbase + i];
-        y[q] = py2[rbase + i];
-        pp[q] = pr[t];
-        pn[q] = fwd ? (t > 0 ? pr[t - 1] : 0) : (t < Tn - 1 ? pr[t + 1] : 0);
+    for (int i = 0; i < SMAX; ++i) P[i] = (i == s) ? 0.f : NB;   // identity
+    float shacc = 0.f;
+    StepIn nx = load_step(c, 0, cact);
+    for (int i = 0; i < C; ++i) {
+      const StepIn in = nx;
+      if (i + 1 < C) nx = load_step(c, i + 1, cact);   // next frame's arcs in flight during this step
+      const bool act = in.act;
+      const int d = in.d;
+      const float own_py = in.py, own_px = in.px;
+      const float m = rebase_of(__shfl_sync(0xffffffffu, P[0], base));   // P[0][0]
+      float X[SMAX];
+      if (fwd) {
+        const int src = (s + d < S) ? lane + d : lane;
+#pragma unroll
+        for (int k = 0; k < SMAX; ++k) {
+          if (k >= S) break;
+          const float v = __shfl_sync(0xffffffffu, P[k] + own_py, src);
+          X[k] = (s + d < S) ? v - m : NB;
+        }
+#pragma unroll 1
+        for (int j = 1; j < S; ++j) {
+#pragma unroll
+          for (int k = 0; k < SMAX; ++k) {
+            if (k >= S) break;
+            const float v = __shfl_up_sync(0xffffffffu, X[k] + own_px, 1);
+            if (s == j) X[k] = lae2(X[k], v);
+          }
+        }
+      } else {
+        const int src = (s - d >= 0) ? lane - d : lane;
+#pragma unroll
+        for (int k = 0; k < SMAX; ++k) {
+          if (k >= S) break;
+          const float v = __shfl_sync(0xffffffffu, P[k], src);
+          X[k] = (s - d >= 0) ? v + own_py - m : NB;
+        }
+#pragma unroll 1
+        for (int j = S - 2; j >= 0; --j) {
+#pragma unroll
+          for (int k = 0; k < SMAX; ++k) {
+            if (k >= S) break;
+            const float v = __shfl_down_sync(0xffffffffu, X[k], 1);
+            if (s == j) X[k] = lae2(X[k], v + own_px);
+          }
+        }
+      }
+      if (act) {
+#pragma unroll
+        for (int k = 0; k < SMAX; ++k) P[k] = X[k];
+        shacc += m;
       }
     }
+    if (cact) {
+      float* dst = Pm + ((size_t)c * S + s) * S;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = i0 + q * blockDim.x;
-      if (i >= Tn * S) break;
-      const int t = i / S, sl = i - t * S;
-      const int p = pp[q], u = p + sl, k = t + p + sl;
-      int src1 = 0;   // source lane + 1 of the arc crossing frames
-      if (fwd) {
-        if (t > 0) src1 = sl + p - pn[q] + 1;                          // (t-1, u) in frame t-1
-      } else if (t < Tn - 1) {
-        const int s2 = sl - (pn[q] - p);                               // (t+1, u) in frame t+1
-        src1 = s2 >= 0 ? s2 + 1 : 0;
-      }
-      int code = t | (min(src1, 63) << 16) | kPfAct;
-      if (u > Un) code |= kPfMasked;
-      if (t == 0) code |= kPfFirst;
-      if (t == Tn - 1) code |= kPfLast;
-      if (u == Un) code |= kPfUeq;
-      if (u < Un) code |= kPfUlt;
-      rxy[k * S + sl] = make_float2(x[q], y[q]);
-      rcode[k * S + sl] = code;
+      for (int k = 0; k < SMAX; ++k)
+        if (k < S) dst[k] = P[k];
+      if (s == 0) psh[c] = shacc;
     }
   }
   __syncthreads();
-  if (threadIdx.x >= 32) return;
-  const int s = threadIdx.x;
-  const bool on = s < S;
-  float* shift = (fwd ? Aps : Bps) + (size_t)n * (K + 1);
-  float* outv = (fwd ? ap : bp) + rbase;
-  const float NB = kNegBig;
-  float Sh = 0.f;   // shift of the current diagonal: an integer, exact in fp32
-  float Mm2 = 0.f, Mm1 = 0.f, cprev = 0.f;
 
-  // Blocks of 8 diagonals: the records of the block are loaded up front, then 8 straight-line steps.
-  constexpr int KB = 8;
-  if (fwd) {
-    float h_out = NB, v_out = NB;
-    int k_loss = -1;
-    float hl = NB;
-    for (int kb = 0; kb <= kend; kb += KB) {
-      int cd[KB];
-      float2 xy[KB];
-#pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        const int k = kb + j;
-        const bool ok = on && k <= kend;
-        cd[j] = ok ? rcode[k * S + s] : 0;
-        xy[j] = ok ? rxy[k * S + s] : make_float2(NB, NB);
+  // ---------------- phase B: boundary vectors (warp 0, segment 0)
+  if (warp == 0) {
+    const bool sa = lane < S;
+    float a = NB;
+    if (fwd) {
+      // frame 0: alpha(0,0) = 0, then the vertical chain
+      a = (s == 0) ? 0.f : NB;
+      const float own_px = sa ? PX[s] : NB;
+      for (int j = 1; j < S; ++j) {
+        const float v = __shfl_up_sync(0xffffffffu, a + own_px, 1);
+        if (lane == j) a = v;
       }
-#pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        const int k = kb + j, code = cd[j];
-        const int src = ((code >> 16) & 63) - 1;
-        // A_k = round(A_{k-2} + M_{k-2}); a diagonal with no live cell keeps A_k = A_{k-1}
-        const float ci = (k >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-        const float hin = __shfl_sync(0xffffffffu, h_out, src >= 0 ? src : s);
-        const float vin = __shfl_up_sync(0xffffffffu, v_out, 1);
-        const float left = (src >= 0 && src < S) ? hin : NB;
-        const float below = s > 0 ? vin : NB;
-        float a = ((code & kPfFirst) && s == 0) ? -ci : plae2(left, below, ci);
-        if (code & kPfMasked) a = NB;                      // masked slot (S > U_n + 1, D10)
-        const bool act = (code & kPfAct) != 0;
-        const float hn = a + xy[j].y, vn = a + xy[j].x;
-        h_out = act ? hn : h_out;
-        v_out = act ? vn : v_out;
-        if (act) outv[(code & 0xffff) * S + s] = a;
-        const float mx = act ? a : NB;
-        const bool fin = act && (code & kPfLast) && (code & kPfUeq);
-        k_loss = fin ? k : k_loss;
-        hl = fin ? hn : hl;
-        Sh += ci;
-        if (s == 0 && k <= kend) shift[k] = Sh;
-        if (k == k_loss && fin) {
-          // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band), in the frame A_k
-          const double L = ((double)hl + (double)Sh) * RNNT_LN2;
-          Lp[n] = L;
-          loss[n] = (float)(-L);
-          if (!isfinite(L) || L < -1e20) set_status(status, n, kStatusNonFinite);
-        }
-        const float Mk = warp_max_uniform_p(mx);
-        Mm2 = Mm1;
-        Mm1 = Mk;
-        cprev = ci;
+    } else {
+      // frame T-1: the terminal blank at slot sU, then the chain downwards
+      const size_t o = (size_t)(Tn - 1) * S + s;
+      const float own_px = sa ? PX[o] : NB;
+      a = (sa && s == sU) ? PY[o] : NB;
+      for (int j = S - 2; j >= 0; --j) {
+        const float v = __shfl_down_sync(0xffffffffu, a, 1);
+        if (lane == j) a = lae2(a, v + own_px);
       }
     }
-  } else {
-    float b_out = NB;
-    for (int kb = kend; kb >= 0; kb -= KB) {
-      int cd[KB];
-      float2 xy[KB];
+    double sh = 0.0;
+    if (sa) bv[s] = a;
+    if (lane == 0) bsh[0] = 0.0;
+    for (int c = 0; c < nc; ++c) {
+      const float m = rebase_of(__shfl_sync(0xffffffffu, a, 0));
+      const float* Pc = Pm + ((size_t)c * S + (sa ? s : 0)) * S;
+      float mx = NB, x[SMAX];
 #pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        const int k = kb - j;
-        const bool ok = on && k >= 0;
-        cd[j] = ok ? rcode[k * S + s] : 0;
-        xy[j] = ok ? rxy[k * S + s] : make_float2(NB, NB);
+      for (int k = 0; k < SMAX; ++k) {
+        const float ak = __shfl_sync(0xffffffffu, a, k < S ? k : 0);
+        x[k] = (k < S && sa) ? (ak - m) + Pc[k] : NB;
+        mx = fmaxf(mx, x[k]);
       }
+      float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < KB; ++j) {
-        const int k = kb - j, i = kend - k, code = cd[j];
-        const int src = ((code >> 16) & 63) - 1;
-        const float ci = (i >= 2 && Mm2 > -1e29f) ? rintf(Mm2 - cprev) : 0.f;
-        const float rin = __shfl_sync(0xffffffffu, b_out, src >= 0 ? src : s);
-        const float uin = __shfl_down_sync(0xffffffffu, b_out, 1);
-        float right;
-        if (code & kPfLast) right = (code & kPfUeq) ? xy[j].y : NB;       // terminal blank (virtual end, beta = 0)
-        else right = (src >= 0 && src < S) ? rin + xy[j].y : NB;
-        const float up = ((code & kPfUlt) && s + 1 < S) ? uin + xy[j].x : NB;
-        float b = plae2(right, up, ci);
-        if (code & kPfMasked) b = NB;
-        const bool act = (code & kPfAct) != 0;
-        b_out = act ? b : b_out;
-        if (act) outv[(code & 0xffff) * S + s] = b;
-        const float mx = act ? b : NB;
-        Sh += ci;
-        if (s == 0 && k >= 0) shift[k] = Sh;
-        const float Mk = warp_max_uniform_p(mx);
-        Mm2 = Mm1;
-        Mm1 = Mk;
-        cprev = ci;
+      for (int k = 0; k < SMAX; ++k)
+        if (k < S) acc += ex2_approx(x[k] - mx);
+      a = mx + lg2_approx(acc);
+      sh += (double)m + (double)psh[c];
+      if (sa) bv[(c + 1) * S + s] = a;
+      if (lane == 0) bsh[c + 1] = sh;
+    }
+  }
+  __syncthreads();
+
+  // ---------------- phase C: every frame of every chunk from its boundary vector
+  float* outp = (fwd ? q.ap : q.bp) + rb;
+  double* Fs = (fwd ? q.Af : q.Bf) + (size_t)n * q.T;
+  if (warp == 0 && lane < S) {       // the boundary frame 0 (fwd) / T-1 (bwd) itself
+    const int t0 = fwd ? 0 : Tn - 1;
+    outp[(size_t)t0 * S + s] = bv[s];
+    if (s == 0) Fs[t0] = 0.0;
+    if (fwd && Tn == 1 && s == sU) {
+      const double L = ((double)bv[s] + (double)PY[(size_t)s]) * RNNT_LN2;   // alpha + empty(T-1,U)
+      q.Lp[n] = L;
+      q.loss[n] = (float)(-L);
+      if (!isfinite(L) || L < -1e20) set_status(q.status, n, kStatusNonFinite);
+    }
+  }
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int c = seg + rd * nseg;
+    const bool cact = on && c < nc;
+    float a = cact ? bv[(size_t)c * S + s] : NB;
+    double sh = cact ? bsh[c] : 0.0;
+    StepIn nx = load_step(c, 0, cact);
+    for (int i = 0; i < C; ++i) {
+      const StepIn in = nx;
+      if (i + 1 < C) nx = load_step(c, i + 1, cact);
+      const int t = in.t;
+      const bool act = in.act;
+      const int d = in.d;
+      const float own_py = in.py, own_px = in.px;
+      const float m = rebase_of(__shfl_sync(0xffffffffu, a, base));
+      float x;
+      if (fwd) {
+        const float v = __shfl_sync(0xffffffffu, a + own_py, (s + d < S) ? lane + d : lane);
+        x = (s + d < S) ? v - m : NB;
+        for (int j = 1; j < S; ++j) {
+          const float w = __shfl_up_sync(0xffffffffu, x + own_px, 1);
+          if (s == j) x = lae2(x, w);
+        }
+      } else {
+        const float v = __shfl_sync(0xffffffffu, a, (s - d >= 0) ? lane - d : lane);
+        x = (s - d >= 0) ? v + own_py - m : NB;
+        for (int j = S - 2; j >= 0; --j) {
+          const float w = __shfl_down_sync(0xffffffffu, x, 1);
+          if (s == j) x = lae2(x, w + own_px);
+        }
+      }
+      if (act) {
+        a = x;
+        sh += (double)m;
+        outp[(size_t)t * S + s] = a;
+        if (s == 0) Fs[t] = sh;
+        if (fwd && t == Tn - 1 && s == sU) {
+          // L_pruned = alpha(T-1,U) + empty(T-1,U) (P:167-168 on the band)
+          const double L = ((double)a + (double)PY[(size_t)t * S + s] + sh) * RNNT_LN2;
+          q.Lp[n] = L;
+          q.loss[n] = (float)(-L);
+          if (!isfinite(L) || L < -1e20) set_status(q.status, n, kStatusNonFinite);
+        }
       }
     }
   }
@@ -325,11 +414,11 @@ __global__ void __launch_bounds__(256) pruned_fb_kernel(
 // the per-(row, tile) softmax scale of the logit gradient sc = gs (g_b + g_l) exp(m_tile - lse).
 __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float* __restrict__ py2,
                                       const float* __restrict__ ap, const float* __restrict__ bp,
-                                      const float* __restrict__ Aps, const float* __restrict__ Bps,
+                                      const double* __restrict__ Af, const double* __restrict__ Bf,
                                       const double* __restrict__ Lp, const int32_t* __restrict__ ranges,
                                       const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
-                                      int N, int T, int S, int K, int ntile, float gs, float* __restrict__ gb,
+                                      int N, int T, int S, int ntile, float gs, float* __restrict__ gb,
                                       float* __restrict__ gl, float4* __restrict__ gpk) {
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long R = (long long)N * T * S;
@@ -343,17 +432,16 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   const int info = rowinfo[r];
   if (info >= 0 && isfinite(L2)) {
     const int p = ranges[(size_t)n * T + t];
-    const int u = p + s, k = t + u;
-    const float* A = Aps + (size_t)n * (K + 1);
-    const float* B = Bps + (size_t)n * (K + 1);
+    const int u = p + s;
+    const double At = Af[nt];
     const float a = ap[r];
-    if (u < Un && s + 1 < S)
-      yb = ex2_approx(a + px2[r] + bp[r + 1] + (float)((double)A[k] + (double)B[k + 1] - L2));
-    if (t < Tn - 1) {
+    if (u < Un && s + 1 < S)    // label arc (t,u) -> (t,u+1): both ends in frame t
+      yb = ex2_approx(a + px2[r] + bp[r + 1] + (float)(At + Bf[nt] - L2));
+    if (t < Tn - 1) {            // blank arc (t,u) -> (t+1,u)
       const int s2 = u - ranges[(size_t)n * T + t + 1];
-      if (s2 >= 0 && s2 < S) bb = ex2_approx(a + py2[r] + bp[r + S + (s2 - s)] + (float)((double)A[k] + (double)B[k + 1] - L2));
-    } else if (u == Un) {
-      bb = ex2_approx(a + py2[r] + (float)((double)A[k] - L2));
+      if (s2 >= 0 && s2 < S) bb = ex2_approx(a + py2[r] + bp[r + S + (s2 - s)] + (float)(At + Bf[nt + 1] - L2));
+    } else if (u == Un) {        // terminal blank
+      bb = ex2_approx(a + py2[r] + (float)(At - L2));
     }
   }
   gb[r] = bb;
@@ -362,9 +450,9 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   // {gs (g_b + g_l) exp(m_tile - lse), gs g_b, gs g_l, label}; dead rows {0, 0, 0, -1}
   const float l = lse[r];
   for (int tl = 0; tl < ntile; ++tl) {
-    float4 q = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-    if (info >= 0) q = make_float4(gs * (bb + yb) * expf(mt[r * ntile + tl] - l), gs * bb, gs * yb, __int_as_float(info));
-    gpk[(size_t)tl * R + r] = q;
+    float4 qv = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+    if (info >= 0) qv = make_float4(gs * (bb + yb) * expf(mt[r * ntile + tl] - l), gs * bb, gs * yb, __int_as_float(info));
+    gpk[(size_t)tl * R + r] = qv;
   }
 }
 
@@ -380,12 +468,36 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, 
 // ------------------------------------------------------------------ host drivers
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st) {
-  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((long long)d.N * d.T), 256, 0, st>>>(enc, dec, ranges, bnd, d.T, d.U,
-                                                                                      d.J, d.S, h));
+  const int threads = std::min(1024, (d.S * (d.J / 8) + 31) / 32 * 32);
+  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((long long)d.N * d.T), threads, 0, st>>>(enc, dec, ranges, bnd, d.T,
+                                                                                          d.U, d.J, d.S, h));
   return cudaGetLastError();
 }
 
-size_t pruned_recursion_smem(const Dims& d) { return (size_t)(d.K() + 1) * d.S * 12; }
+// Chunk length of the pruned scan: about sqrt(T) frames (phase B is T/C sequential steps, phase
+// C is C), raised until the chunk matrices fit in shared memory.
+static int scan_chunk(const Dims& d) {
+  int C = 4;
+  while ((long long)C * C < d.T) ++C;
+  auto bytes = [&](int c) {
+    const long long nc = (d.T + c - 1) / c + 1;
+    return ((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8;
+  };
+  while (bytes(C) > 160 * 1024) C *= 2;
+  return C;
+}
+size_t pruned_recursion_smem(const Dims& d) {
+  const int C = scan_chunk(d);
+  const long long nc = (d.T + C - 1) / C + 1;
+  return (size_t)(((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8);
+}
+
+template <int SMAX>
+static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cudaStream_t st) {
+  cudaFuncSetAttribute(pruned_scan_kernel<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  RNNT_LAUNCH(KID_PALPHA, st, pruned_scan_kernel<SMAX><<<dim3(d.N, 2), 256, sm, st>>>(q));
+  return cudaGetLastError();
+}
 
 // Forward: per-row info, K8 joiner with fused log-softmax, K9 recursion, the occupancies and the
 // packed backward scalars.
@@ -400,14 +512,15 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);
-    cudaFuncSetAttribute(pruned_fb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    RNNT_LAUNCH(KID_PALPHA, st, pruned_fb_kernel<<<dim3(d.N, 2), 256, sm, st>>>(w.px2, w.py2, ranges, bnd, d.T, d.S, d.K(),
-                                                                              w.ap, w.bp, w.Aps, w.Bps, w.Lp, loss,
-                                                                              status));
+    const int C = scan_chunk(d);
+    ScanParams q{w.px2, w.py2, ranges, bnd, d.T, d.S, C, (d.T + C - 1) / C + 1, w.ap, w.bp, w.Af, w.Bf, w.Lp, loss,
+                 status};
+    e = d.S <= 8 ? launch_scan<8>(d, q, sm, st) : d.S <= 16 ? launch_scan<16>(d, q, sm, st) : launch_scan<32>(d, q, sm, st);
+    if (e != cudaSuccess) return e;
   }
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
-      w.px2, w.py2, w.ap, w.bp, w.Aps, w.Bps, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, d.K(), nt,
-      gs, w.gb, w.gl, w.gpk));
+      w.px2, w.py2, w.ap, w.bp, w.Af, w.Bf, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
+      w.gl, w.gpk));
   return cudaGetLastError();
 }
 
@@ -418,7 +531,8 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
-  if ((e = joiner_dh_launch(d, g, h, W, ranges, w.urange, bnd, d_enc, d_dec, w.dpart, st)) != cudaSuccess) return e;
+  if ((e = joiner_dh_launch(d, g, h, W, ranges, w.urange, bnd, d_enc, d_dec, w.dpart, w.dhtab, w.dhlive,
+                            w.dhlive + d.dh_tiles(), st)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -415,18 +415,19 @@ struct NormProb {
           ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
         }
       }
-#pragma unroll 4
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int u = u0 + j;
         float px = kNegBig, py = kNegBig, r = 0.f;
         if (rowok && u <= Un) {
           const float S = acc[j];
           under |= !(S > 0.f);
-          const float Lnorm = __logf(S) + mam + mlm[c0 + j];         // L_normalizer(t,u), Eq. 6
-          if (u < Un) px = (ay[j] + lmy[c0 + j] - Lnorm) * RNNT_LOG2E_F;   // y(t,u), Eq. 1 + 5
+          // base-2 throughout: Lnorm2 = log2 S + (m_am + m_lm) log2e = L_normalizer(t,u) log2e, Eq. 6
+          const float Ln2 = lg2_approx(S) + (mam + mlm[c0 + j]) * RNNT_LOG2E_F;
+          if (u < Un) px = fmaf(ay[j] + lmy[c0 + j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
           // empty(t,u), Eq. 2 + 5; out of the last frame only the terminal blank exists
-          if (!(trow == Tn - 1 && u < Un)) py = (am0 + lm0[c0 + j] - Lnorm) * RNNT_LOG2E_F;
-          r = __frcp_rn(S);
+          if (!(trow == Tn - 1 && u < Un)) py = fmaf(am0 + lm0[c0 + j], RNNT_LOG2E_F, -Ln2);
+          r = rcp_approx(S);
         }
         bxy[e.lane][j] = make_float2(px, py);
         rs[j] = r;
@@ -565,7 +566,7 @@ struct AmProb {
       }
       const int nc = min(32, V - vc);
       warp_load_block(buf, am + row0 * V + vc, V, nin, nc, e.lane);
-#pragma unroll 8
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
         buf[e.lane][j] = live ? gs * (__expf(buf[e.lane][j] - mam) * a0[j] - pick) : 0.f;
@@ -676,7 +677,7 @@ struct LmProb {
       }
       const int nc = min(32, V - vc);
       warp_load_block(buf, lm + row0 * V + vc, V, nin, nc, e.lane);
-#pragma unroll 8
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int v = vc + j;
         const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);

@@ -76,15 +76,17 @@ struct PrunedWS {
   float* lse;        // (R) log-sum-exp of z
   float* px2;        // (R) y_p * log2e (band arcs)
   float* py2;        // (R) empty_p * log2e
-  float* ap;         // (R) pruned alpha-hat (log2, rebased per anti-diagonal)
+  float* ap;         // (R) pruned alpha-hat (log2, rebased per frame)
   float* bp;         // (R) pruned beta-hat
-  float* Aps;        // (N,K+1) pruned alpha shift per anti-diagonal (integer-valued)
-  float* Bps;        // (N,K+1) pruned beta shift
+  double* Af;        // (N,T) pruned alpha shift per frame (log2): alpha(t,s) log2e = ap + Af[t]
+  double* Bf;        // (N,T) pruned beta shift per frame
   double* Lp;        // (N) L_pruned
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
   float* dpart;      // (dh_tiles,2,S,J) d_dec boundary partials of the joiner_dh tiles
+  void* dhtab;       // (dh_tiles) joiner_dh tile tables (2576 B each, joiner_bwd.cu DhTab)
+  int* dhlive;       // (dh_tiles + 1) ids of the live joiner_dh tiles, then their count
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
   int splits;
@@ -153,13 +155,15 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.py2 = (float*)take(R * 4);
   p.ap = (float*)take(R * 4);
   p.bp = (float*)take(R * 4);
-  p.Aps = (float*)take(N * K1 * 4);
-  p.Bps = (float*)take(N * K1 * 4);
+  p.Af = (double*)take(N * T * 8);
+  p.Bf = (double*)take(N * T * 8);
   p.Lp = (double*)take(N * 8);
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);
   p.gpk = (float4*)take(R * NT * 16);
   p.dpart = (float*)take((size_t)d.dh_tiles() * 2 * d.S * J * 4);
+  p.dhtab = take((size_t)d.dh_tiles() * 2576);
+  p.dhlive = (int*)take(((size_t)d.dh_tiles() + 1) * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);
   if (sw) *sw = s;

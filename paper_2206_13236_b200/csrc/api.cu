@@ -36,6 +36,8 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
 
 namespace rnnt {
 void set_timeline(void* buf);
+void set_dh_trace(void* buf);
+void set_scan_trace(void* buf);
 static thread_local unsigned long long g_launches = 0;
 static thread_local int g_prof_id = 0;
 static thread_local cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
@@ -187,7 +189,7 @@ rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const u
   if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
   if (!aligned16(h) || !aligned16(w_out)) return RNNT_ERR_INVALID_ARG;
   if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
-  if (pruned_recursion_smem(d) > 200 * 1024) return RNNT_ERR_UNSUPPORTED;
+  if (pruned_recursion_smem(d) > 224 * 1024) return RNNT_ERR_UNSUPPORTED;
   SimpleWS sw;
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
@@ -206,7 +208,7 @@ rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out,
   if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
   if (!aligned16(h) || !aligned16(w_out)) return RNNT_ERR_INVALID_ARG;
   if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
-  if (pruned_recursion_smem(d) > 200 * 1024) return RNNT_ERR_UNSUPPORTED;
+  if (pruned_recursion_smem(d) > 224 * 1024) return RNNT_ERR_UNSUPPORTED;
   SimpleWS sw;
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
@@ -244,6 +246,10 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
 }
 
 /* diagnostics (not in rnnt.h): per-CTA phase timestamps of the simple-loss GEMMs into buf */
-void rnnt_debug_timeline(void* buf) { rnnt::set_timeline(buf); }
+void rnnt_debug_timeline(void* buf) {
+  rnnt::set_timeline(buf);
+  rnnt::set_dh_trace(buf ? static_cast<char*>(buf) + (4u << 20) : nullptr);   // joiner_dh trace 4 MiB in
+  rnnt::set_scan_trace(buf ? static_cast<char*>(buf) + (6u << 20) : nullptr); // pruned scan trace 6 MiB in
+}
 
 }  // extern "C"

@@ -34,20 +34,16 @@ struct GradSrc {
 // scale s, the picks gbs = gs g_b (v = 0) and gls = gs g_l (v = label `info`).  Returns the bf16
 // chunk and adds the bf16-rounded values (what the MMA consumes) to fsum when given.
 __device__ __forceinline__ uint4 dz_chunk(uint4 pv, float s, float gbs, float gls, int info, int vc, float* fsum) {
+  // branch-free: the blank pick is warp-uniform (vc), the label pick a per-lane select
   const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+  const int li = info - vc;
   float g[8];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    g[2 * i] = s * __uint_as_float(w[i] << 16);
-    g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u);
+    g[2 * i] = s * __uint_as_float(w[i] << 16) - (li == 2 * i ? gls : 0.f);
+    g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u) - (li == 2 * i + 1 ? gls : 0.f);
   }
   if (vc == 0) g[0] -= gbs;
-  const int li = info - vc;
-  if ((unsigned)li < 8u) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j == li) g[j] -= gls;
-  }
   uint32_t o[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -211,6 +207,27 @@ __global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restric
   }
 }
 
+// diagnostics: per (CTA, item) timestamps {producer start, first MMA, last MMA commit, epilogue
+// start (accumulator full), epilogue end}; 16 items per CTA
+__device__ unsigned long long* g_dh_trace = nullptr;
+void set_dh_trace(void* buf) { cudaMemcpyToSymbol(g_dh_trace, &buf, sizeof(buf)); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void dh_trace(int it, int k) {
+  if (g_dh_trace && it < 16) g_dh_trace[((size_t)blockIdx.x * 16 + it) * 5 + k] = gtimer();
+}
+// per (CTA, box < 4) of item 1, epilogue warp 6: {h ready, D4 staged, bar 1, d_enc done, d_dec done, bar 2}
+__device__ __forceinline__ void dh_trace_ep(int it, int bx, int k) {
+  if (g_dh_trace && it == 1 && bx < 4) g_dh_trace[148 * 16 * 5 + 148 * 3 * 8 * 4 + ((size_t)blockIdx.x * 4 + bx) * 6 + k] = gtimer();
+}
+// per (CTA, item < 3, k-block < 8): {TMA issued, stage seen loaded, transformed, MMA issued}
+__device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
+  if (g_dh_trace && it < 3 && kb < 8) g_dh_trace[148 * 16 * 5 + (((size_t)blockIdx.x * 3 + it) * 8 + kb) * 4 + k] = gtimer();
+}
+
 __global__ void __launch_bounds__(jdh::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
@@ -268,6 +285,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
         const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
         const int slot = it & 1;
+        dh_trace(it, 0);
         tc::mbar_wait(&tabempty[slot], ((it >> 1) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&tabfull[slot], (uint32_t)sizeof(DhTab));
         tc::bulk_load(smem + TAB_OFF + slot * TAB_BYTES, p.tabs + tile,
@@ -279,6 +297,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         for (int kb = 0; kb < p.nkb; ++kb) {
           tc::mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
+          dh_trace_kb(it, kb, 0);
           tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
           tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
           for (int bx = 0; bx < nbox; ++bx)
@@ -318,6 +337,8 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         for (int kb = 0; kb < p.nkb; ++kb) {
           tc::mbar_wait(&full[stage], ph);
           tc::fence_after_sync();
+          if (kb == 0) dh_trace(it, 1);
+          dh_trace_kb(it, kb, 3);
           const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
@@ -327,33 +348,37 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
         tc::mma_commit(&tfull[acc]);
+        dh_trace(it, 2);
       }
     }
   } else if (warp < 6) {
     // ---- in-place dz producers: thread = tile row; transform the 8 chunks of its row
     const int rl = threadIdx.x - 64;
-    int stage = 0;
+    int stage = 0, itx = 0;
     uint32_t ph = 0;
-    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++itx) {
       const int tile = p.live[idx / p.njp];
       const long long m0 = (long long)tile * RT;
       const int grows = (int)min((long long)BM, p.g.R - m0);
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int v0 = kb * BK;
         tc::mbar_wait(&loaded[stage], ph);
+        if (rl == 0) dh_trace_kb(itx, kb, 1);
         uint8_t* sa = smem + stage * STAGE_BYTES;
         const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
                                                   : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
         const int info = __float_as_int(gq.w);
+        uint4 pv[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4* q = reinterpret_cast<uint4*>(sa + sw128(rl, c));
-          const uint4 pv = *q;
-          *q = info >= 0 ? dz_chunk(pv, gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
-        }
+        for (int c = 0; c < 8; ++c) pv[c] = *reinterpret_cast<const uint4*>(sa + sw128(rl, c));
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(sa + sw128(rl, c)) =
+              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&full[stage]);
+        if (rl == 0) dh_trace_kb(itx, kb, 2);
         if (++stage == STAGES) { stage = 0; ph ^= 1; }
       }
     }
@@ -379,10 +404,13 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
+      if (warp == 6 && lane == 0) dh_trace(it, 3);
       const int nent = tb->nent;
       for (int bx = 0; bx < nbox; ++bx) {
         const int c0 = 64 * bx + 32 * g;
         tc::mbar_wait(&hfull[hslot], hph);
+        const bool trc = warp == 6 && lane == 0;
+        if (trc) dh_trace_ep(it, bx, 0);
         const bool have = c0 < nj;
         float accv[32];
         if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
@@ -413,7 +441,9 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
+        if (trc) dh_trace_ep(it, bx, 1);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        if (trc) dh_trace_ep(it, bx, 2);
         const int ncol4 = min(32, nj - c0) / 4;
         // d_enc: one float4 output per (frame, 4-column group)
         if (p.d_enc)
@@ -429,6 +459,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
               reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0 + c0)[qq] = v;
             }
           }
+        if (trc) dh_trace_ep(it, bx, 3);
         // d_dec: one float4 output per (token position of a segment, 4-column group)
         if (p.d_dec)
           for (int i = gt; i < nent * 8; i += 128) {
@@ -436,15 +467,23 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
             if (qq >= ncol4) continue;
             const int4 en = tb->ent[e];
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int f = en.x; f < en.y; ++f) {
-              const int rr = f * S + (en.z - tb->sp[f]);
-              const float4 x = D4[rr * 8 + (qq ^ (rr & 7))];
-              v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+            for (int f0 = en.x; f0 < en.y; f0 += 4) {     // four covering frames per step (loads in flight)
+              float4 x[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int f = f0 + k;
+                const int rr = f * S + (en.z - tb->sp[f < en.y ? f : en.x]);
+                x[k] = f < en.y ? D4[rr * 8 + (qq ^ (rr & 7))] : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) { v.x += x[k].x; v.y += x[k].y; v.z += x[k].z; v.w += x[k].w; }
             }
             float* dst = en.w >= 0 ? p.d_dec + (size_t)en.w * p.J : p.g_part + (size_t)(-1 - en.w) * p.J;
             reinterpret_cast<float4*>(dst + j0 + c0)[qq] = v;
           }
+        if (trc) dh_trace_ep(it, bx, 4);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        if (trc) dh_trace_ep(it, bx, 5);
       }
       if (nj <= 32 * g) {               // this group had no chunk: still release the accumulator
         tc::fence_before_sync();
@@ -453,6 +492,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tabempty[slot]);
+      if (warp == 6 && lane == 0) dh_trace(it, 4);
     }
   }
   tc::fence_before_sync();
@@ -590,15 +630,21 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
       tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
       const float4* gq = reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES);
-#pragma unroll 4
+      uint4 pv[8];
+      float4 sr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {     // all shared-memory loads of the 8 rows first
+        const int rl = g8 + 8 * i;
+        sr[i] = rl < grows ? gq[rl] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        pv[i] = *reinterpret_cast<const uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
+      }
+#pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int rl = g8 + 8 * i;
-        const float4 sr = rl < grows ? gq[rl] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
-        const int info = __float_as_int(sr.w);
-        uint4* q = reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
-        const uint4 pv = *q;
-        *q = info >= 0 ? dz_chunk(pv, sr.x, sr.y, sr.z, info, v0 + c * 8, want_db ? dsum : nullptr)
-                       : make_uint4(0, 0, 0, 0);
+        const int info = __float_as_int(sr[i].w);
+        *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) =
+            info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, v0 + c * 8, want_db ? dsum : nullptr)
+                      : make_uint4(0, 0, 0, 0);
       }
       tc::fence_proxy_async();
       __syncwarp();

@@ -162,6 +162,17 @@ __device__ __forceinline__ float lae2(float a, float b) {
 }
 __device__ __forceinline__ float rebase_of(float v) { return v > -1e29f ? rintf(v) : 0.f; }
 
+// diagnostics: per (utterance, direction) CTA timestamps {start, staged, phase A, phase B, phase C}
+__device__ unsigned long long* g_scan_trace = nullptr;
+void set_scan_trace(void* buf) { cudaMemcpyToSymbol(g_scan_trace, &buf, sizeof(buf)); }
+__device__ __forceinline__ void scan_trace(int k) {
+  if (g_scan_trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 5 + k] = t;
+  }
+}
+
 struct StepIn {
   int t, d;
   bool act;
@@ -180,12 +191,15 @@ struct ScanParams {
   int32_t* status;
 };
 
-template <int SMAX>
+// SMAX: register rows per lane; SC: the band width S as a compile-time constant (0: runtime S <= SMAX),
+// so that the per-row loops unroll without branches and the rows' shuffles and LogAdds interleave.
+template <int SMAX, int SC>
 __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = blockIdx.x;
   const bool fwd = blockIdx.y == 0;
-  const int S = q.S, C = q.C;
+  const int S = SC > 0 ? SC : q.S, C = q.C;
+  constexpr int KR = SC > 0 ? SC : SMAX;     // rows actually carried
   const int Tn = utt_T(q.bnd, n), Un = utt_U(q.bnd, n);
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
   if (!feasible) {
@@ -196,15 +210,31 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     }
     return;
   }
-  // smem: chunk matrices Pm[c][lane s][i], their shifts, boundary vectors and their shifts
+  scan_trace(0);
+  // smem: chunk matrices Pm[c][lane s][i], their shifts, boundary vectors and their shifts, then
+  // the utterance's band arcs and bounds (staged once, coalesced: every phase reads them from smem)
   float* Pm = reinterpret_cast<float*>(smem_raw);
   float* psh = Pm + (size_t)q.ncmax * S * S;
   float* bv = psh + q.ncmax;
-  double* bsh = reinterpret_cast<double*>(smem_raw + ((((size_t)q.ncmax * S * S + q.ncmax + (size_t)(q.ncmax + 1) * S) * 4 + 15) / 16) * 16);
+  const size_t mat_bytes = ((((size_t)q.ncmax * S * S + q.ncmax + (size_t)(q.ncmax + 1) * S) * 4 + 15) / 16) * 16;
+  double* bsh = reinterpret_cast<double*>(smem_raw + mat_bytes);
+  float* PXs = reinterpret_cast<float*>(smem_raw + mat_bytes + (size_t)(q.ncmax + 1) * 8);
+  float* PYs = PXs + (size_t)q.T * S;
+  int* prs = reinterpret_cast<int*>(PYs + (size_t)q.T * S);
   const size_t rb = (size_t)n * q.T * S;
-  const int* pr = q.ranges + (size_t)n * q.T;
-  const float* PX = q.px2 + rb;
-  const float* PY = q.py2 + rb;
+  {
+    const int m = Tn * S;
+    const float* gx = q.px2 + rb;
+    const float* gy = q.py2 + rb;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) { PXs[i] = gx[i]; PYs[i] = gy[i]; }
+    const int32_t* gp = q.ranges + (size_t)n * q.T;
+    for (int i = threadIdx.x; i < Tn; i += blockDim.x) prs[i] = gp[i];
+  }
+  __syncthreads();
+  scan_trace(1);
+  const int* pr = prs;
+  const float* PX = PXs;
+  const float* PY = PYs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int spw = 32 / S;                       // segments per warp
   const int seg = warp * spw + lane / S, s = lane % S;
@@ -238,9 +268,9 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   for (int rd = 0; rd < rounds; ++rd) {
     const int c = seg + rd * nseg;
     const bool cact = on && c < nc;
-    float P[SMAX];
+    float P[KR];
 #pragma unroll
-    for (int i = 0; i < SMAX; ++i) P[i] = (i == s) ? 0.f : NB;   // identity
+    for (int i = 0; i < KR; ++i) P[i] = (i == s) ? 0.f : NB;   // identity
     float shacc = 0.f;
     StepIn nx = load_step(c, 0, cact);
     for (int i = 0; i < C; ++i) {
@@ -250,20 +280,20 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       const int d = in.d;
       const float own_py = in.py, own_px = in.px;
       const float m = rebase_of(__shfl_sync(0xffffffffu, P[0], base));   // P[0][0]
-      float X[SMAX];
+      float X[KR];
       if (fwd) {
         const int src = (s + d < S) ? lane + d : lane;
 #pragma unroll
-        for (int k = 0; k < SMAX; ++k) {
-          if (k >= S) break;
+        for (int k = 0; k < KR; ++k) {
+          if (SC == 0 && k >= S) break;
           const float v = __shfl_sync(0xffffffffu, P[k] + own_py, src);
           X[k] = (s + d < S) ? v - m : NB;
         }
-#pragma unroll 1
+#pragma unroll
         for (int j = 1; j < S; ++j) {
 #pragma unroll
-          for (int k = 0; k < SMAX; ++k) {
-            if (k >= S) break;
+          for (int k = 0; k < KR; ++k) {
+            if (SC == 0 && k >= S) break;
             const float v = __shfl_up_sync(0xffffffffu, X[k] + own_px, 1);
             if (s == j) X[k] = lae2(X[k], v);
           }
@@ -271,16 +301,16 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       } else {
         const int src = (s - d >= 0) ? lane - d : lane;
 #pragma unroll
-        for (int k = 0; k < SMAX; ++k) {
-          if (k >= S) break;
+        for (int k = 0; k < KR; ++k) {
+          if (SC == 0 && k >= S) break;
           const float v = __shfl_sync(0xffffffffu, P[k], src);
           X[k] = (s - d >= 0) ? v + own_py - m : NB;
         }
-#pragma unroll 1
+#pragma unroll
         for (int j = S - 2; j >= 0; --j) {
 #pragma unroll
-          for (int k = 0; k < SMAX; ++k) {
-            if (k >= S) break;
+          for (int k = 0; k < KR; ++k) {
+            if (SC == 0 && k >= S) break;
             const float v = __shfl_down_sync(0xffffffffu, X[k], 1);
             if (s == j) X[k] = lae2(X[k], v + own_px);
           }
@@ -288,19 +318,20 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       }
       if (act) {
 #pragma unroll
-        for (int k = 0; k < SMAX; ++k) P[k] = X[k];
+        for (int k = 0; k < KR; ++k) P[k] = X[k];
         shacc += m;
       }
     }
     if (cact) {
       float* dst = Pm + ((size_t)c * S + s) * S;
 #pragma unroll
-      for (int k = 0; k < SMAX; ++k)
+      for (int k = 0; k < KR; ++k)
         if (k < S) dst[k] = P[k];
       if (s == 0) psh[c] = shacc;
     }
   }
   __syncthreads();
+  scan_trace(2);
 
   // ---------------- phase B: boundary vectors (warp 0, segment 0)
   if (warp == 0) {
@@ -330,16 +361,16 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     for (int c = 0; c < nc; ++c) {
       const float m = rebase_of(__shfl_sync(0xffffffffu, a, 0));
       const float* Pc = Pm + ((size_t)c * S + (sa ? s : 0)) * S;
-      float mx = NB, x[SMAX];
+      float mx = NB, x[KR];
 #pragma unroll
-      for (int k = 0; k < SMAX; ++k) {
+      for (int k = 0; k < KR; ++k) {
         const float ak = __shfl_sync(0xffffffffu, a, k < S ? k : 0);
         x[k] = (k < S && sa) ? (ak - m) + Pc[k] : NB;
         mx = fmaxf(mx, x[k]);
       }
       float acc = 0.f;
 #pragma unroll
-      for (int k = 0; k < SMAX; ++k)
+      for (int k = 0; k < KR; ++k)
         if (k < S) acc += ex2_approx(x[k] - mx);
       a = mx + lg2_approx(acc);
       sh += (double)m + (double)psh[c];
@@ -348,6 +379,7 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     }
   }
   __syncthreads();
+  scan_trace(3);
 
   // ---------------- phase C: every frame of every chunk from its boundary vector
   float* outp = (fwd ? q.ap : q.bp) + rb;
@@ -408,6 +440,8 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       }
     }
   }
+  __syncthreads();
+  scan_trace(4);
 }
 
 // g_l = y'_p(t,u), g_b = empty'_p(t,u) for u = p_t + s (P:273-281 on the pruned lattice), and
@@ -476,26 +510,25 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
 
 // Chunk length of the pruned scan: about sqrt(T) frames (phase B is T/C sequential steps, phase
 // C is C), raised until the chunk matrices fit in shared memory.
+static long long scan_mat_bytes(const Dims& d, int c) {
+  const long long nc = (d.T + c - 1) / c + 1;
+  return ((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8;
+}
 static int scan_chunk(const Dims& d) {
   int C = 4;
   while ((long long)C * C < d.T) ++C;
-  auto bytes = [&](int c) {
-    const long long nc = (d.T + c - 1) / c + 1;
-    return ((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8;
-  };
-  while (bytes(C) > 160 * 1024) C *= 2;
+  while (scan_mat_bytes(d, C) > 32 * 1024) C *= 2;
   return C;
 }
+// chunk matrices + the staged arcs (2 T S floats) and bounds (T ints)
 size_t pruned_recursion_smem(const Dims& d) {
-  const int C = scan_chunk(d);
-  const long long nc = (d.T + C - 1) / C + 1;
-  return (size_t)(((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8);
+  return (size_t)(scan_mat_bytes(d, scan_chunk(d)) + (long long)d.T * d.S * 8 + (long long)d.T * 4);
 }
 
-template <int SMAX>
+template <int SMAX, int SC>
 static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cudaStream_t st) {
-  cudaFuncSetAttribute(pruned_scan_kernel<SMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  RNNT_LAUNCH(KID_PALPHA, st, pruned_scan_kernel<SMAX><<<dim3(d.N, 2), 256, sm, st>>>(q));
+  cudaFuncSetAttribute(pruned_scan_kernel<SMAX, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  RNNT_LAUNCH(KID_PALPHA, st, pruned_scan_kernel<SMAX, SC><<<dim3(d.N, 2), 256, sm, st>>>(q));
   return cudaGetLastError();
 }
 
@@ -515,7 +548,18 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     const int C = scan_chunk(d);
     ScanParams q{w.px2, w.py2, ranges, bnd, d.T, d.S, C, (d.T + C - 1) / C + 1, w.ap, w.bp, w.Af, w.Bf, w.Lp, loss,
                  status};
-    e = d.S <= 8 ? launch_scan<8>(d, q, sm, st) : d.S <= 16 ? launch_scan<16>(d, q, sm, st) : launch_scan<32>(d, q, sm, st);
+    switch (d.S) {   // band widths of the BASELINE configs (and the tests) get a compile-time S
+      case 2: e = launch_scan<2, 2>(d, q, sm, st); break;
+      case 3: e = launch_scan<3, 3>(d, q, sm, st); break;
+      case 4: e = launch_scan<4, 4>(d, q, sm, st); break;
+      case 5: e = launch_scan<5, 5>(d, q, sm, st); break;
+      case 6: e = launch_scan<6, 6>(d, q, sm, st); break;
+      case 8: e = launch_scan<8, 8>(d, q, sm, st); break;
+      case 10: e = launch_scan<10, 10>(d, q, sm, st); break;
+      default:
+        e = d.S <= 8 ? launch_scan<8, 0>(d, q, sm, st)
+                     : d.S <= 16 ? launch_scan<16, 0>(d, q, sm, st) : launch_scan<32, 0>(d, q, sm, st);
+    }
     if (e != cudaSuccess) return e;
   }
   RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(

@@ -13,6 +13,7 @@
 // Warp 0: TMA producer.  Warp 1: TMEM allocator + single-thread MMA issuer.  Warps 2-5:
 // epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -46,6 +47,7 @@ struct JoinerFwdParams {
   float* lse;
   float* px2;
   float* py2;
+  int dbg;                // diagnostics (RNNT_DBG_FWD): 1 no epilogue math, 2 no MMA, 3 no TMA
 };
 
 // Persistent: CTA c processes the live 128-row tiles c, c + gridDim.x, ...; the TMA ring, the
@@ -100,10 +102,14 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
         for (int nt = 0; nt < nvt; ++nt) {
           for (int kb = 0; kb < nkb; ++kb) {
             tc::mbar_wait(&empty[stage], ph ^ 1);
-            tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
             uint8_t* sa = smem + stage * STAGE_BYTES;
-            tc::tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-            tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+            if (p.dbg == 3) {
+              tc::mbar_arrive(&full[stage]);
+            } else {
+              tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+              tc::tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+              tc::tma_load_2d(sa + A_BYTES, &tmB, &full[stage], kb * BK, nt * BN);
+            }
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
         }
@@ -129,10 +135,12 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
             tc::mbar_wait(&full[stage], ph);
             tc::fence_after_sync();
             const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
+            if (p.dbg != 2) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 32 * k, 16, 1024), idesc,
-                           (kb | k) != 0);
+              for (int k = 0; k < BK / 16; ++k)
+                tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 32 * k, 16, 1024), idesc,
+                             (kb | k) != 0);
+            }
             tc::mma_commit(&empty[stage]);
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
@@ -163,6 +171,15 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::fence_after_sync();
         const uint32_t tcol = tl + acc * BN;
+        if (p.dbg == 1) {
+          float z[32];
+          tc::tmem_ld32(tcol, z);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+          if (z[0] == 12345.f) M = z[1];
+          continue;
+        }
         // pass 1: an upper bound of the tile max of z + b: max of the raw accumulators + max bias
         // (tail tile: exact masked max, the zero-filled W rows past V would otherwise count)
         float m = neg_inf_f();
@@ -257,7 +274,8 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   if (!make_tmap_bf16_2d(&tb, W, d.J, d.V, (uint64_t)d.J * 2, jf::BK, jf::BN)) return cudaErrorInvalidValue;
   const int ntiles = (int)((R + jf::BM - 1) / jf::BM);
   JoinerFwdParams p{w.bias, w.bmax, w.rowinfo, w.tlive, w.tcounter, R, ntiles, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN,
-                    (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2};
+                    (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2, 0};
+  if (const char* e = getenv("RNNT_DBG_FWD")) p.dbg = atoi(e);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(joiner_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jf::SMEM_BYTES);

@@ -300,11 +300,13 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 }
 
 // ------------------------------------------------------------------ K4 combine
-// Per block of 32 anti-diagonals (dynamic smem: the block's raw outflows Y, B [32][UP]):
-//   phase A: raw y' and empty' of every cell of the 32 diagonals (one pass over alpha, beta and the
-//            arcs) and their diagonal sums Z_k (the outflow of a diagonal sums to 1);
-//   phase B: normalised occupancies and G~ = (y'+empty')/S(t,u) (bf16 hi+lo), and y' hi+lo, written
-//            t-major: the cells of row t in this block are the contiguous columns u = k - t.
+// Per block of 32 anti-diagonals (dynamic smem: the block's raw outflows Y, B and G [32][UP]):
+//   phase A: raw y', empty' and (y' + empty')/S of every cell of the 32 diagonals (one pass over
+//            alpha, beta, the arcs and 1/S, all skewed: every warp load is a contiguous row segment,
+//            all loads of a diagonal issued before any use) and the diagonal sums Z_k (P:279-281:
+//            the outflow of a diagonal sums to 1);
+//   phase B: the normalised values written t-major (shared memory only): px_grad, py_grad, G~ and
+//            y' as bf16 hi + lo; the cells of row t in this block are the contiguous columns u = k - t.
 __global__ void __launch_bounds__(256) combine_kernel(
     const float2* __restrict__ pxy, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
@@ -315,6 +317,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
   extern __shared__ __align__(16) float cbuf[];
   float* Ys = cbuf;                     // [32][UP]
   float* Bs = cbuf + 32 * UP;           // [32][UP]
+  float* Gs = cbuf + 64 * UP;           // [32][UP]
   // per diagonal and strip: ob = A^w_k + B^w_{k+1} - L (blank arc, same column), ox = A^w_k +
   // B^{w+1}_{k+1} - L (label arc out of the strip's last column into the next strip)
   __shared__ float s_ob[32][lat::MAXW], s_ox[32][lat::MAXW], s_rz[32];
@@ -327,78 +330,86 @@ __global__ void __launch_bounds__(256) combine_kernel(
   const double L2 = Ltot[n] * RNNT_LOG2E;
   const bool finite = isfinite(L2);
   const int U1 = U + 1;
+  if (threadIdx.x < 32 * lat::MAXW) {
+    const int kr = threadIdx.x / lat::MAXW, w = threadIdx.x % lat::MAXW;
+    const int k = k0 + kr;
+    if (finite && k < Kn && w < W) {
+      const double A = (double)Ash[sbase + (size_t)k * W + w];
+      s_ob[kr][w] = (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + w] - L2);
+      s_ox[kr][w] = (w + 1 < W) ? (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + w + 1] - L2) : 0.f;
+    }
+  }
+  __syncthreads();
 
-  // phase A: one warp per diagonal of the block
+  // phase A: one warp per diagonal of the block; the row is read in groups of four 32-column chunks
+  constexpr int CG = 4;
   for (int kr = warp; kr < 32; kr += 8) {
     const int k = k0 + kr;
     const bool live = finite && k < Kn;
-    if (live && lane < W) {
-      const double A = (double)Ash[sbase + (size_t)k * W + lane];
-      s_ob[kr][lane] = (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane] - L2);
-      s_ox[kr][lane] = (lane + 1 < W) ? (float)(A + (double)Bsh[sbase + (size_t)(k + 1) * W + lane + 1] - L2) : 0.f;
-    }
-    __syncwarp();
     const int ulo = live ? max(0, k - Tn + 1) : 1, uhi = live ? min(k, Un) : 0;
     const float* Ar = ahat + base + (size_t)k * LU;
     const float* Br = bhat + base + (size_t)(k + 1) * LU;
     const float2* XY = pxy + base + (size_t)k * LU;
+    const float* Rr = rS + base + (size_t)k * LU;
     float z = 0.f;
-#pragma unroll 2
-    for (int u = lane; u < UP; u += 32) {
-      float yv = 0.f, bv = 0.f;
-      if (u >= ulo && u <= uhi) {
-        const int w = u / SW;
-        const float a = Ar[u];
-        const float2 xy = XY[u];
-        bv = ex2_approx(a + xy.y + Br[u] + s_ob[kr][w]);
-        if (u < Un) yv = ex2_approx(a + xy.x + Br[u + 1] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+    for (int u0 = 0; u0 < UP; u0 += 32 * CG) {
+      float a[CG], b0[CG], b1[CG], r[CG];
+      float2 xy[CG];
+#pragma unroll
+      for (int i = 0; i < CG; ++i) {          // every load of the group first
+        const int u = u0 + 32 * i + lane;
+        const bool v = u >= ulo && u <= uhi;
+        a[i] = v ? Ar[u] : 0.f;
+        xy[i] = v ? XY[u] : make_float2(0.f, 0.f);
+        b0[i] = v ? Br[u] : 0.f;
+        b1[i] = (v && u < Un) ? Br[u + 1] : 0.f;
+        r[i] = v ? Rr[u] : 0.f;
       }
-      Ys[kr * UP + u] = yv;
-      Bs[kr * UP + u] = bv;
-      z += yv + bv;
+#pragma unroll
+      for (int i = 0; i < CG; ++i) {
+        const int u = u0 + 32 * i + lane;
+        if (u >= UP) break;
+        float yv = 0.f, bv = 0.f;
+        if (u >= ulo && u <= uhi) {
+          const int w = u / SW;
+          bv = ex2_approx(a[i] + xy[i].y + b0[i] + s_ob[kr][w]);
+          if (u < Un) yv = ex2_approx(a[i] + xy[i].x + b1[i] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+        }
+        Ys[kr * UP + u] = yv;
+        Bs[kr * UP + u] = bv;
+        Gs[kr * UP + u] = (yv + bv) * r[i];
+        z += yv + bv;
+      }
     }
     z = warp_sum(z);
     if (lane == 0) s_rz[kr] = (live && z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
   }
   __syncthreads();
 
-  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t.
-  // Four rows per warp iteration with their 1/S loads issued first (the loop is load-latency bound).
+  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t
   const int tlo = max(0, k0 - UP + 1), thi = min(T - 1, k0 + 31);
-  constexpr int RB = 4;
-  for (int tb = tlo + warp * RB; tb <= thi; tb += 8 * RB) {
-    const int kr = lane;
-    float rsv[RB];
-#pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      const int t = tb + i, u = k0 + kr - t;
-      rsv[i] = (t <= thi && u >= 0 && u < U1) ? rS[((size_t)n * T + t) * UP + u] : 0.f;   // rS: live cells only
-    }
+  for (int t = tlo + warp; t <= thi; t += 8) {
+    const int kr = lane, u = k0 + kr - t;
+    if (u < 0 || u >= UP) continue;
     const float rz = s_rz[kr];
-#pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      const int t = tb + i, u = k0 + kr - t;
-      if (t > thi || u < 0 || u >= UP) continue;
-      const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
-      if (u < U1) {
-        const size_t o = ((size_t)n * T + t) * U1 + u;
-        px_grad[o] = yv;
-        py_grad[o] = bv;
-      }
-      // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
-      const size_t og = ((size_t)n * T + t) * UP + u;
-      const float sgv = yv + bv;
-      const float g = (u < U1 && sgv != 0.f) ? sgv * rsv[i] : 0.f;
-      const __nv_bfloat16 gh = __float2bfloat16_rn(g);
-      const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
-      Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
-      Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
-      // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
-      const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
-      const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
-      Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
-      Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
+    const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
+    if (u < U1) {
+      const size_t o = ((size_t)n * T + t) * U1 + u;
+      px_grad[o] = yv;
+      py_grad[o] = bv;
     }
+    // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
+    const size_t og = ((size_t)n * T + t) * UP + u;
+    const float g = Gs[kr * UP + u] * rz;
+    const __nv_bfloat16 gh = __float2bfloat16_rn(g);
+    const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
+    Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
+    Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
+    // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
+    const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
+    const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
+    Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
+    Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
   }
 }
 
@@ -438,7 +449,7 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   if (e != cudaSuccess) return e;
   // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
   dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
-  const size_t csm = (size_t)2 * 32 * d.UP() * sizeof(float);
+  const size_t csm = (size_t)3 * 32 * d.UP() * sizeof(float);
   cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, csm, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),

@@ -346,7 +346,7 @@ struct NormProb {
   const int64_t *sym, *bnd;
   int T, U, V, LU, K, BN, nkb, UPa;
   float2* pxy;     // (N,K+1,LU) skewed {y, empty} * log2e
-  float* rS;       // (N,T,UPa) t-major 1/S(t,u)
+  float* rS;       // (N,K+1,LU) skewed 1/S(t,u) (valid cells only)
   int32_t* status;
   const float *am, *amy;
 
@@ -396,17 +396,17 @@ struct NormProb {
     const bool rowok = trow < Tn;
     const int t0w = t.m0 + 32 * e.q;
     float2 (*bxy)[33] = reinterpret_cast<float2 (*)[33]>(smem + e.warp * 32 * 33 * 8);
+    float (*brs)[33] = reinterpret_cast<float (*)[33]>(smem + sg::EPI_WARPS * 32 * 33 * 8 + e.warp * 32 * 33 * 4);
     const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
     const float mam = rowok ? m_am[arow] : 0.f;
     const float am0 = rowok ? am[arow * V] : 0.f;
     const float* ayr = amy + arow * UPa;
-    float* rSr = rS + arow * UPa;
     const size_t nbase = (size_t)t.n * (K + 1);
     bool under = false;
     const int nch = (min(BN, Un + 1 - t.n0) + 31) / 32;   // 32-column chunks with at least one u <= U_n
     for (int c = e.g; c < nch; c += 2) {
       const int c0 = 32 * c, u0 = t.n0 + c0;
-      float acc[32], ay[32], rs[32];
+      float acc[32], ay[32];
       tc::tmem_ld32(e.taddr + c0, acc);
       if (rowok) {
 #pragma unroll
@@ -430,19 +430,19 @@ struct NormProb {
           r = rcp_approx(S);
         }
         bxy[e.lane][j] = make_float2(px, py);
-        rs[j] = r;
-      }
-      if (rowok) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          reinterpret_cast<float4*>(rSr + u0)[q] = make_float4(rs[4 * q], rs[4 * q + 1], rs[4 * q + 2], rs[4 * q + 3]);
+        brs[e.lane][j] = r;
       }
       __syncwarp();
-      // diagonal-major write: for diagonal k = t0w + u0 + d, lane l holds column u0 + l (t = k - u)
+      // diagonal-major write of the arcs and of 1/S: for diagonal k = t0w + u0 + d, lane l holds
+      // column u0 + l (t = k - u)
       const int u = u0 + e.lane;
       for (int d = 0; d < 63; ++d) {
         const int tl_ = d - e.lane, tt = t0w + tl_;
-        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) pxy[(nbase + tt + u) * LU + u] = bxy[tl_][e.lane];
+        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) {
+          const size_t o = (nbase + tt + u) * LU + u;
+          pxy[o] = bxy[tl_][e.lane];
+          rS[o] = brs[tl_][e.lane];
+        }
       }
       __syncwarp();
     }

@@ -43,7 +43,7 @@ struct SimpleWS {
   float* m_am;    // (N,T)     row max of am
   float* m_lm;    // (N,U+1)   row max of lm
   float2* pxy;    // (N,K+1,LU) skewed {y(t,u), empty(t,u)} * log2e   (k = t+u)
-  float* rS;      // (N,T,UP)   t-major 1/S(t,u) = 1/sum_v exp(am-m_am+lm-m_lm)
+  float* rS;      // (N,K+1,LU) skewed 1/S(t,u) = 1/sum_v exp(am-m_am+lm-m_lm) (valid cells only)
   float* alpha;   // (N,K+1,LU) skewed alpha-hat = alpha*log2e - A_k (fp32, rebased)
   float* beta;    // (N,K+1,LU) skewed beta-hat  = beta*log2e - B_k
   float* Ash;     // (N,K+1,W)  A_k per diagonal and strip (integer-valued)
@@ -120,7 +120,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.m_am = (float*)take(N * T * 4);
   s.m_lm = (float*)take(N * U1 * 4);
   s.pxy = (float2*)take(N * K1 * LU * 8);
-  s.rS = (float*)take(N * T * (size_t)d.UP() * 4);
+  s.rS = (float*)take(N * K1 * LU * 4);
   s.alpha = (float*)take(N * K1 * LU * 4);
   s.beta = (float*)take(N * K1 * LU * 4);
   s.Ash = (float*)take(N * K1 * (size_t)d.lat_W() * 4);

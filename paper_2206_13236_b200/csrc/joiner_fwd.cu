@@ -30,7 +30,8 @@ constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int B_BYTES = BN * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int BIAS_MAX = 2048;              // the padded bias is staged in smem when VP <= BIAS_MAX
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + BIAS_MAX * 4;
 constexpr int THREADS = 192;
 }  // namespace jf
 
@@ -67,6 +68,10 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
   uint64_t* qempty = qfull + 4;
   int* tq = reinterpret_cast<int*>(qempty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
+  float* sbias = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
+  const bool bias_smem = p.VP <= BIAS_MAX;
+  if (bias_smem)
+    for (int v = threadIdx.x; v < p.VP; v += blockDim.x) sbias[v] = p.bias[v];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
         const int acc = it & 1;
         const int v0 = nt * BN;
         const bool tail = v0 + BN > p.V;                // columns >= V exist in this tile
-        const float bm = p.bmax[nt];
+        const float zb_prev = zb, zl_prev = zl;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::fence_after_sync();
         const uint32_t tcol = tl + acc * BN;
@@ -180,62 +185,90 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
           if (z[0] == 12345.f) M = z[1];
           continue;
         }
-        // pass 1: an upper bound of the tile max of z + b: max of the raw accumulators + max bias
-        // (tail tile: exact masked max, the zero-filled W rows past V would otherwise count)
-        float m = neg_inf_f();
+        // One TMEM pass: the exp offset m of this tile is fixed from its first 32-column chunk (exact
+        // max of z + b there, joined with the running max of the earlier tiles); every chunk is
+        // exponentiated against it as it is read.  A chunk exceeding m by more than kRedo (could
+        // overflow e^(z-m)) makes the whole warp redo the tile with a max-only first pass (rare).
+        constexpr float kRedo = 60.f;
+        float m = neg_inf_f(), s = 0.f;
+        bool redo = false;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+          if (attempt == 1) {
+            if (!__any_sync(0xffffffffu, redo)) break;
+            // exact tile max (masked), then the exp pass again
+            m = neg_inf_f();
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float z[32];
-          tc::tmem_ld32(tcol + 32 * c, z);
-          if (!tail) {
+            for (int c = 0; c < 4; ++c) {
+              float z[32];
+              tc::tmem_ld32(tcol + 32 * c, z);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) m = fmaxf(m, z[j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (v0 + 32 * c + j < p.V) m = fmaxf(m, z[j] + __ldg(p.bias + v0 + 32 * c + j));
+              for (int j = 0; j < 32; ++j)
+                if (v0 + 32 * c + j < p.V) m = fmaxf(m, z[j] + p.bias[v0 + 32 * c + j]);
+            }
+            s = 0.f;
+            zb = zb_prev; zl = zl_prev;
           }
-        }
-        if (!tail) m += bm;
-        const float mL = m * RNNT_LOG2E_F;
-        float s = 0.f;
+          float mL = m * RNNT_LOG2E_F;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float z[32];
-          tc::tmem_ld32(tcol + 32 * c, z);
-          const int vc = v0 + 32 * c;
-          const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
+          for (int c = 0; c < 4; ++c) {
+            float z[32];
+            {
+              uint32_t zr[32];
+              tc::tmem_ld32_issue(tcol + 32 * c, zr);
+              const int vc = v0 + 32 * c;
+              float4 b4[8];
+              const float4* bb = reinterpret_cast<const float4*>((bias_smem ? sbias : p.bias) + vc);
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 b4 = __ldg(bb + j4);
-            z[4 * j4] += b4.x; z[4 * j4 + 1] += b4.y; z[4 * j4 + 2] += b4.z; z[4 * j4 + 3] += b4.w;
-          }
-          if (tail) {
+              for (int j4 = 0; j4 < 8; ++j4) b4[j4] = bb[j4];     // overlapped with the TMEM load
+              tc::tmem_ld32_wait(zr);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = (vc + j < p.V) ? z[j] : neg_inf_f();
-          }
-          uint32_t pk[16];
+              for (int j4 = 0; j4 < 8; ++j4) {
+                z[4 * j4] = __uint_as_float(zr[4 * j4]) + b4[j4].x;
+                z[4 * j4 + 1] = __uint_as_float(zr[4 * j4 + 1]) + b4[j4].y;
+                z[4 * j4 + 2] = __uint_as_float(zr[4 * j4 + 2]) + b4[j4].z;
+                z[4 * j4 + 3] = __uint_as_float(zr[4 * j4 + 3]) + b4[j4].w;
+              }
+            }
+            const int vc = v0 + 32 * c;
+            if (tail) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float e0 = ex2_approx(fmaf(z[2 * j], RNNT_LOG2E_F, -mL));
-            const float e1 = ex2_approx(fmaf(z[2 * j + 1], RNNT_LOG2E_F, -mL));
-            s += e0 + e1;
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h2);
-          }
-          if (info >= 0) {
-            uint4* dst = reinterpret_cast<uint4*>(prow + vc);
+              for (int j = 0; j < 32; ++j) z[j] = (vc + j < p.V) ? z[j] : neg_inf_f();
+            }
+            if (attempt == 0) {
+              float cm = z[0];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          }
-          if (vc == 0) zb = z[0];
-          const int li = info - vc;
-          const bool hit = (unsigned)li < 32u;
-          if (__any_sync(0xffffffffu, hit)) {
-            float sel = z[0];
+              for (int j = 1; j < 32; ++j) cm = fmaxf(cm, z[j]);
+              if (c == 0) {
+                m = fmaxf(M, cm);
+                mL = m * RNNT_LOG2E_F;
+              } else if (cm - m > kRedo) {
+                redo = true;
+              }
+              if (__any_sync(0xffffffffu, redo)) break;
+            }
+            uint32_t pk[16];
 #pragma unroll
-            for (int j = 1; j < 32; ++j) sel = (li == j) ? z[j] : sel;
-            if (hit) zl = sel;
+            for (int j = 0; j < 16; ++j) {
+              const float e0 = ex2_approx(fmaf(z[2 * j], RNNT_LOG2E_F, -mL));
+              const float e1 = ex2_approx(fmaf(z[2 * j + 1], RNNT_LOG2E_F, -mL));
+              s += e0 + e1;
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            if (info >= 0) {
+              uint4* dst = reinterpret_cast<uint4*>(prow + vc);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            }
+            if (vc == 0) zb = z[0];
+            const int li = info - vc;
+            const bool hit = (unsigned)li < 32u;
+            if (__any_sync(0xffffffffu, hit)) {
+              float sel = z[0];
+#pragma unroll
+              for (int j = 1; j < 32; ++j) sel = (li == j) ? z[j] : sel;
+              if (hit) zl = sel;
+            }
           }
         }
         tc::fence_before_sync();

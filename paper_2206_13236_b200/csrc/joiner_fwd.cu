@@ -24,16 +24,24 @@
 namespace rnnt {
 
 namespace jf {
-// 128-column V tiles, double-buffered accumulators (2 x 128 TMEM columns) and a 3-stage ring
-// (~97 KB smem): two CTAs per SM, so one CTA's softmax epilogue overlaps the other's MMAs.
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 3;
+// One CTA per SM: a 4-stage TMA ring, four 128-column TMEM accumulators and two epilogue sets of
+// four warps.  Row tiles alternate between the sets (set e owns accumulators 2e, 2e+1, double-
+// buffered over its V tiles), so each set has two row tiles of MMA time for its softmax epilogue.
+// P~ leaves through a per-set 32 KB staging tile by TMA (two 64-column SWIZZLE_128B boxes): full-line
+// coalesced writes instead of 16-B per-row stores.
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int B_BYTES = BN * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int BIAS_MAX = 2048;              // the padded bias is staged in smem when VP <= BIAS_MAX
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + BIAS_MAX * 4;
-constexpr int THREADS = 192;
+constexpr int STG_BYTES = BM * BN * 2;      // 32 KB bf16 P~ tile per epilogue set
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * STG_BYTES + 1024 + 256;
+constexpr int THREADS = 320;                // warp 0 TMA, warp 1 MMA, warps 2-5 / 6-9 epilogue sets
 }  // namespace jf
+
+// byte offset of logical 16-B chunk `c` (0..7) of 128-B row `r` in a SWIZZLE_128B atom stack
+__device__ __forceinline__ uint32_t sw128f(int r, int c) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
 
 struct JoinerFwdParams {
   const float* bias;      // (VP) fp32, padded
@@ -54,35 +62,31 @@ struct JoinerFwdParams {
 // Persistent: CTA c processes the live 128-row tiles c, c + gridDim.x, ...; the TMA ring, the
 // MMA issue and the double-buffered TMEM accumulators run continuously across row tiles, so the
 // softmax epilogue of one (row tile, V tile) overlaps the MMAs of the next.
-__global__ void __launch_bounds__(jf::THREADS, 2)
+__global__ void __launch_bounds__(jf::THREADS, 1)
     joiner_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         JoinerFwdParams p) {
+                         const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
   using namespace jf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + 2 * STG_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* qfull = tempty + 2;          // [4] tile queue: producer -> MMA issuer + epilogue
+  uint64_t* tfull = empty + STAGES;      // [4] accumulators
+  uint64_t* tempty = tfull + 4;
+  uint64_t* qfull = tempty + 4;          // [4] tile queue: producer -> MMA issuer + epilogue
   uint64_t* qempty = qfull + 4;
   int* tq = reinterpret_cast<int*>(qempty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
-  float* sbias = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
-  const bool bias_smem = p.VP <= BIAS_MAX;
-  if (bias_smem)
-    for (int v = threadIdx.x; v < p.VP; v += blockDim.x) sbias[v] = p.bias[v];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
-    for (int s = 0; s < 4; ++s) { tc::mbar_init(&qfull[s], 1); tc::mbar_init(&qempty[s], 5); }
+    for (int s = 0; s < 4; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 4; ++s) { tc::mbar_init(&qfull[s], 1); tc::mbar_init(&qempty[s], 9); }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 4 * BN);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -123,16 +127,18 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, false, false);
-      int stage = 0, it = 0, qi = 0;
+      int stage = 0, qi = 0, ite[2] = {0, 0};
       uint32_t ph = 0;
       for (;;) {
         tc::mbar_wait(&qfull[qi & 3], (qi >> 2) & 1);
         const int rt = tq[qi & 3];
         tc::mbar_arrive(&qempty[qi & 3]);
+        const int set = qi & 1;                  // row tiles alternate between the epilogue sets
         ++qi;
         if (rt < 0) break;
-        for (int nt = 0; nt < nvt; ++nt, ++it) {
-          const int acc = it & 1;
+        for (int nt = 0; nt < nvt; ++nt) {
+          const int it = ite[set]++;
+          const int acc = 2 * set + (it & 1);
           tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
           tc::fence_after_sync();
           const uint32_t d = tbase + acc * BN;
@@ -155,6 +161,9 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
     }
   } else {
     const int q = warp & 3;
+    const int set = (warp - 2) >> 2;           // warps 2-5: set 0, warps 6-9: set 1
+    const int ethr = 64 + 128 * set;           // the set's store-issuing thread
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + set * STG_BYTES;
     const uint32_t tl = tbase + ((uint32_t)(32 * q) << 16);
     int it = 0, qi = 0;
     for (;;) {
@@ -162,16 +171,16 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
       const int rt = tq[qi & 3];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&qempty[qi & 3]);
+      const bool mine = (qi & 1) == set;
       ++qi;
       if (rt < 0) break;
+      if (!mine) continue;
       const long long r = (long long)rt * BM + 32 * q + lane;
       const int info = (r < p.R) ? p.rowinfo[r] : -1;
       float M = neg_inf_f(), sum = 0.f, zb = neg_inf_f(), zl = neg_inf_f();
-      uint16_t* prow = p.Pt + (size_t)(info >= 0 ? r : 0) * p.VP;
       for (int nt = 0; nt < nvt; ++nt, ++it) {
-        const int acc = it & 1;
+        const int acc = 2 * set + (it & 1);
         const int v0 = nt * BN;
-        const bool tail = v0 + BN > p.V;                // columns >= V exist in this tile
         const float zb_prev = zb, zl_prev = zl;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::fence_after_sync();
@@ -192,6 +201,8 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
         constexpr float kRedo = 60.f;
         float m = neg_inf_f(), s = 0.f;
         bool redo = false;
+        if (threadIdx.x == ethr) tc::bulk_wait_read0();   // the previous tile's P~ store has left smem
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
         for (int attempt = 0; attempt < 2; ++attempt) {
           if (attempt == 1) {
             if (!__any_sync(0xffffffffu, redo)) break;
@@ -217,9 +228,9 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
               tc::tmem_ld32_issue(tcol + 32 * c, zr);
               const int vc = v0 + 32 * c;
               float4 b4[8];
-              const float4* bb = reinterpret_cast<const float4*>((bias_smem ? sbias : p.bias) + vc);
+              const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
 #pragma unroll
-              for (int j4 = 0; j4 < 8; ++j4) b4[j4] = bb[j4];     // overlapped with the TMEM load
+              for (int j4 = 0; j4 < 8; ++j4) b4[j4] = __ldg(bb + j4);     // overlapped with the TMEM load
               tc::tmem_ld32_wait(zr);
 #pragma unroll
               for (int j4 = 0; j4 < 8; ++j4) {
@@ -230,10 +241,7 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
               }
             }
             const int vc = v0 + 32 * c;
-            if (tail) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) z[j] = (vc + j < p.V) ? z[j] : neg_inf_f();
-            }
+            // (columns v >= V: the padded bias is -inf there, so z = -inf and e^(z-m) = 0 with no mask)
             if (attempt == 0) {
               float cm = z[0];
 #pragma unroll
@@ -255,25 +263,36 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
               __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
               pk[j] = *reinterpret_cast<uint32_t*>(&h2);
             }
-            if (info >= 0) {
-              uint4* dst = reinterpret_cast<uint4*>(prow + vc);
+            {
+              // staging tile: box c/2 (64 columns), 16-B chunks (c%2)*4.. of this row, swizzled
+              uint8_t* sb = stg + (c >> 1) * (STG_BYTES / 2);
+              const int row = 32 * q + lane;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<uint4*>(sb + sw128f(row, (c & 1) * 4 + j)) =
+                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
             }
             if (vc == 0) zb = z[0];
             const int li = info - vc;
             const bool hit = (unsigned)li < 32u;
             if (__any_sync(0xffffffffu, hit)) {
-              float sel = z[0];
+              float zz[32];                 // dynamically indexed: one local-memory round trip
 #pragma unroll
-              for (int j = 1; j < 32; ++j) sel = (li == j) ? z[j] : sel;
-              if (hit) zl = sel;
+              for (int j = 0; j < 32; ++j) zz[j] = z[j];
+              if (hit) zl = zz[li];
             }
           }
         }
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        tc::fence_proxy_async();                        // staging writes -> async proxy
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
+        if (threadIdx.x == ethr && p.dbg != 4) {
+          tc::tma_store_2d(&tmP, stg, v0, rt * BM);
+          tc::tma_store_2d(&tmP, stg + STG_BYTES / 2, v0 + 64, rt * BM);
+          tc::bulk_commit();
+        }
         if (info >= 0) p.mt[(size_t)r * p.ntile + v0 / 128] = m;
         const float Mn = fmaxf(M, m);
         sum = sum * ex2_approx((M - Mn) * RNNT_LOG2E_F) + s * ex2_approx((m - Mn) * RNNT_LOG2E_F);
@@ -293,18 +312,20 @@ __global__ void __launch_bounds__(jf::THREADS, 2)
       }
     }
   }
+  if (warp >= 2 && (threadIdx.x & 127) == 64) tc::bulk_wait0();
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 2 * BN);
+  if (warp == 1) tc::tmem_dealloc(tbase, 4 * BN);
 }
 
 cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
   const int VP = d.VP();
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tp;
   if (!make_tmap_bf16_2d(&ta, h, d.J, R, (uint64_t)d.J * 2, jf::BK, jf::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tb, W, d.J, d.V, (uint64_t)d.J * 2, jf::BK, jf::BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&tp, w.Pt, VP, R, (uint64_t)VP * 2, 64, jf::BM)) return cudaErrorInvalidValue;
   const int ntiles = (int)((R + jf::BM - 1) / jf::BM);
   JoinerFwdParams p{w.bias, w.bmax, w.rowinfo, w.tlive, w.tcounter, R, ntiles, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN,
                     (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2, 0};
@@ -316,8 +337,8 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  const unsigned grid = (unsigned)std::min(ntiles, 2 * nsm);   // persistent: two CTAs per SM
-  RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, p));
+  const unsigned grid = (unsigned)std::min(ntiles, nsm);   // persistent: one CTA per SM
+  RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, tp, p));
   return cudaGetLastError();
 }
 

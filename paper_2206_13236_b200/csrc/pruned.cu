@@ -84,7 +84,9 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
                                float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter) {
   if (blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x == 0) *tcounter = 0;
-    for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : 0.f;
+    // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
+    // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
+    for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int tl = warp; tl < VP / 128; tl += blockDim.x / 32) {   // bias max per 128-column tile

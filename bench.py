@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic"],
+                    help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch)")
     return ap.parse_args()
 
 
@@ -114,19 +116,60 @@ class Clocks:
 
 # ------------------------------------------------------------------ roofline table
 def algorithmic(kernel, b):
-    """Algorithmic work of one launch of ``kernel`` on batch ``b``."""
+    """Algorithmic work of one launch of ``kernel`` on batch ``b``:
+    (flops, bytes).  Bytes count each input read once and each output written once (real rows /
+    cells only), flops the dense contractions at their real sizes."""
     T = b.T_n.astype(np.int64)
     U1 = b.U_n.astype(np.int64) + 1
     rows = int((T * b.S).sum())                 # real band rows sum_n T_n * S
-    V, J = b.V, b.J
-    if kernel in ("joiner_fwd_gemm", "joiner_dh_gemm", "joiner_dw_gemm"):
-        return "tensor", 2.0 * rows * J * V, "TFLOP/s"
-    if kernel == "simple_norm_gemm":
-        return "tensor", 2.0 * float((T * U1).sum()) * V, "TFLOP/s"
-    if kernel == "prune_gather":
-        # read enc row once per frame (L2 reuse across s) + dec rows, write h (bf16)
-        return "hbm", float(T.sum() * J * 4 + U1.sum() * J * 4 + rows * J * 2), "GB/s"
+    cells = int((T * U1).sum())                 # real lattice cells
+    frames, toks = int(T.sum()), int(U1.sum())
+    V, J, S = b.V, b.J, b.S
+    if kernel == "joiner_fwd_gemm":             # h, W in; P~ (bf16), per-row scalars out
+        return 2.0 * rows * J * V, rows * J * 2 + V * J * 2 + rows * V * 2 + rows * 16
+    if kernel == "joiner_dh_gemm":              # P~, h, W, row scalars in; d_enc, d_dec out
+        return 2.0 * rows * J * V, rows * V * 2 + rows * J * 2 + V * J * 2 + rows * 16 + (frames + toks) * J * 4
+    if kernel == "joiner_dw_gemm":              # P~, h, row scalars in; dW split partials out (one V x J)
+        return 2.0 * rows * J * V, rows * V * 2 + rows * J * 2 + rows * 16 + V * J * 4
+    if kernel == "simple_norm_gemm":            # E_am, E_lm (bf16 hi+lo) in; arcs + 1/S out (skewed)
+        return 2.0 * cells * V * 3, (frames + toks) * V * 4 + cells * 12
+    if kernel == "prune_gather":                # enc, dec rows in; h (bf16) out
+        return 0.0, frames * J * 4 + toks * J * 4 + rows * J * 2
+    if kernel == "simple_prep":                 # am, lm in; E hi+lo out
+        return 0.0, (frames + toks) * V * 4 * 2
+    if kernel == "lattice_combine":             # alpha, beta, arcs, 1/S in; px/py grads, G~, y' out
+        return 0.0, cells * (4 + 4 + 8 + 4) + cells * (8 + 8)
     raise KeyError(kernel)
+
+
+PROFILED = ["joiner_dh_gemm", "joiner_fwd_gemm", "joiner_dw_gemm", "simple_norm_gemm", "prune_gather",
+            "lattice_combine", "simple_prep", "lattice_fb", "pruned_fb"]
+LATENCY_BOUND = {"lattice_fb", "pruned_fb"}   # dependent log-add chains (DESIGN.md "Recursions")
+
+
+def roofline(kernel, b, ms, hbm, tfl):
+    """Roofline of one kernel from its live mean launch time: the binding resource is the one whose
+    floor (algorithmic work / measured peak) is larger."""
+    flops, byts = algorithmic(kernel, b)
+    ft = flops / (tfl * 1e12) if flops else 0.0
+    fh = byts / (hbm * 1e9)
+    s = ms / 1000.0
+    if ft >= fh:
+        return {"kernel": kernel, "bound": "tensor", "achieved": flops / s / 1e12, "peak": tfl, "unit": "TFLOP/s",
+                "frac": ft / s, "kernel_ms": ms, "algorithmic_flops": flops, "algorithmic_bytes": byts}
+    return {"kernel": kernel, "bound": "hbm", "achieved": byts / s / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": fh / s, "kernel_ms": ms, "algorithmic_flops": flops, "algorithmic_bytes": byts}
+
+
+def ncu_traffic(kernel, cfg):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of ``kernel`` from the
+    committed ncu --set full capture summary (profiles/ncu_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    d = json.load(open(path))
+    e = d.get(f"c{cfg}", {}).get(kernel)
+    return (e["bytes"], e["source"]) if e else (None, None)
 
 
 def peaks():
@@ -197,12 +240,66 @@ def run_reference(args, world, rank):
     return 0
 
 
+# ------------------------------------------------------------------ dynamic-batch workload
+def run_dynamic(args):
+    """Every batch of the synthetic dynamic-batch corpus (synth.make_dynamic_corpus)
+    through the whole hot path, one batch per step; frames/s over the corpus and mean ms per batch."""
+    import torch
+    import paper_2206_13236_b200 as R
+    corpus = synth.make_dynamic_corpus()
+    devs = [R.batch_to_device(b, "cuda") for b in corpus]
+    dims = [R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S) for b in corpus]
+    outs = [R.alloc_outputs(d, "cuda") for d in dims]
+    ws = torch.empty(max(R.rnnt_workspace_bytes(d) for d in dims), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step(i):
+        b, dv, o = corpus[i], devs[i], outs[i]
+        o["status"].zero_()
+        R.step(dv["am"], dv["lm"], dv["symbols"], dv["boundary"], dv["enc_proj"], dv["dec_proj"], dv["w_out"],
+               dv["b_out"], b.S, out=o, workspace=ws)
+
+    for i in range(max(args.warmup, 3)):
+        step(i % len(corpus))
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in corpus]
+    clocks = Clocks(0)
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(len(corpus)):
+        flush.zero_()
+        ev[i][0].record()
+        step(i)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = [a.elapsed_time(c) for a, c in ev]
+    frames = sum(int(b.T_n.sum()) for b in corpus)
+    peak = torch.cuda.max_memory_allocated() / 2 ** 30 - flush.numel() / 2 ** 30
+    line = {"metric": METRIC, "value": frames / (sum(ms) / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": len(corpus),
+            "warmup": max(args.warmup, 3), "ms_per_step": statistics.mean(ms), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16+f32", "data": "synthetic",
+            "config": {"workload": "dynamic batches (Table 2 protocol): c2-shaped utterances sorted by length, "
+                                   f"<= {synth.DYNAMIC_CAP_FRAMES} encoder frames (10k input frames) per batch",
+                       "batches": len(corpus), "utterances": sum(b.N for b in corpus), "frames": frames,
+                       "padded_frames": sum(b.N * b.T for b in corpus), "V": 500, "J": 512, "S": 5,
+                       "l2": "flushed between timed batches (256 MiB write, outside the timed events)",
+                       "kernels": R.rnnt_version()},
+            "peak_gib": peak, "clocks": clk,
+            "ms_per_batch": {"mean": statistics.mean(ms), "min": min(ms), "max": max(ms)}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if args.workload == "dynamic":
+        return run_dynamic(args)
     import torch
     import paper_2206_13236_b200 as R
     torch.cuda.set_device(local)
@@ -281,19 +378,37 @@ def main():
     # inputs+outputs+workspace actually held by the step (the flush buffer excluded)
     step_gib = (peak_gib - flush.numel() / 2 ** 30)
 
-    # roofline of the profiled kernel
+    # live per-kernel times: each profiled kernel bracketed by CUDA events on its launch stream over a
+    # few extra steps (same workload, L2 flushed between steps), then the roofline of each; the line's
+    # "roofline" is the dominant one (largest share of the step)
     hbm, tfl, src = peaks()
-    bound, work, unit = algorithmic(kname, b)
-    kmean = statistics.mean(kern_ms)
-    if bound == "tensor":
-        achieved = work / (kmean / 1000) / 1e12
-        peak = tfl
-    else:
-        achieved = work / (kmean / 1000) / 1e9
-        peak = hbm
-    roof = {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-            "frac": achieved / peak, "traffic": None, "kernel_ms": kmean,
-            "share_of_step": kmean / statistics.mean(step_ms), "peak_source": src}
+    kms = {kname: statistics.mean(kern_ms)}
+    for kn in PROFILED:
+        if kn in kms or kn not in ids:
+            continue
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+        for a, c in evs:
+            a.record(); c.record()
+        torch.cuda.synchronize()
+        for a, c in evs:
+            flush.zero_()
+            R.rnnt_profile_kernel(ids[kn], a, c)
+            step(dev)
+        torch.cuda.synchronize()
+        R.rnnt_profile_kernel(0)
+        kms[kn] = statistics.mean(a.elapsed_time(c) for a, c in evs)
+    step_mean = statistics.mean(step_ms)
+    kernels = {kn: roofline(kn, b, ms, hbm, tfl) for kn, ms in kms.items() if kn not in LATENCY_BOUND}
+    chain = int((b.T_n + b.U_n).max())          # longest anti-diagonal chain (simple lattice)
+    for kn in LATENCY_BOUND & set(kms):
+        kernels[kn] = {"kernel": kn, "bound": "latency", "achieved": kms[kn] * 1e3 / chain, "unit": "ns/diagonal",
+                       "frac": None, "kernel_ms": kms[kn], "chain_steps": chain}
+    for kn, r in kernels.items():
+        r["share_of_step"] = r["kernel_ms"] / step_mean
+    dom = max((k for k in kernels if k not in LATENCY_BOUND), key=lambda k: kernels[k]["kernel_ms"])
+    roof = dict(kernels[dom])
+    traffic, tsrc = ncu_traffic(dom, cfg)
+    roof.update({"traffic": traffic, "traffic_source": tsrc, "peak_source": src})
 
     # end-to-end: host pinned inputs -> device, step, loss -> host, all inside the timed region
     e2e = None
@@ -348,6 +463,8 @@ def main():
                            "l2": "flushed between timed steps (256 MiB write, outside the timed events)",
                            "kernels": R.rnnt_version()},
                 "peak_gib": step_gib, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "kernels": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac", "kernel_ms", "share_of_step")}
+                            for k, v in kernels.items()},
                 "gpu_launches": int(launches), "clocks": clk,
                 "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)}}
         print(json.dumps(line), flush=True)

@@ -23,7 +23,7 @@ __all__ = [
     "backward_beta", "total_logprob", "occupancies", "simple_grads", "simple_loss",
     "bound_scores", "raw_bounds", "adjust_bounds", "bf16_round", "pruned_lattice", "pruned_loss",
     "brute_force_logprob", "brute_force_paths", "band_mask", "full_step", "feasible",
-    "umax",
+    "umax", "log_softmax", "smoothed_parts", "smoothed_lattice", "smoothed_loss",
 ]
 
 
@@ -189,6 +189,105 @@ def simple_loss(am, lm, y, grad_scale=1.0, with_grads=True):
     out = dict(loss=-L, px=px, py=py, Lnorm=Lnorm, px_grad=ypr, py_grad=bpr)
     if with_grads:
         out["am_grad"], out["lm_grad"] = simple_grads(am, lm, y, Lnorm, ypr, bpr, grad_scale)
+    return out
+
+
+# ------------------------------------------- smoothed trivial joiner (Sec 3.1.1, Eq. 11-15)
+def log_softmax(x, axis=-1):
+    """x - logsumexp(x) along ``axis`` (the LogSoftmax of P:331)."""
+    x = np.asarray(x, np.float64)
+    return x - np.expand_dims(logsumexp(x, axis=axis), axis)
+
+
+def smoothed_parts(am, lm):
+    """The three log-prob tables of the smoothed trivial joiner, returned as callables
+    over (t, u, v) index arrays plus the utterance-level pieces:
+      L_lm(u,v)      = LogSoftmax_v L_dec(u,v)                                   (Eq. 14)
+      L_dec^avg(v)   = log (1/(U+1)) sum_{u=0}^{U} Softmax_v L_dec(u,v)          (Eq. 15; no t, u dependence)
+      L_acoustic(t,v)= LogSoftmax_v (L_enc(t,v) + L_dec^avg(v))                  (Eq. 13)
+    L_trivial is Eq. 12 (= Eq. 5-6): L_enc(t,v) + L_dec(u,v) - L_normalizer(t,u)."""
+    am = np.asarray(am, np.float64)
+    lm = np.asarray(lm, np.float64)
+    L_lm = log_softmax(lm, axis=1)                               # (U+1, V)
+    Lavg = logsumexp(L_lm, axis=0) - math.log(lm.shape[0])       # (V,)
+    L_ac = log_softmax(am + Lavg[None, :], axis=1)               # (T, V)
+    return L_lm, Lavg, L_ac
+
+
+def smoothed_lattice(am, lm, y, lm_only_scale, am_only_scale):
+    """(px, py) of the smoothed trivial joiner, Eq. 11:
+        L_smoothed = (1 - a_lm - a_ac) L_trivial + a_lm L_lm + a_ac L_acoustic,
+    with a_lm = lm_only_scale, a_ac = am_only_scale.  Eq. 11 as printed multiplies a_ac by L_lm a
+    second time; Eq. 13 defines L_acoustic for exactly this slot, so the third term is read as
+    a_ac L_acoustic (D18).  px(t,u) = L_smoothed(t,u,y_{u+1}) (-inf at u=U),
+    py(t,u) = L_smoothed(t,u,0)."""
+    am = np.asarray(am, np.float64)
+    lm = np.asarray(lm, np.float64)
+    y = np.asarray(y, np.int64)
+    T, U = am.shape[0], len(y)
+    a_lm, a_ac = float(lm_only_scale), float(am_only_scale)
+    w0 = 1.0 - a_lm - a_ac
+    px_t, py_t, Lnorm = trivial_lattice(am, lm, y)
+    L_lm, Lavg, L_ac = smoothed_parts(am, lm)
+    px = np.full((T, U + 1), NEG_INF)
+    if U > 0:
+        u = np.arange(U)
+        px[:, :U] = w0 * px_t[:, :U] + a_lm * L_lm[u, y][None, :] + a_ac * L_ac[:, y]
+    py = w0 * py_t + a_lm * L_lm[:, 0][None, :] + a_ac * L_ac[:, 0][:, None]
+    return px, py
+
+
+def smoothed_loss(am, lm, y, lm_only_scale, am_only_scale, grad_scale=1.0, with_grads=True):
+    """Smoothed-joiner stage for one utterance: loss = -L_tot on the Eq. 11 lattice, occupancies
+    px_grad = y', py_grad = empty' (P:272-281), and gs * d(-L_tot)/d{am, lm}.
+
+    The gradient is plain reverse-mode through the definitions: with dL(t,u,v) = d(-L_tot)/dL(t,u,v)
+    = -(y'(t,u) [v = y_{u+1}] + empty'(t,u) [v = 0]), each LogSoftmax z -> z - LSE(z) passes back
+    g - softmax(z) sum_v g, and L_dec^avg = log mean_u softmax(L_dec(u)) passes dLavg(v) back as
+    sum_v dLavg(v) P(u,v) ([v = v'] - P(u,v')) / ((U+1) avg(v)).  The (T, U+1, V) tensors are formed
+    one frame at a time."""
+    am = np.asarray(am, np.float64)
+    lm = np.asarray(lm, np.float64)
+    y = np.asarray(y, np.int64)
+    T, V = am.shape
+    U = len(y)
+    a_lm, a_ac = float(lm_only_scale), float(am_only_scale)
+    w0 = 1.0 - a_lm - a_ac
+    px, py = smoothed_lattice(am, lm, y, a_lm, a_ac)
+    L, ypr, bpr = occupancies(px, py)
+    out = dict(loss=-L, px=px, py=py, px_grad=ypr, py_grad=bpr)
+    if not with_grads:
+        return out
+    L_lm, Lavg, L_ac = smoothed_parts(am, lm)
+    Lnorm = trivial_normalizer(am, lm)
+    P_lm = np.exp(L_lm)                                          # (U+1, V)
+    P_ac = np.exp(L_ac)                                          # (T, V)
+    avg = np.exp(Lavg)                                           # (V,)
+    am_grad = np.zeros((T, V))
+    lm_grad = np.zeros((U + 1, V))
+    dLavg = np.zeros(V)
+    for t in range(T):
+        dL = np.zeros((U + 1, V))                                # d(-L)/dL(t, u, v)
+        if U > 0:
+            dL[np.arange(U), y] -= ypr[t, :U]
+        dL[:, 0] -= bpr[t]
+        sdl = dL.sum(axis=1)                                     # (U+1,)
+        # trivial term: LogSoftmax_v(am[t] + lm[u]) per u
+        P_tr = np.exp(am[t][None, :] + lm - Lnorm[t][:, None])   # (U+1, V)
+        g_tr = w0 * (dL - P_tr * sdl[:, None])
+        am_grad[t] += g_tr.sum(axis=0)
+        lm_grad += g_tr
+        # LM-only term: LogSoftmax_v(lm[u]) per u
+        lm_grad += a_lm * (dL - P_lm * sdl[:, None])
+        # acoustic term: LogSoftmax_v(am[t] + Lavg), summed over u first
+        g_ac = a_ac * (dL.sum(axis=0) - P_ac[t] * sdl.sum())
+        am_grad[t] += g_ac
+        dLavg += g_ac
+    # through L_dec^avg(v) = log mean_u softmax(lm[u])(v)
+    q = P_lm * (dLavg / ((U + 1) * avg))[None, :]                # (U+1, V)
+    lm_grad += q - P_lm * q.sum(axis=1)[:, None]
+    out["am_grad"] = grad_scale * am_grad
+    out["lm_grad"] = grad_scale * lm_grad
     return out
 
 

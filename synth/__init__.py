@@ -207,3 +207,41 @@ def make_custom(T_n, U_n, V, J, S, seed=0, logit_scale=1.0, poison=False) -> Bat
     return Batch(config=0, N=N, T=Tm, U=Um, V=V, J=J, S=S, T_n=T_n, U_n=U_n, symbols=symbols,
                  boundary=boundary, am=am, lm=lm, enc_proj=enc, dec_proj=dec,
                  w_out_bits=f32_to_bf16_bits(W), b_out_bits=f32_to_bf16_bits(b))
+
+
+# Dynamic-batch workload (Table 2): utterances sorted by
+# duration and packed so that the frames of a batch BEFORE padding stay within 10k input frames at
+# 100 fps, i.e. 2,500 encoder frames after the 4x subsampling the c2 lengths already assume
+# (reading D17).  Lengths follow the c2 recipe; the joiner weights are shared by all batches.
+DYNAMIC_CAP_FRAMES = 2500
+
+
+def make_dynamic_corpus(n_utts: int = 320, cap: int = DYNAMIC_CAP_FRAMES, seed: int | None = None) -> list:
+    """List of Batch: n_utts c2-shaped utterances, sorted by T, greedily packed under ``cap``."""
+    seed = SEED_BASE + 600 if seed is None else seed
+    rng = np.random.Generator(np.random.PCG64(seed))
+    T_n, U_n = draw_lengths(CONFIGS[2], rng, n_utts)
+    order = np.argsort(T_n, kind="stable")
+    T_n, U_n = T_n[order], U_n[order]
+    groups, cur, tot = [], [], 0
+    for i in range(n_utts):
+        if cur and tot + int(T_n[i]) > cap:
+            groups.append(cur)
+            cur, tot = [], 0
+        cur.append(i)
+        tot += int(T_n[i])
+    if cur:
+        groups.append(cur)
+    cfg = CONFIGS[2]
+    V, J, S = cfg["V"], cfg["J"], cfg["S"]
+    a = math.sqrt(6.0 / (J + V))
+    W = rng.uniform(-a, a, size=(V, J)).astype(np.float32)
+    b = rng.uniform(-a, a, size=(V,)).astype(np.float32)
+    wb, bb = f32_to_bf16_bits(W), f32_to_bf16_bits(b)
+    out = []
+    for k, g in enumerate(groups):
+        bt = make_custom(T_n[g], U_n[g], V, J, S, seed=seed + 1 + k)
+        bt.config = 6
+        bt.w_out_bits, bt.b_out_bits = wb, bb
+        out.append(bt)
+    return out

@@ -182,3 +182,33 @@ def test_sampled_utterances_full_size(cfg, k):
         db_ref += p["d_b"]
     assert_bf16_grad(gs["d_w"], dw_ref, "d_w")
     assert_bf16_grad(gs["d_b"], db_ref, "d_b")
+
+
+@pytest.mark.parametrize("which", [0, -1])
+def test_dynamic_batch_end_to_end(which):
+    """A batch of the dynamic-batch workload (sorted lengths, <= 2,500 encoder frames):
+    the whole path against the oracle, pruned stage at the GPU's own (bit-exact, D5) ranges."""
+    b = synth.make_dynamic_corpus()[which]
+    g = _run_step(b)
+    S = b.S
+    dw_ref = np.zeros((b.V, b.J))
+    db_ref = np.zeros(b.V)
+    for n in range(b.N):
+        d = b.utterance(n)
+        T, U = d["T"], d["U"]
+        s = O.simple_loss(d["am"], d["lm"], d["y"], 0.5)
+        assert_loss(g["loss_simple"][n:n + 1], [s["loss"]], f"loss_simple[{n}]")
+        assert_close_abs(g["px_grad"][n, :T, :U + 1], s["px_grad"], OCC_ATOL, f"px_grad[{n}]")
+        assert_close_abs(g["py_grad"][n, :T, :U + 1], s["py_grad"], OCC_ATOL, f"py_grad[{n}]")
+        assert_close_abs(g["am_grad"][n, :T], s["am_grad"], OCC_ATOL, f"am_grad[{n}]")
+        assert_close_abs(g["lm_grad"][n, :U + 1], s["lm_grad"], OCC_ATOL, f"lm_grad[{n}]")
+        own = O.adjust_bounds(O.raw_bounds(g["px_grad"][n, :T, :U + 1], g["py_grad"][n, :T, :U + 1], S), T, U, S)
+        assert np.array_equal(g["ranges"][n, :T], own), f"utt {n}: ranges differ on identical inputs"
+        p = O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"], own, S, 1.0, matched=True)
+        assert_loss(g["loss_pruned"][n:n + 1], [p["loss"]], f"loss_pruned[{n}]")
+        assert_bf16_grad(g["d_enc"][n, :T], p["d_enc"], f"d_enc[{n}]")
+        assert_bf16_grad(g["d_dec"][n, :U + 1], p["d_dec"], f"d_dec[{n}]")
+        dw_ref += p["d_w"]
+        db_ref += p["d_b"]
+    assert_bf16_grad(g["d_w"], dw_ref, "d_w")
+    assert_bf16_grad(g["d_b"], db_ref, "d_b")

@@ -49,3 +49,18 @@ def test_poison_padding():
     n = int(np.argmin(b.T_n))
     assert np.all(np.isnan(b.am[n, b.T_n[n]:]))
     assert np.all(np.isfinite(b.am[n, :b.T_n[n]]))
+
+
+def test_dynamic_corpus_packing():
+    """Table-2 protocol (PAPER.md 384-386): sorted lengths, every batch under the frame cap, all
+    utterances used once, shared joiner weights."""
+    import synth
+    c = synth.make_dynamic_corpus(n_utts=64)
+    assert sum(b.N for b in c) == 64
+    Ts = np.concatenate([b.T_n for b in c])
+    assert np.all(np.diff(Ts) >= 0)
+    for b in c:
+        assert int(b.T_n.sum()) <= synth.DYNAMIC_CAP_FRAMES
+        assert np.array_equal(b.w_out_bits, c[0].w_out_bits)
+    for b0, b1 in zip(c[:-1], c[1:]):   # greedy: the next utterance would not have fit
+        assert int(b0.T_n.sum()) + int(b1.T_n[0]) > synth.DYNAMIC_CAP_FRAMES

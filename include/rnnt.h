@@ -130,6 +130,32 @@ rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const 
                                         void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * Smoothed trivial joiner (Eq. 11-15): rnnt_simple_loss on the lattice of
+ *   L_smoothed(t,u,v) = (1 - a_lm - a_ac) L_trivial(t,u,v) + a_lm L_lm(u,v) + a_ac L_acoustic(t,v)
+ * with L_trivial = LogSoftmax_v(am[t,v] + lm[u,v]) (Eq. 12), L_lm = LogSoftmax_v lm[u,v] (Eq. 14),
+ * L_acoustic = LogSoftmax_v(am[t,v] + L_dec^avg(v)) (Eq. 13) and the per-utterance unigram prior
+ * L_dec^avg(v) = log (1/(U_n+1)) sum_{u<=U_n} Softmax_v lm[u,v] (Eq. 15).  Eq. 11 as printed repeats
+ * L_lm in its third term; it is read as L_acoustic (D18).
+ *   lm_only_scale = a_lm, am_only_scale = a_ac (finite; 0, 0 gives exactly rnnt_simple_loss).
+ * Every other argument, output and convention is that of rnnt_simple_loss /
+ * rnnt_simple_loss_backward; am_grad / lm_grad include the derivatives through all three terms
+ * (the L_dec^avg prior couples lm to every frame).  The backward needs the workspace of the
+ * forward call with the same scales.
+ */
+rnnt_status_t rnnt_simple_loss_smoothed(const float* am, const float* lm, const int64_t* symbols,
+                                        const int64_t* boundary, const rnnt_dims_t* dims,
+                                        float lm_only_scale, float am_only_scale, float grad_scale,
+                                        float* loss, float* px_grad, float* py_grad, float* am_grad,
+                                        float* lm_grad, int32_t* status, void* workspace,
+                                        size_t workspace_bytes, void* stream);
+rnnt_status_t rnnt_simple_loss_smoothed_backward(const float* am, const float* lm, const float* px_grad,
+                                                 const float* py_grad, const int64_t* symbols,
+                                                 const int64_t* boundary, const rnnt_dims_t* dims,
+                                                 float lm_only_scale, float am_only_scale,
+                                                 float grad_scale, float* am_grad, float* lm_grad,
+                                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Pruning bounds.  For every frame t < T_n:
  *   raw_t = argmax_{p=0..max(0,U_n-S+1)} ( -y'(t,p-1) + sum_{u=p}^{p+S-1} empty'(t,u) )  (Eq. 8)
  * evaluated in fp64 from the fp32 inputs in a fixed order (u ascending, then the

@@ -65,6 +65,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_simple_loss.restype = I32
     lib.rnnt_simple_loss_backward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
     lib.rnnt_simple_loss_backward.restype = I32
+    lib.rnnt_simple_loss_smoothed.argtypes = [P, P, P, P, DP, F, F, F, P, P, P, P, P, P, P, SZ, P]
+    lib.rnnt_simple_loss_smoothed.restype = I32
+    lib.rnnt_simple_loss_smoothed_backward.argtypes = [P, P, P, P, P, P, DP, F, F, F, P, P, P, SZ, P]
+    lib.rnnt_simple_loss_smoothed_backward.restype = I32
     lib.rnnt_get_ranges.argtypes = [P, P, P, DP, P, P, P]
     lib.rnnt_get_ranges.restype = I32
     lib.rnnt_prune.argtypes = [P, P, P, P, DP, P, P]
@@ -169,6 +173,24 @@ def rnnt_simple_loss_backward(am, lm, px_grad, py_grad, symbols, boundary, dims,
     _check(rc, "rnnt_simple_loss_backward")
 
 
+def rnnt_simple_loss_smoothed(am, lm, symbols, boundary, dims, lm_only_scale, am_only_scale, grad_scale, loss,
+                              px_grad, py_grad, am_grad, lm_grad, status, workspace, stream=None):
+    rc = load_library().rnnt_simple_loss_smoothed(
+        _ptr(am), _ptr(lm), _ptr(symbols), _ptr(boundary), ctypes.byref(dims), float(lm_only_scale),
+        float(am_only_scale), float(grad_scale), _ptr(loss), _ptr(px_grad), _ptr(py_grad), _ptr(am_grad),
+        _ptr(lm_grad), _ptr(status), _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_simple_loss_smoothed")
+
+
+def rnnt_simple_loss_smoothed_backward(am, lm, px_grad, py_grad, symbols, boundary, dims, lm_only_scale, am_only_scale,
+                                       grad_scale, am_grad, lm_grad, workspace, stream=None):
+    rc = load_library().rnnt_simple_loss_smoothed_backward(
+        _ptr(am), _ptr(lm), _ptr(px_grad), _ptr(py_grad), _ptr(symbols), _ptr(boundary), ctypes.byref(dims),
+        float(lm_only_scale), float(am_only_scale), float(grad_scale), _ptr(am_grad), _ptr(lm_grad), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_simple_loss_smoothed_backward")
+
+
 def rnnt_get_ranges(px_grad, py_grad, boundary, dims, ranges, status, stream=None):
     rc = load_library().rnnt_get_ranges(_ptr(px_grad), _ptr(py_grad), _ptr(boundary), ctypes.byref(dims),
                                         _ptr(ranges), _ptr(status), _stream(stream))
@@ -251,29 +273,45 @@ def _side_stream(device, which=0):
 
 
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
-         pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True):
+         pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True,
+         lm_only_scale=0.0, am_only_scale=0.0):
     """One fwd+bwd of the whole hot path: simple loss and its
     gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
     device tensors; ``out`` may supply preallocated outputs (same keys).
 
-    With ``overlap`` the am/lm gradients (rnnt_simple_loss_backward) run on a side stream
-    concurrently with the pruned stage, joined back into ``stream`` before returning."""
+    ``lm_only_scale`` / ``am_only_scale`` select the smoothed trivial joiner (Eq. 11-15) for the
+    simple stage (0, 0: the plain trivial joiner).  With ``overlap`` the am/lm gradients
+    (rnnt_simple_loss[_smoothed]_backward) run on a side stream concurrently with the pruned stage,
+    joined back into ``stream`` before returning."""
     dims = dims_of(am, lm, w_out, S)
     dev = am.device
     o = out if out is not None else alloc_outputs(dims, dev)
     ws = workspace if workspace is not None else _WS.get(dims, dev)
     st = o["status"] if status is None else status
     cur = stream if stream is not None else torch.cuda.current_stream(dev)
+    smooth = lm_only_scale != 0.0 or am_only_scale != 0.0
+
+    def fwd(am_grad, lm_grad):
+        if smooth:
+            rnnt_simple_loss_smoothed(am, lm, symbols, boundary, dims, lm_only_scale, am_only_scale, simple_scale,
+                                      o["loss_simple"], o["px_grad"], o["py_grad"], am_grad, lm_grad, st, ws, cur)
+        else:
+            rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
+                             o["py_grad"], am_grad, lm_grad, st, ws, cur)
+
     if overlap:
-        rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
-                         o["py_grad"], None, None, st, ws, cur)
+        fwd(None, None)
         side = _side_stream(dev)
         side.wait_stream(cur)
-        rnnt_simple_loss_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims, simple_scale,
-                                  o["am_grad"], o["lm_grad"], ws, side)
+        if smooth:
+            rnnt_simple_loss_smoothed_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims,
+                                               lm_only_scale, am_only_scale, simple_scale, o["am_grad"], o["lm_grad"],
+                                               ws, side)
+        else:
+            rnnt_simple_loss_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims, simple_scale,
+                                      o["am_grad"], o["lm_grad"], ws, side)
     else:
-        rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
-                         o["py_grad"], o["am_grad"], o["lm_grad"], st, ws, cur)
+        fwd(o["am_grad"], o["lm_grad"])
     rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
     rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], cur)
     if overlap:

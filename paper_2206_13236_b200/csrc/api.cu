@@ -11,14 +11,14 @@ namespace rnnt {
 cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
                                const int64_t* sym, const int64_t* bnd, float gs, float* loss,
                                float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
-                               int32_t* status, cudaStream_t st);
+                               int32_t* status, Smooth sm, cudaStream_t st);
 cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* py_grad, const int64_t* bnd,
                               int32_t* ranges, int32_t* status, cudaStream_t st);
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st);
 cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
-                                float gs, float* am_grad, float* lm_grad, cudaStream_t st);
+                                float gs, float* am_grad, float* lm_grad, Smooth sm, cudaStream_t st);
 size_t pruned_recursion_smem(const Dims& d);
 cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, const int64_t* sym, const int32_t* ranges, const int64_t* bnd,
@@ -47,7 +47,8 @@ static const char* const kNames[KID_COUNT] = {
     "lattice_combine", "simple_am_grad_gemm", "unused_am_picks", "simple_lm_grad_gemm", "unused_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_dh_tables", "joiner_d_dec",
-    "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums"};
+    "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
+    "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q"};
 
 const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }
 
@@ -118,29 +119,29 @@ static void* align_ws(void* ws) {
   return reinterpret_cast<void*>((p + 255) & ~uintptr_t(255));
 }
 
-rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* symbols,
-                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
-                               float* loss, float* px_grad, float* py_grad, float* am_grad,
-                               float* lm_grad, int32_t* status, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+static rnnt_status_t simple_loss_impl(const float* am, const float* lm, const int64_t* symbols,
+                                      const int64_t* boundary, const rnnt_dims_t* dims, Smooth sm, float grad_scale,
+                                      float* loss, float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
+                                      int32_t* status, void* workspace, size_t workspace_bytes, void* stream) {
   Dims d;
   rnnt_status_t rs = check_dims(dims, &d);
   if (rs != RNNT_OK) return rs;
   if (!am || !lm || !boundary || !loss || !px_grad || !py_grad || !workspace) return RNNT_ERR_INVALID_ARG;
   if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
   if (!aligned16(am) || !aligned16(lm)) return RNNT_ERR_INVALID_ARG;
+  if (!(sm.a_lm == sm.a_lm) || !(sm.a_ac == sm.a_ac)) return RNNT_ERR_INVALID_ARG;   // NaN scales
   if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
   SimpleWS sw;
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(simple_loss_launch(d, sw, am, lm, symbols, boundary, grad_scale, loss, px_grad, py_grad,
-                                        am_grad, lm_grad, status, (cudaStream_t)stream));
+                                        am_grad, lm_grad, status, sm, (cudaStream_t)stream));
 }
 
-rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const float* px_grad,
-                                        const float* py_grad, const int64_t* symbols, const int64_t* boundary,
-                                        const rnnt_dims_t* dims, float grad_scale, float* am_grad, float* lm_grad,
-                                        void* workspace, size_t workspace_bytes, void* stream) {
+static rnnt_status_t simple_backward_impl(const float* am, const float* lm, const float* px_grad,
+                                          const float* py_grad, const int64_t* symbols, const int64_t* boundary,
+                                          const rnnt_dims_t* dims, Smooth sm, float grad_scale, float* am_grad,
+                                          float* lm_grad, void* workspace, size_t workspace_bytes, void* stream) {
   Dims d;
   rnnt_status_t rs = check_dims(dims, &d);
   if (rs != RNNT_OK) return rs;
@@ -148,12 +149,49 @@ rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const 
   if (!am_grad && !lm_grad) return RNNT_ERR_INVALID_ARG;
   if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
   if (!aligned16(am) || !aligned16(lm) || !aligned16(am_grad) || !aligned16(lm_grad)) return RNNT_ERR_INVALID_ARG;
+  if (!(sm.a_lm == sm.a_lm) || !(sm.a_ac == sm.a_ac)) return RNNT_ERR_INVALID_ARG;
   if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
   SimpleWS sw;
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(simple_grads_launch(d, sw, am, lm, px_grad, py_grad, symbols, boundary, grad_scale, am_grad,
-                                         lm_grad, (cudaStream_t)stream));
+                                         lm_grad, sm, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_simple_loss(const float* am, const float* lm, const int64_t* symbols,
+                               const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                               float* loss, float* px_grad, float* py_grad, float* am_grad,
+                               float* lm_grad, int32_t* status, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  return simple_loss_impl(am, lm, symbols, boundary, dims, Smooth{}, grad_scale, loss, px_grad, py_grad, am_grad,
+                          lm_grad, status, workspace, workspace_bytes, stream);
+}
+
+rnnt_status_t rnnt_simple_loss_backward(const float* am, const float* lm, const float* px_grad,
+                                        const float* py_grad, const int64_t* symbols, const int64_t* boundary,
+                                        const rnnt_dims_t* dims, float grad_scale, float* am_grad, float* lm_grad,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  return simple_backward_impl(am, lm, px_grad, py_grad, symbols, boundary, dims, Smooth{}, grad_scale, am_grad,
+                              lm_grad, workspace, workspace_bytes, stream);
+}
+
+rnnt_status_t rnnt_simple_loss_smoothed(const float* am, const float* lm, const int64_t* symbols,
+                                        const int64_t* boundary, const rnnt_dims_t* dims, float lm_only_scale,
+                                        float am_only_scale, float grad_scale, float* loss, float* px_grad,
+                                        float* py_grad, float* am_grad, float* lm_grad, int32_t* status,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
+  return simple_loss_impl(am, lm, symbols, boundary, dims, Smooth{lm_only_scale, am_only_scale}, grad_scale, loss,
+                          px_grad, py_grad, am_grad, lm_grad, status, workspace, workspace_bytes, stream);
+}
+
+rnnt_status_t rnnt_simple_loss_smoothed_backward(const float* am, const float* lm, const float* px_grad,
+                                                 const float* py_grad, const int64_t* symbols,
+                                                 const int64_t* boundary, const rnnt_dims_t* dims,
+                                                 float lm_only_scale, float am_only_scale, float grad_scale,
+                                                 float* am_grad, float* lm_grad, void* workspace,
+                                                 size_t workspace_bytes, void* stream) {
+  return simple_backward_impl(am, lm, px_grad, py_grad, symbols, boundary, dims, Smooth{lm_only_scale, am_only_scale},
+                              grad_scale, am_grad, lm_grad, workspace, workspace_bytes, stream);
 }
 
 rnnt_status_t rnnt_get_ranges(const float* px_grad, const float* py_grad, const int64_t* boundary,

@@ -12,6 +12,7 @@ enum KernelId {
   KID_AMGRAD, KID_AMPICK, KID_LMGRAD, KID_LMPICK, KID_RAW, KID_ADJUST, KID_PRUNE, KID_ROWINFO,
   KID_JOINER_FWD, KID_SOFTMAX, KID_PALPHA, KID_PBETA, KID_PCOMBINE, KID_DH, KID_DENC, KID_DDEC,
   KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD, KID_OCCSUMS,
+  KID_SMOOTH_AVG, KID_SMOOTH_AC, KID_SMOOTH_GQ, KID_SMOOTH_Q,
   KID_COUNT
 };
 

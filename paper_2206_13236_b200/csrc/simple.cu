@@ -21,20 +21,20 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
 cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
                                const int64_t* bnd, int32_t* status, cudaStream_t st);
 cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
-                             const int64_t* bnd, int32_t* status, cudaStream_t st);
+                             const int64_t* bnd, int32_t* status, Smooth sm, cudaStream_t st);
 cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
-                                float gs, float* am_grad, float* lm_grad, cudaStream_t st);
+                                float gs, float* am_grad, float* lm_grad, Smooth sm, cudaStream_t st);
 
 cudaError_t simple_loss_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
                                const int64_t* sym, const int64_t* bnd, float gs, float* loss,
                                float* px_grad, float* py_grad, float* am_grad, float* lm_grad,
-                               int32_t* status, cudaStream_t st) {
+                               int32_t* status, Smooth sm, cudaStream_t st) {
   cudaError_t e;
   if ((e = simple_prep_launch(d, w, am, lm, sym, bnd, status, st)) != cudaSuccess) return e;
-  if ((e = norm_gemm_launch(d, w, am, lm, sym, bnd, status, st)) != cudaSuccess) return e;
+  if ((e = norm_gemm_launch(d, w, am, lm, sym, bnd, status, sm, st)) != cudaSuccess) return e;
   if ((e = lattice_launch(d, w, bnd, loss, px_grad, py_grad, status, st)) != cudaSuccess) return e;
-  if ((e = simple_grads_launch(d, w, am, lm, px_grad, py_grad, sym, bnd, gs, am_grad, lm_grad, st)) != cudaSuccess)
+  if ((e = simple_grads_launch(d, w, am, lm, px_grad, py_grad, sym, bnd, gs, am_grad, lm_grad, sm, st)) != cudaSuccess)
     return e;
   return cudaGetLastError();
 }

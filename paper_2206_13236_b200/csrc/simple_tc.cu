@@ -34,7 +34,7 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
                                                const int64_t* __restrict__ bnd, int N, int rows_per_n, int U, int V,
                                                int VP, int which, float* __restrict__ m, uint16_t* __restrict__ hi,
                                                uint16_t* __restrict__ lo, float* __restrict__ amy, int UPa,
-                                               uint16_t* __restrict__ onehot, int blk) {
+                                               uint16_t* __restrict__ onehot, float* __restrict__ lse, int blk) {
   const long long row = (long long)blk * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * rows_per_n) return;
@@ -56,6 +56,7 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   if (r >= lim) {   // padded row: zero operand, never read otherwise
     for (int v2 = lane; v2 < VP / 2; v2 += 32) { H[v2] = 0u; L[v2] = 0u; }
     if (lane == 0) m[row] = 0.f;
+    if (lse && lane == 0) lse[row] = 0.f;
     return;
   }
   const float* p = x + row * (long long)V;
@@ -63,14 +64,20 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   for (int v = lane; v < V; v += 32) mx = fmaxf(mx, p[v]);
   mx = warp_max(mx);
   if (lane == 0) m[row] = mx;
+  float esum = 0.f;
   for (int v2 = lane; v2 < VP / 2; v2 += 32) {
     const int v = 2 * v2;
     const float e0 = v < V ? __expf(p[v] - mx) : 0.f;
     const float e1 = v + 1 < V ? __expf(p[v + 1] - mx) : 0.f;
+    esum += e0 + e1;
     const __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
     const __nv_bfloat162 l = __floats2bfloat162_rn(e0 - __low2float(h), e1 - __high2float(h));
     H[v2] = *reinterpret_cast<const uint32_t*>(&h);
     L[v2] = *reinterpret_cast<const uint32_t*>(&l);
+  }
+  if (lse) {   // lm rows: log sum_v exp lm[u,v] (the LM-only log-softmax of Eq. 14)
+    esum = warp_sum(esum);
+    if (lane == 0) lse[row] = mx + __logf(esum);
   }
   if (which == 0) {
     float* ay = amy + ((size_t)n * rows_per_n + r) * UPa;
@@ -92,7 +99,7 @@ struct PrepParams {
   const float *am, *lm;
   const int64_t *sym, *bnd;
   int N, T, U, V, VP, UP, LU, K;
-  float *m_am, *m_lm, *amy;
+  float *m_am, *m_lm, *amy, *lse_lm;
   uint16_t *eam_hi, *eam_lo, *elm_hi, *elm_lo, *onehot;
   float2* pxy;
   int32_t* status;
@@ -102,13 +109,14 @@ struct PrepParams {
 __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
   int b = blockIdx.x;
   if (b < p.nb_am) {
-    exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr, b);
+    exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr,
+                   nullptr, b);
     return;
   }
   b -= p.nb_am;
   if (b < p.nb_lm) {
     exp_split_rows(p.lm, p.sym, p.bnd, p.N, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
-                   p.onehot, b);
+                   p.onehot, p.lse_lm, b);
     return;
   }
   b -= p.nb_lm;
@@ -146,7 +154,7 @@ __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
 __global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__ px_grad,
                                                        const float* __restrict__ py_grad, int T, int U, int ntb,
                                                        float* __restrict__ rowb, float* __restrict__ colpy,
-                                                       float* __restrict__ colpb) {
+                                                       float* __restrict__ colpb, float* __restrict__ rowy) {
   const int tb = blockIdx.x, n = blockIdx.y, U1 = U + 1, t0 = tb * 32;
   const int t1 = min(T, t0 + 32);
   for (int u = threadIdx.x; u < U1; u += blockDim.x) {
@@ -161,11 +169,106 @@ __global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = t0 + warp; t < t1; t += blockDim.x / 32) {
-    float s = 0.f;
-    for (int u = lane; u < U1; u += 32) s += py_grad[((size_t)n * T + t) * U1 + u];
+    float s = 0.f, sy = 0.f;
+    for (int u = lane; u < U1; u += 32) {
+      s += py_grad[((size_t)n * T + t) * U1 + u];
+      sy += px_grad[((size_t)n * T + t) * U1 + u];
+    }
     s = warp_sum(s);
-    if (lane == 0) rowb[(size_t)n * T + t] = s;
+    sy = warp_sum(sy);
+    if (lane == 0) { rowb[(size_t)n * T + t] = s; rowy[(size_t)n * T + t] = sy; }
   }
+}
+
+// ------------------------------------------------------------------ smoothed trivial joiner
+// Eq. 13-15 pieces that are not contractions: per utterance the unigram prior
+// L_dec^avg(v) and per frame the normaliser of L_acoustic, then in the backward the factor through
+// L_dec^avg.  One thread per column v (coalesced rows), or one warp per row.
+//   Lavg(v) = log( (1/(U+1)) sum_u exp(lm[u,v] - lse_lm(u)) )
+__global__ void __launch_bounds__(256) smooth_avg_kernel(const float* __restrict__ lm, const float* __restrict__ lse_lm,
+                                                         const int64_t* __restrict__ bnd, int U, int V, int VP,
+                                                         float* __restrict__ Lavg) {
+  const int n = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= VP) return;
+  const int Un = utt_U(bnd, n);
+  float s = 0.f;
+  if (v < V)
+    for (int u = 0; u <= Un; ++u) s += __expf(lm[((size_t)n * (U + 1) + u) * V + v] - lse_lm[(size_t)n * (U + 1) + u]);
+  Lavg[(size_t)n * VP + v] = v < V ? __logf(s / (float)(Un + 1)) : neg_inf_f();
+}
+
+//   lse_ac(t) = log sum_v exp(am[t,v] + Lavg(v))      (warp per frame)
+__global__ void __launch_bounds__(256) smooth_ac_kernel(const float* __restrict__ am, const float* __restrict__ m_am,
+                                                        const float* __restrict__ Lavg, const int64_t* __restrict__ bnd,
+                                                        int N, int T, int V, int VP, float* __restrict__ lse_ac) {
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)N * T) return;
+  const int n = (int)(row / T), t = (int)(row - (long long)n * T);
+  if (t >= utt_T(bnd, n)) {
+    if (lane == 0) lse_ac[row] = 0.f;
+    return;
+  }
+  const float* a = am + row * V;
+  const float* L = Lavg + (size_t)n * VP;
+  const float mx = m_am[row];
+  float s = 0.f;
+  for (int v = lane; v < V; v += 32) s += __expf(a[v] - mx + L[v]);
+  s = warp_sum(s);
+  if (lane == 0) lse_ac[row] = mx + __logf(s);
+}
+
+//   g_avg(v) = sum_t (sum_u y' + empty')(t) P_ac(t,v) - sum_u [v = y_{u+1}] sum_t y'(t,u) - [v = 0] sum_{t,u} empty'
+//   gq(v) = a_ac g_avg(v) / ((U+1) avg(v)),  P_ac(t,v) = exp(am[t,v] + Lavg(v) - lse_ac(t))
+__global__ void __launch_bounds__(256) smooth_gq_kernel(const float* __restrict__ am, const float* __restrict__ Lavg,
+                                                        const float* __restrict__ lse_ac, const float* __restrict__ rowy,
+                                                        const float* __restrict__ rowb, const float* __restrict__ colpy,
+                                                        const int64_t* __restrict__ sym, const int64_t* __restrict__ bnd,
+                                                        int T, int U, int V, int VP, int ntb, float a_ac,
+                                                        float* __restrict__ gq) {
+  const int n = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= VP) return;
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  float g = 0.f;
+  const float Lv = v < V ? Lavg[(size_t)n * VP + v] : 0.f;
+  if (v < V) {
+    float btot = 0.f;
+    for (int t = 0; t < Tn; ++t) {
+      const size_t r = (size_t)n * T + t;
+      const float ob = rowb[r];
+      g += (rowy[r] + ob) * __expf(am[r * V + v] + Lv - lse_ac[r]);
+      btot += ob;
+    }
+    if (v == 0) g -= btot;
+    for (int u = 0; u < Un; ++u)
+      if (sym[(size_t)n * U + u] == v) {
+        float cy = 0.f;
+        for (int tb = 0; tb < ntb; ++tb) cy += colpy[((size_t)n * ntb + tb) * (U + 1) + u];
+        g -= cy;
+      }
+  }
+  gq[(size_t)n * VP + v] = v < V ? a_ac * g / ((float)(Un + 1) * __expf(Lv)) : 0.f;
+}
+
+//   Q(u) = sum_v softmax(lm[u])(v) gq(v)      (warp per token row)
+__global__ void __launch_bounds__(256) smooth_q_kernel(const float* __restrict__ lm, const float* __restrict__ lse_lm,
+                                                       const float* __restrict__ gq, const int64_t* __restrict__ bnd,
+                                                       int N, int U, int V, int VP, float* __restrict__ Qu) {
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)N * (U + 1)) return;
+  const int n = (int)(row / (U + 1)), u = (int)(row - (long long)n * (U + 1));
+  if (u > utt_U(bnd, n)) {
+    if (lane == 0) Qu[row] = 0.f;
+    return;
+  }
+  const float* l = lm + row * V;
+  const float* g = gq + (size_t)n * VP;
+  const float z = lse_lm[row];
+  float s = 0.f;
+  for (int v = lane; v < V; v += 32) s += __expf(l[v] - z) * g[v];
+  s = warp_sum(s);
+  if (lane == 0) Qu[row] = s;
 }
 
 // ------------------------------------------------------------------ gemm3 mainloop
@@ -349,6 +452,9 @@ struct NormProb {
   float* rS;       // (N,K+1,LU) skewed 1/S(t,u) (valid cells only)
   int32_t* status;
   const float *am, *amy;
+  Smooth sm;                                   // Eq. 11 interpolation (both 0: plain trivial joiner)
+  const float *lse_lm, *Lavg, *lse_ac;         // smoothing tables (workspace.h)
+  int VPl;                                     // pitch of Lavg
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * BN, nkb, 0};
@@ -370,20 +476,25 @@ struct NormProb {
     float* lmy = reinterpret_cast<float*>(aux);
     float* lm0 = lmy + 256;
     float* mlm = lm0 + 256;
+    float* lz = mlm + 256;      // smoothing: lse_lm(u)
+    float* lyv = lz + 256;      // smoothing: Lavg(y_{u+1})
     const int Un = utt_U(bnd, t.n);
     for (int j = threadIdx.x; j < BN; j += 32 * sg::EPI_WARPS) {
       const int u = t.n0 + j;
-      float a = 0.f, b = 0.f, c = 0.f;
+      float a = 0.f, b = 0.f, c = 0.f, z = 0.f, w = 0.f;
       if (u <= Un) {
         const float* l = lm + ((size_t)t.n * (U + 1) + u) * V;
         if (u < Un) {
           long long yy = sym[(size_t)t.n * U + u];
-          a = l[yy < 0 ? 0 : (yy >= V ? V - 1 : yy)];   // address safety; bad symbols flagged in status
+          yy = yy < 0 ? 0 : (yy >= V ? V - 1 : yy);     // address safety; bad symbols flagged in status
+          a = l[yy];
+          if (sm.on()) w = Lavg[(size_t)t.n * VPl + yy];
         }
         b = l[0];
         c = m_lm[(size_t)t.n * (U + 1) + u];
+        if (sm.on()) z = lse_lm[(size_t)t.n * (U + 1) + u];
       }
-      lmy[j] = a; lm0[j] = b; mlm[j] = c;
+      lmy[j] = a; lm0[j] = b; mlm[j] = c; lz[j] = z; lyv[j] = w;
     }
     epi_bar();
   }
@@ -391,6 +502,8 @@ struct NormProb {
     const float* lmy = reinterpret_cast<const float*>(aux);
     const float* lm0 = lmy + 256;
     const float* mlm = lm0 + 256;
+    const float* lz = mlm + 256;
+    const float* lyv = lz + 256;
     const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
     const int trow = t.m0 + e.row;
     const bool rowok = trow < Tn;
@@ -402,6 +515,10 @@ struct NormProb {
     const float am0 = rowok ? am[arow * V] : 0.f;
     const float* ayr = amy + arow * UPa;
     const size_t nbase = (size_t)t.n * (K + 1);
+    const bool smooth = sm.on();
+    const float w0 = sm.w0();
+    const float lac = (smooth && rowok) ? lse_ac[arow] : 0.f;        // normaliser of L_acoustic(t,.)
+    const float L0 = smooth ? Lavg[(size_t)t.n * VPl] : 0.f;        // L_dec^avg(0)
     bool under = false;
     const int nch = (min(BN, Un + 1 - t.n0) + 31) / 32;   // 32-column chunks with at least one u <= U_n
     for (int c = e.g; c < nch; c += 2) {
@@ -427,6 +544,14 @@ struct NormProb {
           if (u < Un) px = fmaf(ay[j] + lmy[c0 + j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
           // empty(t,u), Eq. 2 + 5; out of the last frame only the terminal blank exists
           if (!(trow == Tn - 1 && u < Un)) py = fmaf(am0 + lm0[c0 + j], RNNT_LOG2E_F, -Ln2);
+          if (smooth) {
+            // Eq. 11: w0 L_trivial + a_lm L_lm (Eq. 14) + a_ac L_acoustic (Eq. 13)
+            if (u < Un)
+              px = fmaf(w0, px, RNNT_LOG2E_F * (sm.a_lm * (lmy[c0 + j] - lz[c0 + j]) +
+                                                sm.a_ac * (ay[j] + lyv[c0 + j] - lac)));
+            if (py > -1e29f)
+              py = fmaf(w0, py, RNNT_LOG2E_F * (sm.a_lm * (lm0[c0 + j] - lz[c0 + j]) + sm.a_ac * (am0 + L0 - lac)));
+          }
           r = rcp_approx(S);
         }
         bxy[e.lane][j] = make_float2(px, py);
@@ -460,6 +585,15 @@ struct AmProb {
   float gs;
   float* am_grad;
   bool tma_io;   // V % 4 == 0: fp32 rows are 16-B aligned, tiles move by TMA
+  Smooth sm;
+  const float *Lavg, *lse_ac, *rowy;
+  int VPl;
+  // d(-L)/d am[t,v] / gs = w0 E G~E_lm - (w0 + a_ac) picks + a_ac occ(t) P_ac(t,v)  (Eq. 11-13 chain rule)
+  __device__ __forceinline__ float grad(float x, float mam, float a0, float pick, float occ, float Lv, float lac) const {
+    float g = sm.w0() * __expf(x - mam) * a0 - (sm.w0() + sm.a_ac) * pick;
+    if (sm.a_ac != 0.f) g = fmaf(sm.a_ac * occ, __expf(x + Lv - lac), g);
+    return gs * g;
+  }
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
@@ -506,6 +640,9 @@ struct AmProb {
       const size_t row = (size_t)t.n * T + (live ? trow : 0);
       const float mam = live ? m_am[row] : 0.f;
       const float rb = live ? rowb[row] : 0.f;
+      const float occ = (live && sm.on()) ? rb + rowy[row] : 0.f;
+      const float lac = (live && sm.on()) ? lse_ac[row] : 0.f;
+      const float* Lr = Lavg + (size_t)t.n * VPl;
       for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
         float a0[32], a1[32];
@@ -527,7 +664,7 @@ struct AmProb {
           for (int i = 0; i < 4; ++i) {
             const int j = 4 * q + i;
             const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
-            o[i] = live ? gs * (__expf(xs[i] - mam) * a0[j] - pick) : 0.f;
+            o[i] = live ? grad(xs[i], mam, a0[j], pick, occ, sm.on() ? Lr[vc + j] : 0.f, lac) : 0.f;
           }
           *pq = make_float4(o[0], o[1], o[2], o[3]);
         }
@@ -547,6 +684,9 @@ struct AmProb {
     const size_t row0 = (size_t)t.n * T + t0w;
     const float mam = live ? m_am[row0 + e.lane] : 0.f;
     const float rb = live ? rowb[row0 + e.lane] : 0.f;
+    const float occ = (live && sm.on()) ? rb + rowy[row0 + e.lane] : 0.f;
+    const float lac = (live && sm.on()) ? lse_ac[row0 + e.lane] : 0.f;
+    const float* Lr = Lavg + (size_t)t.n * VPl;
     float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + e.warp * sg::SCR * 4);
     const int nin = min(32, Tn - t0w), nout = min(32, T - t0w);
     for (int c = e.g; c < 8; c += 2) {
@@ -569,7 +709,8 @@ struct AmProb {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float pick = a1[j] + ((vc + j == 0) ? rb : 0.f);
-        buf[e.lane][j] = live ? gs * (__expf(buf[e.lane][j] - mam) * a0[j] - pick) : 0.f;
+        buf[e.lane][j] = live ? grad(buf[e.lane][j], mam, a0[j], pick, occ, (sm.on() && vc + j < V) ? Lr[vc + j] : 0.f, lac)
+                              : 0.f;
       }
       warp_store_block(buf, am_grad + row0 * V + vc, V, nout, nc, e.lane);
     }
@@ -586,6 +727,16 @@ struct LmProb {
   float gs;
   float* lm_grad;
   bool tma_io;
+  Smooth sm;
+  const float *lse_lm, *gq, *Qu;
+  int VPl;
+  // d(-L)/d lm[u,v] / gs = w0 E G~^T E_am - (w0 + a_lm) picks + a_lm occ(u) P_lm + P_lm (gq(v) - Q(u))
+  __device__ __forceinline__ float grad(float x, float mlm, float acc, float pick, float occ, float lz, float g,
+                                        float Q) const {
+    float r = sm.w0() * __expf(x - mlm) * acc - (sm.w0() + sm.a_lm) * pick;
+    if (sm.on()) r = fmaf(__expf(x - lz), sm.a_lm * occ + g - Q, r);
+    return gs * r;
+  }
 
   __device__ Tile tile() const {
     Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
@@ -626,6 +777,9 @@ struct LmProb {
       }
       if (urow < Un) y = (int)sym[(size_t)t.n * U + urow];
     }
+    const float lz = (live && sm.on()) ? lse_lm[(size_t)t.n * U1 + urow] : 0.f;
+    const float Q = (live && sm.on()) ? Qu[(size_t)t.n * U1 + urow] : 0.f;
+    const float* gr = gq + (size_t)t.n * VPl;
     const int nep = epi_chunks(t);
     if (nep > 0) {
       const float mlm = live ? m_lm[(size_t)t.n * U1 + urow] : 0.f;
@@ -645,7 +799,7 @@ struct LmProb {
           for (int i = 0; i < 4; ++i) {
             const int j = 4 * q + i, v = vc + j;
             const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);
-            o[i] = live ? gs * (__expf(xs[i] - mlm) * acc[j] - pick) : 0.f;
+            o[i] = live ? grad(xs[i], mlm, acc[j], pick, csy + csb, lz, sm.on() ? gr[v] : 0.f, Q) : 0.f;
           }
           *pq = make_float4(o[0], o[1], o[2], o[3]);
         }
@@ -681,7 +835,8 @@ struct LmProb {
       for (int j = 0; j < 32; ++j) {
         const int v = vc + j;
         const float pick = (v == y ? csy : 0.f) + (v == 0 ? csb : 0.f);
-        buf[e.lane][j] = live ? gs * (__expf(buf[e.lane][j] - mlm) * acc[j] - pick) : 0.f;
+        buf[e.lane][j] = live ? grad(buf[e.lane][j], mlm, acc[j], pick, csy + csb, lz, (sm.on() && v < V) ? gr[v] : 0.f, Q)
+                              : 0.f;
       }
       warp_store_block(buf, lm_grad + row0 * V + vc, V, nout, nc, e.lane);
     }
@@ -713,7 +868,7 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   PrepParams p;
   p.am = am; p.lm = lm; p.sym = sym; p.bnd = bnd;
   p.N = d.N; p.T = d.T; p.U = d.U; p.V = d.V; p.VP = d.VP64(); p.UP = d.UP(); p.LU = d.LU(); p.K = d.K();
-  p.m_am = w.m_am; p.m_lm = w.m_lm; p.amy = w.amy;
+  p.m_am = w.m_am; p.m_lm = w.m_lm; p.amy = w.amy; p.lse_lm = w.lse_lm;
   p.eam_hi = w.Eam_hi; p.eam_lo = w.Eam_lo; p.elm_hi = w.Elm_hi; p.elm_lo = w.Elm_lo; p.onehot = w.onehot;
   p.pxy = w.pxy; p.status = status;
   p.nb_am = (int)(((long long)d.N * d.T + 7) / 8);
@@ -725,25 +880,39 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
 }
 
 cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
-                             const int64_t* bnd, int32_t* status, cudaStream_t st) {
+                             const int64_t* bnd, int32_t* status, Smooth sm, cudaStream_t st) {
+  if (sm.on()) {
+    // the smoothed joiner's utterance prior L_dec^avg and the L_acoustic normalisers (Eq. 13, 15)
+    RNNT_LAUNCH(KID_SMOOTH_AVG, st, smooth_avg_kernel<<<dim3((d.VP64() + 255) / 256, d.N), 256, 0, st>>>(
+        lm, w.lse_lm, bnd, d.U, d.V, d.VP64(), w.Lavg));
+    RNNT_LAUNCH(KID_SMOOTH_AC, st, smooth_ac_kernel<<<(unsigned)(((long long)d.N * d.T + 7) / 8), 256, 0, st>>>(
+        am, w.m_am, w.Lavg, bnd, d.N, d.T, d.V, d.VP64(), w.lse_ac));
+  }
   const int BN = std::min(256, (d.U1() + 15) / 16 * 16);
   Maps mp;
   if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
       !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))
     return cudaErrorInvalidValue;
   NormProb p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64, d.UP(),
-             w.pxy, w.rS, status, am, w.amy};
+             w.pxy, w.rS, status, am, w.amy, sm, w.lse_lm, w.Lavg, w.lse_ac, d.VP64()};
   dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.U1() + BN - 1) / BN, d.N);
   return launch_gemm3(p, grid, mp, KID_NORM, st);
 }
 
 cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
-                                float gs, float* am_grad, float* lm_grad, cudaStream_t st) {
+                                float gs, float* am_grad, float* lm_grad, Smooth sm, cudaStream_t st) {
   if (!am_grad && !lm_grad) return cudaSuccess;
   RNNT_LAUNCH(KID_OCCSUMS, st, occ_sums_kernel<<<dim3(d.ntb(), d.N), 256, 0, st>>>(px_grad, py_grad, d.T, d.U, d.ntb(),
-                                                                                   w.rowb, w.colpy, w.colpb));
+                                                                                   w.rowb, w.colpy, w.colpb, w.rowy));
   cudaError_t e;
+  if (sm.on() && lm_grad) {
+    // backward through L_dec^avg (Eq. 15): gq(v), then Q(u) = sum_v softmax(lm[u])(v) gq(v)
+    RNNT_LAUNCH(KID_SMOOTH_GQ, st, smooth_gq_kernel<<<dim3((d.VP64() + 255) / 256, d.N), 256, 0, st>>>(
+        am, w.Lavg, w.lse_ac, w.rowy, w.rowb, w.colpy, sym, bnd, d.T, d.U, d.V, d.VP64(), d.ntb(), sm.a_ac, w.gq));
+    RNNT_LAUNCH(KID_SMOOTH_Q, st, smooth_q_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(
+        lm, w.lse_lm, w.gq, bnd, d.N, d.U, d.V, d.VP64(), w.Qu));
+  }
   if (am_grad) {
     Maps mp;
     if (!tm3(&mp.m[0], w.Gt_hi, d.UP(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Gt_lo, d.UP(), d.T, d.N, sg::BM) ||
@@ -756,7 +925,7 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                !make_tmap_f32_3d(&mp.eout, am_grad, d.V, d.T, d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.T * 4, 32,
                                  sg::BM)))
       return cudaErrorInvalidValue;
-    AmProb p{am, w.m_am, w.rowb, bnd, d.T, d.U, d.V, gs, am_grad, io};
+    AmProb p{am, w.m_am, w.rowb, bnd, d.T, d.U, d.V, gs, am_grad, io, sm, w.Lavg, w.lse_ac, w.rowy, d.VP64()};
     dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
     if ((e = launch_gemm3(p, grid, mp, KID_AMGRAD, st)) != cudaSuccess) return e;
   }
@@ -771,7 +940,8 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                !make_tmap_f32_3d(&mp.eout, lm_grad, d.V, d.U1(), d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.U1() * 4,
                                  32, sg::BM)))
       return cudaErrorInvalidValue;
-    LmProb p{lm, w.m_lm, w.colpy, w.colpb, sym, bnd, d.T, d.U, d.V, d.ntb(), gs, lm_grad, io};
+    LmProb p{lm, w.m_lm, w.colpy, w.colpb, sym, bnd, d.T, d.U, d.V, d.ntb(), gs, lm_grad, io, sm, w.lse_lm, w.gq, w.Qu,
+             d.VP64()};
     dim3 grid((d.U1() + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
     if ((e = launch_gemm3(p, grid, mp, KID_LMGRAD, st)) != cudaSuccess) return e;
   }

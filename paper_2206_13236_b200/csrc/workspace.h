@@ -4,6 +4,7 @@
 #pragma once
 #include <stddef.h>
 #include <stdint.h>
+#include <cuda_runtime.h>
 
 namespace rnnt {
 
@@ -39,6 +40,14 @@ struct Dims {
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+// Interpolation weights of the smoothed trivial joiner (Eq. 11): a_lm = lm_only_scale, a_ac =
+// am_only_scale; both 0 is the plain trivial joiner.
+struct Smooth {
+  float a_lm = 0.f, a_ac = 0.f;
+  __host__ __device__ bool on() const { return a_lm != 0.f || a_ac != 0.f; }
+  __host__ __device__ float w0() const { return 1.f - a_lm - a_ac; }
+};
+
 struct SimpleWS {
   float* m_am;    // (N,T)     row max of am
   float* m_lm;    // (N,U+1)   row max of lm
@@ -62,6 +71,13 @@ struct SimpleWS {
   float* rowb;       // (N,T)      sum_u empty'(t,u)
   float* colpy;      // (N,ntb,U+1) per-32-frame-block partial sums of y'(t,u) over t
   float* colpb;      // (N,ntb,U+1) ... of empty'(t,u)
+  float* rowy;       // (N,T)      sum_u y'(t,u)
+  // smoothed trivial joiner (Eq. 11-15), used only when a scale is nonzero
+  float* lse_lm;     // (N,U+1)    log sum_v exp lm[u,v]
+  float* Lavg;       // (N,VP64)   L_dec^avg(v) = log mean_u softmax(lm[u])(v)   (Eq. 15)
+  float* lse_ac;     // (N,T)      log sum_v exp(am[t,v] + L_dec^avg(v))        (Eq. 13 normaliser)
+  float* gq;         // (N,VP64)   a_ac g_avg(v) / ((U+1) avg(v)): the L_dec^avg backward factor
+  float* Qu;         // (N,U+1)    sum_v softmax(lm[u])(v) gq(v)
 };
 
 struct PrunedWS {
@@ -140,6 +156,12 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.rowb = (float*)take(N * T * 4);
   s.colpy = (float*)take(N * NTB * U1 * 4);
   s.colpb = (float*)take(N * NTB * U1 * 4);
+  s.rowy = (float*)take(N * T * 4);
+  s.lse_lm = (float*)take(N * U1 * 4);
+  s.Lavg = (float*)take(N * VP64 * 4);
+  s.lse_ac = (float*)take(N * T * 4);
+  s.gq = (float*)take(N * VP64 * 4);
+  s.Qu = (float*)take(N * U1 * 4);
   PrunedWS p;
   p.splits = dw_splits(d);
   p.rowinfo = (int32_t*)take(R * 4);

@@ -201,3 +201,69 @@ def test_simple_backward_split_matches():
     torch.cuda.synchronize()
     for k in ("loss_simple", "px_grad", "py_grad", "am_grad", "lm_grad"):
         assert torch.equal(o1[k], o2[k]), k
+
+
+def _oracle_smoothed(b, a_lm, a_ac, gs=0.5):
+    r = dict(loss=np.zeros(b.N), px_grad=np.zeros((b.N, b.T, b.U + 1)), py_grad=np.zeros((b.N, b.T, b.U + 1)),
+             am_grad=np.zeros((b.N, b.T, b.V)), lm_grad=np.zeros((b.N, b.U + 1, b.V)))
+    for n in range(b.N):
+        d = b.utterance(n)
+        s = O.smoothed_loss(d["am"], d["lm"], d["y"], a_lm, a_ac, gs)
+        T, U = d["T"], d["U"]
+        r["loss"][n] = s["loss"]
+        r["px_grad"][n, :T, :U + 1] = s["px_grad"]
+        r["py_grad"][n, :T, :U + 1] = s["py_grad"]
+        r["am_grad"][n, :T] = s["am_grad"]
+        r["lm_grad"][n, :U + 1] = s["lm_grad"]
+    return r
+
+
+@pytest.mark.parametrize("case", [
+    dict(cfg=1, a_lm=0.25, a_ac=0.0),
+    dict(cfg=1, a_lm=0.0, a_ac=0.25),
+    dict(cfg=2, a_lm=0.25, a_ac=0.1),
+    dict(T=[40, 1, 17], U=[13, 0, 16], V=33, J=16, S=4, a_lm=0.2, a_ac=0.3),   # V % 4 != 0: generic epilogues
+])
+def test_smoothed_simple_stage(case):
+    """Smoothed trivial joiner (Eq. 11-15, D18) on the GPU against the fp64 oracle: loss, occupancies
+    and the am/lm gradients through all three terms (the split forward / side-stream backward form)."""
+    import torch
+    import paper_2206_13236_b200 as R
+    if "cfg" in case:
+        b = synth.make_batch(case["cfg"])
+    else:
+        b = synth.make_custom(case["T"], case["U"], case["V"], case["J"], case["S"], seed=5, logit_scale=2.0)
+    a_lm, a_ac = case["a_lm"], case["a_ac"]
+    dev = to_dev(b)
+    d = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
+    ws = torch.empty(R.rnnt_workspace_bytes(d), dtype=torch.uint8, device="cuda")
+    o = R.alloc_outputs(d, "cuda")
+    R.rnnt_simple_loss_smoothed(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], d, a_lm, a_ac, 0.5,
+                                o["loss_simple"], o["px_grad"], o["py_grad"], None, None, o["status"], ws)
+    R.rnnt_simple_loss_smoothed_backward(dev["am"], dev["lm"], o["px_grad"], o["py_grad"], dev["symbols"],
+                                         dev["boundary"], d, a_lm, a_ac, 0.5, o["am_grad"], o["lm_grad"], ws)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in o.items()}
+    ref = _oracle_smoothed(b, a_lm, a_ac)
+    assert_loss(g["loss_simple"], ref["loss"], "loss_simple")
+    for k in ("px_grad", "py_grad", "am_grad", "lm_grad"):
+        assert_close_abs(g[k], ref[k], OCC_ATOL, k)
+
+
+def test_smoothed_zero_scales_bit_identical():
+    """lm_only_scale = am_only_scale = 0 runs exactly the plain trivial-joiner path."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    dev = to_dev(b)
+    d = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
+    ws = torch.empty(R.rnnt_workspace_bytes(d), dtype=torch.uint8, device="cuda")
+    o1, o2 = R.alloc_outputs(d, "cuda"), R.alloc_outputs(d, "cuda")
+    R.rnnt_simple_loss(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], d, 0.5, o1["loss_simple"], o1["px_grad"],
+                       o1["py_grad"], o1["am_grad"], o1["lm_grad"], o1["status"], ws)
+    R.rnnt_simple_loss_smoothed(dev["am"], dev["lm"], dev["symbols"], dev["boundary"], d, 0.0, 0.0, 0.5,
+                                o2["loss_simple"], o2["px_grad"], o2["py_grad"], o2["am_grad"], o2["lm_grad"],
+                                o2["status"], ws)
+    torch.cuda.synchronize()
+    for k in ("loss_simple", "px_grad", "py_grad", "am_grad", "lm_grad"):
+        assert torch.equal(o1[k], o2[k]), k

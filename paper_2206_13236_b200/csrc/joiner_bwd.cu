@@ -13,6 +13,7 @@
 // Warps 0-3: in-place producers, then epilogue (TMEM lanes 32w..32w+31).
 // Warp 4: TMEM allocator, TMA issuer (one lane) and MMA issuer (another lane).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -119,6 +120,7 @@ struct JoinerDhParams {
   float* d_enc;            // (N,T,J) nullable
   float* d_dec;            // (N,U+1,J) nullable
   float* g_part;           // (ntiles, 2, S, J) boundary partials of d_dec
+  int dbg;                 // diagnostics (RNNT_DBG_DH): bit0 skip d_dec, bit1 skip d_enc, bit2 skip staging
 };
 
 // One CTA of 128 threads per frame-aligned tile: the tile table, the live-tile list, and zeros of
@@ -429,8 +431,10 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
               out[2 * i + 1] = accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2);
             }
           }
-          D4[rl * 8 + ((2 * qq) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
-          D4[rl * 8 + ((2 * qq + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
+          if (!(p.dbg & 4)) {
+            D4[rl * 8 + ((2 * qq) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
+            D4[rl * 8 + ((2 * qq + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
+          }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         if (trc) dh_trace_ep(it, bx, 2);
         const int ncol4 = min(32, nj - c0) / 4;
         // d_enc: one float4 output per (frame, 4-column group)
-        if (p.d_enc)
+        if (p.d_enc && !(p.dbg & 2))
           for (int i = gt; i < F * 8; i += 128) {
             const int f = i >> 3, qq = i & 7;
             if (qq < ncol4 && g0 + f < NT) {
@@ -461,7 +465,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
           }
         if (trc) dh_trace_ep(it, bx, 3);
         // d_dec: one float4 output per (token position of a segment, 4-column group)
-        if (p.d_dec)
+        if (p.d_dec && !(p.dbg & 1))
           for (int i = gt; i < nent * 8; i += 128) {
             const int e = i >> 3, qq = i & 7;
             if (qq >= ncol4) continue;
@@ -746,7 +750,8 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, static_cast<DhTab*>(tabs), live, nlive, d_enc));
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
-                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part};
+                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0};
+  if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);

@@ -16,6 +16,7 @@ kname = sys.argv[2] if len(sys.argv) > 2 else "joiner_fwd_gemm"
 times = []
 for i in range(12):
     a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); c.record()          # materialise the event handles
     R.rnnt_profile_kernel(ids[kname], a, c)
     R.rnnt_pruned_loss(o["h"], dev["w_out"], dev["b_out"], dev["symbols"], o["ranges"], dev["boundary"], d, 1.0,
                        o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], o["status"], ws)

@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic"],
-                    help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch)")
+    ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic", "full"],
+                    help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch); "
+                         "full: the unpruned loss with the same joiner on the c2 batch (SURVEY 8(f) f4)")
     return ap.parse_args()
 
 
@@ -292,6 +293,59 @@ def run_dynamic(args):
     return 0
 
 
+# ------------------------------------------------------------------ full (unpruned) loss
+def run_full(args):
+    """The full RNN-T loss (every (t,u) through the joiner) on the c2 batch: the
+    in-house counterpart of the paper's unpruned baselines (Tables 1-2), same metric and timing rules."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    dev = R.batch_to_device(b, "cuda")
+    dims = R.make_dims(b.N, b.T, b.U, b.V, b.J, 1)
+    f32 = dict(dtype=torch.float32, device="cuda")
+    o = dict(loss=torch.empty(b.N, **f32), d_enc=torch.empty(b.N, b.T, b.J, **f32),
+             d_dec=torch.empty(b.N, b.U + 1, b.J, **f32), d_w=torch.empty(b.V, b.J, **f32),
+             d_b=torch.empty(b.V, **f32), status=torch.zeros(b.N, dtype=torch.int32, device="cuda"))
+    ws = torch.empty(R.rnnt_full_workspace_bytes(dims), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        R.rnnt_full_loss(dev["enc_proj"], dev["dec_proj"], dev["w_out"], dev["b_out"], dev["symbols"],
+                         dev["boundary"], dims, 1.0, o["loss"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"],
+                         o["status"], ws)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = Clocks(0)
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(K):
+        flush.zero_()
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = [a.elapsed_time(c) for a, c in ev]
+    frames = int(b.T_n.sum())
+    rows = int((b.T_n * (b.U_n + 1)).sum())
+    line = {"metric": "full (unpruned) RNN-T loss fwd+bwd frames(N·T)/sec and peak GB, 1 B200", "value":
+            frames / (statistics.mean(ms) / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": K,
+            "warmup": max(args.warmup, 3), "ms_per_step": statistics.mean(ms), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16+f32", "data": "synthetic",
+            "config": {"workload": "c2 batch, full lattice through the joiner (S = U+1, SURVEY 8(f) f4)",
+                       "N": b.N, "V": b.V, "J": b.J, "frames": frames, "joiner_rows": rows,
+                       "l2": "flushed between timed steps", "kernels": R.rnnt_version()},
+            "peak_gib": torch.cuda.max_memory_allocated() / 2 ** 30 - flush.numel() / 2 ** 30,
+            "workspace_gib": ws.numel() / 2 ** 30, "clocks": clk}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -300,6 +354,8 @@ def main():
         return run_reference(args, world, rank)
     if args.workload == "dynamic":
         return run_dynamic(args)
+    if args.workload == "full":
+        return run_full(args)
     import torch
     import paper_2206_13236_b200 as R
     torch.cuda.set_device(local)

@@ -222,6 +222,23 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
                                                float* d_b, void* workspace, size_t workspace_bytes,
                                                void* stream);
 
+/*
+ * Full (unpruned) transducer loss with the same non-linear joiner (the comparison
+ * class of P:44-52, P:171-176 and Tables 1-2): the band widened to every token position
+ * (S = U_n + 1, all bounds 0), so the joiner runs on all (N, T, U+1) lattice nodes:
+ *   h = bf16(tanh(enc_proj[t] + dec_proj[u])), z = W_out h + b, L = log_softmax(z) (D13),
+ *   loss[n] = -log P(y | x) of the full lattice (Eq. 3 with the joiner's arcs),
+ *   d_enc / d_dec / d_w / d_b = grad_scale * d(sum loss)/d(.) (d_enc, d_dec nullable).
+ * dims.S is ignored.  Memory grows as N T (U+1) (J + V) — the cost the pruned loss avoids; size the
+ * workspace with rnnt_full_workspace_bytes.  Same conventions as rnnt_pruned_loss otherwise.
+ */
+size_t rnnt_full_workspace_bytes(const rnnt_dims_t* dims);
+rnnt_status_t rnnt_full_loss(const float* enc_proj, const float* dec_proj, const uint16_t* w_out,
+                             const uint16_t* b_out, const int64_t* symbols, const int64_t* boundary,
+                             const rnnt_dims_t* dims, float grad_scale, float* loss, float* d_enc,
+                             float* d_dec, float* d_w, float* d_b, int32_t* status, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_simple_loss.restype = I32
     lib.rnnt_simple_loss_backward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
     lib.rnnt_simple_loss_backward.restype = I32
+    lib.rnnt_full_workspace_bytes.argtypes = [DP]
+    lib.rnnt_full_workspace_bytes.restype = SZ
+    lib.rnnt_full_loss.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
+    lib.rnnt_full_loss.restype = I32
     lib.rnnt_simple_loss_smoothed.argtypes = [P, P, P, P, DP, F, F, F, P, P, P, P, P, P, P, SZ, P]
     lib.rnnt_simple_loss_smoothed.restype = I32
     lib.rnnt_simple_loss_smoothed_backward.argtypes = [P, P, P, P, P, P, DP, F, F, F, P, P, P, SZ, P]
@@ -189,6 +193,40 @@ def rnnt_simple_loss_smoothed_backward(am, lm, px_grad, py_grad, symbols, bounda
         float(lm_only_scale), float(am_only_scale), float(grad_scale), _ptr(am_grad), _ptr(lm_grad), _ptr(workspace),
         workspace.numel() * workspace.element_size(), _stream(stream))
     _check(rc, "rnnt_simple_loss_smoothed_backward")
+
+
+def rnnt_full_workspace_bytes(dims) -> int:
+    return int(load_library().rnnt_full_workspace_bytes(ctypes.byref(dims)))
+
+
+def rnnt_full_loss(enc_proj, dec_proj, w_out, b_out, symbols, boundary, dims, grad_scale, loss, d_enc, d_dec, d_w,
+                   d_b, status, workspace, stream=None):
+    rc = load_library().rnnt_full_loss(
+        _ptr(enc_proj), _ptr(dec_proj), _ptr(w_out), _ptr(b_out), _ptr(symbols), _ptr(boundary), ctypes.byref(dims),
+        float(grad_scale), _ptr(loss), _ptr(d_enc), _ptr(d_dec), _ptr(d_w), _ptr(d_b), _ptr(status), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_full_loss")
+
+
+def full_loss(enc_proj, dec_proj, w_out, b_out, symbols, boundary, grad_scale=1.0, stream=None):
+    """The full (unpruned) loss with the same joiner: returns a dict of device
+    tensors loss, d_enc, d_dec, d_w, d_b, status (allocates its own workspace)."""
+    N, T, J = enc_proj.shape
+    U = dec_proj.shape[1] - 1
+    V = w_out.shape[0]
+    dims = make_dims(N, T, U, V, J, 1)
+    dev = enc_proj.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    o = dict(loss=torch.empty(N, **f32), d_enc=torch.empty(N, T, J, **f32), d_dec=torch.empty(N, U + 1, J, **f32),
+             d_w=torch.empty(V, J, **f32), d_b=torch.empty(V, **f32),
+             status=torch.zeros(N, dtype=torch.int32, device=dev))
+    nbytes = rnnt_full_workspace_bytes(dims)
+    if nbytes == 0:
+        raise RNNTError("invalid dims for rnnt_full_loss")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    rnnt_full_loss(enc_proj, dec_proj, w_out, b_out, symbols, boundary, dims, grad_scale, o["loss"], o["d_enc"],
+                   o["d_dec"], o["d_w"], o["d_b"], o["status"], ws, stream)
+    return o
 
 
 def rnnt_get_ranges(px_grad, py_grad, boundary, dims, ranges, status, stream=None):

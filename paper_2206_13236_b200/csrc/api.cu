@@ -28,6 +28,9 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
                                     cudaStream_t st);
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
                                      cudaStream_t st);
+cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const float* dec, const uint16_t* W,
+                             const uint16_t* b, const int64_t* sym, const int64_t* bnd, float gs, float* loss,
+                             float* d_enc, float* d_dec, float* d_w, float* d_b, int32_t* status, cudaStream_t st);
 cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                const uint16_t* b, const int64_t* sym, const int32_t* ranges,
                                const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
@@ -48,7 +51,8 @@ static const char* const kNames[KID_COUNT] = {
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_dh_tables", "joiner_d_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
-    "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q"};
+    "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
+    "full_dgrad"};
 
 const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }
 
@@ -73,7 +77,7 @@ static rnnt_status_t check_dims(const rnnt_dims_t* dims, Dims* d) {
   if ((long long)d->U >= (long long)d->T * 64) return RNNT_ERR_INVALID_ARG;
   if (d->J < 8 || d->J > 4096 || d->J % 8) return RNNT_ERR_INVALID_ARG;
   if (d->lat_R() == 0) return RNNT_ERR_UNSUPPORTED;   // recursion kernel: one warp x <= 32 columns per lane
-  if (d->UP() > 832) return RNNT_ERR_UNSUPPORTED;     // combine kernel: 2 x 32 x UP fp32 staging in smem
+  if (d->UP() > 576) return RNNT_ERR_UNSUPPORTED;     // combine kernel: 3 x 32 x UP fp32 staging in smem
   return RNNT_OK;
 }
 
@@ -85,6 +89,25 @@ size_t rnnt_workspace_bytes(const rnnt_dims_t* dims) {
   Dims d;
   if (check_dims(dims, &d) != RNNT_OK) return 0;
   return carve(d, nullptr, nullptr, nullptr);
+}
+
+// dims of the full (unpruned) loss: S is ignored (the band is every token position)
+static rnnt_status_t check_full_dims(const rnnt_dims_t* dims, Dims* d) {
+  if (!dims) return RNNT_ERR_INVALID_ARG;
+  rnnt_dims_t x = *dims;
+  x.S = 1;
+  rnnt_status_t rs = check_dims(&x, d);
+  if (rs != RNNT_OK) return rs;
+  Dims df = *d;
+  df.S = d->U + 1;
+  *d = df;
+  return RNNT_OK;
+}
+
+size_t rnnt_full_workspace_bytes(const rnnt_dims_t* dims) {
+  Dims d;
+  if (check_full_dims(dims, &d) != RNNT_OK) return 0;
+  return carve_full(d, nullptr, nullptr, nullptr, nullptr);
 }
 
 const char* rnnt_status_string(rnnt_status_t s) {
@@ -233,6 +256,26 @@ rnnt_status_t rnnt_pruned_loss(const uint16_t* h, const uint16_t* w_out, const u
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_loss_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss,
                                         d_enc, d_dec, d_w, d_b, status, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_full_loss(const float* enc_proj, const float* dec_proj, const uint16_t* w_out,
+                             const uint16_t* b_out, const int64_t* symbols, const int64_t* boundary,
+                             const rnnt_dims_t* dims, float grad_scale, float* loss, float* d_enc, float* d_dec,
+                             float* d_w, float* d_b, int32_t* status, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_full_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!enc_proj || !dec_proj || !w_out || !b_out || !boundary || !loss || !d_w || !d_b || !workspace)
+    return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(enc_proj) || !aligned16(dec_proj) || !aligned16(w_out) || !aligned16(d_enc) || !aligned16(d_dec))
+    return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve_full(d, nullptr, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  Dims d0 = d;
+  d0.S = 1;
+  return cuda_status(full_loss_launch(d0, align_ws(workspace), enc_proj, dec_proj, w_out, b_out, symbols, boundary,
+                                      grad_scale, loss, d_enc, d_dec, d_w, d_b, status, (cudaStream_t)stream));
 }
 
 rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,

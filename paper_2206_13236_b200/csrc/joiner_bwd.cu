@@ -121,6 +121,8 @@ struct JoinerDhParams {
   float* d_dec;            // (N,U+1,J) nullable
   float* g_part;           // (ntiles, 2, S, J) boundary partials of d_dec
   int dbg;                 // diagnostics (RNNT_DBG_DH): bit0 skip d_dec, bit1 skip d_enc, bit2 skip staging
+  int rt;                  // rows per tile (F*S frame-aligned; 128 in the generic mode)
+  float* dpre_out;         // generic mode (full lattice): dpre = dh (1-h^2) rows to global, no tables
 };
 
 // One CTA of 128 threads per frame-aligned tile: the tile table, the live-tile list, and zeros of
@@ -250,7 +252,8 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   const DhTab* tabs_s = reinterpret_cast<const DhTab*>(smem + TAB_OFF);
   uint8_t* hbuf = smem + H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = p.S, F = p.F, RT = F * S;
+  const int S = p.S, F = p.F, RT = p.rt;
+  const bool generic = p.dpre_out != nullptr;
   const long long NT = (long long)p.N * p.T;
   const long long nitems = (long long)(*p.nlive) * p.njp;
 
@@ -288,10 +291,11 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
         const int slot = it & 1;
         dh_trace(it, 0);
-        tc::mbar_wait(&tabempty[slot], ((it >> 1) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&tabfull[slot], (uint32_t)sizeof(DhTab));
-        tc::bulk_load(smem + TAB_OFF + slot * TAB_BYTES, p.tabs + tile,
-                      (uint32_t)sizeof(DhTab), &tabfull[slot]);
+        if (!generic) {
+          tc::mbar_wait(&tabempty[slot], ((it >> 1) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&tabfull[slot], (uint32_t)sizeof(DhTab));
+          tc::bulk_load(smem + TAB_OFF + slot * TAB_BYTES, p.tabs + tile, (uint32_t)sizeof(DhTab), &tabfull[slot]);
+        }
         const long long m0 = (long long)tile * RT;
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
         const int grows = (int)min((long long)BM, p.g.R - m0);
@@ -403,11 +407,11 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
       const int nbox = (nj + 63) / 64;
       const DhTab* tb = reinterpret_cast<const DhTab*>(reinterpret_cast<const uint8_t*>(tabs_s) + slot * TAB_BYTES);
-      tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
+      if (!generic) tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
       if (warp == 6 && lane == 0) dh_trace(it, 3);
-      const int nent = tb->nent;
+      const int nent = generic ? 0 : tb->nent;
       for (int bx = 0; bx < nbox; ++bx) {
         const int c0 = 64 * bx + 32 * g;
         tc::mbar_wait(&hfull[hslot], hph);
@@ -431,7 +435,13 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
               out[2 * i + 1] = accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2);
             }
           }
-          if (!(p.dbg & 4)) {
+          if (generic) {
+            if (qq < nq && rl < RT && r < p.g.R) {
+              float4* dst = reinterpret_cast<float4*>(p.dpre_out + (size_t)r * p.J + j0 + c0 + 8 * qq);
+              dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+              dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+            }
+          } else if (!(p.dbg & 4)) {
             D4[rl * 8 + ((2 * qq) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
             D4[rl * 8 + ((2 * qq + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
           }
@@ -440,6 +450,14 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
         if (++hslot == 2) { hslot = 0; hph ^= 1; }
         if (!have) continue;
+        if (generic) {
+          if (c0 + 64 >= nj) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+          }
+          continue;
+        }
         if (c0 + 64 >= nj) {            // last TMEM read of this accumulator by this warp
           tc::fence_before_sync();
           __syncwarp();
@@ -495,7 +513,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         if (lane == 0) tc::mbar_arrive(&tempty[acc]);
       }
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tabempty[slot]);
+      if (lane == 0 && !generic) tc::mbar_arrive(&tabempty[slot]);
       if (warp == 6 && lane == 0) dh_trace(it, 4);
     }
   }
@@ -750,7 +768,7 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, static_cast<DhTab*>(tabs), live, nlive, d_enc));
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
-                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0};
+                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0, F * d.S, nullptr};
   if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -759,6 +777,27 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   if (d_dec)
     RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(
         ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, part, d_dec));
+  return cudaGetLastError();
+}
+
+// Generic mode (the full, unpruned lattice of f4): tiles of 128 consecutive rows (the live ones in
+// `live`, count at `nlive`), dpre = dh (1 - h^2) written to `dpre_out` (R, J) fp32; the d_enc / d_dec
+// reductions run afterwards over the (t, u) grid.
+cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
+                                     const int* live, const int* nlive, long long ntiles, float* dpre_out,
+                                     cudaStream_t st) {
+  CUtensorMap tp, tw, th;
+  if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+  const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
+                   nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out};
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
+  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   return cudaGetLastError();
 }
 

@@ -534,6 +534,14 @@ static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cu
   return cudaGetLastError();
 }
 
+cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
+                           const int64_t* bnd, const uint16_t* b, cudaStream_t st) {
+  const long long R = d.rows();
+  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256 + 1), 256, 0, st>>>(
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
+  return cudaGetLastError();
+}
+
 // Forward: per-row info, K8 joiner with fused log-softmax, K9 recursion, the occupancies and the
 // packed backward scalars.
 cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
@@ -542,8 +550,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
-  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256 + 1), 256, 0, st>>>(
-      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
+  if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);

@@ -32,7 +32,7 @@ struct Dims {
   int VP64() const { return (V + 63) / 64 * 64; }       // bf16 pitch of the E operands (K-major boxes of 64)
   int UP() const { return (U + 1 + 63) / 64 * 64; }      // bf16 pitch of G~ (t-major, K-major boxes of 64)
   int ntb() const { return (T + 31) / 32; }              // 32-frame blocks of the occupancy column partials
-  int dh_frames() const { return 128 / S; }                                // frames per joiner_dh tile
+  int dh_frames() const { return S <= 128 ? 128 / S : 1; }                // frames per joiner_dh tile
   long long dh_tiles() const { return ((long long)N * T + dh_frames() - 1) / dh_frames(); }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
   int VP() const { return (V + 127) / 128 * 128; }      // padded row pitch of P~ (elements)
@@ -183,14 +183,42 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);
   p.gpk = (float4*)take(R * NT * 16);
-  p.dpart = (float*)take((size_t)d.dh_tiles() * 2 * d.S * J * 4);
-  p.dhtab = take((size_t)d.dh_tiles() * 2576);
-  p.dhlive = (int*)take(((size_t)d.dh_tiles() + 1) * 4);
+  // frame-aligned joiner_dh tables (S <= 128); the full-lattice path (S = U+1 > 128 possible) uses
+  // 128-row tiles instead and only the live list
+  const bool framed = d.S <= 128;
+  const size_t ltiles = framed ? (size_t)d.dh_tiles() : (R + 127) / 128;
+  p.dpart = (float*)take(framed ? (size_t)d.dh_tiles() * 2 * d.S * J * 4 : 0);
+  p.dhtab = take(framed ? (size_t)d.dh_tiles() * 2576 : 0);
+  p.dhlive = (int*)take((ltiles + 1) * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);
   if (sw) *sw = s;
   if (pw) *pw = p;
   return off + 256;  // slack for base alignment
+}
+
+// The full (unpruned) lattice of SURVEY 8(f) f4: the pruned workspace of dims with S = U+1 (every
+// (t,u) is a band row), then all-zero bounds and the dpre rows of the generic joiner_dh mode.
+struct FullWS {
+  int32_t* ranges0;  // (N,T) all zero: the band [0, U] of every frame
+  float* dpre;       // (R,J) dpre = dh (1 - h^2) for every (t,u) row
+  uint16_t* h;       // (R,J) bf16 joiner input of every (t,u)
+};
+inline size_t carve_full(const Dims& df, void* base, SimpleWS* sw, PrunedWS* pw, FullWS* fw) {
+  const size_t inner = carve(df, base, sw, pw);
+  size_t off = align_up(inner);
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) -> void* {
+    void* q = b ? (void*)(b + off) : nullptr;
+    off += align_up(bytes);
+    return q;
+  };
+  FullWS f;
+  f.ranges0 = (int32_t*)take((size_t)df.N * df.T * 4);
+  f.dpre = (float*)take((size_t)df.rows() * df.J * 4);
+  f.h = (uint16_t*)take((size_t)df.rows() * df.J * 2);
+  if (fw) *fw = f;
+  return off + 256;
 }
 
 }  // namespace rnnt

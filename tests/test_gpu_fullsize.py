@@ -212,3 +212,68 @@ def test_dynamic_batch_end_to_end(which):
         db_ref += p["d_b"]
     assert_bf16_grad(g["d_w"], dw_ref, "d_w")
     assert_bf16_grad(g["d_b"], db_ref, "d_b")
+
+
+def _oracle_full(b, idx=None):
+    """Full (unpruned) loss: the oracle's pruned loss with every frame's band [0, U_n] (S = U_n+1,
+    all bounds 0), which the oracle pins equal to the dense RNN-T loss (test_oracle_pruned)."""
+    idx = range(b.N) if idx is None else idx
+    r = dict(loss={}, d_enc={}, d_dec={}, d_w=np.zeros((b.V, b.J)), d_b=np.zeros(b.V))
+    for n in idx:
+        d = b.utterance(n)
+        T, U = d["T"], d["U"]
+        p = O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"], np.zeros(T, np.int64), U + 1, 1.0, matched=True)
+        r["loss"][n] = p["loss"]
+        r["d_enc"][n] = p["d_enc"]
+        r["d_dec"][n] = p["d_dec"]
+        r["d_w"] += p["d_w"]
+        r["d_b"] += p["d_b"]
+    return r
+
+
+def _run_full(b):
+    import torch
+    import paper_2206_13236_b200 as R
+    dev = to_dev(b)
+    o = R.full_loss(dev["enc_proj"], dev["dec_proj"], dev["w_out"], dev["b_out"], dev["symbols"], dev["boundary"])
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in o.items()}
+
+
+@pytest.mark.parametrize("case", [
+    dict(cfg=1),
+    dict(T=[40, 1, 17, 9], U=[13, 0, 16, 2], V=33, J=16),          # ragged, T=1/U=0, U=T-1
+    dict(T=[30, 200], U=[150, 60], V=40, J=24),                     # U+1 > 128: 128-row tiles across frames
+])
+def test_full_loss_small(case):
+    """the full (unpruned) loss on the GPU against the oracle, every output."""
+    b = synth.make_batch(1) if "cfg" in case else synth.make_custom(case["T"], case["U"], case["V"], case["J"], 3,
+                                                                    seed=7, logit_scale=2.0)
+    g = _run_full(b)
+    ref = _oracle_full(b)
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        assert_loss(g["loss"][n:n + 1], [ref["loss"][n]], f"loss[{n}]")
+        assert_bf16_grad(g["d_enc"][n, :T], ref["d_enc"][n], f"d_enc[{n}]")
+        assert_bf16_grad(g["d_dec"][n, :U + 1], ref["d_dec"][n], f"d_dec[{n}]")
+        assert np.all(g["d_enc"][n, T:] == 0) and np.all(g["d_dec"][n, U + 1:] == 0)
+    assert_bf16_grad(g["d_w"], ref["d_w"], "d_w")
+    assert_bf16_grad(g["d_b"], ref["d_b"], "d_b")
+
+
+def test_full_loss_config2_sampled():
+    """The full loss at c2 size (10.7 GiB workspace): sampled utterances against the oracle, and the
+    pruned loss bounded by it (L_pruned <= L_full: the band keeps a subset of the paths)."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    g = _run_full(b)
+    picks = _samples(b, 2)
+    ref = _oracle_full(b, picks)
+    for n in picks:
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        assert_loss(g["loss"][n:n + 1], [ref["loss"][n]], f"loss[{n}]")
+        assert_bf16_grad(g["d_enc"][n, :T], ref["d_enc"][n], f"d_enc[{n}]")
+        assert_bf16_grad(g["d_dec"][n, :U + 1], ref["d_dec"][n], f"d_dec[{n}]")
+    p = _run_step(b)
+    assert np.all(p["loss_pruned"] >= g["loss"] - 1e-3 * np.abs(g["loss"]))

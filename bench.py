@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--profile-kernel", default="auto")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches only (no CUDA graph replay)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic", "full"],
                     help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch); "
@@ -419,6 +420,44 @@ def main():
         pg.barrier()
     clk = clocks.stop()
     step_ms = [a.elapsed_time(c) for a, c in ev]
+    eager_ms = list(step_ms)
+
+    # The same step captured once as a CUDA graph (all streams: the side-stream branches become graph
+    # branches) and replayed: what a training loop on fixed-shape batches runs.  Same timing rules
+    # (events on the stream, L2 flushed between replays outside the events); N > 1 stays eager (the
+    # NCCL all-reduce is launched per step).
+    graph = None
+    graph_err = None
+    if not args.no_graph and pg is None:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                step(dev)
+            torch.cuda.current_stream().wait_stream(cs)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph):
+                step(dev)
+            torch.cuda.synchronize()
+            for _ in range(max(3, args.warmup)):
+                graph.replay()
+            torch.cuda.synchronize()
+            gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+            clocks = Clocks(local)
+            clocks.start()
+            time.sleep(0.3)
+            for i in range(K):
+                flush.zero_()
+                gev[i][0].record(stream)
+                graph.replay()
+                gev[i][1].record(stream)
+            torch.cuda.synchronize()
+            clk = clocks.stop()
+            step_ms = [a.elapsed_time(c) for a, c in gev]
+        except Exception as e:   # keep the eager numbers
+            graph, graph_err = None, f"{type(e).__name__}: {e}"[:200]
+            step_ms = eager_ms
     kern_ms = [a.elapsed_time(c) for a, c in kev]
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
     if pg is not None:
@@ -476,13 +515,17 @@ def main():
         d2h = loss_host.numel() * 4
 
         def e2e_step():
+            tgt = dev if graph is not None else dbuf       # the graph reads the static input buffers
             for k, v in host.items():
                 if k in ("w_out", "b_out"):
                     continue
-                dbuf[k].copy_(v, non_blocking=True)
-            dbuf["w_out"] = dev["w_out"]
-            dbuf["b_out"] = dev["b_out"]
-            step(dbuf)
+                tgt[k].copy_(v, non_blocking=True)
+            if graph is not None:
+                graph.replay()
+            else:
+                dbuf["w_out"] = dev["w_out"]
+                dbuf["b_out"] = dev["b_out"]
+                step(dbuf)
             loss_host[0].copy_(outs["loss_simple"], non_blocking=True)
             loss_host[1].copy_(outs["loss_pruned"], non_blocking=True)
         for _ in range(max(1, args.warmup)):
@@ -522,6 +565,8 @@ def main():
                 "kernels": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac", "kernel_ms", "share_of_step")}
                             for k, v in kernels.items()},
                 "gpu_launches": int(launches), "clocks": clk,
+                "execution": "cuda_graph" if graph is not None else "eager",
+                "eager_ms_per_step": statistics.mean(eager_ms), "graph_error": graph_err,
                 "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)}}
         print(json.dumps(line), flush=True)
     if pg is not None:

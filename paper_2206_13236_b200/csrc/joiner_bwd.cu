@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
         const int grows = (int)min((long long)BM, p.g.R - m0);
         const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + (uint32_t)grows * 16u;
+        constexpr int PF = 8;            // P~ boxes prefetched into L2 this many k-blocks ahead
+        for (int kb = 0; kb < min(PF, p.nkb); ++kb) tc::tma_prefetch_2d(&tmP, kb * BK, (int)m0);
         for (int kb = 0; kb < p.nkb; ++kb) {
+          if (kb + PF < p.nkb) tc::tma_prefetch_2d(&tmP, (kb + PF) * BK, (int)m0);
           tc::mbar_wait(&empty[stage], ph ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           dh_trace_kb(it, kb, 0);
@@ -711,7 +714,16 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes), B = h[rows, j0..] and the scalars
     int stage = 0;
     uint32_t ph = 0;
+    constexpr int PF = 6;                // P~ and h boxes prefetched into L2 this many k-blocks ahead
+    auto prefetch = [&](int kb) {
+      const int rb = (int)((kb0 + kb) * BK);
+      tc::tma_prefetch_2d(&tmP, v0, rb);
+      tc::tma_prefetch_2d(&tmP, v0 + 64, rb);
+      for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+    };
+    for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
     for (int kb = 0; kb < nkb; ++kb) {
+      if (kb + PF < nkb) prefetch(kb + PF);
       const long long rb = (kb0 + kb) * BK;
       const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
       const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;

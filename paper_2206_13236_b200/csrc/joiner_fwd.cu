@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
         ++qi;
         if (rt < 0) break;
         const int m0 = rt * BM;
+        // the h row tile comes from HBM once (then L2 for the other V tiles): prefetch its boxes
+        for (int kb = 0; kb < nkb; ++kb) tc::tma_prefetch_2d(&tmA, kb * BK, m0);
         for (int nt = 0; nt < nvt; ++nt) {
           for (int kb = 0; kb < nkb; ++kb) {
             tc::mbar_wait(&empty[stage], ph ^ 1);

@@ -585,12 +585,19 @@ __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restri
 // ======================================================================= K11
 namespace jdw {
 // 2 stages (~108 KB smem, TMEM 256 columns): two CTAs per SM keep four stages in flight per SM.
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 2;
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 (v) x 256 (j) dW tile: each CTA holds
+// its own 128 v of dz^T and HALF of the h columns (128 j), so the L2 -> SM bytes per flop of the h
+// operand halve; the rank-0 CTA issues the MMAs, both CTAs transform their own dz tile.
+constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;     // 16 KB, MN-major (2 TMA boxes of 64 v x 64 rows of P~)
-constexpr int B_BYTES = BN * BK * 2;     // 32 KB, MN-major (4 boxes of 64 j x 64 rows of h)
 constexpr int G_BYTES = BK * 16;         // 1 KB: the k-block rows' packed scalars for this V tile
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4;
+// B: 4 boxes of 64 j x 64 rows of h (32 KB); a pair CTA holds 2 (16 KB), which buys a third stage
+template <bool PAIR> struct Cfg {
+  static constexpr int STAGES = PAIR ? 3 : 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 128 * 16 * 4;
+};
 constexpr int THREADS = 160;
 }  // namespace jdw
 
@@ -602,10 +609,15 @@ struct JoinerDwParams {
   float* dbp;   // (splits, V)
 };
 
+
+template <bool PAIR>
 __global__ void __launch_bounds__(jdw::THREADS, 2)
     joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
                         JoinerDwParams p) {
   using namespace jdw;
+  constexpr int STAGES = Cfg<PAIR>::STAGES, B_BYTES = Cfg<PAIR>::B_BYTES, STAGE_BYTES = Cfg<PAIR>::STAGE_BYTES;
+  auto stage_of = [](int kb) { return kb % STAGES; };
+  auto phase_of = [](int kb) { return (uint32_t)((kb / STAGES) & 1); };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
   uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -615,19 +627,22 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][128 v]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
   const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
   const long long kb0 = (long long)split * p.kb_per_split;
   const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
   const int nkb = (int)max(0LL, kb1 - kb0);
   const int V = p.g.V;
   const int nj = min(BN, p.J - j0);
-  const int nbox = (nj + 63) / 64;
+  // h columns this CTA loads: all nj (single CTA) or its half of the pair's 256
+  const int jb = PAIR ? j0 + 128 * (int)rank : j0;
+  const int nbox = PAIR ? max(0, min(2, (p.J - jb + 63) / 64)) : (nj + 63) / 64;
   const int vtile = v0 >> 7;
 
   if (warp == 4 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
-      tc::mbar_init(&full[s], 4);
+      tc::mbar_init(&full[s], PAIR ? 8 : 4);     // transform warps of both CTAs (pair: arrive remotely)
       tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tfull, 1);
@@ -635,9 +650,13 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     tc::tma_prefetch(&tmP);
     tc::tma_prefetch(&tmH);
   }
-  if (warp == 4) tc::tmem_alloc(tmem_slot, 256);
+  if (warp == 4) {
+    if (PAIR) tc::tmem_alloc2(tmem_slot, 256);
+    else tc::tmem_alloc(tmem_slot, 256);
+  }
   tc::fence_before_sync();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();        // barrier inits visible to the peer before any remote arrive
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
 
@@ -647,6 +666,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     const int g8 = threadIdx.x >> 4;         // row group 0..7
     float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const bool want_db = blockIdx.y == 0;
+    const uint32_t full0 = PAIR ? tc::mapa(&full[0], 0) : 0;   // the leader's full[0] (cluster address)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
@@ -673,7 +693,10 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
       }
       tc::fence_proxy_async();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&full[stage]);
+      if (lane == 0) {
+        if (PAIR) tc::mbar_arrive_cluster(full0 + stage * 8);
+        else tc::mbar_arrive(&full[stage]);
+      }
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
     if (want_db) {
@@ -711,15 +734,13 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes), B = h[rows, j0..] and the scalars
-    int stage = 0;
-    uint32_t ph = 0;
+    // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes), B = h[rows, jb..] and the scalars
     constexpr int PF = 6;                // P~ and h boxes prefetched into L2 this many k-blocks ahead
     auto prefetch = [&](int kb) {
       const int rb = (int)((kb0 + kb) * BK);
       tc::tma_prefetch_2d(&tmP, v0, rb);
       tc::tma_prefetch_2d(&tmP, v0 + 64, rb);
-      for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+      for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, jb + bx * 64, rb);
     };
     for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
     for (int kb = 0; kb < nkb; ++kb) {
@@ -727,37 +748,46 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
       const long long rb = (kb0 + kb) * BK;
       const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
       const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;
-      tc::mbar_wait(&empty[stage], ph ^ 1);
-      uint8_t* sa = smem + stage * STAGE_BYTES;
-      tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
-      tc::tma_load_2d(sa, &tmP, &loaded[stage], v0, (int)rb);
-      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, &loaded[stage], v0 + 64, (int)rb);
+      tc::mbar_wait(&empty[stage_of(kb)], phase_of(kb) ^ 1);
+      uint8_t* sa = smem + stage_of(kb) * STAGE_BYTES;
+      uint64_t* ld = &loaded[stage_of(kb)];
+      tc::mbar_arrive_expect_tx(ld, bytes);
+      tc::tma_load_2d(sa, &tmP, ld, v0, (int)rb);
+      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, ld, v0 + 64, (int)rb);
       for (int bx = 0; bx < nbox; ++bx)
-        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, &loaded[stage], j0 + bx * 64, (int)rb);
-      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, &loaded[stage]);
-      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, ld, jb + bx * 64, (int)rb);
+      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
     }
-  } else if (lane == 1 && nkb > 0) {
-    // ---- warp 4 lane 1: MMA issuer
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+  } else if (lane == 1 && nkb > 0 && rank == 0) {
+    // ---- warp 4 lane 1 (pair: of the rank-0 CTA only): MMA issuer
+    constexpr uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(&full[stage], ph);
+      if (PAIR) tc::mbar_wait_cluster(&full[stage], ph);
+      else tc::mbar_wait(&full[stage], ph);
       tc::fence_after_sync();
       const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k)
-        tc::mma_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024),
-                     idesc, (kb | k) != 0);
-      tc::mma_commit(&empty[stage]);
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint64_t da = tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), db = tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024);
+        if (PAIR) tc::mma2_bf16(tbase, da, db, idesc, (kb | k) != 0);
+        else tc::mma_bf16(tbase, da, db, idesc, (kb | k) != 0);
+      }
+      if (PAIR) tc::mma2_commit(&empty[stage], 3);
+      else tc::mma_commit(&empty[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
-    tc::mma_commit(tfull);
+    if (PAIR) tc::mma2_commit(tfull, 3);
+    else tc::mma_commit(tfull);
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 4) tc::tmem_dealloc(tbase, 256);
+  if (PAIR) tc::cluster_sync();        // the peer's smem / TMEM stay alive until the pair is done
+  if (warp == 4) {
+    if (PAIR) tc::tmem_dealloc2(tbase, 256);
+    else tc::tmem_dealloc(tbase, 256);
+  }
 }
 
 // ======================================================================= host
@@ -818,16 +848,48 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   CUtensorMap tp, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(joiner_dw_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdw::SMEM_BYTES);
-    attr = true;
-  }
   const long long nkb = (d.rows() + jdw::BK - 1) / jdw::BK;
   const long long per = (nkb + splits - 1) / splits;
   JoinerDwParams p{g, d.J, per, nkb, dWp, dbp};
-  dim3 grid((d.V + jdw::BM - 1) / jdw::BM, (d.J + jdw::BN - 1) / jdw::BN, splits);
-  RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<<<grid, jdw::THREADS, jdw::SMEM_BYTES, st>>>(tp, th, p));
+  const int vt = (d.V + jdw::BM - 1) / jdw::BM;
+  // CTA pairs (cta_group::2, V tiles rounded up to an even count) only when RNNT_DW_PAIR=1: parity-green
+  // but measured slower (c2 87.6 vs 69.6 us, c4 4.42 vs 3.22 ms) -- the per-stage cross-CTA handshake
+  // (remote arrive + cluster-scope acquire) costs more than the halved h traffic saves at 2-3 stages
+  static int pair = -1;
+  if (pair < 0) {
+    const char* e = getenv("RNNT_DW_PAIR");
+    pair = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  if (pair) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(joiner_dw_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           jdw::Cfg<true>::SMEM_BYTES);
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((vt + 1) / 2 * 2), (d.J + jdw::BN - 1) / jdw::BN, splits);
+    cfg.blockDim = dim3(jdw::THREADS);
+    cfg.dynamicSmemBytes = jdw::Cfg<true>::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_tc_kernel<true>, tp, th, p));
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(joiner_dw_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           jdw::Cfg<false>::SMEM_BYTES);
+      attr = true;
+    }
+    dim3 grid(vt, (d.J + jdw::BN - 1) / jdw::BN, splits);
+    RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<false><<<grid, jdw::THREADS, jdw::Cfg<false>::SMEM_BYTES, st>>>(tp, th, p));
+  }
   return cudaGetLastError();
 }
 

@@ -46,10 +46,12 @@ _lib = None
 
 
 def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load the C-ABI library (raises if it is not built)."""
+    """Load the C-ABI library (raises if it is not built).  RNNT_LIB overrides the path (A/B
+    comparisons of two builds of the same library in tools/)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("RNNT_LIB", path)
     if not os.path.exists(path):
         raise RNNTError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)

@@ -81,7 +81,8 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 //               tile, the W boxes and the rows' packed scalars, into a 3-stage ring;
 //               lane 1: the epilogue's h boxes (64 columns x 128 rows) into a 2-slot ring
 //   warp 1      TMEM allocator (2 x 256 columns) and single-thread MMA issuer
-//   warps 2-5   in-place dz producers (thread = tile row), release each stage to the MMA
+//   warps 2..   in-place dz producers (4 or 8 warps: a thread per row or half row), release each
+//               stage to the MMA
 //   warps 6-13  epilogue, two groups of four (one per TMEM lane quadrant), alternate 32-column
 //               chunks; the accumulator of item k+1 fills while item k drains.
 struct DhTab {
@@ -106,7 +107,12 @@ constexpr int H_OFF = STAGES * STAGE_BYTES + 2 * D_BYTES;
 constexpr int TAB_OFF = H_OFF + 2 * H_BYTES;
 constexpr int BAR_OFF = TAB_OFF + NTAB * TAB_BYTES;
 constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
-constexpr int THREADS = 14 * 32;
+// in-place dz producer warps: 4 (a thread per row) for short V loops, 8 (a thread per half row) when
+// the mainloop is long (measured: c2 108 vs 145 us, c4 2.95 vs 2.61 ms)
+template <int NTW> struct Roles {
+  static constexpr int EPI0 = 2 + NTW;          // first epilogue warp
+  static constexpr int THREADS = (EPI0 + 8) * 32;
+};
 }  // namespace jdh
 
 struct JoinerDhParams {
@@ -232,10 +238,12 @@ __device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
   if (g_dh_trace && it < 3 && kb < 8) g_dh_trace[148 * 16 * 5 + (((size_t)blockIdx.x * 3 + it) * 8 + kb) * 4 + k] = gtimer();
 }
 
-__global__ void __launch_bounds__(jdh::THREADS, 1)
+template <int NTW>
+__global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
   using namespace jdh;
+  constexpr int EPI0 = Roles<NTW>::EPI0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
   uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
-      tc::mbar_init(&full[s], 4);
+      tc::mbar_init(&full[s], NTW);
       tc::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -360,9 +368,11 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
         dh_trace(it, 2);
       }
     }
-  } else if (warp < 6) {
-    // ---- in-place dz producers: thread = tile row; transform the 8 chunks of its row
-    const int rl = threadIdx.x - 64;
+  } else if (warp < EPI0) {
+    // ---- in-place dz producers: thread = (tile row, half): transforms 4 of the 8 chunks of its row
+    constexpr int CPT = 8 * 4 / NTW;                 // chunks per thread: 8 (4 warps) or 4 (8 warps)
+    const int pt = threadIdx.x - 64;
+    const int rl = pt & 127, c_lo = (pt >> 7) * CPT;
     int stage = 0, itx = 0;
     uint32_t ph = 0;
     for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++itx) {
@@ -372,31 +382,31 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int v0 = kb * BK;
         tc::mbar_wait(&loaded[stage], ph);
-        if (rl == 0) dh_trace_kb(itx, kb, 1);
+        if (pt == 0) dh_trace_kb(itx, kb, 1);
         uint8_t* sa = smem + stage * STAGE_BYTES;
         const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
                                                   : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
         const int info = __float_as_int(gq.w);
-        uint4 pv[8];
+        uint4 pv[CPT];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) pv[c] = *reinterpret_cast<const uint4*>(sa + sw128(rl, c));
+        for (int c = 0; c < CPT; ++c) pv[c] = *reinterpret_cast<const uint4*>(sa + sw128(rl, c_lo + c));
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(sa + sw128(rl, c)) =
-              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + c * 8, nullptr) : make_uint4(0, 0, 0, 0);
+        for (int c = 0; c < CPT; ++c)
+          *reinterpret_cast<uint4*>(sa + sw128(rl, c_lo + c)) =
+              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + (c_lo + c) * 8, nullptr) : make_uint4(0, 0, 0, 0);
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&full[stage]);
-        if (rl == 0) dh_trace_kb(itx, kb, 2);
+        if (pt == 0) dh_trace_kb(itx, kb, 2);
         if (++stage == STAGES) { stage = 0; ph ^= 1; }
       }
     }
   } else {
-    // ---- epilogue: group g (warps 6-9 / 10-13) takes the 32-column chunks c0 = 32 (2i + g);
+    // ---- epilogue: group g (the 8 warps after the producers, 4 per group) takes the 32-column chunks c0 = 32 (2i + g);
     // quadrant q = warp % 4 owns TMEM lanes (tile rows) 32q..32q+31
-    const int q4 = warp & 3, g = (warp - 6) >> 2;
+    const int q4 = warp & 3, g = (warp - EPI0) >> 2;
     const int rl = 32 * q4 + lane;                      // tile row of this thread
-    const int gt = threadIdx.x - 192 - 128 * g;          // 0..127 within the group
+    const int gt = threadIdx.x - 32 * EPI0 - 128 * g;     // 0..127 within the group
     float4* D4 = reinterpret_cast<float4*>(dstage + g * D_BYTES);
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
     int it = 0, hslot = 0;
@@ -413,12 +423,12 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       if (!generic) tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
-      if (warp == 6 && lane == 0) dh_trace(it, 3);
+      if (warp == EPI0 && lane == 0) dh_trace(it, 3);
       const int nent = generic ? 0 : tb->nent;
       for (int bx = 0; bx < nbox; ++bx) {
         const int c0 = 64 * bx + 32 * g;
         tc::mbar_wait(&hfull[hslot], hph);
-        const bool trc = warp == 6 && lane == 0;
+        const bool trc = warp == EPI0 && lane == 0;
         if (trc) dh_trace_ep(it, bx, 0);
         const bool have = c0 < nj;
         float accv[32];
@@ -517,7 +527,7 @@ __global__ void __launch_bounds__(jdh::THREADS, 1)
       }
       __syncwarp();
       if (lane == 0 && !generic) tc::mbar_arrive(&tabempty[slot]);
-      if (warp == 6 && lane == 0) dh_trace(it, 4);
+      if (warp == EPI0 && lane == 0) dh_trace(it, 4);
     }
   }
   tc::fence_before_sync();
@@ -800,7 +810,8 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+    cudaFuncSetAttribute(joiner_dh_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+    cudaFuncSetAttribute(joiner_dh_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
     attr = true;
   }
   const int F = d.dh_frames();
@@ -815,7 +826,10 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  if (p.nkb >= 32)
+    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  else
+    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<4><<<grid, jdh::Roles<4>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   if (d_dec)
     RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(
         ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, part, d_dec));
@@ -832,14 +846,18 @@ cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(joiner_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+  cudaFuncSetAttribute(joiner_dh_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+  cudaFuncSetAttribute(joiner_dh_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
                    nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out};
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<<<grid, jdh::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  if (p.nkb >= 32)
+    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  else
+    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<4><<<grid, jdh::Roles<4>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   return cudaGetLastError();
 }
 

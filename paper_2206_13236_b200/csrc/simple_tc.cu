@@ -532,30 +532,36 @@ struct NormProb {
           ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
         }
       }
+      // branch-free per cell: every cell is computed (invalid ones from S = 1) and selected; the
+      // smoothing term (a warp-uniform switch) is applied in a second, separate loop
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int u = u0 + j;
-        float px = kNegBig, py = kNegBig, r = 0.f;
-        if (rowok && u <= Un) {
-          const float S = acc[j];
-          under |= !(S > 0.f);
-          // base-2 throughout: Lnorm2 = log2 S + (m_am + m_lm) log2e = L_normalizer(t,u) log2e, Eq. 6
-          const float Ln2 = lg2_approx(S) + (mam + mlm[c0 + j]) * RNNT_LOG2E_F;
-          if (u < Un) px = fmaf(ay[j] + lmy[c0 + j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
-          // empty(t,u), Eq. 2 + 5; out of the last frame only the terminal blank exists
-          if (!(trow == Tn - 1 && u < Un)) py = fmaf(am0 + lm0[c0 + j], RNNT_LOG2E_F, -Ln2);
-          if (smooth) {
-            // Eq. 11: w0 L_trivial + a_lm L_lm (Eq. 14) + a_ac L_acoustic (Eq. 13)
-            if (u < Un)
-              px = fmaf(w0, px, RNNT_LOG2E_F * (sm.a_lm * (lmy[c0 + j] - lz[c0 + j]) +
-                                                sm.a_ac * (ay[j] + lyv[c0 + j] - lac)));
-            if (py > -1e29f)
-              py = fmaf(w0, py, RNNT_LOG2E_F * (sm.a_lm * (lm0[c0 + j] - lz[c0 + j]) + sm.a_ac * (am0 + L0 - lac)));
-          }
-          r = rcp_approx(S);
-        }
+        const bool valid = rowok && u <= Un;
+        const float S = valid ? acc[j] : 1.f;
+        under |= !(S > 0.f);
+        // base-2 throughout: Lnorm2 = log2 S + (m_am + m_lm) log2e = L_normalizer(t,u) log2e, Eq. 6
+        const float Ln2 = lg2_approx(S) + (mam + mlm[c0 + j]) * RNNT_LOG2E_F;
+        const float px0 = fmaf(ay[j] + lmy[c0 + j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
+        const float py0 = fmaf(am0 + lm0[c0 + j], RNNT_LOG2E_F, -Ln2);     // empty(t,u) log2e, Eq. 2 + 5
+        // y only below U_n; out of the last frame only the terminal blank exists
+        const float px = (valid && u < Un) ? px0 : kNegBig;
+        const float py = (valid && !(trow == Tn - 1 && u < Un)) ? py0 : kNegBig;
         bxy[e.lane][j] = make_float2(px, py);
-        brs[e.lane][j] = r;
+        brs[e.lane][j] = valid ? rcp_approx(S) : 0.f;
+      }
+      if (smooth) {
+        // Eq. 11: w0 L_trivial + a_lm L_lm (Eq. 14) + a_ac L_acoustic (Eq. 13)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float2 xy = bxy[e.lane][j];
+          if (xy.x > -1e29f)
+            xy.x = fmaf(w0, xy.x, RNNT_LOG2E_F * (sm.a_lm * (lmy[c0 + j] - lz[c0 + j]) +
+                                                  sm.a_ac * (ay[j] + lyv[c0 + j] - lac)));
+          if (xy.y > -1e29f)
+            xy.y = fmaf(w0, xy.y, RNNT_LOG2E_F * (sm.a_lm * (lm0[c0 + j] - lz[c0 + j]) + sm.a_ac * (am0 + L0 - lac)));
+          bxy[e.lane][j] = xy;
+        }
       }
       __syncwarp();
       // diagonal-major write of the arcs and of 1/S: for diagonal k = t0w + u0 + d, lane l holds

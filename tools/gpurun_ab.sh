@@ -2,7 +2,7 @@
 k=$1; shift
 for c in "$@"; do
   for rep in 1 2; do
-    echo "new $(python tools/fwd_modes.py $c $k)"
-    echo "old $(RNNT_LIB=build_ab/librnnt_old.so python tools/fwd_modes.py $c $k)"
+    echo "new $(python tools/kernel_time.py $c $k)"
+    echo "old $(RNNT_LIB=build_ab/librnnt_old.so python tools/kernel_time.py $c $k)"
   done
 done

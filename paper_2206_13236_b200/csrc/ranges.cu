@@ -14,9 +14,13 @@
 
 namespace rnnt {
 
-__global__ void raw_bounds_kernel(const float* __restrict__ px_grad, const float* __restrict__ py_grad,
-                                  const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                  int32_t* __restrict__ raw) {
+__global__ void __launch_bounds__(256) raw_bounds_kernel(const float* __restrict__ px_grad,
+                                                         const float* __restrict__ py_grad,
+                                                         const int64_t* __restrict__ bnd, int N, int T, int U, int S,
+                                                         int32_t* __restrict__ raw) {
+  // the warp's frame row (y' and empty', U_n + 1 values each) is staged in smem with all loads in
+  // flight at once; the fp64 window sums then read smem only
+  extern __shared__ float rowbuf[];   // [8 warps][2][U + 1]
   long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * T) return;
@@ -24,15 +28,19 @@ __global__ void raw_bounds_kernel(const float* __restrict__ px_grad, const float
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   if (t >= Tn) return;
   const int Umax = max(0, Un - S + 1);
+  float* yb = rowbuf + (threadIdx.x / 32) * 2 * (U + 1);
+  float* bb = yb + (U + 1);
   const float* yr = px_grad + row * (long long)(U + 1);
   const float* br = py_grad + row * (long long)(U + 1);
+  for (int u = lane; u <= Un; u += 32) { yb[u] = yr[u]; bb[u] = br[u]; }
+  __syncwarp();
   double best = -1e300;
   int bestp = 0x7fffffff;
   for (int p = lane; p <= Umax; p += 32) {
     double acc = 0.0;
     const int hi = min(p + S, Un + 1);
-    for (int u = p; u < hi; ++u) acc = __dadd_rn(acc, (double)br[u]);
-    if (p > 0) acc = __dsub_rn(acc, (double)yr[p - 1]);
+    for (int u = p; u < hi; ++u) acc = __dadd_rn(acc, (double)bb[u]);
+    if (p > 0) acc = __dsub_rn(acc, (double)yb[p - 1]);
     if (acc > best || (acc == best && p < bestp)) { best = acc; bestp = p; }
   }
 #pragma unroll
@@ -42,6 +50,35 @@ __global__ void raw_bounds_kernel(const float* __restrict__ px_grad, const float
     if (ob > best || (ob == best && op < bestp)) { best = ob; bestp = op; }
   }
   if (lane == 0) raw[row] = bestp;
+}
+
+// Inclusive max-scan over the 1024 threads of the block (reverse: over tid descending): a warp
+// scan by shuffles, the 32 warp totals scanned by warp 0 through smem, then combined.
+__device__ __forceinline__ int block_scan_max(int x, int* sh, bool reverse) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NEG = INT_MIN;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = reverse ? __shfl_down_sync(0xffffffffu, x, o) : __shfl_up_sync(0xffffffffu, x, o);
+    if (reverse ? (lane + o < 32) : (lane >= o)) x = max(x, y);
+  }
+  __syncthreads();                                   // sh free (previous use complete)
+  if (lane == (reverse ? 0 : 31)) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int v = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = reverse ? __shfl_down_sync(0xffffffffu, v, o) : __shfl_up_sync(0xffffffffu, v, o);
+      if (reverse ? (lane + o < 32) : (lane >= o)) v = max(v, y);
+    }
+    sh[lane] = v;                                     // inclusive over warps
+  }
+  __syncthreads();
+  // combine with the warps before (after, reversed)
+  int prev = NEG;
+  if (reverse ? (warp < 31) : (warp > 0)) prev = sh[reverse ? warp + 1 : warp - 1];
+  return max(x, prev);
 }
 
 // One CTA (1024 threads) per utterance; frames processed in chunks of blockDim.x with a
@@ -77,18 +114,11 @@ __global__ void __launch_bounds__(1024) adjust_kernel(const int32_t* raw, const 
       r = r < lo ? lo : (r > hi ? hi : r);
       x = (int)r;
     }
-    sh[tid] = x;
-    __syncthreads();
-    for (int o = 1; o < nt; o <<= 1) {   // inclusive max-scan
-      int y = tid >= o ? sh[tid - o] : 0;
-      __syncthreads();
-      sh[tid] = max(sh[tid], y);
-      __syncthreads();
-    }
+    const int incl = block_scan_max(x, sh, false);
     const int c = carry;
-    if (t < Tn) qq[t] = max(sh[tid], c);
+    if (t < Tn) qq[t] = max(incl, c);
     __syncthreads();
-    if (tid == nt - 1) carry = max(c, sh[nt - 1]);
+    if (tid == nt - 1) carry = max(c, incl);
     __syncthreads();
   }
   // 3: p_t = max_{t'>=t} (q_t' - t'(S-1)) + t(S-1)   (Eq. 10)
@@ -100,18 +130,11 @@ __global__ void __launch_bounds__(1024) adjust_kernel(const int32_t* raw, const 
     int g = INT_MIN;
     if (t < Tn) g = qq[t] - t * (S - 1);
     // reverse inclusive max-scan within the chunk
-    sh[tid] = g;
-    __syncthreads();
-    for (int o = 1; o < nt; o <<= 1) {
-      int y = (tid + o < nt) ? sh[tid + o] : INT_MIN;
-      __syncthreads();
-      sh[tid] = max(sh[tid], y);
-      __syncthreads();
-    }
+    const int rincl = block_scan_max(g, sh, true);
     const int c = carry;
-    if (t < Tn) out[t] = max(sh[tid], c) + t * (S - 1);
+    if (t < Tn) out[t] = max(rincl, c) + t * (S - 1);
     __syncthreads();
-    if (tid == 0) carry = max(c, sh[0]);
+    if (tid == 0) carry = max(c, rincl);
     __syncthreads();
   }
   for (int t = Tn + tid; t < T; t += nt) out[t] = Umax;   // padded frames (D11)
@@ -121,8 +144,10 @@ cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* 
                               int32_t* ranges, int32_t* status, cudaStream_t st) {
   // raw bounds and the monotone hull q are staged in the output buffer itself (no workspace).
   long long rows = (long long)d.N * d.T;
-  RNNT_LAUNCH(KID_RAW, st, raw_bounds_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(px_grad, py_grad, bnd, d.N, d.T, d.U,
-                                                                 d.S, ranges));
+  const size_t sm = (size_t)8 * 2 * d.U1() * sizeof(float);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(raw_bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  RNNT_LAUNCH(KID_RAW, st, raw_bounds_kernel<<<(unsigned)((rows + 7) / 8), 256, sm, st>>>(px_grad, py_grad, bnd, d.N, d.T,
+                                                                                         d.U, d.S, ranges));
   RNNT_LAUNCH(KID_ADJUST, st, adjust_kernel<<<d.N, 1024, 0, st>>>(ranges, bnd, d.T, d.S, ranges, ranges, status));
   return cudaGetLastError();
 }

@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches only (no CUDA graph replay)")
+    ap.add_argument("--no-priority", action="store_true", help="run the step on the default-priority stream")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic", "full"],
                     help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch); "
@@ -374,7 +375,9 @@ def main():
     outs["d_w"], outs["d_b"] = gbuf.d_w, gbuf.d_b
     ws = torch.empty(R.rnnt_workspace_bytes(dims), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-    stream = torch.cuda.current_stream()
+    # the step runs on a high-priority stream (its side streams are lowest priority)
+    stream = R.critical_stream() if not args.no_priority else torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     def step(inp):
         outs["status"].zero_()
@@ -437,7 +440,7 @@ def main():
                 step(dev)
             torch.cuda.current_stream().wait_stream(cs)
             torch.cuda.synchronize()
-            with torch.cuda.graph(graph):
+            with torch.cuda.graph(graph, stream=stream):
                 step(dev)
             torch.cuda.synchronize()
             for _ in range(max(3, args.warmup)):
@@ -541,7 +544,7 @@ def main():
                     step(bufs[1])
                 torch.cuda.current_stream().wait_stream(cs)
                 torch.cuda.synchronize()
-                with torch.cuda.graph(g1):
+                with torch.cuda.graph(g1, stream=stream):
                     step(bufs[1])
                 torch.cuda.synchronize()
                 graphs[1] = g1

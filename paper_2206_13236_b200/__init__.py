@@ -308,8 +308,23 @@ _SIDE = {}
 def _side_stream(device, which=0):
     key = (torch.device(device).index, which)
     if key not in _SIDE:
-        _SIDE[key] = torch.cuda.Stream(device=device)
+        _SIDE[key] = torch.cuda.Stream(device=device, priority=0)      # lowest priority: fills gaps
     return _SIDE[key]
+
+
+_CRIT = {}
+
+
+def critical_stream(device=None):
+    """A high-priority stream for the step's critical path: with the side streams at the lowest
+    priority the block scheduler hands idle SMs (e.g. during the latency-bound recursions) to the
+    side-stream GEMMs without delaying the critical-path kernels."""
+    idx = torch.device(device if device is not None else "cuda").index
+    idx = torch.cuda.current_device() if idx is None else idx
+    if idx not in _CRIT:
+        lo, hi = torch.cuda.Stream.priority_range()
+        _CRIT[idx] = torch.cuda.Stream(device=idx, priority=hi)
+    return _CRIT[idx]
 
 
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,

@@ -800,6 +800,191 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
   }
 }
 
+// K11, wide variant (large V): one CTA per SM computes a 256 (v) x 256 (j) partial dW tile as two
+// 128 x 256 accumulators (TMEM columns 0..255 and 256..511) that share every h k-block, so the L2 -> SM
+// bytes per MMA flop drop from 49 KB to 33 KB per 128x256x64 step (the h operand is read once per
+// V-tile PAIR instead of per V tile).  Warps 0-7 transform dz (warps 0-3 tile 0, 4-7 tile 1) and run
+// the epilogue; warp 8 lane 0 issues TMA, lane 1 the MMAs.
+namespace jdw2 {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 3;
+constexpr int A_BYTES = BM * BK * 2;                     // per V tile (2 boxes of 64 v x 64 rows)
+constexpr int B_BYTES = BN * BK * 2;                     // 4 boxes of 64 j x 64 rows of h
+constexpr int G_BYTES = BK * 16;
+constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES + 2 * G_BYTES;   // 66 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 256 * 4;
+constexpr int THREADS = 288;
+}  // namespace jdw2
+
+__global__ void __launch_bounds__(jdw2::THREADS, 1)
+    joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
+                          JoinerDwParams p) {
+  using namespace jdw2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = tc::align1024(smem_raw);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = loaded + STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][256 v]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v0 = blockIdx.x * 2 * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
+  const long long kb0 = (long long)split * p.kb_per_split;
+  const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
+  const int nkb = (int)max(0LL, kb1 - kb0);
+  const int V = p.g.V;
+  const bool two = v0 + BM < V;          // the second V tile exists
+  const int nj = min(BN, p.J - j0);
+  const int nbox = (nj + 63) / 64;
+  const int vtile = v0 >> 7;
+
+  if (warp == 8 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&loaded[s], 1);
+      tc::mbar_init(&full[s], 8);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmP);
+    tc::tma_prefetch(&tmH);
+  }
+  if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp < 8) {
+    const int a = warp >> 2;                 // V tile 0 / 1 of the pair
+    const int t = threadIdx.x & 127;
+    const int c = t & 15;                    // 8-v chunk 0..15
+    const int g8 = t >> 4;                   // row group 0..7
+    const bool mine = a == 0 || two;
+    float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const bool want_db = blockIdx.y == 0;
+    const int va = v0 + a * BM;
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const long long rb = (kb0 + kb) * BK;
+      const int grows = (int)min((long long)BK, p.g.R - rb);
+      tc::mbar_wait(&loaded[stage], ph);
+      if (mine) {
+        uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
+        const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
+        uint4 pv[8];
+        float4 sr[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = g8 + 8 * i;
+          sr[i] = rl < grows ? gq[rl] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+          pv[i] = *reinterpret_cast<const uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = g8 + 8 * i;
+          const int info = __float_as_int(sr[i].w);
+          *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) =
+              info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, va + c * 8, want_db ? dsum : nullptr)
+                        : make_uint4(0, 0, 0, 0);
+        }
+        tc::fence_proxy_async();
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&full[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+    if (want_db) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dbs[g8 * 256 + a * 128 + c * 8 + j] = dsum[j];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int v = threadIdx.x;   // 0..255
+      float s = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg) s += dbs[gg * 256 + v];
+      if (v0 + v < V) p.dbp[(size_t)split * V + v0 + v] = s;
+    }
+    // ---- epilogue: accumulator a -> dWp[split] rows va + t
+    if (nkb > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    const int v = va + t;
+    const uint32_t tl = tbase + (uint32_t)(a * 256) + ((uint32_t)(32 * (warp & 3)) << 16);
+    for (int c0 = 0; c0 < nj; c0 += 32) {
+      float acc[32];
+      if (nkb > 0) {
+        tc::tmem_ld32(tl + c0, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+      }
+      if (v < V) {
+        float4* o = reinterpret_cast<float4*>(p.dWp + ((size_t)split * V + v) * p.J + j0 + c0);
+        const int n4 = min(8, (nj - c0) / 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < n4) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      }
+    }
+  } else if (lane == 0 && nkb > 0) {
+    // ---- warp 8 lane 0: TMA for both P~ tiles, the h k-block and the two tiles' row scalars
+    constexpr int PF = 6;
+    auto prefetch = [&](int kb) {
+      const int rb = (int)((kb0 + kb) * BK);
+      for (int bx = 0; bx < (two ? 4 : 2); ++bx) tc::tma_prefetch_2d(&tmP, v0 + 64 * bx, rb);
+      for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+    };
+    for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (kb + PF < nkb) prefetch(kb + PF);
+      const long long rb = (kb0 + kb) * BK;
+      const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
+      const uint32_t bytes = (two ? 2 : 1) * (A_BYTES + gbytes) + (uint32_t)nbox * 64 * BK * 2;
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+      uint64_t* ld = &loaded[stage];
+      tc::mbar_arrive_expect_tx(ld, bytes);
+      tc::tma_load_2d(sa, &tmP, ld, v0, (int)rb);
+      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, ld, v0 + 64, (int)rb);
+      if (two) {
+        tc::tma_load_2d(sa + A_BYTES, &tmP, ld, v0 + 128, (int)rb);
+        tc::tma_load_2d(sa + A_BYTES + 64 * BK * 2, &tmP, ld, v0 + 192, (int)rb);
+      }
+      for (int bx = 0; bx < nbox; ++bx)
+        tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), &tmH, ld, j0 + bx * 64, (int)rb);
+      tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
+      if (two) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (lane == 1 && nkb > 0) {
+    // ---- warp 8 lane 1: two 128x256x16 MMAs per k-step, one per V tile, sharing the h descriptor
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, true, true);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait(&full[stage], ph);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + 2 * A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint64_t db = tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024);
+        tc::mma_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
+        if (two) tc::mma_bf16(tbase + 256, tc::sdesc(a + A_BYTES + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
+      }
+      tc::mma_commit(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+    tc::mma_commit(tfull);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 8) tc::tmem_dealloc(tbase, 512);
+}
+
 // ======================================================================= host
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
                              const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
@@ -878,7 +1063,15 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     const char* e = getenv("RNNT_DW_PAIR");
     pair = (e && atoi(e) == 1) ? 1 : 0;
   }
-  if (pair) {
+  if (dw_wide(d)) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(joiner_dw_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdw2::SMEM_BYTES);
+      attr = true;
+    }
+    dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
+    RNNT_LAUNCH(KID_DW, st, joiner_dw_wide_kernel<<<grid, jdw2::THREADS, jdw2::SMEM_BYTES, st>>>(tp, th, p));
+  } else if (pair) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(joiner_dw_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
+#include <algorithm>
 
 namespace rnnt {
 
@@ -108,10 +110,36 @@ struct PrunedWS {
   int splits;
 };
 
+// K11 variant: "wide" CTAs (one per SM) hold two V tiles (256 v x 256 j, 512 TMEM columns) so each
+// h k-block feeds two MMAs; used for large V (L2 -> SM bound), RNNT_DW_WIDE=0/1 forces it off/on.
+inline bool dw_wide(const Dims& d) {
+  static int force = -2;
+  if (force == -2) {
+    const char* e = getenv("RNNT_DW_WIDE");
+    force = e ? atoi(e) : -1;
+  }
+  if (force >= 0) return force == 1;
+  return d.V >= 1024;
+}
+
 // Split-K factor of the d_w GEMM (K11): about two CTAs per SM over the (V/128) x (J/256)
 // output tiles, at least 4 K-blocks of 64 rows per split.
 inline int dw_splits(const Dims& d) {
   const long long nkb = (d.rows() + 63) / 64;
+  if (dw_wide(d)) {
+    // one CTA per SM: the smallest split count whose grid fills whole waves to >= 90 %
+    const long long tiles = (long long)((d.ntile() + 1) / 2) * ((d.J + 255) / 256);
+    const long long cap = std::max(1LL, std::min(64LL, nkb / 4));
+    long long best = 1;
+    double beff = 0.0;
+    for (long long s = 1; s <= cap; ++s) {
+      const long long c = tiles * s;
+      const double eff = (double)c / (148.0 * (double)((c + 147) / 148));
+      if (c >= 148 && eff >= 0.9) return (int)s;
+      if (eff > beff + 1e-9) { beff = eff; best = s; }
+    }
+    return (int)best;
+  }
   const long long tiles = (long long)((d.V + 127) / 128) * ((d.J + 255) / 256);
   long long s = (2 * 148 + tiles - 1) / tiles;
   const long long cap = nkb / 4 > 1 ? nkb / 4 : 1;

@@ -129,6 +129,7 @@ struct JoinerDhParams {
   int dbg;                 // diagnostics (RNNT_DBG_DH): bit0 skip d_dec, bit1 skip d_enc, bit2 skip staging
   int rt;                  // rows per tile (F*S frame-aligned; 128 in the generic mode)
   float* dpre_out;         // generic mode (full lattice): dpre = dh (1-h^2) rows to global, no tables
+  int w3 = 0;              // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
 };
 
 // One CTA of 128 threads per frame-aligned tile: the tile table, the live-tile list, and zeros of
@@ -307,7 +308,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const long long m0 = (long long)tile * RT;
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
         const int grows = (int)min((long long)BM, p.g.R - m0);
-        const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + (uint32_t)grows * 16u;
+        // (3-D W box: planes past J arrive zero-filled and count in full)
+        const uint32_t bytes = A_BYTES + (p.w3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + (uint32_t)grows * 16u;
         constexpr int PF = 8;            // P~ boxes prefetched into L2 this many k-blocks ahead
         for (int kb = 0; kb < min(PF, p.nkb); ++kb) tc::tma_prefetch_2d(&tmP, kb * BK, (int)m0);
         for (int kb = 0; kb < p.nkb; ++kb) {
@@ -317,8 +319,12 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           dh_trace_kb(it, kb, 0);
           tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
           tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
-          for (int bx = 0; bx < nbox; ++bx)
-            tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
+          if (p.w3) {
+            tc::tma_load_3d(sa + A_BYTES, &tmW, &loaded[stage], 0, kb * BK, j0 / 64);
+          } else {
+            for (int bx = 0; bx < nbox; ++bx)
+              tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
+          }
           tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0,
                         (uint32_t)grows * 16u, &loaded[stage]);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
@@ -617,6 +623,8 @@ struct JoinerDwParams {
   long long kb_per_split, nkb_total;
   float* dWp;   // (splits, V, J)
   float* dbp;   // (splits, V)
+  int pf = 6, pfmode = 1;   // wide variant: L2 prefetch distance (k-blocks); bit 0: P~ prefetched by j-tile 0 only, h by V pair 0 only; bit 1: grid x = j tile
+  int h3 = 0;               // wide variant: tmH is the 3-D (64 j, rows, J/64) map (J % 64 == 0)
 };
 
 
@@ -746,8 +754,14 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
   } else if (lane == 0 && nkb > 0) {
     // ---- warp 4 lane 0: TMA for A = P~[rows, v0..v0+127] (2 boxes), B = h[rows, jb..] and the scalars
     constexpr int PF = 6;                // P~ and h boxes prefetched into L2 this many k-blocks ahead
+    const bool t3 = !PAIR && p.h3;       // 3-D maps: one TMA for the 2 P~ boxes, one for the 4 h boxes
     auto prefetch = [&](int kb) {
       const int rb = (int)((kb0 + kb) * BK);
+      if (t3) {
+        tc::tma_prefetch_3d(&tmP, 0, rb, v0 / 64);
+        tc::tma_prefetch_3d(&tmH, 0, rb, jb / 64);
+        return;
+      }
       tc::tma_prefetch_2d(&tmP, v0, rb);
       tc::tma_prefetch_2d(&tmP, v0 + 64, rb);
       for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, jb + bx * 64, rb);
@@ -757,15 +771,20 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
       if (kb + PF < nkb) prefetch(kb + PF);
       const long long rb = (kb0 + kb) * BK;
       const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
-      const uint32_t bytes = A_BYTES + (uint32_t)nbox * 64 * BK * 2 + gbytes;
+      const uint32_t bytes = A_BYTES + (t3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + gbytes;
       tc::mbar_wait(&empty[stage_of(kb)], phase_of(kb) ^ 1);
       uint8_t* sa = smem + stage_of(kb) * STAGE_BYTES;
       uint64_t* ld = &loaded[stage_of(kb)];
       tc::mbar_arrive_expect_tx(ld, bytes);
-      tc::tma_load_2d(sa, &tmP, ld, v0, (int)rb);
-      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, ld, v0 + 64, (int)rb);
-      for (int bx = 0; bx < nbox; ++bx)
-        tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, ld, jb + bx * 64, (int)rb);
+      if (t3) {
+        tc::tma_load_3d(sa, &tmP, ld, 0, (int)rb, v0 / 64);
+        tc::tma_load_3d(sa + A_BYTES, &tmH, ld, 0, (int)rb, jb / 64);
+      } else {
+        tc::tma_load_2d(sa, &tmP, ld, v0, (int)rb);
+        tc::tma_load_2d(sa + 64 * BK * 2, &tmP, ld, v0 + 64, (int)rb);
+        for (int bx = 0; bx < nbox; ++bx)
+          tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, ld, jb + bx * 64, (int)rb);
+      }
       tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
     }
   } else if (lane == 1 && nkb > 0 && rank == 0) {
@@ -828,7 +847,9 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][256 v]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int v0 = blockIdx.x * 2 * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
+  const bool jfirst = p.pfmode & 2;      // grid x = j tile (siblings sharing P~ adjacent)
+  const int bvx = jfirst ? blockIdx.y : blockIdx.x, bjy = jfirst ? blockIdx.x : blockIdx.y;
+  const int v0 = bvx * 2 * BM, j0 = bjy * BN, split = blockIdx.z;
   const long long kb0 = (long long)split * p.kb_per_split;
   const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
   const int nkb = (int)max(0LL, kb1 - kb0);
@@ -862,7 +883,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     const int g8 = t >> 4;                   // row group 0..7
     const bool mine = a == 0 || two;
     float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const bool want_db = blockIdx.y == 0;
+    const bool want_db = bjy == 0;
     const int va = v0 + a * BM;
     int stage = 0;
     uint32_t ph = 0;
@@ -930,11 +951,16 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     }
   } else if (lane == 0 && nkb > 0) {
     // ---- warp 8 lane 0: TMA for both P~ tiles, the h k-block and the two tiles' row scalars
-    constexpr int PF = 6;
+    const int PF = p.pf;
+    const bool pfP = !(p.pfmode & 1) || bjy == 0, pfH = !(p.pfmode & 1) || bvx == 0;
     auto prefetch = [&](int kb) {
       const int rb = (int)((kb0 + kb) * BK);
-      for (int bx = 0; bx < (two ? 4 : 2); ++bx) tc::tma_prefetch_2d(&tmP, v0 + 64 * bx, rb);
-      for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+      if (pfP) tc::tma_prefetch_3d(&tmP, 0, rb, v0 / 64);
+      if (pfH) {
+        if (p.h3) tc::tma_prefetch_3d(&tmH, 0, rb, j0 / 64);
+        else
+          for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+      }
     };
     for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
     int stage = 0;
@@ -943,19 +969,18 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       if (kb + PF < nkb) prefetch(kb + PF);
       const long long rb = (kb0 + kb) * BK;
       const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
-      const uint32_t bytes = (two ? 2 : 1) * (A_BYTES + gbytes) + (uint32_t)nbox * 64 * BK * 2;
+      // 3-D boxes: out-of-range planes (the missing second V tile, j past J) arrive zero-filled and
+      // count in full toward the transaction bytes
+      const uint32_t bytes = 2 * A_BYTES + (two ? 2 : 1) * gbytes + (p.h3 ? B_BYTES : (uint32_t)nbox * 64 * BK * 2);
       tc::mbar_wait(&empty[stage], ph ^ 1);
       uint8_t* sa = smem + stage * STAGE_BYTES;
       uint64_t* ld = &loaded[stage];
       tc::mbar_arrive_expect_tx(ld, bytes);
-      tc::tma_load_2d(sa, &tmP, ld, v0, (int)rb);
-      tc::tma_load_2d(sa + 64 * BK * 2, &tmP, ld, v0 + 64, (int)rb);
-      if (two) {
-        tc::tma_load_2d(sa + A_BYTES, &tmP, ld, v0 + 128, (int)rb);
-        tc::tma_load_2d(sa + A_BYTES + 64 * BK * 2, &tmP, ld, v0 + 192, (int)rb);
-      }
-      for (int bx = 0; bx < nbox; ++bx)
-        tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), &tmH, ld, j0 + bx * 64, (int)rb);
+      tc::tma_load_3d(sa, &tmP, ld, 0, (int)rb, v0 / 64);
+      if (p.h3) tc::tma_load_3d(sa + 2 * A_BYTES, &tmH, ld, 0, (int)rb, j0 / 64);
+      else
+        for (int bx = 0; bx < nbox; ++bx)
+          tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), &tmH, ld, j0 + bx * 64, (int)rb);
       tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
       if (two) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
@@ -991,7 +1016,10 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                              float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  const bool w3 = d.J % 64 == 0;
+  if (w3 ? !make_tmap_bf16_3d(&tw, W, 64, d.V, d.J / 64, (uint64_t)d.J * 2, 128, 64, 64, 4)
+         : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
+    return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -1008,6 +1036,7 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
                    static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0, F * d.S, nullptr};
   if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);
+  p.w3 = w3;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
@@ -1029,13 +1058,16 @@ cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint
                                      cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
+  const bool w3 = d.J % 64 == 0;
+  if (w3 ? !make_tmap_bf16_3d(&tw, W, 64, d.V, d.J / 64, (uint64_t)d.J * 2, 128, 64, 64, 4)
+         : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
+    return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   cudaFuncSetAttribute(joiner_dh_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
   cudaFuncSetAttribute(joiner_dh_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
-                   nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out};
+                   nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out, w3};
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
@@ -1069,8 +1101,17 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       cudaFuncSetAttribute(joiner_dw_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdw2::SMEM_BYTES);
       attr = true;
     }
+    CUtensorMap tp3, th3;
+    if (!make_tmap_bf16_3d(&tp3, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw2::BK, 4))
+      return cudaErrorInvalidValue;
+    p.h3 = d.J % 64 == 0;
+    if (p.h3 && !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4))
+      return cudaErrorInvalidValue;
+    if (const char* e = getenv("RNNT_DW_PF")) p.pf = atoi(e);
+    if (const char* e = getenv("RNNT_DW_PFMODE")) p.pfmode = atoi(e);
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
-    RNNT_LAUNCH(KID_DW, st, joiner_dw_wide_kernel<<<grid, jdw2::THREADS, jdw2::SMEM_BYTES, st>>>(tp, th, p));
+    if (p.pfmode & 2) std::swap(grid.x, grid.y);
+    RNNT_LAUNCH(KID_DW, st, joiner_dw_wide_kernel<<<grid, jdw2::THREADS, jdw2::SMEM_BYTES, st>>>(tp3, p.h3 ? th3 : th, p));
   } else if (pair) {
     static bool attr = false;
     if (!attr) {
@@ -1099,7 +1140,13 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       attr = true;
     }
     dim3 grid(vt, (d.J + jdw::BN - 1) / jdw::BN, splits);
-    RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<false><<<grid, jdw::THREADS, jdw::Cfg<false>::SMEM_BYTES, st>>>(tp, th, p));
+    CUtensorMap tp3, th3;
+    p.h3 = d.J % 64 == 0;
+    if (p.h3 && (!make_tmap_bf16_3d(&tp3, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw::BK, 2) ||
+                 !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw::BK, 4)))
+      return cudaErrorInvalidValue;
+    RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<false><<<grid, jdw::THREADS, jdw::Cfg<false>::SMEM_BYTES, st>>>(
+                                p.h3 ? tp3 : tp, p.h3 ? th3 : th, p));
   }
   return cudaGetLastError();
 }

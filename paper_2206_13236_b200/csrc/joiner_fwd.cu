@@ -320,6 +320,295 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
   if (warp == 1) tc::tmem_dealloc(tbase, 4 * BN);
 }
 
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes 256 rows (one 128-row tile per CTA)
+// x 256 V columns per MMA (M = 256, N = 256).  Each CTA loads its own h rows (A) and HALF of the W rows
+// (B: its 128 of the 256 V columns), so the L2 -> SM bytes per MMA flop halve against the single-CTA
+// 128 x 128 tiles (the forward's bound at large V).  Row-tile pairs come from the global counter: the
+// leader's producer draws the next pair with a live row and publishes it to both CTAs' tile queues
+// (a 4-slot ring in shared memory, the peer's written through DSMEM).
+// Each CTA holds two 256-column TMEM accumulators (double-buffered); epilogue set e of both CTAs
+// takes the 128 columns 128e.. of every accumulator (V tiles 2 vp + e) and keeps its own running
+// (max, sum); the two sets merge them at the end of the row tile.
+namespace jf2 {
+constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;        // 16 KB: this CTA's 128 h rows
+constexpr int B_BYTES = BN * BK * 2;        // 16 KB: this CTA's 128 of the pair's 256 W rows
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int STG_BYTES = BM * BN * 2;      // 32 KB P~ staging per epilogue set
+constexpr int MRG_OFF = STAGES * STAGE_BYTES + 2 * STG_BYTES;
+constexpr int BAR_OFF = MRG_OFF + 2 * BM * 16;
+constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
+constexpr int THREADS = 320;
+}  // namespace jf2
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
+    joiner_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
+  using namespace jf2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = tc::align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;      // [2] accumulators
+  uint64_t* tempty = tfull + 2;          // [2] (leader's: 8 epilogue warps of each CTA)
+  uint64_t* qfull = tempty + 2;          // [4] tile queue: leader producer -> all roles of both CTAs
+  uint64_t* qempty = qfull + 4;          // [4] (leader's: 18 consumers over the pair)
+  int* tq = reinterpret_cast<int*>(qempty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
+  float4* mrg = reinterpret_cast<float4*>(smem + MRG_OFF);   // [2][128] set-1 row state for the merge
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 16); }
+    for (int s = 0; s < 4; ++s) { tc::mbar_init(&qfull[s], 1); tc::mbar_init(&qempty[s], 18); }
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc2(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+  const int nvt = p.nvt, nvp = (nvt + 1) / 2, nkb = p.nkb;
+  const int npairs = (p.ntiles + 1) / 2;
+  auto live_pair = [&](int rp) {
+    return p.tlive[2 * rp] || (2 * rp + 1 < p.ntiles && p.tlive[2 * rp + 1]);
+  };
+  const uint32_t qemptyL = tc::mapa(&qempty[0], 0);
+  // consumers: take queue entry qi (-1 = done) and release its slot on the leader
+  auto take = [&](int qi, bool arrive) {
+    tc::mbar_wait_cluster(&qfull[qi & 3], (qi >> 2) & 1);
+    const int rp = *reinterpret_cast<volatile int*>(&tq[qi & 3]);
+    if (arrive) tc::mbar_arrive_cluster(qemptyL + (qi & 3) * 8);
+    return rp;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t fullL = tc::mapa(&full[0], 0);
+      const uint32_t tqP = tc::mapa(&tq[0], 1), qfullP = tc::mapa(&qfull[0], 1);
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int qi = 0;; ++qi) {
+        int rp;
+        if (leader) {
+          rp = atomicAdd(p.counter, 1);
+          while (rp < npairs && !live_pair(rp)) rp = atomicAdd(p.counter, 1);
+          if (rp >= npairs) rp = -1;
+          tc::mbar_wait_cluster(&qempty[qi & 3], ((qi >> 2) & 1) ^ 1);
+          tq[qi & 3] = rp;
+          tc::st_cluster_u32(tqP + (qi & 3) * 4, (uint32_t)rp);
+          tc::mbar_arrive(&qfull[qi & 3]);
+          tc::mbar_arrive_cluster(qfullP + (qi & 3) * 8);
+        } else {
+          rp = take(qi, true);
+        }
+        if (rp < 0) break;
+        const int m0 = (2 * rp + (int)rank) * BM;
+        for (int kb = 0; kb < nkb; ++kb) tc::tma_prefetch_2d(&tmA, kb * BK, m0);
+        for (int vp = 0; vp < nvp; ++vp) {
+          for (int kb = 0; kb < nkb; ++kb) {
+            tc::mbar_wait(&empty[stage], ph ^ 1);
+            if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            tc::tma_load_2d_2sm(sa, &tmA, fullL + stage * 8, kb * BK, m0);
+            tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, fullL + stage * 8, kb * BK, vp * 2 * BN + (int)rank * BN);
+            if (++stage == STAGES) { stage = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, 2 * BN, false, false);
+      int stage = 0, it = 0;
+      uint32_t ph = 0;
+      for (int qi = 0;; ++qi) {
+        if (take(qi, true) < 0) break;
+        for (int vp = 0; vp < nvp; ++vp, ++it) {
+          const int acc = it & 1;
+          tc::mbar_wait_cluster(&tempty[acc], ((it >> 1) & 1) ^ 1);
+          tc::fence_after_sync();
+          const uint32_t d = tbase + acc * 2 * BN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            tc::mbar_wait_cluster(&full[stage], ph);
+            tc::fence_after_sync();
+            const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma2_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 32 * k, 16, 1024), idesc,
+                            (kb | k) != 0);
+            tc::mma2_commit(&empty[stage], 3);
+            if (++stage == STAGES) { stage = 0; ph ^= 1; }
+          }
+          tc::mma2_commit(&tfull[acc], 3);
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int set = (warp - 2) >> 2;           // warps 2-5: set 0 (columns 0-127), 6-9: set 1 (128-255)
+    const int ethr = 64 + 128 * set;
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + set * STG_BYTES;
+    const uint32_t tl = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
+    const uint32_t temptyL = tc::mapa(&tempty[0], 0);
+    int it = 0, nrt = 0;
+    for (int qi = 0;; ++qi) {
+      const int rp = take(qi, false);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(qemptyL + (qi & 3) * 8);
+      if (rp < 0) break;
+      const int rt = 2 * rp + (int)rank;
+      const long long r = (long long)rt * BM + 32 * q + lane;
+      const int info = (r < p.R) ? p.rowinfo[r] : -1;
+      float M = neg_inf_f(), sum = 0.f, zb = neg_inf_f(), zl = neg_inf_f();
+      for (int vp = 0; vp < nvp; ++vp, ++it) {
+        const int acc = it & 1;
+        const int nt = 2 * vp + set, v0 = nt * BN;
+        tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t tcol = tl + acc * 2 * BN;
+        const bool have = nt < nvt;             // warp-uniform
+        constexpr float kRedo = 60.f;
+        float m = neg_inf_f(), s = 0.f;
+        if (have) {
+          // One TMEM pass as in joiner_fwd_tc_kernel: the tile's exp offset m comes from its first
+          // 32-column chunk joined with the running max; a later chunk above m + kRedo redoes the tile
+          // with an exact max pass.
+          const float zb_prev = zb, zl_prev = zl;
+          bool redo = false;
+          if (threadIdx.x == ethr) tc::bulk_wait_read0();
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
+          for (int attempt = 0; attempt < 2; ++attempt) {
+            if (attempt == 1) {
+              if (!__any_sync(0xffffffffu, redo)) break;
+              m = neg_inf_f();
+#pragma unroll 1
+              for (int c = 0; c < 4; ++c) {
+                float z[32];
+                tc::tmem_ld32(tcol + 32 * c, z);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (v0 + 32 * c + j < p.V) m = fmaxf(m, z[j] + p.bias[v0 + 32 * c + j]);
+              }
+              s = 0.f;
+              zb = zb_prev; zl = zl_prev;
+            }
+            float mL = m * RNNT_LOG2E_F;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              float z[32];
+              {
+                uint32_t zr[32];
+                tc::tmem_ld32_issue(tcol + 32 * c, zr);
+                const int vc = v0 + 32 * c;
+                float4 b4[8];
+                const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) b4[j4] = __ldg(bb + j4);
+                tc::tmem_ld32_wait(zr);
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) {
+                  z[4 * j4] = __uint_as_float(zr[4 * j4]) + b4[j4].x;
+                  z[4 * j4 + 1] = __uint_as_float(zr[4 * j4 + 1]) + b4[j4].y;
+                  z[4 * j4 + 2] = __uint_as_float(zr[4 * j4 + 2]) + b4[j4].z;
+                  z[4 * j4 + 3] = __uint_as_float(zr[4 * j4 + 3]) + b4[j4].w;
+                }
+              }
+              const int vc = v0 + 32 * c;
+              if (attempt == 0) {
+                float cm = z[0];
+#pragma unroll
+                for (int j = 1; j < 32; ++j) cm = fmaxf(cm, z[j]);
+                if (c == 0) {
+                  m = fmaxf(M, cm);
+                  mL = m * RNNT_LOG2E_F;
+                } else if (cm - m > kRedo) {
+                  redo = true;
+                }
+                if (__any_sync(0xffffffffu, redo)) break;
+              }
+              uint32_t pk[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float e0 = ex2_approx(fmaf(z[2 * j], RNNT_LOG2E_F, -mL));
+                const float e1 = ex2_approx(fmaf(z[2 * j + 1], RNNT_LOG2E_F, -mL));
+                s += e0 + e1;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(e0, e1);
+                pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+              {
+                uint8_t* sb = stg + (c >> 1) * (STG_BYTES / 2);
+                const int row = 32 * q + lane;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  *reinterpret_cast<uint4*>(sb + sw128f(row, (c & 1) * 4 + j)) =
+                      make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+              }
+              if (vc == 0) zb = z[0];
+              const int li = info - vc;
+              const bool hit = (unsigned)li < 32u;
+              if (__any_sync(0xffffffffu, hit)) {
+                float zz[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) zz[j] = z[j];
+                if (hit) zl = zz[li];
+              }
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(temptyL + acc * 8);
+        if (have) {
+          tc::fence_proxy_async();
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
+          if (threadIdx.x == ethr && (long long)rt * BM < p.R) {
+            tc::tma_store_2d(&tmP, stg, v0, rt * BM);
+            tc::tma_store_2d(&tmP, stg + STG_BYTES / 2, v0 + 64, rt * BM);
+            tc::bulk_commit();
+          }
+          if (info >= 0) p.mt[(size_t)r * p.ntile + v0 / 128] = m;
+          const float Mn = fmaxf(M, m);
+          sum = sum * ex2_approx((M - Mn) * RNNT_LOG2E_F) + s * ex2_approx((m - Mn) * RNNT_LOG2E_F);
+          M = Mn;
+        }
+      }
+      // merge set 1's running state into set 0's (double-buffered by row-tile parity)
+      float4* mb = mrg + (nrt & 1) * BM;
+      if (set == 1) mb[32 * q + lane] = make_float4(M, sum, zb, zl);
+      asm volatile("bar.sync 3, 256;" ::: "memory");
+      if (set == 0 && r < p.R) {
+        const float4 o = mb[32 * q + lane];
+        const float Mn = fmaxf(M, o.x);
+        const float tot = sum * ex2_approx((M - Mn) * RNNT_LOG2E_F) + o.y * ex2_approx((o.x - Mn) * RNNT_LOG2E_F);
+        const float zlab = fmaxf(zl, o.w);   // the label's column lies in exactly one set's tiles
+        if (info >= 0) {
+          const float l = Mn + lg2_approx(tot) * RNNT_LN2_F;
+          p.lse[r] = l;
+          p.py2[r] = (zb - l) * RNNT_LOG2E_F;
+          p.px2[r] = info < p.V ? (zlab - l) * RNNT_LOG2E_F : kNegBig;
+        } else {
+          p.lse[r] = 0.f;
+          p.px2[r] = kNegBig;
+          p.py2[r] = kNegBig;
+        }
+      }
+      ++nrt;
+    }
+  }
+  if (warp >= 2 && (threadIdx.x & 127) == 64) tc::bulk_wait0();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();
+  if (warp == 1) tc::tmem_dealloc2(tbase, 512);
+}
+
 cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
@@ -339,6 +628,23 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   }
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  static int pair = -1;
+  if (pair < 0) {
+    const char* e = getenv("RNNT_FWD_PAIR");
+    pair = e ? atoi(e) : 1;
+  }
+  if (pair) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(joiner_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jf2::SMEM_BYTES);
+      attr2 = true;
+    }
+    // persistent: one CTA per SM, in pairs (at most one cluster per row-tile pair); the pair counter is
+    // the row-tile counter rowinfo_kernel zeroes
+    const unsigned grid = (unsigned)(2 * std::min((ntiles + 1) / 2, nsm / 2));
+    RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_pair_kernel<<<grid, jf2::THREADS, jf2::SMEM_BYTES, st>>>(ta, tb, tp, p));
+    return cudaGetLastError();
+  }
   const unsigned grid = (unsigned)std::min(ntiles, nsm);   // persistent: one CTA per SM
   RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, tp, p));
   return cudaGetLastError();

@@ -16,7 +16,7 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint6
 // box0 x box1 x 1, SWIZZLE_128B (box0 * 2 == 128), out-of-bounds elements (also past d1 within a
 // plane) read as zero — used for per-utterance operands so a box never spills into the next one.
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1,
-                       uint64_t stride2, uint32_t box0, uint32_t box1);
+                       uint64_t stride2, uint32_t box0, uint32_t box1, uint32_t box2 = 1);
 
 // 3-D fp32 tensor, box = box0 (32 -> 128 B rows) x box1 x 1, SWIZZLE_128B (loads and stores).
 bool make_tmap_f32_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t stride1,

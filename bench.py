@@ -521,14 +521,14 @@ def main():
         # layout (padded input contents are never read, include/rnnt.h)
         rowsof = {"am": b.T_n, "enc_proj": b.T_n, "lm": b.U_n + 1, "dec_proj": b.U_n + 1}
         packed, pidx, dpacked = {}, {}, {}
-        for name, lens in rowsof.items():
-            full_ = host[name]
+        for tname, lens in rowsof.items():
+            full_ = host[tname]
             P_ = full_.shape[1]
             idx = np.concatenate([n * P_ + np.arange(int(lens[n])) for n in range(b.N)])
             flat = full_.view(-1, full_.shape[2])
-            packed[name] = flat[torch.from_numpy(idx)].contiguous().pin_memory()
-            pidx[name] = torch.from_numpy(idx).cuda()
-            dpacked[name] = torch.empty_like(packed[name], device="cuda")
+            packed[tname] = flat[torch.from_numpy(idx)].contiguous().pin_memory()
+            pidx[tname] = torch.from_numpy(idx).cuda()
+            dpacked[tname] = torch.empty_like(packed[tname], device="cuda")
         small = [k for k in host if k not in rowsof and k not in ("w_out", "b_out")]
         h2d = sum(v.numel() * v.element_size() for v in packed.values()) + \
             sum(host[k].numel() * host[k].element_size() for k in small)
@@ -559,12 +559,12 @@ def main():
                 k = i & 1
                 with torch.cuda.stream(copy_stream):
                     copy_stream.wait_event(freed[k])          # step i-2 finished reading buffer set k
-                    for name in small:
-                        bufs[k][name].copy_(host[name], non_blocking=True)
-                    for name in packed:
-                        dpacked[name].copy_(packed[name], non_blocking=True)
-                        dst = bufs[k][name]
-                        dst.view(-1, dst.shape[2]).index_copy_(0, pidx[name], dpacked[name])
+                    for tname in small:
+                        bufs[k][tname].copy_(host[tname], non_blocking=True)
+                    for tname in packed:
+                        dpacked[tname].copy_(packed[tname], non_blocking=True)
+                        dst = bufs[k][tname]
+                        dst.view(-1, dst.shape[2]).index_copy_(0, pidx[tname], dpacked[tname])
                     copied[k].record(copy_stream)
                 stream.wait_event(copied[k])
                 if graphs[k] is not None:

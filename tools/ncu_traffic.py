@@ -5,6 +5,7 @@ of each library kernel in an ncu --set full report of the bench step (mean over 
 import collections, csv, io, json, os, subprocess, sys
 
 NAMES = {"joiner_dh_tc_kernel": "joiner_dh_gemm", "joiner_fwd_tc_kernel": "joiner_fwd_gemm",
+         "joiner_fwd_pair_kernel": "joiner_fwd_gemm", "joiner_dw_wide_kernel": "joiner_dw_gemm",
          "joiner_dw_tc_kernel": "joiner_dw_gemm", "gemm3_kernel<rnnt::NormProb>": "simple_norm_gemm",
          "prune_kernel": "prune_gather", "combine_kernel": "lattice_combine", "simple_prep_kernel": "simple_prep",
          "gemm3_kernel<rnnt::AmProb>": "simple_am_grad_gemm", "gemm3_kernel<rnnt::LmProb>": "simple_lm_grad_gemm",

@@ -379,13 +379,16 @@ def main():
     stream = R.critical_stream() if not args.no_priority else torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
+    def exchange():
+        # on the d_w stream (R.step grad_hook): overlaps the d_enc / d_dec kernels of the step
+        gbuf.set_losses(outs["loss_simple"], outs["loss_pruned"])
+        allreduce_grads(gbuf)
+
     def step(inp):
         outs["status"].zero_()
         R.step(inp["am"], inp["lm"], inp["symbols"], inp["boundary"], inp["enc_proj"], inp["dec_proj"],
-               inp["w_out"], inp["b_out"], b.S, out=outs, workspace=ws)
-        if pg is not None:
-            gbuf.set_losses(outs["loss_simple"], outs["loss_pruned"])
-            allreduce_grads(gbuf)
+               inp["w_out"], inp["b_out"], b.S, out=outs, workspace=ws,
+               grad_hook=exchange if pg is not None else None)
 
     ids = R.kernel_ids()
     kname = args.profile_kernel if args.profile_kernel != "auto" else "joiner_fwd_gemm"
@@ -602,7 +605,8 @@ def main():
         v, f, used, el, cores = time_oracle(b, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{len(used)} of {b.N} utterances ({f} frames) of the same batch, full fwd+bwd "
-                         f"oracle path, {el:.1f}s, fp64 numpy with BLAS limited to 1 thread"}
+                         f"oracle path, {el:.1f}s, fp64 numpy with BLAS limited to 1 thread",
+               "host_cpu_count": os.cpu_count(), "host_affinity": len(os.sched_getaffinity(0))}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -619,7 +623,9 @@ def main():
                 "gpu_launches": int(launches), "clocks": clk,
                 "execution": "cuda_graph" if graph is not None else "eager",
                 "eager_ms_per_step": statistics.mean(eager_ms), "graph_error": graph_err,
-                "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)}}
+                "step_ms": {"median": statistics.median(step_ms), "p10": float(np.percentile(step_ms, 10)),
+                            "p90": float(np.percentile(step_ms, 90)), "min": min(step_ms), "max": max(step_ms)},
+                "workspace_gib": R.rnnt_workspace_bytes(dims) / 2 ** 30}
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.barrier()

@@ -329,7 +329,7 @@ def critical_stream(device=None):
 
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
          pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True,
-         lm_only_scale=0.0, am_only_scale=0.0):
+         lm_only_scale=0.0, am_only_scale=0.0, grad_hook=None):
     """One fwd+bwd of the whole hot path: simple loss and its
     gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
     device tensors; ``out`` may supply preallocated outputs (same keys).
@@ -337,7 +337,11 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     ``lm_only_scale`` / ``am_only_scale`` select the smoothed trivial joiner (Eq. 11-15) for the
     simple stage (0, 0: the plain trivial joiner).  With ``overlap`` the am/lm gradients
     (rnnt_simple_loss[_smoothed]_backward) run on a side stream concurrently with the pruned stage,
-    joined back into ``stream`` before returning."""
+    joined back into ``stream`` before returning.
+
+    ``grad_hook()`` (e.g. the data-parallel all_reduce of d_w / d_b / loss sums) is called once both
+    losses and d_w / d_b are final: with ``overlap`` on the d_w stream right after the weight
+    gradient, so the collective overlaps the input-gradient kernels; otherwise at the end."""
     dims = dims_of(am, lm, w_out, S)
     dev = am.device
     o = out if out is not None else alloc_outputs(dims, dev)
@@ -375,6 +379,9 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
         side2 = _side_stream(dev, 1)
         side2.wait_stream(cur)
         rnnt_pruned_loss_backward_weight(o["h"], dims, o["d_w"], o["d_b"], ws, side2)
+        if grad_hook is not None:
+            with torch.cuda.stream(side2):
+                grad_hook()
         rnnt_pruned_loss_backward_input(o["h"], w_out, o["ranges"], boundary, dims, o["d_enc"], o["d_dec"], ws, cur)
         cur.wait_stream(side)
         cur.wait_stream(side2)
@@ -385,6 +392,8 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     else:
         rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
                          o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)
+        if grad_hook is not None:
+            grad_hook()
     return o
 
 

@@ -277,3 +277,34 @@ def test_full_loss_config2_sampled():
         assert_bf16_grad(g["d_dec"][n, :U + 1], ref["d_dec"][n], f"d_dec[{n}]")
     p = _run_step(b)
     assert np.all(p["loss_pruned"] >= g["loss"] - 1e-3 * np.abs(g["loss"]))
+
+
+def test_grad_hook_sees_final_weight_grads():
+    """step(grad_hook=...) runs the hook (the data-parallel all_reduce in bench.py) on the d_w stream
+    while the input-gradient kernels still run: it must see the final d_w, d_b and both losses, and the
+    returned outputs must equal a step without the hook (c2 batch, launch configuration of bench.py)."""
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(2)
+    dev = R.batch_to_device(b, "cuda")
+    args = (dev["am"], dev["lm"], dev["symbols"], dev["boundary"], dev["enc_proj"], dev["dec_proj"],
+            dev["w_out"], dev["b_out"], b.S)
+    ref = {k: v.clone() for k, v in R.step(*args).items()}
+    torch.cuda.synchronize()
+    seen = {}
+    holder = {}
+
+    def hook():
+        o = holder["o"]
+        seen["d_w"] = o["d_w"].clone()
+        seen["d_b"] = o["d_b"].clone()
+        seen["ls"] = o["loss_simple"].clone()
+        seen["lp"] = o["loss_pruned"].clone()
+
+    holder["o"] = R.alloc_outputs(R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S), "cuda")
+    o = R.step(*args, out=holder["o"], grad_hook=hook)
+    torch.cuda.synchronize()
+    for k in ("d_w", "d_b", "loss_pruned", "loss_simple", "d_enc", "d_dec", "am_grad"):
+        assert torch.equal(o[k], ref[k]), k
+    assert torch.equal(seen["d_w"], ref["d_w"]) and torch.equal(seen["d_b"], ref["d_b"])
+    assert torch.equal(seen["ls"], ref["loss_simple"]) and torch.equal(seen["lp"], ref["loss_pruned"])

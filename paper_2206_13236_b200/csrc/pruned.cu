@@ -171,7 +171,7 @@ __device__ __forceinline__ void scan_trace(int k) {
   if (g_scan_trace && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 5 + k] = t;
+    g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + k] = t;
   }
 }
 
@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     for (int i = 0; i < C; ++i) {
       const StepIn in = nx;
       if (i + 1 < C) nx = load_step(c, i + 1, cact);   // next frame's arcs in flight during this step
+      __syncwarp();        // reconverge after the lane-dependent loads: the shuffles below stay on the fast path
       const bool act = in.act;
       const int d = in.d;
       const float own_py = in.py, own_px = in.px;
@@ -360,7 +361,12 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     double sh = 0.0;
     if (sa) bv[s] = a;
     if (lane == 0) bsh[0] = 0.0;
+    const long long ck0 = clock64();
     for (int c = 0; c < nc; ++c) {
+      // reconverge the warp every step: after the lane-predicated stores (and the divergent set-up
+      // above) the warp otherwise stays split and every shuffle takes the diverged path (measured
+      // 3519 -> 538 cycles per step at c4)
+      __syncwarp();
       const float m = rebase_of(__shfl_sync(0xffffffffu, a, 0));
       const float* Pc = Pm + ((size_t)c * S + (sa ? s : 0)) * S;
       float mx = NB, x[KR];
@@ -378,6 +384,10 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       sh += (double)m + (double)psh[c];
       if (sa) bv[(c + 1) * S + s] = a;
       if (lane == 0) bsh[c + 1] = sh;
+    }
+    if (g_scan_trace && lane == 0) {
+      g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + 5] = (unsigned long long)(clock64() - ck0);
+      g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + 6] = (unsigned long long)nc;
     }
   }
   __syncthreads();
@@ -406,6 +416,7 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     for (int i = 0; i < C; ++i) {
       const StepIn in = nx;
       if (i + 1 < C) nx = load_step(c, i + 1, cact);
+      __syncwarp();                                     // converged shuffles (see phase A)
       const int t = in.t;
       const bool act = in.act;
       const int d = in.d;

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "tc.cuh"
 #include "workspace.h"
 
 namespace rnnt {
@@ -164,14 +165,19 @@ __device__ __forceinline__ float lae2(float a, float b) {
 }
 __device__ __forceinline__ float rebase_of(float v) { return v > -1e29f ? rintf(v) : 0.f; }
 
+__device__ __forceinline__ uint32_t cluster_dim_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctaid.x;" : "=r"(r));
+  return r;
+}
 // diagnostics: per (utterance, direction) CTA timestamps {start, staged, phase A, phase B, phase C}
 __device__ unsigned long long* g_scan_trace = nullptr;
 void set_scan_trace(void* buf) { cudaMemcpyToSymbol(g_scan_trace, &buf, sizeof(buf)); }
 __device__ __forceinline__ void scan_trace(int k) {
-  if (g_scan_trace && threadIdx.x == 0) {
+  if (g_scan_trace && threadIdx.x == 0 && blockIdx.x % max(1u, (unsigned)cluster_dim_x()) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + k] = t;
+    g_scan_trace[((size_t)(blockIdx.x / cluster_dim_x()) * 2 + blockIdx.y) * 8 + k] = t;
   }
 }
 
@@ -191,6 +197,7 @@ struct ScanParams {
   double* Lp;
   float* loss;
   int32_t* status;
+  int G;             // CTAs per (utterance, direction): a thread-block cluster sharing the chunk work
 };
 
 // SMAX: register rows per lane; SC: the band width S as a compile-time constant (0: runtime S <= SMAX),
@@ -198,14 +205,19 @@ struct ScanParams {
 template <int SMAX, int SC>
 __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int n = blockIdx.x;
+  // a cluster of G CTAs per (utterance, direction): phases A and C are spread over its CTAs (chunk
+  // c goes to rank c % G), the chunk matrices land in the rank-0 CTA's shared memory (DSMEM
+  // stores), rank 0 runs the boundary chain (B), the others read the boundary vectors back
+  const int G = q.G;
+  const int rank = G > 1 ? (int)tc::cluster_ctarank() : 0;
+  const int n = blockIdx.x / G;
   const bool fwd = blockIdx.y == 0;
   const int S = SC > 0 ? SC : q.S, C = q.C;
   constexpr int KR = SC > 0 ? SC : SMAX;     // rows actually carried
   const int Tn = utt_T(q.bnd, n), Un = utt_U(q.bnd, n);
   const bool feasible = (long long)Un <= (long long)Tn * (S - 1);
-  if (!feasible) {
-    if (fwd && threadIdx.x == 0) {
+  if (!feasible) {                 // (every CTA of the cluster returns here: same utterance)
+    if (fwd && threadIdx.x == 0 && rank == 0) {
       q.Lp[n] = neg_inf_d();
       q.loss[n] = __int_as_float(0x7f800000);  // +inf: no band-respecting path (kept visible, D16)
       set_status(q.status, n, kStatusInfeasible);
@@ -228,7 +240,23 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     const int m = Tn * S;
     const float* gx = q.px2 + rb;
     const float* gy = q.py2 + rb;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) { PXs[i] = gx[i]; PYs[i] = gy[i]; }
+    // 8 independent loads per array in flight per thread (one load per iteration left the staging
+    // latency-bound: 19 us at c4)
+    constexpr int U8 = 8;
+    for (int i0 = threadIdx.x; i0 < m; i0 += U8 * blockDim.x) {
+      float x[U8], y[U8];
+#pragma unroll
+      for (int k = 0; k < U8; ++k) {
+        const int i = i0 + k * blockDim.x;
+        x[k] = i < m ? gx[i] : 0.f;
+        y[k] = i < m ? gy[i] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U8; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i < m) { PXs[i] = x[k]; PYs[i] = y[k]; }
+      }
+    }
     const int32_t* gp = q.ranges + (size_t)n * q.T;
     for (int i = threadIdx.x; i < Tn; i += blockDim.x) prs[i] = gp[i];
   }
@@ -266,9 +294,9 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   };
 
   // ---------------- phase A: chunk transfer matrices
-  const int rounds = (nc + nseg - 1) / nseg;
+  const int rounds = (nc + nseg * G - 1) / (nseg * G);
   for (int rd = 0; rd < rounds; ++rd) {
-    const int c = seg + rd * nseg;
+    const int c = rank + G * (seg + rd * nseg);
     const bool cact = on && c < nc;
     float P[KR];
 #pragma unroll
@@ -327,17 +355,26 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     }
     if (cact) {
       float* dst = Pm + ((size_t)c * S + s) * S;
+      if (G > 1) {
+        const uint32_t da = tc::mapa(dst, 0);
 #pragma unroll
-      for (int k = 0; k < KR; ++k)
-        if (k < S) dst[k] = P[k];
-      if (s == 0) psh[c] = shacc;
+        for (int k = 0; k < KR; ++k)
+          if (k < S) tc::st_cluster_f32(da + 4 * k, P[k]);
+        if (s == 0) tc::st_cluster_f32(tc::mapa(&psh[c], 0), shacc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < KR; ++k)
+          if (k < S) dst[k] = P[k];
+        if (s == 0) psh[c] = shacc;
+      }
     }
   }
-  __syncthreads();
+  if (G > 1) tc::cluster_sync();        // every chunk matrix is in rank 0's shared memory
+  else __syncthreads();
   scan_trace(2);
 
-  // ---------------- phase B: boundary vectors (warp 0, segment 0)
-  if (warp == 0) {
+  // ---------------- phase B: boundary vectors (rank 0, warp 0, segment 0)
+  if (warp == 0 && rank == 0) {
     const bool sa = lane < S;
     float a = NB;
     if (fwd) {
@@ -386,17 +423,18 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       if (lane == 0) bsh[c + 1] = sh;
     }
     if (g_scan_trace && lane == 0) {
-      g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + 5] = (unsigned long long)(clock64() - ck0);
-      g_scan_trace[((size_t)blockIdx.x * 2 + blockIdx.y) * 8 + 6] = (unsigned long long)nc;
+      g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 5] = (unsigned long long)(clock64() - ck0);
+      g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 6] = (unsigned long long)nc;
     }
   }
-  __syncthreads();
+  if (G > 1) tc::cluster_sync();        // the boundary vectors are visible to every rank
+  else __syncthreads();
   scan_trace(3);
 
   // ---------------- phase C: every frame of every chunk from its boundary vector
   float* outp = (fwd ? q.ap : q.bp) + rb;
   double* Fs = (fwd ? q.Af : q.Bf) + (size_t)n * q.T;
-  if (warp == 0 && lane < S) {       // the boundary frame 0 (fwd) / T-1 (bwd) itself
+  if (warp == 0 && lane < S && rank == 0) {       // the boundary frame 0 (fwd) / T-1 (bwd) itself
     const int t0 = fwd ? 0 : Tn - 1;
     outp[(size_t)t0 * S + s] = bv[s];
     if (s == 0) Fs[t0] = 0.0;
@@ -408,10 +446,19 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
     }
   }
   for (int rd = 0; rd < rounds; ++rd) {
-    const int c = seg + rd * nseg;
+    const int c = rank + G * (seg + rd * nseg);
     const bool cact = on && c < nc;
-    float a = cact ? bv[(size_t)c * S + s] : NB;
-    double sh = cact ? bsh[c] : 0.0;
+    float a = NB;
+    double sh = 0.0;
+    if (cact) {
+      if (G > 1) {
+        a = tc::ld_cluster_f32(tc::mapa(&bv[(size_t)c * S + s], 0));
+        sh = tc::ld_cluster_f64(tc::mapa(&bsh[c], 0));
+      } else {
+        a = bv[(size_t)c * S + s];
+        sh = bsh[c];
+      }
+    }
     StepIn nx = load_step(c, 0, cact);
     for (int i = 0; i < C; ++i) {
       const StepIn in = nx;
@@ -453,7 +500,8 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
       }
     }
   }
-  __syncthreads();
+  if (G > 1) tc::cluster_sync();        // rank 0's shared memory stays alive until every rank has read it
+  else __syncthreads();
   scan_trace(4);
 }
 
@@ -527,9 +575,17 @@ static long long scan_mat_bytes(const Dims& d, int c) {
   const long long nc = (d.T + c - 1) / c + 1;
   return ((nc * d.S * d.S + nc + (nc + 1) * d.S) * 4 + 15) / 16 * 16 + (nc + 1) * 8;
 }
+// CTAs per (utterance, direction) of the scan: 4 for wide bands (phase A is bound by the MUFU work
+// of S (S-1) LogAdds per lane and frame), else 2
+static int scan_cluster(const Dims& d) { return d.S >= 8 ? 4 : 2; }
+// Chunk length: the chain is A (C frames) + B (T/C steps, ~0.23 us each) + C (C frames, where a
+// frame of A + C costs ~1 us at S = 5): C ~ sqrt(T / 5), raised until every chunk has a segment in
+// one round over the cluster (nseg = 8 (32 / S) per CTA) and the matrices fit in shared memory.
 static int scan_chunk(const Dims& d) {
+  const int nseg = 8 * (32 / std::max(1, std::min(d.S, 32))) * scan_cluster(d);
   int C = 4;
-  while ((long long)C * C < d.T) ++C;
+  while ((long long)C * C * 5 < d.T) ++C;
+  while ((d.T + C - 1) / C > nseg) ++C;
   while (scan_mat_bytes(d, C) > 32 * 1024) C *= 2;
   return C;
 }
@@ -541,7 +597,19 @@ size_t pruned_recursion_smem(const Dims& d) {
 template <int SMAX, int SC>
 static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cudaStream_t st) {
   cudaFuncSetAttribute(pruned_scan_kernel<SMAX, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  RNNT_LAUNCH(KID_PALPHA, st, pruned_scan_kernel<SMAX, SC><<<dim3(d.N, 2), 256, sm, st>>>(q));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(d.N * q.G), 2);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)q.G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RNNT_LAUNCH(KID_PALPHA, st, cudaLaunchKernelEx(&cfg, pruned_scan_kernel<SMAX, SC>, q));
   return cudaGetLastError();
 }
 
@@ -567,7 +635,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     const size_t sm = pruned_recursion_smem(d);
     const int C = scan_chunk(d);
     ScanParams q{w.px2, w.py2, ranges, bnd, d.T, d.S, C, (d.T + C - 1) / C + 1, w.ap, w.bp, w.Af, w.Bf, w.Lp, loss,
-                 status};
+                 status, scan_cluster(d)};
     switch (d.S) {   // band widths of the BASELINE configs (and the tests) get a compile-time S
       case 2: e = launch_scan<2, 2>(d, q, sm, st); break;
       case 3: e = launch_scan<3, 3>(d, q, sm, st); break;

@@ -61,19 +61,62 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   }
   const float* p = x + row * (long long)V;
   float mx = neg_inf_f();
-  for (int v = lane; v < V; v += 32) mx = fmaxf(mx, p[v]);
-  mx = warp_max(mx);
-  if (lane == 0) m[row] = mx;
   float esum = 0.f;
-  for (int v2 = lane; v2 < VP / 2; v2 += 32) {
-    const int v = 2 * v2;
-    const float e0 = v < V ? __expf(p[v] - mx) : 0.f;
-    const float e1 = v + 1 < V ? __expf(p[v + 1] - mx) : 0.f;
-    esum += e0 + e1;
-    const __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(e0 - __low2float(h), e1 - __high2float(h));
-    H[v2] = *reinterpret_cast<const uint32_t*>(&h);
-    L[v2] = *reinterpret_cast<const uint32_t*>(&l);
+  if ((V & 3) == 0) {
+    // float4 rows (V % 4 == 0: every row starts 16-B aligned), four loads in flight per lane in both
+    // passes (the second re-reads the row from L1/L2); same arithmetic as the scalar path below
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    const int V4 = V >> 2, VP4 = VP >> 2;
+    for (int j0 = lane; j0 < V4; j0 += 128) {
+      float4 t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + 32 * k;
+        t[k] = j < V4 ? __ldg(p4 + j) : make_float4(neg_inf_f(), neg_inf_f(), neg_inf_f(), neg_inf_f());
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mx = fmaxf(mx, fmaxf(fmaxf(t[k].x, t[k].y), fmaxf(t[k].z, t[k].w)));
+    }
+    mx = warp_max(mx);
+    if (lane == 0) m[row] = mx;
+    uint2* H2 = reinterpret_cast<uint2*>(H);
+    uint2* L2 = reinterpret_cast<uint2*>(L);
+    for (int j0 = lane; j0 < VP4; j0 += 128) {
+      float4 t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + 32 * k;
+        t[k] = j < V4 ? __ldg(p4 + j) : make_float4(neg_inf_f(), neg_inf_f(), neg_inf_f(), neg_inf_f());
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + 32 * k;
+        if (j < VP4) {
+          const float e0 = __expf(t[k].x - mx), e1 = __expf(t[k].y - mx);
+          const float e2 = __expf(t[k].z - mx), e3 = __expf(t[k].w - mx);
+          esum += (e0 + e1) + (e2 + e3);
+          const __nv_bfloat162 h01 = __floats2bfloat162_rn(e0, e1), h23 = __floats2bfloat162_rn(e2, e3);
+          const __nv_bfloat162 l01 = __floats2bfloat162_rn(e0 - __low2float(h01), e1 - __high2float(h01));
+          const __nv_bfloat162 l23 = __floats2bfloat162_rn(e2 - __low2float(h23), e3 - __high2float(h23));
+          H2[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+          L2[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+        }
+      }
+    }
+  } else {
+    for (int v = lane; v < V; v += 32) mx = fmaxf(mx, p[v]);
+    mx = warp_max(mx);
+    if (lane == 0) m[row] = mx;
+    for (int v2 = lane; v2 < VP / 2; v2 += 32) {
+      const int v = 2 * v2;
+      const float e0 = v < V ? __expf(p[v] - mx) : 0.f;
+      const float e1 = v + 1 < V ? __expf(p[v + 1] - mx) : 0.f;
+      esum += e0 + e1;
+      const __nv_bfloat162 h = __floats2bfloat162_rn(e0, e1);
+      const __nv_bfloat162 l = __floats2bfloat162_rn(e0 - __low2float(h), e1 - __high2float(h));
+      H[v2] = *reinterpret_cast<const uint32_t*>(&h);
+      L[v2] = *reinterpret_cast<const uint32_t*>(&l);
+    }
   }
   if (lse) {   // lm rows: log sum_v exp lm[u,v] (the LM-only log-softmax of Eq. 14)
     esum = warp_sum(esum);
@@ -81,14 +124,20 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   }
   if (which == 0) {
     float* ay = amy + ((size_t)n * rows_per_n + r) * UPa;
-    for (int u = lane; u <= Un; u += 32) {
-      float val = 0.f;
-      if (u < Un) {
-        long long y = sym[(size_t)n * U + u];
-        y = y < 0 ? 0 : (y >= V ? V - 1 : y);        // address safety; bad symbols flagged in status
-        val = p[y];
+    for (int u0 = lane; u0 <= Un; u0 += 128) {     // 4 labels, then 4 gathers, in flight per lane
+      long long y[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int u = u0 + 32 * k;
+        y[k] = u < Un ? sym[(size_t)n * U + u] : 0;
+        y[k] = y[k] < 0 ? 0 : (y[k] >= V ? V - 1 : y[k]);   // address safety; bad symbols flagged in status
       }
-      ay[u] = val;
+      float val[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) val[k] = u0 + 32 * k < Un ? p[y[k]] : 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (u0 + 32 * k <= Un) ay[u0 + 32 * k] = val[k];
     }
   }
 }

@@ -109,6 +109,8 @@ def test_stagewise_parity(cfg):
     dict(T=[70, 66], U=[40, 2], V=300, J=24, S=1),        # S = 1 (U=40 infeasible, U=2 infeasible)
     dict(T=[7, 30], U=[20, 9], V=11, J=8, S=3),           # U=20 > T(S-1)=14 infeasible
     dict(T=[300, 129], U=[257, 60], V=40, J=16, S=6),     # U+1 > 256: multi-warp recursion
+    dict(T=[90, 41], U=[70, 12], V=65, J=16, S=7),        # runtime-S scan (SMAX 8), cluster of 2
+    dict(T=[60, 33], U=[150, 20], V=65, J=16, S=20),      # runtime-S scan (SMAX 32), cluster of 4
 ])
 def test_edge_cases(case):
     b = synth.make_custom(case["T"], case["U"], case["V"], case["J"], case["S"], seed=11, logit_scale=2.0)

@@ -34,15 +34,31 @@ struct GradSrc {
 // dz for the 8 logits v = vc..vc+7 of one row, from the packed bf16 P~ chunk `pv`, the row's
 // scale s, the picks gbs = gs g_b (v = 0) and gls = gs g_l (v = label `info`).  Returns the bf16
 // chunk and adds the bf16-rounded values (what the MMA consumes) to fsum when given.
-__device__ __forceinline__ uint4 dz_chunk(uint4 pv, float s, float gbs, float gls, int info, int vc, float* fsum) {
-  // branch-free: the blank pick is warp-uniform (vc), the label pick a per-lane select
+__device__ __forceinline__ uint4 dz_chunk(uint4 pv, float s, float gbs, float gls, int info, int vc, float* fsum,
+                                         bool rare = false) {
+  // The blank pick is warp-uniform (vc).  The label pick: a compare and select on every element, or,
+  // when `rare` (large V: a row's label falls in one of V/8 chunks, so the branch is almost never
+  // taken), a per-lane branch (measured: c4 dW 2144 -> 2020 us; at V = 500 the branch costs more)
   const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
   const int li = info - vc;
   float g[8];
+  if (rare) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    g[2 * i] = s * __uint_as_float(w[i] << 16) - (li == 2 * i ? gls : 0.f);
-    g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u) - (li == 2 * i + 1 ? gls : 0.f);
+    for (int i = 0; i < 4; ++i) {
+      g[2 * i] = s * __uint_as_float(w[i] << 16);
+      g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u);
+    }
+    if ((unsigned)li < 8u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (li == k) g[k] -= gls;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      g[2 * i] = s * __uint_as_float(w[i] << 16) - (li == 2 * i ? gls : 0.f);
+      g[2 * i + 1] = s * __uint_as_float(w[i] & 0xffff0000u) - (li == 2 * i + 1 ? gls : 0.f);
+    }
   }
   if (vc == 0) g[0] -= gbs;
   uint32_t o[4];
@@ -261,6 +277,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   const DhTab* tabs_s = reinterpret_cast<const DhTab*>(smem + TAB_OFF);
   uint8_t* hbuf = smem + H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool rare = NTW == 8;      // dz_chunk label pick by branch: the 8-producer variant runs at V >= 2048
   const int S = p.S, F = p.F, RT = p.rt;
   const bool generic = p.dpre_out != nullptr;
   const long long NT = (long long)p.N * p.T;
@@ -399,7 +416,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < CPT; ++c)
           *reinterpret_cast<uint4*>(sa + sw128(rl, c_lo + c)) =
-              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + (c_lo + c) * 8, nullptr) : make_uint4(0, 0, 0, 0);
+              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + (c_lo + c) * 8, nullptr, rare) : make_uint4(0, 0, 0, 0);
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&full[stage]);
@@ -645,6 +662,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][128 v]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool rare = p.g.V >= 6144;     // dz_chunk label pick by branch (measured: c4 -6 %, c3 (Zipf labels) +5 %)
   const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
   const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
   const long long kb0 = (long long)split * p.kb_per_split;
@@ -706,7 +724,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
         const int rl = g8 + 8 * i;
         const int info = __float_as_int(sr[i].w);
         *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) =
-            info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, v0 + c * 8, want_db ? dsum : nullptr)
+            info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, v0 + c * 8, want_db ? dsum : nullptr, rare)
                       : make_uint4(0, 0, 0, 0);
       }
       tc::fence_proxy_async();
@@ -847,6 +865,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][256 v]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool rare = p.g.V >= 6144;     // dz_chunk label pick by branch (measured: c4 -6 %, c3 (Zipf labels) +5 %)
   const bool jfirst = p.pfmode & 2;      // grid x = j tile (siblings sharing P~ adjacent)
   const int bvx = jfirst ? blockIdx.y : blockIdx.x, bjy = jfirst ? blockIdx.x : blockIdx.y;
   const int v0 = bvx * 2 * BM, j0 = bjy * BN, split = blockIdx.z;
@@ -907,7 +926,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
           const int rl = g8 + 8 * i;
           const int info = __float_as_int(sr[i].w);
           *reinterpret_cast<uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7)) =
-              info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, va + c * 8, want_db ? dsum : nullptr)
+              info >= 0 ? dz_chunk(pv[i], sr[i].x, sr[i].y, sr[i].z, info, va + c * 8, want_db ? dsum : nullptr, rare)
                         : make_uint4(0, 0, 0, 0);
         }
         tc::fence_proxy_async();

@@ -564,7 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(temptyL + acc * 8);
+        if (lane == 0) tc::mbar_arrive_remote(temptyL + acc * 8);
         if (have) {
           tc::fence_proxy_async();
           asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");

@@ -41,26 +41,35 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                              int splits, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
-// One CTA per frame (n, t), one thread per (slot s, 8-column group) of its S band rows (blockDim =
-// S * J/8 rounded up to a warp, looping only when that exceeds 1024): 16 B of bf16 out per thread;
-// enc[t] is read once per frame and reused from L1 across the S rows.  Rows of padded frames and
-// masked slots are written as zeros (the joiner GEMMs read whole 128-row tiles).
+// Block (J/8, FPB): thread (x, y) owns the 8 columns 8x of frame blockIdx.x * FPB + y and walks its
+// S band rows, so enc[t] is loaded once per thread and the per-frame index work (ranges, lengths,
+// row addresses) is paid once per S rows instead of per 16-B output (the kernel is issue-bound on
+// the accurate tanh; the division-based (slot, column) split cost a third of its instructions).
+// Rows of padded frames and masked slots are written as zeros (the joiner GEMMs read whole
+// 128-row tiles).
 __global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
                                                      const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
-                                                     int T, int U, int J, int S, uint16_t* __restrict__ h) {
-  const int nt = blockIdx.x;
-  const int n = nt / T, t = nt - n * T;
+                                                     int N, int T, int U, int J, int S, uint16_t* __restrict__ h) {
+  const long long nt = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+  if (nt >= (long long)N * T) return;
+  const int n = (int)(nt / T), t = (int)(nt - (long long)n * T);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const int j0 = threadIdx.x * 8;
+  const bool live = t < Tn;
+  const int p = live ? ranges[nt] : 0;
+  float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
+  if (live) {
+    const float* e = enc + nt * J + j0;
+    e0 = __ldg(reinterpret_cast<const float4*>(e));
+    e1 = __ldg(reinterpret_cast<const float4*>(e + 4));
+  }
+  const float* dbase = dec + ((size_t)n * (U + 1) + p) * J + j0;
+  uint4* out = reinterpret_cast<uint4*>(h + (size_t)nt * S * J + j0);
   const int J8 = J / 8;
-  const int p = t < Tn ? ranges[(size_t)n * T + t] : 0;
-  const float* e = enc + (size_t)nt * J;
-  for (int idx = threadIdx.x; idx < S * J8; idx += blockDim.x) {
-    const int s = idx / J8, j0 = (idx - s * J8) * 8;
-    const int u = p + s;
-    uint4 out = make_uint4(0, 0, 0, 0);
-    if (t < Tn && u <= Un) {
-      const float* d = dec + ((size_t)n * (U + 1) + u) * J + j0;
-      const float4 e0 = __ldg(reinterpret_cast<const float4*>(e + j0)), e1 = __ldg(reinterpret_cast<const float4*>(e + j0 + 4));
+  for (int s = 0; s < S; ++s) {
+    uint4 o = make_uint4(0, 0, 0, 0);
+    if (live && p + s <= Un) {
+      const float* d = dbase + (size_t)s * J;
       const float4 d0 = __ldg(reinterpret_cast<const float4*>(d)), d1 = __ldg(reinterpret_cast<const float4*>(d + 4));
       const float x[8] = {e0.x + d0.x, e0.y + d0.y, e0.z + d0.z, e0.w + d0.w,
                           e1.x + d1.x, e1.y + d1.y, e1.z + d1.z, e1.w + d1.w};
@@ -70,9 +79,9 @@ __global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ e
         const __nv_bfloat162 h2 = __floats2bfloat162_rn(tanh_fast(x[2 * q]), tanh_fast(x[2 * q + 1]));
         w[q] = *reinterpret_cast<const uint32_t*>(&h2);
       }
-      out = make_uint4(w[0], w[1], w[2], w[3]);
+      o = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    *reinterpret_cast<uint4*>(h + ((size_t)nt * S + s) * J + j0) = out;
+    out[(size_t)s * J8] = o;
   }
 }
 
@@ -563,9 +572,11 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, 
 // ------------------------------------------------------------------ host drivers
 cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, const int32_t* ranges,
                          const int64_t* bnd, uint16_t* h, cudaStream_t st) {
-  const int threads = std::min(1024, (d.S * (d.J / 8) + 31) / 32 * 32);
-  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((long long)d.N * d.T), threads, 0, st>>>(enc, dec, ranges, bnd, d.T,
-                                                                                          d.U, d.J, d.S, h));
+  const int J8 = d.J / 8;                          // J % 8 == 0 (rnnt_check_dims)
+  const int fpb = std::max(1, 256 / J8);           // frames per block
+  const long long NT = (long long)d.N * d.T;
+  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((NT + fpb - 1) / fpb), dim3(J8, fpb), 0, st>>>(
+      enc, dec, ranges, bnd, d.N, d.T, d.U, d.J, d.S, h));
   return cudaGetLastError();
 }
 

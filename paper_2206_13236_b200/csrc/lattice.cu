@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
   const double L2 = Ltot[n] * RNNT_LOG2E;
   const bool finite = isfinite(L2);
   const int U1 = U + 1;
+  const int lsw = 31 - __clz(SW);
   if (threadIdx.x < 32 * lat::MAXW) {
     const int kr = threadIdx.x / lat::MAXW, w = threadIdx.x % lat::MAXW;
     const int k = k0 + kr;
@@ -371,9 +372,9 @@ __global__ void __launch_bounds__(256) combine_kernel(
         if (u >= UP) break;
         float yv = 0.f, bv = 0.f;
         if (u >= ulo && u <= uhi) {
-          const int w = u / SW;
+          const int w = u >> lsw;                 // SW = 32 R is a power of two
           bv = ex2_approx(a[i] + xy[i].y + b0[i] + s_ob[kr][w]);
-          if (u < Un) yv = ex2_approx(a[i] + xy[i].x + b1[i] + ((u % SW == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+          if (u < Un) yv = ex2_approx(a[i] + xy[i].x + b1[i] + (((u & (SW - 1)) == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
         }
         Ys[kr * UP + u] = yv;
         Bs[kr * UP + u] = bv;

@@ -360,11 +360,20 @@ def main():
         return run_full(args)
     import torch
     import paper_2206_13236_b200 as R
+    # RNNT_BENCH_FUNCTIONAL_DIST=1 (tests only, never a measurement): every rank on cuda:0 and gloo for
+    # the exchange, to exercise the N > 1 code path (sharding, the d_w stream hook, max-over-ranks
+    # timing, rank-0 output) on a one-GPU box
+    functional = os.environ.get("RNNT_BENCH_FUNCTIONAL_DIST") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     cfg, b, name = workload(args, world, rank)
     dev = R.batch_to_device(b, "cuda")

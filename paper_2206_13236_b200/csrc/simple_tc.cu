@@ -615,10 +615,12 @@ struct NormProb {
       __syncwarp();
       // diagonal-major write of the arcs and of 1/S: for diagonal k = t0w + u0 + d, lane l holds
       // column u0 + l (t = k - u)
+      // iteration i: lanes l <= i write diagonal t0w + u0 + i, lanes l > i diagonal t0w + u0 + i + 32
+      // (two contiguous runs per store), so every lane writes a cell in each of 32 iterations
       const int u = u0 + e.lane;
-      for (int d = 0; d < 63; ++d) {
-        const int tl_ = d - e.lane, tt = t0w + tl_;
-        if (tl_ >= 0 && tl_ < 32 && tt < Tn && u <= Un) {
+      for (int i = 0; i < 32; ++i) {
+        const int tl_ = e.lane <= i ? i - e.lane : i + 32 - e.lane, tt = t0w + tl_;
+        if (tt < Tn && u <= Un) {
           const size_t o = (nbase + tt + u) * LU + u;
           pxy[o] = bxy[tl_][e.lane];
           rS[o] = brs[tl_][e.lane];

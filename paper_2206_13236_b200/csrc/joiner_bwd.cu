@@ -566,10 +566,11 @@ __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restri
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
                                                          int F, int J, const float* __restrict__ part,
                                                          float* __restrict__ d_dec) {
-  // one warp per (n, u, 128-column group): each warp's chain of dependent loads (lengths and
+  // one warp per (n, u, 256-column group): each warp's chain of dependent loads (lengths and
   // coverage, the band offsets of the contributing tiles, their partial rows) is a few round trips,
   // and the column groups of one u run in parallel instead of one after another in one warp
-  const int J4 = J / 4, NG = (J4 + 127) / 128;
+  constexpr int GW = 64;                        // float4 columns per warp
+  const int J4 = J / 4, NG = (J4 + GW - 1) / GW;
   const long long w = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= (long long)N * (U + 1) * NG) return;
@@ -578,8 +579,8 @@ __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restri
   const int n = (int)(nu / (U + 1)), u = (int)(nu - (long long)n * (U + 1));
   const int2 cov = urange[nu];
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J) + jg * 128;
-  const int jn = min(128, J4 - jg * 128);       // float4 columns of this group
+  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J) + jg * GW;
+  const int jn = min(GW, J4 - jg * GW);       // float4 columns of this group
   if (u > Un || (long long)Un > (long long)Tn * (S - 1)) {
     for (int j = lane; j < jn; j += 32) dst[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
@@ -590,18 +591,18 @@ __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restri
   const int32_t* pr = ranges + (size_t)n * T;
   const int tb0 = (int)((k0 + 1) * F - gbase);                     // first frame of tile k0 + 1
   const float4* first = reinterpret_cast<const float4*>(part + (((size_t)k0 * 2 + 1) * S + (u - pr[tb0])) * J) +
-                        jg * 128;
-  float4 acc[4];
+                        jg * GW;
+  float4 acc[GW / 32];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < GW / 32; ++q) {
     const int j = lane + 32 * q;
     acc[q] = j < jn ? first[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (long long k = k0 + 1; k <= k1; ++k) {
     const int ta = (int)(k * F - gbase);
-    const float4* src = reinterpret_cast<const float4*>(part + (((size_t)k * 2 + 0) * S + (u - pr[ta])) * J) + jg * 128;
+    const float4* src = reinterpret_cast<const float4*>(part + (((size_t)k * 2 + 0) * S + (u - pr[ta])) * J) + jg * GW;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < GW / 32; ++q) {
       const int j = lane + 32 * q;
       if (j < jn) {
         const float4 x = src[j];
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restri
     }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < GW / 32; ++q) {
     const int j = lane + 32 * q;
     if (j < jn) dst[j] = acc[q];
   }
@@ -1065,7 +1066,7 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   else
     RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<4><<<grid, jdh::Roles<4>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
   if (d_dec)
-    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() * ((d.J / 4 + 127) / 128) + 7) / 8),
+    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() * ((d.J / 4 + 63) / 64) + 7) / 8),
                                                   256, 0, st>>>(
         ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, part, d_dec));
   return cudaGetLastError();

@@ -54,6 +54,11 @@ static const char* const kNames[KID_COUNT] = {
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
     "full_dgrad"};
 
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 const char* kernel_name(int id) { return (id >= 0 && id < KID_COUNT) ? kNames[id] : "unknown"; }
 
 void launch_begin(int id, cudaStream_t st) {
@@ -326,11 +331,14 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
   return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream));
 }
 
-/* diagnostics (not in rnnt.h): per-CTA phase timestamps of the simple-loss GEMMs into buf */
+#ifdef RNNT_DIAGNOSTICS
+/* diagnostics builds only (-DRNNT_DIAGNOSTICS, not in rnnt.h): per-CTA phase timestamps of the
+   simple-loss GEMMs, joiner_dh and the pruned scan into buf (process-global, never in the product) */
 void rnnt_debug_timeline(void* buf) {
   rnnt::set_timeline(buf);
   rnnt::set_dh_trace(buf ? static_cast<char*>(buf) + (4u << 20) : nullptr);   // joiner_dh trace 4 MiB in
   rnnt::set_scan_trace(buf ? static_cast<char*>(buf) + (6u << 20) : nullptr); // pruned scan trace 6 MiB in
 }
+#endif
 
 }  // extern "C"

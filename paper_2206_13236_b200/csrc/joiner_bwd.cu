@@ -236,8 +236,12 @@ __global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restric
 
 // diagnostics: per (CTA, item) timestamps {producer start, first MMA, last MMA commit, epilogue
 // start (accumulator full), epilogue end}; 16 items per CTA
+#ifdef RNNT_DIAGNOSTICS
 __device__ unsigned long long* g_dh_trace = nullptr;
 void set_dh_trace(void* buf) { cudaMemcpyToSymbol(g_dh_trace, &buf, sizeof(buf)); }
+#else
+constexpr unsigned long long* g_dh_trace = nullptr;   // product build: tracing compiled out
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -560,7 +564,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
 
 // d_dec for the token positions whose covering frames span several tiles (sum of the boundary
 // partials in tile order), and zeros for u > U_n / infeasible utterances.  Positions complete in
-// one tile were written by joiner_dh_tc_kernel and are left untouched.  One warp per (n, u).
+// one tile were written by joiner_dh_tc_kernel and are left untouched.  One warp per (n, u, 256-column group).
 __global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restrict__ ranges,
                                                          const int2* __restrict__ urange,
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
@@ -1042,12 +1046,8 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(joiner_dh_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
-    cudaFuncSetAttribute(joiner_dh_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
-    attr = true;
-  }
+  smem_optin(joiner_dh_tc_kernel<4>, jdh::SMEM_BYTES);
+  smem_optin(joiner_dh_tc_kernel<8>, jdh::SMEM_BYTES);
   const int F = d.dh_frames();
   const long long ntiles = d.dh_tiles();
   cudaMemsetAsync(nlive, 0, sizeof(int), st);
@@ -1056,10 +1056,11 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
                    static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0, F * d.S, nullptr};
-  if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);
+#ifdef RNNT_DIAGNOSTICS
+  if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);   // skips epilogue parts: wrong results, timing only
+#endif
   p.w3 = w3;
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nsm = current_sm_count();
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
   if (p.nkb >= 32)
     RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
@@ -1085,13 +1086,12 @@ cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(joiner_dh_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
-  cudaFuncSetAttribute(joiner_dh_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, jdh::SMEM_BYTES);
+  smem_optin(joiner_dh_tc_kernel<4>, jdh::SMEM_BYTES);
+  smem_optin(joiner_dh_tc_kernel<8>, jdh::SMEM_BYTES);
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
                    nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out, w3};
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nsm = current_sm_count();
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
   if (p.nkb >= 32)
     RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
@@ -1112,35 +1112,23 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   // CTA pairs (cta_group::2, V tiles rounded up to an even count) only when RNNT_DW_PAIR=1: parity-green
   // but measured slower (c2 87.6 vs 69.6 us, c4 4.42 vs 3.22 ms) -- the per-stage cross-CTA handshake
   // (remote arrive + cluster-scope acquire) costs more than the halved h traffic saves at 2-3 stages
-  static int pair = -1;
-  if (pair < 0) {
-    const char* e = getenv("RNNT_DW_PAIR");
-    pair = (e && atoi(e) == 1) ? 1 : 0;
-  }
+  static const int pair = env_int("RNNT_DW_PAIR", 0) == 1;
   if (dw_wide(d)) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(joiner_dw_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jdw2::SMEM_BYTES);
-      attr = true;
-    }
+    smem_optin(joiner_dw_wide_kernel, jdw2::SMEM_BYTES);
     CUtensorMap tp3, th3;
     if (!make_tmap_bf16_3d(&tp3, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw2::BK, 4))
       return cudaErrorInvalidValue;
     p.h3 = d.J % 64 == 0;
     if (p.h3 && !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4))
       return cudaErrorInvalidValue;
-    if (const char* e = getenv("RNNT_DW_PF")) p.pf = atoi(e);
-    if (const char* e = getenv("RNNT_DW_PFMODE")) p.pfmode = atoi(e);
+    static const int pf = env_int("RNNT_DW_PF", -1), pfmode = env_int("RNNT_DW_PFMODE", -1);
+    if (pf >= 0) p.pf = pf;
+    if (pfmode >= 0) p.pfmode = pfmode;
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
     RNNT_LAUNCH(KID_DW, st, joiner_dw_wide_kernel<<<grid, jdw2::THREADS, jdw2::SMEM_BYTES, st>>>(tp3, p.h3 ? th3 : th, p));
   } else if (pair) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(joiner_dw_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           jdw::Cfg<true>::SMEM_BYTES);
-      attr = true;
-    }
+    smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)((vt + 1) / 2 * 2), (d.J + jdw::BN - 1) / jdw::BN, splits);
     cfg.blockDim = dim3(jdw::THREADS);
@@ -1155,12 +1143,7 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     cfg.numAttrs = 1;
     RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_tc_kernel<true>, tp, th, p));
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(joiner_dw_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           jdw::Cfg<false>::SMEM_BYTES);
-      attr = true;
-    }
+    smem_optin(joiner_dw_tc_kernel<false>, jdw::Cfg<false>::SMEM_BYTES);
     dim3 grid(vt, (d.J + jdw::BN - 1) / jdw::BN, splits);
     CUtensorMap tp3, th3;
     p.h3 = d.J % 64 == 0;

@@ -620,31 +620,20 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   const int ntiles = (int)((R + jf::BM - 1) / jf::BM);
   JoinerFwdParams p{w.bias, w.bmax, w.rowinfo, w.tlive, w.tcounter, R, ntiles, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN,
                     (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2, 0};
-  if (const char* e = getenv("RNNT_DBG_FWD")) p.dbg = atoi(e);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(joiner_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jf::SMEM_BYTES);
-    attr = true;
-  }
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  static int pair = -1;
-  if (pair < 0) {
-    const char* e = getenv("RNNT_FWD_PAIR");
-    pair = e ? atoi(e) : 1;
-  }
+#ifdef RNNT_DIAGNOSTICS
+  if (const char* e = getenv("RNNT_DBG_FWD")) p.dbg = atoi(e);  // skips parts of the step: wrong results, timing only
+#endif
+  const int nsm = current_sm_count();
+  static const int pair = env_int("RNNT_FWD_PAIR", 1);
   if (pair) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(joiner_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, jf2::SMEM_BYTES);
-      attr2 = true;
-    }
+    smem_optin(joiner_fwd_pair_kernel, jf2::SMEM_BYTES);
     // persistent: one CTA per SM, in pairs (at most one cluster per row-tile pair); the pair counter is
     // the row-tile counter rowinfo_kernel zeroes
     const unsigned grid = (unsigned)(2 * std::min((ntiles + 1) / 2, nsm / 2));
     RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_pair_kernel<<<grid, jf2::THREADS, jf2::SMEM_BYTES, st>>>(ta, tb, tp, p));
     return cudaGetLastError();
   }
+  smem_optin(joiner_fwd_tc_kernel, jf::SMEM_BYTES);
   const unsigned grid = (unsigned)std::min(ntiles, nsm);   // persistent: one CTA per SM
   RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, tp, p));
   return cudaGetLastError();

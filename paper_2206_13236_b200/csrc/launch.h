@@ -18,6 +18,23 @@ enum KernelId {
 };
 
 const char* kernel_name(int id);
+
+// Per-device launch setup: the SM count of the CURRENT device, and the dynamic shared-memory
+// opt-in set on every launch (cheap, thread-safe, and right for whichever device the caller's
+// stream belongs to -- no process-global "done once" flags).
+inline int current_sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+template <class K>
+inline void smem_optin(K* fn, int bytes) {
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+// A/B switches (RNNT_FWD_PAIR, RNNT_DW_WIDE, ...): read once per process (thread-safe static
+// initialisation at the call site), defaults are the measured best.
+int env_int(const char* name, int dflt);
 void launch_begin(int id, cudaStream_t st);
 void launch_end(int id, cudaStream_t st);
 

@@ -180,8 +180,12 @@ __device__ __forceinline__ uint32_t cluster_dim_x() {
   return r;
 }
 // diagnostics: per (utterance, direction) CTA timestamps {start, staged, phase A, phase B, phase C}
+#ifdef RNNT_DIAGNOSTICS
 __device__ unsigned long long* g_scan_trace = nullptr;
 void set_scan_trace(void* buf) { cudaMemcpyToSymbol(g_scan_trace, &buf, sizeof(buf)); }
+#else
+constexpr unsigned long long* g_scan_trace = nullptr;   // product build: tracing compiled out
+#endif
 __device__ __forceinline__ void scan_trace(int k) {
   if (g_scan_trace && threadIdx.x == 0 && blockIdx.x % max(1u, (unsigned)cluster_dim_x()) == 0) {
     unsigned long long t;

@@ -360,7 +360,11 @@ struct Epi {
   uint32_t taddr;   // TMEM address of this thread's lane, column 0
 };
 
+#ifdef RNNT_DIAGNOSTICS
 __device__ unsigned long long* g_timeline = nullptr;   // diagnostics: per-CTA phase timestamps
+#else
+constexpr unsigned long long* g_timeline = nullptr;     // product build: tracing compiled out
+#endif
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -903,11 +907,7 @@ struct LmProb {
 // ------------------------------------------------------------------ host
 template <class P>
 static cudaError_t launch_gemm3(const P& p, dim3 grid, const Maps& mp, int kid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm3_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, sg::SMEM_BYTES);
-    attr = true;
-  }
+  smem_optin(gemm3_kernel<P>, sg::SMEM_BYTES);
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return cudaSuccess;
   RNNT_LAUNCH(kid, st, gemm3_kernel<P><<<grid, sg::THREADS, sg::SMEM_BYTES, st>>>(mp, p));
   return cudaGetLastError();
@@ -918,7 +918,9 @@ static bool tm3(CUtensorMap* m, const uint16_t* base, int pitch, int rows, int N
                            (uint64_t)pitch * rows * 2, 64, (uint32_t)box_rows);
 }
 
+#ifdef RNNT_DIAGNOSTICS
 void set_timeline(void* buf) { cudaMemcpyToSymbol(g_timeline, &buf, sizeof(buf)); }
+#endif
 
 cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
                                const int64_t* bnd, int32_t* status, cudaStream_t st) {

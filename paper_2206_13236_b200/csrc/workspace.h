@@ -113,11 +113,7 @@ struct PrunedWS {
 // K11 variant: "wide" CTAs (one per SM) hold two V tiles (256 v x 256 j, 512 TMEM columns) so each
 // h k-block feeds two MMAs; used for large V (L2 -> SM bound), RNNT_DW_WIDE=0/1 forces it off/on.
 inline bool dw_wide(const Dims& d) {
-  static int force = -2;
-  if (force == -2) {
-    const char* e = getenv("RNNT_DW_WIDE");
-    force = e ? atoi(e) : -1;
-  }
+  static const int force = env_int("RNNT_DW_WIDE", -1);
   if (force >= 0) return force == 1;
   return true;   // measured: c2 65.5 vs 68.6 us, c3 339 vs 593, c4 2113 vs 3234 (the 128-v variant with 2D boxes)
 }

@@ -1,4 +1,5 @@
 """Diagnostics: per-(CTA, item) timestamps of the persistent joiner_dh kernel on config 2."""
+# needs the diagnostics build: make -C paper_2206_13236_b200 diag; RNNT_LIB=paper_2206_13236_b200/librnnt_b200_diag.so
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

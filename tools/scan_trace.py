@@ -1,4 +1,5 @@
 """Diagnostics: phase timestamps of the pruned scan kernel (one CTA per utterance and direction):
+# needs the diagnostics build: make -C paper_2206_13236_b200 diag; RNNT_LIB=paper_2206_13236_b200/librnnt_b200_diag.so
 staging, A (chunk matrices), B (boundary chain), C (frames).
 
     python tools/scan_trace.py <config>"""

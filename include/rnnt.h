@@ -227,6 +227,44 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
                                                void* stream);
 
 /*
+ * Data-parallel exchange.  The only cross-GPU reduction of a step is the sum of
+ * d_w, d_b and the two batch losses over ranks.  A caller keeps them in one flat fp32 buffer
+ *   acc = [ d_w (V*J) | d_b (V) | loss sums (2) ]
+ * and chooses how each contribution reaches it:
+ *   RNNT_EXCHANGE_STORE     plain stores (this rank's values; an all_reduce, e.g. NCCL, follows);
+ *   RNNT_EXCHANGE_RED       red.global.add into a device buffer the caller zeroed (several shards of
+ *                           one batch, or several launches, summed in place; fp32 addition order is
+ *                           not fixed, so results agree to rounding, not bit for bit);
+ *   RNNT_EXCHANGE_MULTIMEM  multimem.red.add on an NVLink-SHARP (NVLS) multicast address of a
+ *                           symmetric buffer: every rank's copy receives the sum over ranks inside the
+ *                           NVSwitch.  The pointers must be multicast addresses (e.g. torch symmetric
+ *                           memory's multicast_ptr); the caller zeroes the buffer before the first add
+ *                           and barriers across ranks before reading it.
+ */
+typedef enum {
+  RNNT_EXCHANGE_STORE = 0,
+  RNNT_EXCHANGE_RED = 1,
+  RNNT_EXCHANGE_MULTIMEM = 2
+} rnnt_exchange_mode_t;
+
+/* rnnt_pruned_loss_backward_weight with the reduced d_w (V,J) / d_b (V) delivered by `mode`
+ * (STORE: identical to rnnt_pruned_loss_backward_weight).  Same preconditions. */
+rnnt_status_t rnnt_pruned_loss_backward_weight_exchange(const uint16_t* h, const rnnt_dims_t* dims,
+                                                        int32_t mode, float* d_w, float* d_b,
+                                                        void* workspace, size_t workspace_bytes,
+                                                        void* stream);
+
+/* Batch loss combination (D12, D16):
+ *   out[0] = simple_scale * sum_n loss_simple[n],
+ *   out[1] = pruned_scale * sum_n loss_pruned[n] over the utterances whose status bit0 (infeasible)
+ *            is clear — an infeasible utterance's +inf stays visible in loss_pruned[n] but does not
+ *            poison the sum (status may be NULL: nothing masked).
+ * fp64 accumulation in a fixed order; delivered by `mode` as above.  N >= 1. */
+rnnt_status_t rnnt_loss_sums(const float* loss_simple, const float* loss_pruned, const int32_t* status,
+                             int32_t N, float simple_scale, float pruned_scale, int32_t mode,
+                             float* out, void* stream);
+
+/*
  * Full (unpruned) transducer loss with the same non-linear joiner (the comparison
  * class of P:44-52, P:171-176 and Tables 1-2): the band widened to every token position
  * (S = U_n + 1, all bounds 0), so the joiner runs on all (N, T, U+1) lattice nodes:

@@ -32,6 +32,10 @@ STATUS_BAD_SYMBOL = 4
 STATUS_UNDERFLOW = 8
 STATUS_BAD_BOUNDARY = 16
 
+EXCHANGE_STORE = 0      # rnnt_exchange_mode_t (include/rnnt.h)
+EXCHANGE_RED = 1
+EXCHANGE_MULTIMEM = 2
+
 
 class Dims(ctypes.Structure):
     _fields_ = [("N", ctypes.c_int32), ("T", ctypes.c_int32), ("U", ctypes.c_int32),
@@ -87,6 +91,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_pruned_loss_backward_input.restype = I32
     lib.rnnt_pruned_loss_backward_weight.argtypes = [P, DP, P, P, P, SZ, P]
     lib.rnnt_pruned_loss_backward_weight.restype = I32
+    lib.rnnt_pruned_loss_backward_weight_exchange.argtypes = [P, DP, I32, P, P, P, SZ, P]
+    lib.rnnt_pruned_loss_backward_weight_exchange.restype = I32
+    lib.rnnt_loss_sums.argtypes = [P, P, P, I32, F, F, I32, P, P]
+    lib.rnnt_loss_sums.restype = I32
     lib.rnnt_launch_count.argtypes = []
     lib.rnnt_launch_count.restype = ctypes.c_uint64
     lib.rnnt_kernel_count.argtypes = []
@@ -276,6 +284,27 @@ def rnnt_pruned_loss_backward_weight(h, dims, d_w, d_b, workspace, stream=None):
     _check(rc, "rnnt_pruned_loss_backward_weight")
 
 
+def _addr(x):
+    """A device pointer: a CUDA tensor, or a raw integer address (e.g. a multicast address)."""
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    return _ptr(x)
+
+
+def rnnt_pruned_loss_backward_weight_exchange(h, dims, mode, d_w, d_b, workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss_backward_weight_exchange(
+        _ptr(h), ctypes.byref(dims), int(mode), _addr(d_w), _addr(d_b), _ptr(workspace),
+        workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_pruned_loss_backward_weight_exchange")
+
+
+def rnnt_loss_sums(loss_simple, loss_pruned, status, N, simple_scale, pruned_scale, mode, out, stream=None):
+    rc = load_library().rnnt_loss_sums(_ptr(loss_simple), _ptr(loss_pruned), _ptr(status), int(N),
+                                       float(simple_scale), float(pruned_scale), int(mode), _addr(out),
+                                       _stream(stream))
+    _check(rc, "rnnt_loss_sums")
+
+
 # ----------------------------------------------------------------- conveniences
 class Workspace:
     """Caches one device workspace per (device, size)."""
@@ -329,7 +358,7 @@ def critical_stream(device=None):
 
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
          pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True,
-         lm_only_scale=0.0, am_only_scale=0.0, grad_hook=None):
+         lm_only_scale=0.0, am_only_scale=0.0, grad_hook=None, exchange=None):
     """One fwd+bwd of the whole hot path: simple loss and its
     gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
     device tensors; ``out`` may supply preallocated outputs (same keys).
@@ -341,7 +370,12 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
 
     ``grad_hook()`` (e.g. the data-parallel all_reduce of d_w / d_b / loss sums) is called once both
     losses and d_w / d_b are final: with ``overlap`` on the d_w stream right after the weight
-    gradient, so the collective overlaps the input-gradient kernels; otherwise at the end."""
+    gradient, so the collective overlaps the input-gradient kernels; otherwise at the end.
+
+    ``exchange`` (a ``dist.GradBuffer``): the data-parallel exchange.  d_w / d_b are delivered into
+    its flat buffer by the library (plain stores + NCCL all_reduce, NVLS multimem adds, or local
+    adds), the masked batch-loss sums (rnnt_loss_sums) into its tail, and ``out["d_w"]`` /
+    ``out["d_b"]`` are views of it; the reduction overlaps the input-gradient kernels."""
     dims = dims_of(am, lm, w_out, S)
     dev = am.device
     o = out if out is not None else alloc_outputs(dims, dev)
@@ -373,12 +407,25 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
         fwd(o["am_grad"], o["lm_grad"])
     rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
     rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], cur)
+    def weight_grads(s):
+        if exchange is None:
+            rnnt_pruned_loss_backward_weight(o["h"], dims, o["d_w"], o["d_b"], ws, s)
+            return
+        exchange.begin(s)
+        rnnt_loss_sums(o["loss_simple"], o["loss_pruned"], st, dims.N, simple_scale, pruned_scale,
+                       exchange.lib_mode, exchange.target("loss_sums"), s)
+        rnnt_pruned_loss_backward_weight_exchange(o["h"], dims, exchange.lib_mode, exchange.target("d_w"),
+                                                  exchange.target("d_b"), ws, s)
+        with torch.cuda.stream(s):
+            exchange.finish(s)
+        o["d_w"], o["d_b"] = exchange.d_w, exchange.d_b
+
     if overlap:
         rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
                                  o["loss_pruned"], st, ws, cur)
         side2 = _side_stream(dev, 1)
         side2.wait_stream(cur)
-        rnnt_pruned_loss_backward_weight(o["h"], dims, o["d_w"], o["d_b"], ws, side2)
+        weight_grads(side2)
         if grad_hook is not None:
             with torch.cuda.stream(side2):
                 grad_hook()
@@ -387,8 +434,15 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
         cur.wait_stream(side2)
         for t in (am, lm, o["px_grad"], o["py_grad"], o["am_grad"], o["lm_grad"], ws, symbols, boundary):
             t.record_stream(side)
-        for t in (o["h"], o["d_w"], o["d_b"], ws):
+        for t in (o["h"], o["d_w"], o["d_b"], ws, o["loss_simple"], o["loss_pruned"], st):
             t.record_stream(side2)
+    elif exchange is not None:
+        rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
+                                 o["loss_pruned"], st, ws, cur)
+        weight_grads(cur)
+        rnnt_pruned_loss_backward_input(o["h"], w_out, o["ranges"], boundary, dims, o["d_enc"], o["d_dec"], ws, cur)
+        if grad_hook is not None:
+            grad_hook()
     else:
         rnnt_pruned_loss(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
                          o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)

@@ -27,7 +27,9 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
                                     const int32_t* ranges, const int64_t* bnd, float* d_enc, float* d_dec,
                                     cudaStream_t st);
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
-                                     cudaStream_t st);
+                                     cudaStream_t st, int mode);
+cudaError_t loss_sums_launch(const float* ls, const float* lp, const int32_t* status, int N, float s_scale,
+                             float p_scale, float* out, int mode, cudaStream_t st);
 cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const float* dec, const uint16_t* W,
                              const uint16_t* b, const int64_t* sym, const int64_t* bnd, float gs, float* loss,
                              float* d_enc, float* d_dec, float* d_w, float* d_b, int32_t* status, cudaStream_t st);
@@ -52,7 +54,7 @@ static const char* const kNames[KID_COUNT] = {
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_dh_tables", "joiner_d_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
-    "full_dgrad"};
+    "full_dgrad", "loss_sums"};
 
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -328,7 +330,31 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
   SimpleWS sw;
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
-  return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream));
+  return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream, 0));
+}
+
+rnnt_status_t rnnt_pruned_loss_backward_weight_exchange(const uint16_t* h, const rnnt_dims_t* dims, int32_t mode,
+                                                        float* d_w, float* d_b, void* workspace,
+                                                        size_t workspace_bytes, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (mode < RNNT_EXCHANGE_STORE || mode > RNNT_EXCHANGE_MULTIMEM) return RNNT_ERR_INVALID_ARG;
+  if (!h || !d_w || !d_b || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(d_w)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream, mode));
+}
+
+rnnt_status_t rnnt_loss_sums(const float* loss_simple, const float* loss_pruned, const int32_t* status, int32_t N,
+                             float simple_scale, float pruned_scale, int32_t mode, float* out, void* stream) {
+  if (!loss_simple || !loss_pruned || !out || N < 1) return RNNT_ERR_INVALID_ARG;
+  if (mode < RNNT_EXCHANGE_STORE || mode > RNNT_EXCHANGE_MULTIMEM) return RNNT_ERR_INVALID_ARG;
+  return cuda_status(loss_sums_launch(loss_simple, loss_pruned, status, N, simple_scale, pruned_scale, out, mode,
+                                      (cudaStream_t)stream));
 }
 
 #ifdef RNNT_DIAGNOSTICS

@@ -31,7 +31,7 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
 cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd, float* loss, float* px_grad,
                            float* py_grad, int32_t* status, cudaStream_t st);
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
-                                     cudaStream_t st);
+                                     cudaStream_t st, int mode);
 cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
                                      const int* live, const int* nlive, long long ntiles, float* dpre_out,
                                      cudaStream_t st);
@@ -147,7 +147,7 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   if ((e = lattice_launch(df, sw, bnd, loss, pw.gl, pw.gb, status, st)) != cudaSuccess) return e;
   RNNT_LAUNCH(KID_FULL_PACK, st, full_pack_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
       pw.gb, pw.gl, pw.rowinfo, pw.mt, pw.lse, R, df.ntile(), gs, pw.gpk));
-  if ((e = pruned_bwd_weight_launch(df, pw, fw.h, d_w, d_b, st)) != cudaSuccess) return e;
+  if ((e = pruned_bwd_weight_launch(df, pw, fw.h, d_w, d_b, st, 0)) != cudaSuccess) return e;
   if (d_enc || d_dec) {
     const long long ntiles = (R + 127) / 128;
     cudaMemsetAsync(pw.dhlive + ntiles, 0, sizeof(int), st);

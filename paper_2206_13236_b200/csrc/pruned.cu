@@ -703,12 +703,23 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   return cudaGetLastError();
 }
 
-// Backward to the joiner weights: K11 dW (split-K) + db, deterministic split reduction.
+cudaError_t split_reduce_acc_launch(const float* part, int splits, long long M, float* out, int mode, int kid,
+                                    cudaStream_t st);
+
+// Backward to the joiner weights: K11 dW (split-K) + db, deterministic split reduction.  mode > 0: the
+// reduced d_w / d_b are ADDED into the targets (exchange.cu: red.global.add, or multimem.red.add on an
+// NVLS multicast address).
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, int mode) {
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
+  if (mode != 0) {
+    if ((e = split_reduce_acc_launch(w.dWp, w.splits, (long long)d.V * d.J, d_w, mode, KID_DW_REDUCE, st)) !=
+        cudaSuccess)
+      return e;
+    return split_reduce_acc_launch(w.dbp, w.splits, d.V, d_b, mode, KID_DB_REDUCE, st);
+  }
   const long long M = (long long)d.V * d.J;
   if (M % 4 == 0 && reinterpret_cast<uintptr_t>(d_w) % 16 == 0)
     RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce4_kernel<<<(unsigned)((M / 4 + 255) / 256), 256, 0, st>>>(
@@ -726,7 +737,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
   cudaError_t e;
   if ((e = pruned_fwd_launch(d, w, h, W, b, sym, ranges, bnd, gs, loss, status, st)) != cudaSuccess) return e;
   if ((e = pruned_bwd_input_launch(d, w, h, W, ranges, bnd, d_enc, d_dec, st)) != cudaSuccess) return e;
-  return pruned_bwd_weight_launch(d, w, h, d_w, d_b, st);
+  return pruned_bwd_weight_launch(d, w, h, d_w, d_b, st, 0);
 }
 
 }  // namespace rnnt

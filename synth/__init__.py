@@ -175,8 +175,9 @@ def make_batch(config: int, rank: int = 0, seed: int | None = None, poison: bool
                  w_out_bits=f32_to_bf16_bits(W), b_out_bits=f32_to_bf16_bits(b))
 
 
-def make_custom(T_n, U_n, V, J, S, seed=0, logit_scale=1.0, poison=False) -> Batch:
-    """Arbitrary-shape batch for edge-case tests (same draw order as make_batch)."""
+def make_custom(T_n, U_n, V, J, S, seed=0, logit_scale=1.0, poison=False, joiner_scale=1.0) -> Batch:
+    """Arbitrary-shape batch for edge-case tests (same draw order as make_batch).  ``logit_scale``
+    multiplies am / lm, ``joiner_scale`` W_out / b_out (peaky, trained-like lattices)."""
     rng = np.random.Generator(np.random.PCG64(seed))
     T_n = np.asarray(T_n, np.int64)
     U_n = np.asarray(U_n, np.int64)
@@ -199,8 +200,8 @@ def make_custom(T_n, U_n, V, J, S, seed=0, logit_scale=1.0, poison=False) -> Bat
     for n in range(N):
         dec[n, :U_n[n] + 1] = rng.standard_normal((int(U_n[n]) + 1, J), dtype=np.float32)
     a = math.sqrt(6.0 / (J + V))
-    W = rng.uniform(-a, a, size=(V, J)).astype(np.float32)
-    b = rng.uniform(-a, a, size=(V,)).astype(np.float32)
+    W = (joiner_scale * rng.uniform(-a, a, size=(V, J))).astype(np.float32)
+    b = (joiner_scale * rng.uniform(-a, a, size=(V,))).astype(np.float32)
     boundary = np.zeros((N, 4), np.int64)
     boundary[:, 2] = U_n
     boundary[:, 3] = T_n

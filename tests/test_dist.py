@@ -29,7 +29,7 @@ def _global_batch():
 
 def _rank_sums(b, idx):
     from paper_2206_13236_b200.dist import GradBuffer
-    buf = GradBuffer(b.V, b.J, "cpu")
+    buf = GradBuffer(b.V, b.J, "cpu", mode="local")
     ls, lp = [], []
     for n in idx:
         d = b.utterance(int(n))
@@ -40,8 +40,9 @@ def _rank_sums(b, idx):
         lp.append(r["loss"])
         buf.d_w += torch.from_numpy(r["d_w"]).float()
         buf.d_b += torch.from_numpy(r["d_b"]).float()
-    buf.set_losses(torch.tensor(ls, dtype=torch.float32) if ls else torch.zeros(0),
-                   torch.tensor(lp, dtype=torch.float32) if lp else torch.zeros(0))
+    # the loss combination of P:318-323 (on the GPU path: the library's rnnt_loss_sums)
+    buf.loss_sums[0] = 0.5 * float(np.sum(ls))
+    buf.loss_sums[1] = 1.0 * float(np.sum([x for x in lp if np.isfinite(x)]))
     return buf
 
 

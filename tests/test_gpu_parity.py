@@ -7,8 +7,8 @@ import pytest
 
 import oracle as O
 import synth
-from gpu_common import (OCC_ATOL, assert_bf16_grad, assert_close_abs, assert_loss, oracle_h_bits,
-                        run_prune, run_pruned, run_ranges, run_simple, to_dev)
+from gpu_common import (H_FLIP_MAX, OCC_ATOL, assert_bf16_grad, assert_close_abs, assert_loss, h_flip_rate,
+                        oracle_h_bits, worst_abs_above_one, run_prune, run_pruned, run_ranges, run_simple, to_dev)
 
 pytestmark = pytest.mark.gpu
 
@@ -65,6 +65,8 @@ def check_simple(b):
     assert_close_abs(g["py_grad"], o["py_grad"], OCC_ATOL, "py_grad")
     assert_close_abs(g["am_grad"], o["am_grad"], OCC_ATOL, "am_grad")
     assert_close_abs(g["lm_grad"], o["lm_grad"], OCC_ATOL, "lm_grad")
+    print(f"worst |d| on |ref|>1 entries (N={b.N} V={b.V}): am_grad "
+          f"{worst_abs_above_one(g['am_grad'], o['am_grad']):.2e}, lm_grad {worst_abs_above_one(g['lm_grad'], o['lm_grad']):.2e}")
     return g, o
 
 
@@ -77,12 +79,18 @@ def check_ranges(b, o):
     return ref
 
 
-def check_prune(b, ranges):
+def check_prune(b, ranges, case=""):
     h = run_prune(b, ranges)
     ref = oracle_h_bits(b, ranges)
-    diff = h.astype(np.int32) - ref.astype(np.int32)
-    assert np.abs(diff).max() <= 1, "h differs by more than one bf16 ulp"
-    assert np.count_nonzero(diff) <= 1e-3 * diff.size, f"{np.count_nonzero(diff)} 1-ulp flips"
+    # rows outside the band / past T_n are exact zeros on both sides and count in the denominator only
+    # through the band rows: the rate is over the band rows actually computed
+    live = np.zeros(h.shape[:3], bool)
+    for n in range(b.N):
+        T, U = int(b.T_n[n]), int(b.U_n[n])
+        live[n, :T] = (ranges[n, :T, None] + np.arange(b.S)[None, :]) <= U
+    rate = h_flip_rate(h[live], ref[live], case or f"N={b.N} V={b.V} J={b.J}")
+    assert rate <= H_FLIP_MAX, f"h flip rate {rate:.2e} > {H_FLIP_MAX}"
+    assert np.array_equal(h[~live], ref[~live])
     return ref
 
 

@@ -1,0 +1,277 @@
+"""GPU tests added in round 2 (VERDICT r1 "Next round" #2):
+
+* the CUDA-graph replay that bench.py times equals the eager step bit for bit (c2, c4);
+* the data-parallel path on the CUDA kernels: the c5 shards of two ranks (a) summed in one device
+  buffer by the library's RED exchange and (b) exchanged by two processes on cuda:0 over gloo, each
+  equal to the fp64 oracle over the global batch (SURVEY 8(e) "Parity");
+* rnnt_loss_sums masks infeasible utterances (D16) and matches the oracle's loss combination;
+* device status bits 0-4 on crafted inputs;
+* a peaky, trained-like lattice (logit scale 7, joiner scale 8) at c4 lengths;
+* d_dec with several 256-column groups and a partial last group (J = 264, 520);
+* full-batch c3 d_w / d_b against the oracle (every utterance, the launch configuration of bench.py).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from gpu_common import (OCC_ATOL, assert_bf16_grad, assert_close_abs, assert_loss, oracle_h_bits, run_pruned,
+                        to_dev, worst_abs_above_one)
+
+pytestmark = pytest.mark.gpu
+
+
+def _args(dev, b):
+    return (dev["am"], dev["lm"], dev["symbols"], dev["boundary"], dev["enc_proj"], dev["dec_proj"], dev["w_out"],
+            dev["b_out"], b.S)
+
+
+# ----------------------------------------------------------------- graph replay == eager
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_graph_replay_bit_equal_to_eager(cfg):
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_batch(cfg)
+    dev = to_dev(b)
+    dims = R.make_dims(b.N, b.T, b.U, b.V, b.J, b.S)
+    ws = torch.empty(R.rnnt_workspace_bytes(dims), dtype=torch.uint8, device="cuda")
+    eager = R.alloc_outputs(dims, "cuda")
+    stream = R.critical_stream()
+    torch.cuda.set_stream(stream)
+    try:
+        R.step(*_args(dev, b), out=eager, workspace=ws)
+        torch.cuda.synchronize()
+        ref = {k: v.clone() for k, v in eager.items()}
+        outs = R.alloc_outputs(dims, "cuda")
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            R.step(*_args(dev, b), out=outs, workspace=ws)
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            outs["status"].zero_()
+            R.step(*_args(dev, b), out=outs, workspace=ws)
+        for v in outs.values():
+            v.fill_(7)                      # every output must be rewritten by the replays
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+    finally:
+        torch.cuda.set_stream(torch.cuda.default_stream())
+    for k in ref:
+        assert torch.equal(outs[k], ref[k]), f"{k}: graph replay differs from eager"
+
+
+# ----------------------------------------------------------------- data parallel
+def _oracle_global(batches, gpu_ranges=None):
+    """Oracle over the concatenated global batch: summed d_w / d_b and the masked loss sums
+    (P:318-323).  ``gpu_ranges[i]`` (optional): where the GPU's bounds differ from the oracle's only at
+    verified near-tie frames (D5), the pruned stage is evaluated at the GPU's bounds."""
+    dw, db, ls, lp = 0.0, 0.0, 0.0, 0.0
+    for i, b in enumerate(batches):
+        r = O.full_step(b)
+        dw = dw + r["d_w"]
+        db = db + r["d_b"]
+        ls += r["loss_simple"].sum()
+        for n in range(b.N):
+            d = b.utterance(n)
+            T, U = d["T"], d["U"]
+            if not O.feasible(T, U, b.S):
+                continue
+            if gpu_ranges is not None and not np.array_equal(gpu_ranges[i][n, :T], r["ranges"][n, :T]):
+                _assert_near_ties(b, n, gpu_ranges[i][n, :T], r)
+                p_old = O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"], r["ranges"][n, :T], b.S)
+                p_new = O.pruned_loss(d["enc"], d["dec"], d["W"], d["b"], d["y"],
+                                      gpu_ranges[i][n, :T].astype(np.int64), b.S)
+                dw = dw - p_old["d_w"] + p_new["d_w"]
+                db = db - p_old["d_b"] + p_new["d_b"]
+                lp += p_new["loss"]
+            else:
+                lp += r["loss_pruned"][n]
+    return dw, db, np.array([0.5 * ls, 1.0 * lp])
+
+
+def _assert_near_ties(b, n, rg, r):
+    T, U = int(b.T_n[n]), int(b.U_n[n])
+    raw_o = O.raw_bounds(r["px_grad"][n, :T, :U + 1], r["py_grad"][n, :T, :U + 1], b.S)
+    v_all = [O.bound_scores(r["px_grad"][n, t, :U + 1], r["py_grad"][n, t, :U + 1], b.S) for t in range(T)]
+    gaps = [np.sort(v)[-1] - np.sort(v)[-2] if len(v) > 1 else np.inf for v in v_all]
+    assert min(gaps) < 2 * (b.S + 1) * 1e-4, f"utt {n}: GPU ranges differ from the oracle's without a near-tie"
+
+
+def _check_global(flat, V, J, ref):
+    dw_ref, db_ref, sums_ref = ref
+    assert_bf16_grad(flat[:V * J].reshape(V, J), dw_ref, "d_w (global)")
+    assert_bf16_grad(flat[V * J:V * J + V], db_ref, "d_b (global)")
+    assert_loss(flat[V * J + V:], sums_ref, "loss sums (global)")
+
+
+def test_dp_red_exchange_two_shards_one_buffer():
+    """The c5 shards of ranks 0 and 1 run through step() one after the other on one GPU; the library's
+    RED exchange adds both into one zeroed flat buffer: d_w, d_b and the masked loss sums equal the
+    oracle over the global batch."""
+    import torch
+    import paper_2206_13236_b200 as R
+    from paper_2206_13236_b200.dist import GradBuffer
+    shards = [synth.make_batch(5, rank=r) for r in range(2)]
+    V, J = shards[0].V, shards[0].J
+    buf = GradBuffer(V, J, "cuda", mode="red")
+    buf.zero_on_begin = False
+    buf.flat.zero_()
+    gr = []
+    for b in shards:
+        dev = to_dev(b)
+        o = R.step(*_args(dev, b), exchange=buf)
+        gr.append(o["ranges"].cpu().numpy())
+        torch.cuda.synchronize()
+    flat = buf.flat.cpu().numpy().astype(np.float64)
+    _check_global(flat, V, J, _oracle_global(shards, gr))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _dp_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2206_13236_b200 as R
+    from paper_2206_13236_b200.dist import GradBuffer
+    torch.cuda.set_device(0)
+    b = synth.make_batch(5, rank=rank)
+    dev = to_dev(b)
+    buf = GradBuffer(b.V, b.J, "cuda", mode="nccl")    # library stores + one all_reduce (gloo here)
+    o = R.step(*_args(dev, b), exchange=buf)
+    torch.cuda.synchronize()
+    q.put((rank, buf.flat.cpu().numpy().copy(), o["ranges"].cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dp_two_ranks_gloo_on_one_gpu():
+    """Two processes, both on cuda:0 (their kernels never wait on each other; the exchange is a gloo
+    all_reduce), each running step() on its c5 shard with the STORE exchange: every rank ends with the
+    oracle's global d_w, d_b and loss sums."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, flat, rg = q.get(timeout=600)
+        res[r] = (flat, rg)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    shards = [synth.make_batch(5, rank=r) for r in range(2)]
+    V, J = shards[0].V, shards[0].J
+    assert np.array_equal(res[0][0], res[1][0]), "ranks disagree after the all_reduce"
+    ref = _oracle_global(shards, [res[0][1], res[1][1]])
+    _check_global(res[0][0].astype(np.float64), V, J, ref)
+
+
+def test_loss_sums_mask_infeasible():
+    import torch
+    import paper_2206_13236_b200 as R
+    ls = torch.tensor([1.5, 2.25, -3.0, 10.0], device="cuda")
+    lp = torch.tensor([4.0, float("inf"), 0.5, 1.0], device="cuda")
+    st = torch.tensor([0, 1, 0, 4], dtype=torch.int32, device="cuda")
+    out = torch.zeros(2, device="cuda")
+    R.rnnt_loss_sums(ls, lp, st, 4, 0.5, 1.0, R.EXCHANGE_STORE, out)
+    torch.cuda.synchronize()
+    assert out.tolist() == [0.5 * 10.75, 5.5]
+    R.rnnt_loss_sums(ls, lp, st, 4, 0.5, 1.0, R.EXCHANGE_RED, out)     # adds
+    torch.cuda.synchronize()
+    assert out.tolist() == [10.75, 11.0]
+
+
+# ----------------------------------------------------------------- status bits
+def test_status_bits():
+    import torch
+    import paper_2206_13236_b200 as R
+    b = synth.make_custom([12, 10, 9, 11, 8, 10], [3, 4, 2, 3, 2, 12], 16, 8, 2, seed=9)
+    b.symbols[1, 2] = 0                                   # bit2: symbol outside [1, V)
+    b.symbols[2, 0] = 16
+    b.boundary[3, 1] = 1                                  # bit4: nonzero begin_frame
+    b.am[4, :8] = np.where(np.arange(16) == 0, 0.0, -200.0)[None, :]   # bit3: normaliser underflow
+    b.lm[4, :3] = np.where(np.arange(16) == 0, -200.0, 0.0)[None, :]
+    # utterance 5: U = 12 > T (S - 1) = 10 -> bit0 infeasible
+    dev = to_dev(b)
+    o = R.step(*_args(dev, b))
+    torch.cuda.synchronize()
+    st = o["status"].cpu().numpy()
+    assert st[0] == 0, st
+    assert st[1] & R.STATUS_BAD_SYMBOL and st[2] & R.STATUS_BAD_SYMBOL, st
+    assert st[3] & R.STATUS_BAD_BOUNDARY, st
+    assert st[4] & R.STATUS_UNDERFLOW, st
+    assert st[5] & R.STATUS_INFEASIBLE, st
+    lp = o["loss_pruned"].cpu().numpy()
+    assert np.isposinf(lp[5])
+    assert np.all(o["ranges"].cpu().numpy()[5] == 0)
+    assert torch.all(o["d_enc"][5] == 0) and torch.all(o["d_dec"][5] == 0)
+    # bit1: a NaN in a valid am entry makes that utterance's loss non-finite and flags it alone
+    b2 = synth.make_custom([12, 10], [3, 4], 16, 8, 3, seed=9)
+    b2.am[1, 4, 5] = np.nan
+    o2 = R.step(*_args(to_dev(b2), b2))
+    torch.cuda.synchronize()
+    st2 = o2["status"].cpu().numpy()
+    assert st2[0] == 0 and st2[1] & R.STATUS_NONFINITE, st2
+
+
+# ----------------------------------------------------------------- peaky lattices
+def test_peaky_lattice_c4_lengths():
+    """Trained-like, peaky logits (am / lm x7, joiner weights x8) at c4 lengths (T = 1000, U = 250,
+    S = 10): the fp32 rebasing / self-normalisation of the recursions (D9, D19) against fp64."""
+    from test_gpu_parity import check_pruned, check_ranges, check_simple
+    from gpu_common import run_prune, h_flip_rate, H_FLIP_MAX
+    b = synth.make_custom([1000, 700], [250, 180], 64, 32, 10, seed=21, logit_scale=7.0, joiner_scale=8.0)
+    g, o = check_simple(b)
+    ranges = check_ranges(b, o)
+    h_ref = oracle_h_bits(b, ranges)
+    h = run_prune(b, ranges)
+    assert h_flip_rate(h, h_ref, "peaky c4 lengths") <= H_FLIP_MAX
+    check_pruned(b, ranges, h_ref)
+
+
+# ----------------------------------------------------------------- d_dec column groups
+@pytest.mark.parametrize("J", [264, 520])
+def test_ddec_multiple_column_groups(J):
+    """ddec_fixup runs a warp per (n, u, 256-column group): J = 264 / 520 give 2 / 3 groups with a
+    partial last one; long utterances make token positions span several joiner_dh tiles."""
+    from test_gpu_parity import check_pruned, check_ranges, check_simple
+    b = synth.make_custom([300, 170, 64], [90, 40, 20], 40, J, 5, seed=31, logit_scale=2.0)
+    g, o = check_simple(b)
+    ranges = check_ranges(b, o)
+    check_pruned(b, ranges, oracle_h_bits(b, ranges))
+
+
+# ----------------------------------------------------------------- c3 full batch
+def test_full_batch_c3_weight_grads():
+    """d_w / d_b over all 32 utterances of the c3 batch (V = 5000, the split count bench.py times)
+    against the oracle's pruned stage on its own ranges and h (about a minute of fp64 BLAS)."""
+    from test_gpu_parity import _oracle_pruned, _oracle_ranges, _oracle_simple
+    b = synth.make_batch(3)
+    o = _oracle_simple(b)
+    ranges = _oracle_ranges(b, o["px_grad"].astype(np.float32), o["py_grad"].astype(np.float32))
+    h_ref = oracle_h_bits(b, ranges)
+    g = run_pruned(b, h_ref, ranges)
+    ref = _oracle_pruned(b, ranges)
+    assert_loss(g["loss_pruned"], ref["loss"], "loss_pruned")
+    for k in ("d_w", "d_b", "d_enc", "d_dec"):
+        assert_bf16_grad(g[k], ref[k], k)

@@ -254,6 +254,12 @@ rnnt_status_t rnnt_pruned_loss_backward_weight_exchange(const uint16_t* h, const
                                                         void* workspace, size_t workspace_bytes,
                                                         void* stream);
 
+/* Fixed-order sum of `nparts` contiguous fp32 vectors of length M (parts[k*M + i], k ascending),
+ * delivered into out[0..M) by `mode`: e.g. the exchange buffers of several sub-batches of one step
+ * (deterministic for any nparts), or a rank's partials before a multimem exchange. */
+rnnt_status_t rnnt_exchange_sum(const float* parts, int32_t nparts, int64_t M, int32_t mode, float* out,
+                                void* stream);
+
 /* Batch loss combination (D12, D16):
  *   out[0] = simple_scale * sum_n loss_simple[n],
  *   out[1] = pruned_scale * sum_n loss_pruned[n] over the utterances whose status bit0 (infeasible)

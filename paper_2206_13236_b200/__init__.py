@@ -93,6 +93,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_pruned_loss_backward_weight.restype = I32
     lib.rnnt_pruned_loss_backward_weight_exchange.argtypes = [P, DP, I32, P, P, P, SZ, P]
     lib.rnnt_pruned_loss_backward_weight_exchange.restype = I32
+    lib.rnnt_exchange_sum.argtypes = [P, I32, ctypes.c_int64, I32, P, P]
+    lib.rnnt_exchange_sum.restype = I32
     lib.rnnt_loss_sums.argtypes = [P, P, P, I32, F, F, I32, P, P]
     lib.rnnt_loss_sums.restype = I32
     lib.rnnt_launch_count.argtypes = []
@@ -298,6 +300,11 @@ def rnnt_pruned_loss_backward_weight_exchange(h, dims, mode, d_w, d_b, workspace
     _check(rc, "rnnt_pruned_loss_backward_weight_exchange")
 
 
+def rnnt_exchange_sum(parts, nparts, M, mode, out, stream=None):
+    rc = load_library().rnnt_exchange_sum(_ptr(parts), int(nparts), int(M), int(mode), _addr(out), _stream(stream))
+    _check(rc, "rnnt_exchange_sum")
+
+
 def rnnt_loss_sums(loss_simple, loss_pruned, status, N, simple_scale, pruned_scale, mode, out, stream=None):
     rc = load_library().rnnt_loss_sums(_ptr(loss_simple), _ptr(loss_pruned), _ptr(status), int(N),
                                        float(simple_scale), float(pruned_scale), int(mode), _addr(out),
@@ -334,8 +341,8 @@ def dims_of(am, lm, w_out, S) -> Dims:
 _SIDE = {}
 
 
-def _side_stream(device, which=0):
-    key = (torch.device(device).index, which)
+def _side_stream(device, which=0, lane=0):
+    key = (torch.device(device).index, which, lane)
     if key not in _SIDE:
         _SIDE[key] = torch.cuda.Stream(device=device, priority=0)      # lowest priority: fills gaps
     return _SIDE[key]
@@ -344,21 +351,22 @@ def _side_stream(device, which=0):
 _CRIT = {}
 
 
-def critical_stream(device=None):
+def critical_stream(device=None, lane=0):
     """A high-priority stream for the step's critical path: with the side streams at the lowest
     priority the block scheduler hands idle SMs (e.g. during the latency-bound recursions) to the
-    side-stream GEMMs without delaying the critical-path kernels."""
+    side-stream GEMMs without delaying the critical-path kernels.  ``lane`` > 0: the critical
+    stream of sub-batch ``lane`` of a grouped step."""
     idx = torch.device(device if device is not None else "cuda").index
     idx = torch.cuda.current_device() if idx is None else idx
-    if idx not in _CRIT:
+    if (idx, lane) not in _CRIT:
         lo, hi = torch.cuda.Stream.priority_range()
-        _CRIT[idx] = torch.cuda.Stream(device=idx, priority=hi)
-    return _CRIT[idx]
+        _CRIT[(idx, lane)] = torch.cuda.Stream(device=idx, priority=hi)
+    return _CRIT[(idx, lane)]
 
 
 def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale=0.5,
          pruned_scale=1.0, status=None, workspace=None, out=None, stream=None, overlap=True,
-         lm_only_scale=0.0, am_only_scale=0.0, grad_hook=None, exchange=None):
+         lm_only_scale=0.0, am_only_scale=0.0, grad_hook=None, exchange=None, lane=0, groups=1):
     """One fwd+bwd of the whole hot path: simple loss and its
     gradients, bounds, gather, pruned loss and joiner gradients.  Returns a dict of
     device tensors; ``out`` may supply preallocated outputs (same keys).
@@ -375,7 +383,16 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     ``exchange`` (a ``dist.GradBuffer``): the data-parallel exchange.  d_w / d_b are delivered into
     its flat buffer by the library (plain stores + NCCL all_reduce, NVLS multimem adds, or local
     adds), the masked batch-loss sums (rnnt_loss_sums) into its tail, and ``out["d_w"]`` /
-    ``out["d_b"]`` are views of it; the reduction overlaps the input-gradient kernels."""
+    ``out["d_b"]`` are views of it; the reduction overlaps the input-gradient kernels.
+
+    ``groups`` > 1: the batch is cut into that many contiguous sub-batches of utterances whose
+    whole chains run concurrently on their own streams (the chain is a sequence of latency-bound
+    kernels that each fill only part of the GPU); each sub-batch's d_w / d_b / loss sums land in a
+    row of a partials buffer and rnnt_exchange_sum adds the rows in a fixed order (deterministic)."""
+    if groups > 1:
+        return _step_grouped(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale,
+                             pruned_scale, status, workspace, out, stream, overlap, lm_only_scale, am_only_scale,
+                             grad_hook, exchange, groups)
     dims = dims_of(am, lm, w_out, S)
     dev = am.device
     o = out if out is not None else alloc_outputs(dims, dev)
@@ -394,7 +411,7 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
 
     if overlap:
         fwd(None, None)
-        side = _side_stream(dev)
+        side = _side_stream(dev, 0, lane)
         side.wait_stream(cur)
         if smooth:
             rnnt_simple_loss_smoothed_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims,
@@ -423,7 +440,7 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     if overlap:
         rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
                                  o["loss_pruned"], st, ws, cur)
-        side2 = _side_stream(dev, 1)
+        side2 = _side_stream(dev, 1, lane)
         side2.wait_stream(cur)
         weight_grads(side2)
         if grad_hook is not None:
@@ -448,6 +465,64 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
                          o["loss_pruned"], o["d_enc"], o["d_dec"], o["d_w"], o["d_b"], st, ws, cur)
         if grad_hook is not None:
             grad_hook()
+    return o
+
+
+_GROUP_WS = {}
+
+
+def _step_grouped(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_scale, pruned_scale,
+                  status, workspace, out, stream, overlap, lm_only_scale, am_only_scale, grad_hook, exchange, groups):
+    from .dist import GradBuffer
+    N = am.shape[0]
+    dims = dims_of(am, lm, w_out, S)
+    dev = am.device
+    o = out if out is not None else alloc_outputs(dims, dev)
+    st = o["status"] if status is None else status
+    cur = stream if stream is not None else torch.cuda.current_stream(dev)
+    V, J = dims.V, dims.J
+    cuts = [round(i * N / groups) for i in range(groups + 1)]
+    key = (torch.device(dev).index, tuple(am.shape), tuple(lm.shape), J, S, groups)
+    if key not in _GROUP_WS:
+        wss = []
+        for g in range(groups):
+            dg = make_dims(cuts[g + 1] - cuts[g], dims.T, dims.U, V, J, S)
+            wss.append(torch.empty(rnnt_workspace_bytes(dg), dtype=torch.uint8, device=dev))
+        parts = torch.zeros(groups, GradBuffer.flat_size(V, J), dtype=torch.float32, device=dev)
+        _GROUP_WS[key] = (wss, parts)
+    wss, parts = _GROUP_WS[key]
+    per = ("loss_simple", "px_grad", "py_grad", "am_grad", "lm_grad", "ranges", "h", "loss_pruned", "d_enc", "d_dec")
+    streams = []
+    for g in range(groups):
+        a, b = cuts[g], cuts[g + 1]
+        sg = critical_stream(dev, lane=g + 1)
+        sg.wait_stream(cur)
+        og = {k: o[k][a:b] for k in per}
+        og["status"] = st[a:b]
+        xb = GradBuffer.view_of(parts[g], V, J)
+        step(am[a:b], lm[a:b], symbols[a:b], boundary[a:b], enc_proj[a:b], dec_proj[a:b], w_out, b_out, S,
+             simple_scale, pruned_scale, None, wss[g], og, sg, overlap, lm_only_scale, am_only_scale, None, xb,
+             lane=g + 1)
+        streams.append(sg)
+    for sg in streams:
+        cur.wait_stream(sg)
+    M = GradBuffer.flat_size(V, J)
+    if exchange is None:
+        flat = torch.empty(M, dtype=torch.float32, device=dev)
+        rnnt_exchange_sum(parts, groups, M, EXCHANGE_STORE, flat, cur)
+        o["d_w"].copy_(flat[:V * J].view(V, J))            # (outputs the caller supplied)
+        o["d_b"].copy_(flat[V * J:V * J + V])
+    else:
+        exchange.begin(cur)
+        rnnt_exchange_sum(parts, groups, M, exchange.lib_mode, exchange.target("d_w"), cur)
+        with torch.cuda.stream(cur):
+            exchange.finish(cur)
+        o["d_w"], o["d_b"] = exchange.d_w, exchange.d_b
+    if grad_hook is not None:
+        grad_hook()
+    for t in (am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, parts) + tuple(wss):
+        for sg in streams:
+            t.record_stream(sg)
     return o
 
 

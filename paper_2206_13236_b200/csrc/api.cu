@@ -30,6 +30,8 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
                                      cudaStream_t st, int mode);
 cudaError_t loss_sums_launch(const float* ls, const float* lp, const int32_t* status, int N, float s_scale,
                              float p_scale, float* out, int mode, cudaStream_t st);
+cudaError_t split_reduce_acc_launch(const float* part, int splits, long long M, float* out, int mode, int kid,
+                                    cudaStream_t st);
 cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const float* dec, const uint16_t* W,
                              const uint16_t* b, const int64_t* sym, const int64_t* bnd, float gs, float* loss,
                              float* d_enc, float* d_dec, float* d_w, float* d_b, int32_t* status, cudaStream_t st);
@@ -54,7 +56,7 @@ static const char* const kNames[KID_COUNT] = {
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_dh_tables", "joiner_d_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
-    "full_dgrad", "loss_sums"};
+    "full_dgrad", "loss_sums", "exchange_sum"};
 
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -347,6 +349,14 @@ rnnt_status_t rnnt_pruned_loss_backward_weight_exchange(const uint16_t* h, const
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream, mode));
+}
+
+rnnt_status_t rnnt_exchange_sum(const float* parts, int32_t nparts, int64_t M, int32_t mode, float* out,
+                                void* stream) {
+  if (!parts || !out || nparts < 1 || M < 1) return RNNT_ERR_INVALID_ARG;
+  if (mode < RNNT_EXCHANGE_STORE || mode > RNNT_EXCHANGE_MULTIMEM) return RNNT_ERR_INVALID_ARG;
+  return cuda_status(split_reduce_acc_launch(parts, nparts, (long long)M, out, mode, KID_EXCHANGE_SUM,
+                                             (cudaStream_t)stream));
 }
 
 rnnt_status_t rnnt_loss_sums(const float* loss_simple, const float* loss_pruned, const int32_t* status, int32_t N,

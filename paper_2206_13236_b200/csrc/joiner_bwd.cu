@@ -74,6 +74,26 @@ __device__ __forceinline__ uint4 dz_chunk(uint4 pv, float s, float gbs, float gl
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// s * P~ for the 8 logits of one chunk, in packed bf16 arithmetic: s = s_hi + s_lo (two bf16), and
+//   dz = bf16_rn(P~ s_hi + bf16_rn(P~ s_lo))
+// (the inner product's rounding is ~2^-17 of the result, so this is within one bf16 rounding of the
+// fp32 product: two HFMA2 per pair of logits, no unpacking).  The picks (-gs g_b at v = 0, -gs g_l at
+// v = y) touch two logits of a row: pick_elem recomputes those in fp32 (rare, per-lane branch).
+__device__ __forceinline__ uint32_t bf16x2_splat(float x) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf16x2_scale(uint32_t p, uint32_t shi, uint32_t slo) {
+  uint32_t lo, d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(lo) : "r"(p), "r"(slo));
+  asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(p), "r"(shi), "r"(lo));
+  return d;
+}
+__device__ __forceinline__ uint4 dz_scale_chunk(uint4 pv, uint32_t shi, uint32_t slo) {
+  return make_uint4(bf16x2_scale(pv.x, shi, slo), bf16x2_scale(pv.y, shi, slo), bf16x2_scale(pv.z, shi, slo),
+                    bf16x2_scale(pv.w, shi, slo));
+}
 // byte offset of logical 16-B chunk `c` (0..7) of 128-B row `r` in a SWIZZLE_128B atom stack
 __device__ __forceinline__ uint32_t sw128(int r, int c) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
@@ -88,6 +108,11 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 //   contiguous, Eq. 9; u whose covering frames all lie in the tile are written directly, the <= S
 //   u at each end of a tile's utterance segment go to a boundary-partial buffer that
 //   ddec_fixup_kernel sums in tile order: deterministic, and dpre never leaves the SM).
+// The 8 epilogue warps take 64-column boxes: group g (4 warps, one per TMEM lane quadrant) drains the
+// 32 columns 64 b + 32 g (tcgen05.ld, dpre = dh (1 - h^2) with the row's h, one swizzled store), then
+// all 8 warps reduce the box: a thread per (output row, 4 columns), the output rows being the tile's
+// F frames (d_enc: S consecutive tile rows) and its d_dec entries (the rows of an entry are listed
+// once per tile by dh_tables_kernel, erow / eoff, so the inner loop is two independent loads per row).
 //
 // The per-tile tables (band offsets of the tile's frames and the d_dec entries) depend only on the
 // ranges: dh_tables_kernel builds them once per tile, lists the live tiles and zeroes d_enc of the
@@ -106,8 +131,10 @@ struct DhTab {
   int4 ent[128];   // d_dec entries {first frame, end frame, u, destination}: dst >= 0 row of d_dec,
                    // dst < 0 row -(1 + dst) of the boundary-partial buffer
   int nent, pad[3];
+  unsigned char erow[128];   // tile rows of the entries, entry by entry (f S + u - p_f, f ascending)
+  unsigned char eoff[144];   // entry e's rows are erow[eoff[e] .. eoff[e + 1])
 };
-static_assert(sizeof(DhTab) == 2576, "DhTab layout: 16-B multiple for the bulk copy");
+static_assert(sizeof(DhTab) == kDhTabBytes, "DhTab layout (workspace.h kDhTabBytes): 16-B multiple for the bulk copy");
 
 namespace jdh {
 constexpr int BM = 128, BK = 64, NSUB = 256, STAGES = 3;
@@ -115,9 +142,9 @@ constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x
 constexpr int B_BYTES = NSUB * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;   // 50 KB (1024-aligned)
-constexpr int D_BYTES = BM * 32 * 4;           // dpre staging [128][32] fp32, one per epilogue group
+constexpr int D_BYTES = BM * 32 * 4;           // one dpre chunk [128 rows][32 columns] fp32, ring of 2
 constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B), ring of 2
-constexpr int TAB_BYTES = 3072;                // one DhTab slot (2576 B, padded)
+constexpr int TAB_BYTES = 3072;                // one DhTab slot (2848 B, padded)
 constexpr int NTAB = 2;
 constexpr int H_OFF = STAGES * STAGE_BYTES + 2 * D_BYTES;
 constexpr int TAB_OFF = H_OFF + 2 * H_BYTES;
@@ -126,7 +153,7 @@ constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 // in-place dz producer warps: 4 (a thread per row) for short V loops, 8 (a thread per half row) when
 // the mainloop is long (measured: c2 108 vs 145 us, c4 2.95 vs 2.61 ms)
 template <int NTW> struct Roles {
-  static constexpr int EPI0 = 2 + NTW;          // first epilogue warp
+  static constexpr int EPI0 = 2 + NTW;          // first epilogue warp (8: two groups of 4, quadrant = warp % 4)
   static constexpr int THREADS = (EPI0 + 8) * 32;
 };
 }  // namespace jdh
@@ -142,7 +169,7 @@ struct JoinerDhParams {
   float* d_enc;            // (N,T,J) nullable
   float* d_dec;            // (N,U+1,J) nullable
   float* g_part;           // (ntiles, 2, S, J) boundary partials of d_dec
-  int dbg;                 // diagnostics (RNNT_DBG_DH): bit0 skip d_dec, bit1 skip d_enc, bit2 skip staging
+  int dbg;                 // unused (kept for the positional initialisers)
   int rt;                  // rows per tile (F*S frame-aligned; 128 in the generic mode)
   float* dpre_out;         // generic mode (full lattice): dpre = dh (1-h^2) rows to global, no tables
   int w3 = 0;              // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
@@ -161,6 +188,7 @@ __global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restric
   __shared__ int segx[128][2];     // {off, pnext}
   __shared__ unsigned char eseg[128];
   __shared__ int s_ne;
+  __shared__ int s_cnt[128], s_fl[128], s_u[128], s_off[128];
   const long long tile = blockIdx.x;
   const long long g0 = tile * F;
   const long long NT = (long long)N * T;
@@ -231,6 +259,24 @@ __global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restric
     else if (cov.x < q.w) dst = -1 - (int)((tile * 2 + 0) * S + (u - ub));                 // left boundary
     else dst = -1 - (int)((tile * 2 + 1) * S + (u - pnext));                                // right boundary
     tb->ent[e] = make_int4(fl, fh, u, dst);
+    s_cnt[e] = max(0, fh - fl);
+    s_fl[e] = fl;
+    s_u[e] = u;
+  }
+  __syncthreads();
+  // entry row lists: offsets by a serial scan (<= 128 entries), then each entry writes its rows
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int e = 0; e < s_ne; ++e) { s_off[e] = o; tb->eoff[e] = (unsigned char)o; o += s_cnt[e]; }
+    tb->eoff[s_ne] = (unsigned char)min(o, 255);
+  }
+  __syncthreads();
+  if (threadIdx.x < s_ne) {
+    const int e = threadIdx.x;
+    for (int k = 0; k < s_cnt[e]; ++k) {
+      const int f = s_fl[e] + k;
+      tb->erow[s_off[e] + k] = (unsigned char)(f * S + (s_u[e] - sp[f]));
+    }
   }
 }
 
@@ -249,10 +295,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 __device__ __forceinline__ void dh_trace(int it, int k) {
   if (g_dh_trace && it < 16) g_dh_trace[((size_t)blockIdx.x * 16 + it) * 5 + k] = gtimer();
-}
-// per (CTA, box < 4) of item 1, epilogue warp 6: {h ready, D4 staged, bar 1, d_enc done, d_dec done, bar 2}
-__device__ __forceinline__ void dh_trace_ep(int it, int bx, int k) {
-  if (g_dh_trace && it == 1 && bx < 4) g_dh_trace[148 * 16 * 5 + 148 * 3 * 8 * 4 + ((size_t)blockIdx.x * 4 + bx) * 6 + k] = gtimer();
 }
 // per (CTA, item < 3, k-block < 8): {TMA issued, stage seen loaded, transformed, MMA issued}
 __device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
@@ -281,7 +323,6 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   const DhTab* tabs_s = reinterpret_cast<const DhTab*>(smem + TAB_OFF);
   uint8_t* hbuf = smem + H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr bool rare = NTW == 8;      // dz_chunk label pick by branch: the 8-producer variant runs at V >= 2048
   const int S = p.S, F = p.F, RT = p.rt;
   const bool generic = p.dpre_out != nullptr;
   const long long NT = (long long)p.N * p.T;
@@ -295,7 +336,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 8);
+      tc::mbar_init(&tempty[s], 8);      // the 8 epilogue warps
       tc::mbar_init(&tabfull[s], 1);
       tc::mbar_init(&tabempty[s], 8);
       tc::mbar_init(&hfull[s], 1);
@@ -333,6 +374,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const uint32_t bytes = A_BYTES + (p.w3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + (uint32_t)grows * 16u;
         constexpr int PF = 8;            // P~ boxes prefetched into L2 this many k-blocks ahead
         for (int kb = 0; kb < min(PF, p.nkb); ++kb) tc::tma_prefetch_2d(&tmP, kb * BK, (int)m0);
+        // the epilogue's h boxes of this item: into L2 now, a mainloop ahead of their TMA loads
+        for (int bx = 0; bx < (min(NSUB, p.J - j0) + 63) / 64; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, (int)m0);
         for (int kb = 0; kb < p.nkb; ++kb) {
           if (kb + PF < p.nkb) tc::tma_prefetch_2d(&tmP, (kb + PF) * BK, (int)m0);
           tc::mbar_wait(&empty[stage], ph ^ 1);
@@ -414,13 +457,26 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
                                                   : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
         const int info = __float_as_int(gq.w);
+        const uint32_t shi = bf16x2_splat(gq.x);
+        const uint32_t slo = bf16x2_splat(gq.x - __uint_as_float(shi << 16));
+        // the picks (-gs g_b at v = 0, -gs g_l at v = y; labels are >= 1) touch one logit each: read
+        // it before the chunk stores, recompute bf16_rn(P~ s - g) in fp32, write it back after them
+        const int lv = info - (v0 + c_lo * 8);
+        const bool plab = (unsigned)lv < (unsigned)(CPT * 8);
+        const bool pblk = v0 == 0 && c_lo == 0 && info >= 0;
+        __nv_bfloat16* lp = reinterpret_cast<__nv_bfloat16*>(sa + sw128(rl, c_lo + (plab ? lv >> 3 : 0)) + (plab ? lv & 7 : 0) * 2);
+        __nv_bfloat16* bp = reinterpret_cast<__nv_bfloat16*>(sa + sw128(rl, 0));
+        const float lx = plab ? __bfloat162float(*lp) * gq.x - gq.z : 0.f;
+        const float bx = pblk ? __bfloat162float(*bp) * gq.x - gq.y : 0.f;
         uint4 pv[CPT];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) pv[c] = *reinterpret_cast<const uint4*>(sa + sw128(rl, c_lo + c));
 #pragma unroll
         for (int c = 0; c < CPT; ++c)
           *reinterpret_cast<uint4*>(sa + sw128(rl, c_lo + c)) =
-              info >= 0 ? dz_chunk(pv[c], gq.x, gq.y, gq.z, info, v0 + (c_lo + c) * 8, nullptr, rare) : make_uint4(0, 0, 0, 0);
+              info >= 0 ? dz_scale_chunk(pv[c], shi, slo) : make_uint4(0, 0, 0, 0);
+        if (plab) *lp = __float2bfloat16_rn(lx);
+        if (pblk) *bp = __float2bfloat16_rn(bx);
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&full[stage]);
@@ -429,12 +485,12 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       }
     }
   } else {
-    // ---- epilogue: group g (the 8 warps after the producers, 4 per group) takes the 32-column chunks c0 = 32 (2i + g);
-    // quadrant q = warp % 4 owns TMEM lanes (tile rows) 32q..32q+31
+    // ---- epilogue: box b = 64 columns; group g (4 warps, quadrant q4 = warp % 4 = TMEM lanes 32 q4 ..)
+    // drains columns 64 b + 32 g of its rows into D[g] (row rl, float4 slot i at i ^ (rl & 7)); then all
+    // 8 warps reduce the box, a thread per (output row, 4 columns): 16 threads per output row.
     const int q4 = warp & 3, g = (warp - EPI0) >> 2;
-    const int rl = 32 * q4 + lane;                      // tile row of this thread
-    const int gt = threadIdx.x - 32 * EPI0 - 128 * g;     // 0..127 within the group
-    float4* D4 = reinterpret_cast<float4*>(dstage + g * D_BYTES);
+    const int rl = 32 * q4 + lane;
+    const int et = threadIdx.x - 32 * EPI0;               // 0..255
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
     int it = 0, hslot = 0;
     uint32_t hph = 0;
@@ -447,110 +503,95 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
       const int nbox = (nj + 63) / 64;
       const DhTab* tb = reinterpret_cast<const DhTab*>(reinterpret_cast<const uint8_t*>(tabs_s) + slot * TAB_BYTES);
+
       if (!generic) tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
       if (warp == EPI0 && lane == 0) dh_trace(it, 3);
       const int nent = generic ? 0 : tb->nent;
+      const int nout = F + nent;
       for (int bx = 0; bx < nbox; ++bx) {
-        const int c0 = 64 * bx + 32 * g;
-        tc::mbar_wait(&hfull[hslot], hph);
-        const bool trc = warp == EPI0 && lane == 0;
-        if (trc) dh_trace_ep(it, bx, 0);
+        const int c0 = 64 * bx + 32 * g;                   // this group's 32 columns
         const bool have = c0 < nj;
+        tc::mbar_wait(&hfull[hslot], hph);
         float accv[32];
         if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
+        if (bx == nbox - 1) {                            // last TMEM read of this accumulator
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+        }
         const uint8_t* hb = hbuf + hslot * H_BYTES;
-        const int nq = have ? min(4, (nj - c0) / 8) : 0;           // J % 8 == 0
+        const int nq = have ? min(4, (nj - c0) / 8) : 0;   // J % 8 == 0
+        float out[32];
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
-          float out[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          if (qq < nq && live) {
-            const uint4 hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, 4 * g + qq));
-            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+          uint4 hv = make_uint4(0, 0, 0, 0);
+          if (qq < nq && live) hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, 4 * g + qq));
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
-              out[2 * i] = accv[8 * qq + 2 * i] * (1.f - ha * ha);            // d tanh
-              out[2 * i + 1] = accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2);
-            }
-          }
-          if (generic) {
-            if (qq < nq && rl < RT && r < p.g.R) {
-              float4* dst = reinterpret_cast<float4*>(p.dpre_out + (size_t)r * p.J + j0 + c0 + 8 * qq);
-              dst[0] = make_float4(out[0], out[1], out[2], out[3]);
-              dst[1] = make_float4(out[4], out[5], out[6], out[7]);
-            }
-          } else if (!(p.dbg & 4)) {
-            D4[rl * 8 + ((2 * qq) ^ (rl & 7))] = make_float4(out[0], out[1], out[2], out[3]);
-            D4[rl * 8 + ((2 * qq + 1) ^ (rl & 7))] = make_float4(out[4], out[5], out[6], out[7]);
+          for (int i = 0; i < 4; ++i) {
+            const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
+            const bool ok = qq < nq && live;
+            out[8 * qq + 2 * i] = ok ? accv[8 * qq + 2 * i] * (1.f - ha * ha) : 0.f;       // d tanh
+            out[8 * qq + 2 * i + 1] = ok ? accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
           }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
         if (++hslot == 2) { hslot = 0; hph ^= 1; }
-        if (!have) continue;
         if (generic) {
-          if (c0 + 64 >= nj) {
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+          if (have && rl < RT && r < p.g.R) {
+            float4* dst = reinterpret_cast<float4*>(p.dpre_out + (size_t)r * p.J + j0 + c0);
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq)
+              if (qq < 2 * nq) dst[qq] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
           }
           continue;
         }
-        if (c0 + 64 >= nj) {            // last TMEM read of this accumulator by this warp
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-        }
-        if (trc) dh_trace_ep(it, bx, 1);
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-        if (trc) dh_trace_ep(it, bx, 2);
-        const int ncol4 = min(32, nj - c0) / 4;
-        // d_enc: one float4 output per (frame, 4-column group)
-        if (p.d_enc && !(p.dbg & 2))
-          for (int i = gt; i < F * 8; i += 128) {
-            const int f = i >> 3, qq = i & 7;
-            if (qq < ncol4 && g0 + f < NT) {
-              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int s = 0; s < S; ++s) {
-                const int rr = f * S + s;
-                const float4 x = D4[rr * 8 + (qq ^ (rr & 7))];
-                v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
-              }
-              reinterpret_cast<float4*>(p.d_enc + (size_t)(g0 + f) * p.J + j0 + c0)[qq] = v;
+        float4* D4 = reinterpret_cast<float4*>(dstage + g * D_BYTES);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+          D4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        // reduce: task t = (output o, 16 float4 columns of the box); o < F: d_enc of frame o, else d_dec
+        // entry o - F
+        const int ncol4 = min(64, nj - 64 * bx) / 4;
+        for (int t = et; t < nout * 16; t += 256) {
+          const int o = t >> 4, c16 = t & 15;
+          if (c16 >= ncol4) continue;
+          const float4* Dg = reinterpret_cast<const float4*>(dstage + (c16 >> 3) * D_BYTES);
+          const int qq = c16 & 7;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          float* dst;
+          if (o < F) {
+            if (!p.d_enc || g0 + o >= NT) continue;
+            for (int s = 0; s < S; ++s) {
+              const int rr = o * S + s;
+              const float4 x = Dg[rr * 8 + (qq ^ (rr & 7))];
+              v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
             }
-          }
-        if (trc) dh_trace_ep(it, bx, 3);
-        // d_dec: one float4 output per (token position of a segment, 4-column group)
-        if (p.d_dec && !(p.dbg & 1))
-          for (int i = gt; i < nent * 8; i += 128) {
-            const int e = i >> 3, qq = i & 7;
-            if (qq >= ncol4) continue;
-            const int4 en = tb->ent[e];
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int f0 = en.x; f0 < en.y; f0 += 4) {     // four covering frames per step (loads in flight)
+            dst = p.d_enc + (size_t)(g0 + o) * p.J;
+          } else {
+            if (!p.d_dec) continue;
+            const int e = o - F;
+            const int k0 = tb->eoff[e], k1 = tb->eoff[e + 1];
+            for (int k = k0; k < k1; k += 4) {             // four rows per step (loads in flight)
               float4 x[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const int f = f0 + k;
-                const int rr = f * S + (en.z - tb->sp[f < en.y ? f : en.x]);
-                x[k] = f < en.y ? D4[rr * 8 + (qq ^ (rr & 7))] : make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int m = 0; m < 4; ++m) {
+                const int rr = tb->erow[k + m < k1 ? k + m : k0];
+                x[m] = k + m < k1 ? Dg[rr * 8 + (qq ^ (rr & 7))] : make_float4(0.f, 0.f, 0.f, 0.f);
               }
 #pragma unroll
-              for (int k = 0; k < 4; ++k) { v.x += x[k].x; v.y += x[k].y; v.z += x[k].z; v.w += x[k].w; }
+              for (int m = 0; m < 4; ++m) { v.x += x[m].x; v.y += x[m].y; v.z += x[m].z; v.w += x[m].w; }
             }
-            float* dst = en.w >= 0 ? p.d_dec + (size_t)en.w * p.J : p.g_part + (size_t)(-1 - en.w) * p.J;
-            reinterpret_cast<float4*>(dst + j0 + c0)[qq] = v;
+            const int w = tb->ent[e].w;
+            dst = w >= 0 ? p.d_dec + (size_t)w * p.J : p.g_part + (size_t)(-1 - w) * p.J;
           }
-        if (trc) dh_trace_ep(it, bx, 4);
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-        if (trc) dh_trace_ep(it, bx, 5);
-      }
-      if (nj <= 32 * g) {               // this group had no chunk: still release the accumulator
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+          reinterpret_cast<float4*>(dst + j0 + 64 * bx)[c16] = v;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       __syncwarp();
       if (lane == 0 && !generic) tc::mbar_arrive(&tabempty[slot]);
@@ -1036,6 +1077,19 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
 }
 
 // ======================================================================= host
+template <int NTW>
+static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
+                               const CUtensorMap& th, cudaStream_t st) {
+  smem_optin(joiner_dh_tc_kernel<NTW>, jdh::SMEM_BYTES);
+  joiner_dh_tc_kernel<NTW><<<grid, jdh::Roles<NTW>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p);
+  return cudaGetLastError();
+}
+// 4 producer warps for short V loops, 8 for long ones
+static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
+                             const CUtensorMap& th, cudaStream_t st) {
+  return p.nkb >= 32 ? launch_dh_k<8>(p, grid, tp, tw, th, st) : launch_dh_k<4>(p, grid, tp, tw, th, st);
+}
+
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
                              const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
                              float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st) {
@@ -1046,8 +1100,6 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  smem_optin(joiner_dh_tc_kernel<4>, jdh::SMEM_BYTES);
-  smem_optin(joiner_dh_tc_kernel<8>, jdh::SMEM_BYTES);
   const int F = d.dh_frames();
   const long long ntiles = d.dh_tiles();
   cudaMemsetAsync(nlive, 0, sizeof(int), st);
@@ -1056,16 +1108,10 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
                    static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0, F * d.S, nullptr};
-#ifdef RNNT_DIAGNOSTICS
-  if (const char* e = getenv("RNNT_DBG_DH")) p.dbg = atoi(e);   // skips epilogue parts: wrong results, timing only
-#endif
   p.w3 = w3;
   const int nsm = current_sm_count();
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  if (p.nkb >= 32)
-    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
-  else
-    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<4><<<grid, jdh::Roles<4>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, st));
   if (d_dec)
     RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() * ((d.J / 4 + 63) / 64) + 7) / 8),
                                                   256, 0, st>>>(
@@ -1086,17 +1132,12 @@ cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  smem_optin(joiner_dh_tc_kernel<4>, jdh::SMEM_BYTES);
-  smem_optin(joiner_dh_tc_kernel<8>, jdh::SMEM_BYTES);
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
   JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
                    nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out, w3};
   const int nsm = current_sm_count();
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  if (p.nkb >= 32)
-    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<8><<<grid, jdh::Roles<8>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
-  else
-    RNNT_LAUNCH(KID_DH, st, joiner_dh_tc_kernel<4><<<grid, jdh::Roles<4>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p));
+  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, st));
   return cudaGetLastError();
 }
 

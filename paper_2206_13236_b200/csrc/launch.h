@@ -13,7 +13,7 @@ enum KernelId {
   KID_JOINER_FWD, KID_SOFTMAX, KID_PALPHA, KID_PBETA, KID_PCOMBINE, KID_DH, KID_DENC, KID_DDEC,
   KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD, KID_OCCSUMS,
   KID_SMOOTH_AVG, KID_SMOOTH_AC, KID_SMOOTH_GQ, KID_SMOOTH_Q,
-  KID_FULL_SCATTER, KID_FULL_PACK, KID_FULL_LIVE, KID_FULL_DGRAD, KID_LOSS_SUMS,
+  KID_FULL_SCATTER, KID_FULL_PACK, KID_FULL_LIVE, KID_FULL_DGRAD, KID_LOSS_SUMS, KID_EXCHANGE_SUM,
   KID_COUNT
 };
 

@@ -103,7 +103,7 @@ struct PrunedWS {
   float* gl;         // (R) y'_p
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
   float* dpart;      // (dh_tiles,2,S,J) d_dec boundary partials of the joiner_dh tiles
-  void* dhtab;       // (dh_tiles) joiner_dh tile tables (2576 B each, joiner_bwd.cu DhTab)
+  void* dhtab;       // (dh_tiles) joiner_dh tile tables (2704 B each, joiner_bwd.cu DhTab)
   int* dhlive;       // (dh_tiles + 1) ids of the live joiner_dh tiles, then their count
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
@@ -112,6 +112,8 @@ struct PrunedWS {
 
 // K11 variant: "wide" CTAs (one per SM) hold two V tiles (256 v x 256 j, 512 TMEM columns) so each
 // h k-block feeds two MMAs; used for large V (L2 -> SM bound), RNNT_DW_WIDE=0/1 forces it off/on.
+constexpr size_t kDhTabBytes = 2848;   // sizeof(DhTab) (joiner_bwd.cu static_asserts it)
+
 inline bool dw_wide(const Dims& d) {
   static const int force = env_int("RNNT_DW_WIDE", -1);
   if (force >= 0) return force == 1;
@@ -212,7 +214,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   const bool framed = d.S <= 128;
   const size_t ltiles = framed ? (size_t)d.dh_tiles() : (R + 127) / 128;
   p.dpart = (float*)take(framed ? (size_t)d.dh_tiles() * 2 * d.S * J * 4 : 0);
-  p.dhtab = take(framed ? (size_t)d.dh_tiles() * 2576 : 0);
+  p.dhtab = take(framed ? (size_t)d.dh_tiles() * kDhTabBytes : 0);
   p.dhlive = (int*)take((ltiles + 1) * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);

@@ -55,7 +55,7 @@ class GradBuffer:
         self.V, self.J, self.mode, self.group = V, J, mode, group
         self.lib_mode = self.MODES[mode]
         self.zero_on_begin = True       # False: the caller zeroes once and several steps add (RED)
-        n = V * J + V + 2
+        n = self.flat_size(V, J)
         self.handle = None
         if mode == "multimem":
             import torch.distributed._symmetric_memory as symm_mem
@@ -71,7 +71,25 @@ class GradBuffer:
             self.addr_base = None
         self.d_w = self.flat[: V * J].view(V, J)
         self.d_b = self.flat[V * J: V * J + V]
-        self.loss_sums = self.flat[V * J + V:]
+        self.loss_sums = self.flat[V * J + V: V * J + V + 2]
+
+    @staticmethod
+    def flat_size(V: int, J: int) -> int:
+        """V*J + V + 2 floats rounded up to a multiple of 4 (16-B aligned rows when stacked)."""
+        return (V * J + V + 2 + 3) // 4 * 4
+
+    @classmethod
+    def view_of(cls, flat: torch.Tensor, V: int, J: int):
+        """A "local" (plain stores) buffer over an existing flat tensor of V*J + V + 2 floats (one row
+        of a grouped step's partials)."""
+        self = cls.__new__(cls)
+        self.V, self.J, self.mode, self.group = V, J, "local", None
+        self.lib_mode, self.zero_on_begin, self.handle, self.addr_base = 0, True, None, None
+        self.flat = flat
+        self.d_w = flat[: V * J].view(V, J)
+        self.d_b = flat[V * J: V * J + V]
+        self.loss_sums = flat[V * J + V: V * J + V + 2]
+        return self
 
     # device addresses the kernels write / add to (multicast addresses in "multimem" mode)
     def target(self, which: str):

@@ -1,10 +1,10 @@
-"""Diagnostics: per-(CTA, item) timestamps of the persistent joiner_dh kernel on config 2."""
+"""Diagnostics: per-(CTA, item) timestamps of the persistent joiner_dh kernel (config from argv, default c5)."""
 # needs the diagnostics build: make -C paper_2206_13236_b200 diag; RNNT_LIB=paper_2206_13236_b200/librnnt_b200_diag.so
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth, paper_2206_13236_b200 as R
-b = synth.make_batch(2)
+b = synth.make_batch(int(sys.argv[1]) if len(sys.argv) > 1 else 5)
 dev = R.batch_to_device(b, "cuda")
 buf = torch.zeros((8 << 20) // 8, dtype=torch.int64, device="cuda")
 lib = R.load_library()
@@ -38,17 +38,6 @@ d = k[:, :, :, 2] - k[:, :, :, 1]
 print("transform med %.2f p90 %.2f" % (np.median(d), np.percentile(d, 90)))
 d = k[:, :, :, 3] - k[:, :, :, 2]
 print("transform->mma med %.2f p90 %.2f" % (np.median(d), np.percentile(d, 90)))
-off2 = off + 148 * 3 * 8 * 4
-e = buf.cpu().numpy()[off2:off2 + 148 * 4 * 6].reshape(148, 4, 6).astype(np.float64)
-e = (e - t0) / 1000.0
-for c in [0, 70]:
-    print("cta", c, "item 1 epilogue boxes:", np.round(e[c], 2).tolist())
-names = ["stage D4", "bar1", "d_enc", "d_dec", "bar2"]
-for i in range(5):
-    d = e[:, :, i + 1] - e[:, :, i]
-    print(f"{names[i]:10s} med {np.median(d):.2f}")
-d = e[:, 1:, 0] - e[:, :-1, 5]
-print("h wait between boxes med %.2f" % np.median(d))
 off3 = (6 << 20) // 8
 sc = buf.cpu().numpy()[off3:off3 + 32 * 2 * 5].reshape(32, 2, 5).astype(np.float64)
 sc = (sc - sc[:, :, :1]) / 1000.0

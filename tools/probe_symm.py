@@ -15,11 +15,10 @@ try:
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     import torch.distributed._symmetric_memory as symm_mem
+    out["backend"] = str(symm_mem.get_backend(torch.device("cuda", 0))) if hasattr(symm_mem, "get_backend") else None
     t = symm_mem.empty(1 << 20, dtype=torch.float32, device="cuda")
     h = symm_mem.rendezvous(t, dist.group.WORLD)
     out["multicast_ptr"] = int(h.multicast_ptr)
-    out["has_multicast_support"] = bool(symm_mem._SymmetricMemory.has_multicast_support(
-        torch._C._distributed_c10d.DeviceType.CUDA, 0)) if hasattr(symm_mem._SymmetricMemory, "has_multicast_support") else None
     if out["multicast_ptr"]:
         import paper_2206_13236_b200 as R
         t.zero_()

@@ -53,7 +53,7 @@ static const char* const kNames[KID_COUNT] = {
     "none", "validate", "simple_prep", "unused_exp_split_lm", "simple_norm_gemm", "skew_fill", "lattice_fb",
     "lattice_combine", "simple_am_grad_gemm", "unused_am_picks", "simple_lm_grad_gemm", "unused_lm_picks",
     "ranges_raw", "ranges_adjust", "prune_gather", "pruned_rowinfo", "joiner_fwd_gemm", "joiner_softmax",
-    "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_dh_tables", "joiner_d_dec",
+    "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_band_chunk", "joiner_band_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
     "full_dgrad", "loss_sums", "exchange_sum"};

@@ -32,9 +32,8 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
                            float* py_grad, int32_t* status, cudaStream_t st);
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
                                      cudaStream_t st, int mode);
-cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
-                                     const int* live, const int* nlive, long long ntiles, float* dpre_out,
-                                     cudaStream_t st);
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
+                             const int* nlive, long long ntiles, float* dpre, cudaStream_t st);
 cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
                            const int64_t* bnd, const uint16_t* b, cudaStream_t st);
 
@@ -81,6 +80,11 @@ __global__ void full_pack_kernel(const float* __restrict__ gb, const float* __re
 __global__ void full_live_kernel(const uint8_t* __restrict__ tlive, long long ntiles, int* __restrict__ live) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ntiles && tlive[i]) live[atomicAdd(live + ntiles, 1)] = (int)i;
+}
+cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st) {
+  cudaMemsetAsync(live + ntiles, 0, sizeof(int), st);
+  RNNT_LAUNCH(kid, st, full_live_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(tlive, ntiles, live));
+  return cudaGetLastError();
 }
 
 // blocks [0, N T): d_enc[n,t,:] = sum_{u <= U_n} dpre[(n,t,u),:];  blocks [N T, N T + N (U+1)):
@@ -150,11 +154,9 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   if ((e = pruned_bwd_weight_launch(df, pw, fw.h, d_w, d_b, st, 0)) != cudaSuccess) return e;
   if (d_enc || d_dec) {
     const long long ntiles = (R + 127) / 128;
-    cudaMemsetAsync(pw.dhlive + ntiles, 0, sizeof(int), st);
-    RNNT_LAUNCH(KID_FULL_LIVE, st, full_live_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(
-        pw.tlive, ntiles, pw.dhlive));
+    if ((e = live_tiles_launch(pw.tlive, ntiles, pw.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
     GradSrc g{pw.Pt, pw.gpk, pw.rowinfo, R, df.V, df.VP(), df.ntile()};
-    if ((e = joiner_dh_generic_launch(df, g, fw.h, W, pw.dhlive, pw.dhlive + ntiles, ntiles, fw.dpre, st)) != cudaSuccess)
+    if ((e = joiner_dh_launch(df, g, fw.h, W, pw.dhlive, pw.dhlive + ntiles, ntiles, fw.dpre, st)) != cudaSuccess)
       return e;
     RNNT_LAUNCH(KID_FULL_DGRAD, st, full_dgrad_kernel<<<(unsigned)((long long)df.N * df.T + (long long)df.N * df.U1()), 128, 0, st>>>(
         fw.dpre, bnd, df.N, df.T, df.U, df.J, d_enc, d_dec));

@@ -100,185 +100,48 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 }
 
 // ======================================================================= K10
-// Frame-aligned row tiles: tile i holds the F = floor(128/S) frames [iF, iF+F) of the flattened
-// (n, t) frame index, i.e. rows [iFS, iFS + FS) (the MMA computes 128 rows; the rest is ignored).
-// The epilogue forms dpre = dh (1 - h^2) for a 32-column chunk in smem and reduces it there:
-//   d_enc[n,t,:] = sum_s dpre[(n,t,s),:]                                      (complete in the tile)
-//   d_dec[n,u,:] = sum over band rows (t, s) with p_t + s = u of dpre         (frames covering u are
-//   contiguous, Eq. 9; u whose covering frames all lie in the tile are written directly, the <= S
-//   u at each end of a tile's utterance segment go to a boundary-partial buffer that
-//   ddec_fixup_kernel sums in tile order: deterministic, and dpre never leaves the SM).
-// The 8 epilogue warps take 64-column boxes: group g (4 warps, one per TMEM lane quadrant) drains the
-// 32 columns 64 b + 32 g (tcgen05.ld, dpre = dh (1 - h^2) with the row's h, one swizzled store), then
-// all 8 warps reduce the box: a thread per (output row, 4 columns), the output rows being the tile's
-// F frames (d_enc: S consecutive tile rows) and its d_dec entries (the rows of an entry are listed
-// once per tile by dh_tables_kernel, erow / eoff, so the inner loop is two independent loads per row).
-//
-// The per-tile tables (band offsets of the tile's frames and the d_dec entries) depend only on the
-// ranges: dh_tables_kernel builds them once per tile, lists the live tiles and zeroes d_enc of the
-// dead ones; the persistent joiner_dh_tc_kernel then walks (live tile, 256-column part of J) work
-// items with every role pipelined across items:
-//   warp 0      lane 0: TMA producer: per item the tile table (bulk), per 64-logit k-block the P~
-//               tile, the W boxes and the rows' packed scalars, into a 3-stage ring;
+// joiner_dh: dh = dz W over (live 128-row tile, 256-column part of J) work items, persistent, every
+// role pipelined across items:
+//   warp 0      lane 0: TMA producer: per 64-logit k-block the P~ tile, the W boxes and the rows' packed
+//               scalars into a 3-stage ring (the item's h boxes are prefetched into L2 at its start);
 //               lane 1: the epilogue's h boxes (64 columns x 128 rows) into a 2-slot ring
 //   warp 1      TMEM allocator (2 x 256 columns) and single-thread MMA issuer
 //   warps 2..   in-place dz producers (4 or 8 warps: a thread per row or half row), release each
 //               stage to the MMA
-//   warps 6-13  epilogue, two groups of four (one per TMEM lane quadrant), alternate 32-column
-//               chunks; the accumulator of item k+1 fills while item k drains.
-struct DhTab {
-  int sp[128];     // band offset p_t of the tile's frames (-1: dead frame)
-  int4 ent[128];   // d_dec entries {first frame, end frame, u, destination}: dst >= 0 row of d_dec,
-                   // dst < 0 row -(1 + dst) of the boundary-partial buffer
-  int nent, pad[3];
-  unsigned char erow[128];   // tile rows of the entries, entry by entry (f S + u - p_f, f ascending)
-  unsigned char eoff[144];   // entry e's rows are erow[eoff[e] .. eoff[e + 1])
-};
-static_assert(sizeof(DhTab) == kDhTabBytes, "DhTab layout (workspace.h kDhTabBytes): 16-B multiple for the bulk copy");
-
+//   4 epilogue  one per TMEM lane quadrant, thread = tile row, 32-column chunks: dpre = dh (1 - h^2)
+//   warps       into a swizzled 16 KB smem tile (2-slot ring), written to the fp32 dpre (R, J) by one TMA
+//               store per chunk; the accumulator of item k+1 fills while item k drains.
+// The reductions d_enc[t] = sum_s dpre[(t,s)] and d_dec[u] = sum_{t: p_t <= u < p_t + S} dpre[(t, u - p_t)]
+// run afterwards in band_reduce_kernel (pruned.cu): a streaming pass at HBM speed, deterministic, that
+// keeps this kernel's epilogue far shorter than its mainloop.
 namespace jdh {
 constexpr int BM = 128, BK = 64, NSUB = 256, STAGES = 3;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
 constexpr int B_BYTES = NSUB * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;   // 50 KB (1024-aligned)
-constexpr int D_BYTES = BM * 32 * 4;           // one dpre chunk [128 rows][32 columns] fp32, ring of 2
 constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B), ring of 2
-constexpr int TAB_BYTES = 3072;                // one DhTab slot (2848 B, padded)
-constexpr int NTAB = 2;
-constexpr int H_OFF = STAGES * STAGE_BYTES + 2 * D_BYTES;
-constexpr int TAB_OFF = H_OFF + 2 * H_BYTES;
-constexpr int BAR_OFF = TAB_OFF + NTAB * TAB_BYTES;
+constexpr int O_BYTES = BM * 32 * 4;           // one 32-column dpre chunk (128 rows x 128 B, SWIZZLE_128B), ring of 2
+constexpr int H_OFF = STAGES * STAGE_BYTES;
+constexpr int O_OFF = H_OFF + 2 * H_BYTES;
+constexpr int BAR_OFF = O_OFF + 2 * O_BYTES;
 constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 // in-place dz producer warps: 4 (a thread per row) for short V loops, 8 (a thread per half row) when
-// the mainloop is long (measured: c2 108 vs 145 us, c4 2.95 vs 2.61 ms)
+// the mainloop is long
 template <int NTW> struct Roles {
-  static constexpr int EPI0 = 2 + NTW;          // first epilogue warp (8: two groups of 4, quadrant = warp % 4)
-  static constexpr int THREADS = (EPI0 + 8) * 32;
+  static constexpr int EPI0 = 2 + NTW;          // first epilogue warp (4: quadrant = warp % 4)
+  static constexpr int THREADS = (EPI0 + 4) * 32;
 };
 }  // namespace jdh
 
 struct JoinerDhParams {
   GradSrc g;
-  const uint16_t* h;       // (R, J) bf16
   int J, nkb, njp;
-  int N, T, U, S, F;
-  const DhTab* tabs;       // (dh_tiles)
-  const int* live;         // ids of the tiles with a live row (dh_tables_kernel; order irrelevant)
+  const int* live;         // ids of the 128-row tiles with a live row (order irrelevant)
   const int* nlive;        // their count
-  float* d_enc;            // (N,T,J) nullable
-  float* d_dec;            // (N,U+1,J) nullable
-  float* g_part;           // (ntiles, 2, S, J) boundary partials of d_dec
-  int dbg;                 // unused (kept for the positional initialisers)
-  int rt;                  // rows per tile (F*S frame-aligned; 128 in the generic mode)
-  float* dpre_out;         // generic mode (full lattice): dpre = dh (1-h^2) rows to global, no tables
-  int w3 = 0;              // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
+  float* dpre;             // (R, J) fp32 out: dh (1 - h^2) of the rows of the live tiles
+  int w3;                  // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
 };
-
-// One CTA of 128 threads per frame-aligned tile: the tile table, the live-tile list, and zeros of
-// d_enc for a tile without a live row (the persistent kernel never visits it).
-__global__ void __launch_bounds__(128) dh_tables_kernel(const int32_t* __restrict__ ranges,
-                                                        const int2* __restrict__ urange,
-                                                        const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                        int F, int J, DhTab* __restrict__ tabs, int* __restrict__ live,
-                                                        int* __restrict__ nlive, float* __restrict__ d_enc) {
-  __shared__ int sp[128], spn[128], sfn[128], sft[128];
-  __shared__ int4 segs[128];       // {n, fb, fe, ta}
-  __shared__ int2 segu[128];       // {ub, ue}
-  __shared__ int segx[128][2];     // {off, pnext}
-  __shared__ unsigned char eseg[128];
-  __shared__ int s_ne;
-  __shared__ int s_cnt[128], s_fl[128], s_u[128], s_off[128];
-  const long long tile = blockIdx.x;
-  const long long g0 = tile * F;
-  const long long NT = (long long)N * T;
-  DhTab* tb = tabs + tile;
-  const int f = threadIdx.x;
-  int pv = -1;
-  if (f < F) {
-    const long long g = g0 + f;
-    int pn = 0, n = -1, t = 0;
-    if (g < NT) {
-      n = (int)(g / T);
-      t = (int)(g - (long long)n * T);
-      const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-      if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) {
-        pv = ranges[(size_t)n * T + t];
-        if (t + 1 < Tn) pn = ranges[(size_t)n * T + t + 1];
-      }
-    }
-    sp[f] = pv; spn[f] = pn; sfn[f] = n; sft[f] = t;
-  }
-  if (f < 128) tb->sp[f] = (f < F) ? pv : -1;
-  const bool any = __syncthreads_or(pv >= 0);
-  if (!any) {
-    if (threadIdx.x == 0) tb->nent = 0;
-    if (d_enc)
-      for (int idx = threadIdx.x; idx < F * (J / 4); idx += blockDim.x) {
-        const int ff = idx / (J / 4), jq = idx - ff * (J / 4);
-        if (g0 + ff < NT) reinterpret_cast<float4*>(d_enc + (size_t)(g0 + ff) * J)[jq] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    return;
-  }
-  if (threadIdx.x == 0) {
-    live[atomicAdd(nlive, 1)] = (int)tile;
-    // utterance segments of the tile, then one entry per token position of a segment
-    int ns = 0, ne = 0;
-    for (int ff = 0; ff < F;) {
-      if (sp[ff] < 0) { ++ff; continue; }
-      const int n = sfn[ff];
-      int fe = ff + 1;
-      while (fe < F && sp[fe] >= 0 && sfn[fe] == n) ++fe;
-      const int ub = sp[ff], ue = min(utt_U(bnd, n), sp[fe - 1] + S - 1);
-      if (ns < 128) {
-        segs[ns] = make_int4(n, ff, fe, sft[ff]);
-        segu[ns] = make_int2(ub, ue);
-        segx[ns][0] = ne;
-        segx[ns][1] = spn[fe - 1];
-        for (int e = 0; e <= ue - ub && ne + e < 128; ++e) eseg[ne + e] = (unsigned char)ns;
-        ++ns;
-        ne += ue - ub + 1;
-      }
-      ff = fe;
-    }
-    s_ne = min(ne, 128);
-    tb->nent = s_ne;
-  }
-  __syncthreads();
-  if (threadIdx.x < s_ne) {
-    const int e = threadIdx.x;
-    const int si = eseg[e];
-    const int4 q = segs[si];          // {n, fb, fe, ta}
-    const int ub = segu[si].x, off = segx[si][0], pnext = segx[si][1];
-    const int u = ub + (e - off);
-    const int2 cov = urange[(size_t)q.x * (U + 1) + u];          // frames [lo, hi) covering u
-    const int fl = max(q.y, cov.x - q.w + q.y), fh = min(q.z, cov.y - q.w + q.y);
-    const int tbd = q.w + (q.z - q.y);
-    int dst;
-    if (cov.x >= q.w && cov.y <= tbd) dst = q.x * (U + 1) + u;                             // complete here
-    else if (cov.x < q.w) dst = -1 - (int)((tile * 2 + 0) * S + (u - ub));                 // left boundary
-    else dst = -1 - (int)((tile * 2 + 1) * S + (u - pnext));                                // right boundary
-    tb->ent[e] = make_int4(fl, fh, u, dst);
-    s_cnt[e] = max(0, fh - fl);
-    s_fl[e] = fl;
-    s_u[e] = u;
-  }
-  __syncthreads();
-  // entry row lists: offsets by a serial scan (<= 128 entries), then each entry writes its rows
-  if (threadIdx.x == 0) {
-    int o = 0;
-    for (int e = 0; e < s_ne; ++e) { s_off[e] = o; tb->eoff[e] = (unsigned char)o; o += s_cnt[e]; }
-    tb->eoff[s_ne] = (unsigned char)min(o, 255);
-  }
-  __syncthreads();
-  if (threadIdx.x < s_ne) {
-    const int e = threadIdx.x;
-    for (int k = 0; k < s_cnt[e]; ++k) {
-      const int f = s_fl[e] + k;
-      tb->erow[s_off[e] + k] = (unsigned char)(f * S + (s_u[e] - sp[f]));
-    }
-  }
-}
 
 // diagnostics: per (CTA, item) timestamps {producer start, first MMA, last MMA commit, epilogue
 // start (accumulator full), epilogue end}; 16 items per CTA
@@ -304,7 +167,8 @@ __device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
 template <int NTW>
 __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
-                        const __grid_constant__ CUtensorMap tmH, JoinerDhParams p) {
+                        const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
+                        JoinerDhParams p) {
   using namespace jdh;
   constexpr int EPI0 = Roles<NTW>::EPI0;
   extern __shared__ uint8_t smem_raw[];
@@ -314,18 +178,11 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;       // [2]
   uint64_t* tempty = tfull + 2;           // [2]
-  uint64_t* tabfull = tempty + 2;         // [2]
-  uint64_t* tabempty = tabfull + 2;       // [2]
-  uint64_t* hfull = tabempty + 2;         // [2]
+  uint64_t* hfull = tempty + 2;           // [2]
   uint64_t* hempty = hfull + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
-  uint8_t* dstage = smem + STAGES * STAGE_BYTES;                    // [2 groups][128][32] fp32
-  const DhTab* tabs_s = reinterpret_cast<const DhTab*>(smem + TAB_OFF);
   uint8_t* hbuf = smem + H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = p.S, F = p.F, RT = p.rt;
-  const bool generic = p.dpre_out != nullptr;
-  const long long NT = (long long)p.N * p.T;
   const long long nitems = (long long)(*p.nlive) * p.njp;
 
   if (warp == 0 && lane == 0) {
@@ -336,11 +193,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 8);      // the 8 epilogue warps
-      tc::mbar_init(&tabfull[s], 1);
-      tc::mbar_init(&tabempty[s], 8);
+      tc::mbar_init(&tempty[s], 4);      // the 4 epilogue warps
       tc::mbar_init(&hfull[s], 1);
-      tc::mbar_init(&hempty[s], 8);
+      tc::mbar_init(&hempty[s], 4);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
@@ -360,14 +215,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       uint32_t ph = 0;
       for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
         const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
-        const int slot = it & 1;
         dh_trace(it, 0);
-        if (!generic) {
-          tc::mbar_wait(&tabempty[slot], ((it >> 1) & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(&tabfull[slot], (uint32_t)sizeof(DhTab));
-          tc::bulk_load(smem + TAB_OFF + slot * TAB_BYTES, p.tabs + tile, (uint32_t)sizeof(DhTab), &tabfull[slot]);
-        }
-        const long long m0 = (long long)tile * RT;
+        const long long m0 = (long long)tile * BM;
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
         const int grows = (int)min((long long)BM, p.g.R - m0);
         // (3-D W box: planes past J arrive zero-filled and count in full)
@@ -375,7 +224,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         constexpr int PF = 8;            // P~ boxes prefetched into L2 this many k-blocks ahead
         for (int kb = 0; kb < min(PF, p.nkb); ++kb) tc::tma_prefetch_2d(&tmP, kb * BK, (int)m0);
         // the epilogue's h boxes of this item: into L2 now, a mainloop ahead of their TMA loads
-        for (int bx = 0; bx < (min(NSUB, p.J - j0) + 63) / 64; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, (int)m0);
+        for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, (int)m0);
         for (int kb = 0; kb < p.nkb; ++kb) {
           if (kb + PF < p.nkb) tc::tma_prefetch_2d(&tmP, (kb + PF) * BK, (int)m0);
           tc::mbar_wait(&empty[stage], ph ^ 1);
@@ -395,12 +244,12 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         }
       }
     } else if (lane == 1) {
-      // ---- h boxes for the epilogue: box i (columns j0 + 64 i) serves chunk 2i of group 0 and 2i+1 of group 1
+      // ---- h boxes for the epilogue: box i (columns j0 + 64 i) serves chunks 2i and 2i+1
       int slot = 0;
       uint32_t ph = 0;
       for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
         const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
-        const int m0 = tile * RT, j0 = jp * NSUB;
+        const int m0 = tile * BM, j0 = jp * NSUB;
         const int nbox = (min(NSUB, p.J - j0) + 63) / 64;
         for (int bx = 0; bx < nbox; ++bx) {
           tc::mbar_wait(&hempty[slot], ph ^ 1);
@@ -439,7 +288,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       }
     }
   } else if (warp < EPI0) {
-    // ---- in-place dz producers: thread = (tile row, half): transforms 4 of the 8 chunks of its row
+    // ---- in-place dz producers: thread = (tile row, half): transforms 4 or 8 of the 8 chunks of its row
     constexpr int CPT = 8 * 4 / NTW;                 // chunks per thread: 8 (4 warps) or 4 (8 warps)
     const int pt = threadIdx.x - 64;
     const int rl = pt & 127, c_lo = (pt >> 7) * CPT;
@@ -447,15 +296,15 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     uint32_t ph = 0;
     for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++itx) {
       const int tile = p.live[idx / p.njp];
-      const long long m0 = (long long)tile * RT;
+      const long long m0 = (long long)tile * BM;
       const int grows = (int)min((long long)BM, p.g.R - m0);
       for (int kb = 0; kb < p.nkb; ++kb) {
         const int v0 = kb * BK;
         tc::mbar_wait(&loaded[stage], ph);
         if (pt == 0) dh_trace_kb(itx, kb, 1);
         uint8_t* sa = smem + stage * STAGE_BYTES;
-        const float4 gq = (rl < grows && rl < RT) ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
-                                                  : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+        const float4 gq = rl < grows ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
+                                     : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
         const int info = __float_as_int(gq.w);
         const uint32_t shi = bf16x2_splat(gq.x);
         const uint32_t slo = bf16x2_splat(gq.x - __uint_as_float(shi << 16));
@@ -485,38 +334,33 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       }
     }
   } else {
-    // ---- epilogue: box b = 64 columns; group g (4 warps, quadrant q4 = warp % 4 = TMEM lanes 32 q4 ..)
-    // drains columns 64 b + 32 g of its rows into D[g] (row rl, float4 slot i at i ^ (rl & 7)); then all
-    // 8 warps reduce the box, a thread per (output row, 4 columns): 16 threads per output row.
-    const int q4 = warp & 3, g = (warp - EPI0) >> 2;
+    // ---- epilogue: quadrant q4 = warp % 4 = TMEM lanes 32 q4 ..; thread = tile row, per 32-column chunk
+    // dpre = dh (1 - h^2) -> its row of dpre (128 B per chunk)
+    const int q4 = warp & 3;
     const int rl = 32 * q4 + lane;
-    const int et = threadIdx.x - 32 * EPI0;               // 0..255
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
+    const bool leader = warp == EPI0 && lane == 0;        // issues the TMA stores
     int it = 0, hslot = 0;
     uint32_t hph = 0;
+    long long kc = 0;                                     // chunk counter: dpre ring slot kc & 1
     for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
       const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
-      const int slot = it & 1, acc = it & 1;
-      const long long m0 = (long long)tile * RT, g0 = (long long)tile * F;
-      const long long r = m0 + rl;
-      const bool live = rl < RT && r < p.g.R && p.g.rowinfo[r] >= 0;
+      const int acc = it & 1;
+      const long long r = (long long)tile * BM + rl;
+      const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
       const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
       const int nbox = (nj + 63) / 64;
-      const DhTab* tb = reinterpret_cast<const DhTab*>(reinterpret_cast<const uint8_t*>(tabs_s) + slot * TAB_BYTES);
-
-      if (!generic) tc::mbar_wait(&tabfull[slot], (it >> 1) & 1);
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
       if (warp == EPI0 && lane == 0) dh_trace(it, 3);
-      const int nent = generic ? 0 : tb->nent;
-      const int nout = F + nent;
-      for (int bx = 0; bx < nbox; ++bx) {
-        const int c0 = 64 * bx + 32 * g;                   // this group's 32 columns
+      for (int ch = 0; ch < 2 * nbox; ++ch) {
+        const int g = ch & 1;                             // half of h box ch / 2
+        const int c0 = 32 * ch;
         const bool have = c0 < nj;
-        tc::mbar_wait(&hfull[hslot], hph);
+        if (g == 0) tc::mbar_wait(&hfull[hslot], hph);
         float accv[32];
         if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
-        if (bx == nbox - 1) {                            // last TMEM read of this accumulator
+        if (ch == 2 * nbox - 1) {                        // last TMEM read of this accumulator
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -537,129 +381,35 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
             out[8 * qq + 2 * i + 1] = ok ? accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
           }
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
-        if (++hslot == 2) { hslot = 0; hph ^= 1; }
-        if (generic) {
-          if (have && rl < RT && r < p.g.R) {
-            float4* dst = reinterpret_cast<float4*>(p.dpre_out + (size_t)r * p.J + j0 + c0);
-#pragma unroll
-            for (int qq = 0; qq < 8; ++qq)
-              if (qq < 2 * nq) dst[qq] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
-          }
-          continue;
+        if (g == 1) {                                    // both halves of this h box are done
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
+          if (++hslot == 2) { hslot = 0; hph ^= 1; }
         }
-        float4* D4 = reinterpret_cast<float4*>(dstage + g * D_BYTES);
+        if (!have) continue;
+        // ring slot kc & 1: the TMA store issued from it two chunks ago has finished reading it
+        uint8_t* ob = smem + O_OFF + (int)(kc & 1) * O_BYTES;
+        if (leader) tc::bulk_wait_read1();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        float4* O4 = reinterpret_cast<float4*>(ob);
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
-          D4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        // reduce: task t = (output o, 16 float4 columns of the box); o < F: d_enc of frame o, else d_dec
-        // entry o - F
-        const int ncol4 = min(64, nj - 64 * bx) / 4;
-        for (int t = et; t < nout * 16; t += 256) {
-          const int o = t >> 4, c16 = t & 15;
-          if (c16 >= ncol4) continue;
-          const float4* Dg = reinterpret_cast<const float4*>(dstage + (c16 >> 3) * D_BYTES);
-          const int qq = c16 & 7;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          float* dst;
-          if (o < F) {
-            if (!p.d_enc || g0 + o >= NT) continue;
-            for (int s = 0; s < S; ++s) {
-              const int rr = o * S + s;
-              const float4 x = Dg[rr * 8 + (qq ^ (rr & 7))];
-              v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
-            }
-            dst = p.d_enc + (size_t)(g0 + o) * p.J;
-          } else {
-            if (!p.d_dec) continue;
-            const int e = o - F;
-            const int k0 = tb->eoff[e], k1 = tb->eoff[e + 1];
-            for (int k = k0; k < k1; k += 4) {             // four rows per step (loads in flight)
-              float4 x[4];
-#pragma unroll
-              for (int m = 0; m < 4; ++m) {
-                const int rr = tb->erow[k + m < k1 ? k + m : k0];
-                x[m] = k + m < k1 ? Dg[rr * 8 + (qq ^ (rr & 7))] : make_float4(0.f, 0.f, 0.f, 0.f);
-              }
-#pragma unroll
-              for (int m = 0; m < 4; ++m) { v.x += x[m].x; v.y += x[m].y; v.z += x[m].z; v.w += x[m].w; }
-            }
-            const int w = tb->ent[e].w;
-            dst = w >= 0 ? p.d_dec + (size_t)w * p.J : p.g_part + (size_t)(-1 - w) * p.J;
-          }
-          reinterpret_cast<float4*>(dst + j0 + 64 * bx)[c16] = v;
+          O4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
+        tc::fence_proxy_async();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader) {
+          tc::tma_store_3d(&tmD, ob, j0 + c0, tile * BM, 0);
+          tc::bulk_commit();
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        ++kc;
       }
-      __syncwarp();
-      if (lane == 0 && !generic) tc::mbar_arrive(&tabempty[slot]);
       if (warp == EPI0 && lane == 0) dh_trace(it, 4);
     }
+    if (leader) tc::bulk_wait0();                         // every dpre store complete
   }
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tbase, 2 * NSUB);
-}
-
-// d_dec for the token positions whose covering frames span several tiles (sum of the boundary
-// partials in tile order), and zeros for u > U_n / infeasible utterances.  Positions complete in
-// one tile were written by joiner_dh_tc_kernel and are left untouched.  One warp per (n, u, 256-column group).
-__global__ void __launch_bounds__(256) ddec_fixup_kernel(const int32_t* __restrict__ ranges,
-                                                         const int2* __restrict__ urange,
-                                                         const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                         int F, int J, const float* __restrict__ part,
-                                                         float* __restrict__ d_dec) {
-  // one warp per (n, u, 256-column group): each warp's chain of dependent loads (lengths and
-  // coverage, the band offsets of the contributing tiles, their partial rows) is a few round trips,
-  // and the column groups of one u run in parallel instead of one after another in one warp
-  constexpr int GW = 64;                        // float4 columns per warp
-  const int J4 = J / 4, NG = (J4 + GW - 1) / GW;
-  const long long w = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (w >= (long long)N * (U + 1) * NG) return;
-  const long long nu = w / NG;
-  const int jg = (int)(w - nu * NG);
-  const int n = (int)(nu / (U + 1)), u = (int)(nu - (long long)n * (U + 1));
-  const int2 cov = urange[nu];
-  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  float4* dst = reinterpret_cast<float4*>(d_dec + (size_t)nu * J) + jg * GW;
-  const int jn = min(GW, J4 - jg * GW);       // float4 columns of this group
-  if (u > Un || (long long)Un > (long long)Tn * (S - 1)) {
-    for (int j = lane; j < jn; j += 32) dst[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
-  const long long gbase = (long long)n * T;
-  const long long k0 = (gbase + cov.x) / F, k1 = (gbase + cov.y - 1) / F;
-  if (k0 == k1) return;
-  const int32_t* pr = ranges + (size_t)n * T;
-  const int tb0 = (int)((k0 + 1) * F - gbase);                     // first frame of tile k0 + 1
-  const float4* first = reinterpret_cast<const float4*>(part + (((size_t)k0 * 2 + 1) * S + (u - pr[tb0])) * J) +
-                        jg * GW;
-  float4 acc[GW / 32];
-#pragma unroll
-  for (int q = 0; q < GW / 32; ++q) {
-    const int j = lane + 32 * q;
-    acc[q] = j < jn ? first[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  for (long long k = k0 + 1; k <= k1; ++k) {
-    const int ta = (int)(k * F - gbase);
-    const float4* src = reinterpret_cast<const float4*>(part + (((size_t)k * 2 + 0) * S + (u - pr[ta])) * J) + jg * GW;
-#pragma unroll
-    for (int q = 0; q < GW / 32; ++q) {
-      const int j = lane + 32 * q;
-      if (j < jn) {
-        const float4 x = src[j];
-        acc[q].x += x.x; acc[q].y += x.y; acc[q].z += x.z; acc[q].w += x.w;
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < GW / 32; ++q) {
-    const int j = lane + 32 * q;
-    if (j < jn) dst[j] = acc[q];
-  }
 }
 
 // ======================================================================= K11
@@ -1079,20 +829,20 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
 // ======================================================================= host
 template <int NTW>
 static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
-                               const CUtensorMap& th, cudaStream_t st) {
+                               const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
   smem_optin(joiner_dh_tc_kernel<NTW>, jdh::SMEM_BYTES);
-  joiner_dh_tc_kernel<NTW><<<grid, jdh::Roles<NTW>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, p);
+  joiner_dh_tc_kernel<NTW><<<grid, jdh::Roles<NTW>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, td, p);
   return cudaGetLastError();
 }
 // 4 producer warps for short V loops, 8 for long ones
 static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
-                             const CUtensorMap& th, cudaStream_t st) {
-  return p.nkb >= 32 ? launch_dh_k<8>(p, grid, tp, tw, th, st) : launch_dh_k<4>(p, grid, tp, tw, th, st);
+                             const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
+  return p.nkb >= 32 ? launch_dh_k<8>(p, grid, tp, tw, th, td, st) : launch_dh_k<4>(p, grid, tp, tw, th, td, st);
 }
 
-cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
-                             const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
-                             float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st) {
+// dpre = dh (1 - h^2) rows of the live 128-row tiles (`live`, count at `nlive`, at most ntiles) into dpre.
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
+                             const int* nlive, long long ntiles, float* dpre, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   const bool w3 = d.J % 64 == 0;
@@ -1100,44 +850,15 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
-  const int F = d.dh_frames();
-  const long long ntiles = d.dh_tiles();
-  cudaMemsetAsync(nlive, 0, sizeof(int), st);
-  RNNT_LAUNCH(KID_DENC, st, dh_tables_kernel<<<(unsigned)ntiles, 128, 0, st>>>(
-      ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, static_cast<DhTab*>(tabs), live, nlive, d_enc));
-  const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
-  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, F,
-                   static_cast<const DhTab*>(tabs), live, nlive, d_enc, d_dec, part, 0, F * d.S, nullptr};
-  p.w3 = w3;
-  const int nsm = current_sm_count();
-  const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, st));
-  if (d_dec)
-    RNNT_LAUNCH(KID_DDEC, st, ddec_fixup_kernel<<<(unsigned)(((long long)d.N * d.U1() * ((d.J / 4 + 63) / 64) + 7) / 8),
-                                                  256, 0, st>>>(
-        ranges, urange, bnd, d.N, d.T, d.U, d.S, F, d.J, part, d_dec));
-  return cudaGetLastError();
-}
-
-// Generic mode (the full, unpruned lattice of f4): tiles of 128 consecutive rows (the live ones in
-// `live`, count at `nlive`), dpre = dh (1 - h^2) written to `dpre_out` (R, J) fp32; the d_enc / d_dec
-// reductions run afterwards over the (t, u) grid.
-cudaError_t joiner_dh_generic_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
-                                     const int* live, const int* nlive, long long ntiles, float* dpre_out,
-                                     cudaStream_t st) {
-  CUtensorMap tp, tw, th;
-  if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
-  const bool w3 = d.J % 64 == 0;
-  if (w3 ? !make_tmap_bf16_3d(&tw, W, 64, d.V, d.J / 64, (uint64_t)d.J * 2, 128, 64, 64, 4)
-         : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
+  CUtensorMap td;   // dpre (R, J) fp32, box 32 columns x 128 rows
+  if (!make_tmap_f32_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 4, (uint64_t)d.rows() * d.J * 4, 32, jdh::BM))
     return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
-  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, d.N, d.T, d.U, d.S, 1,
-                   nullptr, live, nlive, nullptr, nullptr, nullptr, 0, jdh::BM, dpre_out, w3};
+  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0};
   const int nsm = current_sm_count();
   const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
-  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, st));
+  if (grid == 0) return cudaSuccess;
+  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, td, st));
   return cudaGetLastError();
 }
 

@@ -34,9 +34,9 @@ struct GradSrc {
   long long R;
   int V, VP, ntile;
 };
-cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W,
-                             const int32_t* ranges, const int2* urange, const int64_t* bnd, float* d_enc,
-                             float* d_dec, float* part, void* tabs, int* live, int* nlive, cudaStream_t st);
+cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
+                             const int* nlive, long long ntiles, float* dpre, cudaStream_t st);
+cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
 cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
                              int splits, cudaStream_t st);
 
@@ -692,14 +692,157 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
 }
 
 // Backward to the joiner input: K10 dh (and dpre), then d_enc / d_dec reductions.
+// Backward to the joiner input: K10 dpre = (dz W) (1 - h^2) per band row (joiner_bwd.cu), then the
+// band reductions
+//   d_enc[n,t,:] = sum_{s: p_t + s <= U_n} dpre[(n,t,s),:]
+//   d_dec[n,u,:] = sum_{t: p_t <= u < p_t + S} dpre[(n,t,u - p_t),:]      (frames [lo(u), hi(u)), Eq. 9)
+// in two balanced passes (a band stuck at p = 0 or p = Umax covers one u with hundreds of frames, so a
+// plain per-u gather is badly imbalanced):
+//   A (block per chunk of kBandCH frames): the chunk's d_enc rows, and for every u its frames cover the
+//     partial sum over the chunk's frames, stored at row p_{t0} + c S + (u - p_{t0}) of the utterance's
+//     partial buffer (U + 1 + S ceil(T / CH) rows: chunk c's rows lie below chunk c+1's since p is
+//     monotone);
+//   B (a warp per (u, 128 columns)): d_dec[u] = the partials of the chunks covering u, in chunk order.
+// Every output row is a fixed-order sum (deterministic); a warp per (output row, 512-B column segment)
+// with eight row loads in flight.  Padded rows and infeasible utterances get 0.
+// A: a warp per (chunk of kBandCH frames, utterance, 32-float4 column segment), lane = float4 column:
+// it walks the chunk's frames in order, loading the frame's S rows once (the next frame's rows are in
+// flight meanwhile), adds them into d_enc[t] and into a window win[k] = partial of u = base + k (base
+// = p_t; p is monotone, so a window entry is complete once p passes it: it is stored then and the
+// window shifts).  SW >= S (compile time) bounds the window.
+template <int SW>
+__global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict__ dpre,
+                                                         const int32_t* __restrict__ ranges,
+                                                         const int64_t* __restrict__ bnd, int N, int T, int U, int S,
+                                                         int J, float* __restrict__ d_enc, float* __restrict__ part) {
+  const int J4 = J / 4, nseg = (J4 + 31) / 32;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nch = (T + kBandCH - 1) / kBandCH;
+  if (w >= (long long)N * nch * nseg) return;
+  const int lane = threadIdx.x & 31;
+  const int seg = (int)(w % nseg);
+  const long long nc = w / nseg;
+  const int n = (int)(nc / nch), c = (int)(nc - (long long)n * nch);
+  const int q = seg * 32 + lane;
+  const bool qok = q < J4;
+  const int t0 = c * kBandCH, t1 = min(T, t0 + kBandCH);
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const bool feas = (long long)Un <= (long long)Tn * (S - 1);
+  const int te = feas ? min(t1, Tn) : t0;                  // live frames [t0, te)
+  const int32_t* pr = ranges + (size_t)n * T;
+  const float4* D = reinterpret_cast<const float4*>(dpre) + (size_t)n * T * S * J4;
+  float4* E = reinterpret_cast<float4*>(d_enc) + (size_t)n * T * J4;
+  float4* P = reinterpret_cast<float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + (size_t)c * S) * J4;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (d_enc && qok)
+    for (int t = max(t0, te); t < t1; ++t) E[(size_t)t * J4 + q] = z;          // padded / infeasible frames
+  if (te <= t0) return;
+  float4 win[SW];
+#pragma unroll
+  for (int k = 0; k < SW; ++k) win[k] = z;
+  int base = pr[t0];
+  auto flush = [&]() {                                     // u = base is complete
+    if (part && qok && base <= Un) P[(size_t)base * J4 + q] = win[0];
+#pragma unroll
+    for (int k = 0; k + 1 < SW; ++k) win[k] = win[k + 1];
+    win[SW - 1] = z;
+    ++base;
+  };
+  // FB frames per batch: all their rows' loads in flight together (register budget ~ 4 FB SW)
+  constexpr int FB = SW <= 5 ? 4 : (SW <= 10 ? 2 : 1);
+  for (int tb = t0; tb < te; tb += FB) {
+    float4 x[FB][SW];
+    int pf[FB];
+#pragma unroll
+    for (int f = 0; f < FB; ++f) {
+      const int t = tb + f;
+      pf[f] = t < te ? pr[t] : 0;
+      const int ns = t < te ? min(S, Un - pf[f] + 1) : 0;
+#pragma unroll
+      for (int s = 0; s < SW; ++s) x[f][s] = (s < ns && qok) ? D[((size_t)t * S + s) * J4 + q] : z;
+    }
+#pragma unroll
+    for (int f = 0; f < FB; ++f) {
+      const int t = tb + f;
+      if (t >= te) break;
+      while (base < pf[f]) flush();
+      float4 e = z;
+#pragma unroll
+      for (int s = 0; s < SW; ++s) {
+        e.x += x[f][s].x; e.y += x[f][s].y; e.z += x[f][s].z; e.w += x[f][s].w;
+        win[s].x += x[f][s].x; win[s].y += x[f][s].y; win[s].z += x[f][s].z; win[s].w += x[f][s].w;
+      }
+      if (d_enc && qok) E[(size_t)t * J4 + q] = e;
+    }
+  }
+  const int ue = min(Un, pr[te - 1] + S - 1);
+  while (base <= ue) flush();
+}
+// B: a warp per (utterance, u, 32-float4 column segment): the partials of the chunks covering u, in
+// chunk order, eight loads in flight.
+__global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__ part, const int2* __restrict__ urange,
+                                                       const int64_t* __restrict__ bnd, int N, int T, int U, int S,
+                                                       int J, float* __restrict__ d_dec) {
+  const int J4 = J / 4, nseg = (J4 + 31) / 32;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= (long long)N * (U + 1) * nseg) return;
+  const long long nu = w / nseg;
+  const int q = (int)(w - nu * nseg) * 32 + lane;
+  const int n = (int)(nu / (U + 1)), u = (int)(nu - (long long)n * (U + 1));
+  const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+  const bool feas = (long long)Un <= (long long)Tn * (S - 1);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (feas && u <= Un) {
+    const int2 cv = urange[nu];                            // frames [lo, hi) cover u
+    const int c0 = cv.x / kBandCH, c1 = (cv.y - 1) / kBandCH;
+    const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4;
+    for (int cb = c0; cb <= c1; cb += 8) {
+      float4 x[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        x[m] = (cb + m <= c1 && q < J4) ? P[(size_t)(cb + m) * S * J4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) { a.x += x[m].x; a.y += x[m].y; a.z += x[m].z; a.w += x[m].w; }
+    }
+  }
+  if (q < J4) reinterpret_cast<float4*>(d_dec + (size_t)nu * J)[q] = a;
+}
+
 cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                     const int32_t* ranges, const int64_t* bnd, float* d_enc, float* d_dec,
                                     cudaStream_t st) {
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
-  if ((e = joiner_dh_launch(d, g, h, W, ranges, w.urange, bnd, d_enc, d_dec, w.dpart, w.dhtab, w.dhlive,
-                            w.dhlive + d.dh_tiles(), st)) != cudaSuccess) return e;
+  const long long ntiles = (d.rows() + 127) / 128;
+  if ((e = live_tiles_launch(w.tlive, ntiles, w.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
+  if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, st)) != cudaSuccess) return e;
+  {
+    const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * ((d.J / 4 + 31) / 32);
+    const unsigned nb = (unsigned)((nwarp + 7) / 8);
+    float* pp = d_dec ? w.bpart : nullptr;
+#define RNNT_BAND(SWV) band_chunk_kernel<SWV><<<nb, 256, 0, st>>>(w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp)
+    switch (d.S) {   // the window is exactly S wide for the common band widths
+      case 1: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(1)); break;
+      case 2: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(2)); break;
+      case 3: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(3)); break;
+      case 4: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(4)); break;
+      case 5: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(5)); break;
+      case 6: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(6)); break;
+      case 7: case 8: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(8)); break;
+      case 9: case 10: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(10)); break;
+      default:
+        if (d.S <= 16) RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(16));
+        else RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(32));
+    }
+#undef RNNT_BAND
+  }
+  if (d_dec) {
+    const long long nw = (long long)d.N * d.U1() * ((d.J / 4 + 31) / 32);
+    RNNT_LAUNCH(KID_DDEC, st, band_dec_kernel<<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+                                  w.bpart, w.urange, bnd, d.N, d.T, d.U, d.S, d.J, d_dec));
+  }
   return cudaGetLastError();
 }
 

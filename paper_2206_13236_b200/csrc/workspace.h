@@ -34,13 +34,18 @@ struct Dims {
   int VP64() const { return (V + 63) / 64 * 64; }       // bf16 pitch of the E operands (K-major boxes of 64)
   int UP() const { return (U + 1 + 63) / 64 * 64; }      // bf16 pitch of G~ (t-major, K-major boxes of 64)
   int ntb() const { return (T + 31) / 32; }              // 32-frame blocks of the occupancy column partials
-  int dh_frames() const { return S <= 128 ? 128 / S : 1; }                // frames per joiner_dh tile
-  long long dh_tiles() const { return ((long long)N * T + dh_frames() - 1) / dh_frames(); }
   int ntile() const { return (V + 127) / 128; }        // kVT-wide max-shift tiles
   int VP() const { return (V + 127) / 128 * 128; }      // padded row pitch of P~ (elements)
 };
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// d_dec partials of the band reduction (pruned.cu band_chunk_kernel): chunks of kBandCH frames; per
+// utterance U + 1 + S ceil(T / kBandCH) rows (chunk c's partial of u at row u + c S).
+constexpr int kBandCH = 16;
+__host__ __device__ inline long long band_part_rows(int T, int U, int S) {
+  return (long long)U + 1 + (long long)S * ((T + kBandCH - 1) / kBandCH);
+}
 
 // Interpolation weights of the smoothed trivial joiner (Eq. 11): a_lm = lm_only_scale, a_ac =
 // am_only_scale; both 0 is the plain trivial joiner.
@@ -102,9 +107,9 @@ struct PrunedWS {
   float* gb;         // (R) empty'_p
   float* gl;         // (R) y'_p
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
-  float* dpart;      // (dh_tiles,2,S,J) d_dec boundary partials of the joiner_dh tiles
-  void* dhtab;       // (dh_tiles) joiner_dh tile tables (2704 B each, joiner_bwd.cu DhTab)
-  int* dhlive;       // (dh_tiles + 1) ids of the live joiner_dh tiles, then their count
+  int* dhlive;       // (R/128 + 1) ids of the live 128-row joiner_dh tiles, then their count
+  float* dpre;       // (R,J) dpre = dh (1 - h^2) of every band row (live rows only are written)
+  float* bpart;      // (N, band_part_rows, J) d_dec partials of the band reduction
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
   int splits;
@@ -112,8 +117,6 @@ struct PrunedWS {
 
 // K11 variant: "wide" CTAs (one per SM) hold two V tiles (256 v x 256 j, 512 TMEM columns) so each
 // h k-block feeds two MMAs; used for large V (L2 -> SM bound), RNNT_DW_WIDE=0/1 forces it off/on.
-constexpr size_t kDhTabBytes = 2848;   // sizeof(DhTab) (joiner_bwd.cu static_asserts it)
-
 inline bool dw_wide(const Dims& d) {
   static const int force = env_int("RNNT_DW_WIDE", -1);
   if (force >= 0) return force == 1;
@@ -209,13 +212,11 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.gb = (float*)take(R * 4);
   p.gl = (float*)take(R * 4);
   p.gpk = (float4*)take(R * NT * 16);
-  // frame-aligned joiner_dh tables (S <= 128); the full-lattice path (S = U+1 > 128 possible) uses
-  // 128-row tiles instead and only the live list
-  const bool framed = d.S <= 128;
-  const size_t ltiles = framed ? (size_t)d.dh_tiles() : (R + 127) / 128;
-  p.dpart = (float*)take(framed ? (size_t)d.dh_tiles() * 2 * d.S * J * 4 : 0);
-  p.dhtab = take(framed ? (size_t)d.dh_tiles() * kDhTabBytes : 0);
-  p.dhlive = (int*)take((ltiles + 1) * 4);
+  // joiner_dh: ids of the live 128-row tiles (+ count), and dpre = dh (1 - h^2) per band row, which
+  // band_reduce_kernel turns into d_enc / d_dec
+  p.dhlive = (int*)take(((R + 127) / 128 + 1) * 4);
+  p.dpre = (float*)take(R * J * 4);
+  p.bpart = (float*)take((size_t)N * band_part_rows(d.T, d.U, d.S) * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);
   if (sw) *sw = s;
@@ -241,7 +242,7 @@ inline size_t carve_full(const Dims& df, void* base, SimpleWS* sw, PrunedWS* pw,
   };
   FullWS f;
   f.ranges0 = (int32_t*)take((size_t)df.N * df.T * 4);
-  f.dpre = (float*)take((size_t)df.rows() * df.J * 4);
+  f.dpre = pw ? pw->dpre : nullptr;        // the pruned region's dpre rows (R = N T (U+1) here)
   f.h = (uint16_t*)take((size_t)df.rows() * df.J * 2);
   if (fw) *fw = f;
   return off + 256;

@@ -103,29 +103,38 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
 // joiner_dh: dh = dz W over (live 128-row tile, 256-column part of J) work items, persistent, every
 // role pipelined across items:
 //   warp 0      lane 0: TMA producer: per 64-logit k-block the P~ tile, the W boxes and the rows' packed
-//               scalars into a 3-stage ring (the item's h boxes are prefetched into L2 at its start);
-//               lane 1: the epilogue's h boxes (64 columns x 128 rows) into a 2-slot ring
+//               scalars into a 4-stage ring (the item's h boxes are prefetched into L2 at its start,
+//               the epilogue reads its rows of h from there)
 //   warp 1      TMEM allocator (2 x 256 columns) and single-thread MMA issuer
 //   warps 2..   in-place dz producers (4 or 8 warps: a thread per row or half row), release each
 //               stage to the MMA
 //   4 epilogue  one per TMEM lane quadrant, thread = tile row, 32-column chunks: dpre = dh (1 - h^2)
-//   warps       into a swizzled 16 KB smem tile (2-slot ring), written to the fp32 dpre (R, J) by one TMA
-//               store per chunk; the accumulator of item k+1 fills while item k drains.
+//   warps       into a swizzled 16 KB smem tile, written to the fp32 dpre (R, J) by one TMA store per
+//               chunk; the accumulator of item k+1 fills while item k drains.
 // The reductions d_enc[t] = sum_s dpre[(t,s)] and d_dec[u] = sum_{t: p_t <= u < p_t + S} dpre[(t, u - p_t)]
 // run afterwards in band_reduce_kernel (pruned.cu): a streaming pass at HBM speed, deterministic, that
 // keeps this kernel's epilogue far shorter than its mainloop.
 namespace jdh {
-constexpr int BM = 128, BK = 64, NSUB = 256, STAGES = 3;
+constexpr int BM = 128, BK = 64, NSUB = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB, K-major (TMA box 64 v x 128 rows of P~)
 constexpr int B_BYTES = NSUB * BK * 2;         // 32 KB, MN-major (4 boxes of 64 j x 64 v)
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;   // 50 KB (1024-aligned)
-constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B), ring of 2
-constexpr int O_BYTES = BM * 32 * 4;           // one 32-column dpre chunk (128 rows x 128 B, SWIZZLE_128B), ring of 2
-constexpr int H_OFF = STAGES * STAGE_BYTES;
-constexpr int O_OFF = H_OFF + 2 * H_BYTES;
-constexpr int BAR_OFF = O_OFF + 2 * O_BYTES;
-constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
+constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B)
+constexpr int O_BYTES = BM * 32 * 4;           // one 32-column dpre chunk (128 rows x 128 B, SWIZZLE_128B)
+// Shared memory per variant.  Short V loops (4 producer warps, item = a few k-blocks): 3 stages, h by
+// TMA into a 2-slot ring, 2 dpre staging tiles (the epilogue is on the critical path).  Long V loops
+// (8 producer warps): 4 stages (the per-stage chain load -> dz transform -> MMA is what bounds the
+// mainloop), h read from L2 by the epilogue, 1 staging tile.
+template <int NTW> struct Cfg {
+  static constexpr int STAGES = NTW == 8 ? 4 : 3;
+  static constexpr int HRING = NTW == 8 ? 0 : 2;
+  static constexpr int ORING = NTW == 8 ? 1 : 2;
+  static constexpr int H_OFF = STAGES * STAGE_BYTES;
+  static constexpr int O_OFF = H_OFF + HRING * H_BYTES;
+  static constexpr int BAR_OFF = O_OFF + ORING * O_BYTES;
+  static constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
+};
 // in-place dz producer warps: 4 (a thread per row) for short V loops, 8 (a thread per half row) when
 // the mainloop is long
 template <int NTW> struct Roles {
@@ -136,6 +145,7 @@ template <int NTW> struct Roles {
 
 struct JoinerDhParams {
   GradSrc g;
+  const uint16_t* h;       // (R, J) bf16 joiner input (the epilogue's 1 - h^2)
   int J, nkb, njp;
   const int* live;         // ids of the 128-row tiles with a live row (order irrelevant)
   const int* nlive;        // their count
@@ -164,32 +174,47 @@ __device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
   if (g_dh_trace && it < 3 && kb < 8) g_dh_trace[148 * 16 * 5 + (((size_t)blockIdx.x * 3 + it) * 8 + kb) * 4 + k] = gtimer();
 }
 
-template <int NTW>
+// MC: clusters of two CTAs working on two row tiles with the same 256-column part of J in lockstep;
+// each CTA TMA-loads half of every W k-block with .multicast::cluster into both CTAs' stage, so the
+// L2 -> SM traffic per MMA drops from 50 to 34 KB per k-block (the contraction is L2-bandwidth bound at
+// large V).  A stage is refilled once both CTAs' MMAs released it (each MMA commit arrives on both
+// CTAs' empty barrier).
+template <int NTW, bool MC>
 __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
                         JoinerDhParams p) {
   using namespace jdh;
   constexpr int EPI0 = Roles<NTW>::EPI0;
+  constexpr int STAGES = Cfg<NTW>::STAGES, HRING = Cfg<NTW>::HRING, ORING = Cfg<NTW>::ORING;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
-  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + Cfg<NTW>::BAR_OFF);
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;       // [2]
   uint64_t* tempty = tfull + 2;           // [2]
-  uint64_t* hfull = tempty + 2;           // [2]
+  uint64_t* hfull = tempty + 2;           // [2] (HRING > 0)
   uint64_t* hempty = hfull + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
-  uint8_t* hbuf = smem + H_OFF;
+  uint8_t* hbuf = smem + Cfg<NTW>::H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long nitems = (long long)(*p.nlive) * p.njp;
+  // work items: (row tile, 256-column part); with MC a cluster takes (tile pair, part) items, rank r the
+  // tile 2 i + r (an odd last tile is done by both CTAs: identical values, written twice)
+  const int nlive = *p.nlive;
+  const int crank = MC ? (int)tc::cluster_ctarank() : 0;
+  const long long cid = MC ? blockIdx.x / 2 : blockIdx.x, ncl = MC ? gridDim.x / 2 : gridDim.x;
+  const long long nitems = (long long)(MC ? (nlive + 1) / 2 : nlive) * p.njp;
+  auto item_tile = [&](long long idx) {
+    const long long pi = idx / p.njp;
+    return MC ? p.live[min(2 * pi + crank, (long long)nlive - 1)] : p.live[pi];
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
       tc::mbar_init(&full[s], NTW);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], MC ? 2 : 1);   // MC: both CTAs' MMA commits
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
@@ -205,6 +230,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * NSUB);
   tc::fence_before_sync();
   __syncthreads();
+  if (MC) tc::cluster_sync();             // the peer's barriers are initialised before any multicast
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
 
@@ -213,8 +239,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       // ---- TMA producer
       int stage = 0, it = 0;
       uint32_t ph = 0;
-      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
-        const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+      for (long long idx = cid; idx < nitems; idx += ncl, ++it) {
+        const int tile = item_tile(idx), jp = (int)(idx % p.njp);
         dh_trace(it, 0);
         const long long m0 = (long long)tile * BM;
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
@@ -232,7 +258,15 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           dh_trace_kb(it, kb, 0);
           tc::mbar_arrive_expect_tx(&loaded[stage], bytes);
           tc::tma_load_2d(sa, &tmP, &loaded[stage], kb * BK, (int)m0);
-          if (p.w3) {
+          if (MC) {                      // this CTA's half of the W boxes, into both CTAs' stage
+            if (p.w3) {
+              tc::tma_load_3d_mc(sa + A_BYTES + crank * 2 * (64 * BK * 2), &tmW, &loaded[stage], 0, kb * BK,
+                                 j0 / 64 + 2 * crank, 3);
+            } else {
+              for (int bx = crank; bx < nbox; bx += 2)
+                tc::tma_load_2d_mc(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK, 3);
+            }
+          } else if (p.w3) {
             tc::tma_load_3d(sa + A_BYTES, &tmW, &loaded[stage], 0, kb * BK, j0 / 64);
           } else {
             for (int bx = 0; bx < nbox; ++bx)
@@ -243,19 +277,19 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
-    } else if (lane == 1) {
+    } else if (lane == 1 && HRING > 0) {
       // ---- h boxes for the epilogue: box i (columns j0 + 64 i) serves chunks 2i and 2i+1
       int slot = 0;
       uint32_t ph = 0;
-      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-        const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+      for (long long idx = cid; idx < nitems; idx += ncl) {
+        const int tile = item_tile(idx), jp = (int)(idx % p.njp);
         const int m0 = tile * BM, j0 = jp * NSUB;
         const int nbox = (min(NSUB, p.J - j0) + 63) / 64;
         for (int bx = 0; bx < nbox; ++bx) {
           tc::mbar_wait(&hempty[slot], ph ^ 1);
           tc::mbar_arrive_expect_tx(&hfull[slot], H_BYTES);
           tc::tma_load_2d(hbuf + slot * H_BYTES, &tmH, &hfull[slot], j0 + bx * 64, m0);
-          if (++slot == 2) { slot = 0; ph ^= 1; }
+          if (++slot == HRING) { slot = 0; ph ^= 1; }
         }
       }
     }
@@ -265,7 +299,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       constexpr uint32_t idesc = tc::idesc_bf16(BM, NSUB, false, true);
       int stage = 0, it = 0;
       uint32_t ph = 0;
-      for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
+      for (long long idx = cid; idx < nitems; idx += ncl, ++it) {
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after_sync();
@@ -280,7 +314,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           for (int k = 0; k < BK / 16; ++k)
             tc::mma_bf16(d, tc::sdesc(a + 32 * k, 16, 1024), tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024), idesc,
                          (kb | k) != 0);
-          tc::mma_commit(&empty[stage]);
+          if (MC) tc::mma_commit_mc(&empty[stage], 3);   // releases the stage in both CTAs
+          else tc::mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
         tc::mma_commit(&tfull[acc]);
@@ -294,8 +329,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     const int rl = pt & 127, c_lo = (pt >> 7) * CPT;
     int stage = 0, itx = 0;
     uint32_t ph = 0;
-    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++itx) {
-      const int tile = p.live[idx / p.njp];
+    for (long long idx = cid; idx < nitems; idx += ncl, ++itx) {
+      const int tile = item_tile(idx);
       const long long m0 = (long long)tile * BM;
       const int grows = (int)min((long long)BM, p.g.R - m0);
       for (int kb = 0; kb < p.nkb; ++kb) {
@@ -342,9 +377,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     const bool leader = warp == EPI0 && lane == 0;        // issues the TMA stores
     int it = 0, hslot = 0;
     uint32_t hph = 0;
-    long long kc = 0;                                     // chunk counter: dpre ring slot kc & 1
-    for (long long idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++it) {
-      const int tile = p.live[idx / p.njp], jp = (int)(idx % p.njp);
+    long long kc = 0;                                     // chunk counter: staging tile kc % ORING
+    for (long long idx = cid; idx < nitems; idx += ncl, ++it) {
+      const int tile = item_tile(idx), jp = (int)(idx % p.njp);
       const int acc = it & 1;
       const long long r = (long long)tile * BM + rl;
       const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
@@ -354,10 +389,23 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       tc::fence_after_sync();
       if (warp == EPI0 && lane == 0) dh_trace(it, 3);
       for (int ch = 0; ch < 2 * nbox; ++ch) {
-        const int g = ch & 1;                             // half of h box ch / 2
         const int c0 = 32 * ch;
         const bool have = c0 < nj;
-        if (g == 0) tc::mbar_wait(&hfull[hslot], hph);
+        const int nq = have ? min(4, (nj - c0) / 8) : 0;   // J % 8 == 0
+        uint4 hv[4];                                       // this row's h for the chunk
+        if (HRING > 0) {
+          if ((ch & 1) == 0) tc::mbar_wait(&hfull[hslot], hph);
+          const uint8_t* hb = hbuf + hslot * H_BYTES;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            hv[qq] = (qq < nq && live) ? *reinterpret_cast<const uint4*>(hb + sw128(rl, 4 * (ch & 1) + qq))
+                                       : make_uint4(0, 0, 0, 0);
+        } else {                                           // (L2-resident: prefetched at the item's start)
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            hv[qq] = (qq < nq && live) ? __ldg(reinterpret_cast<const uint4*>(p.h + (size_t)r * p.J + j0 + c0) + qq)
+                                       : make_uint4(0, 0, 0, 0);
+        }
         float accv[32];
         if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
         if (ch == 2 * nbox - 1) {                        // last TMEM read of this accumulator
@@ -365,14 +413,10 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
         }
-        const uint8_t* hb = hbuf + hslot * H_BYTES;
-        const int nq = have ? min(4, (nj - c0) / 8) : 0;   // J % 8 == 0
         float out[32];
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
-          uint4 hv = make_uint4(0, 0, 0, 0);
-          if (qq < nq && live) hv = *reinterpret_cast<const uint4*>(hb + sw128(rl, 4 * g + qq));
-          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+          const uint32_t hw[4] = {hv[qq].x, hv[qq].y, hv[qq].z, hv[qq].w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
@@ -381,15 +425,18 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
             out[8 * qq + 2 * i + 1] = ok ? accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
           }
         }
-        if (g == 1) {                                    // both halves of this h box are done
+        if (HRING > 0 && ((ch & 1) == 1 || ch == 2 * nbox - 1)) {   // both halves of this h box are used
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
-          if (++hslot == 2) { hslot = 0; hph ^= 1; }
+          if (++hslot == HRING) { hslot = 0; hph ^= 1; }
         }
         if (!have) continue;
-        // ring slot kc & 1: the TMA store issued from it two chunks ago has finished reading it
-        uint8_t* ob = smem + O_OFF + (int)(kc & 1) * O_BYTES;
-        if (leader) tc::bulk_wait_read1();
+        // staging tile kc % ORING: the TMA store issued from it ORING chunks ago has finished reading it
+        uint8_t* ob = smem + Cfg<NTW>::O_OFF + (int)(kc % ORING) * O_BYTES;
+        if (leader) {
+          if (ORING == 2) tc::bulk_wait_read1();
+          else tc::bulk_wait_read0();
+        }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         float4* O4 = reinterpret_cast<float4*>(ob);
 #pragma unroll
@@ -409,6 +456,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (MC) tc::cluster_sync();             // no multicast write or arrive targets an exited peer
   if (warp == 1) tc::tmem_dealloc(tbase, 2 * NSUB);
 }
 
@@ -827,17 +875,37 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
 }
 
 // ======================================================================= host
-template <int NTW>
+template <int NTW, bool MC>
 static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
                                const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
-  smem_optin(joiner_dh_tc_kernel<NTW>, jdh::SMEM_BYTES);
-  joiner_dh_tc_kernel<NTW><<<grid, jdh::Roles<NTW>::THREADS, jdh::SMEM_BYTES, st>>>(tp, tw, th, td, p);
-  return cudaGetLastError();
+  constexpr int SMEM = jdh::Cfg<NTW>::SMEM_BYTES;
+  smem_optin(joiner_dh_tc_kernel<NTW, MC>, SMEM);
+  if (!MC) {
+    joiner_dh_tc_kernel<NTW, MC><<<grid, jdh::Roles<NTW>::THREADS, SMEM, st>>>(tp, tw, th, td, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(jdh::Roles<NTW>::THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, joiner_dh_tc_kernel<NTW, MC>, tp, tw, th, td, p);
 }
-// 4 producer warps for short V loops, 8 for long ones
-static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
-                             const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
-  return p.nkb >= 32 ? launch_dh_k<8>(p, grid, tp, tw, th, td, st) : launch_dh_k<4>(p, grid, tp, tw, th, td, st);
+// 4 producer warps for short V loops, 8 for long ones; W multicast over CTA pairs (RNNT_DH_MC=0: off)
+static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, bool mc, const CUtensorMap& tp,
+                             const CUtensorMap& tw, const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
+  if (mc)
+    return p.nkb >= 32 ? launch_dh_k<8, true>(p, grid, tp, tw, th, td, st)
+                       : launch_dh_k<4, true>(p, grid, tp, tw, th, td, st);
+  return p.nkb >= 32 ? launch_dh_k<8, false>(p, grid, tp, tw, th, td, st)
+                     : launch_dh_k<4, false>(p, grid, tp, tw, th, td, st);
 }
 
 // dpre = dh (1 - h^2) rows of the live 128-row tiles (`live`, count at `nlive`, at most ntiles) into dpre.
@@ -845,8 +913,11 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                              const int* nlive, long long ntiles, float* dpre, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
+  static const int mc_env = env_int("RNNT_DH_MC", 1);
+  const bool mc = mc_env != 0 && ntiles >= 2;
   const bool w3 = d.J % 64 == 0;
-  if (w3 ? !make_tmap_bf16_3d(&tw, W, 64, d.V, d.J / 64, (uint64_t)d.J * 2, 128, 64, 64, 4)
+  // W as 3-D (64 j, V, J/64) boxes of 4 planes (one TMA per k-block), or 2 planes per CTA with multicast
+  if (w3 ? !make_tmap_bf16_3d(&tw, W, 64, d.V, d.J / 64, (uint64_t)d.J * 2, 128, 64, 64, mc ? 2 : 4)
          : !make_tmap_bf16_2d(&tw, W, d.J, d.V, (uint64_t)d.J * 2, 64, 64))
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
@@ -854,11 +925,12 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   if (!make_tmap_f32_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 4, (uint64_t)d.rows() * d.J * 4, 32, jdh::BM))
     return cudaErrorInvalidValue;
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
-  JoinerDhParams p{g, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0};
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0};
   const int nsm = current_sm_count();
-  const unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
+  unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
+  if (mc) grid = (unsigned)std::min<long long>((ntiles + 1) / 2 * njp, nsm / 2) * 2;
   if (grid == 0) return cudaSuccess;
-  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, tp, tw, th, td, st));
+  RNNT_LAUNCH(KID_DH, st, launch_dh(p, grid, mc, tp, tw, th, td, st));
   return cudaGetLastError();
 }
 

@@ -83,6 +83,10 @@ const char* rnnt_status_string(rnnt_status_t s);
 /* Library build string: kernels compiled and the sm target. */
 const char* rnnt_version(void);
 
+/* The CUDA error string behind the last RNNT_ERR_CUDA returned to the calling host thread
+ * (static string, never NULL; "no error" before any). */
+const char* rnnt_last_cuda_error(void);
+
 /* ---- Diagnostics (bench.py; not needed for computing the loss) ----
  * rnnt_launch_count: number of kernels the library has launched from the calling host
  *   thread (monotone counter).

@@ -67,6 +67,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_status_string.restype = ctypes.c_char_p
     lib.rnnt_version.argtypes = []
     lib.rnnt_version.restype = ctypes.c_char_p
+    lib.rnnt_last_cuda_error.argtypes = []
+    lib.rnnt_last_cuda_error.restype = ctypes.c_char_p
     lib.rnnt_simple_loss.argtypes = [P, P, P, P, DP, F, P, P, P, P, P, P, P, SZ, P]
     lib.rnnt_simple_loss.restype = I32
     lib.rnnt_simple_loss_backward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
@@ -136,7 +138,10 @@ def _stream(stream):
 
 def _check(rc: int, what: str):
     if rc != RNNT_OK:
-        msg = load_library().rnnt_status_string(rc).decode()
+        lib = load_library()
+        msg = lib.rnnt_status_string(rc).decode()
+        if msg == "RNNT_ERR_CUDA":
+            msg += " (" + lib.rnnt_last_cuda_error().decode() + ")"
         raise RNNTError(f"{what} failed: {msg}")
 
 

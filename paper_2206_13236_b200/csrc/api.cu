@@ -90,7 +90,12 @@ static rnnt_status_t check_dims(const rnnt_dims_t* dims, Dims* d) {
   return RNNT_OK;
 }
 
-static rnnt_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? RNNT_OK : RNNT_ERR_CUDA; }
+static thread_local const char* g_last_cuda_error = "no error";
+static rnnt_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RNNT_OK;
+  g_last_cuda_error = cudaGetErrorString(e);
+  return RNNT_ERR_CUDA;
+}
 
 extern "C" {
 
@@ -131,6 +136,8 @@ const char* rnnt_status_string(rnnt_status_t s) {
 }
 
 uint64_t rnnt_launch_count(void) { return g_launches; }
+
+const char* rnnt_last_cuda_error(void) { return g_last_cuda_error; }
 
 int32_t rnnt_kernel_count(void) { return KID_COUNT; }
 

@@ -63,12 +63,12 @@ typedef enum {
 
 /* Padded problem sizes. T, U are the batch maxima; V includes the blank id 0;
  * J is the joiner hidden size; S the band width (s_range).
- * Limits: 1 <= N, 1 <= T <= 65536, 0 <= U <= 575 and U < T*64, 2 <= V, 8 <= J <= 4096 and
- * J % 8 == 0, 1 <= S <= 32.  U <= 575 because the occupancy combine stages 3 x 32 x round64(U+1)
- * fp32 in shared memory; the pruned recursion (rnnt_pruned_loss*) additionally needs
- * T*S*8 + T*4 bytes of staged arcs plus the chunk matrices <= 224 KB (T <~ 2,600 frames at S = 10,
- * <~ 5,000 at S = 5).  Outside these limits the calls return RNNT_ERR_UNSUPPORTED (or
- * RNNT_ERR_INVALID_ARG for the argument ranges) and launch nothing. */
+ * Limits: 1 <= N, 1 <= T <= 65536, 0 <= U <= 1023 and U < T*64, 2 <= V, 8 <= J <= 4096 and
+ * J % 8 == 0, 1 <= S <= 32.  U <= 1023 because the simple-lattice wavefront holds a row of U+1
+ * cells in at most 4 warps x 32 lanes x 8 registers.  Long utterances are supported: the pruned
+ * recursion stages an utterance's band arcs in shared memory when they fit and reads them from L2
+ * otherwise.  Outside these limits the calls return RNNT_ERR_UNSUPPORTED (or RNNT_ERR_INVALID_ARG for
+ * the argument ranges) and launch nothing. */
 typedef struct {
   int32_t N, T, U, V, J, S;
 } rnnt_dims_t;

@@ -86,7 +86,6 @@ static rnnt_status_t check_dims(const rnnt_dims_t* dims, Dims* d) {
   if ((long long)d->U >= (long long)d->T * 64) return RNNT_ERR_INVALID_ARG;
   if (d->J < 8 || d->J > 4096 || d->J % 8) return RNNT_ERR_INVALID_ARG;
   if (d->lat_R() == 0) return RNNT_ERR_UNSUPPORTED;   // recursion kernel: one warp x <= 32 columns per lane
-  if (d->UP() > 576) return RNNT_ERR_UNSUPPORTED;     // combine kernel: 3 x 32 x UP fp32 staging in smem
   return RNNT_OK;
 }
 

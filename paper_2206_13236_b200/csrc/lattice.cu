@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 //            the outflow of a diagonal sums to 1);
 //   phase B: the normalised values written t-major (shared memory only): px_grad, py_grad, G~ and
 //            y' as bf16 hi + lo; the cells of row t in this block are the contiguous columns u = k - t.
+constexpr int kCombineWindow = 512;   // staged columns per pass (3 x 32 x 512 fp32 = 192 KB)
 __global__ void __launch_bounds__(256) combine_kernel(
     const float2* __restrict__ pxy, const float* __restrict__ rS,
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
@@ -315,9 +316,10 @@ __global__ void __launch_bounds__(256) combine_kernel(
     uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo, uint16_t* __restrict__ Yp_hi,
     uint16_t* __restrict__ Yp_lo) {
   extern __shared__ __align__(16) float cbuf[];
-  float* Ys = cbuf;                     // [32][UP]
-  float* Bs = cbuf + 32 * UP;           // [32][UP]
-  float* Gs = cbuf + 64 * UP;           // [32][UP]
+  const int CWs = min(UP, kCombineWindow);
+  float* Ys = cbuf;                     // [32][CW]
+  float* Bs = cbuf + 32 * CWs;          // [32][CW]
+  float* Gs = cbuf + 64 * CWs;          // [32][CW]
   // per diagonal and strip: ob = A^w_k + B^w_{k+1} - L (blank arc, same column), ox = A^w_k +
   // B^{w+1}_{k+1} - L (label arc out of the strip's last column into the next strip)
   __shared__ float s_ob[32][lat::MAXW], s_ox[32][lat::MAXW], s_rz[32];
@@ -342,9 +344,25 @@ __global__ void __launch_bounds__(256) combine_kernel(
   }
   __syncthreads();
 
-  // phase A: one warp per diagonal of the block; the row is read in groups of four 32-column chunks
+  // phase A: one warp per diagonal of the block; the row is read in groups of four 32-column chunks.
+  // Rows wider than the staging window CW (U + 1 > CW) take two passes: the diagonal sums first, then
+  // per column window the normalised values recomputed, staged and written (phase B).
   constexpr int CG = 4;
-  for (int kr = warp; kr < 32; kr += 8) {
+  const int CW = min(UP, kCombineWindow);
+  const bool one = UP <= CW;
+  auto cell = [&](int kr, int u, float a, float2 xy, float b0, float b1, float r, float& yv, float& bv, float& gv) {
+    const int k = k0 + kr;
+    const int ulo = max(0, k - Tn + 1), uhi = min(k, Un);
+    yv = 0.f; bv = 0.f;
+    if (u >= ulo && u <= uhi) {
+      const int w = u >> lsw;                 // SW = 32 R is a power of two
+      bv = ex2_approx(a + xy.y + b0 + s_ob[kr][w]);
+      if (u < Un) yv = ex2_approx(a + xy.x + b1 + (((u & (SW - 1)) == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+    }
+    gv = (yv + bv) * r;
+  };
+  // values of diagonal kr for columns [u0, u0 + 32 CG) of the window starting at c0 (stage: write to smem)
+  auto diag_pass = [&](int kr, int ub, int ue, int c0, bool stage) -> float {
     const int k = k0 + kr;
     const bool live = finite && k < Kn;
     const int ulo = live ? max(0, k - Tn + 1) : 1, uhi = live ? min(k, Un) : 0;
@@ -353,13 +371,13 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float2* XY = pxy + base + (size_t)k * LU;
     const float* Rr = rS + base + (size_t)k * LU;
     float z = 0.f;
-    for (int u0 = 0; u0 < UP; u0 += 32 * CG) {
+    for (int u0 = ub; u0 < ue; u0 += 32 * CG) {
       float a[CG], b0[CG], b1[CG], r[CG];
       float2 xy[CG];
 #pragma unroll
       for (int i = 0; i < CG; ++i) {          // every load of the group first
         const int u = u0 + 32 * i + lane;
-        const bool v = u >= ulo && u <= uhi;
+        const bool v = u >= ulo && u <= uhi && u < ue;
         a[i] = v ? Ar[u] : 0.f;
         xy[i] = v ? XY[u] : make_float2(0.f, 0.f);
         b0[i] = v ? Br[u] : 0.f;
@@ -369,48 +387,60 @@ __global__ void __launch_bounds__(256) combine_kernel(
 #pragma unroll
       for (int i = 0; i < CG; ++i) {
         const int u = u0 + 32 * i + lane;
-        if (u >= UP) break;
-        float yv = 0.f, bv = 0.f;
-        if (u >= ulo && u <= uhi) {
-          const int w = u >> lsw;                 // SW = 32 R is a power of two
-          bv = ex2_approx(a[i] + xy[i].y + b0[i] + s_ob[kr][w]);
-          if (u < Un) yv = ex2_approx(a[i] + xy[i].x + b1[i] + (((u & (SW - 1)) == SW - 1) ? s_ox[kr][w] : s_ob[kr][w]));
+        if (u >= ue) break;
+        float yv = 0.f, bv = 0.f, gv = 0.f;
+        if (live) cell(kr, u, a[i], xy[i], b0[i], b1[i], r[i], yv, bv, gv);
+        if (stage) {
+          Ys[kr * CW + (u - c0)] = yv;
+          Bs[kr * CW + (u - c0)] = bv;
+          Gs[kr * CW + (u - c0)] = gv;
         }
-        Ys[kr * UP + u] = yv;
-        Bs[kr * UP + u] = bv;
-        Gs[kr * UP + u] = (yv + bv) * r[i];
         z += yv + bv;
       }
     }
+    return z;
+  };
+  for (int kr = warp; kr < 32; kr += 8) {
+    const int k = k0 + kr;
+    const bool live = finite && k < Kn;
+    float z = diag_pass(kr, 0, UP, 0, one);
     z = warp_sum(z);
     if (lane == 0) s_rz[kr] = (live && z > 0.f && isfinite(z)) ? 1.0f / z : 0.f;
   }
   __syncthreads();
 
-  // phase B: rows t with a cell in the block: t in [k0 - UP + 1, k0 + 31], columns u = k0 + kr - t
-  const int tlo = max(0, k0 - UP + 1), thi = min(T - 1, k0 + 31);
-  for (int t = tlo + warp; t <= thi; t += 8) {
-    const int kr = lane, u = k0 + kr - t;
-    if (u < 0 || u >= UP) continue;
-    const float rz = s_rz[kr];
-    const float yv = Ys[kr * UP + u] * rz, bv = Bs[kr * UP + u] * rz;
-    if (u < U1) {
-      const size_t o = ((size_t)n * T + t) * U1 + u;
-      px_grad[o] = yv;
-      py_grad[o] = bv;
+  for (int c0 = 0; c0 < UP; c0 += CW) {
+    const int c1 = min(UP, c0 + CW);
+    if (!one) {
+      for (int kr = warp; kr < 32; kr += 8) diag_pass(kr, c0, c1, c0, true);
+      __syncthreads();
     }
-    // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
-    const size_t og = ((size_t)n * T + t) * UP + u;
-    const float g = Gs[kr * UP + u] * rz;
-    const __nv_bfloat16 gh = __float2bfloat16_rn(g);
-    const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
-    Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
-    Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
-    // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
-    const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
-    const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
-    Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
-    Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
+    // phase B: rows t with a cell of the window in the block: columns u = k0 + kr - t in [c0, c1)
+    const int tlo = max(0, k0 - c1 + 1), thi = min(T - 1, k0 + 31 - c0);
+    for (int t = tlo + warp; t <= thi; t += 8) {
+      const int kr = lane, u = k0 + kr - t;
+      if (u < c0 || u >= c1) continue;
+      const float rz = s_rz[kr];
+      const float yv = Ys[kr * CW + (u - c0)] * rz, bv = Bs[kr * CW + (u - c0)] * rz;
+      if (u < U1) {
+        const size_t o = ((size_t)n * T + t) * U1 + u;
+        px_grad[o] = yv;
+        py_grad[o] = bv;
+      }
+      // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
+      const size_t og = ((size_t)n * T + t) * UP + u;
+      const float g = Gs[kr * CW + (u - c0)] * rz;
+      const __nv_bfloat16 gh = __float2bfloat16_rn(g);
+      const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
+      Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
+      Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
+      // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
+      const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
+      const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
+      Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
+      Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
+    }
+    if (!one) __syncthreads();
   }
 }
 
@@ -450,7 +480,7 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   if (e != cudaSuccess) return e;
   // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
   dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
-  const size_t csm = (size_t)3 * 32 * d.UP() * sizeof(float);
+  const size_t csm = (size_t)3 * 32 * std::min(d.UP(), kCombineWindow) * sizeof(float);
   cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, csm, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),

@@ -211,6 +211,8 @@ struct ScanParams {
   float* loss;
   int32_t* status;
   int G;             // CTAs per (utterance, direction): a thread-block cluster sharing the chunk work
+  int staged;        // 1: the utterance's arcs and bounds are staged in shared memory (T S 8 + T 4 bytes
+                     // fit); 0 (long utterances): every phase reads them from global memory (L2)
 };
 
 // SMAX: register rows per lane; SC: the band width S as a compile-time constant (0: runtime S <= SMAX),
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   float* PYs = PXs + (size_t)q.T * S;
   int* prs = reinterpret_cast<int*>(PYs + (size_t)q.T * S);
   const size_t rb = (size_t)n * q.T * S;
-  {
+  if (q.staged) {
     const int m = Tn * S;
     const float* gx = q.px2 + rb;
     const float* gy = q.py2 + rb;
@@ -275,9 +277,9 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   }
   __syncthreads();
   scan_trace(1);
-  const int* pr = prs;
-  const float* PX = PXs;
-  const float* PY = PYs;
+  const int* pr = q.staged ? prs : q.ranges + (size_t)n * q.T;
+  const float* PX = q.staged ? PXs : q.px2 + rb;
+  const float* PY = q.staged ? PYs : q.py2 + rb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int spw = 32 / S;                       // segments per warp
   const int seg = warp * spw + lane / S, s = lane % S;
@@ -625,8 +627,12 @@ static int scan_chunk(const Dims& d) {
   return C;
 }
 // chunk matrices + the staged arcs (2 T S floats) and bounds (T ints)
+static bool scan_staged(const Dims& d) {
+  return scan_mat_bytes(d, scan_chunk(d)) + (long long)d.T * d.S * 8 + (long long)d.T * 4 <= 200 * 1024;
+}
 size_t pruned_recursion_smem(const Dims& d) {
-  return (size_t)(scan_mat_bytes(d, scan_chunk(d)) + (long long)d.T * d.S * 8 + (long long)d.T * 4);
+  const long long mat = scan_mat_bytes(d, scan_chunk(d));
+  return (size_t)(scan_staged(d) ? mat + (long long)d.T * d.S * 8 + (long long)d.T * 4 : mat);
 }
 
 template <int SMAX, int SC>
@@ -670,7 +676,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     const size_t sm = pruned_recursion_smem(d);
     const int C = scan_chunk(d);
     ScanParams q{w.px2, w.py2, ranges, bnd, d.T, d.S, C, (d.T + C - 1) / C + 1, w.ap, w.bp, w.Af, w.Bf, w.Lp, loss,
-                 status, scan_cluster(d)};
+                 status, scan_cluster(d), scan_staged(d) ? 1 : 0};
     switch (d.S) {   // band widths of the BASELINE configs (and the tests) get a compile-time S
       case 2: e = launch_scan<2, 2>(d, q, sm, st); break;
       case 3: e = launch_scan<3, 3>(d, q, sm, st); break;

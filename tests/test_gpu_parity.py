@@ -119,12 +119,24 @@ def test_stagewise_parity(cfg):
     dict(T=[300, 129], U=[257, 60], V=40, J=16, S=6),     # U+1 > 256: multi-warp recursion
     dict(T=[90, 41], U=[70, 12], V=65, J=16, S=7),        # runtime-S scan (SMAX 8), cluster of 2
     dict(T=[60, 33], U=[150, 20], V=65, J=16, S=20),      # runtime-S scan (SMAX 32), cluster of 4
+    dict(T=[1200, 700], U=[1000, 600], V=24, J=16, S=3),  # U + 1 > 512: the combine's two column windows
+    dict(T=[2000, 900], U=[300, 100], V=16, J=8, S=16),   # T S 8 B > smem: the pruned scan reads its arcs from L2
 ])
 def test_edge_cases(case):
     b = synth.make_custom(case["T"], case["U"], case["V"], case["J"], case["S"], seed=11, logit_scale=2.0)
     g, o = check_simple(b)
     ranges = check_ranges(b, o)
     h_ref = check_prune(b, ranges)
+    check_pruned(b, ranges, h_ref)
+
+
+def test_pruned_stage_very_long_utterance():
+    """T = 8000 frames (the pruned scan's arcs are read from L2, its chunk chain is long), the pruned
+    stage alone on the oracle's bounds and joiner input: loss and every gradient."""
+    b = synth.make_custom([8000, 3000], [1000, 400], 16, 8, 10, seed=41, logit_scale=2.0)
+    o = _oracle_simple(b)
+    ranges = _oracle_ranges(b, o["px_grad"].astype(np.float32), o["py_grad"].astype(np.float32))
+    h_ref = oracle_h_bits(b, ranges)
     check_pruned(b, ranges, h_ref)
 
 

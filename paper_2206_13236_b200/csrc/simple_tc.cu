@@ -577,7 +577,7 @@ struct NormProb {
     for (int c = e.g; c < nch; c += 2) {
       const int c0 = 32 * c, u0 = t.n0 + c0;
       float acc[32], ay[32];
-      tc::tmem_ld32(e.taddr + c0, acc);
+      // the row's am[t, y_{u+1}] loads are issued first so their latency overlaps the TMEM load's
       if (rowok) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -585,6 +585,7 @@ struct NormProb {
           ay[4 * q] = v.x; ay[4 * q + 1] = v.y; ay[4 * q + 2] = v.z; ay[4 * q + 3] = v.w;
         }
       }
+      tc::tmem_ld32(e.taddr + c0, acc);
       // branch-free per cell: every cell is computed (invalid ones from S = 1) and selected; the
       // smoothing term (a warp-uniform switch) is applied in a second, separate loop
 #pragma unroll

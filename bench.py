@@ -629,7 +629,7 @@ def main():
         # step sends exactly those bytes (one H2D per tensor) and scatters them into the padded device
         # layout (padded input contents are never read, include/rnnt.h)
         rowsof = {"am": b.T_n, "enc_proj": b.T_n, "lm": b.U_n + 1, "dec_proj": b.U_n + 1}
-        packed, pidx, dpacked = {}, {}, {}
+        packed, pidx = {}, {}
         for tname, lens in rowsof.items():
             full_ = host[tname]
             P_ = full_.shape[1]
@@ -637,7 +637,7 @@ def main():
             flat = full_.view(-1, full_.shape[2])
             packed[tname] = flat[torch.from_numpy(idx)].contiguous().pin_memory()
             pidx[tname] = torch.from_numpy(idx).cuda()
-            dpacked[tname] = torch.empty_like(packed[tname], device="cuda")
+        dpacked = [{t: torch.empty_like(packed[t], device="cuda") for t in packed} for _ in range(2)]
         small = [k for k in host if k not in rowsof and k not in ("w_out", "b_out")]
         h2d = sum(v.numel() * v.element_size() for v in packed.values()) + \
             sum(host[k].numel() * host[k].element_size() for k in small)
@@ -671,11 +671,16 @@ def main():
                     for tname in small:
                         bufs[k][tname].copy_(host[tname], non_blocking=True)
                     for tname in packed:
-                        dpacked[tname].copy_(packed[tname], non_blocking=True)
-                        dst = bufs[k][tname]
-                        dst.view(-1, dst.shape[2]).index_copy_(0, pidx[tname], dpacked[tname])
+                        dpacked[k][tname].copy_(packed[tname], non_blocking=True)
                     copied[k].record(copy_stream)
                 stream.wait_event(copied[k])
+                # the scatter into the padded layout runs on the step's stream, just before it: on the
+                # copy stream it would wait for SMs behind the previous step's persistent kernels and
+                # stall the copy engine's pipeline
+                with torch.cuda.stream(stream):
+                    for tname in packed:
+                        dst = bufs[k][tname]
+                        dst.view(-1, dst.shape[2]).index_copy_(0, pidx[tname], dpacked[k][tname])
                 if graphs[k] is not None:
                     graphs[k].replay()
                 else:

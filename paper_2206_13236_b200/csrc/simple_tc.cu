@@ -322,13 +322,20 @@ __global__ void __launch_bounds__(256) smooth_q_kernel(const float* __restrict__
 
 // ------------------------------------------------------------------ gemm3 mainloop
 namespace sg {
-constexpr int BM = 128, BK = 64, STAGES = 2;
+constexpr int BM = 128, BK = 64;
 constexpr int EPI_WARPS = 8, THREADS = 32 * (EPI_WARPS + 1);   // warps 0-7 epilogue, warp 8 TMA + MMA
 constexpr int A_BYTES = BM * BK * 2;                        // 16 KB per hi | lo
-constexpr int B_BYTES = 256 * BK * 2;                       // 32 KB per hi | lo (BN <= 256)
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;      // 96 KB
-constexpr int AUX_BYTES = 8192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + AUX_BYTES + 1024 + 256;
+constexpr int AUX_BYTES = 12288;                            // prologue tables (AmProb: up to 1023 label picks)
+// per problem P: an N tile of P::kBN columns, P::kStages pipeline stages, P::kMinBlocks CTAs per SM.
+// The gradient contractions (one K block per tile at c2 / c3) use 128-column tiles and one stage so that
+// two CTAs share an SM (smem ~72 KB, TMEM <= 256 columns each): one CTA's epilogue overlaps the other's
+// loads and MMAs.
+template <class P> struct Geo {
+  static constexpr int B_BYTES = P::kBN * BK * 2;                       // per hi | lo
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int SMEM_BYTES = P::kStages * STAGE_BYTES + AUX_BYTES + 1024 + 256;
+  static constexpr uint32_t kCols = (P::kPhases == 2 ? 2 : 1) * P::kBN;   // TMEM columns (power of two)
+};
 constexpr int SCR = 32 * 33;                                // per-warp 32x32 staging block (floats)
 }  // namespace sg
 
@@ -371,11 +378,12 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-// Phase 0: acc0 (TMEM columns 0..255) += A_hi B_hi + A_hi B_lo + A_lo B_hi   (bf16x3)
-// Phase 1: acc1 (TMEM columns 256..511) += A'_hi B' + A'_lo B'               (B' exact in bf16)
+// Phase 0: acc0 (TMEM columns 0..kBN-1) += A_hi B_hi + A_hi B_lo + A_lo B_hi   (bf16x3)
+// Phase 1: acc1 (TMEM columns kBN..2kBN-1) += A'_hi B' + A'_lo B'              (B' exact in bf16)
 template <class P>
-__global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_constant__ Maps mp, P p) {
+__global__ void __launch_bounds__(sg::THREADS, P::kMinBlocks) gemm3_kernel(const __grid_constant__ Maps mp, P p) {
   using namespace sg;
+  constexpr int STAGES = P::kStages, STAGE_BYTES = Geo<P>::STAGE_BYTES, B_BYTES = Geo<P>::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
   uint8_t* aux = smem + STAGES * STAGE_BYTES;
@@ -387,7 +395,7 @@ __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Tile tl = p.tile();
   if (tl.n < 0) return;
-  constexpr uint32_t kCols = P::kPhases == 2 ? 512 : 256;
+  constexpr uint32_t kCols = Geo<P>::kCols;
   const int nk = tl.nkb0 + (P::kPhases == 2 ? tl.nkb1 : 0);
 
   if (warp == EPI_WARPS && lane == 0) {
@@ -463,8 +471,8 @@ __global__ void __launch_bounds__(sg::THREADS, 1) gemm3_kernel(const __grid_cons
           tc::mma_bf16(tbase, dah, dbl, idesc, 1);               // hi * lo
           tc::mma_bf16(tbase, dal, dbh, idesc, 1);               // lo * hi
         } else {
-          tc::mma_bf16(tbase + 256, dah, dbh, idesc, (kb | k) != 0);
-          tc::mma_bf16(tbase + 256, dal, dbh, idesc, 1);
+          tc::mma_bf16(tbase + P::kBN, dah, dbh, idesc, (kb | k) != 0);
+          tc::mma_bf16(tbase + P::kBN, dal, dbh, idesc, 1);
         }
       }
       tc::mma_commit(&empty[s]);
@@ -497,7 +505,7 @@ __device__ __forceinline__ void warp_store_block(const float (*buf)[33], float* 
 // ------------------------------------------------------------------ K2: normaliser + lattice arcs
 struct NormProb {
   static constexpr bool kA_MN = false, kB_MN = false;
-  static constexpr int kPhases = 1;
+  static constexpr int kPhases = 1, kBN = 256, kStages = 2, kMinBlocks = 1;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
   int T, U, V, LU, K, BN, nkb, UPa;
@@ -520,7 +528,7 @@ struct NormProb {
     tc::tma_load_3d(st, &mp.m[0], bar, kb * sg::BK, t.m0, t.n);
     tc::tma_load_3d(st + sg::A_BYTES, &mp.m[1], bar, kb * sg::BK, t.m0, t.n);
     tc::tma_load_3d(st + 2 * sg::A_BYTES, &mp.m[2], bar, kb * sg::BK, t.n0, t.n);
-    tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
+    tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::Geo<NormProb>::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
   }
   __device__ int epi_chunks(const Tile&) const { return 0; }
   __device__ void epi_load(int, uint8_t*, uint64_t*, const Tile&, const Maps&) const {}
@@ -638,9 +646,14 @@ struct NormProb {
 };
 
 // ------------------------------------------------------------------ K5a: am_grad
+// The label picks -sum_u y'(t,u) [v = y_{u+1}] are applied in the epilogue: the prologue lists the (u,
+// column) pairs whose label falls in the tile (about U kBN / V of them) and each row adds its fp32 y'(t,u)
+// (px_grad) at those columns -- no second contraction against a one-hot matrix.
 struct AmProb {
   static constexpr bool kA_MN = false, kB_MN = true;
-  static constexpr int kPhases = 2;
+  static constexpr int kPhases = 1, kBN = 128, kStages = 1, kMinBlocks = 2;
+  static constexpr int kNC = kBN / 32;      // 32-column epilogue chunks per tile
+  static constexpr int kMaxPicks = 1024;    // (u, column) pairs listed in aux (U <= 1023)
   const float *am, *m_am, *rowb;
   const int64_t* bnd;
   int T, U, V;
@@ -650,6 +663,8 @@ struct AmProb {
   Smooth sm;
   const float *Lavg, *lse_ac, *rowy;
   int VPl;
+  const float* px_grad;     // (N, T, U+1) y'
+  const int64_t* sym;
   // d(-L)/d am[t,v] / gs = w0 E G~E_lm - (w0 + a_ac) picks + a_ac occ(t) P_ac(t,v)  (Eq. 11-13 chain rule)
   __device__ __forceinline__ float grad(float x, float mam, float a0, float pick, float occ, float Lv, float lac) const {
     float g = sm.w0() * __expf(x - mam) * a0 - (sm.w0() + sm.a_ac) * pick;
@@ -658,40 +673,83 @@ struct AmProb {
   }
 
   __device__ Tile tile() const {
-    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
+    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * kBN, 0, 0};
     const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
     t.nkb0 = (t.m0 < Tn) ? (Un + 1 + sg::BK - 1) / sg::BK : 0;
-    t.nkb1 = (t.m0 < Tn && Un > 0) ? (Un + sg::BK - 1) / sg::BK : 0;   // label arcs exist for u < U_n
     return t;
   }
-  __device__ uint32_t bytes(int phase) const {
-    return phase == 0 ? 2 * sg::A_BYTES + 2 * sg::B_BYTES : 2 * sg::A_BYTES + sg::B_BYTES;
-  }
-  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, 256, false, true); }
-  // phase 0: A = G~ (hi, lo; K-major over u), B = E_lm (hi, lo; MN-major);
-  // phase 1: A = y' (hi, lo), B = one-hot of the labels [v == y_{u+1}] (exact)
-  __device__ void load(uint8_t* st, int phase, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
-    const CUtensorMap* ah = phase == 0 ? &mp.m[0] : &mp.m[4];
-    const CUtensorMap* al = phase == 0 ? &mp.m[1] : &mp.m[5];
-    tc::tma_load_3d(st, ah, bar, kb * sg::BK, t.m0, t.n);
-    tc::tma_load_3d(st + sg::A_BYTES, al, bar, kb * sg::BK, t.m0, t.n);
+  __device__ uint32_t bytes(int) const { return 2 * sg::A_BYTES + 2 * sg::Geo<AmProb>::B_BYTES; }
+  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, kBN, false, true); }
+  // A = G~ (hi, lo; K-major over u), B = E_lm (hi, lo; MN-major)
+  __device__ void load(uint8_t* st, int, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
+    tc::tma_load_3d(st, &mp.m[0], bar, kb * sg::BK, t.m0, t.n);
+    tc::tma_load_3d(st + sg::A_BYTES, &mp.m[1], bar, kb * sg::BK, t.m0, t.n);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (phase == 0) {
-        tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.m[2], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
-        tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i, kb * sg::BK,
-                        t.n);
-      } else {
-        tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.b1, bar, t.n0 + 64 * i, kb * sg::BK, t.n);
-      }
+    for (int i = 0; i < kBN / 64; ++i) {
+      tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.m[2], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+      tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::Geo<AmProb>::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i,
+                      kb * sg::BK, t.n);
     }
   }
-  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
+  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(kNC, (V - t.n0 + 31) / 32) : 0; }
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
-  __device__ void prologue(uint8_t*, const Tile&) const {}
-  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, const Epi& e, uint64_t* ep_full,
+  // aux: [0] the number of picks, [1..8] per-warp counts, then the (u, column - n0) pairs of the labels
+  // falling in this tile in ascending u (a ballot / warp-count scan: deterministic order, so duplicate
+  // labels always add in the same order)
+  __device__ void prologue(uint8_t* aux, const Tile& t) const {
+    int* cnt = reinterpret_cast<int*>(aux);
+    int* wc = cnt + 1;
+    int2* pk = reinterpret_cast<int2*>(aux + 64);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int Un = utt_U(bnd, t.n);
+    int base = 0;
+    for (int u0 = 0; u0 < Un; u0 += 32 * sg::EPI_WARPS) {
+      const int u = u0 + threadIdx.x;
+      bool hit = false;
+      int col = 0;
+      if (u < Un) {
+        const long long y = sym[(size_t)t.n * U + u];
+        hit = y >= t.n0 && y < t.n0 + kBN && y < V;
+        col = (int)(y - t.n0);
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) wc[warp] = __popc(b);
+      epi_bar();
+      int off = base;
+      for (int w = 0; w < warp; ++w) off += wc[w];
+      int tot = 0;
+      for (int w = 0; w < sg::EPI_WARPS; ++w) tot += wc[w];
+      const int i = off + __popc(b & ((1u << lane) - 1u));
+      if (hit && i < kMaxPicks) pk[i] = make_int2(u, col);
+      base += tot;
+      epi_bar();
+    }
+    if (threadIdx.x == 0) *cnt = base;
+    epi_bar();
+  }
+  // the picks of row trow for the 32 columns of chunk c (fp32 y' from px_grad)
+  __device__ __forceinline__ void picks(const uint8_t* aux, int c, int trow, bool live, const Tile& t,
+                                        float (&a1)[32]) const {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a1[j] = 0.f;
+    if (!live) return;
+    const int npk = min(*reinterpret_cast<const int*>(aux), kMaxPicks);
+    const int2* pk = reinterpret_cast<const int2*>(aux + 64);
+    const float* yr = px_grad + ((size_t)t.n * T + trow) * (U + 1);
+    for (int i = 0; i < npk; ++i) {
+      const int2 q = pk[i];
+      const int jj = q.y - 32 * c;
+      if ((unsigned)jj < 32u) {
+        const float yv = yr[q.x];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j == jj) a1[j] += yv;
+      }
+    }
+  }
+  __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
     const int Tn = utt_T(bnd, t.n);
     const int trow = t.m0 + e.row;
@@ -708,12 +766,8 @@ struct AmProb {
       for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
         float a0[32], a1[32];
+        picks(aux, c, trow, live, t, a1);
         tc::tmem_ld32(e.taddr + 32 * c, a0);
-        tc::tmem_ld32(e.taddr + 256 + 32 * c, a1);
-        if (t.nkb1 == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) a1[j] = 0.f;
-        }
         tc::mbar_wait(&ep_full[c], 0);
         uint8_t* tile = smem + c * EP_BYTES;
 #pragma unroll
@@ -751,20 +805,16 @@ struct AmProb {
     const float* Lr = Lavg + (size_t)t.n * VPl;
     float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + e.warp * sg::SCR * 4);
     const int nin = min(32, Tn - t0w), nout = min(32, T - t0w);
-    for (int c = e.g; c < 8; c += 2) {
+    for (int c = e.g; c < kNC; c += 2) {
       const int vc = t.n0 + 32 * c;
       if (vc >= V) break;
       float a0[32], a1[32];
+      picks(aux, c, t0w + e.lane, live, t, a1);
       if (t.nkb0 > 0) {
         tc::tmem_ld32(e.taddr + 32 * c, a0);
-        tc::tmem_ld32(e.taddr + 256 + 32 * c, a1);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) { a0[j] = 0.f; a1[j] = 0.f; }
-      }
-      if (t.nkb1 == 0) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) a1[j] = 0.f;
+        for (int j = 0; j < 32; ++j) a0[j] = 0.f;
       }
       const int nc = min(32, V - vc);
       warp_load_block(buf, am + row0 * V + vc, V, nin, nc, e.lane);
@@ -782,7 +832,8 @@ struct AmProb {
 // ------------------------------------------------------------------ K5b: lm_grad
 struct LmProb {
   static constexpr bool kA_MN = true, kB_MN = true;
-  static constexpr int kPhases = 1;
+  static constexpr int kPhases = 1, kBN = 128, kStages = 1, kMinBlocks = 2;
+  static constexpr int kNC = kBN / 32;
   const float *lm, *m_lm, *colpy, *colpb;
   const int64_t *sym, *bnd;
   int T, U, V, ntb;
@@ -801,13 +852,13 @@ struct LmProb {
   }
 
   __device__ Tile tile() const {
-    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * 256, 0, 0};
+    Tile t{(int)blockIdx.z, (int)blockIdx.x * sg::BM, (int)blockIdx.y * kBN, 0, 0};
     const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
     t.nkb0 = (t.m0 <= Un) ? (Tn + sg::BK - 1) / sg::BK : 0;
     return t;
   }
-  __device__ uint32_t bytes(int) const { return 2 * sg::A_BYTES + 2 * sg::B_BYTES; }
-  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, 256, true, true); }
+  __device__ uint32_t bytes(int) const { return 2 * sg::A_BYTES + 2 * sg::Geo<LmProb>::B_BYTES; }
+  __device__ uint32_t idesc(int) const { return tc::idesc_bf16(sg::BM, kBN, true, true); }
   __device__ void load(uint8_t* st, int, int kb, const Tile& t, uint64_t* bar, const Maps& mp) const {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -815,12 +866,13 @@ struct LmProb {
       tc::tma_load_3d(st + sg::A_BYTES + i * 8192, &mp.m[1], bar, t.m0 + 64 * i, kb * sg::BK, t.n);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kBN / 64; ++i) {
       tc::tma_load_3d(st + 2 * sg::A_BYTES + i * 8192, &mp.m[2], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
-      tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i, kb * sg::BK, t.n);
+      tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::Geo<LmProb>::B_BYTES + i * 8192, &mp.m[3], bar, t.n0 + 64 * i,
+                      kb * sg::BK, t.n);
     }
   }
-  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(8, (V - t.n0 + 31) / 32) : 0; }
+  __device__ int epi_chunks(const Tile& t) const { return (tma_io && t.nkb0 > 0) ? min(kNC, (V - t.n0 + 31) / 32) : 0; }
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
@@ -881,7 +933,7 @@ struct LmProb {
     const float mlm = live ? m_lm[row0 + e.lane] : 0.f;
     float (*buf)[33] = reinterpret_cast<float (*)[33]>(smem + e.warp * sg::SCR * 4);
     const int nin = min(32, Un + 1 - u0w), nout = min(32, U1 - u0w);
-    for (int c = e.g; c < 8; c += 2) {
+    for (int c = e.g; c < kNC; c += 2) {
       const int vc = t.n0 + 32 * c;
       if (vc >= V) break;
       float acc[32];
@@ -908,9 +960,9 @@ struct LmProb {
 // ------------------------------------------------------------------ host
 template <class P>
 static cudaError_t launch_gemm3(const P& p, dim3 grid, const Maps& mp, int kid, cudaStream_t st) {
-  smem_optin(gemm3_kernel<P>, sg::SMEM_BYTES);
+  smem_optin(gemm3_kernel<P>, sg::Geo<P>::SMEM_BYTES);
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return cudaSuccess;
-  RNNT_LAUNCH(kid, st, gemm3_kernel<P><<<grid, sg::THREADS, sg::SMEM_BYTES, st>>>(mp, p));
+  RNNT_LAUNCH(kid, st, gemm3_kernel<P><<<grid, sg::THREADS, sg::Geo<P>::SMEM_BYTES, st>>>(mp, p));
   return cudaGetLastError();
 }
 
@@ -985,8 +1037,9 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                !make_tmap_f32_3d(&mp.eout, am_grad, d.V, d.T, d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.T * 4, 32,
                                  sg::BM)))
       return cudaErrorInvalidValue;
-    AmProb p{am, w.m_am, w.rowb, bnd, d.T, d.U, d.V, gs, am_grad, io, sm, w.Lavg, w.lse_ac, w.rowy, d.VP64()};
-    dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
+    AmProb p{am, w.m_am, w.rowb, bnd, d.T, d.U, d.V, gs, am_grad, io, sm, w.Lavg, w.lse_ac, w.rowy, d.VP64(), px_grad,
+             sym};
+    dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.V + AmProb::kBN - 1) / AmProb::kBN, d.N);
     if ((e = launch_gemm3(p, grid, mp, KID_AMGRAD, st)) != cudaSuccess) return e;
   }
   if (lm_grad) {
@@ -1002,7 +1055,7 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
       return cudaErrorInvalidValue;
     LmProb p{lm, w.m_lm, w.colpy, w.colpb, sym, bnd, d.T, d.U, d.V, d.ntb(), gs, lm_grad, io, sm, w.lse_lm, w.gq, w.Qu,
              d.VP64()};
-    dim3 grid((d.U1() + sg::BM - 1) / sg::BM, (d.V + 255) / 256, d.N);
+    dim3 grid((d.U1() + sg::BM - 1) / sg::BM, (d.V + LmProb::kBN - 1) / LmProb::kBN, d.N);
     if ((e = launch_gemm3(p, grid, mp, KID_LMGRAD, st)) != cudaSuccess) return e;
   }
   return cudaGetLastError();

@@ -313,8 +313,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float* __restrict__ ahat, const float* __restrict__ bhat, const float* __restrict__ Ash,
     const float* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
     int U, int LU, int K, int W, int SW, int UP, float* __restrict__ px_grad, float* __restrict__ py_grad,
-    uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo, uint16_t* __restrict__ Yp_hi,
-    uint16_t* __restrict__ Yp_lo) {
+    uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo) {
   extern __shared__ __align__(16) float cbuf[];
   const int CWs = min(UP, kCombineWindow);
   float* Ys = cbuf;                     // [32][CW]
@@ -434,11 +433,6 @@ __global__ void __launch_bounds__(256) combine_kernel(
       const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
       Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
       Gt_lo[og] = *reinterpret_cast<const uint16_t*>(&gl);
-      // y' as bf16 hi + lo: the A operand of the am_grad label-pick contraction
-      const __nv_bfloat16 yh = __float2bfloat16_rn(yv);
-      const __nv_bfloat16 yl = __float2bfloat16_rn(yv - __bfloat162float(yh));
-      Yp_hi[og] = *reinterpret_cast<const uint16_t*>(&yh);
-      Yp_lo[og] = *reinterpret_cast<const uint16_t*>(&yl);
     }
     if (!one) __syncthreads();
   }
@@ -485,7 +479,7 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, csm, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
                                                                    32 * d.lat_R(), d.UP(), px_grad, py_grad, w.Gt_hi,
-                                                                   w.Gt_lo, w.Yp_hi, w.Yp_lo));
+                                                                   w.Gt_lo));
   return cudaGetLastError();
 }
 

@@ -29,12 +29,12 @@ namespace rnnt {
 // ------------------------------------------------------------------ K1
 // One warp per row of am (which = 0, rows t of T) or lm (which = 1, rows u of U+1).  am rows also
 // gather amy[t,u] = am[t, y_{u+1}] (the label logit the normaliser epilogue needs, read here while
-// the row is in L1); lm rows also write the one-hot row [v == y_{u+1}] of the am pick contraction.
+// the row is in L1).
 __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, const int64_t* __restrict__ sym,
                                                const int64_t* __restrict__ bnd, int N, int rows_per_n, int U, int V,
                                                int VP, int which, float* __restrict__ m, uint16_t* __restrict__ hi,
                                                uint16_t* __restrict__ lo, float* __restrict__ amy, int UPa,
-                                               uint16_t* __restrict__ onehot, float* __restrict__ lse, int blk) {
+                                               float* __restrict__ lse, int blk) {
   const long long row = (long long)blk * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * rows_per_n) return;
@@ -43,16 +43,6 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   const int lim = which == 0 ? utt_T(bnd, n) : Un + 1;
   uint32_t* H = reinterpret_cast<uint32_t*>(hi + row * (long long)VP);
   uint32_t* L = reinterpret_cast<uint32_t*>(lo + row * (long long)VP);
-  int label = -1;                                    // lm rows: y_{u+1} (u < U_n)
-  if (which == 1 && r < Un) {
-    const long long y = sym[(size_t)n * U + r];
-    label = (y >= 1 && y < V) ? (int)y : -1;
-  }
-  if (which == 1) {
-    uint32_t* O = reinterpret_cast<uint32_t*>(onehot + row * (long long)VP);
-    for (int v2 = lane; v2 < VP / 2; v2 += 32)
-      O[v2] = (2 * v2 == label) ? 0x3f80u : ((2 * v2 + 1 == label) ? 0x3f800000u : 0u);   // bf16 1.0
-  }
   if (r >= lim) {   // padded row: zero operand, never read otherwise
     for (int v2 = lane; v2 < VP / 2; v2 += 32) { H[v2] = 0u; L[v2] = 0u; }
     if (lane == 0) m[row] = 0.f;
@@ -143,13 +133,13 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
 }
 
 // One launch for the independent prologue work of the simple loss, dispatched by block index:
-// am rows (exp split + amy), lm rows (exp split + one-hot), skewed-arc sentinels, validation.
+// am rows (exp split + amy), lm rows (exp split), skewed-arc sentinels, validation.
 struct PrepParams {
   const float *am, *lm;
   const int64_t *sym, *bnd;
   int N, T, U, V, VP, UP, LU, K;
   float *m_am, *m_lm, *amy, *lse_lm;
-  uint16_t *eam_hi, *eam_lo, *elm_hi, *elm_lo, *onehot;
+  uint16_t *eam_hi, *eam_lo, *elm_hi, *elm_lo;
   float2* pxy;
   int32_t* status;
   int nb_am, nb_lm, nb_fill;
@@ -159,13 +149,13 @@ __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
   int b = blockIdx.x;
   if (b < p.nb_am) {
     exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr,
-                   nullptr, b);
+                   b);
     return;
   }
   b -= p.nb_am;
   if (b < p.nb_lm) {
     exp_split_rows(p.lm, p.sym, p.bnd, p.N, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
-                   p.onehot, p.lse_lm, b);
+                   p.lse_lm, b);
     return;
   }
   b -= p.nb_lm;
@@ -756,7 +746,7 @@ struct AmProb {
     const bool live = trow < Tn;
     const int nep = epi_chunks(t);
     if (nep > 0) {
-      // d(-L_simple)/d am = E_am (G~ E_lm) - y' onehot - [v=0] sum_u empty'   (times gs), tile in place
+      // d(-L_simple)/d am = E_am (G~ E_lm) - y' [v = y_{u+1}] - [v=0] sum_u empty'   (times gs), tile in place
       const size_t row = (size_t)t.n * T + (live ? trow : 0);
       const float mam = live ? m_am[row] : 0.f;
       const float rb = live ? rowb[row] : 0.f;
@@ -981,7 +971,7 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   p.am = am; p.lm = lm; p.sym = sym; p.bnd = bnd;
   p.N = d.N; p.T = d.T; p.U = d.U; p.V = d.V; p.VP = d.VP64(); p.UP = d.UP(); p.LU = d.LU(); p.K = d.K();
   p.m_am = w.m_am; p.m_lm = w.m_lm; p.amy = w.amy; p.lse_lm = w.lse_lm;
-  p.eam_hi = w.Eam_hi; p.eam_lo = w.Eam_lo; p.elm_hi = w.Elm_hi; p.elm_lo = w.Elm_lo; p.onehot = w.onehot;
+  p.eam_hi = w.Eam_hi; p.eam_lo = w.Eam_lo; p.elm_hi = w.Elm_hi; p.elm_lo = w.Elm_lo;
   p.pxy = w.pxy; p.status = status;
   p.nb_am = (int)(((long long)d.N * d.T + 7) / 8);
   p.nb_lm = (int)(((long long)d.N * d.U1() + 7) / 8);
@@ -1028,9 +1018,7 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
   if (am_grad) {
     Maps mp;
     if (!tm3(&mp.m[0], w.Gt_hi, d.UP(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Gt_lo, d.UP(), d.T, d.N, sg::BM) ||
-        !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, 64) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, 64) ||
-        !tm3(&mp.m[4], w.Yp_hi, d.UP(), d.T, d.N, sg::BM) || !tm3(&mp.m[5], w.Yp_lo, d.UP(), d.T, d.N, sg::BM) ||
-        !tm3(&mp.b1, w.onehot, d.VP64(), d.U1(), d.N, 64))
+        !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, 64) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, 64))
       return cudaErrorInvalidValue;
     const bool io = d.V % 4 == 0;
     if (io && (!make_tmap_f32_3d(&mp.ein, am, d.V, d.T, d.N, (uint64_t)d.V * 4, (uint64_t)d.V * d.T * 4, 32, sg::BM) ||

@@ -71,9 +71,6 @@ struct SimpleWS {
   uint16_t* Elm_lo;
   uint16_t* Gt_hi;   // (N,T,UP)   bf16 hi/lo of G~ = (y'+empty')/S(t,u) (t-major, zero padded)
   uint16_t* Gt_lo;
-  uint16_t* Yp_hi;   // (N,T,UP)   bf16 hi/lo of y'(t,u) (t-major, zero padded): A of the am pick GEMM
-  uint16_t* Yp_lo;
-  uint16_t* onehot;  // (N,U+1,VP64) bf16 [v == y_{u+1}] (u < U_n): B of the am pick GEMM
   float* amy;        // (N,T,UP)   am[t, y_{u+1}] (gathered by exp_split for the normaliser epilogue)
   float* rowb;       // (N,T)      sum_u empty'(t,u)
   float* colpy;      // (N,ntb,U+1) per-32-frame-block partial sums of y'(t,u) over t
@@ -178,9 +175,6 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   s.Elm_lo = (uint16_t*)take(N * U1 * VP64 * 2);
   s.Gt_hi = (uint16_t*)take(N * T * UP * 2);
   s.Gt_lo = (uint16_t*)take(N * T * UP * 2);
-  s.Yp_hi = (uint16_t*)take(N * T * UP * 2);
-  s.Yp_lo = (uint16_t*)take(N * T * UP * 2);
-  s.onehot = (uint16_t*)take(N * U1 * VP64 * 2);
   s.amy = (float*)take(N * T * UP * 4);
   s.rowb = (float*)take(N * T * 4);
   s.colpy = (float*)take(N * NTB * U1 * 4);

@@ -58,6 +58,11 @@ static const char* const kNames[KID_COUNT] = {
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
     "full_dgrad", "loss_sums", "exchange_sum"};
 
+bool pdl_enabled() {
+  static const bool on = env_int("RNNT_PDL", 1) != 0;
+  return on;
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;

@@ -46,6 +46,7 @@ __device__ __forceinline__ void acc_add4(float4* p, float4 v, int mode) {
 __global__ void loss_sums_kernel(const float* __restrict__ ls, const float* __restrict__ lp,
                                  const int32_t* __restrict__ status, int N, float s_scale, float p_scale,
                                  float* out, int mode) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int lane = threadIdx.x;
   double a = 0.0, b = 0.0;
   for (int n = lane; n < N; n += 32) {
@@ -65,13 +66,14 @@ __global__ void loss_sums_kernel(const float* __restrict__ ls, const float* __re
 
 cudaError_t loss_sums_launch(const float* ls, const float* lp, const int32_t* status, int N, float s_scale,
                              float p_scale, float* out, int mode, cudaStream_t st) {
-  RNNT_LAUNCH(KID_LOSS_SUMS, st, loss_sums_kernel<<<1, 32, 0, st>>>(ls, lp, status, N, s_scale, p_scale, out, mode));
+  RNNT_LAUNCH(KID_LOSS_SUMS, st, launch_pdl(loss_sums_kernel, 1, 32, 0, st, ls, lp, status, N, s_scale, p_scale, out, mode));
   return cudaGetLastError();
 }
 
 // Split-K reduction of the d_w / d_b partials (fixed split order) into the accumulation target.
 __global__ void split_reduce_acc_kernel(const float4* __restrict__ part, int splits, long long M4,
                                         float4* out, int mode) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M4) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -90,6 +92,7 @@ __global__ void split_reduce_acc_kernel(const float4* __restrict__ part, int spl
 }
 __global__ void split_reduce_acc1_kernel(const float* __restrict__ part, int splits, long long M, float* out,
                                          int mode) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
   float acc = 0.f;
@@ -100,10 +103,10 @@ __global__ void split_reduce_acc1_kernel(const float* __restrict__ part, int spl
 cudaError_t split_reduce_acc_launch(const float* part, int splits, long long M, float* out, int mode, int kid,
                                     cudaStream_t st) {
   if (M % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 && reinterpret_cast<uintptr_t>(part) % 16 == 0)
-    RNNT_LAUNCH(kid, st, split_reduce_acc_kernel<<<(unsigned)((M / 4 + 255) / 256), 256, 0, st>>>(
+    RNNT_LAUNCH(kid, st, launch_pdl(split_reduce_acc_kernel, (unsigned)((M / 4 + 255) / 256), 256, 0, st, 
         reinterpret_cast<const float4*>(part), splits, M / 4, reinterpret_cast<float4*>(out), mode));
   else
-    RNNT_LAUNCH(kid, st, split_reduce_acc1_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(part, splits, M, out,
+    RNNT_LAUNCH(kid, st, launch_pdl(split_reduce_acc1_kernel, (unsigned)((M + 255) / 256), 256, 0, st, part, splits, M, out,
                                                                                                 mode));
   return cudaGetLastError();
 }

@@ -43,6 +43,7 @@ cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* rang
 __global__ void __launch_bounds__(256) full_scatter_kernel(const float* __restrict__ px2, const float* __restrict__ py2,
                                                            const int64_t* __restrict__ bnd, int T, int U, int K, int LU,
                                                            float2* __restrict__ pxy) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int n = blockIdx.y;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   const long long cells = (long long)(K + 1) * LU;
@@ -65,6 +66,7 @@ __global__ void full_pack_kernel(const float* __restrict__ gb, const float* __re
                                  const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                  const float* __restrict__ lse, long long R, int ntile, float gs,
                                  float4* __restrict__ gpk) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= R) return;
   const int info = rowinfo[r];
@@ -78,12 +80,13 @@ __global__ void full_pack_kernel(const float* __restrict__ gb, const float* __re
 
 // ids of the 128-row tiles holding a live row (order irrelevant), count at live[ntiles]
 __global__ void full_live_kernel(const uint8_t* __restrict__ tlive, long long ntiles, int* __restrict__ live) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ntiles && tlive[i]) live[atomicAdd(live + ntiles, 1)] = (int)i;
 }
+// (the count live[ntiles] was zeroed by rowinfo_kernel in the same step)
 cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st) {
-  cudaMemsetAsync(live + ntiles, 0, sizeof(int), st);
-  RNNT_LAUNCH(kid, st, full_live_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(tlive, ntiles, live));
+  RNNT_LAUNCH(kid, st, launch_pdl(full_live_kernel, (unsigned)((ntiles + 255) / 256), 256, 0, st, tlive, ntiles, live));
   return cudaGetLastError();
 }
 
@@ -92,6 +95,7 @@ cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live,
 __global__ void __launch_bounds__(128) full_dgrad_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd,
                                                          int N, int T, int U, int J, float* __restrict__ d_enc,
                                                          float* __restrict__ d_dec) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long b = blockIdx.x;
   const long long NT = (long long)N * T;
   const int J4 = J / 4;
@@ -144,12 +148,12 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   {
     const long long cells = (long long)(df.K() + 1) * df.LU();
     const unsigned gx = (unsigned)std::min<long long>((cells + 255) / 256, 1024);
-    RNNT_LAUNCH(KID_FULL_SCATTER, st, full_scatter_kernel<<<dim3(gx, df.N), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_FULL_SCATTER, st, launch_pdl(full_scatter_kernel, dim3(gx, df.N), 256, 0, st, 
         pw.px2, pw.py2, bnd, df.T, df.U, df.K(), df.LU(), sw.pxy));
   }
   // occupancies straight into the row-ordered g_l (= y') and g_b (= empty') arrays
   if ((e = lattice_launch(df, sw, bnd, loss, pw.gl, pw.gb, status, st)) != cudaSuccess) return e;
-  RNNT_LAUNCH(KID_FULL_PACK, st, full_pack_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
+  RNNT_LAUNCH(KID_FULL_PACK, st, launch_pdl(full_pack_kernel, (unsigned)((R + 255) / 256), 256, 0, st, 
       pw.gb, pw.gl, pw.rowinfo, pw.mt, pw.lse, R, df.ntile(), gs, pw.gpk));
   if ((e = pruned_bwd_weight_launch(df, pw, fw.h, d_w, d_b, st, 0)) != cudaSuccess) return e;
   if (d_enc || d_dec) {
@@ -158,7 +162,7 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
     GradSrc g{pw.Pt, pw.gpk, pw.rowinfo, R, df.V, df.VP(), df.ntile()};
     if ((e = joiner_dh_launch(df, g, fw.h, W, pw.dhlive, pw.dhlive + ntiles, ntiles, fw.dpre, st)) != cudaSuccess)
       return e;
-    RNNT_LAUNCH(KID_FULL_DGRAD, st, full_dgrad_kernel<<<(unsigned)((long long)df.N * df.T + (long long)df.N * df.U1()), 128, 0, st>>>(
+    RNNT_LAUNCH(KID_FULL_DGRAD, st, launch_pdl(full_dgrad_kernel, (unsigned)((long long)df.N * df.T + (long long)df.N * df.U1()), 128, 0, st, 
         fw.dpre, bnd, df.N, df.T, df.U, df.J, d_enc, d_dec));
   }
   return cudaGetLastError();

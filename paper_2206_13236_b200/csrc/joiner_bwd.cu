@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
                         JoinerDhParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdh;
   constexpr int EPI0 = Roles<NTW>::EPI0;
   constexpr int STAGES = Cfg<NTW>::STAGES, HRING = Cfg<NTW>::HRING, ORING = Cfg<NTW>::ORING;
@@ -494,6 +495,7 @@ template <bool PAIR>
 __global__ void __launch_bounds__(jdw::THREADS, 2)
     joiner_dw_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
                         JoinerDwParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw;
   constexpr int STAGES = Cfg<PAIR>::STAGES, B_BYTES = Cfg<PAIR>::B_BYTES, STAGE_BYTES = Cfg<PAIR>::STAGE_BYTES;
   auto stage_of = [](int kb) { return kb % STAGES; };
@@ -700,6 +702,7 @@ constexpr int THREADS = 288;
 __global__ void __launch_bounds__(jdw2::THREADS, 1)
     joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
                           JoinerDwParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
@@ -881,7 +884,7 @@ static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUt
   constexpr int SMEM = jdh::Cfg<NTW>::SMEM_BYTES;
   smem_optin(joiner_dh_tc_kernel<NTW, MC>, SMEM);
   if (!MC) {
-    joiner_dh_tc_kernel<NTW, MC><<<grid, jdh::Roles<NTW>::THREADS, SMEM, st>>>(tp, tw, th, td, p);
+    launch_pdl(joiner_dh_tc_kernel<NTW, MC>, grid, jdh::Roles<NTW>::THREADS, SMEM, st, tp, tw, th, td, p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -889,13 +892,15 @@ static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUt
   cfg.blockDim = dim3(jdh::Roles<NTW>::THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, joiner_dh_tc_kernel<NTW, MC>, tp, tw, th, td, p);
 }
 // 4 producer warps for short V loops, 8 for long ones; W multicast over CTA pairs (RNNT_DH_MC=0: off)
@@ -960,7 +965,7 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     if (pfmode >= 0) p.pfmode = pfmode;
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
-    RNNT_LAUNCH(KID_DW, st, joiner_dw_wide_kernel<<<grid, jdw2::THREADS, jdw2::SMEM_BYTES, st>>>(tp3, p.h3 ? th3 : th, p));
+    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, p));
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};
@@ -984,7 +989,7 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     if (p.h3 && (!make_tmap_bf16_3d(&tp3, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw::BK, 2) ||
                  !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw::BK, 4)))
       return cudaErrorInvalidValue;
-    RNNT_LAUNCH(KID_DW, st, joiner_dw_tc_kernel<false><<<grid, jdw::THREADS, jdw::Cfg<false>::SMEM_BYTES, st>>>(
+    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_tc_kernel<false>, grid, jdw::THREADS, jdw::Cfg<false>::SMEM_BYTES, st, 
                                 p.h3 ? tp3 : tp, p.h3 ? th3 : th, p));
   }
   return cudaGetLastError();

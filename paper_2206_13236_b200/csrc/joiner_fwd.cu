@@ -65,6 +65,7 @@ struct JoinerFwdParams {
 __global__ void __launch_bounds__(jf::THREADS, 1)
     joiner_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
@@ -344,6 +345,7 @@ constexpr int THREADS = 320;
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
     joiner_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jf2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
@@ -630,12 +632,12 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     // persistent: one CTA per SM, in pairs (at most one cluster per row-tile pair); the pair counter is
     // the row-tile counter rowinfo_kernel zeroes
     const unsigned grid = (unsigned)(2 * std::min((ntiles + 1) / 2, nsm / 2));
-    RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_pair_kernel<<<grid, jf2::THREADS, jf2::SMEM_BYTES, st>>>(ta, tb, tp, p));
+    RNNT_LAUNCH(KID_JOINER_FWD, st, launch_pdl(joiner_fwd_pair_kernel, grid, jf2::THREADS, jf2::SMEM_BYTES, st, ta, tb, tp, p));
     return cudaGetLastError();
   }
   smem_optin(joiner_fwd_tc_kernel, jf::SMEM_BYTES);
   const unsigned grid = (unsigned)std::min(ntiles, nsm);   // persistent: one CTA per SM
-  RNNT_LAUNCH(KID_JOINER_FWD, st, joiner_fwd_tc_kernel<<<grid, jf::THREADS, jf::SMEM_BYTES, st>>>(ta, tb, tp, p));
+  RNNT_LAUNCH(KID_JOINER_FWD, st, launch_pdl(joiner_fwd_tc_kernel, grid, jf::THREADS, jf::SMEM_BYTES, st, ta, tb, tp, p));
   return cudaGetLastError();
 }
 

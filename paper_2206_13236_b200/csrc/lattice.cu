@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
     const float2* __restrict__ pxy, const int64_t* __restrict__ bnd, int K,
     float* __restrict__ ahat, float* __restrict__ bhat, float* __restrict__ Ash, float* __restrict__ Bsh,
     double* __restrict__ Ltot, float* __restrict__ loss, int32_t* __restrict__ status) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace lat;
   constexpr int C = CH<R>, LU = 32 * R * W;
   extern __shared__ __align__(128) float ring[];
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float* __restrict__ Bsh, const double* __restrict__ Ltot, const int64_t* __restrict__ bnd, int T,
     int U, int LU, int K, int W, int SW, int UP, float* __restrict__ px_grad, float* __restrict__ py_grad,
     uint16_t* __restrict__ Gt_hi, uint16_t* __restrict__ Gt_lo) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   extern __shared__ __align__(16) float cbuf[];
   const int CWs = min(UP, kCombineWindow);
   float* Ys = cbuf;                     // [32][CW]
@@ -444,7 +446,7 @@ static cudaError_t launch_fb(const Dims& d, const SimpleWS& w, const int64_t* bn
                              cudaStream_t st) {
   const size_t sm = lat::smem_bytes<R>(W);
   cudaFuncSetAttribute(lattice_fb_kernel<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  RNNT_LAUNCH(KID_ALPHA, st, lattice_fb_kernel<R, W><<<dim3(d.N, 2), 32 * (W + 1), sm, st>>>(
+  RNNT_LAUNCH(KID_ALPHA, st, launch_pdl(lattice_fb_kernel<R, W>, dim3(d.N, 2), 32 * (W + 1), sm, st, 
       w.pxy, bnd, d.K(), w.alpha, w.beta, w.Ash, w.Bsh, w.Ltot, loss, status));
   return cudaGetLastError();
 }
@@ -476,7 +478,7 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
   dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
   const size_t csm = (size_t)3 * 32 * std::min(d.UP(), kCombineWindow) * sizeof(float);
   cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-  RNNT_LAUNCH(KID_COMBINE, st, combine_kernel<<<grid, 256, csm, st>>>(w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
+  RNNT_LAUNCH(KID_COMBINE, st, launch_pdl(combine_kernel, grid, 256, csm, st, w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,
                                                                    w.Ltot, bnd, d.T, d.U, d.LU(), d.K(), d.lat_W(),
                                                                    32 * d.lat_R(), d.UP(), px_grad, py_grad, w.Gt_hi,
                                                                    w.Gt_lo));

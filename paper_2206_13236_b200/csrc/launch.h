@@ -4,6 +4,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace rnnt {
 
 enum KernelId {
@@ -38,7 +40,36 @@ int env_int(const char* name, int dflt);
 void launch_begin(int id, cudaStream_t st);
 void launch_end(int id, cudaStream_t st);
 
+// Programmatic dependent launch: every library kernel is launched with programmatic stream
+// serialization and starts with RNNT_GDC(), which waits for the preceding grid on the stream (its
+// results visible).  No early launch_dependents trigger: the dependent grid is launched as the primary's
+// blocks exit, so its launch processing overlaps the primary's tail without its blocks taking SM slots
+// while the primary still runs (an early trigger measured 7% slower at c5: the waiting blocks cost the
+// running kernel occupancy).  Measured: c5 eager 0.527 -> 0.502 ms, graph replay unchanged within noise.
+// RNNT_PDL=0 turns the attribute off (plain stream order; griddepcontrol.wait is then a no-op).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 }  // namespace rnnt
+
+#define RNNT_GDC()                                                      \
+  do {                                                                  \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                  \
+  } while (0)
 
 #define RNNT_LAUNCH(id, st, ...)           \
   do {                                     \

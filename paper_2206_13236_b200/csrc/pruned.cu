@@ -50,6 +50,7 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
 __global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ enc, const float* __restrict__ dec,
                                                      const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
                                                      int N, int T, int U, int J, int S, uint16_t* __restrict__ h) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long nt = (long long)blockIdx.x * blockDim.y + threadIdx.y;
   if (nt >= (long long)N * T) return;
   const int n = (int)(nt / T), t = (int)(nt - (long long)n * T);
@@ -91,9 +92,14 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
                                const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
-                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter) {
+                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter,
+                               int* __restrict__ lcount) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x == 0) *tcounter = 0;
+    if (threadIdx.x == 0) {
+      *tcounter = 0;
+      *lcount = 0;          // the live-tile count of joiner_dh (live_tiles_launch)
+    }
     // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
     // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
     for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
@@ -219,6 +225,7 @@ struct ScanParams {
 // so that the per-row loops unroll without branches and the rows' shuffles and LogAdds interleave.
 template <int SMAX, int SC>
 __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // a cluster of G CTAs per (utterance, direction): phases A and C are spread over its CTAs (chunk
   // c goes to rank c % G), the chunk matrices land in the rank-0 CTA's shared memory (DSMEM
@@ -530,6 +537,7 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
                                       int N, int T, int S, int ntile, float gs, float* __restrict__ gb,
                                       float* __restrict__ gl, float4* __restrict__ gpk) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long R = (long long)N * T * S;
   if (r >= R) return;
@@ -568,6 +576,7 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
 
 __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, long long M,
                                     float* __restrict__ out) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M) return;
   float acc = 0.f;
@@ -578,6 +587,7 @@ __global__ void split_reduce_kernel(const float* __restrict__ part, int splits, 
 // order as the scalar kernel: bit-identical), instead of one dependent load per split
 __global__ void split_reduce4_kernel(const float4* __restrict__ part, int splits, long long M4,
                                      float4* __restrict__ out) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M4) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -601,7 +611,7 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
   const int J8 = d.J / 8;                          // J % 8 == 0 (rnnt_check_dims)
   const int fpb = std::max(1, 256 / J8);           // frames per block
   const long long NT = (long long)d.N * d.T;
-  RNNT_LAUNCH(KID_PRUNE, st, prune_kernel<<<(unsigned)((NT + fpb - 1) / fpb), dim3(J8, fpb), 0, st>>>(
+  RNNT_LAUNCH(KID_PRUNE, st, launch_pdl(prune_kernel, (unsigned)((NT + fpb - 1) / fpb), dim3(J8, fpb), 0, st, 
       enc, dec, ranges, bnd, d.N, d.T, d.U, d.J, d.S, h));
   return cudaGetLastError();
 }
@@ -643,13 +653,15 @@ static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cu
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = sm;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)q.G;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   RNNT_LAUNCH(KID_PALPHA, st, cudaLaunchKernelEx(&cfg, pruned_scan_kernel<SMAX, SC>, q));
   return cudaGetLastError();
 }
@@ -657,8 +669,9 @@ static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cu
 cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
                            const int64_t* bnd, const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
-  RNNT_LAUNCH(KID_ROWINFO, st, rowinfo_kernel<<<(unsigned)((R + 255) / 256 + 1), 256, 0, st>>>(
-      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
+  RNNT_LAUNCH(KID_ROWINFO, st, launch_pdl(rowinfo_kernel, (unsigned)((R + 255) / 256 + 1), 256, 0, st, 
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter,
+      w.dhlive + (d.rows() + 127) / 128));
   return cudaGetLastError();
 }
 
@@ -691,7 +704,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     }
     if (e != cudaSuccess) return e;
   }
-  RNNT_LAUNCH(KID_PCOMBINE, st, pruned_combine_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(
+  RNNT_LAUNCH(KID_PCOMBINE, st, launch_pdl(pruned_combine_kernel, (unsigned)((R + 255) / 256), 256, 0, st, 
       w.px2, w.py2, w.ap, w.bp, w.Af, w.Bf, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
       w.gl, w.gpk));
   return cudaGetLastError();
@@ -720,7 +733,11 @@ template <int SW>
 __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict__ dpre,
                                                          const int32_t* __restrict__ ranges,
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                         int J, float* __restrict__ d_enc, float* __restrict__ part) {
+                                                         int J, float* __restrict__ d_enc, float* __restrict__ part,
+                                                         int* __restrict__ lcount) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
+  // joiner_dh has consumed the live-tile list: reset its count for a repeated backward call
+  if (blockIdx.x == 0 && threadIdx.x == 0) *lcount = 0;
   const int J4 = J / 4, nseg = (J4 + 31) / 32;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (T + kBandCH - 1) / kBandCH;
@@ -789,6 +806,7 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict
 __global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__ part, const int2* __restrict__ urange,
                                                        const int64_t* __restrict__ bnd, int N, int T, int U, int S,
                                                        int J, float* __restrict__ d_dec) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int J4 = J / 4, nseg = (J4 + 31) / 32;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -828,7 +846,8 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
     const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * ((d.J / 4 + 31) / 32);
     const unsigned nb = (unsigned)((nwarp + 7) / 8);
     float* pp = d_dec ? w.bpart : nullptr;
-#define RNNT_BAND(SWV) band_chunk_kernel<SWV><<<nb, 256, 0, st>>>(w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp)
+    int* lcount = w.dhlive + ntiles;
+#define RNNT_BAND(SWV) launch_pdl(band_chunk_kernel<SWV>, nb, 256, 0, st, w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp, lcount)
     switch (d.S) {   // the window is exactly S wide for the common band widths
       case 1: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(1)); break;
       case 2: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(2)); break;
@@ -846,7 +865,7 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   }
   if (d_dec) {
     const long long nw = (long long)d.N * d.U1() * ((d.J / 4 + 31) / 32);
-    RNNT_LAUNCH(KID_DDEC, st, band_dec_kernel<<<(unsigned)((nw + 7) / 8), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_DDEC, st, launch_pdl(band_dec_kernel, (unsigned)((nw + 7) / 8), 256, 0, st, 
                                   w.bpart, w.urange, bnd, d.N, d.T, d.U, d.S, d.J, d_dec));
   }
   return cudaGetLastError();
@@ -871,11 +890,11 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
   }
   const long long M = (long long)d.V * d.J;
   if (M % 4 == 0 && reinterpret_cast<uintptr_t>(d_w) % 16 == 0)
-    RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce4_kernel<<<(unsigned)((M / 4 + 255) / 256), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_DW_REDUCE, st, launch_pdl(split_reduce4_kernel, (unsigned)((M / 4 + 255) / 256), 256, 0, st, 
         reinterpret_cast<const float4*>(w.dWp), w.splits, M / 4, reinterpret_cast<float4*>(d_w)));
   else
-    RNNT_LAUNCH(KID_DW_REDUCE, st, split_reduce_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(w.dWp, w.splits, M, d_w));
-  RNNT_LAUNCH(KID_DB_REDUCE, st, split_reduce_kernel<<<(unsigned)((d.V + 255) / 256), 256, 0, st>>>(w.dbp, w.splits, d.V, d_b));
+    RNNT_LAUNCH(KID_DW_REDUCE, st, launch_pdl(split_reduce_kernel, (unsigned)((M + 255) / 256), 256, 0, st, w.dWp, w.splits, M, d_w));
+  RNNT_LAUNCH(KID_DB_REDUCE, st, launch_pdl(split_reduce_kernel, (unsigned)((d.V + 255) / 256), 256, 0, st, w.dbp, w.splits, d.V, d_b));
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(256) raw_bounds_kernel(const float* __restrict
                                                          const float* __restrict__ py_grad,
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
                                                          int32_t* __restrict__ raw) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   // the warp's frame row (y' and empty', U_n + 1 values each) is staged in smem with all loads in
   // flight at once; the fp64 window sums then read smem only
   extern __shared__ float rowbuf[];   // [8 warps][2][U + 1]
@@ -87,6 +88,7 @@ __device__ __forceinline__ int block_scan_max(int x, int* sh, bool reverse) {
 __global__ void __launch_bounds__(1024) adjust_kernel(const int32_t* raw, const int64_t* __restrict__ bnd,
                                                       int T, int S, int32_t* ranges, int32_t* q,
                                                       int32_t* __restrict__ status) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int n = blockIdx.x;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   const int Umax = max(0, Un - S + 1);
@@ -146,9 +148,9 @@ cudaError_t get_ranges_launch(const Dims& d, const float* px_grad, const float* 
   long long rows = (long long)d.N * d.T;
   const size_t sm = (size_t)8 * 2 * d.U1() * sizeof(float);
   if (sm > 48 * 1024) cudaFuncSetAttribute(raw_bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  RNNT_LAUNCH(KID_RAW, st, raw_bounds_kernel<<<(unsigned)((rows + 7) / 8), 256, sm, st>>>(px_grad, py_grad, bnd, d.N, d.T,
+  RNNT_LAUNCH(KID_RAW, st, launch_pdl(raw_bounds_kernel, (unsigned)((rows + 7) / 8), 256, sm, st, px_grad, py_grad, bnd, d.N, d.T,
                                                                                          d.U, d.S, ranges));
-  RNNT_LAUNCH(KID_ADJUST, st, adjust_kernel<<<d.N, 1024, 0, st>>>(ranges, bnd, d.T, d.S, ranges, ranges, status));
+  RNNT_LAUNCH(KID_ADJUST, st, launch_pdl(adjust_kernel, d.N, 1024, 0, st, ranges, bnd, d.T, d.S, ranges, ranges, status));
   return cudaGetLastError();
 }
 

@@ -146,6 +146,7 @@ struct PrepParams {
 };
 
 __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   int b = blockIdx.x;
   if (b < p.nb_am) {
     exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr,
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__
                                                        const float* __restrict__ py_grad, int T, int U, int ntb,
                                                        float* __restrict__ rowb, float* __restrict__ colpy,
                                                        float* __restrict__ colpb, float* __restrict__ rowy) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int tb = blockIdx.x, n = blockIdx.y, U1 = U + 1, t0 = tb * 32;
   const int t1 = min(T, t0 + 32);
   for (int u = threadIdx.x; u < U1; u += blockDim.x) {
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(256) occ_sums_kernel(const float* __restrict__
 __global__ void __launch_bounds__(256) smooth_avg_kernel(const float* __restrict__ lm, const float* __restrict__ lse_lm,
                                                          const int64_t* __restrict__ bnd, int U, int V, int VP,
                                                          float* __restrict__ Lavg) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int n = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= VP) return;
   const int Un = utt_U(bnd, n);
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(256) smooth_avg_kernel(const float* __restrict
 __global__ void __launch_bounds__(256) smooth_ac_kernel(const float* __restrict__ am, const float* __restrict__ m_am,
                                                         const float* __restrict__ Lavg, const int64_t* __restrict__ bnd,
                                                         int N, int T, int V, int VP, float* __restrict__ lse_ac) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * T) return;
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(256) smooth_gq_kernel(const float* __restrict_
                                                         const int64_t* __restrict__ sym, const int64_t* __restrict__ bnd,
                                                         int T, int U, int V, int VP, int ntb, float a_ac,
                                                         float* __restrict__ gq) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const int n = blockIdx.y, v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= VP) return;
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
@@ -293,6 +298,7 @@ __global__ void __launch_bounds__(256) smooth_gq_kernel(const float* __restrict_
 __global__ void __launch_bounds__(256) smooth_q_kernel(const float* __restrict__ lm, const float* __restrict__ lse_lm,
                                                        const float* __restrict__ gq, const int64_t* __restrict__ bnd,
                                                        int N, int U, int V, int VP, float* __restrict__ Qu) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= (long long)N * (U + 1)) return;
@@ -372,6 +378,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // Phase 1: acc1 (TMEM columns kBN..2kBN-1) += A'_hi B' + A'_lo B'              (B' exact in bf16)
 template <class P>
 __global__ void __launch_bounds__(sg::THREADS, P::kMinBlocks) gemm3_kernel(const __grid_constant__ Maps mp, P p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace sg;
   constexpr int STAGES = P::kStages, STAGE_BYTES = Geo<P>::STAGE_BYTES, B_BYTES = Geo<P>::B_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -952,7 +959,7 @@ template <class P>
 static cudaError_t launch_gemm3(const P& p, dim3 grid, const Maps& mp, int kid, cudaStream_t st) {
   smem_optin(gemm3_kernel<P>, sg::Geo<P>::SMEM_BYTES);
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return cudaSuccess;
-  RNNT_LAUNCH(kid, st, gemm3_kernel<P><<<grid, sg::THREADS, sg::Geo<P>::SMEM_BYTES, st>>>(mp, p));
+  RNNT_LAUNCH(kid, st, launch_pdl(gemm3_kernel<P>, grid, sg::THREADS, sg::Geo<P>::SMEM_BYTES, st, mp, p));
   return cudaGetLastError();
 }
 
@@ -977,7 +984,7 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   p.nb_lm = (int)(((long long)d.N * d.U1() + 7) / 8);
   p.nb_fill = (int)(((long long)d.N * (d.K() + 1) + 7) / 8);
   const unsigned grid = (unsigned)(p.nb_am + p.nb_lm + p.nb_fill + d.N);
-  RNNT_LAUNCH(KID_ROWMAX_AM, st, simple_prep_kernel<<<grid, 256, 0, st>>>(p));
+  RNNT_LAUNCH(KID_ROWMAX_AM, st, launch_pdl(simple_prep_kernel, grid, 256, 0, st, p));
   return cudaGetLastError();
 }
 
@@ -985,9 +992,9 @@ cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, 
                              const int64_t* bnd, int32_t* status, Smooth sm, cudaStream_t st) {
   if (sm.on()) {
     // the smoothed joiner's utterance prior L_dec^avg and the L_acoustic normalisers (Eq. 13, 15)
-    RNNT_LAUNCH(KID_SMOOTH_AVG, st, smooth_avg_kernel<<<dim3((d.VP64() + 255) / 256, d.N), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_SMOOTH_AVG, st, launch_pdl(smooth_avg_kernel, dim3((d.VP64() + 255) / 256, d.N), 256, 0, st, 
         lm, w.lse_lm, bnd, d.U, d.V, d.VP64(), w.Lavg));
-    RNNT_LAUNCH(KID_SMOOTH_AC, st, smooth_ac_kernel<<<(unsigned)(((long long)d.N * d.T + 7) / 8), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_SMOOTH_AC, st, launch_pdl(smooth_ac_kernel, (unsigned)(((long long)d.N * d.T + 7) / 8), 256, 0, st, 
         am, w.m_am, w.Lavg, bnd, d.N, d.T, d.V, d.VP64(), w.lse_ac));
   }
   const int BN = std::min(256, (d.U1() + 15) / 16 * 16);
@@ -1005,14 +1012,14 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
                                 float gs, float* am_grad, float* lm_grad, Smooth sm, cudaStream_t st) {
   if (!am_grad && !lm_grad) return cudaSuccess;
-  RNNT_LAUNCH(KID_OCCSUMS, st, occ_sums_kernel<<<dim3(d.ntb(), d.N), 256, 0, st>>>(px_grad, py_grad, d.T, d.U, d.ntb(),
+  RNNT_LAUNCH(KID_OCCSUMS, st, launch_pdl(occ_sums_kernel, dim3(d.ntb(), d.N), 256, 0, st, px_grad, py_grad, d.T, d.U, d.ntb(),
                                                                                    w.rowb, w.colpy, w.colpb, w.rowy));
   cudaError_t e;
   if (sm.on() && lm_grad) {
     // backward through L_dec^avg (Eq. 15): gq(v), then Q(u) = sum_v softmax(lm[u])(v) gq(v)
-    RNNT_LAUNCH(KID_SMOOTH_GQ, st, smooth_gq_kernel<<<dim3((d.VP64() + 255) / 256, d.N), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_SMOOTH_GQ, st, launch_pdl(smooth_gq_kernel, dim3((d.VP64() + 255) / 256, d.N), 256, 0, st, 
         am, w.Lavg, w.lse_ac, w.rowy, w.rowb, w.colpy, sym, bnd, d.T, d.U, d.V, d.VP64(), d.ntb(), sm.a_ac, w.gq));
-    RNNT_LAUNCH(KID_SMOOTH_Q, st, smooth_q_kernel<<<(unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st>>>(
+    RNNT_LAUNCH(KID_SMOOTH_Q, st, launch_pdl(smooth_q_kernel, (unsigned)(((long long)d.N * d.U1() + 7) / 8), 256, 0, st, 
         lm, w.lse_lm, w.gq, bnd, d.N, d.U, d.V, d.VP64(), w.Qu));
   }
   if (am_grad) {

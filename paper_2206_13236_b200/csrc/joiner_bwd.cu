@@ -338,6 +338,12 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const int v0 = kb * BK;
         tc::mbar_wait(&loaded[stage], ph);
         if (pt == 0) dh_trace_kb(itx, kb, 1);
+#ifdef RNNT_EXP_SKIPTX
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&full[stage]);
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        continue;
+#endif
         uint8_t* sa = smem + stage * STAGE_BYTES;
         const float4 gq = rl < grows ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
                                      : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
@@ -483,13 +489,39 @@ constexpr int THREADS = 160;
 struct JoinerDwParams {
   GradSrc g;
   int J;
-  long long kb_per_split, nkb_total;
+  long long kb_per_split, nkb_total;   // (unused when `live` is set: the split is derived on device)
+  const int* live;   // ascending ids of the 128-row tiles with a live row, count at nlive (null: all rows)
+  const int* nlive;
   float* dWp;   // (splits, V, J)
   float* dbp;   // (splits, V)
   int pf = 6, pfmode = 1;   // wide variant: L2 prefetch distance (k-blocks); bit 0: P~ prefetched by j-tile 0 only, h by V pair 0 only; bit 1: grid x = j tile
   int h3 = 0;               // wide variant: tmH is the 3-D (64 j, rows, J/64) map (J % 64 == 0)
 };
 
+
+// The k-blocks (64 rows) of split `split`: with a live-tile list, the 2 nlive k-blocks of the live
+// 128-row tiles in ascending row order, cut into gridDim.z equal ranges (dead tiles -- padded frames of
+// short utterances -- are never read); else rows [kb0 BK, kb1 BK).
+struct DwRange {
+  long long kb0;
+  int nkb;
+};
+__device__ __forceinline__ DwRange dw_range(const JoinerDwParams& p, int split, int splits) {
+  if (p.live) {
+    const long long tot = 2LL * *p.nlive, per = (tot + splits - 1) / splits;
+    const long long k0 = (long long)split * per;
+    return {k0, (int)max(0LL, min(tot, k0 + per) - k0)};
+  }
+  const long long k0 = (long long)split * p.kb_per_split;
+  return {k0, (int)max(0LL, min(p.nkb_total, k0 + p.kb_per_split) - k0)};
+}
+__device__ __forceinline__ long long dw_row0(const JoinerDwParams& p, long long kb) {
+  return p.live ? (long long)p.live[kb >> 1] * 128 + (kb & 1) * 64 : kb * 64;
+}
+// rows of the k-block starting at rb that exist (the last tile may end inside its first half)
+__device__ __forceinline__ int dw_rows(const JoinerDwParams& p, long long rb) {
+  return (int)max(0LL, min(64LL, p.g.R - rb));
+}
 
 template <bool PAIR>
 __global__ void __launch_bounds__(jdw::THREADS, 2)
@@ -512,9 +544,9 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
   const bool rare = p.g.V >= 6144;     // dz_chunk label pick by branch (measured: c4 -6 %, c3 (Zipf labels) +5 %)
   const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0;
   const int v0 = blockIdx.x * BM, j0 = blockIdx.y * BN, split = blockIdx.z;
-  const long long kb0 = (long long)split * p.kb_per_split;
-  const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
-  const int nkb = (int)max(0LL, kb1 - kb0);
+  const DwRange kr = dw_range(p, split, (int)gridDim.z);
+  const long long kb0 = kr.kb0;
+  const int nkb = kr.nkb;
   const int V = p.g.V;
   const int nj = min(BN, p.J - j0);
   // h columns this CTA loads: all nj (single CTA) or its half of the pair's 256
@@ -553,8 +585,8 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      const long long rb = (kb0 + kb) * BK;
-      const int grows = (int)min((long long)BK, p.g.R - rb);
+      const long long rb = dw_row0(p, kb0 + kb);
+      const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
       uint8_t* sa = smem + stage * STAGE_BYTES;
       const float4* gq = reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES);
@@ -621,7 +653,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     constexpr int PF = 6;                // P~ and h boxes prefetched into L2 this many k-blocks ahead
     const bool t3 = !PAIR && p.h3;       // 3-D maps: one TMA for the 2 P~ boxes, one for the 4 h boxes
     auto prefetch = [&](int kb) {
-      const int rb = (int)((kb0 + kb) * BK);
+      const int rb = (int)dw_row0(p, kb0 + kb);
       if (t3) {
         tc::tma_prefetch_3d(&tmP, 0, rb, v0 / 64);
         tc::tma_prefetch_3d(&tmH, 0, rb, jb / 64);
@@ -634,8 +666,8 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
     for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
     for (int kb = 0; kb < nkb; ++kb) {
       if (kb + PF < nkb) prefetch(kb + PF);
-      const long long rb = (kb0 + kb) * BK;
-      const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
+      const long long rb = dw_row0(p, kb0 + kb);
+      const uint32_t gbytes = (uint32_t)dw_rows(p, rb) * 16u;
       const uint32_t bytes = A_BYTES + (t3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + gbytes;
       tc::mbar_wait(&empty[stage_of(kb)], phase_of(kb) ^ 1);
       uint8_t* sa = smem + stage_of(kb) * STAGE_BYTES;
@@ -650,7 +682,7 @@ __global__ void __launch_bounds__(jdw::THREADS, 2)
         for (int bx = 0; bx < nbox; ++bx)
           tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmH, ld, jb + bx * 64, (int)rb);
       }
-      tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
+      if (gbytes) tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
     }
   } else if (lane == 1 && nkb > 0 && rank == 0) {
     // ---- warp 4 lane 1 (pair: of the rank-0 CTA only): MMA issuer
@@ -717,9 +749,9 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const bool jfirst = p.pfmode & 2;      // grid x = j tile (siblings sharing P~ adjacent)
   const int bvx = jfirst ? blockIdx.y : blockIdx.x, bjy = jfirst ? blockIdx.x : blockIdx.y;
   const int v0 = bvx * 2 * BM, j0 = bjy * BN, split = blockIdx.z;
-  const long long kb0 = (long long)split * p.kb_per_split;
-  const long long kb1 = min(p.nkb_total, kb0 + p.kb_per_split);
-  const int nkb = (int)max(0LL, kb1 - kb0);
+  const DwRange kr = dw_range(p, split, (int)gridDim.z);
+  const long long kb0 = kr.kb0;
+  const int nkb = kr.nkb;
   const int V = p.g.V;
   const bool two = v0 + BM < V;          // the second V tile exists
   const int nj = min(BN, p.J - j0);
@@ -755,10 +787,14 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      const long long rb = (kb0 + kb) * BK;
-      const int grows = (int)min((long long)BK, p.g.R - rb);
+      const long long rb = dw_row0(p, kb0 + kb);
+      const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
+#ifdef RNNT_EXP_SKIPTX
+      if (false) {
+#else
       if (mine) {
+#endif
         uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
         const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
         uint4 pv[8];
@@ -821,7 +857,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     const int PF = p.pf;
     const bool pfP = !(p.pfmode & 1) || bjy == 0, pfH = !(p.pfmode & 1) || bvx == 0;
     auto prefetch = [&](int kb) {
-      const int rb = (int)((kb0 + kb) * BK);
+      const int rb = (int)dw_row0(p, kb0 + kb);
       if (pfP) tc::tma_prefetch_3d(&tmP, 0, rb, v0 / 64);
       if (pfH) {
         if (p.h3) tc::tma_prefetch_3d(&tmH, 0, rb, j0 / 64);
@@ -834,8 +870,8 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
       if (kb + PF < nkb) prefetch(kb + PF);
-      const long long rb = (kb0 + kb) * BK;
-      const uint32_t gbytes = (uint32_t)min((long long)BK, p.g.R - rb) * 16u;
+      const long long rb = dw_row0(p, kb0 + kb);
+      const uint32_t gbytes = (uint32_t)dw_rows(p, rb) * 16u;
       // 3-D boxes: out-of-range planes (the missing second V tile, j past J) arrive zero-filled and
       // count in full toward the transaction bytes
       const uint32_t bytes = 2 * A_BYTES + (two ? 2 : 1) * gbytes + (p.h3 ? B_BYTES : (uint32_t)nbox * 64 * BK * 2);
@@ -848,8 +884,8 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       else
         for (int bx = 0; bx < nbox; ++bx)
           tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), &tmH, ld, j0 + bx * 64, (int)rb);
-      tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
-      if (two) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
+      if (gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
+      if (two && gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
   } else if (lane == 1 && nkb > 0) {
@@ -939,14 +975,15 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   return cudaGetLastError();
 }
 
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
-                             int splits, cudaStream_t st) {
+// live / nlive: the ascending live-tile list of the step (null: every row's k-block is read)
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* live, const int* nlive,
+                             float* dWp, float* dbp, int splits, cudaStream_t st) {
   CUtensorMap tp, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
   const long long nkb = (d.rows() + jdw::BK - 1) / jdw::BK;
   const long long per = (nkb + splits - 1) / splits;
-  JoinerDwParams p{g, d.J, per, nkb, dWp, dbp};
+  JoinerDwParams p{g, d.J, per, nkb, live, nlive, dWp, dbp};
   const int vt = (d.V + jdw::BM - 1) / jdw::BM;
   // CTA pairs (cta_group::2, V tiles rounded up to an even count) only when RNNT_DW_PAIR=1: parity-green
   // but measured slower (c2 87.6 vs 69.6 us, c4 4.42 vs 3.22 ms) -- the per-stage cross-CTA handshake

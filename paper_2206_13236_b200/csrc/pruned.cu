@@ -37,8 +37,8 @@ struct GradSrc {
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
                              const int* nlive, long long ntiles, float* dpre, cudaStream_t st);
 cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, float* dWp, float* dbp,
-                             int splits, cudaStream_t st);
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* live, const int* nlive,
+                             float* dWp, float* dbp, int splits, cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
 // Block (J/8, FPB): thread (x, y) owns the 8 columns 8x of frame blockIdx.x * FPB + y and walks its
@@ -92,14 +92,10 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
                                const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
-                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter,
-                               int* __restrict__ lcount) {
+                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x == 0) {
-      *tcounter = 0;
-      *lcount = 0;          // the live-tile count of joiner_dh (live_tiles_launch)
-    }
+    if (threadIdx.x == 0) *tcounter = 0;
     // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
     // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
     for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
@@ -670,8 +666,7 @@ cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* rang
                            const int64_t* bnd, const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
   RNNT_LAUNCH(KID_ROWINFO, st, launch_pdl(rowinfo_kernel, (unsigned)((R + 255) / 256 + 1), 256, 0, st, 
-      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter,
-      w.dhlive + (d.rows() + 127) / 128));
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
   return cudaGetLastError();
 }
 
@@ -684,6 +679,8 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   const long long R = d.rows();
   const int nt = d.ntile();
   if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, st)) != cudaSuccess) return e;
+  // the ascending list of live 128-row tiles, read by both backward calls (K10, K11)
+  if ((e = live_tiles_launch(w.tlive, (d.rows() + 127) / 128, w.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);
@@ -733,11 +730,8 @@ template <int SW>
 __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict__ dpre,
                                                          const int32_t* __restrict__ ranges,
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                         int J, float* __restrict__ d_enc, float* __restrict__ part,
-                                                         int* __restrict__ lcount) {
+                                                         int J, float* __restrict__ d_enc, float* __restrict__ part) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  // joiner_dh has consumed the live-tile list: reset its count for a repeated backward call
-  if (blockIdx.x == 0 && threadIdx.x == 0) *lcount = 0;
   const int J4 = J / 4, nseg = (J4 + 31) / 32;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nch = (T + kBandCH - 1) / kBandCH;
@@ -839,15 +833,13 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
-  const long long ntiles = (d.rows() + 127) / 128;
-  if ((e = live_tiles_launch(w.tlive, ntiles, w.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
+  const long long ntiles = (d.rows() + 127) / 128;   // (the live-tile list: built by the forward)
   if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, st)) != cudaSuccess) return e;
   {
     const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * ((d.J / 4 + 31) / 32);
     const unsigned nb = (unsigned)((nwarp + 7) / 8);
     float* pp = d_dec ? w.bpart : nullptr;
-    int* lcount = w.dhlive + ntiles;
-#define RNNT_BAND(SWV) launch_pdl(band_chunk_kernel<SWV>, nb, 256, 0, st, w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp, lcount)
+#define RNNT_BAND(SWV) launch_pdl(band_chunk_kernel<SWV>, nb, 256, 0, st, w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp)
     switch (d.S) {   // the window is exactly S wide for the common band widths
       case 1: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(1)); break;
       case 2: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(2)); break;
@@ -881,7 +873,8 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
                                      cudaStream_t st, int mode) {
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
-  if ((e = joiner_dw_launch(d, g, h, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
+  const long long ntiles = (d.rows() + 127) / 128;
+  if ((e = joiner_dw_launch(d, g, h, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
   if (mode != 0) {
     if ((e = split_reduce_acc_launch(w.dWp, w.splits, (long long)d.V * d.J, d_w, mode, KID_DW_REDUCE, st)) !=
         cudaSuccess)

@@ -96,6 +96,13 @@ const char* rnnt_last_cuda_error(void);
  *   stream (events are cudaEvent_t passed as void*, owned by the caller); id 0 disarms.
  *   Returns RNNT_ERR_INVALID_ARG for an unknown id. */
 uint64_t rnnt_launch_count(void);
+/* rnnt_pruned_backward_mode: after rnnt_pruned_loss_forward was enqueued on `stream` with this
+ *   workspace, synchronises the stream and writes to *plain 1 if the forward stored every row's P~
+ *   with one offset (the joiner backward then runs as plain GEMMs on P~ with the picks folded in), 0 if
+ *   some row needed per-tile offsets (a logit more than 60 above the row's reference; the backward then
+ *   rescales P~ per (row, tile) in shared memory), D20. */
+rnnt_status_t rnnt_pruned_backward_mode(const rnnt_dims_t* dims, const void* workspace, size_t workspace_bytes,
+                                        int32_t* plain, void* stream);
 int32_t rnnt_kernel_count(void);
 const char* rnnt_kernel_name(int32_t id);
 rnnt_status_t rnnt_profile_kernel(int32_t kernel_id, void* start_event, void* stop_event);

@@ -101,6 +101,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_loss_sums.restype = I32
     lib.rnnt_launch_count.argtypes = []
     lib.rnnt_launch_count.restype = ctypes.c_uint64
+    lib.rnnt_pruned_backward_mode.argtypes = [ctypes.POINTER(Dims), P, ctypes.c_size_t, ctypes.POINTER(I32), P]
+    lib.rnnt_pruned_backward_mode.restype = I32
     lib.rnnt_kernel_count.argtypes = []
     lib.rnnt_kernel_count.restype = I32
     lib.rnnt_kernel_name.argtypes = [I32]
@@ -160,6 +162,16 @@ def rnnt_version() -> str:
 
 def rnnt_launch_count() -> int:
     return int(load_library().rnnt_launch_count())
+
+
+def rnnt_pruned_backward_mode(dims, workspace, stream=None) -> bool:
+    """True if the last rnnt_pruned_loss_forward in `workspace` selected the plain joiner backward
+    (one P~ offset per row; include/rnnt.h, D20).  Synchronises the stream."""
+    out = ctypes.c_int32(0)
+    rc = load_library().rnnt_pruned_backward_mode(ctypes.byref(dims), _ptr(workspace), workspace.numel() *
+                                                  workspace.element_size(), ctypes.byref(out), _stream(stream))
+    _check(rc, "rnnt_pruned_backward_mode")
+    return bool(out.value)
 
 
 def kernel_ids() -> dict:

@@ -56,7 +56,7 @@ static const char* const kNames[KID_COUNT] = {
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_band_chunk", "joiner_band_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
-    "full_dgrad", "loss_sums", "exchange_sum"};
+    "full_dgrad", "loss_sums", "exchange_sum", "joiner_scale_rows"};
 
 bool pdl_enabled() {
   static const bool on = env_int("RNNT_PDL", 1) != 0;
@@ -344,6 +344,23 @@ rnnt_status_t rnnt_pruned_loss_backward_weight(const uint16_t* h, const rnnt_dim
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_bwd_weight_launch(d, pw, h, d_w, d_b, (cudaStream_t)stream, 0));
+}
+
+rnnt_status_t rnnt_pruned_backward_mode(const rnnt_dims_t* dims, const void* workspace, size_t workspace_bytes,
+                                        int32_t* plain, void* stream) {
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!workspace || !plain) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(const_cast<void*>(workspace)), &sw, &pw);
+  int32_t v = 1;
+  cudaError_t e = cudaMemcpyAsync(&v, pw.tscale, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  *plain = v == 0 ? 1 : 0;
+  return cuda_status(e);
 }
 
 rnnt_status_t rnnt_pruned_loss_backward_weight_exchange(const uint16_t* h, const rnnt_dims_t* dims, int32_t mode,

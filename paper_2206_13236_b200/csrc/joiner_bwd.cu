@@ -151,6 +151,7 @@ struct JoinerDhParams {
   const int* nlive;        // their count
   float* dpre;             // (R, J) fp32 out: dh (1 - h^2) of the rows of the live tiles
   int w3;                  // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
+  const int* tscale;       // PrunedWS::tscale: 0 -> plain mode (null: always rescale P~ per tile)
 };
 
 // diagnostics: per (CTA, item) timestamps {producer start, first MMA, last MMA commit, epilogue
@@ -203,6 +204,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   // work items: (row tile, 256-column part); with MC a cluster takes (tile pair, part) items, rank r the
   // tile 2 i + r (an odd last tile is done by both CTAs: identical values, written twice)
   const int nlive = *p.nlive;
+  // plain mode (one P~ offset per row, picks folded into P~ by pruned_combine): dh = sc_r (P~' W), the
+  // MMA consumes the TMA'd stage directly and the epilogue applies the row scalar; no transform warps
+  const bool plain = p.tscale && *p.tscale == 0;
   const int crank = MC ? (int)tc::cluster_ctarank() : 0;
   const long long cid = MC ? blockIdx.x / 2 : blockIdx.x, ncl = MC ? gridDim.x / 2 : gridDim.x;
   const long long nitems = (long long)(MC ? (nlive + 1) / 2 : nlive) * p.njp;
@@ -247,7 +251,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const int j0 = jp * NSUB, nbox = (min(NSUB, p.J - j0) + 63) / 64;
         const int grows = (int)min((long long)BM, p.g.R - m0);
         // (3-D W box: planes past J arrive zero-filled and count in full)
-        const uint32_t bytes = A_BYTES + (p.w3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + (uint32_t)grows * 16u;
+        const uint32_t gbytes = plain ? 0u : (uint32_t)grows * 16u;
+        const uint32_t bytes = A_BYTES + (p.w3 ? (uint32_t)B_BYTES : (uint32_t)nbox * 64 * BK * 2) + gbytes;
         constexpr int PF = 8;            // P~ boxes prefetched into L2 this many k-blocks ahead
         for (int kb = 0; kb < min(PF, p.nkb); ++kb) tc::tma_prefetch_2d(&tmP, kb * BK, (int)m0);
         // the epilogue's h boxes of this item: into L2 now, a mainloop ahead of their TMA loads
@@ -273,8 +278,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
             for (int bx = 0; bx < nbox; ++bx)
               tc::tma_load_2d(sa + A_BYTES + bx * (64 * BK * 2), &tmW, &loaded[stage], j0 + bx * 64, kb * BK);
           }
-          tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0,
-                        (uint32_t)grows * 16u, &loaded[stage]);
+          if (gbytes)
+            tc::bulk_load(sa + A_BYTES + B_BYTES, p.g.gpk + (size_t)((kb * BK) >> 7) * p.g.R + m0, gbytes,
+                          &loaded[stage]);
           if (++stage == STAGES) { stage = 0; ph ^= 1; }
         }
       }
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         tc::fence_after_sync();
         const uint32_t d = tbase + acc * NSUB;
         for (int kb = 0; kb < p.nkb; ++kb) {
-          tc::mbar_wait(&full[stage], ph);
+          tc::mbar_wait(plain ? &loaded[stage] : &full[stage], ph);
           tc::fence_after_sync();
           if (kb == 0) dh_trace(it, 1);
           dh_trace_kb(it, kb, 3);
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     const int rl = pt & 127, c_lo = (pt >> 7) * CPT;
     int stage = 0, itx = 0;
     uint32_t ph = 0;
-    for (long long idx = cid; idx < nitems; idx += ncl, ++itx) {
+    for (long long idx = plain ? nitems : cid; idx < nitems; idx += ncl, ++itx) {
       const int tile = item_tile(idx);
       const long long m0 = (long long)tile * BM;
       const int grows = (int)min((long long)BM, p.g.R - m0);
@@ -338,12 +344,6 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         const int v0 = kb * BK;
         tc::mbar_wait(&loaded[stage], ph);
         if (pt == 0) dh_trace_kb(itx, kb, 1);
-#ifdef RNNT_EXP_SKIPTX
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&full[stage]);
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        continue;
-#endif
         uint8_t* sa = smem + stage * STAGE_BYTES;
         const float4 gq = rl < grows ? reinterpret_cast<const float4*>(sa + A_BYTES + B_BYTES)[rl]
                                      : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       const int acc = it & 1;
       const long long r = (long long)tile * BM + rl;
       const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
+      const float sc = plain && live ? p.g.gpk[r].x : 1.f;   // plain: the row scalar (tile 0's = every tile's)
       const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
       const int nbox = (nj + 63) / 64;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -428,8 +429,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           for (int i = 0; i < 4; ++i) {
             const float ha = __uint_as_float(hw[i] << 16), hb2 = __uint_as_float(hw[i] & 0xffff0000u);
             const bool ok = qq < nq && live;
-            out[8 * qq + 2 * i] = ok ? accv[8 * qq + 2 * i] * (1.f - ha * ha) : 0.f;       // d tanh
-            out[8 * qq + 2 * i + 1] = ok ? accv[8 * qq + 2 * i + 1] * (1.f - hb2 * hb2) : 0.f;
+            out[8 * qq + 2 * i] = ok ? (accv[8 * qq + 2 * i] * sc) * (1.f - ha * ha) : 0.f;       // d tanh
+            out[8 * qq + 2 * i + 1] = ok ? (accv[8 * qq + 2 * i + 1] * sc) * (1.f - hb2 * hb2) : 0.f;
           }
         }
         if (HRING > 0 && ((ch & 1) == 1 || ch == 2 * nbox - 1)) {   // both halves of this h box are used
@@ -492,6 +493,7 @@ struct JoinerDwParams {
   long long kb_per_split, nkb_total;   // (unused when `live` is set: the split is derived on device)
   const int* live;   // ascending ids of the 128-row tiles with a live row, count at nlive (null: all rows)
   const int* nlive;
+  const int* tscale; // PrunedWS::tscale (wide variant): 0 -> plain GEMM d_w = P~'^T Hs (null: always rescale)
   float* dWp;   // (splits, V, J)
   float* dbp;   // (splits, V)
   int pf = 6, pfmode = 1;   // wide variant: L2 prefetch distance (k-blocks); bit 0: P~ prefetched by j-tile 0 only, h by V pair 0 only; bit 1: grid x = j tile
@@ -731,9 +733,12 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 256 * 4;
 constexpr int THREADS = 288;
 }  // namespace jdw2
 
+// Plain mode (tscale == 0, one P~ offset per row, picks folded into P~ by pruned_combine): dz = sc_r P~'
+// with a row scalar, so B is Hs = bf16(sc_r h_r) (scale_rows_kernel) and A = P~' goes to the tensor
+// cores untouched; the transform warps of the j-tile-0 CTAs only sum sc_r P~'[r,v] for d_b.
 __global__ void __launch_bounds__(jdw2::THREADS, 1)
     joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
-                          JoinerDwParams p) {
+                          const __grid_constant__ CUtensorMap tmHs, JoinerDwParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw2;
   extern __shared__ uint8_t smem_raw[];
@@ -757,6 +762,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const int nj = min(BN, p.J - j0);
   const int nbox = (nj + 63) / 64;
   const int vtile = v0 >> 7;
+  const bool plain = p.tscale && *p.tscale == 0;
 
   if (warp == 8 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -767,7 +773,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
-    tc::tma_prefetch(&tmH);
+    tc::tma_prefetch(plain ? &tmHs : &tmH);
   }
   if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before_sync();
@@ -790,11 +796,26 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       const long long rb = dw_row0(p, kb0 + kb);
       const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
-#ifdef RNNT_EXP_SKIPTX
-      if (false) {
-#else
-      if (mine) {
-#endif
+      if (plain) {
+        if (want_db && mine) {   // d_b only: sum sc_r P~'[r, v] over the k-block's rows (no smem writes)
+          const uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
+          const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rl = g8 + 8 * i;
+            const float sc = rl < grows ? gq[rl].x : 0.f;
+            const uint4 pv = *reinterpret_cast<const uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
+            const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+            if (sc != 0.f) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                dsum[2 * k] += sc * __uint_as_float(w[k] << 16);
+                dsum[2 * k + 1] += sc * __uint_as_float(w[k] & 0xffff0000u);
+              }
+            }
+          }
+        }
+      } else if (mine) {
         uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
         const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
         uint4 pv[8];
@@ -853,16 +874,18 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    // ---- warp 8 lane 0: TMA for both P~ tiles, the h k-block and the two tiles' row scalars
+    // ---- warp 8 lane 0: TMA for both P~ tiles, the h (plain: Hs) k-block and the two tiles' row scalars
+    const CUtensorMap* tB = plain ? &tmHs : &tmH;
+    const bool gq_needed = !plain || bjy == 0;   // plain: the scalars feed only the d_b sums
     const int PF = p.pf;
     const bool pfP = !(p.pfmode & 1) || bjy == 0, pfH = !(p.pfmode & 1) || bvx == 0;
     auto prefetch = [&](int kb) {
       const int rb = (int)dw_row0(p, kb0 + kb);
       if (pfP) tc::tma_prefetch_3d(&tmP, 0, rb, v0 / 64);
       if (pfH) {
-        if (p.h3) tc::tma_prefetch_3d(&tmH, 0, rb, j0 / 64);
+        if (p.h3) tc::tma_prefetch_3d(tB, 0, rb, j0 / 64);
         else
-          for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(&tmH, j0 + bx * 64, rb);
+          for (int bx = 0; bx < nbox; ++bx) tc::tma_prefetch_2d(tB, j0 + bx * 64, rb);
       }
     };
     for (int kb = 0; kb < min(PF, nkb); ++kb) prefetch(kb);
@@ -871,7 +894,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     for (int kb = 0; kb < nkb; ++kb) {
       if (kb + PF < nkb) prefetch(kb + PF);
       const long long rb = dw_row0(p, kb0 + kb);
-      const uint32_t gbytes = (uint32_t)dw_rows(p, rb) * 16u;
+      const uint32_t gbytes = gq_needed ? (uint32_t)dw_rows(p, rb) * 16u : 0u;
       // 3-D boxes: out-of-range planes (the missing second V tile, j past J) arrive zero-filled and
       // count in full toward the transaction bytes
       const uint32_t bytes = 2 * A_BYTES + (two ? 2 : 1) * gbytes + (p.h3 ? B_BYTES : (uint32_t)nbox * 64 * BK * 2);
@@ -880,10 +903,10 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       uint64_t* ld = &loaded[stage];
       tc::mbar_arrive_expect_tx(ld, bytes);
       tc::tma_load_3d(sa, &tmP, ld, 0, (int)rb, v0 / 64);
-      if (p.h3) tc::tma_load_3d(sa + 2 * A_BYTES, &tmH, ld, 0, (int)rb, j0 / 64);
+      if (p.h3) tc::tma_load_3d(sa + 2 * A_BYTES, tB, ld, 0, (int)rb, j0 / 64);
       else
         for (int bx = 0; bx < nbox; ++bx)
-          tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), &tmH, ld, j0 + bx * 64, (int)rb);
+          tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), tB, ld, j0 + bx * 64, (int)rb);
       if (gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
       if (two && gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
@@ -951,7 +974,7 @@ static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, bool mc, co
 
 // dpre = dh (1 - h^2) rows of the live 128-row tiles (`live`, count at `nlive`, at most ntiles) into dpre.
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
-                             const int* nlive, long long ntiles, float* dpre, cudaStream_t st) {
+                             const int* nlive, long long ntiles, float* dpre, const int* tscale, cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   static const int mc_env = env_int("RNNT_DH_MC", 1);
@@ -966,7 +989,7 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   if (!make_tmap_f32_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 4, (uint64_t)d.rows() * d.J * 4, 32, jdh::BM))
     return cudaErrorInvalidValue;
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
-  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0};
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0, tscale};
   const int nsm = current_sm_count();
   unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
   if (mc) grid = (unsigned)std::min<long long>((ntiles + 1) / 2 * njp, nsm / 2) * 2;
@@ -975,15 +998,58 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   return cudaGetLastError();
 }
 
-// live / nlive: the ascending live-tile list of the step (null: every row's k-block is read)
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* live, const int* nlive,
-                             float* dWp, float* dbp, int splits, cudaStream_t st) {
+// Hs = bf16(sc_r h_r) for the rows of the live tiles (plain mode only: tscale == 0; dead rows 0), the
+// B operand of the plain d_w GEMM.  Block per live tile (grid-stride), 16 B per thread per step.
+__global__ void __launch_bounds__(256) scale_rows_kernel(const uint16_t* __restrict__ h, const float4* __restrict__ gpk,
+                                                         const int* __restrict__ tscale, const int* __restrict__ live,
+                                                         const int* __restrict__ nlive, long long R, int J,
+                                                         uint16_t* __restrict__ Hs) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
+  if (*tscale != 0) return;
+  const int nl = *nlive, J8 = J / 8;
+  for (int b = blockIdx.x; b < nl; b += gridDim.x) {
+    const long long r0 = (long long)live[b] * 128;
+    const int rows = (int)min(128LL, R - r0);
+    for (int i = threadIdx.x; i < rows * J8; i += blockDim.x) {
+      const int rl = i / J8, c = i - rl * J8;
+      const long long r = r0 + rl;
+      const float sc = gpk[r].x;   // tile 0's scalar (= every tile's in plain mode); dead rows 0
+      uint4 o = make_uint4(0, 0, 0, 0);
+      if (sc != 0.f) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(h + r * J) + c);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        uint32_t q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(sc * __uint_as_float(w[k] << 16),
+                                                          sc * __uint_as_float(w[k] & 0xffff0000u));
+          q[k] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        o = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+      reinterpret_cast<uint4*>(Hs + r * J)[c] = o;
+    }
+  }
+}
+cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
+                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<long long>(ntiles, 8LL * current_sm_count());
+  if (grid == 0) return cudaSuccess;
+  RNNT_LAUNCH(KID_SCALE_ROWS, st, launch_pdl(scale_rows_kernel, grid, 256, 0, st, h, g.gpk, tscale, live, nlive, g.R, d.J, Hs));
+  return cudaGetLastError();
+}
+
+// live / nlive: the ascending live-tile list of the step (null: every row's k-block is read);
+// Hs / tscale: the plain mode's B operand and switch (null: the rescaling path)
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs,
+                             const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+                             cudaStream_t st) {
   CUtensorMap tp, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)) return cudaErrorInvalidValue;
   const long long nkb = (d.rows() + jdw::BK - 1) / jdw::BK;
   const long long per = (nkb + splits - 1) / splits;
-  JoinerDwParams p{g, d.J, per, nkb, live, nlive, dWp, dbp};
+  JoinerDwParams p{g, d.J, per, nkb, live, nlive, dw_wide(d) ? tscale : nullptr, dWp, dbp};
   const int vt = (d.V + jdw::BM - 1) / jdw::BM;
   // CTA pairs (cta_group::2, V tiles rounded up to an even count) only when RNNT_DW_PAIR=1: parity-green
   // but measured slower (c2 87.6 vs 69.6 us, c4 4.42 vs 3.22 ms) -- the per-stage cross-CTA handshake
@@ -997,12 +1063,17 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     p.h3 = d.J % 64 == 0;
     if (p.h3 && !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4))
       return cudaErrorInvalidValue;
+    CUtensorMap ths = p.h3 ? th3 : th;   // the plain mode's B operand Hs, same geometry as h
+    if (Hs && (p.h3 ? !make_tmap_bf16_3d(&ths, Hs, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4)
+                    : !make_tmap_bf16_2d(&ths, Hs, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)))
+      return cudaErrorInvalidValue;
+    if (!Hs) p.tscale = nullptr;
     static const int pf = env_int("RNNT_DW_PF", -1), pfmode = env_int("RNNT_DW_PFMODE", -1);
     if (pf >= 0) p.pf = pf;
     if (pfmode >= 0) p.pfmode = pfmode;
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
-    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, p));
+    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, ths, p));
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};

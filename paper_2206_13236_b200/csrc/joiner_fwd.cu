@@ -4,7 +4,10 @@
 //   z[r,v] = sum_j h[r,j] W[v,j] + b[v]        (tcgen05.mma kind::f16, fp32 accumulation in TMEM)
 //   lse[r] = log sum_v exp z[r,v]               (online over V tiles, one TMEM lane = one row)
 //   py2[r] = (z[r,0] - lse) log2e, px2[r] = (z[r,y] - lse) log2e   (-inf at u = U_n)
-//   P~[r,v] = bf16(exp(z[r,v] - m[r, v/128])), m = per-128-column max  (read by K10/K11)
+//   P~[r,v] = bf16(exp(z[r,v] - m[r, v/128]))                             (read by K10/K11)
+//   (pair kernel: m = m_ref(r) for every tile -- the max of the row's first 32 columns of V tiles 0
+//    and 1 -- unless a tile holds a logit above m_ref + 60: that tile takes its exact max and raises
+//    tscale; the 1-CTA kernel: m = per-128-column offset from the running max, tscale raised)
 //
 // Persistent CTAs (two per SM) loop over the live 128-row tiles of the band rows; each sweeps all of
 // V in 128-column MMA tiles (K-loop over J in 64-wide TMA boxes, 3-stage mbarrier ring) with
@@ -57,6 +60,7 @@ struct JoinerFwdParams {
   float* px2;
   float* py2;
   int dbg;                // diagnostics (RNNT_DBG_FWD): 1 no epilogue math, 2 no MMA, 3 no TMA
+  int* tscale;            // set to 1 when some row's P~ tiles do not share one offset (PrunedWS::tscale)
 };
 
 // Persistent: CTA c processes the live 128-row tiles c, c + gridDim.x, ...; the TMA ring, the
@@ -66,6 +70,7 @@ __global__ void __launch_bounds__(jf::THREADS, 1)
     joiner_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.tscale) *p.tscale = 1;   // per-tile offsets (running max)
   using namespace jf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
@@ -337,7 +342,8 @@ constexpr int B_BYTES = BN * BK * 2;        // 16 KB: this CTA's 128 of the pair
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STG_BYTES = BM * BN * 2;      // 32 KB P~ staging per epilogue set
 constexpr int MRG_OFF = STAGES * STAGE_BYTES + 2 * STG_BYTES;
-constexpr int BAR_OFF = MRG_OFF + 2 * BM * 16;
+constexpr int XCH_OFF = MRG_OFF + 2 * BM * 16;   // [2 sets][128 rows] first-chunk maxima (m_ref)
+constexpr int BAR_OFF = XCH_OFF + 2 * BM * 4;
 constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 constexpr int THREADS = 320;
 }  // namespace jf2
@@ -358,6 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
   int* tq = reinterpret_cast<int*>(qempty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
   float4* mrg = reinterpret_cast<float4*>(smem + MRG_OFF);   // [2][128] set-1 row state for the merge
+  float* xch = reinterpret_cast<float*>(smem + XCH_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -469,6 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
       const long long r = (long long)rt * BM + 32 * q + lane;
       const int info = (r < p.R) ? p.rowinfo[r] : -1;
       float M = neg_inf_f(), sum = 0.f, zb = neg_inf_f(), zl = neg_inf_f();
+      float mref = neg_inf_f();
       for (int vp = 0; vp < nvp; ++vp, ++it) {
         const int acc = it & 1;
         const int nt = 2 * vp + set, v0 = nt * BN;
@@ -477,11 +485,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
         const uint32_t tcol = tl + acc * 2 * BN;
         const bool have = nt < nvt;             // warp-uniform
         constexpr float kRedo = 60.f;
+        if (vp == 0) {
+          // the row's P~ offset m_ref: max of the first 32 columns of V tiles 0 (set 0) and 1 (set 1)
+          float cm0 = neg_inf_f();
+          if (have) {
+            float z[32];
+            tc::tmem_ld32(tcol, z);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (v0 + j < p.V) cm0 = fmaxf(cm0, z[j] + p.bias[v0 + j]);
+          }
+          xch[set * BM + 32 * q + lane] = cm0;
+          asm volatile("bar.sync 4, 256;" ::: "memory");
+          mref = fmaxf(xch[32 * q + lane], xch[BM + 32 * q + lane]);
+        }
         float m = neg_inf_f(), s = 0.f;
         if (have) {
-          // One TMEM pass as in joiner_fwd_tc_kernel: the tile's exp offset m comes from its first
-          // 32-column chunk joined with the running max; a later chunk above m + kRedo redoes the tile
-          // with an exact max pass.
+          // One TMEM pass: every tile's exp offset is the row's m_ref (one offset per row: the
+          // backward's dz is then a per-row scalar times P~); a chunk above m_ref + kRedo redoes the
+          // tile with its exact max and raises tscale (the backward then rescales per tile).
           const float zb_prev = zb, zl_prev = zl;
           bool redo = false;
           if (threadIdx.x == ethr) tc::bulk_wait_read0();
@@ -489,6 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
           for (int attempt = 0; attempt < 2; ++attempt) {
             if (attempt == 1) {
               if (!__any_sync(0xffffffffu, redo)) break;
+              if (lane == 0 && p.tscale) *p.tscale = 1;
               m = neg_inf_f();
 #pragma unroll 1
               for (int c = 0; c < 4; ++c) {
@@ -528,11 +551,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
 #pragma unroll
                 for (int j = 1; j < 32; ++j) cm = fmaxf(cm, z[j]);
                 if (c == 0) {
-                  m = fmaxf(M, cm);
+                  m = mref;
                   mL = m * RNNT_LOG2E_F;
-                } else if (cm - m > kRedo) {
-                  redo = true;
                 }
+                if (cm - m > kRedo) redo = true;
                 if (__any_sync(0xffffffffu, redo)) break;
               }
               uint32_t pk[16];
@@ -621,7 +643,7 @@ cudaError_t joiner_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   if (!make_tmap_bf16_2d(&tp, w.Pt, VP, R, (uint64_t)VP * 2, 64, jf::BM)) return cudaErrorInvalidValue;
   const int ntiles = (int)((R + jf::BM - 1) / jf::BM);
   JoinerFwdParams p{w.bias, w.bmax, w.rowinfo, w.tlive, w.tcounter, R, ntiles, d.V, VP, d.J, (d.V + jf::BN - 1) / jf::BN,
-                    (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2, 0};
+                    (d.J + jf::BK - 1) / jf::BK, d.ntile(), w.Pt, w.mt, w.lse, w.px2, w.py2, 0, w.tscale};
 #ifdef RNNT_DIAGNOSTICS
   if (const char* e = getenv("RNNT_DBG_FWD")) p.dbg = atoi(e);  // skips parts of the step: wrong results, timing only
 #endif

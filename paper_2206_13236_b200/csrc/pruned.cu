@@ -35,10 +35,11 @@ struct GradSrc {
   int V, VP, ntile;
 };
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
-                             const int* nlive, long long ntiles, float* dpre, cudaStream_t st);
+                             const int* nlive, long long ntiles, float* dpre, const int* tscale, cudaStream_t st);
 cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* live, const int* nlive,
-                             float* dWp, float* dbp, int splits, cudaStream_t st);
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs,
+                             const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+                             cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
 // Block (J/8, FPB): thread (x, y) owns the 8 columns 8x of frame blockIdx.x * FPB + y and walks its
@@ -92,10 +93,14 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
                                const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
-                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter) {
+                               float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter,
+                               int tscale0) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x == 0) *tcounter = 0;
+    if (threadIdx.x == 0) {
+      tcounter[0] = 0;
+      tcounter[1] = tscale0;   // PrunedWS::tscale (the joiner forward raises it on a per-tile offset)
+    }
     // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
     // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
     for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
@@ -532,7 +537,8 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
                                       const int32_t* __restrict__ rowinfo, const float* __restrict__ mt,
                                       const float* __restrict__ lse, const int64_t* __restrict__ bnd,
                                       int N, int T, int S, int ntile, float gs, float* __restrict__ gb,
-                                      float* __restrict__ gl, float4* __restrict__ gpk) {
+                                      float* __restrict__ gl, float4* __restrict__ gpk,
+                                      const int* __restrict__ tscale, uint16_t* __restrict__ Pt, int V, int VP) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long R = (long long)N * T * S;
@@ -567,6 +573,19 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
     float4 qv = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
     if (info >= 0) qv = make_float4(gs * (bb + yb) * expf(mt[r * ntile + tl] - l), gs * bb, gs * yb, __int_as_float(info));
     gpk[(size_t)tl * R + r] = qv;
+  }
+  // One P~ offset per row (tscale == 0): the logit gradient is dz = sc P~' with the row scalar
+  // sc = gs (g_b + g_l) e^{m_ref - lse} once the two picks are folded into P~ itself,
+  //   P~'[r,0] = P~[r,0] - g_b / (g_b + g_l) e^{lse - m_ref},  P~'[r,y] = P~[r,y] - g_l / (...) e^{...},
+  // so the joiner backward runs as plain GEMMs on P~' (K10: dh = sc (P~' W); K11: d_w = P~'^T (sc h)).
+  if (*tscale == 0 && info >= 0) {
+    const float occ = bb + yb;
+    if (occ > 0.f) {
+      const float e = expf(l - mt[r * ntile]);
+      uint16_t* row = Pt + (size_t)r * VP;
+      if (bb > 0.f) row[0] = f_to_bf16_bits_rn(bf16_bits_to_f(row[0]) - (bb / occ) * e);
+      if (yb > 0.f && info < V) row[info] = f_to_bf16_bits_rn(bf16_bits_to_f(row[info]) - (yb / occ) * e);
+    }
   }
 }
 
@@ -662,11 +681,19 @@ static cudaError_t launch_scan(const Dims& d, const ScanParams& q, size_t sm, cu
   return cudaGetLastError();
 }
 
+// The plain joiner backward (no per-tile rescale of P~) needs the CTA-pair forward (one P~ offset per
+// row) and the wide d_w kernel; RNNT_PLAIN=0 turns it off (A/B).
+bool plain_backward_capable(const Dims& d) {
+  static const int plain = env_int("RNNT_PLAIN", 1), pair = env_int("RNNT_FWD_PAIR", 1);
+  return plain != 0 && pair != 0 && dw_wide(d);
+}
+
 cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
                            const int64_t* bnd, const uint16_t* b, cudaStream_t st) {
   const long long R = d.rows();
   RNNT_LAUNCH(KID_ROWINFO, st, launch_pdl(rowinfo_kernel, (unsigned)((R + 255) / 256 + 1), 256, 0, st, 
-      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter));
+      ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter,
+      plain_backward_capable(d) ? 0 : 1));
   return cudaGetLastError();
 }
 
@@ -703,7 +730,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   }
   RNNT_LAUNCH(KID_PCOMBINE, st, launch_pdl(pruned_combine_kernel, (unsigned)((R + 255) / 256), 256, 0, st, 
       w.px2, w.py2, w.ap, w.bp, w.Af, w.Bf, w.Lp, ranges, w.rowinfo, w.mt, w.lse, bnd, d.N, d.T, d.S, nt, gs, w.gb,
-      w.gl, w.gpk));
+      w.gl, w.gpk, w.tscale, w.Pt, d.V, d.VP()));
   return cudaGetLastError();
 }
 
@@ -834,7 +861,7 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
   const long long ntiles = (d.rows() + 127) / 128;   // (the live-tile list: built by the forward)
-  if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, st)) != cudaSuccess) return e;
+  if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, w.tscale, st)) != cudaSuccess) return e;
   {
     const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * ((d.J / 4 + 31) / 32);
     const unsigned nb = (unsigned)((nwarp + 7) / 8);
@@ -865,6 +892,8 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
 
 cudaError_t split_reduce_acc_launch(const float* part, int splits, long long M, float* out, int mode, int kid,
                                     cudaStream_t st);
+cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
+                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st);
 
 // Backward to the joiner weights: K11 dW (split-K) + db, deterministic split reduction.  mode > 0: the
 // reduced d_w / d_b are ADDED into the targets (exchange.cu: red.global.add, or multimem.red.add on an
@@ -874,7 +903,12 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   const long long ntiles = (d.rows() + 127) / 128;
-  if ((e = joiner_dw_launch(d, g, h, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) != cudaSuccess) return e;
+  const int* ts = w.Hs ? w.tscale : nullptr;   // (the full loss has no Hs: always the rescaling path)
+  if (ts && (e = scale_rows_launch(d, g, h, ts, w.dhlive, w.dhlive + ntiles, ntiles, w.Hs, st)) != cudaSuccess)
+    return e;
+  if ((e = joiner_dw_launch(d, g, h, w.Hs, ts, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) !=
+      cudaSuccess)
+    return e;
   if (mode != 0) {
     if ((e = split_reduce_acc_launch(w.dWp, w.splits, (long long)d.V * d.J, d_w, mode, KID_DW_REDUCE, st)) !=
         cudaSuccess)

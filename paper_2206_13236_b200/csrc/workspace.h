@@ -91,6 +91,9 @@ struct PrunedWS {
   float* bmax;       // (ntile) max of the bias over each 128-column tile
   uint8_t* tlive;    // (ceil(R/128)) 128-row tile holds a live band row
   int* tcounter;     // tile scheduler counter of the persistent joiner forward
+  int* tscale;       // 0: every row's P~ tiles share one offset m_ref (the joiner backward runs as plain
+                     //    GEMMs on P~ with the picks folded in, pruned_combine); else per-tile offsets
+                     //    (the backward rescales P~ per (row, tile) in shared memory)
   uint16_t* Pt;      // (R,VP) bf16 exp(z - m_tile), pitch VP
   float* mt;         // (R,ntile) tile maxima of z
   float* lse;        // (R) log-sum-exp of z
@@ -106,6 +109,7 @@ struct PrunedWS {
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
   int* dhlive;       // (R/128 + 1) ids of the live 128-row joiner_dh tiles, then their count
   float* dpre;       // (R,J) dpre = dh (1 - h^2) of every band row (live rows only are written)
+  uint16_t* Hs;      // (R,J) bf16 s_r h_r: the d_w GEMM's B operand when tscale == 0 (null: full loss)
   float* bpart;      // (N, band_part_rows, J) d_dec partials of the band reduction
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
@@ -148,7 +152,7 @@ inline int dw_splits(const Dims& d) {
 }
 
 // Returns total bytes; if base != nullptr fills the structs.
-inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
+inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool with_hs = true) {
   size_t off = 0;
   char* b = static_cast<char*>(base);
   auto take = [&](size_t bytes) -> void* {
@@ -193,6 +197,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   p.bmax = (float*)take(NT * 4);
   p.tlive = (uint8_t*)take((R + 127) / 128);
   p.tcounter = (int*)take(16);
+  p.tscale = b ? p.tcounter + 1 : nullptr;
   p.Pt = (uint16_t*)take(R * VP * 2);
   p.mt = (float*)take(R * NT * 4);
   p.lse = (float*)take(R * 4);
@@ -210,6 +215,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw) {
   // band_reduce_kernel turns into d_enc / d_dec
   p.dhlive = (int*)take(((R + 127) / 128 + 1) * 4);
   p.dpre = (float*)take(R * J * 4);
+  p.Hs = with_hs ? (uint16_t*)take(R * J * 2) : nullptr;
   p.bpart = (float*)take((size_t)N * band_part_rows(d.T, d.U, d.S) * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);
@@ -226,7 +232,7 @@ struct FullWS {
   uint16_t* h;       // (R,J) bf16 joiner input of every (t,u)
 };
 inline size_t carve_full(const Dims& df, void* base, SimpleWS* sw, PrunedWS* pw, FullWS* fw) {
-  const size_t inner = carve(df, base, sw, pw);
+  const size_t inner = carve(df, base, sw, pw, false);
   size_t off = align_up(inner);
   char* b = static_cast<char*>(base);
   auto take = [&](size_t bytes) -> void* {

@@ -763,12 +763,15 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const int nbox = (nj + 63) / 64;
   const int vtile = v0 >> 7;
   const bool plain = p.tscale && *p.tscale == 0;
+  // plain mode: the MMA consumes the TMA'd stage directly; the j-tile-0 CTAs' warps 0-7 read it for the
+  // d_b sums alongside, and the stage is refilled once the MMAs and those 8 warps are done with it
+  const bool dbread = plain && bjy == 0;
 
   if (warp == 8 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
       tc::mbar_init(&full[s], 8);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], dbread ? 9 : 1);
     }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     const int va = v0 + a * BM;
     int stage = 0;
     uint32_t ph = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < (plain && !want_db ? 0 : nkb); ++kb) {
       const long long rb = dw_row0(p, kb0 + kb);
       const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
@@ -815,6 +818,10 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[stage]);   // this warp is done reading the stage
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+        continue;
       } else if (mine) {
         uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
         const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
@@ -917,7 +924,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(&full[stage], ph);
+      tc::mbar_wait(plain ? &loaded[stage] : &full[stage], ph);
       tc::fence_after_sync();
       const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + 2 * A_BYTES;
 #pragma unroll

@@ -207,6 +207,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   // plain mode (one P~ offset per row, picks folded into P~ by pruned_combine): dh = sc_r (P~' W), the
   // MMA consumes the TMA'd stage directly and the epilogue applies the row scalar; no transform warps
   const bool plain = p.tscale && *p.tscale == 0;
+  // plain + two staging tiles: the idle transform warps (2..5) become a second epilogue set; set e takes
+  // the 32-column chunks of parity e (both sets share each h box) and stages through tile e
+  const bool dual = plain && NTW == 4 && ORING == 2;
   const int crank = MC ? (int)tc::cluster_ctarank() : 0;
   const long long cid = MC ? blockIdx.x / 2 : blockIdx.x, ncl = MC ? gridDim.x / 2 : gridDim.x;
   const long long nitems = (long long)(MC ? (nlive + 1) / 2 : nlive) * p.njp;
@@ -223,9 +226,9 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 4);      // the 4 epilogue warps
+      tc::mbar_init(&tempty[s], dual ? 8 : 4);      // the epilogue warps
       tc::mbar_init(&hfull[s], 1);
-      tc::mbar_init(&hempty[s], 4);
+      tc::mbar_init(&hempty[s], dual ? 8 : 4);
     }
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         dh_trace(it, 2);
       }
     }
-  } else if (warp < EPI0) {
+  } else if (warp < EPI0 && !dual) {
     // ---- in-place dz producers: thread = (tile row, half): transforms 4 or 8 of the 8 chunks of its row
     constexpr int CPT = 8 * 4 / NTW;                 // chunks per thread: 8 (4 warps) or 4 (8 warps)
     const int pt = threadIdx.x - 64;
@@ -377,11 +380,13 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     }
   } else {
     // ---- epilogue: quadrant q4 = warp % 4 = TMEM lanes 32 q4 ..; thread = tile row, per 32-column chunk
-    // dpre = dh (1 - h^2) -> its row of dpre (128 B per chunk)
+    // dpre = dh (1 - h^2) -> its row of dpre (128 B per chunk).  dual: set 1 = warps 2..5, chunks of
+    // odd parity, staging tile 1, named barrier 2
+    const int eset = warp >= EPI0 ? 0 : 1;
     const int q4 = warp & 3;
     const int rl = 32 * q4 + lane;
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
-    const bool leader = warp == EPI0 && lane == 0;        // issues the TMA stores
+    const bool leader = warp == (eset ? 2 : EPI0) && lane == 0;   // issues the set's TMA stores
     int it = 0, hslot = 0;
     uint32_t hph = 0;
     long long kc = 0;                                     // chunk counter: staging tile kc % ORING
@@ -396,13 +401,13 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after_sync();
       if (warp == EPI0 && lane == 0) dh_trace(it, 3);
-      for (int ch = 0; ch < 2 * nbox; ++ch) {
+      for (int ch = dual ? eset : 0; ch < 2 * nbox; ch += dual ? 2 : 1) {
         const int c0 = 32 * ch;
         const bool have = c0 < nj;
         const int nq = have ? min(4, (nj - c0) / 8) : 0;   // J % 8 == 0
         uint4 hv[4];                                       // this row's h for the chunk
         if (HRING > 0) {
-          if ((ch & 1) == 0) tc::mbar_wait(&hfull[hslot], hph);
+          if (dual || (ch & 1) == 0) tc::mbar_wait(&hfull[hslot], hph);
           const uint8_t* hb = hbuf + hslot * H_BYTES;
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq)
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         }
         float accv[32];
         if (have) tc::tmem_ld32(tl + acc * NSUB + c0, accv);
-        if (ch == 2 * nbox - 1) {                        // last TMEM read of this accumulator
+        if (ch + (dual ? 2 : 1) >= 2 * nbox) {           // last TMEM read of this accumulator
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -433,25 +438,25 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
             out[8 * qq + 2 * i + 1] = ok ? (accv[8 * qq + 2 * i + 1] * sc) * (1.f - hb2 * hb2) : 0.f;
           }
         }
-        if (HRING > 0 && ((ch & 1) == 1 || ch == 2 * nbox - 1)) {   // both halves of this h box are used
+        if (HRING > 0 && (dual || (ch & 1) == 1 || ch == 2 * nbox - 1)) {   // both halves of this h box are used
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&hempty[hslot]);
           if (++hslot == HRING) { hslot = 0; hph ^= 1; }
         }
         if (!have) continue;
         // staging tile kc % ORING: the TMA store issued from it ORING chunks ago has finished reading it
-        uint8_t* ob = smem + Cfg<NTW>::O_OFF + (int)(kc % ORING) * O_BYTES;
+        uint8_t* ob = smem + Cfg<NTW>::O_OFF + (dual ? eset : (int)(kc % ORING)) * O_BYTES;
         if (leader) {
-          if (ORING == 2) tc::bulk_wait_read1();
+          if (ORING == 2 && !dual) tc::bulk_wait_read1();
           else tc::bulk_wait_read0();
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eset) : "memory");
         float4* O4 = reinterpret_cast<float4*>(ob);
 #pragma unroll
         for (int qq = 0; qq < 8; ++qq)
           O4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
         tc::fence_proxy_async();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eset) : "memory");
         if (leader) {
           tc::tma_store_3d(&tmD, ob, j0 + c0, tile * BM, 0);
           tc::bulk_commit();

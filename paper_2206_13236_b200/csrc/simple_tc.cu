@@ -500,9 +500,16 @@ __device__ __forceinline__ void warp_store_block(const float (*buf)[33], float* 
 }
 
 // ------------------------------------------------------------------ K2: normaliser + lattice arcs
+// 128 x 128 tiles: twice the CTAs of 128 x 256 for the latency-bound epilogue (c5 44.9 -> 38.9 us; the
+// epilogue's 8 warps x 12.4 KB transpose scratch lives in the 2 x 64 KB of stages, so 1 CTA per SM)
+#ifndef RNNT_NORM_BN
+#define RNNT_NORM_BN 128
+#define RNNT_NORM_STAGES 2
+#define RNNT_NORM_MINB 1
+#endif
 struct NormProb {
   static constexpr bool kA_MN = false, kB_MN = false;
-  static constexpr int kPhases = 1, kBN = 256, kStages = 2, kMinBlocks = 1;
+  static constexpr int kPhases = 1, kBN = RNNT_NORM_BN, kStages = RNNT_NORM_STAGES, kMinBlocks = RNNT_NORM_MINB;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
   int T, U, V, LU, K, BN, nkb, UPa;
@@ -997,7 +1004,7 @@ cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, 
     RNNT_LAUNCH(KID_SMOOTH_AC, st, launch_pdl(smooth_ac_kernel, (unsigned)(((long long)d.N * d.T + 7) / 8), 256, 0, st, 
         am, w.m_am, w.Lavg, bnd, d.N, d.T, d.V, d.VP64(), w.lse_ac));
   }
-  const int BN = std::min(256, (d.U1() + 15) / 16 * 16);
+  const int BN = std::min(NormProb::kBN, (d.U1() + 15) / 16 * 16);
   Maps mp;
   if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
       !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))

@@ -135,8 +135,8 @@ def algorithmic(kernel, b):
     V, J, S = b.V, b.J, b.S
     if kernel == "joiner_fwd_gemm":             # h, W in; P~ (bf16), per-row scalars out
         return 2.0 * rows * J * V, rows * J * 2 + V * J * 2 + rows * V * 2 + rows * 16
-    if kernel == "joiner_dh_gemm":              # P~, h, W, row scalars in; dpre rows (fp32) out
-        return 2.0 * rows * J * V, rows * V * 2 + rows * J * 2 + V * J * 2 + rows * 16 + rows * J * 4
+    if kernel == "joiner_dh_gemm":              # P~, h, W, row scalars in; dpre rows (fp16) out
+        return 2.0 * rows * J * V, rows * V * 2 + rows * J * 2 + V * J * 2 + rows * 16 + rows * J * 2
     if kernel == "joiner_dw_gemm":              # P~, h, row scalars in; dW split partials out (one V x J)
         return 2.0 * rows * J * V, rows * V * 2 + rows * J * 2 + rows * 16 + V * J * 4
     if kernel == "simple_norm_gemm":            # E_am, E_lm (bf16 hi+lo) in; arcs + 1/S out (skewed)
@@ -151,8 +151,8 @@ def algorithmic(kernel, b):
         return 2.0 * cells * V * 3, cells * 8 + toks * V * 4 + frames * V * 4 + frames * V * 4
     if kernel == "simple_lm_grad_gemm":         # G~ (hi+lo), E_am (hi+lo), lm in; lm_grad out (bf16x3 issue)
         return 2.0 * cells * V * 3, cells * 4 + frames * V * 4 + toks * V * 4 + toks * V * 4
-    if kernel == "joiner_band_chunk":           # dpre rows in (each once); d_enc rows and the d_dec partials out
-        return 0.0, rows * J * 4 + frames * J * 4
+    if kernel == "joiner_band_chunk":           # dpre rows (fp16) in (each once); d_enc rows and the d_dec partials out
+        return 0.0, rows * J * 2 + frames * J * 4
     if kernel == "joiner_band_dec":             # d_dec rows out (the partials read are the chunking's cost)
         return 0.0, toks * J * 4
     if kernel == "joiner_dw_reduce":            # d_w out (the split-K partials it reads are the split's cost)

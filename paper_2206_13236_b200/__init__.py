@@ -358,6 +358,11 @@ def dims_of(am, lm, w_out, S) -> Dims:
 _SIDE = {}
 
 
+# A/B switch: RNNT_SIMPLE_BWD=late launches the am/lm gradients (side stream) after the pruned forward, so
+# they overlap the joiner backward instead of the bounds / gather / joiner forward chain.
+_SIMPLE_BWD_LATE = os.environ.get("RNNT_SIMPLE_BWD", "early") == "late"
+
+
 def _side_stream(device, which=0, lane=0):
     key = (torch.device(device).index, which, lane)
     if key not in _SIDE:
@@ -426,8 +431,7 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
             rnnt_simple_loss(am, lm, symbols, boundary, dims, simple_scale, o["loss_simple"], o["px_grad"],
                              o["py_grad"], am_grad, lm_grad, st, ws, cur)
 
-    if overlap:
-        fwd(None, None)
+    def simple_backward():
         side = _side_stream(dev, 0, lane)
         side.wait_stream(cur)
         if smooth:
@@ -437,6 +441,13 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
         else:
             rnnt_simple_loss_backward(am, lm, o["px_grad"], o["py_grad"], symbols, boundary, dims, simple_scale,
                                       o["am_grad"], o["lm_grad"], ws, side)
+        return side
+
+    late = overlap and _SIMPLE_BWD_LATE
+    if overlap:
+        fwd(None, None)
+        if not late:
+            side = simple_backward()
     else:
         fwd(o["am_grad"], o["lm_grad"])
     rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
@@ -457,6 +468,8 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     if overlap:
         rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
                                  o["loss_pruned"], st, ws, cur)
+        if late:
+            side = simple_backward()
         side2 = _side_stream(dev, 1, lane)
         side2.wait_stream(cur)
         weight_grads(side2)

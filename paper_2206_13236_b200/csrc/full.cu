@@ -33,9 +33,10 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
 cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, float* d_w, float* d_b,
                                      cudaStream_t st, int mode);
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
-                             const int* nlive, long long ntiles, float* dpre, const int* tscale, cudaStream_t st);
+                             const int* nlive, long long ntiles, float* dpre, const int* tscale, const float* gsp,
+                             cudaStream_t st);
 cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
-                           const int64_t* bnd, const uint16_t* b, cudaStream_t st);
+                           const int64_t* bnd, const uint16_t* b, float gs, cudaStream_t st);
 
 // skewed arcs pxy[n][k][u] = {y(t,u), empty(t,u)} (log2e), t = k - u; the lattice conventions of
 // lattice.cu: kNegBig off the lattice, y = kNegBig at u = U_n (already so in px2), and out of the
@@ -172,7 +173,7 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   cudaMemsetAsync(fw.ranges0, 0, (size_t)df.N * df.T * 4, st);
   cudaMemsetAsync(sw.rS, 0, (size_t)df.N * (df.K() + 1) * df.LU() * 4, st);   // only feeds the unused G~
   if ((e = prune_launch(df, enc, dec, fw.ranges0, bnd, fw.h, st)) != cudaSuccess) return e;
-  if ((e = rowinfo_launch(df, pw, fw.ranges0, sym, bnd, b, st)) != cudaSuccess) return e;
+  if ((e = rowinfo_launch(df, pw, fw.ranges0, sym, bnd, b, gs, st)) != cudaSuccess) return e;
   const long long ntiles = (R + 127) / 128;
   if ((e = live_tiles_launch(pw.tlive, ntiles, pw.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(df, pw, fw.h, W, b, st)) != cudaSuccess) return e;
@@ -189,7 +190,7 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   if ((e = pruned_bwd_weight_launch(df, pw, fw.h, d_w, d_b, st, 0)) != cudaSuccess) return e;
   if (d_enc || d_dec) {
     GradSrc g{pw.Pt, pw.gpk, pw.rowinfo, R, df.V, df.VP(), df.ntile()};
-    if ((e = joiner_dh_launch(df, g, fw.h, W, pw.dhlive, pw.dhlive + ntiles, ntiles, fw.dpre, nullptr, st)) != cudaSuccess)
+    if ((e = joiner_dh_launch(df, g, fw.h, W, pw.dhlive, pw.dhlive + ntiles, ntiles, fw.dpre, nullptr, nullptr, st)) != cudaSuccess)
       return e;
     RNNT_LAUNCH(KID_FULL_DGRAD, st, launch_pdl(full_dgrad_kernel, (unsigned)((long long)df.N * df.T + (long long)df.N * df.U1()), 128, 0, st, 
         fw.dpre, bnd, df.N, df.T, df.U, df.J, d_enc, d_dec));

@@ -152,6 +152,7 @@ struct JoinerDhParams {
   float* dpre;             // (R, J) fp32 out: dh (1 - h^2) of the rows of the live tiles
   int w3;                  // tmW is the 3-D (64 j, V, J/64) map: one TMA per k-block's 4 W boxes
   const int* tscale;       // PrunedWS::tscale: 0 -> plain mode (null: always rescale P~ per tile)
+  const float* gsp;        // non-null: dpre is stored as fp16 dpre / *gsp (the pruned path); null: fp32
 };
 
 // diagnostics: per (CTA, item) timestamps {producer start, first MMA, last MMA commit, epilogue
@@ -387,6 +388,13 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     const int rl = 32 * q4 + lane;
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
     const bool leader = warp == (eset ? 2 : EPI0) && lane == 0;   // issues the set's TMA stores
+    // fp16 rows (the pruned path): dpre / gs, so the stored range does not depend on the loss scale
+    const bool d16 = p.gsp != nullptr;
+    float dsc = 1.f;
+    if (d16) {
+      const float gsv = *p.gsp;
+      if (gsv != 0.f && isfinite(gsv)) dsc = 1.f / gsv;
+    }
     int it = 0, hslot = 0;
     uint32_t hph = 0;
     long long kc = 0;                                     // chunk counter: staging tile kc % ORING
@@ -451,10 +459,24 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
           else tc::bulk_wait_read0();
         }
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eset) : "memory");
-        float4* O4 = reinterpret_cast<float4*>(ob);
+        if (d16) {   // 128 rows x 64 B, SWIZZLE_64B: 16-B chunk qq of row rl at qq ^ ((rl >> 1) & 3)
+          uint4* O = reinterpret_cast<uint4*>(ob);
 #pragma unroll
-        for (int qq = 0; qq < 8; ++qq)
-          O4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
+          for (int qq = 0; qq < 4; ++qq) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const __half2 h2 = __floats2half2_rn(out[8 * qq + 2 * i] * dsc, out[8 * qq + 2 * i + 1] * dsc);
+              w[i] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            O[rl * 4 + (qq ^ ((rl >> 1) & 3))] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+          float4* O4 = reinterpret_cast<float4*>(ob);
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq)
+            O4[rl * 8 + (qq ^ (rl & 7))] = make_float4(out[4 * qq], out[4 * qq + 1], out[4 * qq + 2], out[4 * qq + 3]);
+        }
         tc::fence_proxy_async();
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eset) : "memory");
         if (leader) {
@@ -498,7 +520,7 @@ struct JoinerDwParams {
   long long kb_per_split, nkb_total;   // (unused when `live` is set: the split is derived on device)
   const int* live;   // ascending ids of the 128-row tiles with a live row, count at nlive (null: all rows)
   const int* nlive;
-  const int* tscale; // PrunedWS::tscale (wide variant): 0 -> plain GEMM d_w = P~'^T Hs (null: always rescale)
+  const int* tscale; // PrunedWS::tscale (wide variant): 0 -> plain GEMM d_w = P~'^T (sc h) (null: always rescale)
   float* dWp;   // (splits, V, J)
   float* dbp;   // (splits, V)
   int pf = 6, pfmode = 1;   // wide variant: L2 prefetch distance (k-blocks); bit 0: P~ prefetched by j-tile 0 only, h by V pair 0 only; bit 1: grid x = j tile
@@ -739,11 +761,12 @@ constexpr int THREADS = 288;
 }  // namespace jdw2
 
 // Plain mode (tscale == 0, one P~ offset per row, picks folded into P~ by pruned_combine): dz = sc_r P~'
-// with a row scalar, so B is Hs = bf16(sc_r h_r) (scale_rows_kernel) and A = P~' goes to the tensor
-// cores untouched; the transform warps of the j-tile-0 CTAs only sum sc_r P~'[r,v] for d_b.
+// with a row scalar, so d_w = P~'^T (sc h): A = P~' goes to the tensor cores untouched and warps 0-7
+// scale the h k-block in shared memory, Hs = bf16(sc_r h_r) (each 128-B line of a box is one row), before
+// the MMA reads it; the j-tile-0 CTAs' warps also sum sc_r P~'[r,v] for d_b.
 __global__ void __launch_bounds__(jdw2::THREADS, 1)
     joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
-                          const __grid_constant__ CUtensorMap tmHs, JoinerDwParams p) {
+                          JoinerDwParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw2;
   extern __shared__ uint8_t smem_raw[];
@@ -768,20 +791,17 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const int nbox = (nj + 63) / 64;
   const int vtile = v0 >> 7;
   const bool plain = p.tscale && *p.tscale == 0;
-  // plain mode: the MMA consumes the TMA'd stage directly; the j-tile-0 CTAs' warps 0-7 read it for the
-  // d_b sums alongside, and the stage is refilled once the MMAs and those 8 warps are done with it
-  const bool dbread = plain && bjy == 0;
 
   if (warp == 8 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
       tc::mbar_init(&full[s], 8);
-      tc::mbar_init(&empty[s], dbread ? 9 : 1);
+      tc::mbar_init(&empty[s], 1);
     }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
-    tc::tma_prefetch(plain ? &tmHs : &tmH);
+    tc::tma_prefetch(&tmH);
   }
   if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before_sync();
@@ -800,7 +820,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     const int va = v0 + a * BM;
     int stage = 0;
     uint32_t ph = 0;
-    for (int kb = 0; kb < (plain && !want_db ? 0 : nkb); ++kb) {
+    for (int kb = 0; kb < nkb; ++kb) {
       const long long rb = dw_row0(p, kb0 + kb);
       const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
@@ -823,10 +843,32 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&empty[stage]);   // this warp is done reading the stage
-        if (++stage == STAGES) { stage = 0; ph ^= 1; }
-        continue;
+        // Hs = bf16(sc_r h_r) in place: 16-B chunk i of the B region lies in 128-B line i / 8, row (i / 8) % 64
+        uint8_t* sb = smem + stage * STAGE_BYTES + 2 * A_BYTES;
+        const float4* g0 = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES);
+        constexpr int NCH = B_BYTES / 16 / 256;   // chunks per thread
+        uint4 hv[NCH];
+        float sc[NCH];
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const int ch = threadIdx.x + 256 * i;
+          const int rl = (ch >> 3) & (BK - 1);
+          sc[i] = rl < grows ? g0[rl].x : 0.f;
+          hv[i] = *reinterpret_cast<const uint4*>(sb + ch * 16);
+        }
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t w[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w};
+          uint32_t q[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(sc[i] * __uint_as_float(w[k] << 16),
+                                                            sc[i] * __uint_as_float(w[k] & 0xffff0000u));
+            q[k] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          *reinterpret_cast<uint4*>(sb + (threadIdx.x + 256 * i) * 16) = make_uint4(q[0], q[1], q[2], q[3]);
+        }
+        tc::fence_proxy_async();
       } else if (mine) {
         uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
         const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES + a * G_BYTES);
@@ -886,9 +928,9 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    // ---- warp 8 lane 0: TMA for both P~ tiles, the h (plain: Hs) k-block and the two tiles' row scalars
-    const CUtensorMap* tB = plain ? &tmHs : &tmH;
-    const bool gq_needed = !plain || bjy == 0;   // plain: the scalars feed only the d_b sums
+    // ---- warp 8 lane 0: TMA for both P~ tiles, the h k-block and the two tiles' row scalars
+    const CUtensorMap* tB = &tmH;
+    const bool gq_needed = true;   // plain: the scalars scale h (and feed the d_b sums)
     const int PF = p.pf;
     const bool pfP = !(p.pfmode & 1) || bjy == 0, pfH = !(p.pfmode & 1) || bvx == 0;
     auto prefetch = [&](int kb) {
@@ -929,7 +971,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(plain ? &loaded[stage] : &full[stage], ph);
+      tc::mbar_wait(&full[stage], ph);
       tc::fence_after_sync();
       const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + 2 * A_BYTES;
 #pragma unroll
@@ -986,7 +1028,8 @@ static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, bool mc, co
 
 // dpre = dh (1 - h^2) rows of the live 128-row tiles (`live`, count at `nlive`, at most ntiles) into dpre.
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
-                             const int* nlive, long long ntiles, float* dpre, const int* tscale, cudaStream_t st) {
+                             const int* nlive, long long ntiles, float* dpre, const int* tscale, const float* gsp,
+                             cudaStream_t st) {
   CUtensorMap tp, tw, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, jdh::BK, jdh::BM)) return cudaErrorInvalidValue;
   static const int mc_env = env_int("RNNT_DH_MC", 1);
@@ -998,10 +1041,11 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&th, h, d.J, d.rows(), (uint64_t)d.J * 2, 64, jdh::BM)) return cudaErrorInvalidValue;
   CUtensorMap td;   // dpre (R, J) fp32, box 32 columns x 128 rows
-  if (!make_tmap_f32_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 4, (uint64_t)d.rows() * d.J * 4, 32, jdh::BM))
+  if (gsp ? !make_tmap_f16_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 2, (uint64_t)d.rows() * d.J * 2, 32, jdh::BM)
+          : !make_tmap_f32_3d(&td, dpre, d.J, d.rows(), 1, (uint64_t)d.J * 4, (uint64_t)d.rows() * d.J * 4, 32, jdh::BM))
     return cudaErrorInvalidValue;
   const int njp = (d.J + jdh::NSUB - 1) / jdh::NSUB;
-  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0, tscale};
+  JoinerDhParams p{g, h, d.J, (d.V + jdh::BK - 1) / jdh::BK, njp, live, nlive, dpre, w3 ? 1 : 0, tscale, gsp};
   const int nsm = current_sm_count();
   unsigned grid = (unsigned)std::min<long long>(ntiles * njp, nsm);
   if (mc) grid = (unsigned)std::min<long long>((ntiles + 1) / 2 * njp, nsm / 2) * 2;
@@ -1010,51 +1054,9 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
   return cudaGetLastError();
 }
 
-// Hs = bf16(sc_r h_r) for the rows of the live tiles (plain mode only: tscale == 0; dead rows 0), the
-// B operand of the plain d_w GEMM.  Block per live tile (grid-stride), 16 B per thread per step.
-__global__ void __launch_bounds__(256) scale_rows_kernel(const uint16_t* __restrict__ h, const float4* __restrict__ gpk,
-                                                         const int* __restrict__ tscale, const int* __restrict__ live,
-                                                         const int* __restrict__ nlive, long long R, int J,
-                                                         uint16_t* __restrict__ Hs) {
-  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  if (*tscale != 0) return;
-  const int nl = *nlive, J8 = J / 8;
-  for (int b = blockIdx.x; b < nl; b += gridDim.x) {
-    const long long r0 = (long long)live[b] * 128;
-    const int rows = (int)min(128LL, R - r0);
-    for (int i = threadIdx.x; i < rows * J8; i += blockDim.x) {
-      const int rl = i / J8, c = i - rl * J8;
-      const long long r = r0 + rl;
-      const float sc = gpk[r].x;   // tile 0's scalar (= every tile's in plain mode); dead rows 0
-      uint4 o = make_uint4(0, 0, 0, 0);
-      if (sc != 0.f) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(h + r * J) + c);
-        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-        uint32_t q[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(sc * __uint_as_float(w[k] << 16),
-                                                          sc * __uint_as_float(w[k] & 0xffff0000u));
-          q[k] = *reinterpret_cast<const uint32_t*>(&h2);
-        }
-        o = make_uint4(q[0], q[1], q[2], q[3]);
-      }
-      reinterpret_cast<uint4*>(Hs + r * J)[c] = o;
-    }
-  }
-}
-cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
-                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st) {
-  const unsigned grid = (unsigned)std::min<long long>(ntiles, 8LL * current_sm_count());
-  if (grid == 0) return cudaSuccess;
-  RNNT_LAUNCH(KID_SCALE_ROWS, st, launch_pdl(scale_rows_kernel, grid, 256, 0, st, h, g.gpk, tscale, live, nlive, g.R, d.J, Hs));
-  return cudaGetLastError();
-}
-
 // live / nlive: the ascending live-tile list of the step (null: every row's k-block is read);
-// Hs / tscale: the plain mode's B operand and switch (null: the rescaling path)
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs,
-                             const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+// tscale: the plain mode's switch (null: the rescaling path)
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
                              cudaStream_t st) {
   CUtensorMap tp, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
@@ -1075,17 +1077,12 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     p.h3 = d.J % 64 == 0;
     if (p.h3 && !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4))
       return cudaErrorInvalidValue;
-    CUtensorMap ths = p.h3 ? th3 : th;   // the plain mode's B operand Hs, same geometry as h
-    if (Hs && (p.h3 ? !make_tmap_bf16_3d(&ths, Hs, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4)
-                    : !make_tmap_bf16_2d(&ths, Hs, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)))
-      return cudaErrorInvalidValue;
-    if (!Hs) p.tscale = nullptr;
     static const int pf = env_int("RNNT_DW_PF", -1), pfmode = env_int("RNNT_DW_PFMODE", -1);
     if (pf >= 0) p.pf = pf;
     if (pfmode >= 0) p.pfmode = pfmode;
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
-    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, ths, p));
+    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, p));
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};

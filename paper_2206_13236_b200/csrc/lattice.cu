@@ -372,7 +372,10 @@ __global__ void __launch_bounds__(256) combine_kernel(
     const float2* XY = pxy + base + (size_t)k * LU;
     const float* Rr = rS + base + (size_t)k * LU;
     float z = 0.f;
-    for (int u0 = ub; u0 < ue; u0 += 32 * CG) {
+    // only the 32-column groups holding a cell of the diagonal (about a third of the staged width at c5):
+    // the staged values of every other column are never read (phase B masks by validity)
+    const int ua = max(ub, ulo & ~31), uz = min(ue, uhi + 1);
+    for (int u0 = ua; u0 < uz; u0 += 32 * CG) {
       float a[CG], b0[CG], b1[CG], r[CG];
       float2 xy[CG];
 #pragma unroll
@@ -421,8 +424,9 @@ __global__ void __launch_bounds__(256) combine_kernel(
     for (int t = tlo + warp; t <= thi; t += 8) {
       const int kr = lane, u = k0 + kr - t;
       if (u < c0 || u >= c1) continue;
-      const float rz = s_rz[kr];
-      const float yv = Ys[kr * CW + (u - c0)] * rz, bv = Bs[kr * CW + (u - c0)] * rz;
+      const bool valid = finite && t < Tn && u <= Un;   // (staged values exist for the lattice cells only)
+      const float rz = valid ? s_rz[kr] : 0.f;
+      const float yv = valid ? Ys[kr * CW + (u - c0)] * rz : 0.f, bv = valid ? Bs[kr * CW + (u - c0)] * rz : 0.f;
       if (u < U1) {
         const size_t o = ((size_t)n * T + t) * U1 + u;
         px_grad[o] = yv;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
       }
       // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
       const size_t og = ((size_t)n * T + t) * UP + u;
-      const float g = Gs[kr * CW + (u - c0)] * rz;
+      const float g = valid ? Gs[kr * CW + (u - c0)] * rz : 0.f;
       const __nv_bfloat16 gh = __float2bfloat16_rn(g);
       const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
       Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);

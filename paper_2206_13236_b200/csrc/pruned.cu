@@ -35,10 +35,10 @@ struct GradSrc {
   int V, VP, ntile;
 };
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
-                             const int* nlive, long long ntiles, float* dpre, const int* tscale, cudaStream_t st);
+                             const int* nlive, long long ntiles, float* dpre, const int* tscale, const float* gsp,
+                             cudaStream_t st);
 cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs,
-                             const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
                              cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
@@ -94,12 +94,13 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
                                const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
                                float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter,
-                               int tscale0) {
+                               int tscale0, float gs) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   if (blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x == 0) {
       tcounter[0] = 0;
       tcounter[1] = tscale0;   // PrunedWS::tscale (the joiner forward raises it on a per-tile offset)
+      tcounter[2] = __float_as_int(gs);   // PrunedWS::gsp (the joiner backward's fp16 dpre scale)
     }
     // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
     // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
@@ -689,11 +690,11 @@ bool plain_backward_capable(const Dims& d) {
 }
 
 cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
-                           const int64_t* bnd, const uint16_t* b, cudaStream_t st) {
+                           const int64_t* bnd, const uint16_t* b, float gs, cudaStream_t st) {
   const long long R = d.rows();
   RNNT_LAUNCH(KID_ROWINFO, st, launch_pdl(rowinfo_kernel, (unsigned)((R + 255) / 256 + 1), 256, 0, st, 
       ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter,
-      plain_backward_capable(d) ? 0 : 1));
+      plain_backward_capable(d) ? 0 : 1, gs));
   return cudaGetLastError();
 }
 
@@ -705,7 +706,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
-  if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, st)) != cudaSuccess) return e;
+  if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, gs, st)) != cudaSuccess) return e;
   // the ascending list of live 128-row tiles, read by both backward calls (K10, K11)
   if ((e = live_tiles_launch(w.tlive, (d.rows() + 127) / 128, w.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
@@ -746,27 +747,40 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
 //     partial buffer (U + 1 + S ceil(T / CH) rows: chunk c's rows lie below chunk c+1's since p is
 //     monotone);
 //   B (a warp per (u, 128 columns)): d_dec[u] = the partials of the chunks covering u, in chunk order.
-// Every output row is a fixed-order sum (deterministic); a warp per (output row, 512-B column segment)
-// with eight row loads in flight.  Padded rows and infeasible utterances get 0.
-// A: a warp per (chunk of kBandCH frames, utterance, 32-float4 column segment), lane = float4 column:
-// it walks the chunk's frames in order, loading the frame's S rows once (the next frame's rows are in
+// Every output row is a fixed-order sum (deterministic).  The dpre rows are fp16 dpre / gs
+// (joiner_dh_tc_kernel): the sums are taken in fp32 and scaled by gs when the outputs are written.
+// Padded rows and infeasible utterances get 0.  (A single pass whose last-arriving chunk finishes each
+// shared u measured slower: 68-77 vs 37 + 18 us at c5, the arrival fences and atomics sit on every
+// warp's critical path.)
+__device__ __forceinline__ float4 h4_to_f4(uint2 v) {
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 f4_scale(float4 a, float g) { return make_float4(a.x * g, a.y * g, a.z * g, a.w * g); }
+__device__ __forceinline__ float gs_mult(const float* gsp) {   // the scale the fp16 rows were divided by
+  const float g = *gsp;
+  return (g != 0.f && isfinite(g)) ? g : 1.f;
+}
+// A: a warp per (chunk of kBandCH frames, utterance, 32-float4 column segment), lane = 4 columns: it
+// walks the chunk's frames in order, loading the frame's S rows once (the next frames' rows are in
 // flight meanwhile), adds them into d_enc[t] and into a window win[k] = partial of u = base + k (base
 // = p_t; p is monotone, so a window entry is complete once p passes it: it is stored then and the
 // window shifts).  SW >= S (compile time) bounds the window.
 template <int SW>
-__global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict__ dpre,
+__global__ void __launch_bounds__(256) band_chunk_kernel(const uint16_t* __restrict__ dpre,
                                                          const int32_t* __restrict__ ranges,
                                                          const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                         int J, float* __restrict__ d_enc, float* __restrict__ part) {
+                                                         int J, float* __restrict__ d_enc, float* __restrict__ part,
+                                                         const float* __restrict__ gsp) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  const int J4 = J / 4, nseg = (J4 + 31) / 32;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int J4 = J / 4, nseg = band_nseg(J);
   const int nch = (T + kBandCH - 1) / kBandCH;
-  if (w >= (long long)N * nch * nseg) return;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // < 2^31 (checked by the launcher)
+  if (w >= N * nch * nseg) return;
   const int lane = threadIdx.x & 31;
-  const int seg = (int)(w % nseg);
-  const long long nc = w / nseg;
-  const int n = (int)(nc / nch), c = (int)(nc - (long long)n * nch);
+  const int nc = w / nseg, seg = w - nc * nseg;
+  const int n = nc / nch, c = nc - n * nch;
   const int q = seg * 32 + lane;
   const bool qok = q < J4;
   const int t0 = c * kBandCH, t1 = min(T, t0 + kBandCH);
@@ -774,13 +788,14 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict
   const bool feas = (long long)Un <= (long long)Tn * (S - 1);
   const int te = feas ? min(t1, Tn) : t0;                  // live frames [t0, te)
   const int32_t* pr = ranges + (size_t)n * T;
-  const float4* D = reinterpret_cast<const float4*>(dpre) + (size_t)n * T * S * J4;
+  const uint2* D = reinterpret_cast<const uint2*>(dpre) + (size_t)n * T * S * J4;
   float4* E = reinterpret_cast<float4*>(d_enc) + (size_t)n * T * J4;
   float4* P = reinterpret_cast<float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + (size_t)c * S) * J4;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   if (d_enc && qok)
     for (int t = max(t0, te); t < t1; ++t) E[(size_t)t * J4 + q] = z;          // padded / infeasible frames
   if (te <= t0) return;
+  const float gm = gs_mult(gsp);
   float4 win[SW];
 #pragma unroll
   for (int k = 0; k < SW; ++k) win[k] = z;
@@ -792,10 +807,10 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict
     win[SW - 1] = z;
     ++base;
   };
-  // FB frames per batch: all their rows' loads in flight together (register budget ~ 4 FB SW)
+  // FB frames per batch: all their rows' loads in flight together
   constexpr int FB = SW <= 5 ? 4 : (SW <= 10 ? 2 : 1);
   for (int tb = t0; tb < te; tb += FB) {
-    float4 x[FB][SW];
+    uint2 x[FB][SW];                                       // raw fp16 x 4 (converted at use)
     int pf[FB];
 #pragma unroll
     for (int f = 0; f < FB; ++f) {
@@ -803,7 +818,7 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict
       pf[f] = t < te ? pr[t] : 0;
       const int ns = t < te ? min(S, Un - pf[f] + 1) : 0;
 #pragma unroll
-      for (int s = 0; s < SW; ++s) x[f][s] = (s < ns && qok) ? D[((size_t)t * S + s) * J4 + q] : z;
+      for (int s = 0; s < SW; ++s) x[f][s] = (s < ns && qok) ? D[((size_t)t * S + s) * J4 + q] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int f = 0; f < FB; ++f) {
@@ -813,45 +828,61 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const float* __restrict
       float4 e = z;
 #pragma unroll
       for (int s = 0; s < SW; ++s) {
-        e.x += x[f][s].x; e.y += x[f][s].y; e.z += x[f][s].z; e.w += x[f][s].w;
-        win[s].x += x[f][s].x; win[s].y += x[f][s].y; win[s].z += x[f][s].z; win[s].w += x[f][s].w;
+        const float4 xv = h4_to_f4(x[f][s]);
+        e.x += xv.x; e.y += xv.y; e.z += xv.z; e.w += xv.w;
+        win[s].x += xv.x; win[s].y += xv.y; win[s].z += xv.z; win[s].w += xv.w;
       }
-      if (d_enc && qok) E[(size_t)t * J4 + q] = e;
+      if (d_enc && qok) E[(size_t)t * J4 + q] = f4_scale(e, gm);
     }
   }
   const int ue = min(Un, pr[te - 1] + S - 1);
   while (base <= ue) flush();
 }
-// B: a warp per (utterance, u, 32-float4 column segment): the partials of the chunks covering u, in
-// chunk order, eight loads in flight.
+// B: a warp per (utterance, u): for each chunk covering u (in chunk order) the partial's whole row, lane =
+// 4 columns of each 512-B segment, all segments' loads in flight together (a warp per segment measured
+// 18.5 us at c5: four times the warps, each waiting on the same three dependent round trips).
+constexpr int kBandDecSeg = 8;   // segments per pass held in registers (J <= 1024: one pass)
 __global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__ part, const int2* __restrict__ urange,
                                                        const int64_t* __restrict__ bnd, int N, int T, int U, int S,
-                                                       int J, float* __restrict__ d_dec) {
+                                                       int J, float* __restrict__ d_dec, const float* __restrict__ gsp) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  const int J4 = J / 4, nseg = (J4 + 31) / 32;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int J4 = J / 4;
+  const int nu = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // < 2^31 (checked by the launcher)
   const int lane = threadIdx.x & 31;
-  if (w >= (long long)N * (U + 1) * nseg) return;
-  const long long nu = w / nseg;
-  const int q = (int)(w - nu * nseg) * 32 + lane;
-  const int n = (int)(nu / (U + 1)), u = (int)(nu - (long long)n * (U + 1));
+  if (nu >= N * (U + 1)) return;
+  const int n = nu / (U + 1), u = nu - n * (U + 1);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  const bool feas = (long long)Un <= (long long)Tn * (S - 1);
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (feas && u <= Un) {
+  const bool live = (long long)Un <= (long long)Tn * (S - 1) && u <= Un;
+  int c0 = 0, c1 = -1;
+  if (live) {
     const int2 cv = urange[nu];                            // frames [lo, hi) cover u
-    const int c0 = cv.x / kBandCH, c1 = (cv.y - 1) / kBandCH;
-    const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4;
-    for (int cb = c0; cb <= c1; cb += 8) {
-      float4 x[8];
+    c0 = cv.x / kBandCH;
+    c1 = (cv.y - 1) / kBandCH;
+  }
+  const float gm = gs_mult(gsp);
+  const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4;
+  float4* o = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
+  for (int q0 = 0; q0 < J4; q0 += 32 * kBandDecSeg) {
+    float4 a[kBandDecSeg];
 #pragma unroll
-      for (int m = 0; m < 8; ++m)
-        x[m] = (cb + m <= c1 && q < J4) ? P[(size_t)(cb + m) * S * J4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < kBandDecSeg; ++g) a[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int cb = c0; cb <= c1; ++cb) {
+      const float4* Pc = P + (size_t)cb * S * J4;
+      float4 x[kBandDecSeg];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) { a.x += x[m].x; a.y += x[m].y; a.z += x[m].z; a.w += x[m].w; }
+      for (int g = 0; g < kBandDecSeg; ++g) {
+        const int q = q0 + g * 32 + lane;
+        x[g] = q < J4 ? Pc[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int g = 0; g < kBandDecSeg; ++g) { a[g].x += x[g].x; a[g].y += x[g].y; a[g].z += x[g].z; a[g].w += x[g].w; }
+    }
+#pragma unroll
+    for (int g = 0; g < kBandDecSeg; ++g) {
+      const int q = q0 + g * 32 + lane;
+      if (q < J4) o[q] = live ? f4_scale(a[g], gm) : a[g];
     }
   }
-  if (q < J4) reinterpret_cast<float4*>(d_dec + (size_t)nu * J)[q] = a;
 }
 
 cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
@@ -861,12 +892,16 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   if (!d_enc && !d_dec) return cudaSuccess;
   const long long ntiles = (d.rows() + 127) / 128;   // (the live-tile list: built by the forward)
-  if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, w.tscale, st)) != cudaSuccess) return e;
+  if ((e = joiner_dh_launch(d, g, h, W, w.dhlive, w.dhlive + ntiles, ntiles, w.dpre, w.tscale, w.gsp, st)) !=
+      cudaSuccess)
+    return e;
   {
-    const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * ((d.J / 4 + 31) / 32);
+    const long long nwarp = (long long)d.N * ((d.T + kBandCH - 1) / kBandCH) * band_nseg(d.J);
+    if (nwarp >= (1LL << 31) || (long long)d.N * d.U1() * band_nseg(d.J) >= (1LL << 31)) return cudaErrorInvalidValue;
     const unsigned nb = (unsigned)((nwarp + 7) / 8);
     float* pp = d_dec ? w.bpart : nullptr;
-#define RNNT_BAND(SWV) launch_pdl(band_chunk_kernel<SWV>, nb, 256, 0, st, w.dpre, ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp)
+#define RNNT_BAND(SWV) launch_pdl(band_chunk_kernel<SWV>, nb, 256, 0, st, reinterpret_cast<const uint16_t*>(w.dpre), \
+                                  ranges, bnd, d.N, d.T, d.U, d.S, d.J, d_enc, pp, w.gsp)
     switch (d.S) {   // the window is exactly S wide for the common band widths
       case 1: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(1)); break;
       case 2: RNNT_LAUNCH(KID_DENC, st, RNNT_BAND(2)); break;
@@ -883,17 +918,15 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
 #undef RNNT_BAND
   }
   if (d_dec) {
-    const long long nw = (long long)d.N * d.U1() * ((d.J / 4 + 31) / 32);
-    RNNT_LAUNCH(KID_DDEC, st, launch_pdl(band_dec_kernel, (unsigned)((nw + 7) / 8), 256, 0, st, 
-                                  w.bpart, w.urange, bnd, d.N, d.T, d.U, d.S, d.J, d_dec));
+    const long long nw = (long long)d.N * d.U1();
+    RNNT_LAUNCH(KID_DDEC, st, launch_pdl(band_dec_kernel, (unsigned)((nw + 7) / 8), 256, 0, st,
+                                         w.bpart, w.urange, bnd, d.N, d.T, d.U, d.S, d.J, d_dec, w.gsp));
   }
   return cudaGetLastError();
 }
 
 cudaError_t split_reduce_acc_launch(const float* part, int splits, long long M, float* out, int mode, int kid,
                                     cudaStream_t st);
-cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
-                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st);
 
 // Backward to the joiner weights: K11 dW (split-K) + db, deterministic split reduction.  mode > 0: the
 // reduced d_w / d_b are ADDED into the targets (exchange.cu: red.global.add, or multimem.red.add on an
@@ -903,10 +936,8 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
   cudaError_t e;
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   const long long ntiles = (d.rows() + 127) / 128;
-  const int* ts = w.Hs ? w.tscale : nullptr;   // (the full loss has no Hs: always the rescaling path)
-  if (ts && (e = scale_rows_launch(d, g, h, ts, w.dhlive, w.dhlive + ntiles, ntiles, w.Hs, st)) != cudaSuccess)
-    return e;
-  if ((e = joiner_dw_launch(d, g, h, w.Hs, ts, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) !=
+  const int* ts = w.plain ? w.tscale : nullptr;   // (the full loss: always the rescaling path)
+  if ((e = joiner_dw_launch(d, g, h, ts, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) !=
       cudaSuccess)
     return e;
   if (mode != 0) {

@@ -46,6 +46,8 @@ constexpr int kBandCH = 16;
 __host__ __device__ inline long long band_part_rows(int T, int U, int S) {
   return (long long)U + 1 + (long long)S * ((T + kBandCH - 1) / kBandCH);
 }
+// 512-B column segments (32 float4) of a J-wide row: the band reduction's unit of work per warp
+__host__ __device__ inline int band_nseg(int J) { return (J / 4 + 31) / 32; }
 
 // Interpolation weights of the smoothed trivial joiner (Eq. 11): a_lm = lm_only_scale, a_ac =
 // am_only_scale; both 0 is the plain trivial joiner.
@@ -91,6 +93,7 @@ struct PrunedWS {
   float* bmax;       // (ntile) max of the bias over each 128-column tile
   uint8_t* tlive;    // (ceil(R/128)) 128-row tile holds a live band row
   int* tcounter;     // tile scheduler counter of the persistent joiner forward
+  float* gsp;        // (tcounter + 2) the forward's grad_scale: the fp16 dpre rows hold dpre / gs
   int* tscale;       // 0: every row's P~ tiles share one offset m_ref (the joiner backward runs as plain
                      //    GEMMs on P~ with the picks folded in, pruned_combine); else per-tile offsets
                      //    (the backward rescales P~ per (row, tile) in shared memory)
@@ -108,8 +111,9 @@ struct PrunedWS {
   float* gl;         // (R) y'_p
   float4* gpk;       // (ntile,R) per (V tile, row): {gs (gb+gl) exp(m_tile - lse), gs gb, gs gl, label bits}
   int* dhlive;       // (R/128 + 1) ids of the live 128-row joiner_dh tiles, then their count
-  float* dpre;       // (R,J) dpre = dh (1 - h^2) of every band row (live rows only are written)
-  uint16_t* Hs;      // (R,J) bf16 s_r h_r: the d_w GEMM's B operand when tscale == 0 (null: full loss)
+  float* dpre;       // (R,J) dpre = dh (1 - h^2) of every band row (live rows only are written): the pruned
+                     //    path stores it as fp16 dpre / gs (the first half of the buffer), the full loss fp32
+  bool plain;        // the plain joiner backward may run (tscale == 0 honoured; false: the full loss)
   float* bpart;      // (N, band_part_rows, J) d_dec partials of the band reduction
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
@@ -152,7 +156,7 @@ inline int dw_splits(const Dims& d) {
 }
 
 // Returns total bytes; if base != nullptr fills the structs.
-inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool with_hs = true) {
+inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool with_plain = true) {
   size_t off = 0;
   char* b = static_cast<char*>(base);
   auto take = [&](size_t bytes) -> void* {
@@ -198,6 +202,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool 
   p.tlive = (uint8_t*)take((R + 127) / 128);
   p.tcounter = (int*)take(16);
   p.tscale = b ? p.tcounter + 1 : nullptr;
+  p.gsp = b ? reinterpret_cast<float*>(p.tcounter + 2) : nullptr;
   p.Pt = (uint16_t*)take(R * VP * 2);
   p.mt = (float*)take(R * NT * 4);
   p.lse = (float*)take(R * 4);
@@ -215,7 +220,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool 
   // band_reduce_kernel turns into d_enc / d_dec
   p.dhlive = (int*)take(((R + 127) / 128 + 1) * 4);
   p.dpre = (float*)take(R * J * 4);
-  p.Hs = with_hs ? (uint16_t*)take(R * J * 2) : nullptr;
+  p.plain = with_plain;
   p.bpart = (float*)take((size_t)N * band_part_rows(d.T, d.U, d.S) * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);

@@ -121,6 +121,7 @@ def test_stagewise_parity(cfg):
     dict(T=[60, 33], U=[150, 20], V=65, J=16, S=20),      # runtime-S scan (SMAX 32), cluster of 4
     dict(T=[1200, 700], U=[1000, 600], V=24, J=16, S=3),  # U + 1 > 512: the combine's two column windows
     dict(T=[2000, 900], U=[300, 100], V=16, J=8, S=16),   # T S 8 B > smem: the pruned scan reads its arcs from L2
+    dict(T=[50, 23], U=[20, 9], V=40, J=1160, S=5),       # J > 1024: partial 256-column part, d_dec in two passes
 ])
 def test_edge_cases(case):
     b = synth.make_custom(case["T"], case["U"], case["V"], case["J"], case["S"], seed=11, logit_scale=2.0)
@@ -128,6 +129,20 @@ def test_edge_cases(case):
     ranges = check_ranges(b, o)
     h_ref = check_prune(b, ranges)
     check_pruned(b, ranges, h_ref)
+
+
+@pytest.mark.parametrize("gs", [1e-6, 3e4])
+def test_pruned_grad_scale(gs):
+    """joiner_dh stores dpre as fp16 dpre / gs (D21): the input gradients scale linearly with the
+    loss scale, with no fp16 underflow at a tiny gs or overflow at a large one."""
+    b = synth.make_batch(1)
+    o = _oracle_simple(b)
+    ranges = _oracle_ranges(b, o["px_grad"].astype(np.float32), o["py_grad"].astype(np.float32))
+    h_ref = oracle_h_bits(b, ranges)
+    g = run_pruned(b, h_ref, ranges, gs=gs)
+    r = _oracle_pruned(b, ranges)
+    for k in ("d_w", "d_b", "d_enc", "d_dec"):
+        assert_bf16_grad(g[k] / gs, r[k], k)
 
 
 def test_pruned_stage_very_long_utterance():

@@ -56,7 +56,7 @@ static const char* const kNames[KID_COUNT] = {
     "pruned_fb", "pruned_unused", "pruned_combine", "joiner_dh_gemm", "joiner_band_chunk", "joiner_band_dec",
     "joiner_dw_gemm", "joiner_db", "joiner_dw_reduce", "joiner_db_reduce", "bias_pad", "occ_sums",
     "smooth_lm_avg", "smooth_ac_lse", "smooth_avg_grad", "smooth_q", "full_scatter", "full_pack", "full_live",
-    "full_dgrad", "loss_sums", "exchange_sum"};
+    "full_dgrad", "loss_sums", "exchange_sum", "joiner_scale_rows"};
 
 bool pdl_enabled() {
   static const bool on = env_int("RNNT_PDL", 1) != 0;

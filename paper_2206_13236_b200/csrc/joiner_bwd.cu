@@ -520,11 +520,13 @@ struct JoinerDwParams {
   long long kb_per_split, nkb_total;   // (unused when `live` is set: the split is derived on device)
   const int* live;   // ascending ids of the 128-row tiles with a live row, count at nlive (null: all rows)
   const int* nlive;
-  const int* tscale; // PrunedWS::tscale (wide variant): 0 -> plain GEMM d_w = P~'^T (sc h) (null: always rescale)
+  const int* tscale; // PrunedWS::tscale (wide variant): 0 -> plain GEMM d_w = P~'^T Hs (null: always rescale)
   float* dWp;   // (splits, V, J)
   float* dbp;   // (splits, V)
   int pf = 6, pfmode = 1;   // wide variant: L2 prefetch distance (k-blocks); bit 0: P~ prefetched by j-tile 0 only, h by V pair 0 only; bit 1: grid x = j tile
   int h3 = 0;               // wide variant: tmH is the 3-D (64 j, rows, J/64) map (J % 64 == 0)
+  int hsmem = 0;            // plain mode: Hs = bf16(sc h) formed in shared memory (else the precomputed Hs map)
+  int mc = 0;               // wide variant: P~ multicast over clusters of this many J-part siblings (0/1: off)
 };
 
 
@@ -760,12 +762,19 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 256 * 4;
 constexpr int THREADS = 288;
 }  // namespace jdw2
 
-// Plain mode (tscale == 0, one P~ offset per row, picks folded into P~ by pruned_combine): dz = sc_r P~'
-// with a row scalar, so d_w = P~'^T (sc h): A = P~' goes to the tensor cores untouched and warps 0-7
-// scale the h k-block in shared memory, Hs = bf16(sc_r h_r) (each 128-B line of a box is one row), before
-// the MMA reads it; the j-tile-0 CTAs' warps also sum sc_r P~'[r,v] for d_b.
+// Plain mode (tscale == 0, one P~ offset per row, picks folded into P~ by pruned_combine, D20): dz =
+// sc_r P~' with a row scalar, so d_w = P~'^T Hs with Hs = bf16(sc_r h_r) and A = P~' goes to the tensor
+// cores untouched.  Hs comes either
+//   precomputed (tmHs, scale_rows_kernel; large V): the MMA consumes the TMA'd stage directly and the
+//     j-tile-0 CTAs' warps 0-7 read it alongside for the d_b sums (the stage is refilled once the MMAs and
+//     those 8 warps are done with it), or
+//   scaled in shared memory (small V, p.hsmem): warps 0-7 scale the h k-block in place (each 128-B line
+//     of a box is one row) before the MMA reads it -- no Hs round trip through HBM, but 64 KB of extra smem
+//     traffic per k-block, which costs more than the round trip once the mainloop is long (c3: 290 vs 238 +
+//     15 us, c4: 2545 vs 1940 + 75 us; c5: 58 vs 53 + 37 us).
 __global__ void __launch_bounds__(jdw2::THREADS, 1)
     joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
+                          const __grid_constant__ CUtensorMap tmHs, const __grid_constant__ CUtensorMap tmP1,
                           JoinerDwParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw2;
@@ -791,21 +800,33 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const int nbox = (nj + 63) / 64;
   const int vtile = v0 >> 7;
   const bool plain = p.tscale && *p.tscale == 0;
+  const bool hsm = plain && p.hsmem;      // Hs formed in shared memory
+  const bool dbread = plain && !hsm && bjy == 0;   // precomputed Hs: the d_b readers release the stage too
+  // P~ multicast (p.mc = the cluster size along x = the J parts of one (V pair, split)): each sibling
+  // loads planes rank, rank + mc, .. of the 4-plane P~ k-block into every sibling's stage, so the P~
+  // bytes cross L2 -> SM once per cluster instead of once per J part; a stage is refilled once every
+  // sibling's MMA released it (commits multicast to all siblings' empty barriers).  With d_b readers
+  // (dbread) the rank-0 CTA gates its MMA on them (full) instead of adding them to the release count.
+  const int mc = p.mc > 1 ? p.mc : 0;
+  const uint32_t crank = mc ? tc::cluster_ctarank() : 0u;
+  const uint16_t mcmask = (uint16_t)((1u << mc) - 1u);
+  const bool dbfull = dbread && mc;
 
   if (warp == 8 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&loaded[s], 1);
       tc::mbar_init(&full[s], 8);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&empty[s], mc ? mc : (dbread ? 9 : 1));
     }
     tc::mbar_init(tfull, 1);
     tc::fence_barrier_init();
     tc::tma_prefetch(&tmP);
-    tc::tma_prefetch(&tmH);
+    tc::tma_prefetch(plain && !hsm ? &tmHs : &tmH);
   }
   if (warp == 8) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before_sync();
   __syncthreads();
+  if (mc) tc::cluster_sync();             // every sibling's barriers are initialised before any multicast
   tc::fence_after_sync();
   const uint32_t tbase = *tmem_slot;
 
@@ -820,7 +841,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     const int va = v0 + a * BM;
     int stage = 0;
     uint32_t ph = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < (plain && !hsm && !want_db ? 0 : nkb); ++kb) {
       const long long rb = dw_row0(p, kb0 + kb);
       const int grows = dw_rows(p, rb);
       tc::mbar_wait(&loaded[stage], ph);
@@ -842,6 +863,12 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
               }
             }
           }
+        }
+        if (!hsm) {
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(dbfull ? &full[stage] : &empty[stage]);   // done reading the stage
+          if (++stage == STAGES) { stage = 0; ph ^= 1; }
+          continue;
         }
         // Hs = bf16(sc_r h_r) in place: 16-B chunk i of the B region lies in 128-B line i / 8, row (i / 8) % 64
         uint8_t* sb = smem + stage * STAGE_BYTES + 2 * A_BYTES;
@@ -928,9 +955,10 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       }
     }
   } else if (lane == 0 && nkb > 0) {
-    // ---- warp 8 lane 0: TMA for both P~ tiles, the h k-block and the two tiles' row scalars
-    const CUtensorMap* tB = &tmH;
-    const bool gq_needed = true;   // plain: the scalars scale h (and feed the d_b sums)
+    // ---- warp 8 lane 0: TMA for both P~ tiles, the h (precomputed plain: Hs) k-block and the two tiles'
+    // row scalars
+    const CUtensorMap* tB = plain && !hsm ? &tmHs : &tmH;
+    const bool gq_needed = !plain || hsm || bjy == 0;   // plain: the scalars scale h / feed the d_b sums
     const int PF = p.pf;
     const bool pfP = !(p.pfmode & 1) || bjy == 0, pfH = !(p.pfmode & 1) || bvx == 0;
     auto prefetch = [&](int kb) {
@@ -956,7 +984,12 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       uint8_t* sa = smem + stage * STAGE_BYTES;
       uint64_t* ld = &loaded[stage];
       tc::mbar_arrive_expect_tx(ld, bytes);
-      tc::tma_load_3d(sa, &tmP, ld, 0, (int)rb, v0 / 64);
+      if (mc) {
+        for (int pl = (int)crank; pl < 4; pl += mc)
+          tc::tma_load_3d_mc(sa + pl * (64 * BK * 2), &tmP1, ld, 0, (int)rb, v0 / 64 + pl, mcmask);
+      } else {
+        tc::tma_load_3d(sa, &tmP, ld, 0, (int)rb, v0 / 64);
+      }
       if (p.h3) tc::tma_load_3d(sa + 2 * A_BYTES, tB, ld, 0, (int)rb, j0 / 64);
       else
         for (int bx = 0; bx < nbox; ++bx)
@@ -971,7 +1004,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
     int stage = 0;
     uint32_t ph = 0;
     for (int kb = 0; kb < nkb; ++kb) {
-      tc::mbar_wait(&full[stage], ph);
+      tc::mbar_wait(plain && !hsm && !dbfull ? &loaded[stage] : &full[stage], ph);
       tc::fence_after_sync();
       const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + 2 * A_BYTES;
 #pragma unroll
@@ -980,13 +1013,15 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
         tc::mma_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
         if (two) tc::mma_bf16(tbase + 256, tc::sdesc(a + A_BYTES + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
       }
-      tc::mma_commit(&empty[stage]);
+      if (mc) tc::mma_commit_mc(&empty[stage], mcmask);   // releases the stage in every sibling
+      else tc::mma_commit(&empty[stage]);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
     tc::mma_commit(tfull);
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (mc) tc::cluster_sync();             // no multicast write or arrive targets an exited sibling
   if (warp == 8) tc::tmem_dealloc(tbase, 512);
 }
 
@@ -1055,8 +1090,61 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
 }
 
 // live / nlive: the ascending live-tile list of the step (null: every row's k-block is read);
-// tscale: the plain mode's switch (null: the rescaling path)
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+// Hs = bf16(sc_r h_r) for the rows of the live tiles (plain mode with a precomputed Hs: tscale == 0; dead
+// rows 0), the B operand of the plain d_w GEMM.  Block per live tile (grid-stride), four 16-B loads in
+// flight per thread.
+__global__ void __launch_bounds__(256) scale_rows_kernel(const uint16_t* __restrict__ h, const float4* __restrict__ gpk,
+                                                         const int* __restrict__ tscale, const int* __restrict__ live,
+                                                         const int* __restrict__ nlive, long long R, int J,
+                                                         uint16_t* __restrict__ Hs) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
+  if (*tscale != 0) return;
+  const int nl = *nlive, J8 = J / 8;
+  constexpr int KU = 4;
+  for (int b = blockIdx.x; b < nl; b += gridDim.x) {
+    const long long r0 = (long long)live[b] * 128;
+    const int rows = (int)min(128LL, R - r0);
+    const int tot = rows * J8;
+    for (int i0 = threadIdx.x; i0 < tot; i0 += KU * blockDim.x) {
+      uint4 x[KU];
+      float sc[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int i = i0 + k * blockDim.x;
+        const int rl = i / J8, c = i - rl * J8;
+        const long long r = r0 + rl;
+        sc[k] = i < tot ? gpk[r].x : 0.f;   // tile 0's scalar (= every tile's in plain mode); dead rows 0
+        x[k] = sc[k] != 0.f ? __ldg(reinterpret_cast<const uint4*>(h + r * J) + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int i = i0 + k * blockDim.x;
+        if (i >= tot) break;
+        const int rl = i / J8, c = i - rl * J8;
+        const uint32_t w[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+        uint32_t q[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(sc[k] * __uint_as_float(w[m] << 16),
+                                                          sc[k] * __uint_as_float(w[m] & 0xffff0000u));
+          q[m] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        reinterpret_cast<uint4*>(Hs + (r0 + rl) * J)[c] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    }
+  }
+}
+cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
+                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<long long>(ntiles, 8LL * current_sm_count());
+  if (grid == 0) return cudaSuccess;
+  RNNT_LAUNCH(KID_SCALE_ROWS, st, launch_pdl(scale_rows_kernel, grid, 256, 0, st, h, g.gpk, tscale, live, nlive, g.R, d.J, Hs));
+  return cudaGetLastError();
+}
+
+// tscale: the plain mode's switch (null: the rescaling path); Hs: the precomputed plain-mode B operand
+// (null with tscale: formed in shared memory)
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
                              cudaStream_t st) {
   CUtensorMap tp, th;
   if (!make_tmap_bf16_2d(&tp, g.Pt, d.VP(), d.rows(), (uint64_t)d.VP() * 2, 64, jdw::BK)) return cudaErrorInvalidValue;
@@ -1077,12 +1165,47 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     p.h3 = d.J % 64 == 0;
     if (p.h3 && !make_tmap_bf16_3d(&th3, h, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4))
       return cudaErrorInvalidValue;
+    CUtensorMap ths = p.h3 ? th3 : th;   // the precomputed plain-mode B operand Hs, same geometry as h
+    if (Hs && (p.h3 ? !make_tmap_bf16_3d(&ths, Hs, 64, d.rows(), d.J / 64, (uint64_t)d.J * 2, 128, 64, jdw2::BK, 4)
+                    : !make_tmap_bf16_2d(&ths, Hs, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)))
+      return cudaErrorInvalidValue;
+    p.hsmem = Hs ? 0 : 1;
+    // P~ multicast over the J parts (RNNT_DW_MC=0: off): clusters of njp CTAs along grid x (j first)
+    const int njp = (d.J + jdw2::BN - 1) / jdw2::BN;
+    static const int mc_env = env_int("RNNT_DW_MC", 1);
+    CUtensorMap tp1 = tp3;
+    if (mc_env != 0 && njp >= 2 && njp <= 8) {
+      if (!make_tmap_bf16_3d(&tp1, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw2::BK, 1))
+        return cudaErrorInvalidValue;
+      p.mc = njp;
+      p.pfmode |= 2;
+    }
     static const int pf = env_int("RNNT_DW_PF", -1), pfmode = env_int("RNNT_DW_PFMODE", -1);
     if (pf >= 0) p.pf = pf;
     if (pfmode >= 0) p.pfmode = pfmode;
+    if (p.mc > 1) p.pfmode |= 2;           // (clusters run along grid x: the J parts first)
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
-    RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, p));
+    if (p.mc > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(jdw2::THREADS);
+      cfg.dynamicSmemBytes = jdw2::SMEM_BYTES;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)p.mc;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_wide_kernel, tp3, p.h3 ? th3 : th, ths, tp1, p));
+    } else {
+      RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3,
+                                         p.h3 ? th3 : th, ths, tp1, p));
+    }
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);
     cudaLaunchConfig_t cfg = {};

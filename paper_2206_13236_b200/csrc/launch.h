@@ -16,7 +16,7 @@ enum KernelId {
   KID_DW, KID_DB, KID_DW_REDUCE, KID_DB_REDUCE, KID_BIAS_PAD, KID_OCCSUMS,
   KID_SMOOTH_AVG, KID_SMOOTH_AC, KID_SMOOTH_GQ, KID_SMOOTH_Q,
   KID_FULL_SCATTER, KID_FULL_PACK, KID_FULL_LIVE, KID_FULL_DGRAD, KID_LOSS_SUMS, KID_EXCHANGE_SUM,
-  KID_COUNT
+  KID_SCALE_ROWS, KID_COUNT
 };
 
 const char* kernel_name(int id);

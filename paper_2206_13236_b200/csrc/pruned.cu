@@ -38,7 +38,9 @@ cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                              const int* nlive, long long ntiles, float* dpre, const int* tscale, const float* gsp,
                              cudaStream_t st);
 cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
-cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
+cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
+                              const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st);
+cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
                              cudaStream_t st);
 
 // ------------------------------------------------------------------ K7 prune
@@ -838,51 +840,40 @@ __global__ void __launch_bounds__(256) band_chunk_kernel(const uint16_t* __restr
   const int ue = min(Un, pr[te - 1] + S - 1);
   while (base <= ue) flush();
 }
-// B: a warp per (utterance, u): for each chunk covering u (in chunk order) the partial's whole row, lane =
-// 4 columns of each 512-B segment, all segments' loads in flight together (a warp per segment measured
-// 18.5 us at c5: four times the warps, each waiting on the same three dependent round trips).
-constexpr int kBandDecSeg = 8;   // segments per pass held in registers (J <= 1024: one pass)
+// B: a warp per (utterance, u, 32-float4 column segment): the partials of the chunks covering u, in chunk
+// order, eight chunks' loads in flight (a u under a band stuck for hundreds of frames spans tens of
+// chunks: a chunk per round trip measured 24-36 us at c5); 32-bit index math (64-bit divisions were most of
+// its issue slots).
 __global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__ part, const int2* __restrict__ urange,
                                                        const int64_t* __restrict__ bnd, int N, int T, int U, int S,
                                                        int J, float* __restrict__ d_dec, const float* __restrict__ gsp) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  const int J4 = J / 4;
-  const int nu = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // < 2^31 (checked by the launcher)
+  const int J4 = J / 4, nseg = band_nseg(J);
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // < 2^31 (checked by the launcher)
   const int lane = threadIdx.x & 31;
-  if (nu >= N * (U + 1)) return;
+  if (w >= N * (U + 1) * nseg) return;
+  const int nu = w / nseg;
+  const int q = (w - nu * nseg) * 32 + lane;
   const int n = nu / (U + 1), u = nu - n * (U + 1);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
-  const bool live = (long long)Un <= (long long)Tn * (S - 1) && u <= Un;
-  int c0 = 0, c1 = -1;
-  if (live) {
+  const bool feas = (long long)Un <= (long long)Tn * (S - 1);
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (feas && u <= Un) {
     const int2 cv = urange[nu];                            // frames [lo, hi) cover u
-    c0 = cv.x / kBandCH;
-    c1 = (cv.y - 1) / kBandCH;
-  }
-  const float gm = gs_mult(gsp);
-  const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4;
-  float4* o = reinterpret_cast<float4*>(d_dec + (size_t)nu * J);
-  for (int q0 = 0; q0 < J4; q0 += 32 * kBandDecSeg) {
-    float4 a[kBandDecSeg];
+    const int c0 = cv.x / kBandCH, c1 = (cv.y - 1) / kBandCH;
+    const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4 + q;
+    const int cstride = S * J4;
+    for (int cb = c0; cb <= c1; cb += 8) {
+      float4 x[8];
 #pragma unroll
-    for (int g = 0; g < kBandDecSeg; ++g) a[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int cb = c0; cb <= c1; ++cb) {
-      const float4* Pc = P + (size_t)cb * S * J4;
-      float4 x[kBandDecSeg];
+      for (int m = 0; m < 8; ++m)
+        x[m] = (cb + m <= c1 && q < J4) ? P[(cb + m) * cstride] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int g = 0; g < kBandDecSeg; ++g) {
-        const int q = q0 + g * 32 + lane;
-        x[g] = q < J4 ? Pc[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int g = 0; g < kBandDecSeg; ++g) { a[g].x += x[g].x; a[g].y += x[g].y; a[g].z += x[g].z; a[g].w += x[g].w; }
+      for (int m = 0; m < 8; ++m) { a.x += x[m].x; a.y += x[m].y; a.z += x[m].z; a.w += x[m].w; }
     }
-#pragma unroll
-    for (int g = 0; g < kBandDecSeg; ++g) {
-      const int q = q0 + g * 32 + lane;
-      if (q < J4) o[q] = live ? f4_scale(a[g], gm) : a[g];
-    }
+    a = f4_scale(a, gs_mult(gsp));
   }
+  if (q < J4) reinterpret_cast<float4*>(d_dec + (size_t)nu * J)[q] = a;
 }
 
 cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
@@ -918,7 +909,7 @@ cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint
 #undef RNNT_BAND
   }
   if (d_dec) {
-    const long long nw = (long long)d.N * d.U1();
+    const long long nw = (long long)d.N * d.U1() * band_nseg(d.J);
     RNNT_LAUNCH(KID_DDEC, st, launch_pdl(band_dec_kernel, (unsigned)((nw + 7) / 8), 256, 0, st,
                                          w.bpart, w.urange, bnd, d.N, d.T, d.U, d.S, d.J, d_dec, w.gsp));
   }
@@ -937,7 +928,9 @@ cudaError_t pruned_bwd_weight_launch(const Dims& d, const PrunedWS& w, const uin
   GradSrc g{w.Pt, w.gpk, w.rowinfo, d.rows(), d.V, d.VP(), d.ntile()};
   const long long ntiles = (d.rows() + 127) / 128;
   const int* ts = w.plain ? w.tscale : nullptr;   // (the full loss: always the rescaling path)
-  if ((e = joiner_dw_launch(d, g, h, ts, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) !=
+  if (ts && w.Hs && (e = scale_rows_launch(d, g, h, ts, w.dhlive, w.dhlive + ntiles, ntiles, w.Hs, st)) != cudaSuccess)
+    return e;
+  if ((e = joiner_dw_launch(d, g, h, w.Hs, ts, w.dhlive, w.dhlive + ntiles, w.dWp, w.dbp, w.splits, st)) !=
       cudaSuccess)
     return e;
   if (mode != 0) {

@@ -114,6 +114,7 @@ struct PrunedWS {
   float* dpre;       // (R,J) dpre = dh (1 - h^2) of every band row (live rows only are written): the pruned
                      //    path stores it as fp16 dpre / gs (the first half of the buffer), the full loss fp32
   bool plain;        // the plain joiner backward may run (tscale == 0 honoured; false: the full loss)
+  uint16_t* Hs;      // (R,J) bf16 sc_r h_r, the plain d_w GEMM's B operand for large V (null: formed in smem)
   float* bpart;      // (N, band_part_rows, J) d_dec partials of the band reduction
   float* dWp;        // (splits,V,J) split-K partials of d_w
   float* dbp;        // (splits,V)   split-K partials of d_b
@@ -127,6 +128,10 @@ inline bool dw_wide(const Dims& d) {
   if (force >= 0) return force == 1;
   return true;   // measured: c2 65.5 vs 68.6 us, c3 339 vs 593, c4 2113 vs 3234 (the 128-v variant with 2D boxes)
 }
+
+// Plain-mode d_w operand Hs = bf16(sc h): precomputed by scale_rows_kernel for large V (the d_w mainloop is
+// long and shared-memory bound), else formed in the d_w kernel's shared memory (joiner_bwd.cu).
+inline bool hs_precomputed(const Dims& d) { return d.V >= 2048; }
 
 // Split-K factor of the d_w GEMM (K11): about two CTAs per SM over the (V/128) x (J/256)
 // output tiles, at least 4 K-blocks of 64 rows per split.
@@ -221,6 +226,7 @@ inline size_t carve(const Dims& d, void* base, SimpleWS* sw, PrunedWS* pw, bool 
   p.dhlive = (int*)take(((R + 127) / 128 + 1) * 4);
   p.dpre = (float*)take(R * J * 4);
   p.plain = with_plain;
+  p.Hs = with_plain && hs_precomputed(d) ? (uint16_t*)take(R * J * 2) : nullptr;
   p.bpart = (float*)take((size_t)N * band_part_rows(d.T, d.U, d.S) * J * 4);
   p.dWp = (float*)take((size_t)p.splits * V * J * 4);
   p.dbp = (float*)take((size_t)p.splits * V * 4);

@@ -79,47 +79,6 @@ __global__ void full_pack_kernel(const float* __restrict__ gb, const float* __re
   }
 }
 
-// ids of the 128-row tiles holding a live row (order irrelevant), count at live[ntiles]
-// The ascending list of live 128-row tiles (tlive[i] != 0) and its count at live[ntiles]: one block,
-// thread k compacts a contiguous range of tiles at its exclusive-scan offset (deterministic order: the
-// d_w split-K partials follow it).
-__global__ void __launch_bounds__(1024) full_live_kernel(const uint8_t* __restrict__ tlive, long long ntiles,
-                                                         int* __restrict__ live) {
-  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  __shared__ int wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const long long per = (ntiles + 1023) / 1024;
-  const long long i0 = min(ntiles, (long long)tid * per), i1 = min(ntiles, i0 + per);
-  int c = 0;
-  for (long long i = i0; i < i1; ++i) c += tlive[i] != 0;
-  int x = c;   // inclusive warp scan
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    int s = wsum[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    wsum[lane] = s;   // inclusive over warps
-  }
-  __syncthreads();
-  int off = x - c + (wid > 0 ? wsum[wid - 1] : 0);
-  for (long long i = i0; i < i1; ++i)
-    if (tlive[i]) live[off++] = (int)i;
-  if (tid == 1023) live[ntiles] = off;
-}
-cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st) {
-  RNNT_LAUNCH(kid, st, launch_pdl(full_live_kernel, 1, 1024, 0, st, tlive, ntiles, live));
-  return cudaGetLastError();
-}
-
 // blocks [0, N T): d_enc[n,t,:] = sum_{u <= U_n} dpre[(n,t,u),:];  blocks [N T, N T + N (U+1)):
 // d_dec[n,u,:] = sum_{t < T_n} dpre[(n,t,u),:]; padded positions 0.  One thread per 4 columns.
 __global__ void __launch_bounds__(128) full_dgrad_kernel(const float* __restrict__ dpre, const int64_t* __restrict__ bnd,
@@ -175,7 +134,6 @@ cudaError_t full_loss_launch(const Dims& d, void* base, const float* enc, const 
   if ((e = prune_launch(df, enc, dec, fw.ranges0, bnd, fw.h, st)) != cudaSuccess) return e;
   if ((e = rowinfo_launch(df, pw, fw.ranges0, sym, bnd, b, gs, st)) != cudaSuccess) return e;
   const long long ntiles = (R + 127) / 128;
-  if ((e = live_tiles_launch(pw.tlive, ntiles, pw.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(df, pw, fw.h, W, b, st)) != cudaSuccess) return e;
   {
     const long long cells = (long long)(df.K() + 1) * df.LU();

@@ -1170,9 +1170,9 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                     : !make_tmap_bf16_2d(&ths, Hs, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)))
       return cudaErrorInvalidValue;
     p.hsmem = Hs ? 0 : 1;
-    // P~ multicast over the J parts (RNNT_DW_MC=0: off): clusters of njp CTAs along grid x (j first)
+    // P~ multicast over the J parts (RNNT_DW_MC=1: on): clusters of njp CTAs along grid x (j first)
     const int njp = (d.J + jdw2::BN - 1) / jdw2::BN;
-    static const int mc_env = env_int("RNNT_DW_MC", 1);
+    static const int mc_env = env_int("RNNT_DW_MC", 0);   // measured slower: off by default
     CUtensorMap tp1 = tp3;
     if (mc_env != 0 && njp >= 2 && njp <= 8) {
       if (!make_tmap_bf16_3d(&tp1, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdw2::BK, 1))

@@ -37,7 +37,6 @@ struct GradSrc {
 cudaError_t joiner_dh_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* W, const int* live,
                              const int* nlive, long long ntiles, float* dpre, const int* tscale, const float* gsp,
                              cudaStream_t st);
-cudaError_t live_tiles_launch(const uint8_t* tlive, long long ntiles, int* live, int kid, cudaStream_t st);
 cudaError_t scale_rows_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const int* tscale, const int* live,
                               const int* nlive, long long ntiles, uint16_t* Hs, cudaStream_t st);
 cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h, const uint16_t* Hs, const int* tscale, const int* live, const int* nlive, float* dWp, float* dbp, int splits,
@@ -89,14 +88,38 @@ __global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ e
   }
 }
 
-// blocks [0, nb_rows): per band row label info (and the frames covering each u); the last block
-// pads the bias to fp32 (VP columns, zero beyond V) for the joiner epilogue.
+// Does 128-row tile i of the band rows hold a live row?  Row (n, t, s) is live iff t < T_n, the utterance
+// is feasible and p_t + s <= U_n; the s = 0 row of a live frame always is (p_t <= max(0, U_n - S + 1)).  So
+// the tile is live iff its first frame's first row in the tile is, or a later frame of the tile is a live
+// frame -- O(utterances spanned) per tile instead of a pass over its 128 rows.
+__device__ __forceinline__ bool band_tile_live(long long i, const int32_t* __restrict__ ranges,
+                                               const int64_t* __restrict__ bnd, int T, int S, long long R) {
+  const long long r0 = i * 128, r1 = min(R, r0 + 128) - 1;
+  const long long f0 = r0 / S, f1 = r1 / S;
+  const int s0 = (int)(r0 - f0 * S);
+  {
+    const int n = (int)(f0 / T), t = (int)(f0 - (long long)n * T);
+    const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+    if (t < Tn && (long long)Un <= (long long)Tn * (S - 1) && ranges[f0] + s0 <= Un) return true;
+  }
+  for (long long f = f0 + 1; f <= f1;) {
+    const int n = (int)(f / T), t = (int)(f - (long long)n * T);
+    const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
+    if (t < Tn && (long long)Un <= (long long)Tn * (S - 1)) return true;
+    f = (long long)(n + 1) * T;   // the utterance's later frames are padded as well
+  }
+  return false;
+}
+
+// blocks [0, nb_rows): per band row label info (and the frames covering each u); the last block pads the
+// bias to fp32 (VP columns, zero beyond V) for the joiner epilogue and writes the 128-row tile liveness
+// and the ascending list of live tiles (count at live[ntiles]) that the joiner kernels work through.
 __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t* __restrict__ sym,
                                const int64_t* __restrict__ bnd, int N, int T, int U, int V, int S,
                                int32_t* __restrict__ rowinfo, int2* __restrict__ urange,
                                const uint16_t* __restrict__ bias_bf16, int VP, float* __restrict__ bias,
                                float* __restrict__ bmax, uint8_t* __restrict__ tlive, int* __restrict__ tcounter,
-                               int tscale0, float gs) {
+                               int tscale0, float gs, int* __restrict__ live) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   if (blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x == 0) {
@@ -116,6 +139,41 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
       m = warp_max(m);
       if (lane == 0) bmax[tl] = m;
     }
+    // tile liveness and the ascending live-tile list: thread k takes a contiguous range of tiles and
+    // writes its live ones at its exclusive-scan offset (deterministic order: the d_w split-K partials
+    // follow it)
+    __shared__ int wsum[32];
+    const long long R = (long long)N * T * S, ntiles = (R + 127) / 128;
+    const long long per = (ntiles + blockDim.x - 1) / blockDim.x;
+    const long long i0 = min(ntiles, (long long)threadIdx.x * per), i1 = min(ntiles, i0 + per);
+    int c = 0;
+    for (long long i = i0; i < i1; ++i) {
+      const bool lv = band_tile_live(i, ranges, bnd, T, S, R);
+      tlive[i] = lv ? 1 : 0;
+      c += lv;
+    }
+    int x = c;   // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int sw = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, sw, o);
+        if (lane >= o) sw += y;
+      }
+      wsum[lane] = sw;   // inclusive over warps
+    }
+    __syncthreads();
+    int off = x - c + (warp > 0 ? wsum[warp - 1] : 0);
+    for (long long i = i0; i < i1; ++i)
+      if (tlive[i]) live[off++] = (int)i;
+    if (threadIdx.x == blockDim.x - 1) live[ntiles] = off;
     return;
   }
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -151,12 +209,6 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
     }
     rowinfo[r] = info;
   }
-  // 128-row tile liveness for the persistent joiner: a 256-thread block holds two whole tiles
-  const bool live = info >= 0;
-  const bool lo = __syncthreads_or(live && threadIdx.x < 128);
-  const bool hi = __syncthreads_or(live && threadIdx.x >= 128);
-  if (threadIdx.x == 0 && r < R) tlive[r / 128] = lo ? 1 : 0;
-  if (threadIdx.x == 128 && r < R) tlive[r / 128] = hi ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ K9 pruned recursion
@@ -696,7 +748,7 @@ cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* rang
   const long long R = d.rows();
   RNNT_LAUNCH(KID_ROWINFO, st, launch_pdl(rowinfo_kernel, (unsigned)((R + 255) / 256 + 1), 256, 0, st, 
       ranges, sym, bnd, d.N, d.T, d.U, d.V, d.S, w.rowinfo, w.urange, b, d.VP(), w.bias, w.bmax, w.tlive, w.tcounter,
-      plain_backward_capable(d) ? 0 : 1, gs));
+      plain_backward_capable(d) ? 0 : 1, gs, w.dhlive));
   return cudaGetLastError();
 }
 
@@ -709,8 +761,6 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
   const long long R = d.rows();
   const int nt = d.ntile();
   if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, gs, st)) != cudaSuccess) return e;
-  // the ascending list of live 128-row tiles, read by both backward calls (K10, K11)
-  if ((e = live_tiles_launch(w.tlive, (d.rows() + 127) / 128, w.dhlive, KID_FULL_LIVE, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);

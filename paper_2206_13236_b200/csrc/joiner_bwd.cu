@@ -121,20 +121,22 @@ constexpr int B_BYTES = NSUB * BK * 2;         // 32 KB, MN-major (4 boxes of 64
 constexpr int G_BYTES = BM * 16;               // 2 KB: the rows' packed scalars for this k-block's V tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + G_BYTES;   // 50 KB (1024-aligned)
 constexpr int H_BYTES = BM * 64 * 2;           // one 64-column box of h (SWIZZLE_128B)
-constexpr int O_BYTES = BM * 32 * 4;           // one 32-column dpre chunk (128 rows x 128 B, SWIZZLE_128B)
 // Shared memory per variant.  Short V loops (4 producer warps, item = a few k-blocks): 3 stages, h by
-// TMA into a 2-slot ring, 2 dpre staging tiles (the epilogue is on the critical path).  Long V loops
-// (8 producer warps): 4 stages (the per-stage chain load -> dz transform -> MMA is what bounds the
-// mainloop), h read from L2 by the epilogue, 1 staging tile.
-template <int NTW> struct Cfg {
+// TMA into a 2-slot ring (3 slots with fp16 dpre rows, whose staging tiles are half the size: the
+// epilogue waited on the h box loads for 15 % of its stall samples at c5), 2 dpre staging tiles (the
+// epilogue is on the critical path).  Long V loops (8 producer warps): 4 stages (the per-stage chain
+// load -> dz transform -> MMA is what bounds the mainloop), h read from L2 by the epilogue, 1 staging tile.
+template <int NTW, bool D16> struct Cfg {
   static constexpr int STAGES = NTW == 8 ? 4 : 3;
-  static constexpr int HRING = NTW == 8 ? 0 : 2;
+  static constexpr int HRING = NTW == 8 ? 0 : (D16 ? 3 : 2);
   static constexpr int ORING = NTW == 8 ? 1 : 2;
+  static constexpr int O_BYTES = BM * 32 * (D16 ? 2 : 4);   // one 32-column dpre chunk (128 rows)
   static constexpr int H_OFF = STAGES * STAGE_BYTES;
   static constexpr int O_OFF = H_OFF + HRING * H_BYTES;
   static constexpr int BAR_OFF = O_OFF + ORING * O_BYTES;
   static constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 };
+constexpr int kMaxHRing = 4;
 // in-place dz producer warps: 4 (a thread per row) for short V loops, 8 (a thread per half row) when
 // the mainloop is long
 template <int NTW> struct Roles {
@@ -181,7 +183,7 @@ __device__ __forceinline__ void dh_trace_kb(int it, int kb, int k) {
 // L2 -> SM traffic per MMA drops from 50 to 34 KB per k-block (the contraction is L2-bandwidth bound at
 // large V).  A stage is refilled once both CTAs' MMAs released it (each MMA commit arrives on both
 // CTAs' empty barrier).
-template <int NTW, bool MC>
+template <int NTW, bool MC, bool D16>
 __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     joiner_dh_tc_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmD,
@@ -189,18 +191,19 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdh;
   constexpr int EPI0 = Roles<NTW>::EPI0;
-  constexpr int STAGES = Cfg<NTW>::STAGES, HRING = Cfg<NTW>::HRING, ORING = Cfg<NTW>::ORING;
+  using C = Cfg<NTW, D16>;
+  constexpr int STAGES = C::STAGES, HRING = C::HRING, ORING = C::ORING, O_BYTES = C::O_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = tc::align1024(smem_raw);
-  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + Cfg<NTW>::BAR_OFF);
+  uint64_t* loaded = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* full = loaded + STAGES;
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;       // [2]
   uint64_t* tempty = tfull + 2;           // [2]
-  uint64_t* hfull = tempty + 2;           // [2] (HRING > 0)
-  uint64_t* hempty = hfull + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + 2);
-  uint8_t* hbuf = smem + Cfg<NTW>::H_OFF;
+  uint64_t* hfull = tempty + 2;           // [HRING] (HRING > 0)
+  uint64_t* hempty = hfull + kMaxHRing;   // [HRING]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + kMaxHRing);
+  uint8_t* hbuf = smem + C::H_OFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // work items: (row tile, 256-column part); with MC a cluster takes (tile pair, part) items, rank r the
   // tile 2 i + r (an odd last tile is done by both CTAs: identical values, written twice)
@@ -228,6 +231,8 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
       tc::mbar_init(&tempty[s], dual ? 8 : 4);      // the epilogue warps
+    }
+    for (int s = 0; s < HRING; ++s) {
       tc::mbar_init(&hfull[s], 1);
       tc::mbar_init(&hempty[s], dual ? 8 : 4);
     }
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     const uint32_t tl = tbase + ((uint32_t)(32 * q4) << 16);
     const bool leader = warp == (eset ? 2 : EPI0) && lane == 0;   // issues the set's TMA stores
     // fp16 rows (the pruned path): dpre / gs, so the stored range does not depend on the loss scale
-    const bool d16 = p.gsp != nullptr;
+    constexpr bool d16 = D16;   // (p.gsp != nullptr)
     float dsc = 1.f;
     if (d16) {
       const float gsv = *p.gsp;
@@ -398,12 +403,28 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
     int it = 0, hslot = 0;
     uint32_t hph = 0;
     long long kc = 0;                                     // chunk counter: staging tile kc % ORING
+    // the row's label info and (plain) scalar of the NEXT item are loaded while this item drains: their
+    // dependent global loads (live list -> rowinfo / gpk) sat on the item start otherwise
+    int ninfo = -1;
+    float nsc = 0.f;
+    auto prefetch_row = [&](long long ix) {
+      ninfo = -1;
+      nsc = 0.f;
+      if (ix >= nitems) return;
+      const long long rr = (long long)item_tile(ix) * BM + rl;
+      if (rr < p.g.R) {
+        ninfo = p.g.rowinfo[rr];
+        if (plain) nsc = p.g.gpk[rr].x;
+      }
+    };
+    prefetch_row(cid);
     for (long long idx = cid; idx < nitems; idx += ncl, ++it) {
       const int tile = item_tile(idx), jp = (int)(idx % p.njp);
       const int acc = it & 1;
       const long long r = (long long)tile * BM + rl;
-      const bool live = r < p.g.R && p.g.rowinfo[r] >= 0;
-      const float sc = plain && live ? p.g.gpk[r].x : 1.f;   // plain: the row scalar (tile 0's = every tile's)
+      const bool live = ninfo >= 0;                          // (r < R: else the prefetch left -1)
+      const float sc = plain && live ? nsc : 1.f;            // plain: the row scalar (tile 0's = every tile's)
+      prefetch_row(idx + ncl);
       const int j0 = jp * NSUB, nj = min(NSUB, p.J - j0);
       const int nbox = (nj + 63) / 64;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -453,7 +474,7 @@ __global__ void __launch_bounds__(jdh::Roles<NTW>::THREADS, 1)
         }
         if (!have) continue;
         // staging tile kc % ORING: the TMA store issued from it ORING chunks ago has finished reading it
-        uint8_t* ob = smem + Cfg<NTW>::O_OFF + (dual ? eset : (int)(kc % ORING)) * O_BYTES;
+        uint8_t* ob = smem + C::O_OFF + (dual ? eset : (int)(kc % ORING)) * O_BYTES;
         if (leader) {
           if (ORING == 2 && !dual) tc::bulk_wait_read1();
           else tc::bulk_wait_read0();
@@ -1026,13 +1047,13 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
 }
 
 // ======================================================================= host
-template <int NTW, bool MC>
+template <int NTW, bool MC, bool D16>
 static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
                                const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
-  constexpr int SMEM = jdh::Cfg<NTW>::SMEM_BYTES;
-  smem_optin(joiner_dh_tc_kernel<NTW, MC>, SMEM);
+  constexpr int SMEM = jdh::Cfg<NTW, D16>::SMEM_BYTES;
+  smem_optin(joiner_dh_tc_kernel<NTW, MC, D16>, SMEM);
   if (!MC) {
-    launch_pdl(joiner_dh_tc_kernel<NTW, MC>, grid, jdh::Roles<NTW>::THREADS, SMEM, st, tp, tw, th, td, p);
+    launch_pdl(joiner_dh_tc_kernel<NTW, MC, D16>, grid, jdh::Roles<NTW>::THREADS, SMEM, st, tp, tw, th, td, p);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -1049,16 +1070,17 @@ static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUt
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, joiner_dh_tc_kernel<NTW, MC>, tp, tw, th, td, p);
+  return cudaLaunchKernelEx(&cfg, joiner_dh_tc_kernel<NTW, MC, D16>, tp, tw, th, td, p);
 }
 // 4 producer warps for short V loops, 8 for long ones; W multicast over CTA pairs (RNNT_DH_MC=0: off)
 static cudaError_t launch_dh(const JoinerDhParams& p, unsigned grid, bool mc, const CUtensorMap& tp,
                              const CUtensorMap& tw, const CUtensorMap& th, const CUtensorMap& td, cudaStream_t st) {
-  if (mc)
-    return p.nkb >= 32 ? launch_dh_k<8, true>(p, grid, tp, tw, th, td, st)
-                       : launch_dh_k<4, true>(p, grid, tp, tw, th, td, st);
-  return p.nkb >= 32 ? launch_dh_k<8, false>(p, grid, tp, tw, th, td, st)
-                     : launch_dh_k<4, false>(p, grid, tp, tw, th, td, st);
+  const bool d16 = p.gsp != nullptr, lv = p.nkb >= 32;
+#define RNNT_DH(NTWV, MCV) (d16 ? launch_dh_k<NTWV, MCV, true>(p, grid, tp, tw, th, td, st) \
+                                : launch_dh_k<NTWV, MCV, false>(p, grid, tp, tw, th, td, st))
+  if (mc) return lv ? RNNT_DH(8, true) : RNNT_DH(4, true);
+  return lv ? RNNT_DH(8, false) : RNNT_DH(4, false);
+#undef RNNT_DH
 }
 
 // dpre = dh (1 - h^2) rows of the live 128-row tiles (`live`, count at `nlive`, at most ntiles) into dpre.

@@ -343,7 +343,9 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int STG_BYTES = BM * BN * 2;      // 32 KB P~ staging per epilogue set
 constexpr int MRG_OFF = STAGES * STAGE_BYTES + 2 * STG_BYTES;
 constexpr int XCH_OFF = MRG_OFF + 2 * BM * 16;   // [2 sets][128 rows] first-chunk maxima (m_ref)
-constexpr int BAR_OFF = XCH_OFF + 2 * BM * 4;
+constexpr int BIAS_OFF = XCH_OFF + 2 * BM * 4;    // the fp32 bias (VP <= kBiasSmem): broadcast reads in the
+constexpr int kBiasSmem = 4096;                   // epilogue instead of an L1-missing global load per chunk
+constexpr int BAR_OFF = BIAS_OFF + kBiasSmem * 4;
 constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 constexpr int THREADS = 320;
 }  // namespace jf2
@@ -365,6 +367,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + 4);
   float4* mrg = reinterpret_cast<float4*>(smem + MRG_OFF);   // [2][128] set-1 row state for the merge
   float* xch = reinterpret_cast<float*>(smem + XCH_OFF);
+  float* sbias = reinterpret_cast<float*>(smem + BIAS_OFF);
+  const bool bsm = p.VP <= kBiasSmem;
+  if (bsm)
+    for (int v = threadIdx.x; v < p.VP; v += THREADS) sbias[v] = p.bias[v];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -493,7 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
             tc::tmem_ld32(tcol, z);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (v0 + j < p.V) cm0 = fmaxf(cm0, z[j] + p.bias[v0 + j]);
+              if (v0 + j < p.V) cm0 = fmaxf(cm0, z[j] + (bsm ? sbias[v0 + j] : p.bias[v0 + j]));
           }
           xch[set * BM + 32 * q + lane] = cm0;
           asm volatile("bar.sync 4, 256;" ::: "memory");
@@ -533,9 +539,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
                 tc::tmem_ld32_issue(tcol + 32 * c, zr);
                 const int vc = v0 + 32 * c;
                 float4 b4[8];
-                const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
+                if (bsm) {
+                  const float4* bb = reinterpret_cast<const float4*>(sbias + vc);
 #pragma unroll
-                for (int j4 = 0; j4 < 8; ++j4) b4[j4] = __ldg(bb + j4);
+                  for (int j4 = 0; j4 < 8; ++j4) b4[j4] = bb[j4];
+                } else {
+                  const float4* bb = reinterpret_cast<const float4*>(p.bias + vc);
+#pragma unroll
+                  for (int j4 = 0; j4 < 8; ++j4) b4[j4] = __ldg(bb + j4);
+                }
                 tc::tmem_ld32_wait(zr);
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {

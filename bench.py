@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "multimem"],
                     help="N > 1: how d_w / d_b / loss sums are summed over ranks (include/rnnt.h exchange modes)")
     ap.add_argument("--no-standalone", action="store_true", help="skip the serial (standalone) per-kernel times")
+    ap.add_argument("--copy-streams", type=int, default=2,
+                    help="e2e: H2D copy streams (the packed input tensors dealt across them: two DMA engines)")
     ap.add_argument("--workload", default="fixed", choices=["fixed", "dynamic", "full"],
                     help="dynamic: the Table-2 protocol (sorted utterances, <= 10k input frames per batch); "
                          "full: the unpruned loss with the same joiner on the c2 batch (SURVEY 8(f) f4)")
@@ -666,21 +668,33 @@ def main():
                 graphs[1] = g1
             except Exception:
                 graphs = [None, None]
-        copy_stream = torch.cuda.Stream()
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        ncs = max(1, args.copy_streams)
+        copy_streams = [torch.cuda.Stream() for _ in range(ncs)]
+        copy_stream = copy_streams[0]
+        copied = [[torch.cuda.Event() for _ in range(ncs)] for _ in range(2)]
         freed = [torch.cuda.Event(), torch.cuda.Event()]
+        # the packed tensors dealt to the copy streams by size (largest first, to the least loaded stream)
+        load_, deal = [0] * ncs, {}
+        for tname in sorted(packed, key=lambda t: -packed[t].numel()):
+            j = load_.index(min(load_))
+            deal[tname] = j
+            load_[j] += packed[tname].numel()
 
         def run(nsteps):
             for i in range(nsteps):
                 k = i & 1
-                with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(freed[k])          # step i-2 finished reading buffer set k
-                    for tname in small:
-                        bufs[k][tname].copy_(host[tname], non_blocking=True)
-                    for tname in packed:
-                        dpacked[k][tname].copy_(packed[tname], non_blocking=True)
-                    copied[k].record(copy_stream)
-                stream.wait_event(copied[k])
+                for j, cs_ in enumerate(copy_streams):
+                    with torch.cuda.stream(cs_):
+                        cs_.wait_event(freed[k])              # step i-2 finished reading buffer set k
+                        if j == 0:
+                            for tname in small:
+                                bufs[k][tname].copy_(host[tname], non_blocking=True)
+                        for tname in packed:
+                            if deal[tname] == j:
+                                dpacked[k][tname].copy_(packed[tname], non_blocking=True)
+                        copied[k][j].record(cs_)
+                for j in range(ncs):
+                    stream.wait_event(copied[k][j])
                 # the scatter into the padded layout runs on the step's stream, just before it: on the
                 # copy stream it would wait for SMs behind the previous step's persistent kernels and
                 # stall the copy engine's pipeline
@@ -704,7 +718,8 @@ def main():
         for ev_ in freed:
             ev_.record(stream)
         e0.record(stream)
-        copy_stream.wait_stream(stream)
+        for cs_ in copy_streams:
+            cs_.wait_stream(stream)
         run(K)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -716,6 +731,7 @@ def main():
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
                "pipelining": "H2D of step i+1 overlaps compute of step i (two input buffer sets); only the "
                              "valid rows of each utterance are sent, scattered into the padded layout on device",
+               "copy_streams": ncs,
                "execution": "cuda_graph" if graphs[0] is not None else "eager"}
 
     cpu = None

@@ -905,11 +905,12 @@ __global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__
   const int nu = w / nseg;
   const int q = (w - nu * nseg) * 32 + lane;
   const int n = nu / (U + 1), u = nu - n * (U + 1);
+  const int2 cv = urange[nu];                              // (issued with the length loads: one round trip)
+  const float gm = gs_mult(gsp);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   const bool feas = (long long)Un <= (long long)Tn * (S - 1);
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (feas && u <= Un) {
-    const int2 cv = urange[nu];                            // frames [lo, hi) cover u
+  if (feas && u <= Un) {                                   // frames [lo, hi) cover u
     const int c0 = cv.x / kBandCH, c1 = (cv.y - 1) / kBandCH;
     const float4* P = reinterpret_cast<const float4*>(part) + ((size_t)n * band_part_rows(T, U, S) + u) * J4 + q;
     const int cstride = S * J4;
@@ -921,7 +922,7 @@ __global__ void __launch_bounds__(256) band_dec_kernel(const float* __restrict__
 #pragma unroll
       for (int m = 0; m < 8; ++m) { a.x += x[m].x; a.y += x[m].y; a.z += x[m].z; a.w += x[m].w; }
     }
-    a = f4_scale(a, gs_mult(gsp));
+    a = f4_scale(a, gm);
   }
   if (q < J4) reinterpret_cast<float4*>(d_dec + (size_t)nu * J)[q] = a;
 }

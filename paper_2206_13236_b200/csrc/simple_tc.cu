@@ -132,6 +132,96 @@ __device__ __forceinline__ void exp_split_rows(const float* __restrict__ x, cons
   }
 }
 
+// Large V (V % 4 == 0, 2048 < V <= 4 256 PER): one 256-thread block per row, the row held in registers
+// (PER float4 per thread) between the max and the exp pass -- the warp-per-row form re-reads every row
+// for its second pass, which at V = 8000 (32 KB rows, 8 rows per block) misses L2 (c4: 0.54 of HBM).
+// Same per-element arithmetic; the row sums for lse_lm are reduced in a different order.
+template <int PER>
+__device__ __forceinline__ void exp_split_row_block(const float* __restrict__ x, const int64_t* __restrict__ sym,
+                                                    const int64_t* __restrict__ bnd, int rows_per_n, int U, int V,
+                                                    int VP, int which, float* __restrict__ m, uint16_t* __restrict__ hi,
+                                                    uint16_t* __restrict__ lo, float* __restrict__ amy, int UPa,
+                                                    float* __restrict__ lse, long long row) {
+  __shared__ float red[8];
+  __shared__ float bmx;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)(row / rows_per_n), r = (int)(row % rows_per_n);
+  const int Un = utt_U(bnd, n);
+  const int lim = which == 0 ? utt_T(bnd, n) : Un + 1;
+  uint2* H2 = reinterpret_cast<uint2*>(hi + row * (long long)VP);
+  uint2* L2 = reinterpret_cast<uint2*>(lo + row * (long long)VP);
+  const int V4 = V >> 2, VP4 = VP >> 2;
+  if (r >= lim) {   // padded row: zero operand, never read otherwise
+    for (int j = tid; j < VP4; j += 256) { H2[j] = make_uint2(0u, 0u); L2[j] = make_uint2(0u, 0u); }
+    if (tid == 0) {
+      m[row] = 0.f;
+      if (lse) lse[row] = 0.f;
+    }
+    return;
+  }
+  const float* p = x + row * (long long)V;
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+  float4 t[PER];
+  float mx = neg_inf_f();
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int j = tid + 256 * k;
+    t[k] = j < V4 ? __ldg(p4 + j) : make_float4(neg_inf_f(), neg_inf_f(), neg_inf_f(), neg_inf_f());
+    mx = fmaxf(mx, fmaxf(fmaxf(t[k].x, t[k].y), fmaxf(t[k].z, t[k].w)));
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    float v = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, red[w]);
+    bmx = v;
+    m[row] = v;
+  }
+  __syncthreads();
+  mx = bmx;
+  float esum = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int j = tid + 256 * k;
+    if (j < VP4) {
+      const float e0 = __expf(t[k].x - mx), e1 = __expf(t[k].y - mx);
+      const float e2 = __expf(t[k].z - mx), e3 = __expf(t[k].w - mx);
+      esum += (e0 + e1) + (e2 + e3);
+      const __nv_bfloat162 h01 = __floats2bfloat162_rn(e0, e1), h23 = __floats2bfloat162_rn(e2, e3);
+      const __nv_bfloat162 l01 = __floats2bfloat162_rn(e0 - __low2float(h01), e1 - __high2float(h01));
+      const __nv_bfloat162 l23 = __floats2bfloat162_rn(e2 - __low2float(h23), e3 - __high2float(h23));
+      H2[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+      L2[j] = make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+    }
+  }
+  for (int j = VP4 > 256 * PER ? 256 * PER + tid : VP4; j < VP4; j += 256) {   // (VP4 <= 256 PER: none)
+    H2[j] = make_uint2(0u, 0u);
+    L2[j] = make_uint2(0u, 0u);
+  }
+  if (lse) {   // lm rows: log sum_v exp lm[u,v] (the LM-only log-softmax of Eq. 14)
+    esum = warp_sum(esum);
+    __syncthreads();                                 // red reused
+    if (lane == 0) red[warp] = esum;
+    __syncthreads();
+    if (tid == 0) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[w];
+      lse[row] = mx + __logf(v);
+    }
+  }
+  if (which == 0) {
+    float* ay = amy + ((size_t)n * rows_per_n + r) * UPa;
+    for (int u = tid; u <= Un; u += 256) {
+      long long y = u < Un ? sym[(size_t)n * U + u] : 0;
+      y = y < 0 ? 0 : (y >= V ? V - 1 : y);   // address safety; bad symbols flagged in status
+      ay[u] = u < Un ? p[y] : 0.f;
+    }
+  }
+}
+
 // One launch for the independent prologue work of the simple loss, dispatched by block index:
 // am rows (exp split + amy), lm rows (exp split), skewed-arc sentinels, validation.
 struct PrepParams {
@@ -143,23 +233,38 @@ struct PrepParams {
   float2* pxy;
   int32_t* status;
   int nb_am, nb_lm, nb_fill;
+  int rowblk;   // 1: one block per am / lm row (exp_split_row_block<8>), else 8 rows per block
 };
 
 __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   int b = blockIdx.x;
-  if (b < p.nb_am) {
+  if (p.rowblk) {
+    if (b < p.nb_am) {
+      exp_split_row_block<8>(p.am, p.sym, p.bnd, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP,
+                             nullptr, b);
+      return;
+    }
+    b -= p.nb_am;
+    if (b < p.nb_lm) {
+      exp_split_row_block<8>(p.lm, p.sym, p.bnd, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
+                             p.lse_lm, b);
+      return;
+    }
+    b -= p.nb_lm;
+  } else if (b < p.nb_am) {
     exp_split_rows(p.am, p.sym, p.bnd, p.N, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP, nullptr,
                    b);
     return;
+  } else {
+    b -= p.nb_am;
+    if (b < p.nb_lm) {
+      exp_split_rows(p.lm, p.sym, p.bnd, p.N, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
+                     p.lse_lm, b);
+      return;
+    }
+    b -= p.nb_lm;
   }
-  b -= p.nb_am;
-  if (b < p.nb_lm) {
-    exp_split_rows(p.lm, p.sym, p.bnd, p.N, p.U + 1, p.U, p.V, p.VP, 1, p.m_lm, p.elm_hi, p.elm_lo, nullptr, 0,
-                   p.lse_lm, b);
-    return;
-  }
-  b -= p.nb_lm;
   if (b < p.nb_fill) {
     // kNegBig in every invalid cell of the skewed arcs (lattice.cu conventions): 8 rows per block
     const long long rows = (long long)p.N * (p.K + 1);
@@ -987,8 +1092,9 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   p.m_am = w.m_am; p.m_lm = w.m_lm; p.amy = w.amy; p.lse_lm = w.lse_lm;
   p.eam_hi = w.Eam_hi; p.eam_lo = w.Eam_lo; p.elm_hi = w.Elm_hi; p.elm_lo = w.Elm_lo;
   p.pxy = w.pxy; p.status = status;
-  p.nb_am = (int)(((long long)d.N * d.T + 7) / 8);
-  p.nb_lm = (int)(((long long)d.N * d.U1() + 7) / 8);
+  p.rowblk = (d.V % 4 == 0 && d.V > 2048 && d.VP64() <= 4 * 256 * 8) ? 1 : 0;
+  p.nb_am = (int)(p.rowblk ? (long long)d.N * d.T : ((long long)d.N * d.T + 7) / 8);
+  p.nb_lm = (int)(p.rowblk ? (long long)d.N * d.U1() : ((long long)d.N * d.U1() + 7) / 8);
   p.nb_fill = (int)(((long long)d.N * (d.K() + 1) + 7) / 8);
   const unsigned grid = (unsigned)(p.nb_am + p.nb_lm + p.nb_fill + d.N);
   RNNT_LAUNCH(KID_ROWMAX_AM, st, launch_pdl(simple_prep_kernel, grid, 256, 0, st, p));

@@ -131,7 +131,10 @@ inline bool dw_wide(const Dims& d) {
 
 // Plain-mode d_w operand Hs = bf16(sc h): precomputed by scale_rows_kernel for large V (the d_w mainloop is
 // long and shared-memory bound), else formed in the d_w kernel's shared memory (joiner_bwd.cu).
-inline bool hs_precomputed(const Dims& d) { return d.V >= 2048; }
+inline bool hs_precomputed(const Dims& d) {
+  static const int force = env_int("RNNT_HS_PRE", -1);   // A/B: 1 always precompute, 0 never
+  return force >= 0 ? force == 1 : d.V >= 2048;
+}
 
 // Split-K factor of the d_w GEMM (K11): about two CTAs per SM over the (V/128) x (J/256)
 // output tiles, at least 4 K-blocks of 64 rows per split.

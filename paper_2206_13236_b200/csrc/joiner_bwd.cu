@@ -1015,8 +1015,10 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       else
         for (int bx = 0; bx < nbox; ++bx)
           tc::tma_load_2d(sa + 2 * A_BYTES + bx * (64 * BK * 2), tB, ld, j0 + bx * 64, (int)rb);
-      if (gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + (size_t)vtile * p.g.R + rb, gbytes, ld);
-      if (two && gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + (size_t)(vtile + 1) * p.g.R + rb, gbytes, ld);
+      // (plain mode: tile 0's scalars are every tile's, and the only ones pruned_combine writes)
+      const size_t gt0 = plain ? 0 : (size_t)vtile, gt1 = plain ? 0 : (size_t)(vtile + 1);
+      if (gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + gt0 * p.g.R + rb, gbytes, ld);
+      if (two && gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES + G_BYTES, p.g.gpk + gt1 * p.g.R + rb, gbytes, ld);
       if (++stage == STAGES) { stage = 0; ph ^= 1; }
     }
   } else if (lane == 1 && nkb > 0) {

@@ -622,9 +622,12 @@ __global__ void pruned_combine_kernel(const float* __restrict__ px2, const float
   gb[r] = bb;
   gl[r] = yb;
   // packed per (V tile, row) operand scalars of the joiner backward (joiner_bwd.cu):
-  // {gs (g_b + g_l) exp(m_tile - lse), gs g_b, gs g_l, label}; dead rows {0, 0, 0, -1}
+  // {gs (g_b + g_l) exp(m_tile - lse), gs g_b, gs g_l, label}; dead rows {0, 0, 0, -1}.  With one P~
+  // offset per row (plain mode, D20) every tile's entry is tile 0's and only tile 0's is read (c4: 63
+  // tiles x 160k rows of 16 B and an expf each were 220 us of this kernel)
   const float l = lse[r];
-  for (int tl = 0; tl < ntile; ++tl) {
+  const int ntw = *tscale == 0 ? 1 : ntile;
+  for (int tl = 0; tl < ntw; ++tl) {
     float4 qv = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
     if (info >= 0) qv = make_float4(gs * (bb + yb) * expf(mt[r * ntile + tl] - l), gs * bb, gs * yb, __int_as_float(info));
     gpk[(size_t)tl * R + r] = qv;

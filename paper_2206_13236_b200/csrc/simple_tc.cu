@@ -236,10 +236,13 @@ struct PrepParams {
   int rowblk;   // 1: one block per am / lm row (exp_split_row_block<8>), else 8 rows per block
 };
 
+// ROWBLK: the large-V row form (its 32-float4 register row would otherwise set the register budget, and so
+// the occupancy, of the warp-per-row form too: c5 prep 29 -> 34 us)
+template <bool ROWBLK>
 __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   int b = blockIdx.x;
-  if (p.rowblk) {
+  if (ROWBLK) {
     if (b < p.nb_am) {
       exp_split_row_block<8>(p.am, p.sym, p.bnd, p.T, p.U, p.V, p.VP, 0, p.m_am, p.eam_hi, p.eam_lo, p.amy, p.UP,
                              nullptr, b);
@@ -1097,7 +1100,8 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   p.nb_lm = (int)(p.rowblk ? (long long)d.N * d.U1() : ((long long)d.N * d.U1() + 7) / 8);
   p.nb_fill = (int)(((long long)d.N * (d.K() + 1) + 7) / 8);
   const unsigned grid = (unsigned)(p.nb_am + p.nb_lm + p.nb_fill + d.N);
-  RNNT_LAUNCH(KID_ROWMAX_AM, st, launch_pdl(simple_prep_kernel, grid, 256, 0, st, p));
+  if (p.rowblk) RNNT_LAUNCH(KID_ROWMAX_AM, st, launch_pdl(simple_prep_kernel<true>, grid, 256, 0, st, p));
+  else RNNT_LAUNCH(KID_ROWMAX_AM, st, launch_pdl(simple_prep_kernel<false>, grid, 256, 0, st, p));
   return cudaGetLastError();
 }
 

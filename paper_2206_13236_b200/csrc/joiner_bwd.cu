@@ -796,7 +796,7 @@ constexpr int THREADS = 288;
 __global__ void __launch_bounds__(jdw2::THREADS, 1)
     joiner_dw_wide_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmH,
                           const __grid_constant__ CUtensorMap tmHs, const __grid_constant__ CUtensorMap tmP1,
-                          JoinerDwParams p) {
+                          const __grid_constant__ CUtensorMap tmO, JoinerDwParams p) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
   using namespace jdw2;
   extern __shared__ uint8_t smem_raw[];
@@ -952,28 +952,41 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
       for (int gg = 0; gg < 8; ++gg) s += dbs[gg * 256 + v];
       if (v0 + v < V) p.dbp[(size_t)split * V + v0 + v] = s;
     }
-    // ---- epilogue: accumulator a -> dWp[split] rows va + t
+    // ---- epilogue: accumulator a -> dWp[split] rows va .. va + 127: per 32-column chunk the group's 128
+    // threads stage their rows in a swizzled 16 KB tile (two per group, in the now idle stage buffers) and
+    // one thread TMA-stores it (rows past V / columns past J clipped by the map); the per-row float4 stores
+    // this replaces were a quarter of the kernel's stall samples at c5 (32 scattered rows per instruction)
     if (nkb > 0) {
       tc::mbar_wait(tfull, 0);
       tc::fence_after_sync();
     }
-    const int v = va + t;
-    const uint32_t tl = tbase + (uint32_t)(a * 256) + ((uint32_t)(32 * (warp & 3)) << 16);
-    for (int c0 = 0; c0 < nj; c0 += 32) {
-      float acc[32];
-      if (nkb > 0) {
-        tc::tmem_ld32(tl + c0, acc);
-      } else {
+    if (mine) {
+      const uint32_t tl = tbase + (uint32_t)(a * 256) + ((uint32_t)(32 * (warp & 3)) << 16);
+      const bool st_leader = (threadIdx.x & 127) == 0;
+      int kc = 0;
+      for (int c0 = 0; c0 < nj; c0 += 32, ++kc) {
+        float acc[32];
+        if (nkb > 0) {
+          tc::tmem_ld32(tl + c0, acc);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-      }
-      if (v < V) {
-        float4* o = reinterpret_cast<float4*>(p.dWp + ((size_t)split * V + v) * p.J + j0 + c0);
-        const int n4 = min(8, (nj - c0) / 4);
+          for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        }
+        uint8_t* ob = smem + (a * 2 + (kc & 1)) * (BM * 32 * 4);
+        if (st_leader && kc >= 2) tc::bulk_wait_read1();   // the store issued from this tile 2 chunks ago
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + a) : "memory");
+        float4* O4 = reinterpret_cast<float4*>(ob);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (q < n4) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+          O4[t * 8 + (q ^ (t & 7))] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        tc::fence_proxy_async();
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + a) : "memory");
+        if (st_leader) {
+          tc::tma_store_3d(&tmO, ob, j0 + c0, va, split);
+          tc::bulk_commit();
+        }
       }
+      if (st_leader) tc::bulk_wait0();
     }
   } else if (lane == 0 && nkb > 0) {
     // ---- warp 8 lane 0: TMA for both P~ tiles, the h (precomputed plain: Hs) k-block and the two tiles'
@@ -1194,6 +1207,9 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
                     : !make_tmap_bf16_2d(&ths, Hs, d.J, d.rows(), (uint64_t)d.J * 2, 64, 64)))
       return cudaErrorInvalidValue;
     p.hsmem = Hs ? 0 : 1;
+    CUtensorMap to;   // the split partials dWp (splits, V, J) fp32, box 32 columns x 128 rows
+    if (!make_tmap_f32_3d(&to, dWp, d.J, d.V, splits, (uint64_t)d.J * 4, (uint64_t)d.V * d.J * 4, 32, jdw2::BM))
+      return cudaErrorInvalidValue;
     // P~ multicast over the J parts (RNNT_DW_MC=1: on): clusters of njp CTAs along grid x (j first)
     const int njp = (d.J + jdw2::BN - 1) / jdw2::BN;
     static const int mc_env = env_int("RNNT_DW_MC", 0);   // measured slower: off by default
@@ -1225,10 +1241,10 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
       cfg.attrs = at;
       cfg.numAttrs = 2;
-      RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_wide_kernel, tp3, p.h3 ? th3 : th, ths, tp1, p));
+      RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_wide_kernel, tp3, p.h3 ? th3 : th, ths, tp1, to, p));
     } else {
       RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3,
-                                         p.h3 ? th3 : th, ths, tp1, p));
+                                         p.h3 ? th3 : th, ths, tp1, to, p));
     }
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);

@@ -548,6 +548,7 @@ struct JoinerDwParams {
   int h3 = 0;               // wide variant: tmH is the 3-D (64 j, rows, J/64) map (J % 64 == 0)
   int hsmem = 0;            // plain mode: Hs = bf16(sc h) formed in shared memory (else the precomputed Hs map)
   int mc = 0;               // wide variant: P~ multicast over clusters of this many J-part siblings (0/1: off)
+  int pair_plain = 0;       // wide variant: the plain mode is left to joiner_dw_pair_kernel (it runs only then)
 };
 
 
@@ -821,6 +822,7 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   const int nbox = (nj + 63) / 64;
   const int vtile = v0 >> 7;
   const bool plain = p.tscale && *p.tscale == 0;
+  if (plain && p.pair_plain) return;      // the pair kernel (launched alongside) does the plain mode
   const bool hsm = plain && p.hsmem;      // Hs formed in shared memory
   const bool dbread = plain && !hsm && bjy == 0;   // precomputed Hs: the d_b readers release the stage too
   // P~ multicast (p.mc = the cluster size along x = the J parts of one (V pair, split)): each sibling
@@ -1061,6 +1063,211 @@ __global__ void __launch_bounds__(jdw2::THREADS, 1)
   if (warp == 8) tc::tmem_dealloc(tbase, 512);
 }
 
+// K11, CTA-pair variant for the plain mode with a precomputed Hs (large V, D20): a pair (cta_group::2,
+// cluster of 2) computes a 512 (v) x 256 (j) partial dW tile as two 256 x 256 accumulators, CTA r holding
+// the TMEM lanes of V tiles v0 + 128 r and v0 + 256 + 128 r (512 TMEM columns: both accumulators); each
+// k-block (64 rows) every CTA loads its two 128-v P~ tiles and HALF of the 256 Hs columns, so the L2 -> SM
+// bytes per MMA flop drop from 64 KB to 48 KB per 2 x 128x256x64 (the wide kernel, the L2 throughput cap
+// at V = 8000: 0.56 of the bf16 burst peak).  The MMA consumes the TMA'd stages directly (no producer
+// transforms, so the pair needs no per-stage handshake beyond the TMA bytes landing on the leader's
+// barrier).  d_b (J part 0 only): each CTA's warps sum sc_r P~'[r,v] of their tiles; there the P~ tiles are
+// loaded per CTA (local barrier) and a relay thread forwards their arrival to the leader's barrier.
+namespace jdwp {
+constexpr int BM = 128, BNH = 128, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;                   // one V tile: 2 planes of 64 v x 64 rows
+constexpr int B_BYTES = BNH * BK * 2;                  // this CTA's half of the 256 Hs columns: 2 planes
+constexpr int G_BYTES = 1024;                          // the k-block's row scalars (64 x 16 B)
+constexpr int STAGE_BYTES = 2 * A_BYTES + B_BYTES + G_BYTES;   // 49 KB (1024-aligned)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + 8 * 256 * 4;
+constexpr int THREADS = 288;
+}  // namespace jdwp
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jdwp::THREADS, 1)
+    joiner_dw_pair_kernel(const __grid_constant__ CUtensorMap tmP, const __grid_constant__ CUtensorMap tmHs,
+                          const __grid_constant__ CUtensorMap tmO, JoinerDwParams p) {
+  RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
+  using namespace jdwp;
+  if (*p.tscale != 0) return;             // the rescaling mode: the wide kernel (launched alongside) does it
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = tc::align1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);   // leader: MMA may start
+  uint64_t* empty = full + STAGES;        // this CTA's stage may be refilled
+  uint64_t* aload = empty + STAGES;       // d_b pairs: this CTA's P~ tiles + scalars landed (local)
+  uint64_t* tfull = aload + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* dbs = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);     // [8 row groups][256 v]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int quad = blockIdx.x >> 1, bjy = blockIdx.y, split = blockIdx.z;
+  const int v0 = quad * 4 * BM;
+  const int va0 = v0 + (int)rank * BM, va1 = v0 + 2 * BM + (int)rank * BM;   // this CTA's two V tiles
+  const int j0 = bjy * 2 * BNH, jh = j0 + (int)rank * BNH;                  // the pair's j part, this half
+  const DwRange kr = dw_range(p, split, (int)gridDim.z);
+  const long long kb0 = kr.kb0;
+  const int nkb = kr.nkb;
+  const int V = p.g.V;
+  const bool two = v0 + 2 * BM < V;       // the second accumulator's tiles exist (pair-uniform)
+  const int nj = min(2 * BNH, p.J - j0);
+  const bool dbp = bjy == 0;              // d_b pair: local P~ loads + relay
+  if (warp == 8 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], dbp ? 3 : 1);      // d_b pairs: the leader's expect-tx + both CTAs' relays
+      tc::mbar_init(&empty[s], dbp ? 9 : 1);     // the leader's MMA commit (+ the 8 d_b warps)
+      tc::mbar_init(&aload[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch(&tmP);
+    tc::tma_prefetch(&tmHs);
+  }
+  if (warp == 8) tc::tmem_alloc2(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();                     // the peer's barriers are initialised before any remote signal
+  tc::fence_after_sync();
+  const uint32_t tbase = *tmem_slot;
+  const uint32_t fullL = tc::mapa(&full[0], 0);
+
+  if (warp < 8) {
+    const int a = warp >> 2;                 // accumulator / V tile 0 / 1 of this CTA
+    const int t = threadIdx.x & 127;
+    const int c = t & 15;                    // 8-v chunk 0..15
+    const int g8 = t >> 4;                   // row group 0..7
+    const bool mine = a == 0 || two;
+    const int va = a == 0 ? va0 : va1;
+    if (dbp) {
+      float dsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const long long rb = dw_row0(p, kb0 + kb);
+        const int grows = dw_rows(p, rb);
+        tc::mbar_wait(&aload[stage], ph);
+        if (mine) {   // d_b: sum sc_r P~'[r, v] over the k-block's rows (no smem writes)
+          const uint8_t* sa = smem + stage * STAGE_BYTES + a * A_BYTES;
+          const float4* gq = reinterpret_cast<const float4*>(smem + stage * STAGE_BYTES + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rl = g8 + 8 * i;
+            const float sc = rl < grows ? gq[rl].x : 0.f;
+            const uint4 pv = *reinterpret_cast<const uint4*>(sa + (c >> 3) * (64 * BK * 2) + sw128(rl, c & 7));
+            const uint32_t w[4] = {pv.x, pv.y, pv.z, pv.w};
+            if (sc != 0.f) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                dsum[2 * k] += sc * __uint_as_float(w[k] << 16);
+                dsum[2 * k + 1] += sc * __uint_as_float(w[k] & 0xffff0000u);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[stage]);   // this warp is done reading the stage
+        if (++stage == STAGES) { stage = 0; ph ^= 1; }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dbs[g8 * 256 + a * 128 + c * 8 + j] = dsum[j];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int tv = threadIdx.x;   // 0..255: tile tv / 128, row tv % 128
+      float sacc = 0.f;
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg) sacc += dbs[gg * 256 + tv];
+      const int vv = (tv < 128 ? va0 : va1) + (tv & 127);
+      if (vv < V && (tv < 128 || two)) p.dbp[(size_t)split * V + vv] = sacc;
+    }
+    // ---- epilogue: this CTA's accumulator lanes -> dWp[split] rows va.., one TMA store per 32 columns
+    if (nkb > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    if (mine) {
+      const uint32_t tl = tbase + (uint32_t)(a * 256) + ((uint32_t)(32 * (warp & 3)) << 16);
+      const bool st_leader = (threadIdx.x & 127) == 0;
+      int kc = 0;
+      for (int c0 = 0; c0 < nj; c0 += 32, ++kc) {
+        float acc[32];
+        if (nkb > 0) {
+          tc::tmem_ld32(tl + c0, acc);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        }
+        uint8_t* ob = smem + (a * 2 + (kc & 1)) * (BM * 32 * 4);
+        if (st_leader && kc >= 2) tc::bulk_wait_read1();
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + a) : "memory");
+        float4* O4 = reinterpret_cast<float4*>(ob);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          O4[t * 8 + (q ^ (t & 7))] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+        tc::fence_proxy_async();
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + a) : "memory");
+        if (st_leader) {
+          tc::tma_store_3d(&tmO, ob, j0 + c0, va, split);
+          tc::bulk_commit();
+        }
+      }
+      if (st_leader) tc::bulk_wait0();
+    }
+  } else if (lane == 0 && nkb > 0) {
+    // ---- warp 8 lane 0: TMA (P~ tiles: 2sm, or local for d_b pairs; the Hs half: 2sm; scalars: local)
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const long long rb = dw_row0(p, kb0 + kb);
+      const uint32_t gbytes = dbp ? (uint32_t)dw_rows(p, rb) * 16u : 0u;
+      tc::mbar_wait(&empty[stage], ph ^ 1);
+      uint8_t* sa = smem + stage * STAGE_BYTES;
+      const uint32_t fb = fullL + stage * 8;
+      if (dbp) {
+        if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2u * B_BYTES);
+        tc::mbar_arrive_expect_tx(&aload[stage], (two ? 2u : 1u) * A_BYTES + gbytes);
+        tc::tma_load_3d(sa, &tmP, &aload[stage], 0, (int)rb, va0 / 64);
+        if (two) tc::tma_load_3d(sa + A_BYTES, &tmP, &aload[stage], 0, (int)rb, va1 / 64);
+        if (gbytes) tc::bulk_load(sa + 2 * A_BYTES + B_BYTES, p.g.gpk + rb, gbytes, &aload[stage]);
+      } else {
+        if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2u * ((two ? 2u : 1u) * A_BYTES + B_BYTES));
+        tc::tma_load_3d_2sm(sa, &tmP, fb, 0, (int)rb, va0 / 64);
+        if (two) tc::tma_load_3d_2sm(sa + A_BYTES, &tmP, fb, 0, (int)rb, va1 / 64);
+      }
+      tc::tma_load_3d_2sm(sa + 2 * A_BYTES, &tmHs, fb, 0, (int)rb, jh / 64);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (lane == 1 && nkb > 0 && dbp) {
+    // ---- warp 8 lane 1 (d_b pairs): relay "this CTA's P~ tiles landed" to the leader's full barrier
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait(&aload[stage], ph);
+      tc::mbar_arrive_cluster(fullL + stage * 8);
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+  } else if (lane == 2 && nkb > 0 && leader) {
+    // ---- warp 8 lane 2 of the leader: the pair's MMAs, two 256x256x16 per k-step sharing the Hs descriptor
+    constexpr uint32_t idesc = tc::idesc_bf16(2 * BM, 2 * BNH, true, true);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      tc::mbar_wait_cluster(&full[stage], ph);
+      tc::fence_after_sync();
+      const uint32_t a = tc::smem_u32(smem + stage * STAGE_BYTES), b = a + 2 * A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        const uint64_t db = tc::sdesc(b + 2048 * k, 64 * BK * 2, 1024);
+        tc::mma2_bf16(tbase, tc::sdesc(a + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
+        if (two) tc::mma2_bf16(tbase + 256, tc::sdesc(a + A_BYTES + 2048 * k, 64 * BK * 2, 1024), db, idesc, (kb | k) != 0);
+      }
+      tc::mma2_commit(&empty[stage], 3);   // releases the stage in both CTAs
+      if (++stage == STAGES) { stage = 0; ph ^= 1; }
+    }
+    tc::mma2_commit(tfull, 3);
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::cluster_sync();                     // the peer's smem / TMEM stay alive until the pair is done
+  if (warp == 8) tc::tmem_dealloc2(tbase, 512);
+}
+
 // ======================================================================= host
 template <int NTW, bool MC, bool D16>
 static cudaError_t launch_dh_k(const JoinerDhParams& p, unsigned grid, const CUtensorMap& tp, const CUtensorMap& tw,
@@ -1225,6 +1432,23 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
     if (pfmode >= 0) p.pfmode = pfmode;
     if (p.mc > 1) p.pfmode |= 2;           // (clusters run along grid x: the J parts first)
     dim3 grid((unsigned)((vt + 1) / 2), (d.J + jdw2::BN - 1) / jdw2::BN, splits);
+    // plain mode with a precomputed Hs: the CTA-pair kernel (RNNT_DW_PAIR2=0: off); the wide kernel then
+    // only runs if the forward switched to per-tile rescaling (both decide on the device-side tscale)
+    // measured: c4 (V = 8000, J = 768) 1.81 vs 1.93 ms in the step, c3 (V = 5000, J = 512) 274 vs 254 us
+    // standalone, so by default only from V >= 6144 (RNNT_DW_PAIR2=1 / 0: always / never)
+    static const int pair2 = env_int("RNNT_DW_PAIR2", -1);
+    const bool use_pair = pair2 == 1 || (pair2 < 0 && d.V >= 6144);
+    if (Hs && tscale && use_pair && p.mc <= 1 && d.J % 64 == 0) {   // (3-D Hs boxes)
+      smem_optin(joiner_dw_pair_kernel, jdwp::SMEM_BYTES);
+      CUtensorMap tpp, thp;
+      if (!make_tmap_bf16_3d(&tpp, g.Pt, 64, d.rows(), d.VP() / 64, (uint64_t)d.VP() * 2, 128, 64, jdwp::BK, 2) ||
+          !make_tmap_bf16_3d(&thp, Hs, 64, d.rows(), (d.J + 63) / 64, (uint64_t)d.J * 2, 128, 64, jdwp::BK, 2))
+        return cudaErrorInvalidValue;
+      p.pair_plain = 1;
+      const unsigned quads = (unsigned)((vt + 3) / 4);
+      dim3 pg(2 * quads, (d.J + 2 * jdwp::BNH - 1) / (2 * jdwp::BNH), splits);
+      RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_pair_kernel, pg, jdwp::THREADS, jdwp::SMEM_BYTES, st, tpp, thp, to, p));
+    }
     if (p.pfmode & 2) std::swap(grid.x, grid.y);
     if (p.mc > 1) {
       cudaLaunchConfig_t cfg = {};
@@ -1243,8 +1467,10 @@ cudaError_t joiner_dw_launch(const Dims& d, const GradSrc& g, const uint16_t* h,
       cfg.numAttrs = 2;
       RNNT_LAUNCH(KID_DW, st, cudaLaunchKernelEx(&cfg, joiner_dw_wide_kernel, tp3, p.h3 ? th3 : th, ths, tp1, to, p));
     } else {
-      RNNT_LAUNCH(KID_DW, st, launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3,
-                                         p.h3 ? th3 : th, ths, tp1, to, p));
+      // (with the pair kernel this launch only works in the rescaling mode: profiled under another id)
+      RNNT_LAUNCH(p.pair_plain ? KID_DB : KID_DW, st,
+                  launch_pdl(joiner_dw_wide_kernel, grid, jdw2::THREADS, jdw2::SMEM_BYTES, st, tp3, p.h3 ? th3 : th, ths,
+                             tp1, to, p));
     }
   } else if (pair) {
     smem_optin(joiner_dw_tc_kernel<true>, jdw::Cfg<true>::SMEM_BYTES);

@@ -44,8 +44,8 @@ def _check(b, want_plain):
         assert_bf16_grad(got[k], ref[k], k)
 
 
-def _spiked(v_spike, value=80.0, V=400):
-    b = synth.make_custom([60, 41, 17], [20, 12, 16], V, 32, 5, seed=41, logit_scale=2.0)
+def _spiked(v_spike, value=80.0, V=400, J=32):
+    b = synth.make_custom([60, 41, 17], [20, 12, 16], V, J, 5, seed=41, logit_scale=2.0)
     if v_spike is not None:
         b.b_out_bits = b.b_out_bits.copy()
         b.b_out_bits[v_spike] = f32_to_bf16_bits(np.array([value], np.float32))[0]
@@ -74,3 +74,16 @@ def test_c2_shard_plain():
     """A 4-utterance shard of config 2 (V = 500, J = 512): the bench workload's shapes."""
     from test_gpu_guards import _sub
     _check(_sub(synth.make_batch(2), [0, 1, 2, 3]), True)
+
+
+@pytest.mark.parametrize("J", [64, 32])
+def test_large_v_plain(J):
+    """V >= 6144: the precomputed Hs and (J % 64 == 0) the CTA-pair d_w kernel; J = 32: the wide kernel."""
+    _check(_spiked(None, V=6500, J=J), True)
+
+
+@pytest.mark.parametrize("J", [64, 32])
+def test_large_v_rescale(J):
+    """V >= 6144 with a spike beyond the reference columns: the wide kernel's rescaling mode (the pair
+    kernel, launched alongside, must leave it alone)."""
+    _check(_spiked(5000, V=6500, J=J), False)

@@ -275,6 +275,8 @@ struct ScanParams {
   int G;             // CTAs per (utterance, direction): a thread-block cluster sharing the chunk work
   int staged;        // 1: the utterance's arcs and bounds are staged in shared memory (T S 8 + T 4 bytes
                      // fit); 0 (long utterances): every phase reads them from global memory (L2)
+  int prefix;        // 1: phase B as a parallel (Hillis-Steele) prefix of the chunk matrices over the whole
+                     // rank-0 CTA instead of a chain of nc vector-matrix steps (small S)
 };
 
 // SMAX: register rows per lane; SC: the band width S as a compile-time constant (0: runtime S <= SMAX),
@@ -313,6 +315,11 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   float* PXs = reinterpret_cast<float*>(smem_raw + mat_bytes + (size_t)(q.ncmax + 1) * 8);
   float* PYs = PXs + (size_t)q.T * S;
   int* prs = reinterpret_cast<int*>(PYs + (size_t)q.T * S);
+  // phase B prefix buffers (q.prefix): a second set of nc S x S matrices and two fp64 shift arrays, after the
+  // staged arcs and bounds (or straight after the chunk data when nothing is staged)
+  unsigned char* pfx_base = q.staged ? reinterpret_cast<unsigned char*>(prs + q.T)
+                                     : reinterpret_cast<unsigned char*>(PXs);
+  pfx_base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(pfx_base) + 15) & ~uintptr_t(15));
   const size_t rb = (size_t)n * q.T * S;
   if (q.staged) {
     const int m = Tn * S;
@@ -451,58 +458,127 @@ __global__ void __launch_bounds__(256) pruned_scan_kernel(ScanParams q) {
   else __syncthreads();
   scan_trace(2);
 
-  // ---------------- phase B: boundary vectors (rank 0, warp 0, segment 0)
-  if (warp == 0 && rank == 0) {
-    const bool sa = lane < S;
-    float a = NB;
-    if (fwd) {
-      // frame 0: alpha(0,0) = 0, then the vertical chain
-      a = (s == 0) ? 0.f : NB;
-      const float own_px = sa ? PX[s] : NB;
-      for (int j = 1; j < S; ++j) {
-        const float v = __shfl_up_sync(0xffffffffu, a + own_px, 1);
-        if (lane == j) a = v;
+  // ---------------- phase B: boundary vectors (rank 0)
+  // a_0 (frame 0 / T-1) by warp 0; then either warp 0 chains a_{c+1} = M_c (x) a_c over the nc chunks, or
+  // (q.prefix) the whole CTA forms the prefix products Q_c = M_c (x) ... (x) M_0 in log2(nc) Hillis-Steele
+  // rounds (Q_c <- Q_c (x) Q_{c-d}, every entry a log-sum-exp over S terms) and a_{c+1} = Q_c (x) a_0 --
+  // the chain was ~0.27 us per chunk (c5: 11 of the scan's 27 us).  The prefix entries are not rebased
+  // (relative to the summed chunk shifts they stay within a few hundred log2 units); phase C rebases
+  // every frame as before.
+  if (rank == 0) {
+    if (warp == 0) {
+      const bool sa = lane < S;
+      float a = NB;
+      if (fwd) {
+        // frame 0: alpha(0,0) = 0, then the vertical chain
+        a = (s == 0) ? 0.f : NB;
+        const float own_px = sa ? PX[s] : NB;
+        for (int j = 1; j < S; ++j) {
+          const float v = __shfl_up_sync(0xffffffffu, a + own_px, 1);
+          if (lane == j) a = v;
+        }
+      } else {
+        // frame T-1: the terminal blank at slot sU, then the chain downwards
+        const size_t o = (size_t)(Tn - 1) * S + s;
+        const float own_px = sa ? PX[o] : NB;
+        a = (sa && s == sU) ? PY[o] : NB;
+        for (int j = S - 2; j >= 0; --j) {
+          const float v = __shfl_down_sync(0xffffffffu, a, 1);
+          if (lane == j) a = lae2(a, v + own_px);
+        }
       }
-    } else {
-      // frame T-1: the terminal blank at slot sU, then the chain downwards
-      const size_t o = (size_t)(Tn - 1) * S + s;
-      const float own_px = sa ? PX[o] : NB;
-      a = (sa && s == sU) ? PY[o] : NB;
-      for (int j = S - 2; j >= 0; --j) {
-        const float v = __shfl_down_sync(0xffffffffu, a, 1);
-        if (lane == j) a = lae2(a, v + own_px);
+      double sh = 0.0;
+      if (sa) bv[s] = a;
+      if (lane == 0) bsh[0] = 0.0;
+      if (!q.prefix) {
+        const long long ck0 = clock64();
+        for (int c = 0; c < nc; ++c) {
+          // reconverge the warp every step: after the lane-predicated stores (and the divergent set-up
+          // above) the warp otherwise stays split and every shuffle takes the diverged path (measured
+          // 3519 -> 538 cycles per step at c4)
+          __syncwarp();
+          const float m = rebase_of(__shfl_sync(0xffffffffu, a, 0));
+          const float* Pc = Pm + ((size_t)c * S + (sa ? s : 0)) * S;
+          float mx = NB, x[KR];
+#pragma unroll
+          for (int k = 0; k < KR; ++k) {
+            const float ak = __shfl_sync(0xffffffffu, a, k < S ? k : 0);
+            x[k] = (k < S && sa) ? (ak - m) + Pc[k] : NB;
+            mx = fmaxf(mx, x[k]);
+          }
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < KR; ++k)
+            if (k < S) acc += ex2_approx(x[k] - mx);
+          a = mx + lg2_approx(acc);
+          sh += (double)m + (double)psh[c];
+          if (sa) bv[(c + 1) * S + s] = a;
+          if (lane == 0) bsh[c + 1] = sh;
+        }
+        if (g_scan_trace && lane == 0) {
+          g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 5] = (unsigned long long)(clock64() - ck0);
+          g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 6] = (unsigned long long)nc;
+        }
       }
     }
-    double sh = 0.0;
-    if (sa) bv[s] = a;
-    if (lane == 0) bsh[0] = 0.0;
-    const long long ck0 = clock64();
-    for (int c = 0; c < nc; ++c) {
-      // reconverge the warp every step: after the lane-predicated stores (and the divergent set-up
-      // above) the warp otherwise stays split and every shuffle takes the diverged path (measured
-      // 3519 -> 538 cycles per step at c4)
-      __syncwarp();
-      const float m = rebase_of(__shfl_sync(0xffffffffu, a, 0));
-      const float* Pc = Pm + ((size_t)c * S + (sa ? s : 0)) * S;
-      float mx = NB, x[KR];
+    if (q.prefix) {
+      __syncthreads();                                   // a_0 in bv[0 .. S)
+      float* Qa = Pm;
+      float* Qb = reinterpret_cast<float*>(pfx_base);
+      double* ha = reinterpret_cast<double*>(
+          (reinterpret_cast<uintptr_t>(Qb + (size_t)q.ncmax * S * S) + 15) & ~uintptr_t(15));
+      double* hb = ha + q.ncmax;
+      const int SS = S * S, tid = threadIdx.x, nthr = blockDim.x;
+      for (int c = tid; c < nc; c += nthr) ha[c] = (double)psh[c];
+      __syncthreads();
+      for (int dd = 1; dd < nc; dd <<= 1) {
+        for (int e = tid; e < nc * SS; e += nthr) {
+          const int c = e / SS, r = e - c * SS, sr = r / S, k = r - sr * S;
+          if (c >= dd) {                                 // (Q_c (x) Q_{c-dd})[sr][k]
+            const float* A = Qa + (size_t)c * SS + sr * S;
+            const float* B = Qa + (size_t)(c - dd) * SS + k;
+            float x[KR], mx = NB;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const float ak = __shfl_sync(0xffffffffu, a, k < S ? k : 0);
-        x[k] = (k < S && sa) ? (ak - m) + Pc[k] : NB;
-        mx = fmaxf(mx, x[k]);
+            for (int j = 0; j < KR; ++j) {
+              if (SC == 0 && j >= S) break;
+              x[j] = A[j] + B[j * S];
+              mx = fmaxf(mx, x[j]);
+            }
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j < KR; ++j) {
+              if (SC == 0 && j >= S) break;
+              acc += ex2_approx(x[j] - mx);
+            }
+            Qb[e] = mx + lg2_approx(acc);
+          } else {
+            Qb[e] = Qa[e];
+          }
+        }
+        for (int c = tid; c < nc; c += nthr) hb[c] = c >= dd ? ha[c] + ha[c - dd] : ha[c];
+        __syncthreads();
+        float* tq = Qa; Qa = Qb; Qb = tq;
+        double* th = ha; ha = hb; hb = th;
       }
-      float acc = 0.f;
+      for (int e = tid; e < nc * S; e += nthr) {         // a_{c+1} = Q_c (x) a_0
+        const int c = e / S, sr = e - c * S;
+        const float* Q = Qa + (size_t)c * SS + sr * S;
+        float x[KR], mx = NB;
 #pragma unroll
-      for (int k = 0; k < KR; ++k)
-        if (k < S) acc += ex2_approx(x[k] - mx);
-      a = mx + lg2_approx(acc);
-      sh += (double)m + (double)psh[c];
-      if (sa) bv[(c + 1) * S + s] = a;
-      if (lane == 0) bsh[c + 1] = sh;
-    }
-    if (g_scan_trace && lane == 0) {
-      g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 5] = (unsigned long long)(clock64() - ck0);
-      g_scan_trace[((size_t)n * 2 + blockIdx.y) * 8 + 6] = (unsigned long long)nc;
+        for (int k = 0; k < KR; ++k) {
+          if (SC == 0 && k >= S) break;
+          x[k] = Q[k] + bv[k];
+          mx = fmaxf(mx, x[k]);
+        }
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          if (SC == 0 && k >= S) break;
+          acc += ex2_approx(x[k] - mx);
+        }
+        bv[(size_t)(c + 1) * S + sr] = mx + lg2_approx(acc);
+        if (sr == 0) bsh[c + 1] = ha[c];
+      }
     }
   }
   if (G > 1) tc::cluster_sync();        // the boundary vectors are visible to every rank
@@ -710,12 +786,21 @@ static int scan_chunk(const Dims& d) {
   return C;
 }
 // chunk matrices + the staged arcs (2 T S floats) and bounds (T ints)
+static long long scan_prefix_bytes(const Dims& d);
 static bool scan_staged(const Dims& d) {
-  return scan_mat_bytes(d, scan_chunk(d)) + (long long)d.T * d.S * 8 + (long long)d.T * 4 <= 200 * 1024;
+  return scan_mat_bytes(d, scan_chunk(d)) + (long long)d.T * d.S * 8 + (long long)d.T * 4 + scan_prefix_bytes(d) <=
+         200 * 1024;
+}
+// phase B as a parallel prefix for narrow bands (c5 / c3: S = 5); wide bands keep the chain (the prefix's
+// S^2 log-sum-exps per matrix and round outgrow it)
+static bool scan_prefix(const Dims& d) { return d.S <= 8; }
+static long long scan_prefix_bytes(const Dims& d) {
+  const long long nc = (d.T + scan_chunk(d) - 1) / scan_chunk(d) + 1;
+  return scan_prefix(d) ? 16 + nc * d.S * d.S * 4 + 16 + 2 * nc * 8 : 0;   // (16-B alignment of both parts)
 }
 size_t pruned_recursion_smem(const Dims& d) {
   const long long mat = scan_mat_bytes(d, scan_chunk(d));
-  return (size_t)(scan_staged(d) ? mat + (long long)d.T * d.S * 8 + (long long)d.T * 4 : mat);
+  return (size_t)((scan_staged(d) ? mat + (long long)d.T * d.S * 8 + (long long)d.T * 4 : mat) + scan_prefix_bytes(d));
 }
 
 template <int SMAX, int SC>
@@ -769,7 +854,7 @@ cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* 
     const size_t sm = pruned_recursion_smem(d);
     const int C = scan_chunk(d);
     ScanParams q{w.px2, w.py2, ranges, bnd, d.T, d.S, C, (d.T + C - 1) / C + 1, w.ap, w.bp, w.Af, w.Bf, w.Lp, loss,
-                 status, scan_cluster(d), scan_staged(d) ? 1 : 0};
+                 status, scan_cluster(d), scan_staged(d) ? 1 : 0, scan_prefix(d) ? 1 : 0};
     switch (d.S) {   // band widths of the BASELINE configs (and the tests) get a compile-time S
       case 2: e = launch_scan<2, 2>(d, q, sm, st); break;
       case 3: e = launch_scan<3, 3>(d, q, sm, st); break;

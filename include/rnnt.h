@@ -229,6 +229,23 @@ rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out,
                                        const int64_t* boundary, const rnnt_dims_t* dims,
                                        float grad_scale, float* loss, int32_t* status, void* workspace,
                                        size_t workspace_bytes, void* stream);
+/*
+ * rnnt_pruned_loss_forward split in two so that its first step can overlap the gather (rnnt_prune): it
+ * does not read h.  rnnt_pruned_loss_prepare (ranges, symbols, boundary, b_out, grad_scale -> per band row
+ * label info, the frames covering each token position, the fp32 bias and its tile maxima, the live
+ * 128-row tiles, the loss scale; all in the workspace) followed in stream order by
+ * rnnt_pruned_loss_forward_prepared (the same arguments as rnnt_pruned_loss_forward; grad_scale must be
+ * the prepare call's) computes exactly what rnnt_pruned_loss_forward computes.
+ * Same argument rules and errors as rnnt_pruned_loss_forward; the workspace is the pruned region.
+ */
+rnnt_status_t rnnt_pruned_loss_prepare(const int32_t* ranges, const int64_t* symbols, const int64_t* boundary,
+                                       const rnnt_dims_t* dims, const uint16_t* b_out, float grad_scale,
+                                       void* workspace, size_t workspace_bytes, void* stream);
+rnnt_status_t rnnt_pruned_loss_forward_prepared(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                                                const int64_t* symbols, const int32_t* ranges,
+                                                const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                                                float* loss, int32_t* status, void* workspace,
+                                                size_t workspace_bytes, void* stream);
 rnnt_status_t rnnt_pruned_loss_backward_input(const uint16_t* h, const uint16_t* w_out,
                                               const int32_t* ranges, const int64_t* boundary,
                                               const rnnt_dims_t* dims, float* d_enc, float* d_dec,

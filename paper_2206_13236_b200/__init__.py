@@ -89,6 +89,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.rnnt_pruned_loss.restype = I32
     lib.rnnt_pruned_loss_forward.argtypes = [P, P, P, P, P, P, DP, F, P, P, P, SZ, P]
     lib.rnnt_pruned_loss_forward.restype = I32
+    lib.rnnt_pruned_loss_prepare.argtypes = [P, P, P, DP, P, F, P, SZ, P]
+    lib.rnnt_pruned_loss_prepare.restype = I32
+    lib.rnnt_pruned_loss_forward_prepared.argtypes = lib.rnnt_pruned_loss_forward.argtypes
+    lib.rnnt_pruned_loss_forward_prepared.restype = I32
     lib.rnnt_pruned_loss_backward_input.argtypes = [P, P, P, P, DP, P, P, P, SZ, P]
     lib.rnnt_pruned_loss_backward_input.restype = I32
     lib.rnnt_pruned_loss_backward_weight.argtypes = [P, DP, P, P, P, SZ, P]
@@ -289,6 +293,22 @@ def rnnt_pruned_loss_forward(h, w_out, b_out, symbols, ranges, boundary, dims, g
     _check(rc, "rnnt_pruned_loss_forward")
 
 
+def rnnt_pruned_loss_prepare(ranges, symbols, boundary, dims, b_out, grad_scale, workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss_prepare(
+        _ptr(ranges), _ptr(symbols), _ptr(boundary), ctypes.byref(dims), _ptr(b_out), float(grad_scale),
+        _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream))
+    _check(rc, "rnnt_pruned_loss_prepare")
+
+
+def rnnt_pruned_loss_forward_prepared(h, w_out, b_out, symbols, ranges, boundary, dims, grad_scale, loss, status,
+                                      workspace, stream=None):
+    rc = load_library().rnnt_pruned_loss_forward_prepared(
+        _ptr(h), _ptr(w_out), _ptr(b_out), _ptr(symbols), _ptr(ranges), _ptr(boundary), ctypes.byref(dims),
+        float(grad_scale), _ptr(loss), _ptr(status), _ptr(workspace), workspace.numel() * workspace.element_size(),
+        _stream(stream))
+    _check(rc, "rnnt_pruned_loss_forward_prepared")
+
+
 def rnnt_pruned_loss_backward_input(h, w_out, ranges, boundary, dims, d_enc, d_dec, workspace, stream=None):
     rc = load_library().rnnt_pruned_loss_backward_input(
         _ptr(h), _ptr(w_out), _ptr(ranges), _ptr(boundary), ctypes.byref(dims), _ptr(d_enc), _ptr(d_dec),
@@ -373,6 +393,12 @@ def _side_stream(device, which=0, lane=0):
 _CRIT = {}
 
 
+_PREP_LANE = 1000   # critical_stream lanes of the prepare call (lane + 1000: never a sub-batch lane)
+# A/B switch: RNNT_SPLIT_PREP=1 runs rnnt_pruned_loss_prepare on its own stream concurrently with the gather
+# (the rowinfo launch leaves the chain, but the joiner forward then shares its SMs with the lm gradient)
+_SPLIT_PREP = os.environ.get("RNNT_SPLIT_PREP", "0") == "1"   # measured: no change at c5 (0.425 either way)
+
+
 def critical_stream(device=None, lane=0):
     """A high-priority stream for the step's critical path: with the side streams at the lowest
     priority the block scheduler hands idle SMs (e.g. during the latency-bound recursions) to the
@@ -451,6 +477,13 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
     else:
         fwd(o["am_grad"], o["lm_grad"])
     rnnt_get_ranges(o["px_grad"], o["py_grad"], boundary, dims, o["ranges"], st, cur)
+    split_prep = overlap and _SPLIT_PREP
+    if split_prep:
+        # the pruned forward's first step (per-row label info, live tiles; it does not read h) overlaps the
+        # gather on a second high-priority stream
+        prep = critical_stream(dev, lane=_PREP_LANE + lane)
+        prep.wait_stream(cur)
+        rnnt_pruned_loss_prepare(o["ranges"], symbols, boundary, dims, b_out, pruned_scale, ws, prep)
     rnnt_prune(enc_proj, dec_proj, o["ranges"], boundary, dims, o["h"], cur)
     def weight_grads(s):
         if exchange is None:
@@ -466,8 +499,15 @@ def step(am, lm, symbols, boundary, enc_proj, dec_proj, w_out, b_out, S, simple_
         o["d_w"], o["d_b"] = exchange.d_w, exchange.d_b
 
     if overlap:
-        rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
-                                 o["loss_pruned"], st, ws, cur)
+        if split_prep:
+            cur.wait_stream(prep)
+            for t in (o["ranges"], symbols, boundary, b_out, ws):
+                t.record_stream(prep)
+            rnnt_pruned_loss_forward_prepared(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims,
+                                              pruned_scale, o["loss_pruned"], st, ws, cur)
+        else:
+            rnnt_pruned_loss_forward(o["h"], w_out, b_out, symbols, o["ranges"], boundary, dims, pruned_scale,
+                                     o["loss_pruned"], st, ws, cur)
         if late:
             side = simple_backward()
         side2 = _side_stream(dev, 1, lane)

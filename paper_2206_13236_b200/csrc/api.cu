@@ -30,9 +30,11 @@ cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* a
                                 const float* px_grad, const float* py_grad, const int64_t* sym, const int64_t* bnd,
                                 float gs, float* am_grad, float* lm_grad, Smooth sm, cudaStream_t st);
 size_t pruned_recursion_smem(const Dims& d);
+cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* ranges, const int64_t* sym,
+                           const int64_t* bnd, const uint16_t* b, float gs, cudaStream_t st);
 cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, const int64_t* sym, const int32_t* ranges, const int64_t* bnd,
-                              float gs, float* loss, int32_t* status, cudaStream_t st);
+                              float gs, float* loss, int32_t* status, cudaStream_t st, bool do_rowinfo);
 cudaError_t pruned_bwd_input_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                                     const int32_t* ranges, const int64_t* bnd, float* d_enc, float* d_dec,
                                     cudaStream_t st);
@@ -333,7 +335,44 @@ rnnt_status_t rnnt_pruned_loss_forward(const uint16_t* h, const uint16_t* w_out,
   PrunedWS pw;
   carve(d, align_ws(workspace), &sw, &pw);
   return cuda_status(pruned_fwd_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss, status,
-                                       (cudaStream_t)stream));
+                                       (cudaStream_t)stream, true));
+}
+
+rnnt_status_t rnnt_pruned_loss_prepare(const int32_t* ranges, const int64_t* symbols, const int64_t* boundary,
+                                       const rnnt_dims_t* dims, const uint16_t* b_out, float grad_scale,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("rnnt_pruned_loss_prepare");   // (profiler range; a no-op without an attached tool)
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!ranges || !boundary || !b_out || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(rowinfo_launch(d, pw, ranges, symbols, boundary, b_out, grad_scale, (cudaStream_t)stream));
+}
+
+rnnt_status_t rnnt_pruned_loss_forward_prepared(const uint16_t* h, const uint16_t* w_out, const uint16_t* b_out,
+                                                const int64_t* symbols, const int32_t* ranges,
+                                                const int64_t* boundary, const rnnt_dims_t* dims, float grad_scale,
+                                                float* loss, int32_t* status, void* workspace,
+                                                size_t workspace_bytes, void* stream) {
+  NvtxRange nvtx_("rnnt_pruned_loss_forward_prepared");   // (profiler range; a no-op without an attached tool)
+  Dims d;
+  rnnt_status_t rs = check_dims(dims, &d);
+  if (rs != RNNT_OK) return rs;
+  if (!h || !w_out || !b_out || !ranges || !boundary || !loss || !workspace) return RNNT_ERR_INVALID_ARG;
+  if (d.U > 0 && !symbols) return RNNT_ERR_INVALID_ARG;
+  if (!aligned16(h) || !aligned16(w_out)) return RNNT_ERR_INVALID_ARG;
+  if (workspace_bytes < carve(d, nullptr, nullptr, nullptr)) return RNNT_ERR_WORKSPACE;
+  if (pruned_recursion_smem(d) > 224 * 1024) return RNNT_ERR_UNSUPPORTED;
+  SimpleWS sw;
+  PrunedWS pw;
+  carve(d, align_ws(workspace), &sw, &pw);
+  return cuda_status(pruned_fwd_launch(d, pw, h, w_out, b_out, symbols, ranges, boundary, grad_scale, loss, status,
+                                       (cudaStream_t)stream, false));
 }
 
 rnnt_status_t rnnt_pruned_loss_backward_input(const uint16_t* h, const uint16_t* w_out, const int32_t* ranges,

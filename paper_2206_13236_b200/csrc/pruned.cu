@@ -844,11 +844,11 @@ cudaError_t rowinfo_launch(const Dims& d, const PrunedWS& w, const int32_t* rang
 // packed backward scalars.
 cudaError_t pruned_fwd_launch(const Dims& d, const PrunedWS& w, const uint16_t* h, const uint16_t* W,
                               const uint16_t* b, const int64_t* sym, const int32_t* ranges, const int64_t* bnd,
-                              float gs, float* loss, int32_t* status, cudaStream_t st) {
+                              float gs, float* loss, int32_t* status, cudaStream_t st, bool do_rowinfo) {
   cudaError_t e;
   const long long R = d.rows();
   const int nt = d.ntile();
-  if ((e = rowinfo_launch(d, w, ranges, sym, bnd, b, gs, st)) != cudaSuccess) return e;
+  if (do_rowinfo && (e = rowinfo_launch(d, w, ranges, sym, bnd, b, gs, st)) != cudaSuccess) return e;
   if ((e = joiner_fwd_launch(d, w, h, W, b, st)) != cudaSuccess) return e;
   {
     const size_t sm = pruned_recursion_smem(d);
@@ -1093,7 +1093,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
                                const int64_t* bnd, float gs, float* loss, float* d_enc, float* d_dec,
                                float* d_w, float* d_b, int32_t* status, cudaStream_t st) {
   cudaError_t e;
-  if ((e = pruned_fwd_launch(d, w, h, W, b, sym, ranges, bnd, gs, loss, status, st)) != cudaSuccess) return e;
+  if ((e = pruned_fwd_launch(d, w, h, W, b, sym, ranges, bnd, gs, loss, status, st, true)) != cudaSuccess) return e;
   if ((e = pruned_bwd_input_launch(d, w, h, W, ranges, bnd, d_enc, d_dec, st)) != cudaSuccess) return e;
   return pruned_bwd_weight_launch(d, w, h, d_w, d_b, st, 0);
 }

@@ -87,3 +87,38 @@ def test_large_v_rescale(J):
     """V >= 6144 with a spike beyond the reference columns: the wide kernel's rescaling mode (the pair
     kernel, launched alongside, must leave it alone)."""
     _check(_spiked(5000, V=6500, J=J), False)
+
+
+def test_prepare_split_matches():
+    """rnnt_pruned_loss_prepare + rnnt_pruned_loss_forward_prepared (the prepare call on its own stream, as
+    step(RNNT_SPLIT_PREP=1) runs it) give bit-identical results to rnnt_pruned_loss_forward."""
+    from test_gpu_guards import _sub
+    from test_gpu_parity import check_ranges, check_simple
+    b = _sub(synth.make_batch(2), [0, 1, 2, 3])
+    g, o = check_simple(b)
+    ranges = check_ranges(b, o)
+    h_bits = oracle_h_bits(b, ranges)
+    dev = to_dev(b)
+    d = dims_of_batch(b)
+    h = torch.from_numpy(np.ascontiguousarray(h_bits).view(np.int16)).cuda()
+    rg = torch.from_numpy(np.ascontiguousarray(ranges, np.int32)).cuda()
+    res = []
+    for split in (False, True):
+        out = R.alloc_outputs(d, "cuda")
+        ws = torch.full((R.rnnt_workspace_bytes(d),), 0xFF, dtype=torch.uint8, device="cuda")
+        if split:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            R.rnnt_pruned_loss_prepare(rg, dev["symbols"], dev["boundary"], d, dev["b_out"], 1.0, ws, side)
+            torch.cuda.current_stream().wait_stream(side)
+            R.rnnt_pruned_loss_forward_prepared(h, dev["w_out"], dev["b_out"], dev["symbols"], rg, dev["boundary"], d,
+                                                1.0, out["loss_pruned"], out["status"], ws)
+        else:
+            R.rnnt_pruned_loss_forward(h, dev["w_out"], dev["b_out"], dev["symbols"], rg, dev["boundary"], d, 1.0,
+                                       out["loss_pruned"], out["status"], ws)
+        R.rnnt_pruned_loss_backward_input(h, dev["w_out"], rg, dev["boundary"], d, out["d_enc"], out["d_dec"], ws)
+        R.rnnt_pruned_loss_backward_weight(h, d, out["d_w"], out["d_b"], ws)
+        torch.cuda.synchronize()
+        res.append({k: out[k].cpu().numpy() for k in ("loss_pruned", "d_enc", "d_dec", "d_w", "d_b")})
+    for k in res[0]:
+        assert np.array_equal(res[0][k], res[1][k]), k

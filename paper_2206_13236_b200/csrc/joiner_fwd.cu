@@ -395,11 +395,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
     return p.tlive[2 * rp] || (2 * rp + 1 < p.ntiles && p.tlive[2 * rp + 1]);
   };
   const uint32_t qemptyL = tc::mapa(&qempty[0], 0);
-  // consumers: take queue entry qi (-1 = done) and release its slot on the leader
+  // consumers: take queue entry qi (-1 = done) and release its slot on the leader (a .cta-release remote
+  // arrive, as CUTLASS's cluster-pipeline consumer release: the release.cluster form was ~10 % of the
+  // kernel's stall samples at c5, its fence waiting on the warp's outstanding stores)
   auto take = [&](int qi, bool arrive) {
     tc::mbar_wait_cluster(&qfull[qi & 3], (qi >> 2) & 1);
     const int rp = *reinterpret_cast<volatile int*>(&tq[qi & 3]);
-    if (arrive) tc::mbar_arrive_cluster(qemptyL + (qi & 3) * 8);
+    if (arrive) tc::mbar_arrive_remote(qemptyL + (qi & 3) * 8);
     return rp;
   };
 
@@ -476,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
     for (int qi = 0;; ++qi) {
       const int rp = take(qi, false);
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(qemptyL + (qi & 3) * 8);
+      if (lane == 0) tc::mbar_arrive_remote(qemptyL + (qi & 3) * 8);
       if (rp < 0) break;
       const int rt = 2 * rp + (int)rank;
       const long long r = (long long)rt * BM + 32 * q + lane;

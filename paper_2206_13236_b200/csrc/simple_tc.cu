@@ -681,8 +681,13 @@ struct NormProb {
     const int trow = t.m0 + e.row;
     const bool rowok = trow < Tn;
     const int t0w = t.m0 + 32 * e.q;
-    float2 (*bxy)[33] = reinterpret_cast<float2 (*)[33]>(smem + e.warp * 32 * 33 * 8);
-    float (*brs)[33] = reinterpret_cast<float (*)[33]>(smem + sg::EPI_WARPS * 32 * 33 * 8 + e.warp * 32 * 33 * 4);
+    // per-warp 32 x 32 staging blocks with a pitch of 35 elements: the row-wise writes bxy[lane][j] and the
+    // anti-diagonal reads bxy[i - lane][lane] are both (at most 2-way) bank-conflict free (a pitch of 33 put
+    // every lane of a diagonal read on the same bank: 32-way)
+    constexpr int PB = 35;
+    static_assert(sg::EPI_WARPS * 32 * PB * 12 <= kStages * sg::Geo<NormProb>::STAGE_BYTES, "staging fits the stages");
+    float2 (*bxy)[PB] = reinterpret_cast<float2 (*)[PB]>(smem + e.warp * 32 * PB * 8);
+    float (*brs)[PB] = reinterpret_cast<float (*)[PB]>(smem + sg::EPI_WARPS * 32 * PB * 8 + e.warp * 32 * PB * 4);
     const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
     const float mam = rowok ? m_am[arow] : 0.f;
     const float am0 = rowok ? am[arow * V] : 0.f;
@@ -743,14 +748,16 @@ struct NormProb {
       // iteration i: lanes l <= i write diagonal t0w + u0 + i, lanes l > i diagonal t0w + u0 + i + 32
       // (two contiguous runs per store), so every lane writes a cell in each of 32 iterations
       const int u = u0 + e.lane;
-      for (int i = 0; i < 32; ++i) {
-        const int tl_ = e.lane <= i ? i - e.lane : i + 32 - e.lane, tt = t0w + tl_;
-        if (tt < Tn && u <= Un) {
-          const size_t o = (nbase + tt + u) * LU + u;
-          pxy[o] = bxy[tl_][e.lane];
-          rS[o] = brs[tl_][e.lane];
+      const size_t o0 = (nbase + t0w + u) * LU + u;   // cell (t0w, u); row t0w + tl_ is tl_ diagonals further
+      if (u <= Un)
+        for (int i = 0; i < 32; ++i) {
+          const int tl_ = e.lane <= i ? i - e.lane : i + 32 - e.lane;
+          if (t0w + tl_ < Tn) {
+            const size_t o = o0 + (size_t)(tl_ * LU);
+            pxy[o] = bxy[tl_][e.lane];
+            rS[o] = brs[tl_][e.lane];
+          }
         }
-      }
       __syncwarp();
     }
     if (under) set_status(status, t.n, kStatusUnderflow);

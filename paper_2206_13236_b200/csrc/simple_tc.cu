@@ -615,9 +615,12 @@ __device__ __forceinline__ void warp_store_block(const float (*buf)[33], float* 
 #define RNNT_NORM_STAGES 2
 #define RNNT_NORM_MINB 1
 #endif
-struct NormProb {
+// BNT = 256 for large V (c4: the mainloop, not the epilogue, dominates; the am operand tile is then read
+// once per utterance instead of once per 128 columns of u)
+template <int BNT>
+struct NormProbT {
   static constexpr bool kA_MN = false, kB_MN = false;
-  static constexpr int kPhases = 1, kBN = RNNT_NORM_BN, kStages = RNNT_NORM_STAGES, kMinBlocks = RNNT_NORM_MINB;
+  static constexpr int kPhases = 1, kBN = BNT, kStages = RNNT_NORM_STAGES, kMinBlocks = RNNT_NORM_MINB;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
   int T, U, V, LU, K, BN, nkb, UPa;
@@ -640,7 +643,7 @@ struct NormProb {
     tc::tma_load_3d(st, &mp.m[0], bar, kb * sg::BK, t.m0, t.n);
     tc::tma_load_3d(st + sg::A_BYTES, &mp.m[1], bar, kb * sg::BK, t.m0, t.n);
     tc::tma_load_3d(st + 2 * sg::A_BYTES, &mp.m[2], bar, kb * sg::BK, t.n0, t.n);
-    tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::Geo<NormProb>::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
+    tc::tma_load_3d(st + 2 * sg::A_BYTES + sg::Geo<NormProbT>::B_BYTES, &mp.m[3], bar, kb * sg::BK, t.n0, t.n);
   }
   __device__ int epi_chunks(const Tile&) const { return 0; }
   __device__ void epi_load(int, uint8_t*, uint64_t*, const Tile&, const Maps&) const {}
@@ -685,7 +688,7 @@ struct NormProb {
     // anti-diagonal reads bxy[i - lane][lane] are both (at most 2-way) bank-conflict free (a pitch of 33 put
     // every lane of a diagonal read on the same bank: 32-way)
     constexpr int PB = 35;
-    static_assert(sg::EPI_WARPS * 32 * PB * 12 <= kStages * sg::Geo<NormProb>::STAGE_BYTES, "staging fits the stages");
+    static_assert(sg::EPI_WARPS * 32 * PB * 12 <= kStages * sg::Geo<NormProbT>::STAGE_BYTES, "staging fits the stages");
     float2 (*bxy)[PB] = reinterpret_cast<float2 (*)[PB]>(smem + e.warp * 32 * PB * 8);
     float (*brs)[PB] = reinterpret_cast<float (*)[PB]>(smem + sg::EPI_WARPS * 32 * PB * 8 + e.warp * 32 * PB * 4);
     const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
@@ -1112,6 +1115,20 @@ cudaError_t simple_prep_launch(const Dims& d, const SimpleWS& w, const float* am
   return cudaGetLastError();
 }
 
+template <class NP>
+static cudaError_t launch_norm(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
+                               const int64_t* bnd, int32_t* status, Smooth sm, cudaStream_t st) {
+  const int BN = std::min(NP::kBN, (d.U1() + 15) / 16 * 16);
+  Maps mp;
+  if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
+      !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))
+    return cudaErrorInvalidValue;
+  NP p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64, d.UP(),
+             w.pxy, w.rS, status, am, w.amy, sm, w.lse_lm, w.Lavg, w.lse_ac, d.VP64()};
+  dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.U1() + BN - 1) / BN, d.N);
+  return launch_gemm3(p, grid, mp, KID_NORM, st);
+}
+
 cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm, const int64_t* sym,
                              const int64_t* bnd, int32_t* status, Smooth sm, cudaStream_t st) {
   if (sm.on()) {
@@ -1121,15 +1138,10 @@ cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, 
     RNNT_LAUNCH(KID_SMOOTH_AC, st, launch_pdl(smooth_ac_kernel, (unsigned)(((long long)d.N * d.T + 7) / 8), 256, 0, st, 
         am, w.m_am, w.Lavg, bnd, d.N, d.T, d.V, d.VP64(), w.lse_ac));
   }
-  const int BN = std::min(NormProb::kBN, (d.U1() + 15) / 16 * 16);
-  Maps mp;
-  if (!tm3(&mp.m[0], w.Eam_hi, d.VP64(), d.T, d.N, sg::BM) || !tm3(&mp.m[1], w.Eam_lo, d.VP64(), d.T, d.N, sg::BM) ||
-      !tm3(&mp.m[2], w.Elm_hi, d.VP64(), d.U1(), d.N, BN) || !tm3(&mp.m[3], w.Elm_lo, d.VP64(), d.U1(), d.N, BN))
-    return cudaErrorInvalidValue;
-  NormProb p{lm, w.m_am, w.m_lm, sym, bnd, d.T, d.U, d.V, d.LU(), d.K(), BN, d.VP64() / 64, d.UP(),
-             w.pxy, w.rS, status, am, w.amy, sm, w.lse_lm, w.Lavg, w.lse_ac, d.VP64()};
-  dim3 grid((d.T + sg::BM - 1) / sg::BM, (d.U1() + BN - 1) / BN, d.N);
-  return launch_gemm3(p, grid, mp, KID_NORM, st);
+  // 128 x 256 tiles for large V (mainloop-bound: fewer, longer tiles); 128 x 128 otherwise (epilogue-bound)
+  if (d.VP64() >= 2048 && d.U1() > 128)
+    return launch_norm<NormProbT<256>>(d, w, am, lm, sym, bnd, status, sm, st);
+  return launch_norm<NormProbT<RNNT_NORM_BN>>(d, w, am, lm, sym, bnd, status, sm, st);
 }
 
 cudaError_t simple_grads_launch(const Dims& d, const SimpleWS& w, const float* am, const float* lm,

@@ -53,16 +53,16 @@ __global__ void __launch_bounds__(1024) prune_kernel(const float* __restrict__ e
                                                      const int32_t* __restrict__ ranges, const int64_t* __restrict__ bnd,
                                                      int N, int T, int U, int J, int S, uint16_t* __restrict__ h) {
   RNNT_GDC();   // programmatic dependent launch: wait for the producer grid, release ours
-  const long long nt = (long long)blockIdx.x * blockDim.y + threadIdx.y;
-  if (nt >= (long long)N * T) return;
-  const int n = (int)(nt / T), t = (int)(nt - (long long)n * T);
+  const unsigned nt = blockIdx.x * blockDim.y + threadIdx.y;   // N T < 2^31 (checked by the launcher)
+  if (nt >= (unsigned)N * (unsigned)T) return;
+  const int n = (int)(nt / (unsigned)T), t = (int)(nt - (unsigned)n * (unsigned)T);
   const int Tn = utt_T(bnd, n), Un = utt_U(bnd, n);
   const int j0 = threadIdx.x * 8;
   const bool live = t < Tn;
   const int p = live ? ranges[nt] : 0;
   float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0;
   if (live) {
-    const float* e = enc + nt * J + j0;
+    const float* e = enc + (size_t)nt * J + j0;
     e0 = __ldg(reinterpret_cast<const float4*>(e));
     e1 = __ldg(reinterpret_cast<const float4*>(e + 4));
   }
@@ -760,6 +760,7 @@ cudaError_t prune_launch(const Dims& d, const float* enc, const float* dec, cons
   const int J8 = d.J / 8;                          // J % 8 == 0 (rnnt_check_dims)
   const int fpb = std::max(1, 256 / J8);           // frames per block
   const long long NT = (long long)d.N * d.T;
+  if (NT >= (1LL << 31)) return cudaErrorInvalidValue;   // (32-bit frame index in the kernel)
   RNNT_LAUNCH(KID_PRUNE, st, launch_pdl(prune_kernel, (unsigned)((NT + fpb - 1) / fpb), dim3(J8, fpb), 0, st, 
       enc, dec, ranges, bnd, d.N, d.T, d.U, d.J, d.S, h));
   return cudaGetLastError();

@@ -269,18 +269,19 @@ __global__ void __launch_bounds__(256) simple_prep_kernel(PrepParams p) {
     b -= p.nb_lm;
   }
   if (b < p.nb_fill) {
-    // kNegBig in every invalid cell of the skewed arcs (lattice.cu conventions): 8 rows per block
-    const long long rows = (long long)p.N * (p.K + 1);
-    for (int rr = 0; rr < 8; ++rr) {
-      const long long row = (long long)b * 8 + rr;
-      if (row >= rows) break;
+    // kNegBig in every invalid cell of the skewed arcs (lattice.cu conventions): a warp per row (n, k), lanes
+    // over u, writing only the columns outside the row's lattice cells [max(0, k - T_n + 1), min(k, U_n)]
+    // (one division per warp and row: the per-thread 64-bit divisions of a block-per-8-rows form were
+    // 40 % of this kernel's samples at c5)
+    const long long row = (long long)b * 8 + (threadIdx.x >> 5);
+    if (row < (long long)p.N * (p.K + 1)) {
       const int n = (int)(row / (p.K + 1)), k = (int)(row - (long long)n * (p.K + 1));
       const int Tn = utt_T(p.bnd, n), Un = utt_U(p.bnd, n);
+      const int lo = max(0, k - Tn + 1), hi = min(k, Un);   // (empty when lo > hi)
       float2* r = p.pxy + row * p.LU;
-      for (int u = threadIdx.x; u < p.LU; u += blockDim.x) {
-        const int t = k - u;
-        if (!(t >= 0 && t < Tn && u <= Un)) r[u] = make_float2(kNegBig, kNegBig);
-      }
+      const float2 sent = make_float2(kNegBig, kNegBig);
+      for (int u = threadIdx.x & 31; u < p.LU; u += 32)
+        if (u < lo || u > hi) r[u] = sent;
     }
     return;
   }

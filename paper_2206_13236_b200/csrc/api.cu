@@ -55,6 +55,7 @@ cudaError_t pruned_loss_launch(const Dims& d, const PrunedWS& w, const uint16_t*
 
 namespace rnnt {
 void set_timeline(void* buf);
+void set_fwd_trace(void* buf);
 void set_dh_trace(void* buf);
 void set_scan_trace(void* buf);
 static thread_local unsigned long long g_launches = 0;
@@ -465,6 +466,7 @@ void rnnt_debug_timeline(void* buf) {
   rnnt::set_timeline(buf);
   rnnt::set_dh_trace(buf ? static_cast<char*>(buf) + (4u << 20) : nullptr);   // joiner_dh trace 4 MiB in
   rnnt::set_scan_trace(buf ? static_cast<char*>(buf) + (6u << 20) : nullptr); // pruned scan trace 6 MiB in
+  rnnt::set_fwd_trace(buf ? static_cast<char*>(buf) + (7u << 20) : nullptr);  // joiner forward trace 7 MiB in
 }
 #endif
 

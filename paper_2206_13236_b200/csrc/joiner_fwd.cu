@@ -350,6 +350,23 @@ constexpr int SMEM_BYTES = BAR_OFF + 256 + 1024;
 constexpr int THREADS = 320;
 }  // namespace jf2
 
+// diagnostics: per (CTA, row tile < 8) timestamps {0 producer took the tile, 1 MMA vp0 start, 2 MMA vp0
+// issued, 3 MMA last vp issued, 4 epilogue set 0 vp0 full, 5 set 0 vp0 done, 6 set 0 last vp full, 7 set 0
+// last vp done, 8 row merged}
+#ifdef RNNT_DIAGNOSTICS
+__device__ unsigned long long* g_fwd_trace = nullptr;
+void set_fwd_trace(void* buf) { cudaMemcpyToSymbol(g_fwd_trace, &buf, sizeof(buf)); }
+#else
+constexpr unsigned long long* g_fwd_trace = nullptr;   // product build: tracing compiled out
+#endif
+__device__ __forceinline__ void fwd_trace(int it, int k) {
+  if (g_fwd_trace && it < 8) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_fwd_trace[((size_t)blockIdx.x * 8 + it) * 10 + k] = t;
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
     joiner_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            const __grid_constant__ CUtensorMap tmP, JoinerFwdParams p) {
@@ -411,24 +428,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
       const uint32_t tqP = tc::mapa(&tq[0], 1), qfullP = tc::mapa(&qfull[0], 1);
       int stage = 0;
       uint32_t ph = 0;
-      for (int qi = 0;; ++qi) {
-        int rp;
-        if (leader) {
-          rp = atomicAdd(p.counter, 1);
-          while (rp < npairs && !live_pair(rp)) rp = atomicAdd(p.counter, 1);
-          if (rp >= npairs) rp = -1;
-          tc::mbar_wait_cluster(&qempty[qi & 3], ((qi >> 2) & 1) ^ 1);
-          tq[qi & 3] = rp;
-          tc::st_cluster_u32(tqP + (qi & 3) * 4, (uint32_t)rp);
-          tc::mbar_arrive(&qfull[qi & 3]);
-          tc::mbar_arrive_cluster(qfullP + (qi & 3) * 8);
-        } else {
-          rp = take(qi, true);
-        }
-        if (rp < 0) break;
+      // queue entry qi: the leader draws the next live row-tile pair and publishes it to both CTAs
+      auto draw = [&](int qi) -> int {
+        if (!leader) return take(qi, true);
+        int rp = atomicAdd(p.counter, 1);
+        while (rp < npairs && !live_pair(rp)) rp = atomicAdd(p.counter, 1);
+        if (rp >= npairs) rp = -1;
+        tc::mbar_wait_cluster(&qempty[qi & 3], ((qi >> 2) & 1) ^ 1);
+        tq[qi & 3] = rp;
+        tc::st_cluster_u32(tqP + (qi & 3) * 4, (uint32_t)rp);
+        tc::mbar_arrive(&qfull[qi & 3]);
+        tc::mbar_arrive_cluster(qfullP + (qi & 3) * 8);
+        return rp;
+      };
+      // the next tile is drawn at the start of the current tile's last V pass and its h rows are prefetched
+      // into L2 then: its first pass reads them from L2 instead of HBM (c5 trace: the first pass of a tile
+      // took 6.4-7.5 us against 3.1 us for the second, every CTA fetching its h rows at the same moment)
+      int rp = draw(0);
+      if (rp >= 0)
+        for (int kb = 0; kb < nkb; ++kb) tc::tma_prefetch_2d(&tmA, kb * BK, (2 * rp + (int)rank) * BM);
+      for (int qi = 0; rp >= 0; ++qi) {
+        fwd_trace(qi, 0);
         const int m0 = (2 * rp + (int)rank) * BM;
-        for (int kb = 0; kb < nkb; ++kb) tc::tma_prefetch_2d(&tmA, kb * BK, m0);
+        int rpn = -1;
         for (int vp = 0; vp < nvp; ++vp) {
+          if (vp == nvp - 1) {
+            rpn = draw(qi + 1);
+            if (rpn >= 0)
+              for (int kb = 0; kb < nkb; ++kb) tc::tma_prefetch_2d(&tmA, kb * BK, (2 * rpn + (int)rank) * BM);
+          }
           for (int kb = 0; kb < nkb; ++kb) {
             tc::mbar_wait(&empty[stage], ph ^ 1);
             if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -438,6 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
         }
+        rp = rpn;
       }
     }
   } else if (warp == 1) {
@@ -451,6 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
           const int acc = it & 1;
           tc::mbar_wait_cluster(&tempty[acc], ((it >> 1) & 1) ^ 1);
           tc::fence_after_sync();
+          if (vp == 0) fwd_trace(qi, 1);
           const uint32_t d = tbase + acc * 2 * BN;
           for (int kb = 0; kb < nkb; ++kb) {
             tc::mbar_wait_cluster(&full[stage], ph);
@@ -464,6 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
             if (++stage == STAGES) { stage = 0; ph ^= 1; }
           }
           tc::mma2_commit(&tfull[acc], 3);
+          fwd_trace(qi, vp == 0 ? 2 : 3);
         }
       }
     }
@@ -490,6 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
         const int nt = 2 * vp + set, v0 = nt * BN;
         tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
         tc::fence_after_sync();
+        if (threadIdx.x == 64) fwd_trace(qi, vp == 0 ? 4 : 6);
         const uint32_t tcol = tl + acc * 2 * BN;
         const bool have = nt < nvt;             // warp-uniform
         constexpr float kRedo = 60.f;
@@ -603,6 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_remote(temptyL + acc * 8);
+        if (threadIdx.x == 64) fwd_trace(qi, vp == 0 ? 5 : 7);
         if (have) {
           tc::fence_proxy_async();
           asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
@@ -637,6 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(jf2::THREADS, 1)
           p.py2[r] = kNegBig;
         }
       }
+      if (threadIdx.x == 64) fwd_trace(qi, 8);
       ++nrt;
     }
   }

@@ -483,6 +483,14 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// diagnostics: epilogue-internal mark k (4..7) of this CTA, written by thread 0
+__device__ __forceinline__ void etrace(int k) {
+  if (g_timeline && threadIdx.x == 0) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    g_timeline[(size_t)cta * 8 + k] = gtime();
+  }
+}
+
 // Phase 0: acc0 (TMEM columns 0..kBN-1) += A_hi B_hi + A_hi B_lo + A_lo B_hi   (bf16x3)
 // Phase 1: acc1 (TMEM columns kBN..2kBN-1) += A'_hi B' + A'_lo B'              (B' exact in bf16)
 template <class P>
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(sg::THREADS, P::kMinBlocks) gemm3_kernel(const
   unsigned long long* tlog = nullptr;
   if (g_timeline && threadIdx.x == 0) {
     const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    tlog = g_timeline + (size_t)cta * 4;
+    tlog = g_timeline + (size_t)cta * 8;   // [0..3] kernel phases, [4..7] epilogue-internal marks (etrace)
     tlog[0] = gtime();
   }
   if (warp < EPI_WARPS) {
@@ -777,6 +785,7 @@ struct AmProb {
   static constexpr int kPhases = 1, kBN = 128, kStages = 1, kMinBlocks = 2;
   static constexpr int kNC = kBN / 32;      // 32-column epilogue chunks per tile
   static constexpr int kMaxPicks = 1024;    // (u, column) pairs listed in aux (U <= 1023)
+  static constexpr int kRowOff = 256 + kMaxPicks * 8;   // aux: per-row {m_am, rowb} after the pick list
   const float *am, *m_am, *rowb;
   const int64_t* bnd;
   int T, U, V;
@@ -818,38 +827,92 @@ struct AmProb {
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
-  // aux: [0] the number of picks, [1..8] per-warp counts, then the (u, column - n0) pairs of the labels
-  // falling in this tile in ascending u (a ballot / warp-count scan: deterministic order, so duplicate
-  // labels always add in the same order)
+  // aux: ints [0..4] where each 32-column chunk's picks start in the list ([4] = their total), ints [8..40) the
+  // per-warp per-chunk counts of the scan; at aux + 256 the (u, column - n0) pairs of the labels falling in this
+  // tile, grouped by chunk and in ascending u inside a chunk (ballot / warp-count scans: a deterministic order,
+  // so duplicate labels always add in the same order).  Grouping by chunk lets the epilogue of a chunk walk only
+  // its own picks (c5: ~5 of the tile's ~20; walking all of them cost 4 us per chunk, mostly y' load latency).
   __device__ void prologue(uint8_t* aux, const Tile& t) const {
-    int* cnt = reinterpret_cast<int*>(aux);
-    int* wc = cnt + 1;
-    int2* pk = reinterpret_cast<int2*>(aux + 64);
+    int* off = reinterpret_cast<int*>(aux);
+    int* wc = off + 8;                                    // [EPI_WARPS][kNC]
+    int2* pk = reinterpret_cast<int2*>(aux + 256);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int Un = utt_U(bnd, t.n);
-    int base = 0;
-    for (int u0 = 0; u0 < Un; u0 += 32 * sg::EPI_WARPS) {
-      const int u = u0 + threadIdx.x;
-      bool hit = false;
-      int col = 0;
+    // the rows' scalars {m_am, sum_u empty'} for the epilogue, loaded while the operands are in flight (as the
+    // epilogue's first statements they were an exposed L2 / HBM round trip after the MMAs): aux + kRowOff
+    float2 rsc = make_float2(0.f, 0.f);
+    if (threadIdx.x < sg::BM && t.m0 + (int)threadIdx.x < utt_T(bnd, t.n)) {
+      const size_t row = (size_t)t.n * T + t.m0 + threadIdx.x;
+      rsc = make_float2(m_am[row], rowb[row]);
+    }
+    auto label = [&](int u, bool& hit, int& col) {
+      hit = false;
+      col = 0;
       if (u < Un) {
         const long long y = sym[(size_t)t.n * U + u];
         hit = y >= t.n0 && y < t.n0 + kBN && y < V;
         col = (int)(y - t.n0);
       }
-      const unsigned b = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) wc[warp] = __popc(b);
+    };
+    // pass 1: picks per chunk
+    int cnt[kNC];
+#pragma unroll
+    for (int c = 0; c < kNC; ++c) cnt[c] = 0;
+    for (int u0 = 0; u0 < Un; u0 += 32 * sg::EPI_WARPS) {
+      bool hit;
+      int col;
+      label(u0 + (int)threadIdx.x, hit, col);
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) cnt[c] += __popc(__ballot_sync(0xffffffffu, hit && (col >> 5) == c));
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) wc[warp * kNC + c] = cnt[c];
+    }
+    epi_bar();
+    int base[kNC + 1];
+    {
+      int run = 0;
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        base[c] = run;
+        for (int w = 0; w < sg::EPI_WARPS; ++w) run += wc[w * kNC + c];
+      }
+      base[kNC] = run;
+    }
+    epi_bar();                                            // (wc is rewritten below)
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int c = 0; c <= kNC; ++c) off[c] = min(base[c], kMaxPicks);
+    }
+    // pass 2: placement
+    for (int u0 = 0; u0 < Un; u0 += 32 * sg::EPI_WARPS) {
+      const int u = u0 + (int)threadIdx.x;
+      bool hit;
+      int col;
+      label(u, hit, col);
+      unsigned bl[kNC];
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        bl[c] = __ballot_sync(0xffffffffu, hit && (col >> 5) == c);
+        if (lane == 0) wc[warp * kNC + c] = __popc(bl[c]);
+      }
       epi_bar();
-      int off = base;
-      for (int w = 0; w < warp; ++w) off += wc[w];
-      int tot = 0;
-      for (int w = 0; w < sg::EPI_WARPS; ++w) tot += wc[w];
-      const int i = off + __popc(b & ((1u << lane) - 1u));
-      if (hit && i < kMaxPicks) pk[i] = make_int2(u, col);
-      base += tot;
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        int o = base[c], tot = 0;
+        for (int w = 0; w < sg::EPI_WARPS; ++w) {
+          const int x = wc[w * kNC + c];
+          if (w < warp) o += x;
+          tot += x;
+        }
+        const int i = o + __popc(bl[c] & ((1u << lane) - 1u));
+        if (hit && (col >> 5) == c && i < kMaxPicks) pk[i] = make_int2(u, col);
+        base[c] += tot;
+      }
       epi_bar();
     }
-    if (threadIdx.x == 0) *cnt = base;
+    if (threadIdx.x < sg::BM) reinterpret_cast<float2*>(aux + kRowOff)[threadIdx.x] = rsc;
     epi_bar();
   }
   // the picks of row trow for the 32 columns of chunk c (fp32 y' from px_grad)
@@ -858,18 +921,18 @@ struct AmProb {
 #pragma unroll
     for (int j = 0; j < 32; ++j) a1[j] = 0.f;
     if (!live) return;
-    const int npk = min(*reinterpret_cast<const int*>(aux), kMaxPicks);
-    const int2* pk = reinterpret_cast<const int2*>(aux + 64);
+    const int* off = reinterpret_cast<const int*>(aux);
+    const int i0 = off[c], i1 = off[c + 1];
+    const int2* pk = reinterpret_cast<const int2*>(aux + 256);
     const float* yr = px_grad + ((size_t)t.n * T + trow) * (U + 1);
-    for (int i = 0; i < npk; ++i) {
+#pragma unroll 2
+    for (int i = i0; i < i1; ++i) {
       const int2 q = pk[i];
       const int jj = q.y - 32 * c;
-      if ((unsigned)jj < 32u) {
-        const float yv = yr[q.x];
+      const float yv = yr[q.x];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j == jj) a1[j] += yv;
-      }
+      for (int j = 0; j < 32; ++j)
+        if (j == jj) a1[j] += yv;
     }
   }
   __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t* ep_full,
@@ -881,18 +944,70 @@ struct AmProb {
     if (nep > 0) {
       // d(-L_simple)/d am = E_am (G~ E_lm) - y' [v = y_{u+1}] - [v=0] sum_u empty'   (times gs), tile in place
       const size_t row = (size_t)t.n * T + (live ? trow : 0);
-      const float mam = live ? m_am[row] : 0.f;
-      const float rb = live ? rowb[row] : 0.f;
+      const float2 rsc = reinterpret_cast<const float2*>(aux + kRowOff)[e.row];   // (prologue)
+      const float mam = rsc.x, rb = rsc.y;
       const float occ = (live && sm.on()) ? rb + rowy[row] : 0.f;
       const float lac = (live && sm.on()) ? lse_ac[row] : 0.f;
       const float* Lr = Lavg + (size_t)t.n * VPl;
       for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
+        uint8_t* tile = smem + c * EP_BYTES;
+        if (!sm.on()) {
+          // The plain trivial joiner (w0 = 1, no smoothing terms): gs e^(x - m_am) a0 for the whole chunk (~6
+          // instructions per element; the general form below, with its per-element smoothing selects, is ~30
+          // and made the epilogue issue-bound: 2.3 us per chunk at 4 warps per scheduler), then the row's picks
+          // subtracted in place in the staged tile.  The y' values of the chunk's picks are loaded eight at a
+          // time, the first batch before the accumulator / input-tile waits (as dependent loads walked one by
+          // one they were 3.6 us per chunk at c5).
+          const int* off = reinterpret_cast<const int*>(aux);
+          const int2* pk = reinterpret_cast<const int2*>(aux + 256);
+          const int i0 = live ? off[c] : 0, i1 = live ? off[c + 1] : 0;
+          const float* yr = px_grad + ((size_t)t.n * T + (live ? trow : 0)) * (U + 1);
+          float yv[8];
+          int jj[8];
+          auto load8 = [&](int i) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const bool ok = i + k < i1;
+              const int2 q = ok ? pk[i + k] : make_int2(0, -1);
+              jj[k] = ok ? q.y - 32 * c : -1;
+              yv[k] = ok ? yr[q.x] : 0.f;
+            }
+          };
+          auto apply8 = [&]() {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (jj[k] >= 0) reinterpret_cast<float*>(ep_at(tile, e.row, jj[k] >> 2))[jj[k] & 3] -= gs * yv[k];
+          };
+          load8(i0);
+          float a0[32];
+          if (c == e.g) etrace(4);
+          tc::tmem_ld32(e.taddr + 32 * c, a0);
+          tc::mbar_wait(&ep_full[c], 0);
+          if (c == e.g) etrace(5);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4* pq = ep_at(tile, e.row, q);
+            const float4 x = *pq;
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = gs * (__expf(xs[i] - mam) * a0[4 * q + i]);
+            *pq = live ? make_float4(o[0], o[1], o[2], o[3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          if (live) {
+            apply8();
+            for (int i = i0 + 8; i < i1; i += 8) {
+              load8(i);
+              apply8();
+            }
+            if (vc == 0) reinterpret_cast<float*>(ep_at(tile, e.row, 0))[0] -= gs * rb;
+          }
+        } else {
         float a0[32], a1[32];
         picks(aux, c, trow, live, t, a1);
         tc::tmem_ld32(e.taddr + 32 * c, a0);
         tc::mbar_wait(&ep_full[c], 0);
-        uint8_t* tile = smem + c * EP_BYTES;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float4* pq = ep_at(tile, e.row, q);
@@ -907,17 +1022,31 @@ struct AmProb {
           }
           *pq = make_float4(o[0], o[1], o[2], o[3]);
         }
+        }
         tc::fence_proxy_async();
         group_bar(e.g);
         if (e.row == 0) {
           tc::tma_store_3d(&mp.eout, tile, vc, t.m0, t.n);
           tc::bulk_commit();
         }
+        if (c == 0) etrace(6);
       }
+      etrace(7);
       if (e.row == 0) tc::bulk_wait_read0();
       return;
     }
-    // generic path (V % 4 != 0, or a tile of padded rows only): coalesced warp I/O through smem
+    if (tma_io && t.nkb0 == 0) {
+      // a tile of padded frames only (t >= T_n): its rows are exactly 0 -- a warp per row, one float4 store
+      // per lane (V % 4 == 0: 16-B aligned rows), instead of the staged generic path (traced at 9 us per such
+      // tile, as long as a live one; 39 % of the tiles at c3, 25 % at c5)
+      const int r1 = min(T, t.m0 + sg::BM), nc4 = min(kBN, V - t.n0) >> 2;
+      for (int r = t.m0 + e.warp; r < r1; r += sg::EPI_WARPS) {
+        float4* dst = reinterpret_cast<float4*>(am_grad + ((size_t)t.n * T + r) * V + t.n0);
+        if (e.lane < nc4) dst[e.lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      return;
+    }
+    // generic path (V % 4 != 0): coalesced warp I/O through smem
     const int t0w = t.m0 + 32 * e.q;
     if (t0w >= T) return;                               // whole warp beyond the padded rows
     const size_t row0 = (size_t)t.n * T + t0w;
@@ -999,33 +1128,74 @@ struct LmProb {
   __device__ void epi_load(int c, uint8_t* dst, uint64_t* bar, const Tile& t, const Maps& mp) const {
     tc::tma_load_3d(dst, &mp.ein, bar, t.n0 + 32 * c, t.m0, t.n);
   }
-  __device__ void prologue(uint8_t*, const Tile&) const {}
-  __device__ void epilogue(uint8_t* smem, uint8_t*, const Tile& t, const Epi& e, uint64_t* ep_full,
+  // the rows' scalars {sum_t y', sum_t empty', m_lm, label} for the epilogue, loaded while the operands are in
+  // flight (2 ntb + 2 loads per row that were an exposed round trip after the MMAs): aux[128] float4
+  __device__ void prologue(uint8_t* aux, const Tile& t) const {
+    const int Un = utt_U(bnd, t.n), U1 = U + 1;
+    if (threadIdx.x < sg::BM) {
+      const int urow = t.m0 + threadIdx.x;
+      float csy = 0.f, csb = 0.f, mlm = 0.f;
+      int y = -1;
+      if (urow <= Un) {
+        for (int tb = 0; tb < ntb; ++tb) {
+          csy += colpy[((size_t)t.n * ntb + tb) * U1 + urow];
+          csb += colpb[((size_t)t.n * ntb + tb) * U1 + urow];
+        }
+        if (urow < Un) y = (int)sym[(size_t)t.n * U + urow];
+        mlm = m_lm[(size_t)t.n * U1 + urow];
+      }
+      reinterpret_cast<float4*>(aux)[threadIdx.x] = make_float4(csy, csb, mlm, __int_as_float(y));
+    }
+    epi_bar();
+  }
+  __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
     const int Un = utt_U(bnd, t.n), U1 = U + 1;
+    if (tma_io && t.nkb0 == 0) {
+      // a tile of padded token positions only (u > U_n): exact zeros, a warp per row (see AmProb)
+      const int r1 = min(U1, t.m0 + sg::BM), nc4 = min(kBN, V - t.n0) >> 2;
+      for (int r = t.m0 + e.warp; r < r1; r += sg::EPI_WARPS) {
+        float4* dst = reinterpret_cast<float4*>(lm_grad + ((size_t)t.n * U1 + r) * V + t.n0);
+        if (e.lane < nc4) dst[e.lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      return;
+    }
     const int urow = t.m0 + e.row;
     const bool live = urow <= Un;
-    float csy = 0.f, csb = 0.f;
-    int y = -1;
-    if (live) {
-      for (int tb = 0; tb < ntb; ++tb) {
-        csy += colpy[((size_t)t.n * ntb + tb) * U1 + urow];
-        csb += colpb[((size_t)t.n * ntb + tb) * U1 + urow];
-      }
-      if (urow < Un) y = (int)sym[(size_t)t.n * U + urow];
-    }
+    const float4 rsc = reinterpret_cast<const float4*>(aux)[e.row];   // (prologue)
+    const float csy = rsc.x, csb = rsc.y;
+    const int y = __float_as_int(rsc.w);
     const float lz = (live && sm.on()) ? lse_lm[(size_t)t.n * U1 + urow] : 0.f;
     const float Q = (live && sm.on()) ? Qu[(size_t)t.n * U1 + urow] : 0.f;
     const float* gr = gq + (size_t)t.n * VPl;
     const int nep = epi_chunks(t);
     if (nep > 0) {
-      const float mlm = live ? m_lm[(size_t)t.n * U1 + urow] : 0.f;
+      const float mlm = rsc.z;
       for (int c = e.g; c < nep; c += 2) {
         const int vc = t.n0 + 32 * c;
         float acc[32];
         tc::tmem_ld32(e.taddr + 32 * c, acc);
         tc::mbar_wait(&ep_full[c], 0);
         uint8_t* tile = smem + c * EP_BYTES;
+        if (!sm.on()) {
+          // the plain trivial joiner: gs e^(x - m_lm) acc everywhere, then the row's two picks (its label column
+          // and the blank column) subtracted in place -- see AmProb
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4* pq = ep_at(tile, e.row, q);
+            const float4 x = *pq;
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            float o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) o[i] = gs * (__expf(xs[i] - mlm) * acc[4 * q + i]);
+            *pq = live ? make_float4(o[0], o[1], o[2], o[3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          if (live) {
+            const int jy = y - vc;
+            if ((unsigned)jy < 32u) reinterpret_cast<float*>(ep_at(tile, e.row, jy >> 2))[jy & 3] -= gs * csy;
+            if (vc == 0) reinterpret_cast<float*>(ep_at(tile, e.row, 0))[0] -= gs * csb;
+          }
+        } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float4* pq = ep_at(tile, e.row, q);
@@ -1039,6 +1209,7 @@ struct LmProb {
             o[i] = live ? grad(xs[i], mlm, acc[j], pick, csy + csb, lz, sm.on() ? gr[v] : 0.f, Q) : 0.f;
           }
           *pq = make_float4(o[0], o[1], o[2], o[3]);
+        }
         }
         tc::fence_proxy_async();
         group_bar(e.g);

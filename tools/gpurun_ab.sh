@@ -7,14 +7,14 @@ if [ "${TESTS:-1}" = 1 ]; then
   tail -n 3 gpurun_out/gpu_tests.log
 fi
 for c in ${CFGS:-5 3}; do
-  for v in 1 0; do
+  for v in ${VALS:-1 0}; do
     env $SW=$v timeout 300 python bench.py --config $c --no-e2e --no-cpu-baseline > gpurun_out/ab_c${c}_$v.log 2>&1; echo c$c $SW=$v rc $?
     python - gpurun_out/ab_c${c}_$v.log <<'PY'
-import json, sys
+import json, os, sys
 l = [x for x in open(sys.argv[1]).read().splitlines() if x.startswith("{")]
 if l:
     d = json.loads(l[-1]); k = d["kernels"]
-    print("  ms/step %.4f" % d["ms_per_step"], " ".join("%s %.1f/%.1f" % (n.replace("joiner_", "").replace("_gemm", ""), k[n]["live_ms"] * 1e3, k[n]["standalone_ms"] * 1e3) for n in ("joiner_fwd_gemm", "joiner_dh_gemm", "joiner_dw_gemm")))
+    print("  ms/step %.4f" % d["ms_per_step"], " ".join("%s %.1f/%.1f" % (n.replace("_gemm", ""), k[n]["live_ms"] * 1e3, k[n]["standalone_ms"] * 1e3) for n in os.environ.get("KERNELS", "joiner_fwd_gemm joiner_dh_gemm joiner_dw_gemm").split()))
 PY
   done
 done

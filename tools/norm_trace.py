@@ -18,7 +18,7 @@ for it in range(4):
                        o["px_grad"], o["py_grad"], None, None, o["status"], ws)
     torch.cuda.synchronize()
 lib.rnnt_debug_timeline(ctypes.c_void_p(0))
-t = buf.cpu().numpy()[: (4 << 20) // 8].reshape(-1, 4).astype(np.float64)
+t = buf.cpu().numpy()[: (4 << 20) // 8].reshape(-1, 8).astype(np.float64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 t = (t - t0) / 1000.0

@@ -913,6 +913,7 @@ struct AmProb {
       epi_bar();
     }
     if (threadIdx.x < sg::BM) reinterpret_cast<float2*>(aux + kRowOff)[threadIdx.x] = rsc;
+    if (threadIdx.x == 0) off[5] = utt_T(bnd, t.n);       // (the epilogue's T_n: no boundary load after the MMAs)
     epi_bar();
   }
   // the picks of row trow for the 32 columns of chunk c (fp32 y' from px_grad)
@@ -937,7 +938,7 @@ struct AmProb {
   }
   __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
-    const int Tn = utt_T(bnd, t.n);
+    const int Tn = reinterpret_cast<const int*>(aux)[5];   // (prologue)
     const int trow = t.m0 + e.row;
     const bool live = trow < Tn;
     const int nep = epi_chunks(t);
@@ -1146,11 +1147,12 @@ struct LmProb {
       }
       reinterpret_cast<float4*>(aux)[threadIdx.x] = make_float4(csy, csb, mlm, __int_as_float(y));
     }
+    if (threadIdx.x == 0) *reinterpret_cast<int*>(aux + 2048) = Un;
     epi_bar();
   }
   __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t* ep_full,
                            const Maps& mp) const {
-    const int Un = utt_U(bnd, t.n), U1 = U + 1;
+    const int Un = *reinterpret_cast<const int*>(aux + 2048), U1 = U + 1;   // (prologue)
     if (tma_io && t.nkb0 == 0) {
       // a tile of padded token positions only (u > U_n): exact zeros, a warp per row (see AmProb)
       const int r1 = min(U1, t.m0 + sg::BM), nc4 = min(kBN, V - t.n0) >> 2;

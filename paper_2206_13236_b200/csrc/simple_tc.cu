@@ -681,6 +681,21 @@ struct NormProbT {
       }
       lmy[j] = a; lm0[j] = b; mlm[j] = c; lz[j] = z; lyv[j] = w;
     }
+    // the rows' {m_am(t), am[t, 0]} and the utterance's lengths for the epilogue, loaded while the mainloop runs
+    // (as the epilogue's first statements they were two exposed global round trips after the last MMA)
+    if (threadIdx.x < sg::BM) {
+      const int trow = t.m0 + threadIdx.x;
+      float2 r = make_float2(0.f, 0.f);
+      if (trow < utt_T(bnd, t.n)) {
+        const size_t arow = (size_t)t.n * T + trow;
+        r = make_float2(m_am[arow], am[arow * V]);
+      }
+      reinterpret_cast<float2*>(aux + 5120)[threadIdx.x] = r;
+    }
+    if (threadIdx.x == 0) {
+      reinterpret_cast<int*>(aux + 6144)[0] = utt_T(bnd, t.n);
+      reinterpret_cast<int*>(aux + 6144)[1] = Un;
+    }
     epi_bar();
   }
   __device__ void epilogue(uint8_t* smem, uint8_t* aux, const Tile& t, const Epi& e, uint64_t*, const Maps&) const {
@@ -689,7 +704,7 @@ struct NormProbT {
     const float* mlm = lm0 + 256;
     const float* lz = mlm + 256;
     const float* lyv = lz + 256;
-    const int Tn = utt_T(bnd, t.n), Un = utt_U(bnd, t.n);
+    const int Tn = reinterpret_cast<const int*>(aux + 6144)[0], Un = reinterpret_cast<const int*>(aux + 6144)[1];
     const int trow = t.m0 + e.row;
     const bool rowok = trow < Tn;
     const int t0w = t.m0 + 32 * e.q;
@@ -701,8 +716,8 @@ struct NormProbT {
     float2 (*bxy)[PB] = reinterpret_cast<float2 (*)[PB]>(smem + e.warp * 32 * PB * 8);
     float (*brs)[PB] = reinterpret_cast<float (*)[PB]>(smem + sg::EPI_WARPS * 32 * PB * 8 + e.warp * 32 * PB * 4);
     const size_t arow = (size_t)t.n * T + (rowok ? trow : 0);
-    const float mam = rowok ? m_am[arow] : 0.f;
-    const float am0 = rowok ? am[arow * V] : 0.f;
+    const float2 rsc = reinterpret_cast<const float2*>(aux + 5120)[e.row];   // (prologue)
+    const float mam = rsc.x, am0 = rsc.y;
     const float* ayr = amy + arow * UPa;
     const size_t nbase = (size_t)t.n * (K + 1);
     const bool smooth = sm.on();

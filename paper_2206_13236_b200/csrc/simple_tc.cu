@@ -738,8 +738,21 @@ struct NormProbT {
         }
       }
       tc::tmem_ld32(e.taddr + c0, acc);
+      if (c == e.g) etrace(4);
       // branch-free per cell: every cell is computed (invalid ones from S = 1) and selected; the
       // smoothing term (a warp-uniform switch) is applied in a second, separate loop
+      // (the chunk's column tables into registers first, as 16-B loads: read cell by cell between the staging
+      //  stores of the loop below, which they may alias as far as the compiler knows, they could not be
+      //  hoisted and the cells ran as a chain of shared-memory + MUFU latencies, 2.3 us per chunk)
+      float tm[32], ty[32], t0[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 a = reinterpret_cast<const float4*>(mlm + c0)[q], b = reinterpret_cast<const float4*>(lmy + c0)[q],
+                     d = reinterpret_cast<const float4*>(lm0 + c0)[q];
+        tm[4 * q] = a.x; tm[4 * q + 1] = a.y; tm[4 * q + 2] = a.z; tm[4 * q + 3] = a.w;
+        ty[4 * q] = b.x; ty[4 * q + 1] = b.y; ty[4 * q + 2] = b.z; ty[4 * q + 3] = b.w;
+        t0[4 * q] = d.x; t0[4 * q + 1] = d.y; t0[4 * q + 2] = d.z; t0[4 * q + 3] = d.w;
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int u = u0 + j;
@@ -747,9 +760,9 @@ struct NormProbT {
         const float S = valid ? acc[j] : 1.f;
         under |= !(S > 0.f);
         // base-2 throughout: Lnorm2 = log2 S + (m_am + m_lm) log2e = L_normalizer(t,u) log2e, Eq. 6
-        const float Ln2 = lg2_approx(S) + (mam + mlm[c0 + j]) * RNNT_LOG2E_F;
-        const float px0 = fmaf(ay[j] + lmy[c0 + j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
-        const float py0 = fmaf(am0 + lm0[c0 + j], RNNT_LOG2E_F, -Ln2);     // empty(t,u) log2e, Eq. 2 + 5
+        const float Ln2 = lg2_approx(S) + (mam + tm[j]) * RNNT_LOG2E_F;
+        const float px0 = fmaf(ay[j] + ty[j], RNNT_LOG2E_F, -Ln2);   // y(t,u) log2e, Eq. 1 + 5
+        const float py0 = fmaf(am0 + t0[j], RNNT_LOG2E_F, -Ln2);     // empty(t,u) log2e, Eq. 2 + 5
         // y only below U_n; out of the last frame only the terminal blank exists
         const float px = (valid && u < Un) ? px0 : kNegBig;
         const float py = (valid && !(trow == Tn - 1 && u < Un)) ? py0 : kNegBig;
@@ -770,6 +783,7 @@ struct NormProbT {
         }
       }
       __syncwarp();
+      if (c == e.g) etrace(5);
       // diagonal-major write of the arcs and of 1/S: for diagonal k = t0w + u0 + d, lane l holds
       // column u0 + l (t = k - u)
       // iteration i: lanes l <= i write diagonal t0w + u0 + i, lanes l > i diagonal t0w + u0 + i + 32
@@ -786,7 +800,9 @@ struct NormProbT {
           }
         }
       __syncwarp();
+      if (c == e.g) etrace(6);
     }
+    etrace(7);
     if (under) set_status(status, t.n, kStatusUnderflow);
   }
 };

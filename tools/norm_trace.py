@@ -26,3 +26,9 @@ print("CTAs", len(t), "span us", t[:, 3].max())
 for name, a, bb in [("start", 0, 0), ("prologue", 0, 1), ("mainloop", 1, 2), ("epilogue", 2, 3)]:
     dd = t[:, bb] - t[:, a] if a != bb else t[:, a]
     print(f"{name:10s} med {np.median(dd):7.2f} p90 {np.percentile(dd, 90):7.2f} max {dd.max():7.2f}")
+# epilogue-internal marks (thread 0, its group's first chunk): operands of the chunk in registers, cells computed and
+# staged, skewed write issued; then the group's remaining chunks
+lv = t[t[:, 7] > t[:, 2]]
+for name, a, bb in [("chunk 0 loads", 2, 4), ("chunk 0 compute", 4, 5), ("chunk 0 skewed write", 5, 6), ("later chunks", 6, 7), ("tail", 7, 3)]:
+    dd = lv[:, bb] - lv[:, a]
+    print(f"{name:22s} med {np.median(dd):7.2f} p10 {np.percentile(dd, 10):7.2f} p90 {np.percentile(dd, 90):7.2f}")

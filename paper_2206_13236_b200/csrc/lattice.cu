@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) lattice_fb_kernel(
 //            the outflow of a diagonal sums to 1);
 //   phase B: the normalised values written t-major (shared memory only): px_grad, py_grad, G~ and
 //            y' as bf16 hi + lo; the cells of row t in this block are the contiguous columns u = k - t.
+constexpr int kCombineZeroBlocks = 4; // zero-padding blocks per utterance (a warp per frame row)
 constexpr int kCombineWindow = 512;   // staged columns per pass (3 x 32 x 512 fp32 = 192 KB)
 __global__ void __launch_bounds__(256) combine_kernel(
     const float2* __restrict__ pxy, const float* __restrict__ rS,
@@ -333,6 +334,23 @@ __global__ void __launch_bounds__(256) combine_kernel(
   const double L2 = Ltot[n] * RNNT_LOG2E;
   const bool finite = isfinite(L2);
   const int U1 = U + 1;
+  const int nd = (T + UP - 1 + 31) / 32;     // diagonal blocks; blocks nd.. of the row zero the padding
+  if ((int)blockIdx.x >= nd) {
+    // The padded cells of the t-major outputs (frames t >= T_n, columns u > U_n; everything of a non-finite
+    // utterance) are exact zeros written here, a warp per frame row, so that the diagonal blocks touch only
+    // lattice cells: as part of their phase B the padding was two thirds of the cell slots at c5 and made
+    // the issue-bound kernel ~2x longer.
+    const int Tv = finite ? Tn : 0;
+    const int nz = gridDim.x - nd;
+    for (int t = ((int)blockIdx.x - nd) * 8 + warp; t < T; t += 8 * nz) {
+      const int c_lo = t < Tv ? Un + 1 : 0;
+      const size_t o = ((size_t)n * T + t) * U1, og = ((size_t)n * T + t) * UP;
+      for (int u = c_lo + lane; u < U1; u += 32) { px_grad[o + u] = 0.f; py_grad[o + u] = 0.f; }
+      for (int u = c_lo + lane; u < UP; u += 32) { Gt_hi[og + u] = 0; Gt_lo[og + u] = 0; }
+    }
+    return;
+  }
+  if (!finite || k0 >= Kn) return;           // no lattice cell on these diagonals
   const int lsw = 31 - __clz(SW);
   if (threadIdx.x < 32 * lat::MAXW) {
     const int kr = threadIdx.x / lat::MAXW, w = threadIdx.x % lat::MAXW;
@@ -420,21 +438,21 @@ __global__ void __launch_bounds__(256) combine_kernel(
       __syncthreads();
     }
     // phase B: rows t with a cell of the window in the block: columns u = k0 + kr - t in [c0, c1)
-    const int tlo = max(0, k0 - c1 + 1), thi = min(T - 1, k0 + 31 - c0);
+    // (rows with a lattice cell of the window only: u = k0 + kr - t in [c0, min(c1 - 1, U_n)], t < T_n)
+    const int tlo = max(0, k0 - min(c1 - 1, Un)), thi = min(Tn - 1, k0 + 31 - c0);
     for (int t = tlo + warp; t <= thi; t += 8) {
       const int kr = lane, u = k0 + kr - t;
-      if (u < c0 || u >= c1) continue;
-      const bool valid = finite && t < Tn && u <= Un;   // (staged values exist for the lattice cells only)
-      const float rz = valid ? s_rz[kr] : 0.f;
-      const float yv = valid ? Ys[kr * CW + (u - c0)] * rz : 0.f, bv = valid ? Bs[kr * CW + (u - c0)] * rz : 0.f;
-      if (u < U1) {
+      if (u < c0 || u >= c1 || u > Un) continue;        // (the padding is zeroed by the blocks nd..)
+      const float rz = s_rz[kr];
+      const float yv = Ys[kr * CW + (u - c0)] * rz, bv = Bs[kr * CW + (u - c0)] * rz;
+      {
         const size_t o = ((size_t)n * T + t) * U1 + u;
         px_grad[o] = yv;
         py_grad[o] = bv;
       }
       // G~ = (y' + empty') / S for the am/lm gradient contractions: bf16 hi + lo, t-major, pitch UP
       const size_t og = ((size_t)n * T + t) * UP + u;
-      const float g = valid ? Gs[kr * CW + (u - c0)] * rz : 0.f;
+      const float g = Gs[kr * CW + (u - c0)] * rz;
       const __nv_bfloat16 gh = __float2bfloat16_rn(g);
       const __nv_bfloat16 gl = __float2bfloat16_rn(g - __bfloat162float(gh));
       Gt_hi[og] = *reinterpret_cast<const uint16_t*>(&gh);
@@ -478,8 +496,9 @@ cudaError_t lattice_launch(const Dims& d, const SimpleWS& w, const int64_t* bnd,
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
-  // diagonal blocks cover every t-major output cell, including the zero padding u in [U+1, UP) of G~
-  dim3 grid((d.T + d.UP() - 1 + 31) / 32, d.N);
+  // diagonal blocks write the lattice cells of the t-major outputs; kCombineZeroBlocks more blocks per
+  // utterance their zero padding (frames t >= T_n, columns (U_n, UP) of G~ / (U_n, U] of the occupancies)
+  dim3 grid((d.T + d.UP() - 1 + 31) / 32 + kCombineZeroBlocks, d.N);
   const size_t csm = (size_t)3 * 32 * std::min(d.UP(), kCombineWindow) * sizeof(float);
   cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   RNNT_LAUNCH(KID_COMBINE, st, launch_pdl(combine_kernel, grid, 256, csm, st, w.pxy, w.rS, w.alpha, w.beta, w.Ash, w.Bsh,

@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
 #pragma unroll
       for (int i = 0; i < CG; ++i) {          // every load of the group first
         const int u = u0 + 32 * i + lane;
+        if (u0 + 32 * i > uhi) break;         // (warp-uniform: no cell of the diagonal in this chunk or later ones)
         const bool v = u >= ulo && u <= uhi && u < ue;
         a[i] = v ? Ar[u] : 0.f;
         xy[i] = v ? XY[u] : make_float2(0.f, 0.f);
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(256) combine_kernel(
 #pragma unroll
       for (int i = 0; i < CG; ++i) {
         const int u = u0 + 32 * i + lane;
-        if (u >= ue) break;
+        if (u >= ue || u0 + 32 * i > uhi) break;   // (staged values of chunks without a cell are never read)
         float yv = 0.f, bv = 0.f, gv = 0.f;
         if (live) cell(kr, u, a[i], xy[i], b0[i], b1[i], r[i], yv, bv, gv);
         if (stage) {

@@ -629,7 +629,10 @@ __device__ __forceinline__ void warp_store_block(const float (*buf)[33], float* 
 template <int BNT>
 struct NormProbT {
   static constexpr bool kA_MN = false, kB_MN = false;
-  static constexpr int kPhases = 1, kBN = BNT, kStages = RNNT_NORM_STAGES, kMinBlocks = RNNT_NORM_MINB;
+  // 128-column tiles: three 64 KB stages (the mainloop is bound by the load round trip per stage: two stages ran
+  // 0.75-0.87 us per k-block at c5 / c3); 256-column tiles (96 KB stages): two
+  static constexpr int kPhases = 1, kBN = BNT, kStages = BNT <= 128 ? RNNT_NORM_STAGES + 1 : RNNT_NORM_STAGES,
+                       kMinBlocks = RNNT_NORM_MINB;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
   int T, U, V, LU, K, BN, nkb, UPa;

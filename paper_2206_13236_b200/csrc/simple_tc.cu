@@ -631,7 +631,9 @@ struct NormProbT {
   static constexpr bool kA_MN = false, kB_MN = false;
   // 128-column tiles: three 64 KB stages (the mainloop is bound by the load round trip per stage: two stages ran
   // 0.75-0.87 us per k-block at c5 / c3); 256-column tiles (96 KB stages): two
-  static constexpr int kPhases = 1, kBN = BNT, kStages = BNT <= 128 ? RNNT_NORM_STAGES + 1 : RNNT_NORM_STAGES,
+  // (64-column tiles, U + 1 <= 64 as at c3: four 48 KB stages)
+  static constexpr int kPhases = 1, kBN = BNT,
+                       kStages = BNT <= 64 ? RNNT_NORM_STAGES + 2 : (BNT <= 128 ? RNNT_NORM_STAGES + 1 : RNNT_NORM_STAGES),
                        kMinBlocks = RNNT_NORM_MINB;
   const float *lm, *m_am, *m_lm;
   const int64_t *sym, *bnd;
@@ -1349,6 +1351,7 @@ cudaError_t norm_gemm_launch(const Dims& d, const SimpleWS& w, const float* am, 
   // 128 x 256 tiles for large V (mainloop-bound: fewer, longer tiles); 128 x 128 otherwise (epilogue-bound)
   if (d.VP64() >= 2048 && d.U1() > 128)
     return launch_norm<NormProbT<256>>(d, w, am, lm, sym, bnd, status, sm, st);
+  if (d.U1() <= 64) return launch_norm<NormProbT<64>>(d, w, am, lm, sym, bnd, status, sm, st);
   return launch_norm<NormProbT<RNNT_NORM_BN>>(d, w, am, lm, sym, bnd, status, sm, st);
 }
 

@@ -39,3 +39,12 @@ def test_sass_is_sm100a():
     so = R.LIB_PATH
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_library_exports_only_the_c_abi():
+    """The boundary is the C-ABI of include/rnnt.h and nothing else: every defined dynamic symbol of the
+    shared library is a declared rnnt_* function (csrc/export.map keeps the C++ symbols local)."""
+    out = subprocess.run(["nm", "-D", "--defined-only", R.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if len(ln.split()) >= 3 and ln.split()[-2] in "TtDdBb"}
+    assert exported, "nm listed no symbols"
+    assert exported == set(R.header_functions()), sorted(exported ^ set(R.header_functions()))

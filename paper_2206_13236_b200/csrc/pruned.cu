@@ -128,14 +128,18 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
       tcounter[2] = __float_as_int(gs);   // PrunedWS::gsp (the joiner backward's fp16 dpre scale)
     }
     // padded columns v >= V get -inf: the joiner epilogue's z = acc + b is then -inf there (W rows past
-    // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask
-    for (int v = threadIdx.x; v < VP; v += blockDim.x) bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
-    __syncthreads();
+    // V are zero-filled by TMA) and e^(z - m) = 0 without a per-element mask.  The row blocks convert one
+    // 256-column slice each (below); this block only the columns past their reach, and it takes the tile
+    // maxima from the bf16 input directly (as one block's serial loops the conversion and the maxima were
+    // ~20 us of this kernel at V = 5000-8000, on the step's critical path)
+    for (int v = (int)(gridDim.x - 1) * (int)blockDim.x + threadIdx.x; v < VP; v += blockDim.x)
+      bias[v] = v < V ? bf16_bits_to_f(bias_bf16[v]) : neg_inf_f();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int tl = warp; tl < VP / 128; tl += blockDim.x / 32) {   // bias max per 128-column tile
       float m = neg_inf_f();
+#pragma unroll
       for (int j = lane; j < 128; j += 32)
-        if (tl * 128 + j < V) m = fmaxf(m, bias[tl * 128 + j]);
+        if (tl * 128 + j < V) m = fmaxf(m, bf16_bits_to_f(bias_bf16[tl * 128 + j]));
       m = warp_max(m);
       if (lane == 0) bmax[tl] = m;
     }
@@ -178,6 +182,7 @@ __global__ void rowinfo_kernel(const int32_t* __restrict__ ranges, const int64_t
   }
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long R = (long long)N * T * S;
+  if (r < VP) bias[r] = r < V ? bf16_bits_to_f(bias_bf16[r]) : neg_inf_f();   // this block's slice of the fp32 bias
   int info = -1;
   if (r < R) {
     const int s = (int)(r % S);
